@@ -1,0 +1,477 @@
+"""Pin the CPU oracle to things other than itself (runs on CPU: -m "not gpu").
+
+Pins: SPEC worked examples (tests/golden/spec_examples.json, each cited),
+exact Fraction brute force (oracle/brute.py) on tiny inputs, closed forms,
+library special cases (numpy searchsorted / lexsort / bincount) and the
+invariants SPEC states.
+"""
+import json
+import math
+import os
+from fractions import Fraction as Fr
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st, HealthCheck
+
+from oracle import brute
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ------------------------------------------------------------- Stage 1 (A3) ---
+@pytest.mark.parametrize("ex", GOLD["kmeans"], ids=lambda e: e["cite"][:20])
+def test_kmeans_golden(orc, ex):
+    assert orc.kmeans(ex["values"], ex["k"]) == ex["expected"]
+
+
+@settings(max_examples=150, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(st.lists(st.integers(1, 60), min_size=3, max_size=14), st.integers(1, 3))
+def test_kmeans_vs_exhaustive_fraction(orc, xs, k):
+    """Oracle's cut attains the exact minimum SSE over ALL contiguous k-partitions
+    (S:131 exhaustive search), and equals it when the optimum is unique."""
+    k = min(k, len(set(xs)))
+    got = orc.kmeans(xs, k)
+    best, args = brute.kmeans_brute(xs, k)
+    sse = sum(brute._sse(p) for p in got)
+    assert sse == best
+    if len(args) == 1:
+        assert got == args[0]
+
+
+def test_kmeans_invalid_k(orc):
+    with pytest.raises(ValueError):
+        orc.kmeans([1, 2], 3)
+
+
+# ------------------------------------------------------------- Stage 2 (A4) ---
+@pytest.mark.parametrize("ex", GOLD["refine"], ids=lambda e: e["cite"][:20])
+def test_refine_golden(orc, ex):
+    assert orc.refine(ex["values"], ex["alpha"], ex["min_width"]) == ex["expected"]
+
+
+@settings(max_examples=300, deadline=None)
+@given(st.lists(st.integers(1, 400), min_size=1, max_size=40),
+       st.sampled_from([1.25, 1.5, 2.0, 2.5, 3.0, 4.0]), st.sampled_from([1, 2, 5, 50]))
+def test_refine_vs_literal_eq2(orc, xs, alpha, mw):
+    """Eq. 2 with mean(G) as the literal mean of the gap list (exact Fractions)
+    reproduces the oracle's telescoped g*(n-1) > alpha*span test at every node
+    (acceptance #5's per-node re-check).  Dyadic alpha keeps alpha*span exact."""
+    assert orc.refine(xs, alpha, mw) == brute.refine_brute(xs, alpha, mw)
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.lists(st.integers(1, 300), min_size=2, max_size=60))
+def test_refine_concatenation_preserves_input(orc, xs):
+    """refine output concatenated in order equals its input."""
+    parts = orc.refine(xs, 2.0, 1)
+    assert sum(parts, []) == sorted(xs)
+
+
+# ------------------------------------------------------------- Stage 3 (A6) ---
+@pytest.mark.parametrize("ex", GOLD["utility"], ids=lambda e: e["cite"][:20])
+def test_utility_golden(orc, ex):
+    got = orc.utility(ex["rho"][0], ex["rho"][1], ex["mean"][0], ex["mean"][1], ex["eps"])
+    assert got == pytest.approx(ex["expected"], rel=1e-15, abs=0)
+
+
+def _prune_args(queues):
+    lo = [q[0] for q in queues]; hi = [q[1] for q in queues]
+    cnt = [len(q[2]) for q in queues]; s1 = [sum(q[2]) for q in queues]; s2 = [sum(x * x for x in q[2]) for q in queues]
+    return lo, hi, cnt, s1, s2
+
+
+@pytest.mark.parametrize("ex", GOLD["prune"], ids=lambda e: e["cite"][:20])
+def test_prune_golden(orc, ex):
+    lo, hi, cnt, s1, s2 = _prune_args(ex["queues"])
+    if "expected_u" in ex:   # the constructed utilities really are 0.5 and 2.0
+        r = [c / (h - l) for l, h, c in zip(lo, hi, cnt)]
+        mu = [a / c for a, c in zip(s1, cnt)]
+        u = [orc.utility(r[i], r[i + 1], mu[i], mu[i + 1], ex["eps"]) for i in range(2)]
+        assert u == pytest.approx(ex["expected_u"], rel=1e-12)
+    L, H, *_ = orc.prune(lo, hi, cnt, s1, s2, ex["max_queues"], ex["eps"])
+    assert [[int(a), int(b)] for a, b in zip(L, H)] == ex["expected_bounds"]
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.lists(st.tuples(st.integers(1, 9), st.lists(st.integers(0, 8), min_size=1, max_size=6)),
+                min_size=1, max_size=12),
+       st.integers(1, 6), st.sampled_from(["min", "max"]))
+def test_prune_vs_fraction_bruteforce(orc, spec, maxq, rule):
+    """Merge sequence of Eq. 3 with exact rationals vs the fp64 oracle.
+    Inputs are built so that the exact utilities have no near-ties."""
+    queues, lo = [], 0
+    for width, offs in spec:
+        members = sorted(lo + (o % width) for o in offs)
+        queues.append((lo, lo + width, members))
+        lo += width
+    # skip inputs with exact ties / near-ties in some iteration (fp64 may order them differently)
+    eps = 2.0 ** -10
+    ref = brute.prune_brute(queues, maxq, eps, rule)
+    args = _prune_args(queues)
+    L, H, cnt, s1, s2, merges = orc.prune(*args, maxq, eps, 0 if rule == "min" else 1)
+    if not _no_near_ties(queues, maxq, eps, rule):
+        return
+    assert [(int(a), int(b)) for a, b in zip(L, H)] == [(q[0], q[1]) for q in ref]
+    assert list(cnt) == [len(q[2]) for q in ref]
+    assert merges == len(queues) - len(ref)
+
+
+def _no_near_ties(queues, maxq, eps, rule):
+    qs = [(lo, hi, list(m)) for lo, hi, m in queues]
+    e = Fr(eps)
+    while len(qs) > maxq and len(qs) > 1:
+        us = []
+        for p in range(len(qs) - 1):
+            (l1, h1, m1), (l2, h2, m2) = qs[p], qs[p + 1]
+            us.append((Fr(len(m1), h1 - l1) + Fr(len(m2), h2 - l2)) / (abs(Fr(sum(m2), len(m2)) - Fr(sum(m1), len(m1))) + e))
+        s = sorted(us)
+        if len(s) > 1:
+            a, b = (s[0], s[1]) if rule == "min" else (s[-1], s[-2])
+            if abs(a - b) <= abs(a) * Fr(1, 10 ** 9):
+                return False
+        t = min(us) if rule == "min" else max(us)
+        p = us.index(t)
+        (l1, h1, m1), (l2, h2, m2) = qs[p], qs[p + 1]
+        qs[p:p + 2] = [(l1, h2, m1 + m2)]
+    return True
+
+
+# ------------------------------------------------------ R&P pipeline (A1-A6) ---
+def _check_partition_invariants(orc, xs, part, maxq):
+    qs = part.queues()
+    assert 1 <= len(qs) <= maxq
+    for a, b in zip(qs, qs[1:]):
+        assert a["max_len"] == b["min_len"]                           # S:115 contiguity
+    for q in qs:
+        assert q["min_len"] < q["max_len"]
+    assert [q["index"] for q in qs] == list(range(1, len(qs) + 1))
+    v = np.asarray(xs)
+    v = v[v >= 1]
+    assert qs[0]["min_len"] == v.min() and qs[-1]["max_len"] == v.max() + 1   # coverage
+    # every history value lands in exactly one queue, counts and sums match
+    bounds = np.array([q["min_len"] for q in qs])
+    pos = np.searchsorted(bounds, v, side="right") - 1
+    assert (pos >= 0).all()
+    cnt = np.bincount(pos, minlength=len(qs))
+    s1 = np.bincount(pos, weights=v.astype(np.float64), minlength=len(qs))
+    assert cnt.tolist() == [q["count"] for q in qs]
+    assert s1.astype(np.int64).tolist() == [q["sum"] for q in qs]
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.lists(st.integers(1, 3000), min_size=1, max_size=300), st.integers(1, 12),
+       st.sampled_from([1.5, 2.0, 3.0]))
+def test_partition_invariants_random(orc, xs, maxq, alpha):
+    """Acceptance #5: contiguity, disjointness, |Q| <= max_queues."""
+    s, part, stt = orc.partition(xs, alpha=alpha, max_queues=maxq)
+    assert s == orc.OK
+    _check_partition_invariants(orc, xs, part, maxq)
+    assert stt.segments - stt.merges == part.n
+
+
+def test_partition_bimodal_split_in_gap(orc):
+    """bimodal trace -> >= 2 queues with a boundary inside the empty gap.
+
+    Holds under the MAX_U switch.  Under the literal MIN_U rule (R17, the default)
+    Stage 3 degenerates as documented in DESIGN.md: 31 single-length queues
+    [32,33)..[62,63) and one mega-queue [63, max+1) holding ~89% of the history
+    (|Δb̄| in Eq. 3's denominator makes the growing merged queue the argmin)."""
+    import workload
+    xs = workload.bimodal(10000, 101)
+    s, part, _ = orc.partition(xs, merge_rule=orc.MAX_U)
+    qs = part.queues()
+    assert s == orc.OK and len(qs) >= 2
+    assert any(257 <= q["max_len"] <= 4096 for q in qs[:-1])
+    _check_partition_invariants(orc, xs, part, 32)
+    s, part, _ = orc.partition(xs)
+    qs = part.queues()
+    assert [(q["min_len"], q["max_len"]) for q in qs[:31]] == [(L, L + 1) for L in range(32, 63)]
+    assert qs[31]["min_len"] == 63 and qs[31]["count"] / len(xs) > 0.85
+    _check_partition_invariants(orc, xs, part, 32)
+
+
+def test_partition_identical_lengths_one_queue(orc):
+    s, part, _ = orc.partition([777] * 50)
+    assert s == orc.OK and part.n == 1
+    assert (part.q[0].min_len, part.q[0].max_len, part.q[0].count) == (777, 778, 50)
+
+
+def test_partition_determinism_and_empty(orc):
+    import workload
+    xs = workload.heavy(20000, 5)
+    a = orc.partition(xs)[1].queues()
+    b = orc.partition(xs)[1].queues()
+    assert a == b
+    assert orc.partition([])[0] == orc.EMPTY
+    assert orc.partition([0, -3])[0] == orc.EMPTY
+    assert orc.partition([5, 6], alpha=1.0)[0] == orc.INVALID         # S:121 alpha > 1
+
+
+def test_partition_stage_composition_small(orc):
+    """R&P on tiny data == kmeans -> refine per cluster -> prune, via the brute references."""
+    xs = [1, 2, 3, 5, 100, 101, 103, 180, 1000, 1001, 1003, 1500]
+    s, part, st_ = orc.partition(xs, max_queues=3, epsilon=2.0 ** -10)
+    _, args = brute.kmeans_brute(xs, 3)
+    segs = []
+    for c in args[0]:
+        segs += brute.refine_brute(c, 2.0, 1)
+    # midpoint finalization (R15)
+    lo = [segs[0][0]]
+    hi = []
+    for i in range(len(segs) - 1):
+        b = (segs[i][-1] + segs[i + 1][0]) // 2 + 1
+        hi.append(b); lo.append(b)
+    hi.append(segs[-1][-1] + 1)
+    ref = brute.prune_brute(list(zip(lo, hi, segs)), 3, 2.0 ** -10)
+    assert [(q["min_len"], q["max_len"]) for q in part.queues()] == [(a, b) for a, b, _ in ref]
+
+
+# ------------------------------------------------------------ weights (A7) ---
+@pytest.mark.parametrize("ex", GOLD["weights"], ids=lambda e: e["cite"][:20])
+def test_weights_golden(orc, ex):
+    w = orc.weights(orc.meta(**ex["theta"]), ex["mean"])
+    which = {"S:309": 1, "S:310": 1, "S:311": 2}[ex["cite"][:5]]
+    assert w[which] == pytest.approx(ex["expected"], abs=1e-7)
+
+
+# -------------------------------------------------------- routing (A8, A9) ---
+@pytest.mark.parametrize("ex", GOLD["route"], ids=lambda e: e["cite"][:20])
+def test_route_golden(orc, ex):
+    part = orc.make_partition(ex["bounds"])
+    s, qid, *_ = orc.route([ex["b"]], part, 64)
+    assert qid[0] == ex["expected_pos"]
+
+
+@settings(max_examples=100, deadline=None)
+@given(st.lists(st.integers(2, 50), min_size=1, max_size=20), st.lists(st.integers(-5, 1200), min_size=1, max_size=200))
+def test_route_contiguous_is_searchsorted(orc, widths, lens):
+    """On a contiguous partition routing reduces to searchsorted(min_len, b, 'right') - 1
+    (SURVEY pins A8); nothing outside creates bubbles except off-range lengths."""
+    edges = np.concatenate([[1], 1 + np.cumsum(widths)])
+    bounds = list(zip(edges[:-1], edges[1:]))
+    part = orc.make_partition(bounds)
+    inside = [x for x in lens if 1 <= x < edges[-1]]
+    s, qid, bad, made, dropped = orc.route(inside, part, 64)
+    assert made == 0 and bad == 0
+    np.testing.assert_array_equal(qid, np.searchsorted(edges[:-1], inside, side="right") - 1)
+
+
+@pytest.mark.parametrize("ex", GOLD["bubble"], ids=lambda e: e["cite"][:20])
+def test_bubble_golden(orc, ex):
+    part = orc.make_partition([(1, ex["left_max"]), (ex["right_min"], 1000)])
+    s, qid, bad, made, _ = orc.route([ex["L"]], part, ex["width"])
+    qs = part.queues()
+    if ex["expected"] == "left":
+        assert qid[0] == 0 and made == 0
+    elif ex["expected"] == "right":
+        assert qid[0] == 1 and made == 0
+    else:
+        assert made == 1 and qs[1]["is_bubble"] == 1
+        assert [qs[1]["min_len"], qs[1]["max_len"]] == ex["expected"]
+        assert qid[0] == qs[1]["id"] == 2 and [q["index"] for q in qs] == [1, 2, 3]
+
+
+@pytest.mark.parametrize("width", [40, 41, 1, 7, 100, 1000])
+def test_bubble_exhaustive_sweep(orc, width):
+    """Acceptance #6: every integer L in [100, 200] against the
+    line-by-line exact-rational Alg. 2, fresh partition each time."""
+    for L in range(100, 200):
+        part = orc.make_partition([(1, 100), (200, 1000)])
+        s, qid, bad, made, _ = orc.route([L], part, width)
+        exp = brute.bubble_brute(L, 100, 200, width)
+        qs = part.queues()
+        if exp == "left":
+            assert qid[0] == 0 and made == 0, L
+        elif exp == "right":
+            assert qid[0] == 1 and made == 0, L
+        else:
+            assert made == 1, L
+            assert (qs[1]["min_len"], qs[1]["max_len"]) == exp, L
+            assert qs[1]["min_len"] <= L < qs[1]["max_len"]
+            assert qs[1]["mean"] == L                                  # R21
+
+
+def test_bubble_edges_and_sequence(orc):
+    """Below the first / above the last queue (R20); later gap requests see the
+    bubbles created before them (R22, pool-index order); indices renumbered."""
+    part = orc.make_partition([(100, 200), (400, 500)])
+    s, qid, bad, made, _ = orc.route([10, 12, 300, 305, 900, 0, 150], part, 40)
+    qs = part.queues()
+    assert [(q["min_len"], q["max_len"]) for q in qs] == [(1, 30), (100, 200), (280, 320), (400, 500), (880, 920)]
+    assert [q["index"] for q in qs] == [1, 2, 3, 4, 5]
+    ids = {(q["min_len"]): q["id"] for q in qs}
+    assert list(qid) == [ids[1], ids[1], ids[280], ids[280], ids[880], -1, ids[100]]
+    assert bad == 1 and made == 3
+
+
+def test_bubble_capacity(orc):
+    part = orc.make_partition([(1000 + i, 1001 + i) for i in range(200)])
+    lens = [int(1400 * 1.25 ** j) for j in range(62)]     # each > 1.1x the previous bubble
+    s, qid, bad, made, dropped = orc.route(lens, part, 2)
+    assert part.n == 256 and made == 56 and dropped == 6 and bad == 0 and s == orc.CAPACITY
+    assert (qid[56:] == -1).all() and (qid[:56] >= 200).all()
+
+
+# ------------------------------------------------------------ scoring (A10) ---
+@pytest.mark.parametrize("ex", GOLD["score"], ids=lambda e: e["cite"][:20])
+def test_score_golden(orc, ex):
+    # W and C realised through now/arrival and a cost field
+    sp = orc.select_params(now=float(ex["W"]))
+    phi = orc.score_one(ex["b"], 0.0, ex["index"], ex["w"], sp, cost=ex["C"])
+    assert phi == pytest.approx(ex["expected"], rel=1e-15)
+
+
+@pytest.mark.parametrize("ex", GOLD["prefill_cost"], ids=lambda e: e["cite"])
+def test_prefill_cost_golden(orc, ex):
+    """C_prefill via the cost=NULL path: weights (0,1,0), index b+1, W=1 -> Φ = 1/C."""
+    c = ex["c"]
+    sp = orc.select_params(now=1.0, c0=c[0], c1=c[1], c2=c[2])
+    phi = orc.score_one(ex["b"], 0.0, ex["b"] + 1, [0, 1, 0], sp)
+    assert 1.0 / phi == pytest.approx(ex["expected"], rel=2e-7)       # fp32-stored coefficients
+
+
+def test_score_exclusions(orc):
+    sp = orc.select_params(now=10.0)
+    assert orc.score_one(5, 11.0, 1, [1, 1, 1], sp, cost=1.0) is None       # W < 0
+    assert orc.score_one(5, 1.0, 1, [1, 1, 1], sp, cost=0.0) is None        # C <= 0
+    assert orc.score_one(5, float("nan"), 1, [1, 1, 1], sp, cost=1.0) is None
+    assert orc.score_one(5, 10.0, 1, [1, 1, 1], sp, cost=1.0) is not None   # W = 0 ok
+
+
+def test_score_vs_exact_rational(orc):
+    rng = np.random.default_rng(3)
+    for _ in range(500):
+        b = int(rng.integers(1, 40000)); idx = int(rng.integers(1, 33))
+        w = np.float32(rng.random(3) * 4)
+        arr = np.float32(rng.random() * 600); cost = np.float32(rng.random() * 5 + 1e-3)
+        sp = orc.select_params(now=600.0)
+        got = orc.score_one(b, float(arr), idx, w, sp, cost=float(cost))
+        W = Fr(float(np.float32(600.0))) - Fr(float(arr))
+        ref = brute.score_exact(idx, b, W, Fr(float(cost)), float(w[0]), float(w[1]), float(w[2]))
+        assert abs(Fr(got) - ref) <= abs(ref) * Fr(1, 10 ** 13)
+
+
+@settings(max_examples=500, deadline=None)
+@given(st.integers(1, 32768), st.integers(1, 64), st.floats(0.0, 5.0), st.floats(1e-3, 5.0),
+       st.floats(0.0, 5.0), st.floats(0.0, 500.0), st.floats(0.01, 100.0), st.floats(1e-3, 10.0))
+def test_starvation_freedom_monotone_unbounded(orc, b, idx, wb, wu, wf, arr, delta, cost):
+    """Acceptance #4: with w_urg > 0 the score strictly
+    increases with now, and the closed-form inversion W* reaches any target."""
+    w = np.float32([wb, wu, wf])
+    now1 = np.float32(arr + 1.0)
+    now2 = np.float32(now1 + delta)
+    p1 = orc.score_one(b, arr, idx, w, orc.select_params(now=float(now1)), cost=cost)
+    p2 = orc.score_one(b, arr, idx, w, orc.select_params(now=float(now2)), cost=cost)
+    assert p2 > p1
+    target = p1 * 1000.0 + 1.0
+    qf = idx / (b + 1.0)
+    c32 = float(np.float32(cost))
+    Wstar = (target / qf - float(w[0]) - float(w[2]) * math.log(b + 1.0)) * c32 / float(w[1])
+    p3 = orc.score_one(b, 0.0, idx, w, orc.select_params(now=float(np.float32(Wstar * 1.001 + 1))), cost=cost)
+    assert p3 >= target
+
+
+def test_score_scale_covariance(orc):
+    """weights × c multiply every score by c."""
+    rng = np.random.default_rng(9)
+    for _ in range(200):
+        b = int(rng.integers(1, 5000)); w = rng.random(3).astype(np.float32)
+        sp = orc.select_params(now=100.0)
+        p = orc.score_one(b, 3.0, 4, w, sp, cost=0.7)
+        q = orc.score_one(b, 3.0, 4, (w * np.float32(4.0)).astype(np.float32), sp, cost=0.7)
+        assert q == pytest.approx(4.0 * p, rel=1e-15)
+
+
+# ---------------------------------------------------------- selection (A11) ---
+def _small_pool(rng, n):
+    lens = rng.integers(1, 60, size=n).astype(np.int32)
+    arr = np.float32(rng.integers(0, 8, size=n) * 0.5)          # many equal arrivals -> index ties
+    cost = (rng.integers(1, 4, size=n) * 0.25).astype(np.float32)
+    return lens, arr, cost
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("seed", range(25))
+def test_select_vs_subset_enumeration(orc, mode, seed):
+    """North_star: brute-force optimal selection agrees on pools of <= 20 requests."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 19))
+    lens, arr, cost = _small_pool(rng, n)
+    part = orc.make_partition([(1, 20), (20, 40), (40, 60)])
+    K = int(rng.integers(1, 7))
+    sp = orc.select_params(k=K, mode=mode, now=5.0)
+    theta = orc.meta(a_b=0.01, b_b=0.2, a_u=-0.01, b_u=1.0, a_f=0.02, b_f=0.1)
+    res = orc.tick(lens, arr, cost, part, theta, sp, global_base=1000)
+    qid = res["qid"]
+    for p in range(3):
+        members = [r for r in range(n) if qid[r] == p]
+        w = orc.weights(theta, part.q[p].mean)
+        phi = {r: orc.score_one(int(lens[r]), float(arr[r]), p + 1, w, sp, cost=float(cost[r])) for r in members}
+        members = [r for r in members if phi[r] is not None]
+        assert res["count"][p] == len(members)
+        if not members:
+            assert res["topk_id"][p].tolist() == [-1] * K and res["head_id"][p] == -1
+            continue
+        keys = [(phi[r], -r) if mode == 0 else (-float(arr[r]), -r) for r in members]
+        best = brute.topk_brute(keys, K)
+        got = [int(i) - 1000 for i in res["topk_id"][p] if i >= 0]
+        assert set(got) == {members[i] for i in best}
+        # ordering: best first
+        order = sorted(members, key=(lambda r: (-phi[r], r)) if mode == 0 else (lambda r: (float(arr[r]), r)))
+        assert got == order[:K]
+        head = min(members, key=lambda r: (float(arr[r]), r))
+        assert res["head_id"][p] == head + 1000
+        assert res["head_score"][p] == phi[head]
+        assert res["max_score"][p] == max(phi.values() if not None else [])
+    ne = [p for p in range(3) if res["count"][p] > 0]
+    if ne:
+        exp = max(ne, key=lambda p: (res["head_score"][p], -p))
+        assert res["primary"] == exp
+    else:
+        assert res["primary"] == -1
+
+
+def test_select_sjf_and_fcfs_degeneracies(orc):
+    """One queue, weights (1,0,0): SCORE order is SJF (shortest first, ties by
+    index).  FIFO mode with one queue is FCFS."""
+    rng = np.random.default_rng(1)
+    n = 300
+    lens = rng.integers(1, 500, size=n).astype(np.int32)
+    arr = np.float32(rng.random(n) * 10)
+    part = orc.make_partition([(1, 1000)])
+    theta = orc.meta(a_b=0, b_b=1, a_u=0, b_u=0, a_f=0, b_f=0)
+    r = orc.tick(lens, arr, None, part, theta, orc.select_params(k=300, mode=0, now=20.0))
+    np.testing.assert_array_equal(r["topk_id"][0], np.lexsort((np.arange(n), lens)))
+    r = orc.tick(lens, arr, None, part, theta, orc.select_params(k=300, mode=1, now=20.0))
+    np.testing.assert_array_equal(r["topk_id"][0], np.lexsort((np.arange(n), arr)))
+
+
+def test_tick_domain_and_invalid(orc):
+    part = orc.make_partition([(1, 10), (10, 100)])
+    lens = np.array([5, 0, 50, 7], np.int32)
+    arr = np.float32([1.0, 1.0, 99.0, 2.0])
+    r = orc.tick(lens, arr, None, part, orc.meta(), orc.select_params(k=2, now=10.0))
+    assert r["status"] == orc.DOMAIN and r["n_invalid"] == 1 and r["n_excluded"] == 1
+    assert r["qid"].tolist() == [0, -1, 1, 0]
+    assert r["count"].tolist() == [2, 0]
+    assert r["primary"] == 0
+
+
+def test_alpha_monotonicity_is_per_node_only(orc):
+    """S:183 claims raising α never increases the number of splits.  With the
+    per-sub-cluster mean(G) of S:192 (R12) that holds at one node but not for the
+    whole recursion; the exact-rational literal Eq. 2 agrees with the oracle on a
+    counterexample (recorded in DESIGN.md §3)."""
+    xs = [157, 293, 19, 67, 139, 150, 290, 119, 125]
+    assert len(orc.refine(xs, 1.5)) == len(brute.refine_brute(xs, 1.5)) == 3
+    assert len(orc.refine(xs, 2.0)) == len(brute.refine_brute(xs, 2.0)) == 4
+    rng = np.random.default_rng(0)
+    for _ in range(500):     # one node: the qualifying-gap set shrinks as alpha grows
+        v = np.sort(rng.integers(1, 300, size=int(rng.integers(2, 40))))
+        g = np.diff(v); n = len(v); span = int(v[-1] - v[0])
+        prev = None
+        for a in (1.25, 1.5, 2.0, 3.0, 5.0):
+            cur = {int(j) for j in np.nonzero(g * (n - 1) > a * span)[0]}
+            assert prev is None or cur <= prev
+            prev = cur
