@@ -1,0 +1,271 @@
+/*
+ * ewsjf.h — C ABI of libewsjf, the B200-native (sm_100a) data-parallel core of
+ * one EWSJF scheduling tick (arXiv 2601.21758, "EWSJF").
+ *
+ * Citation format: P:n = PAPER.md line n, S:n = SPEC.md line n; readings of
+ * silent/ambiguous passages R1..R27 are listed in DESIGN.md §3.
+ *
+ * Conventions (apply to every entry point):
+ *  - All functions return ewsjf_status and never throw or abort across the ABI.
+ *  - d_ prefix: device pointer (CUDA global memory of the ctx's device),
+ *    caller-owned; h_ prefix: host pointer, caller-owned.  The library never
+ *    frees caller memory.  Device inputs are read-only unless marked "out".
+ *  - Work is enqueued on the ctx's CUDA stream and is asynchronous unless an
+ *    h_ output is requested (then the call synchronises the stream).
+ *  - EWSJF_ERR_INVALID_ARG: a parameter is out of range; nothing was launched.
+ *    EWSJF_ERR_DOMAIN: some elements violated a precondition (len < 1, S:223;
+ *    now < arrival; cost <= 0 or NaN; unknown qid); ALL outputs were
+ *    written, the offending elements were excluded and counted.
+ *    EWSJF_ERR_CAPACITY: more than EWSJF_MAX_QUEUES queues (incl. bubbles) or
+ *    the gap list overflowed; outputs are written for what fitted.
+ *    EWSJF_ERR_CUDA: a CUDA call failed (message: ewsjf_last_error()).
+ *  - Layouts are structure-of-arrays, one element per request, contiguous.
+ *    Request ids written by the library are GLOBAL pool indices
+ *    (global_base + local index), < 2^32 - 1.
+ *  - Per-queue outputs are indexed by queue POSITION (q_i - 1, ascending by
+ *    prompt length) of the partition the call ends with, and must be sized for
+ *    EWSJF_MAX_QUEUES queues (× k for top-k arrays).
+ */
+#ifndef EWSJF_H
+#define EWSJF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EWSJF_ABI_VERSION 1
+#define EWSJF_MAX_QUEUES 256      /* hard cap on queues incl. bubbles */
+#define EWSJF_MAX_K 256           /* largest per-queue selection depth */
+
+typedef enum {
+    EWSJF_OK = 0,
+    EWSJF_ERR_INVALID_ARG = 1,
+    EWSJF_ERR_DOMAIN = 2,
+    EWSJF_ERR_EMPTY = 3,          /* empty history (no length >= 1)          */
+    EWSJF_ERR_CAPACITY = 4,
+    EWSJF_ERR_CUDA = 5,
+    EWSJF_ERR_UNSUPPORTED = 6     /* e.g. a history length above the kernel's range */
+} ewsjf_status;
+
+typedef struct ewsjf_ctx ewsjf_ctx;
+
+/* --------------------------------------------------------------- context --- */
+int          ewsjf_abi_version(void);
+const char  *ewsjf_status_str(ewsjf_status s);
+/* Last error message recorded on ctx (static storage owned by ctx). */
+const char  *ewsjf_last_error(const ewsjf_ctx *ctx);
+
+/* Create a context on `device`, enqueueing on `cuda_stream` (cudaStream_t, NULL
+ * = legacy default stream).  The ctx owns ALL scratch, sized once here for
+ * pools of up to max_pool requests, histories of up to max_history lengths
+ * and selection depth up to max_k (1..EWSJF_MAX_K): no allocation happens on a
+ * later call.  *out receives the ctx.  Not thread-safe; one ctx per stream.  */
+ewsjf_status ewsjf_ctx_create(int device, void *cuda_stream, int64_t max_pool, int64_t max_history,
+                              int32_t max_k, ewsjf_ctx **out);
+ewsjf_status ewsjf_ctx_set_stream(ewsjf_ctx *ctx, void *cuda_stream);
+ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx *ctx);
+/* Number of SMs the ctx launches persistent kernels over (the "CTA rows"). */
+int32_t      ewsjf_ctx_num_ctas(const ewsjf_ctx *ctx);
+
+/* ------------------------------------------------------------- partition --- */
+/* Refine-and-Prune parameters (§4.2). alpha > 1 (Eq. 2 significance
+ * ratio); min_width >= 1 (Stage-2 width stop, R13); max_queues in
+ * 1..EWSJF_MAX_QUEUES (Stage-3 budget); epsilon > 0 (Eq. 3);
+ * coarse_k in 1..3 (Stage 1); merge_rule 0 = MIN_U (literal
+ * "lowest utility merged", default), 1 = MAX_U (R17).                      */
+typedef struct {
+    double  alpha;
+    int32_t min_width;
+    int32_t max_queues;
+    double  epsilon;
+    int32_t coarse_k;
+    int32_t merge_rule;
+} ewsjf_partition_params;
+
+/* One queue q_i = [min_len, max_len). */
+typedef struct {
+    int32_t id;          /* stable id (never renumbered; qid values refer to it) */
+    int32_t index;       /* 1-based ordinal q_i ascending by length (R3)  */
+    int32_t min_len;
+    int32_t max_len;
+    int64_t count;       /* history members n                                    */
+    int64_t sum;         /* S1 = Σ b                                             */
+    int64_t sumsq;       /* S2 = Σ b²                                            */
+    double  mean;        /* b̄ = S1/n (a bubble: its creating length L, R21)     */
+    double  density;     /* ρ = n / (max_len - min_len) (R16)                    */
+    double  sse;         /* S2 - S1²/n (informational)                           */
+    int32_t is_bubble;
+    int32_t empty_count; /* Alg. 1 line 9 counter (maintained by the caller)     */
+} ewsjf_queue;
+
+/* Host POD, caller-owned, queues sorted by min_len.  (Named _t because the
+ * function ewsjf_partition() takes the plain name.)                        */
+typedef struct {
+    int32_t     n;
+    int32_t     next_id;
+    uint64_t    version;
+    ewsjf_queue q[EWSJF_MAX_QUEUES];
+} ewsjf_partition_t;
+
+typedef struct {
+    int64_t n_valid, n_invalid;   /* history entries with len >= 1 / < 1       */
+    int64_t distinct;             /* M distinct lengths                         */
+    int32_t k_used, t1, t2;       /* Stage-1 k and distinct-index cuts          */
+    int64_t segments;             /* m after Stage 2                            */
+    int32_t depth;                /* Stage-2 recursion depth                    */
+    int64_t merges;               /* Stage-3 merges                             */
+    float   ms_hist, ms_kmeans, ms_refine, ms_prune, ms_total;   /* device times */
+} ewsjf_partition_stats;
+
+/* Strategic loop, offline mode: Refine-and-Prune over the device array
+ * d_len[n] (int32 prompt lengths of the history window D) on the ctx
+ * stream: counting sort + segmented prefix statistics (A1-A2), exact k-means
+ * k<=3 (Stage 1, A3), Eq. 2 refinement (Stage 2, A4), midpoint finalisation
+ * (A5), Eq. 3 pruning (Stage 3, A6).  Writes *out (ids 0..n-1, version
+ * incremented from out->version) and optional *stats.  Synchronises.
+ * Lengths < 1 are excluded and counted (DOMAIN); lengths above 2^20 ->
+ * UNSUPPORTED; n > max_history -> INVALID_ARG; no valid length -> EMPTY.    */
+ewsjf_status ewsjf_partition(ewsjf_ctx *ctx, const int32_t *d_len, int64_t n,
+                             const ewsjf_partition_params *params, ewsjf_partition_t *out,
+                             ewsjf_partition_stats *stats);
+
+/* --------------------------------------------------------------- tactical -- */
+/* Scoring part of Θ (§4.4.2): w_x(b̄) = a_x b̄ + b_x. */
+typedef struct { double a_b, b_b, a_u, b_u, a_f, b_f; } ewsjf_meta;
+/* Per-queue weights, clamped >= 0 (R8). */
+typedef struct { float w_base, w_urg, w_fair; } ewsjf_weights;
+
+/* A7 (host, O(n)): out[p] = fp32(max(0, a_x * q[p].mean + b_x)), p = position. */
+ewsjf_status ewsjf_weights_from_meta(const ewsjf_meta *theta, const ewsjf_partition_t *part,
+                                     ewsjf_weights *out);
+
+/* C_prefill(b) = c0 + c1 b + c2 b² seconds (R4) — used when d_cost is NULL. */
+typedef struct { float c0, c1, c2; } ewsjf_cost_params;
+
+typedef enum { EWSJF_SELECT_SCORE = 0, EWSJF_SELECT_FIFO = 1 } ewsjf_select_mode;
+
+/* k: per-queue selection depth (1..ctx max_k).  mode: top-k key, SCORE =
+ * (Φ desc, id asc) or FIFO = (arrival asc, id asc) (R1).  now: the clock,
+ * seconds in the same epoch as arrival (W_t = now - arrival, R5).           */
+typedef struct {
+    int32_t           k;
+    int32_t           mode;
+    float             now;
+    ewsjf_cost_params cost;
+} ewsjf_select_params;
+
+/* Device summary of one tick / selection. */
+typedef struct {
+    int32_t n_queues;      /* queues after the call (incl. bubbles created)        */
+    int32_t primary;       /* Alg. 1 ArgMax position, -1 if all empty (R24) */
+    int64_t n_invalid;     /* len < 1, unknown qid, or refused at the queue cap     */
+    int64_t n_excluded;    /* W < 0, C <= 0 or NaN                                  */
+    int64_t n_gap;         /* gap-falling requests handled by Alg. 2                */
+    int64_t n_bubbles;     /* bubble queues created (App. D)                        */
+    int64_t n_dropped;     /* gap requests refused at EWSJF_MAX_QUEUES              */
+    int32_t status;        /* ewsjf_status of the device-side work                  */
+    int32_t pad;
+} ewsjf_summary;
+
+/* Outputs of a selection (all caller-owned device buffers unless h_).
+ * d_topk_id / d_topk_score: [EWSJF_MAX_QUEUES * k], row p = queue position p,
+ *   best first, id -1 / score 0 padding.  Φ per Eq. 4 in fp32.
+ * d_count [MAXQ]: scored members per queue.  d_head_id / d_head_score [MAXQ]:
+ *   the queue head (oldest by (arrival, id), R26) and its Φ — Alg. 1's
+ *   per-queue score.  d_max_score [MAXQ]: max Φ in the queue.
+ * d_summary [1] (nullable -> ctx scratch): see ewsjf_summary.
+ * h_summary (optional): if non-NULL the call synchronises, copies the summary
+ *   and (ewsjf_tick / ewsjf_tick_merge) writes bubbles created into *part.   */
+typedef struct {
+    int64_t           *d_topk_id;
+    float             *d_topk_score;
+    int64_t           *d_count;
+    int64_t           *d_head_id;
+    float             *d_head_score;
+    float             *d_max_score;
+    ewsjf_summary     *d_summary;
+    ewsjf_summary     *h_summary;
+} ewsjf_select_out;
+
+/* A8+A9 Dispatcher (App. D Alg. 2): d_qid[r] = stable id of
+ * the queue whose [min_len, max_len) contains d_len[r]; gap-falling lengths
+ * go through Alg. 2 in pool-index order (R22) creating bubble queues of width
+ * bubble_width (>= 1) inserted into *part (in/out; ids from part->next_id,
+ * indices renumbered).  d_qid[r] = -1 for len < 1 or a request refused
+ * at the cap.  Synchronises (the host partition is updated).                */
+ewsjf_status ewsjf_route(ewsjf_ctx *ctx, const int32_t *d_len, int64_t n, ewsjf_partition_t *part,
+                         int32_t bubble_width, int32_t *d_qid, ewsjf_summary *h_summary);
+
+/* A10+A11 over an already-routed pool: Eq. 4 score of every request
+ * Φ = q_i/(b+1) (w_base + w_urg W/C + w_fair ln(b+1)) (R2-R5) with
+ * per-queue weights w[position] (d_cost NULL -> C from params->cost), then per
+ * queue count, FIFO head, top-k, max score and the ArgMax queue (Alg. 1).
+ * d_qid holds stable ids of *part (unknown / -1 -> excluded, counted). Async
+ * unless out->h_summary.                                                     */
+ewsjf_status ewsjf_score_select(ewsjf_ctx *ctx, const int32_t *d_len, const float *d_arrival,
+                                const float *d_cost, const int32_t *d_qid, int64_t n,
+                                const ewsjf_partition_t *part, const ewsjf_weights *w,
+                                const ewsjf_select_params *params, ewsjf_select_out *out);
+
+/* The fused tick: route (A8) + bubbles (A9) + weights from Θ (A7) + score (A10)
+ * + select (A11) over the whole pending pool d_len/d_arrival/d_cost[n] (d_cost
+ * may be NULL).  Request ids are global_base + r.  d_qid_out (nullable) gets
+ * the stable queue ids.  Bubbles created by this tick (App. D) are written
+ * back into *part when out->h_summary is non-NULL (synchronous call); an
+ * asynchronous call leaves *part unchanged.                                  */
+ewsjf_status ewsjf_tick(ewsjf_ctx *ctx, const int32_t *d_len, const float *d_arrival, const float *d_cost,
+                        int64_t n, int64_t global_base, ewsjf_partition_t *part, int32_t bubble_width,
+                        const ewsjf_meta *theta, const ewsjf_select_params *params,
+                        int32_t *d_qid_out, ewsjf_select_out *out);
+
+/* Host-buffer variant of ewsjf_tick for end-to-end use: copies h_len /
+ * h_arrival / h_cost[n] (pinned host memory recommended) into ctx scratch,
+ * runs the tick, copies qid into h_qid_out[n] (nullable) and the per-queue
+ * results into the h_ arrays (same layouts as ewsjf_select_out, host side;
+ * each nullable) and the summary into *h_summary (required).  Synchronises. */
+ewsjf_status ewsjf_tick_host(ewsjf_ctx *ctx, const int32_t *h_len, const float *h_arrival, const float *h_cost,
+                             int64_t n, int64_t global_base, ewsjf_partition_t *part, int32_t bubble_width,
+                             const ewsjf_meta *theta, const ewsjf_select_params *params,
+                             int32_t *h_qid_out, int64_t *h_topk_id, float *h_topk_score, int64_t *h_count,
+                             int64_t *h_head_id, float *h_head_score, float *h_max_score,
+                             ewsjf_summary *h_summary);
+
+/* ------------------------------------------------- multi-GPU --- */
+/* Rank-local half of a sharded tick.  The pool is sharded by index: this rank
+ * owns global ids [global_base, global_base + n).  Routes, scores and reduces
+ * its shard to a fixed-size exchange record written to d_exchange
+ * (ewsjf_exchange_bytes(ctx, part->n, k) bytes, 256-byte aligned): per-queue
+ * top-k keys with their scores, member counts, head candidates and the
+ * shard's gap requests (capacity-bounded).  The caller all-gathers the
+ * records of all ranks (NCCL over NVLink) and calls ewsjf_tick_merge.       */
+int64_t      ewsjf_exchange_bytes(const ewsjf_ctx *ctx, int32_t n_queues, int32_t k);
+ewsjf_status ewsjf_tick_local(ewsjf_ctx *ctx, const int32_t *d_len, const float *d_arrival, const float *d_cost,
+                              int64_t n, int64_t global_base, const ewsjf_partition_t *part,
+                              const ewsjf_meta *theta, const ewsjf_select_params *params,
+                              int32_t *d_qid_out, void *d_exchange);
+/* Global half: merges `world` exchange records (contiguous, rank order) into
+ * the replicated global result (identical on every rank), running Alg. 2 over
+ * the union of gap requests in global index order (R22) and writing this
+ * rank's gap requests' qids into d_qid_local[0..n_local) (global ids
+ * [global_base, global_base + n_local)).                                     */
+ewsjf_status ewsjf_tick_merge(ewsjf_ctx *ctx, const void *d_exchange_all, int32_t world,
+                              int64_t global_base, int64_t n_local, int32_t *d_qid_local,
+                              ewsjf_partition_t *part, int32_t bubble_width, const ewsjf_meta *theta,
+                              const ewsjf_select_params *params, ewsjf_select_out *out);
+
+/* ----------------------------------------------- Θ sweep (A12, config C5) --- */
+/* For each of n_theta meta-parameter vectors (§4.4.2): A7 -> A10 ->
+ * A11 over one routed snapshot.  outs[t] receives the selection for thetas[t]
+ * (device buffers as in ewsjf_select_out; h_summary ignored).  Async.        */
+ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx *ctx, const int32_t *d_len, const float *d_arrival,
+                                      const float *d_cost, const int32_t *d_qid, int64_t n,
+                                      const ewsjf_partition_t *part, const ewsjf_meta *thetas,
+                                      int32_t n_theta, const ewsjf_select_params *params,
+                                      ewsjf_select_out *outs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EWSJF_H */

@@ -119,6 +119,8 @@ def lib():
                                    P(SelectParams), P(C.c_double)]
         L.or_score_select.argtypes = [P(C.c_int32), P(C.c_float), P(C.c_float), P(C.c_int32), C.c_int64,
                                       C.c_int64, P(Partition), P(C.c_float), P(SelectParams), P(SelectOut)]
+        L.or_score_all.argtypes = [P(C.c_int32), P(C.c_float), P(C.c_float), P(C.c_int32), C.c_int64, P(Partition),
+                                   P(C.c_float), P(SelectParams), P(C.c_double), P(C.c_int8)]
         L.or_tick.argtypes = [P(C.c_int32), P(C.c_float), P(C.c_float), C.c_int64, C.c_int64, P(Partition),
                               C.c_int32, P(Meta), P(SelectParams), P(C.c_int32), P(SelectOut)]
     return _lib
@@ -302,6 +304,20 @@ def score_select(lengths, arrival, cost, qid, part: Partition, w, sp: SelectPara
                               _p(q, C.c_int32), len(x), global_base, C.byref(part), _p(wf, C.c_float),
                               C.byref(sp), C.byref(o.s))
     return o.result(part.n, sp.k, s, part)
+
+
+def score_all(lengths, arrival, cost, qid, part: Partition, theta: Meta, sp: SelectParams):
+    """O9 for every request of a routed pool with weights O7(theta, queue mean): (phi, valid)."""
+    x = _i32(lengths); a = _f32(arrival); q = _i32(qid)
+    cst = _f32(cost) if cost is not None else None
+    w = np.concatenate([weights(theta, part.q[i].mean) for i in range(part.n)] or [np.zeros(0, np.float32)])
+    w = _f32(w)
+    phi = np.zeros(max(len(x), 1), np.float64)
+    valid = np.zeros(max(len(x), 1), np.int8)
+    lib().or_score_all(_p(x, C.c_int32), _p(a, C.c_float), _p(cst, C.c_float) if cst is not None else None,
+                       _p(q, C.c_int32), len(x), C.byref(part), _p(w, C.c_float) if len(w) else None,
+                       C.byref(sp), _p(phi, C.c_double), _p(valid, C.c_int8))
+    return phi[: len(x)], valid[: len(x)].astype(bool)
 
 
 def tick(lengths, arrival, cost, part: Partition, theta: Meta, sp: SelectParams, bubble_width=64, global_base=0):

@@ -474,3 +474,20 @@ int or_tick(const int32_t *len, const float *arrival, const float *cost, int64_t
     if (ss == OR_DOMAIN || inv) return OR_DOMAIN;
     return ss;
 }
+
+/* O9 over a routed pool (for comparators): phi[r] and valid[r] per request. */
+void or_score_all(const int32_t *len, const float *arrival, const float *cost, const int32_t *qid, int64_t n,
+                  const or_partition *part, const float *w, const or_select_params *sp,
+                  double *phi, int8_t *valid) {
+    for (int64_t r = 0; r < n; r++) {
+        valid[r] = 0; phi[r] = 0.0;
+        if (qid[r] < 0 || len[r] < 1) continue;
+        int32_t p = -1;
+        for (int32_t i = 0; i < part->n; i++) if (part->q[i].id == qid[r]) { p = i; break; }
+        if (p < 0) continue;
+        double f;
+        if (!or_score_one(len[r], arrival[r], cost ? &cost[r] : NULL, part->q[p].index, &w[3 * p], sp, &f)) {
+            phi[r] = f; valid[r] = 1;
+        }
+    }
+}

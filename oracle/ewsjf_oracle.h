@@ -153,6 +153,11 @@ int     or_score_select(const int32_t *len, const float *arrival, const float *c
                         const or_partition *part, const float *w,
                         const or_select_params *sp, or_select_out *out);
 
+/* O9 over a routed pool: phi[r] (fp64) and valid[r] (1 = scored). */
+void    or_score_all(const int32_t *len, const float *arrival, const float *cost, const int32_t *qid, int64_t n,
+                     const or_partition *part, const float *w, const or_select_params *sp,
+                     double *phi, int8_t *valid);
+
 /* O8 + O7 + O9 + O10: one tick (part is in/out: bubbles). */
 int     or_tick(const int32_t *len, const float *arrival, const float *cost, int64_t n,
                 int64_t global_base, or_partition *part, int32_t bubble_width,

@@ -1,0 +1,593 @@
+// api.cu — C ABI of libewsjf (include/ewsjf.h): context, policy upload,
+// launch orchestration of the tick / score_select / route / sharded tick.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+#include "tick.cuh"
+
+namespace ewsjf {
+cudaError_t launch_partial(const PartialArgs& A, const Policy& P, bool route, bool has_cost, bool use_lut, int grid,
+                           cudaStream_t st);
+int64_t partial_smem_bytes(bool route, bool has_cost, bool tma, int lut_size, int nslots, int nids, int pass0, int ngs,
+                           int cap);
+cudaError_t launch_merge(const MergeArgs& A, const Policy& P, bool has_cost, int grid, cudaStream_t st);
+int64_t merge_smem_total(int in_mode);
+}  // namespace ewsjf
+
+using namespace ewsjf;
+
+struct ewsjf_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t max_pool = 0, max_history = 0;
+    int32_t max_k = 0;
+    int num_sms = 0;
+    int smem_optin = 0;
+    int32_t cap_max = 0;
+    char err[512] = {0};
+    // scratch
+    Rows rows{};
+    u64* gthr = nullptr;
+    Counters* ctr = nullptr;
+    GapEntry* gap = nullptr;
+    int32_t gap_cap = 8192;
+    BubbleLog* d_blog = nullptr;
+    BubbleLog* h_blog = nullptr;        // pinned
+    ewsjf_summary* d_summary = nullptr;
+    ewsjf_summary* h_summary = nullptr; // pinned
+    // host-variant staging (tick_host)
+    int32_t* d_len = nullptr;
+    float* d_arr = nullptr;
+    float* d_cost = nullptr;
+    int32_t* d_qid = nullptr;
+    int64_t* d_topk_id = nullptr;
+    float* d_topk_score = nullptr;
+    int64_t* d_count = nullptr;
+    int64_t* d_head_id = nullptr;
+    float* d_head_score = nullptr;
+    float* d_max_score = nullptr;
+    // partition (R&P) scratch lives in partition.cu
+    void* rp = nullptr;
+};
+
+namespace ewsjf {
+void rp_free(ewsjf_ctx* ctx);
+}
+
+static ewsjf_status fail(ewsjf_ctx* ctx, ewsjf_status s, const char* fmt, ...) {
+    if (ctx) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(ctx->err, sizeof ctx->err, fmt, ap);
+        va_end(ap);
+    }
+    return s;
+}
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(ctx, EWSJF_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                       \
+    } while (0)
+
+// ------------------------------------------------------------------ misc ---
+extern "C" int ewsjf_abi_version(void) { return EWSJF_ABI_VERSION; }
+
+extern "C" const char* ewsjf_status_str(ewsjf_status s) {
+    switch (s) {
+        case EWSJF_OK: return "ok";
+        case EWSJF_ERR_INVALID_ARG: return "invalid argument";
+        case EWSJF_ERR_DOMAIN: return "domain error (elements excluded)";
+        case EWSJF_ERR_EMPTY: return "empty input";
+        case EWSJF_ERR_CAPACITY: return "capacity exceeded";
+        case EWSJF_ERR_CUDA: return "CUDA error";
+        case EWSJF_ERR_UNSUPPORTED: return "unsupported input";
+    }
+    return "unknown status";
+}
+
+extern "C" const char* ewsjf_last_error(const ewsjf_ctx* ctx) { return ctx ? ctx->err : "null ctx"; }
+
+extern "C" int32_t ewsjf_ctx_num_ctas(const ewsjf_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
+
+static int32_t cap_for(int32_t K) {
+    int32_t c = std::max(2 * K, 64);
+    return (c + 31) & ~31;
+}
+
+// --------------------------------------------------------------- context ---
+extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t max_pool, int64_t max_history,
+                                         int32_t max_k, ewsjf_ctx** out) {
+    if (!out || max_pool < 0 || max_history < 0 || max_k < 1 || max_k > EWSJF_MAX_K || max_pool >= 0xffffffffll)
+        return EWSJF_ERR_INVALID_ARG;
+    *out = nullptr;
+    ewsjf_ctx* ctx = new ewsjf_ctx();
+    ctx->device = device;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    ctx->max_pool = max_pool;
+    ctx->max_history = max_history;
+    ctx->max_k = max_k;
+    ctx->cap_max = cap_for(max_k);
+    auto bad = [&](ewsjf_status s) { ewsjf_ctx_destroy(ctx); return s; };
+    if (cudaSetDevice(device) != cudaSuccess) return bad(EWSJF_ERR_CUDA);
+    if (cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+        return bad(EWSJF_ERR_CUDA);
+    cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    const int G = ctx->num_sms;
+    const size_t nrow = (size_t)kMaxSlots * G;
+    bool ok = cudaMalloc(&ctx->rows.keys, nrow * ctx->cap_max * sizeof(u64)) == cudaSuccess &&
+              cudaMalloc(&ctx->rows.cnt, nrow * sizeof(int32_t)) == cudaSuccess &&
+              cudaMalloc(&ctx->rows.members, nrow * sizeof(int64_t)) == cudaSuccess &&
+              cudaMalloc(&ctx->rows.sec, nrow * sizeof(u64)) == cudaSuccess &&
+              cudaMalloc(&ctx->gthr, kMaxSlots * sizeof(u64)) == cudaSuccess &&
+              cudaMalloc(&ctx->ctr, sizeof(Counters)) == cudaSuccess &&
+              cudaMalloc(&ctx->gap, (size_t)ctx->gap_cap * sizeof(GapEntry)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_blog, sizeof(BubbleLog)) == cudaSuccess &&
+              cudaMallocHost(&ctx->h_blog, sizeof(BubbleLog)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_summary, sizeof(ewsjf_summary)) == cudaSuccess &&
+              cudaMallocHost(&ctx->h_summary, sizeof(ewsjf_summary)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_topk_id, (size_t)kMaxSlots * max_k * 8) == cudaSuccess &&
+              cudaMalloc(&ctx->d_topk_score, (size_t)kMaxSlots * max_k * 4) == cudaSuccess &&
+              cudaMalloc(&ctx->d_count, kMaxSlots * 8) == cudaSuccess &&
+              cudaMalloc(&ctx->d_head_id, kMaxSlots * 8) == cudaSuccess &&
+              cudaMalloc(&ctx->d_head_score, kMaxSlots * 4) == cudaSuccess &&
+              cudaMalloc(&ctx->d_max_score, kMaxSlots * 4) == cudaSuccess;
+    if (ok && max_pool > 0) {
+        ok = cudaMalloc(&ctx->d_len, (size_t)max_pool * 4) == cudaSuccess &&
+             cudaMalloc(&ctx->d_arr, (size_t)max_pool * 4) == cudaSuccess &&
+             cudaMalloc(&ctx->d_cost, (size_t)max_pool * 4) == cudaSuccess &&
+             cudaMalloc(&ctx->d_qid, (size_t)max_pool * 4) == cudaSuccess;
+    }
+    if (!ok) return bad(EWSJF_ERR_CUDA);
+    ok = cudaMemset(ctx->gthr, 0, kMaxSlots * sizeof(u64)) == cudaSuccess &&
+         cudaMemset(ctx->ctr, 0, sizeof(Counters)) == cudaSuccess &&
+         cudaMemset(ctx->rows.cnt, 0, nrow * sizeof(int32_t)) == cudaSuccess &&
+         cudaMemset(ctx->rows.members, 0, nrow * sizeof(int64_t)) == cudaSuccess &&
+         cudaMemset(ctx->rows.sec, 0, nrow * sizeof(u64)) == cudaSuccess &&
+         cudaDeviceSynchronize() == cudaSuccess;
+    if (!ok) return bad(EWSJF_ERR_CUDA);
+    ctx->rows.G = G;
+    *out = ctx;
+    return EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_ctx_set_stream(ewsjf_ctx* ctx, void* cuda_stream) {
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    return EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
+    if (!ctx) return EWSJF_OK;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    void* d[] = {ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->ctr, ctx->gap,
+                 ctx->d_blog, ctx->d_summary, ctx->d_len, ctx->d_arr, ctx->d_cost, ctx->d_qid, ctx->d_topk_id,
+                 ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score, ctx->d_max_score};
+    for (void* p : d)
+        if (p) cudaFree(p);
+    if (ctx->h_blog) cudaFreeHost(ctx->h_blog);
+    if (ctx->h_summary) cudaFreeHost(ctx->h_summary);
+    rp_free(ctx);
+    delete ctx;
+    return EWSJF_OK;
+}
+
+// ---------------------------------------------------------------- policy ---
+static ewsjf_status check_partition(ewsjf_ctx* ctx, const ewsjf_partition_t* part) {
+    if (!part) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null partition");
+    if (part->n < 0 || part->n > EWSJF_MAX_QUEUES) return fail(ctx, EWSJF_ERR_INVALID_ARG, "partition n=%d", part->n);
+    for (int i = 0; i < part->n; i++) {
+        const ewsjf_queue& q = part->q[i];
+        if (q.min_len >= q.max_len) return fail(ctx, EWSJF_ERR_INVALID_ARG, "queue %d: min_len >= max_len", i);
+        if (i > 0 && part->q[i - 1].max_len > q.min_len)
+            return fail(ctx, EWSJF_ERR_INVALID_ARG, "queues %d,%d overlap or are unsorted", i - 1, i);
+        if (q.id < 0 || q.id >= part->next_id)
+            return fail(ctx, EWSJF_ERR_INVALID_ARG, "queue %d: id %d outside [0, next_id)", i, q.id);
+    }
+    for (int i = 0; i < part->n; i++)
+        for (int j = i + 1; j < part->n; j++)
+            if (part->q[i].id == part->q[j].id) return fail(ctx, EWSJF_ERR_INVALID_ARG, "duplicate queue id");
+    return EWSJF_OK;
+}
+
+// A7 on the host: w_x = fp32(max(0, a_x * b̄ + b_x)), fp64 with
+// no contraction (this file is compiled with -fmad=false for host code too).
+static inline float clamp_w(double a, double mean, double b) {
+    volatile double t = a * mean;
+    double v = t + b;
+    return (float)(v > 0.0 ? v : 0.0);
+}
+
+extern "C" ewsjf_status ewsjf_weights_from_meta(const ewsjf_meta* th, const ewsjf_partition_t* part,
+                                                ewsjf_weights* out) {
+    if (!th || !part || !out || part->n < 0 || part->n > EWSJF_MAX_QUEUES) return EWSJF_ERR_INVALID_ARG;
+    for (int i = 0; i < part->n; i++) {
+        const double m = part->q[i].mean;
+        out[i].w_base = clamp_w(th->a_b, m, th->b_b);
+        out[i].w_urg = clamp_w(th->a_u, m, th->b_u);
+        out[i].w_fair = clamp_w(th->a_f, m, th->b_f);
+    }
+    return EWSJF_OK;
+}
+
+static void fill_policy(const ewsjf_partition_t* part, const ewsjf_weights* w, Policy* P) {
+    memset(P, 0, sizeof *P);
+    P->nslots = part->n;
+    for (int i = 0; i < part->n; i++) {
+        P->min_len[i] = part->q[i].min_len;
+        P->max_len[i] = part->q[i].max_len;
+        P->sid[i] = part->q[i].id;
+        P->wb[i] = w[i].w_base;
+        P->wu[i] = w[i].w_urg;
+        volatile double f = (double)w[i].w_fair * 0.69314718055994530942;
+        P->wf[i] = (float)f;
+    }
+}
+
+static ewsjf_status check_select(ewsjf_ctx* ctx, const ewsjf_select_params* sp) {
+    if (!sp) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null select params");
+    if (sp->k < 1 || sp->k > ctx->max_k) return fail(ctx, EWSJF_ERR_INVALID_ARG, "k=%d outside 1..%d", sp->k, ctx->max_k);
+    if (sp->mode != EWSJF_SELECT_SCORE && sp->mode != EWSJF_SELECT_FIFO)
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad select mode");
+    return EWSJF_OK;
+}
+
+static ScoreParams score_params(const ewsjf_select_params* sp) {
+    ScoreParams s;
+    s.now = sp->now;
+    s.c0 = sp->cost.c0;
+    s.c1 = sp->cost.c1;
+    s.c2 = sp->cost.c2;
+    s.mode = sp->mode;
+    s.k = sp->k;
+    return s;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// Run the partial pass(es) of a tick / score_select / route over [len, n).
+static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, const float* d_cost,
+                                const int32_t* d_qid_in, int32_t* d_qid_out, int64_t n, int64_t gbase,
+                                const ewsjf_partition_t* part, const Policy& P, const ewsjf_select_params* sp,
+                                bool route, bool select) {
+    const int nslots = part->n;
+    const bool has_cost = d_cost != nullptr;
+    const int K = select ? sp->k : 1;
+    const int cap = cap_for(K);
+    PartialArgs A;
+    memset(&A, 0, sizeof A);
+    A.len = d_len;
+    A.arrival = d_arr;
+    A.cost = d_cost;
+    A.qid_in = d_qid_in;
+    A.qid_out = d_qid_out;
+    A.n = n;
+    A.gbase = (uint32_t)gbase;
+    A.tma = aligned16(d_len) && aligned16(d_arr) && (!has_cost || aligned16(d_cost)) &&
+            (route ? (!d_qid_out || aligned16(d_qid_out)) : aligned16(d_qid_in));
+    A.K = K;
+    A.cap = cap;
+    A.tgt = (K + cap) / 2;
+    A.select = select ? 1 : 0;
+    A.sp = select ? score_params(sp) : ScoreParams{0.f, 0.f, 0.f, 0.f, 0, 1};
+    A.rows = ctx->rows;
+    A.rows.cap = cap;
+    A.gthr = ctx->gthr;
+    A.gap = ctx->gap;
+    A.gap_cap = ctx->gap_cap;
+    A.ctr = ctx->ctr;
+    bool use_lut = false;
+    if (route && nslots > 0 && nslots <= 250 && part->q[nslots - 1].max_len <= kLutCap) {
+        use_lut = true;
+        A.lut_size = part->q[nslots - 1].max_len;
+    }
+    if (!route) {
+        std::vector<std::pair<int, int>> ids;
+        for (int i = 0; i < nslots; i++) ids.push_back({part->q[i].id, i});
+        std::sort(ids.begin(), ids.end());
+        A.nids = nslots;
+        for (int i = 0; i < nslots; i++) { A.sorted_ids[i] = ids[i].first; A.sorted_slot[i] = ids[i].second; }
+    }
+    // slot groups so that the candidate buffers fit in shared memory
+    int ngs = std::max(nslots, 1);
+    const int budget = ctx->smem_optin > 0 ? ctx->smem_optin : 232448;
+    while (ngs > 1 && partial_smem_bytes(route, has_cost, A.tma, use_lut ? A.lut_size : 0, nslots, A.nids, 1, ngs,
+                                         cap) > budget)
+        ngs = (ngs + 1) / 2;
+    if (partial_smem_bytes(route, has_cost, A.tma, use_lut ? A.lut_size : 0, nslots, A.nids, 1, ngs, cap) > budget)
+        return fail(ctx, EWSJF_ERR_UNSUPPORTED, "tick does not fit shared memory (k=%d)", K);
+    const int passes = select ? std::max(1, (nslots + ngs - 1) / ngs) : 1;
+    for (int p = 0; p < passes; p++) {
+        A.pass0 = p == 0;
+        A.g_lo = select ? std::min(nslots, p * ngs) : 0;
+        A.g_hi = select ? std::min(nslots, (p + 1) * ngs) : 0;
+        cudaError_t e = launch_partial(A, P, route, has_cost, use_lut, ctx->num_sms, ctx->stream);
+        if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "partial kernel: %s", cudaGetErrorString(e));
+    }
+    return EWSJF_OK;
+}
+
+static MergeArgs merge_args(ewsjf_ctx* ctx, const ewsjf_partition_t* part, const ewsjf_select_params* sp,
+                            const ewsjf_meta* theta, int32_t bubble_width) {
+    MergeArgs M;
+    memset(&M, 0, sizeof M);
+    M.K = sp ? sp->k : 1;
+    M.nq = part->n;
+    M.next_id = part->next_id;
+    M.bubble_width = bubble_width;
+    M.sp = sp ? score_params(sp) : ScoreParams{0.f, 0.f, 0.f, 0.f, 0, 1};
+    if (theta) {
+        M.theta[0] = theta->a_b; M.theta[1] = theta->b_b; M.theta[2] = theta->a_u;
+        M.theta[3] = theta->b_u; M.theta[4] = theta->a_f; M.theta[5] = theta->b_f;
+    }
+    M.rows = ctx->rows;
+    M.rows.cap = cap_for(M.K);
+    M.ctr = ctx->ctr;
+    M.gap = ctx->gap;
+    M.gap_cap = ctx->gap_cap;
+    M.gthr = ctx->gthr;
+    M.blog = ctx->d_blog;
+    return M;
+}
+
+static int merge_grid(ewsjf_ctx* ctx, int nq, bool may_bubble) {
+    int g = nq + (may_bubble ? 8 : 0);
+    g = std::max(g, 1);
+    return std::min(g, ctx->num_sms);
+}
+
+// Replay the device bubble log into the host partition.
+static void apply_bubbles(const BubbleLog* log, ewsjf_partition_t* part) {
+    if (!log || log->n <= 0) return;
+    for (int b = 0; b < log->n; b++) {
+        const int pos = log->pos[b];
+        for (int i = part->n; i > pos; i--) part->q[i] = part->q[i - 1];
+        ewsjf_queue& q = part->q[pos];
+        memset(&q, 0, sizeof q);
+        q.id = part->next_id++;
+        q.min_len = log->lo[b];
+        q.max_len = log->hi[b];
+        q.mean = (double)log->L[b];
+        q.is_bubble = 1;
+        part->n++;
+    }
+    for (int i = 0; i < part->n; i++) part->q[i].index = i + 1;
+    part->version++;
+}
+
+static ewsjf_status finish_sync(ewsjf_ctx* ctx, ewsjf_partition_t* part_update, ewsjf_summary* h_out,
+                                const ewsjf_summary* d_sum) {
+    CU(cudaMemcpyAsync(ctx->h_summary, d_sum, sizeof(ewsjf_summary), cudaMemcpyDeviceToHost, ctx->stream));
+    if (part_update) CU(cudaMemcpyAsync(ctx->h_blog, ctx->d_blog, sizeof(BubbleLog), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (h_out) *h_out = *ctx->h_summary;
+    if (part_update && ctx->h_summary->n_bubbles > 0) apply_bubbles(ctx->h_blog, part_update);
+    return (ewsjf_status)ctx->h_summary->status;
+}
+
+static ewsjf_status check_out(ewsjf_ctx* ctx, const ewsjf_select_out* out) {
+    if (!out || !out->d_topk_id || !out->d_topk_score || !out->d_count || !out->d_head_id || !out->d_head_score ||
+        !out->d_max_score)
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "select outputs must all be non-NULL device buffers");
+    return EWSJF_OK;
+}
+
+static ewsjf_status tick_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, const float* d_cost, int64_t n,
+                              int64_t gbase, ewsjf_partition_t* part, int32_t bubble_width, const ewsjf_meta* theta,
+                              const ewsjf_select_params* sp, int32_t* d_qid_out, const ewsjf_select_out* out) {
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    ewsjf_status s;
+    if ((s = check_partition(ctx, part)) != EWSJF_OK) return s;
+    if ((s = check_select(ctx, sp)) != EWSJF_OK) return s;
+    if ((s = check_out(ctx, out)) != EWSJF_OK) return s;
+    if (!theta) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null theta");
+    if (bubble_width < 1) return fail(ctx, EWSJF_ERR_INVALID_ARG, "bubble_width < 1");
+    if (n < 0 || (n > 0 && (!d_len || !d_arr))) return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad pool");
+    if (gbase < 0 || gbase + n >= 0xffffffffll) return fail(ctx, EWSJF_ERR_INVALID_ARG, "global ids must be < 2^32-1");
+    CU(cudaSetDevice(ctx->device));
+    ewsjf_weights w[EWSJF_MAX_QUEUES];
+    ewsjf_weights_from_meta(theta, part, w);
+    static thread_local Policy P;
+    fill_policy(part, w, &P);
+    if ((s = run_partial(ctx, d_len, d_arr, d_cost, nullptr, d_qid_out, n, gbase, part, P, sp, true, true)) != EWSJF_OK)
+        return s;
+    MergeArgs M = merge_args(ctx, part, sp, theta, bubble_width);
+    M.in_mode = MERGE_IN_ROWS;
+    M.out_mode = MERGE_OUT_FINAL;
+    M.len = d_len; M.arrival = d_arr; M.cost = d_cost;
+    M.gbase = (uint32_t)gbase;
+    M.n_local = n;
+    M.topk_id = out->d_topk_id; M.topk_score = out->d_topk_score; M.count = out->d_count;
+    M.head_id = out->d_head_id; M.head_score = out->d_head_score; M.max_score = out->d_max_score;
+    M.summary = out->d_summary ? out->d_summary : ctx->d_summary;
+    M.qid = d_qid_out;
+    cudaError_t e = launch_merge(M, P, d_cost != nullptr, merge_grid(ctx, part->n, true), ctx->stream);
+    if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "merge kernel: %s", cudaGetErrorString(e));
+    if (out->h_summary) return finish_sync(ctx, part, out->h_summary, M.summary);
+    return EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_tick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arrival, const float* d_cost,
+                                   int64_t n, int64_t global_base, ewsjf_partition_t* part, int32_t bubble_width,
+                                   const ewsjf_meta* theta, const ewsjf_select_params* params, int32_t* d_qid_out,
+                                   ewsjf_select_out* out) {
+    return tick_impl(ctx, d_len, d_arrival, d_cost, n, global_base, part, bubble_width, theta, params, d_qid_out, out);
+}
+
+extern "C" ewsjf_status ewsjf_tick_host(ewsjf_ctx* ctx, const int32_t* h_len, const float* h_arrival,
+                                        const float* h_cost, int64_t n, int64_t global_base, ewsjf_partition_t* part,
+                                        int32_t bubble_width, const ewsjf_meta* theta,
+                                        const ewsjf_select_params* params, int32_t* h_qid_out, int64_t* h_topk_id,
+                                        float* h_topk_score, int64_t* h_count, int64_t* h_head_id,
+                                        float* h_head_score, float* h_max_score, ewsjf_summary* h_summary) {
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    if (!h_summary) return fail(ctx, EWSJF_ERR_INVALID_ARG, "h_summary required");
+    if (n < 0 || n > ctx->max_pool) return fail(ctx, EWSJF_ERR_INVALID_ARG, "n=%lld > max_pool", (long long)n);
+    if (n > 0 && (!h_len || !h_arrival)) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null host pool");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    if (n > 0) {
+        CU(cudaMemcpyAsync(ctx->d_len, h_len, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(ctx->d_arr, h_arrival, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+        if (h_cost) CU(cudaMemcpyAsync(ctx->d_cost, h_cost, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    }
+    ewsjf_select_out out{ctx->d_topk_id, ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score,
+                         ctx->d_max_score, ctx->d_summary, nullptr};
+    ewsjf_status s = tick_impl(ctx, ctx->d_len, ctx->d_arr, h_cost ? ctx->d_cost : nullptr, n, global_base, part,
+                               bubble_width, theta, params, ctx->d_qid, &out);
+    if (s != EWSJF_OK) return s;
+    const int K = params->k;
+    if (h_qid_out && n > 0) CU(cudaMemcpyAsync(h_qid_out, ctx->d_qid, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    if (h_topk_id) CU(cudaMemcpyAsync(h_topk_id, ctx->d_topk_id, (size_t)kMaxSlots * K * 8, cudaMemcpyDeviceToHost, st));
+    if (h_topk_score)
+        CU(cudaMemcpyAsync(h_topk_score, ctx->d_topk_score, (size_t)kMaxSlots * K * 4, cudaMemcpyDeviceToHost, st));
+    if (h_count) CU(cudaMemcpyAsync(h_count, ctx->d_count, kMaxSlots * 8, cudaMemcpyDeviceToHost, st));
+    if (h_head_id) CU(cudaMemcpyAsync(h_head_id, ctx->d_head_id, kMaxSlots * 8, cudaMemcpyDeviceToHost, st));
+    if (h_head_score) CU(cudaMemcpyAsync(h_head_score, ctx->d_head_score, kMaxSlots * 4, cudaMemcpyDeviceToHost, st));
+    if (h_max_score) CU(cudaMemcpyAsync(h_max_score, ctx->d_max_score, kMaxSlots * 4, cudaMemcpyDeviceToHost, st));
+    return finish_sync(ctx, part, h_summary, ctx->d_summary);
+}
+
+extern "C" ewsjf_status ewsjf_score_select(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arrival,
+                                           const float* d_cost, const int32_t* d_qid, int64_t n,
+                                           const ewsjf_partition_t* part, const ewsjf_weights* w,
+                                           const ewsjf_select_params* sp, ewsjf_select_out* out) {
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    ewsjf_status s;
+    if ((s = check_partition(ctx, part)) != EWSJF_OK) return s;
+    if ((s = check_select(ctx, sp)) != EWSJF_OK) return s;
+    if ((s = check_out(ctx, out)) != EWSJF_OK) return s;
+    if (!w) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null weights");
+    if (n < 0 || (n > 0 && (!d_len || !d_arrival || !d_qid))) return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad pool");
+    if (n >= 0xffffffffll) return fail(ctx, EWSJF_ERR_INVALID_ARG, "pool too large");
+    for (int i = 0; i < part->n; i++)
+        if (!(w[i].w_base >= 0.f && w[i].w_urg >= 0.f && w[i].w_fair >= 0.f))
+            return fail(ctx, EWSJF_ERR_INVALID_ARG, "weights must be >= 0 (S:306)");
+    CU(cudaSetDevice(ctx->device));
+    static thread_local Policy P;
+    fill_policy(part, w, &P);
+    if ((s = run_partial(ctx, d_len, d_arrival, d_cost, d_qid, nullptr, n, 0, part, P, sp, false, true)) != EWSJF_OK)
+        return s;
+    MergeArgs M = merge_args(ctx, part, sp, nullptr, 1);
+    M.in_mode = MERGE_IN_ROWS;
+    M.out_mode = MERGE_OUT_FINAL;
+    M.len = d_len; M.arrival = d_arrival; M.cost = d_cost;
+    M.n_local = n;
+    M.topk_id = out->d_topk_id; M.topk_score = out->d_topk_score; M.count = out->d_count;
+    M.head_id = out->d_head_id; M.head_score = out->d_head_score; M.max_score = out->d_max_score;
+    M.summary = out->d_summary ? out->d_summary : ctx->d_summary;
+    M.blog = nullptr;
+    cudaError_t e = launch_merge(M, P, d_cost != nullptr, merge_grid(ctx, part->n, false), ctx->stream);
+    if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "merge kernel: %s", cudaGetErrorString(e));
+    if (out->h_summary) return finish_sync(ctx, nullptr, out->h_summary, M.summary);
+    return EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_route(ewsjf_ctx* ctx, const int32_t* d_len, int64_t n, ewsjf_partition_t* part,
+                                    int32_t bubble_width, int32_t* d_qid, ewsjf_summary* h_summary) {
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    ewsjf_status s;
+    if ((s = check_partition(ctx, part)) != EWSJF_OK) return s;
+    if (bubble_width < 1) return fail(ctx, EWSJF_ERR_INVALID_ARG, "bubble_width < 1");
+    if (n < 0 || (n > 0 && (!d_len || !d_qid))) return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad pool");
+    if (n >= 0xffffffffll) return fail(ctx, EWSJF_ERR_INVALID_ARG, "pool too large");
+    CU(cudaSetDevice(ctx->device));
+    ewsjf_weights w[EWSJF_MAX_QUEUES];
+    memset(w, 0, sizeof w);
+    static thread_local Policy P;
+    fill_policy(part, w, &P);
+    // route-only pass: arrival is not read (the TMA path loads it; pass len as a dummy 16B-aligned source)
+    if ((s = run_partial(ctx, d_len, (const float*)d_len, nullptr, nullptr, d_qid, n, 0, part, P, nullptr, true,
+                         false)) != EWSJF_OK)
+        return s;
+    MergeArgs M = merge_args(ctx, part, nullptr, nullptr, bubble_width);
+    M.in_mode = MERGE_IN_ROWS;
+    M.out_mode = MERGE_OUT_ROUTE;
+    M.n_local = n;
+    M.qid = d_qid;
+    M.summary = ctx->d_summary;
+    cudaError_t e = launch_merge(M, P, false, 1, ctx->stream);
+    if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "merge kernel: %s", cudaGetErrorString(e));
+    ewsjf_summary tmp;
+    return finish_sync(ctx, part, h_summary ? h_summary : &tmp, ctx->d_summary);
+}
+
+// ---------------------------------------------------------- sharded tick ---
+extern "C" int64_t ewsjf_exchange_bytes(const ewsjf_ctx* ctx, int32_t n_queues, int32_t k) {
+    (void)ctx;
+    if (n_queues < 0 || n_queues > EWSJF_MAX_QUEUES || k < 1 || k > EWSJF_MAX_K) return -1;
+    return ex_layout(n_queues, k).total;
+}
+
+extern "C" ewsjf_status ewsjf_tick_local(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arrival,
+                                         const float* d_cost, int64_t n, int64_t global_base,
+                                         const ewsjf_partition_t* part, const ewsjf_meta* theta,
+                                         const ewsjf_select_params* sp, int32_t* d_qid_out, void* d_exchange) {
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    ewsjf_status s;
+    if ((s = check_partition(ctx, part)) != EWSJF_OK) return s;
+    if ((s = check_select(ctx, sp)) != EWSJF_OK) return s;
+    if (!theta || !d_exchange || ((uintptr_t)d_exchange & 255)) return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad theta/exchange");
+    if (n < 0 || (n > 0 && (!d_len || !d_arrival))) return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad pool");
+    if (global_base < 0 || global_base + n >= 0xffffffffll) return fail(ctx, EWSJF_ERR_INVALID_ARG, "ids >= 2^32-1");
+    CU(cudaSetDevice(ctx->device));
+    ewsjf_weights w[EWSJF_MAX_QUEUES];
+    ewsjf_weights_from_meta(theta, part, w);
+    static thread_local Policy P;
+    fill_policy(part, w, &P);
+    if ((s = run_partial(ctx, d_len, d_arrival, d_cost, nullptr, d_qid_out, n, global_base, part, P, sp, true,
+                         true)) != EWSJF_OK)
+        return s;
+    CU(cudaMemsetAsync(d_exchange, 0, ex_layout(part->n, sp->k).total, ctx->stream));
+    MergeArgs M = merge_args(ctx, part, sp, theta, 1);
+    M.in_mode = MERGE_IN_ROWS;
+    M.out_mode = MERGE_OUT_EXCHANGE;
+    M.len = d_len; M.arrival = d_arrival; M.cost = d_cost;
+    M.gbase = (uint32_t)global_base;
+    M.n_local = n;
+    M.ex_out = (unsigned char*)d_exchange;
+    M.blog = nullptr;
+    cudaError_t e = launch_merge(M, P, d_cost != nullptr, merge_grid(ctx, part->n, false), ctx->stream);
+    if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "local reduce: %s", cudaGetErrorString(e));
+    return EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_tick_merge(ewsjf_ctx* ctx, const void* d_exchange_all, int32_t world,
+                                         int64_t global_base, int64_t n_local, int32_t* d_qid_local,
+                                         ewsjf_partition_t* part, int32_t bubble_width, const ewsjf_meta* theta,
+                                         const ewsjf_select_params* sp, ewsjf_select_out* out) {
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    ewsjf_status s;
+    if ((s = check_partition(ctx, part)) != EWSJF_OK) return s;
+    if ((s = check_select(ctx, sp)) != EWSJF_OK) return s;
+    if ((s = check_out(ctx, out)) != EWSJF_OK) return s;
+    if (!theta || !d_exchange_all || world < 1 || world > 1024 || bubble_width < 1)
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad merge arguments");
+    CU(cudaSetDevice(ctx->device));
+    ewsjf_weights w[EWSJF_MAX_QUEUES];
+    ewsjf_weights_from_meta(theta, part, w);
+    static thread_local Policy P;
+    fill_policy(part, w, &P);
+    MergeArgs M = merge_args(ctx, part, sp, theta, bubble_width);
+    M.in_mode = MERGE_IN_EXCHANGE;
+    M.out_mode = MERGE_OUT_FINAL;
+    M.ex_in = (const unsigned char*)d_exchange_all;
+    M.world = world;
+    M.ex_bytes = ex_layout(part->n, sp->k).total;
+    M.gbase = (uint32_t)global_base;
+    M.n_local = n_local;
+    M.qid = d_qid_local;
+    M.topk_id = out->d_topk_id; M.topk_score = out->d_topk_score; M.count = out->d_count;
+    M.head_id = out->d_head_id; M.head_score = out->d_head_score; M.max_score = out->d_max_score;
+    M.summary = out->d_summary ? out->d_summary : ctx->d_summary;
+    cudaError_t e = launch_merge(M, P, false, merge_grid(ctx, part->n, true), ctx->stream);
+    if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "global merge: %s", cudaGetErrorString(e));
+    if (out->h_summary) return finish_sync(ctx, part, out->h_summary, M.summary);
+    return EWSJF_OK;
+}

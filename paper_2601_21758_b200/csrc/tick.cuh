@@ -1,0 +1,132 @@
+// tick.cuh — argument blocks shared by tick.cu and api.cu.
+#pragma once
+#include "common.cuh"
+
+namespace ewsjf {
+
+// One gap-falling request, captured by the partial pass for Alg. 2 (App. D).
+struct GapEntry {
+    uint32_t gid;        // global id
+    int32_t len;
+    float arrival;
+    float cost;          // NaN if the pool has no cost field
+};
+
+// Scratch produced by the partial pass ("CTA rows"), consumed by the merge.
+struct Rows {
+    u64* keys;           // [nslots][G][cap]
+    int32_t* cnt;        // [nslots][G]  entries in row
+    int64_t* members;    // [nslots][G]  scored members seen by the CTA
+    u64* sec;            // [nslots][G]  secondary top-1 key
+    int32_t G, cap;
+};
+
+struct Counters {        // device-global, zeroed by the merge for the next call
+    unsigned long long n_invalid;
+    unsigned long long n_excluded;
+    unsigned long long gap_count;
+    unsigned int ticket;
+    unsigned int pad;
+};
+
+struct PartialArgs {
+    const int32_t* len;
+    const float* arrival;
+    const float* cost;          // nullable
+    const int32_t* qid_in;      // score_select: routed stable ids
+    int32_t* qid_out;           // tick/route: nullable
+    int64_t n;
+    uint32_t gbase;             // global id of element 0
+    int32_t tma;                // 1: pipelined TMA path (aligned pointers)
+    int32_t K, cap, tgt;        // selection depth, row capacity, compaction target
+    int32_t g_lo, g_hi;         // slot group handled by this pass (candidates)
+    int32_t pass0;              // counts, qid, gaps, counters
+    int32_t select;             // 0 = route only
+    int32_t lut_size;           // LUT covers lengths [0, lut_size); 0 = binary search
+    ScoreParams sp;
+    Rows rows;
+    u64* gthr;                  // [nslots] cross-CTA filter thresholds
+    GapEntry* gap;
+    int32_t gap_cap;
+    Counters* ctr;
+    // score_select: stable id -> slot map (sorted ids)
+    int32_t nids;
+    int32_t sorted_ids[kMaxSlots];
+    int32_t sorted_slot[kMaxSlots];
+};
+
+// Bubble creation log written by the merge (host replays it into *part).
+struct BubbleLog {
+    int32_t n;
+    int32_t pad;
+    int32_t pos[kMaxSlots];     // insertion position at creation time
+    int32_t lo[kMaxSlots], hi[kMaxSlots], L[kMaxSlots];
+};
+
+// Exchange record (one per rank) for the sharded tick.  Byte offsets.
+struct ExLayout {
+    int64_t hdr, members, sec, sec_sp, cnt, keys, sp, gaps, total;
+    int32_t nq, k, gap_cap;
+};
+constexpr int kExGap = 1024;
+__host__ __device__ inline ExLayout ex_layout(int nq, int k) {
+    auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
+    ExLayout L;
+    L.nq = nq; L.k = k; L.gap_cap = kExGap;
+    int64_t o = 0;
+    L.hdr = o;      o = al(o + 64);
+    L.members = o;  o = al(o + 8 * (int64_t)nq);
+    L.sec = o;      o = al(o + 8 * (int64_t)nq);
+    L.sec_sp = o;   o = al(o + 4 * (int64_t)nq);
+    L.cnt = o;      o = al(o + 4 * (int64_t)nq);
+    L.keys = o;     o = al(o + 8 * (int64_t)nq * k);
+    L.sp = o;       o = al(o + 4 * (int64_t)nq * k);
+    L.gaps = o;     o = al(o + (int64_t)sizeof(GapEntry) * kExGap);
+    L.total = o;
+    return L;
+}
+struct ExHeader {                // at L.hdr
+    int64_t gap_count, n_invalid, n_excluded, pad[5];
+};
+
+// Inputs of the merge.
+enum { MERGE_IN_ROWS = 0, MERGE_IN_EXCHANGE = 1 };
+enum { MERGE_OUT_FINAL = 0, MERGE_OUT_EXCHANGE = 1, MERGE_OUT_ROUTE = 2 };
+
+struct MergeArgs {
+    int32_t in_mode, out_mode;
+    int32_t K;
+    int32_t nq;                 // queues of the input partition
+    int32_t next_id;            // for bubble ids
+    int32_t bubble_width;
+    ScoreParams sp;
+    double theta[6];            // a_b, b_b, a_u, b_u, a_f, b_f (bubble weights, R21)
+    // --- rows input (in_mode ROWS)
+    Rows rows;
+    const int32_t* len;         // local pool (payload recompute)
+    const float* arrival;
+    const float* cost;
+    uint32_t gbase;
+    int64_t n_local;
+    const GapEntry* gap;        // single gap list
+    Counters* ctr;
+    int32_t gap_cap;
+    // --- exchange input (in_mode EXCHANGE)
+    const unsigned char* ex_in; // world records
+    int32_t world;
+    int64_t ex_bytes;
+    // --- outputs
+    unsigned char* ex_out;      // out_mode EXCHANGE: this rank's record
+    int64_t* topk_id;
+    float* topk_score;
+    int64_t* count;
+    int64_t* head_id;
+    float* head_score;
+    float* max_score;
+    ewsjf_summary* summary;
+    BubbleLog* blog;
+    int32_t* qid;               // gap requests' qid write-back (local pool)
+    u64* gthr;                  // zeroed for the next call
+};
+
+}  // namespace ewsjf
