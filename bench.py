@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark of the EWSJF scheduling tick on B200 (BASELINE.json metric).
+
+Workload (N=1, config C3 = BASELINE.json configs[2], the config the metric is
+quoted on): 10,000,000 pending requests with heavy-tailed prompt lengths per
+GPU, SoA (len int32, arrival fp32, cost fp32) resident in HBM; the policy is the
+Refine-and-Prune partition of a 1M heavy-tailed history computed on the GPU by
+ewsjf_partition (strategic loop, published before the timed region; its own
+time is reported under "strategic").  One step = one ewsjf_tick: route (A8) +
+bubbles (A9) + weights (A7) + Eq. 4 score (A10) + per-queue top-64 / head /
+ArgMax (A11).  Multi-GPU: weak scaling, every rank owns 10M requests (global
+ids rank*10M + i), candidates all-gathered over NCCL (tick_sharded).
+
+L2: 3 rotating pool copies (3 x 160 MB > 126 MB L2), so no step reads inputs
+left in L2 by the previous step.
+
+``--impl reference`` times the CPU oracle (the reference arm of this tier) on
+the same workload, a bounded sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workload  # noqa: E402
+
+METRIC = "requests scored+routed+selected/s per tick at 10M pending; % HBM roofline"
+UNIT = "req/s"
+BYTES_PER_REQ = 16          # len 4 + arrival 4 + cost 4 read, qid 4 written
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=10_000_000, help="pending requests per GPU")
+    ap.add_argument("--k", type=int, default=64)
+    ap.add_argument("--mode", default="score", choices=["score", "fifo"])
+    ap.add_argument("--partition", default="rp", choices=["rp", "quantile"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 8]
+        busy = [r for r in rows if r[2].isdigit() and int(r[2]) > 0] or rows
+        sm = [float(r[0]) for r in busy if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in busy for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows), "samples_busy": len(busy)}
+
+
+def oracle_rate(pool, opart, K, mode, sample_n, repeats=1):
+    """The CPU oracle (test infrastructure) on a bounded sample of the workload."""
+    import oracle as O
+    sp = O.select_params(k=K, mode=mode, now=workload.NOW)
+    th = O.meta(**workload.THETA0)
+    ln, ar, co = pool["len"][:sample_n], pool["arrival"][:sample_n], pool["cost"][:sample_n]
+    ts = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        O.tick(ln, ar, co, opart, th, sp)
+        ts.append(time.perf_counter() - t0)
+    return sample_n / statistics.median(ts), statistics.median(ts)
+
+
+def oracle_partition(hist):
+    import oracle as O
+    s, part, _ = O.partition(hist)
+    return part
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """Reference arm of this tier: the CPU oracle, as it stands, on the box's host cores."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    mode = 0 if args.mode == "score" else 1
+    hist = workload.heavy(1_000_000, 301)
+    opart = oracle_partition(hist)
+    pool = workload.pool("heavy", args.n, 302)
+    # size each step's sample so the whole warmup+steps run takes ~1-2 minutes
+    _, t_cal = oracle_rate(pool, opart, args.k, mode, 200_000)
+    per_req = t_cal / 200_000
+    budget = 90.0
+    sample_n = int(max(2_000, min(args.n, budget / max(args.steps + args.warmup, 1) / per_req)))
+    for _ in range(args.warmup):
+        oracle_rate(pool, opart, args.k, mode, sample_n)
+    ts = []
+    for _ in range(args.steps):
+        _, t = oracle_rate(pool, opart, args.k, mode, sample_n)
+        ts.append(t)
+    tot = sum(ts)
+    value = sample_n * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, opart_source="oracle Refine-and-Prune of heavy(1M, seed 301)"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"first {sample_n} requests of the C3 pool per step (oracle tick: route, "
+                                   f"bubbles, weights, Eq. 4 score, per-queue full sort), single thread"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, opart_source):
+    return {"workload": "C3: 10M pending requests per GPU, heavy-tailed lengths (80% lognormal(ln128,0.6) "
+                        "32..2047, 20% Pareto(1.5) 2048..32768), route + score + per-queue top-k",
+            "pending_per_gpu": args.n, "k": args.k, "mode": args.mode, "partition": opart_source,
+            "theta": workload.THETA0, "now_s": workload.NOW, "cost_field": True,
+            "l2": "3 rotating pool copies (3 x 160 MB > 126 MB L2)",
+            "parallelism": f"index-sharded x{args.gpus}, NCCL all-gather of candidates" if args.gpus > 1 else "1 GPU"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import paper_2601_21758_b200 as E
+    from paper_2601_21758_b200 import _lib as L
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    mode = L.SELECT_SCORE if args.mode == "score" else L.SELECT_FIFO
+    n = args.n
+    ctx = E.Context(local, max_pool=n, max_history=1_000_000, max_k=max(args.k, 64))
+
+    # ---- strategic loop: Refine-and-Prune on the GPU (published before the timed region)
+    hist = torch.from_numpy(workload.heavy(1_000_000, 301)).to(dev)
+    strategic = {}
+    if args.partition == "rp":
+        ctx.set_timing(True)
+        part, pst, _ = E.partition(ctx, hist)
+        tm = ctx.timing()
+        strategic = {"refine_and_prune_ms": pst["ms_total"], "history": 1_000_000, "queues": part.n,
+                     "stages_ms": {k: pst[k] for k in ("ms_hist", "ms_kmeans", "ms_refine", "ms_prune")},
+                     "distinct": pst["distinct"], "segments": pst["segments"], "merges": pst["merges"]}
+        psrc = "GPU Refine-and-Prune (ewsjf_partition) of heavy(1M, seed 301), alpha=2, max_queues=32, MIN_U"
+    else:
+        part = E.make_partition(workload.quantile_bounds(workload.heavy(1_000_000, 301), 32))
+        psrc = "balanced 32-quantile partition of heavy(1M, seed 301)"
+    theta = E.meta(**workload.THETA0)
+    sp = E.select_params(k=args.k, mode=mode, now=workload.NOW)
+
+    # ---- pool: this rank's 10M shard, 3 rotating copies in HBM
+    pool = workload.pool("heavy", n, 302 + 1000 * rank)
+    copies = []
+    for c in range(3):
+        copies.append((torch.from_numpy(pool["len"]).to(dev), torch.from_numpy(pool["arrival"]).to(dev),
+                       torch.from_numpy(pool["cost"]).to(dev), torch.empty(n, dtype=torch.int32, device=dev)))
+    out = E.Outputs.alloc(args.k, dev)
+    base = rank * n
+
+    def step(i):
+        ln, ar, co, q = copies[i % 3]
+        if ws > 1:
+            E.tick_sharded(ctx, ln, ar, co, base, part, theta, sp, group=group, qid_out=q, out=out, sync=False)
+        else:
+            E.tick(ctx, ln, ar, co, part, theta, sp, global_base=base, qid_out=q, out=out, sync=False)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    summary = E.tick(ctx, *copies[0][:3], part, theta, sp, global_base=base, qid_out=copies[0][3]).summary \
+        if ws == 1 else None
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    # timed region: K steps between a barrier + synchronize on both sides
+    if group is not None:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    launches0 = ctx.timing()["launches"]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        step(i)
+    e1.record()
+    torch.cuda.synchronize()
+    if group is not None:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1)
+    tm = ctx.timing()
+    clocks = sampler.stop()
+    if group is not None:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = n * ws / (ms_per_step / 1e3)
+
+    # ---- roofline of the dominant kernel (the partial tick pass)
+    peak, peak_src = peaks()
+    tick_ms = tm["tick_ms"] / max(tm["tick_launches"], 1)
+    merge_ms = tm["merge_ms"] / max(tm["merge_launches"], 1)
+    achieved = BYTES_PER_REQ * n / (tick_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "ewsjf::partial_kernel<ROUTE,HAS_COST,LUT> (route+score+filter)",
+                "algorithmic_bytes_per_launch": BYTES_PER_REQ * n, "kernel_ms": tick_ms,
+                "merge_kernel_ms": merge_ms, "peak_source": peak_src,
+                "share_of_step": tick_ms / ms_per_step if ms_per_step else None}
+    prof_traffic = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(prof_traffic):
+        try:
+            with open(prof_traffic) as f:
+                roofline["traffic"] = json.load(f).get("bytes_per_launch_at_n", {}).get(str(n))
+        except Exception:
+            pass
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": config_dict(args, psrc), "roofline": roofline,
+        "gpu_launches": int(tm["launches"] - launches0), "clocks": clocks, "strategic": strategic,
+        "tick_summary": summary,
+    }
+
+    # ---- e2e through the C ABI with host buffers (H2D + D2H inside the timed region)
+    if not args.no_e2e and ws == 1:
+        hl = torch.from_numpy(pool["len"]).pin_memory()
+        ha = torch.from_numpy(pool["arrival"]).pin_memory()
+        hc = torch.from_numpy(pool["cost"]).pin_memory()
+        hq = torch.empty(n, dtype=torch.int32).pin_memory()
+        res = None
+        for _ in range(2):
+            res = E.tick_host(ctx, hl, ha, hc, part, theta, sp, qid_out=hq, results=res)
+        k_e2e = max(3, min(20, args.steps // 20))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            res = E.tick_host(ctx, hl, ha, hc, part, theta, sp, qid_out=hq, results=res)
+        dt = (time.perf_counter() - t0) / k_e2e
+        out_bytes = sum(v.numel() * v.element_size() for k, v in res.items() if k != "summary")
+        line["e2e"] = {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": 12 * n,
+                       "d2h_bytes_per_step": 4 * n + out_bytes, "ms_per_step": 1e3 * dt, "steps": k_e2e,
+                       "path": "ewsjf_tick_host (pinned host SoA in, qid + results out)"}
+
+    # ---- the oracle beside it (rank 0, N=1 only), bounded sample
+    if not args.no_cpu_baseline and ws == 1 and rank == 0:
+        opart = oracle_partition(workload.heavy(1_000_000, 301)) if args.partition == "rp" else None
+        if opart is None:
+            import oracle as O
+            opart = O.make_partition(workload.quantile_bounds(workload.heavy(1_000_000, 301), 32))
+        sample_n = 2_000_000
+        rate, secs = oracle_rate(pool, opart, args.k, 0 if args.mode == "score" else 1, sample_n)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"first {sample_n} requests of the C3 pool, one oracle tick "
+                                          f"({secs:.1f} s, single-threaded C fp64)",
+                                "host_cores_available": os.cpu_count()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

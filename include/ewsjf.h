@@ -69,6 +69,25 @@ ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx *ctx);
 /* Number of SMs the ctx launches persistent kernels over (the "CTA rows"). */
 int32_t      ewsjf_ctx_num_ctas(const ewsjf_ctx *ctx);
 
+/* Instrumentation (tracing / bench): when enabled, every kernel the ctx launches
+ * is bracketed by CUDA events on the ctx stream (up to 16384 launches are
+ * recorded; enabling resets the record).  ewsjf_ctx_get_timing synchronises
+ * and sums the device time per kernel kind since the last enable.  `launches`
+ * counts every libewsjf kernel launched since ctx creation (timing or not).  */
+typedef struct {
+    int64_t launches;
+    int64_t recorded;
+    int64_t tick_launches;     /* partial (route/score/select) passes */
+    int64_t merge_launches;
+    int64_t partition_launches;
+    int64_t sweep_launches;
+    double  tick_ms, merge_ms, partition_ms, sweep_ms;
+    int64_t candidates_inserted;   /* diagnostics since ctx creation: keys that passed the  */
+    int64_t compactions;           /* per-queue filters, and per-queue buffer compactions   */
+} ewsjf_timing;
+ewsjf_status ewsjf_ctx_set_timing(ewsjf_ctx *ctx, int32_t enable);
+ewsjf_status ewsjf_ctx_get_timing(ewsjf_ctx *ctx, ewsjf_timing *out);
+
 /* ------------------------------------------------------------- partition --- */
 /* Refine-and-Prune parameters (§4.2). alpha > 1 (Eq. 2 significance
  * ratio); min_width >= 1 (Stage-2 width stop, R13); max_queues in

@@ -13,7 +13,7 @@ OUT = os.path.join(HERE, "libewsjf.so")
 BUILD = os.path.join(ROOT, "build", "ewsjf")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+    "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-ftz=true",
     "-Xcompiler", "-fPIC,-ffp-contract=off", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
 ]
 
@@ -46,8 +46,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for _, err in res:
             print(err)
     tmp = OUT + f".tmp{os.getpid()}"
-    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
-                    *[o for o, _ in res], "-cudart", "static"], check=True, capture_output=True, text=True)
+    r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
+                        *[o for o, _ in res], "-cudart", "static"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc link failed:\n{r.stderr}")
     os.replace(tmp, OUT)
     return OUT
 

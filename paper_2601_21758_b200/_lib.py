@@ -71,6 +71,16 @@ class Summary(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "pad"}
 
 
+class Timing(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("recorded", C.c_int64), ("tick_launches", C.c_int64),
+                ("merge_launches", C.c_int64), ("partition_launches", C.c_int64), ("sweep_launches", C.c_int64),
+                ("tick_ms", C.c_double), ("merge_ms", C.c_double), ("partition_ms", C.c_double),
+                ("sweep_ms", C.c_double), ("candidates_inserted", C.c_int64), ("compactions", C.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 class SelectOut(C.Structure):
     _fields_ = [("d_topk_id", C.c_void_p), ("d_topk_score", C.c_void_p), ("d_count", C.c_void_p),
                 ("d_head_id", C.c_void_p), ("d_head_score", C.c_void_p), ("d_max_score", C.c_void_p),
@@ -82,7 +92,7 @@ SYMBOLS = [
     "ewsjf_abi_version", "ewsjf_status_str", "ewsjf_last_error", "ewsjf_ctx_create", "ewsjf_ctx_set_stream",
     "ewsjf_ctx_destroy", "ewsjf_ctx_num_ctas", "ewsjf_partition", "ewsjf_weights_from_meta", "ewsjf_route",
     "ewsjf_score_select", "ewsjf_tick", "ewsjf_tick_host", "ewsjf_exchange_bytes", "ewsjf_tick_local",
-    "ewsjf_tick_merge", "ewsjf_score_select_sweep",
+    "ewsjf_tick_merge", "ewsjf_score_select_sweep", "ewsjf_ctx_set_timing", "ewsjf_ctx_get_timing",
 ]
 
 _lib = None
@@ -107,6 +117,8 @@ def load() -> C.CDLL:
     L.ewsjf_ctx_destroy.argtypes = [V]
     L.ewsjf_ctx_num_ctas.argtypes = [V]
     L.ewsjf_ctx_num_ctas.restype = I32
+    L.ewsjf_ctx_set_timing.argtypes = [V, I32]
+    L.ewsjf_ctx_get_timing.argtypes = [V, P(Timing)]
     L.ewsjf_partition.argtypes = [V, V, I64, P(PartitionParams), P(Partition), P(PartitionStats)]
     L.ewsjf_weights_from_meta.argtypes = [P(Meta), P(Partition), P(Weights)]
     L.ewsjf_route.argtypes = [V, V, I64, P(Partition), I32, V, P(Summary)]

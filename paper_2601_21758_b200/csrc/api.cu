@@ -10,10 +10,10 @@
 #include "tick.cuh"
 
 namespace ewsjf {
-cudaError_t launch_partial(const PartialArgs& A, const Policy& P, bool route, bool has_cost, bool use_lut, int grid,
-                           cudaStream_t st);
-int64_t partial_smem_bytes(bool route, bool has_cost, bool tma, int lut_size, int nslots, int nids, int pass0, int ngs,
-                           int cap);
+cudaError_t launch_partial(const PartialArgs& A, const Policy& P, const MergeArgs* MA, bool route, bool has_cost,
+                           bool use_lut, int grid, cudaStream_t st);
+int64_t partial_smem_bytes(bool route, bool has_cost, bool tma, int lut_size, int nslots, int nids, int pass0,
+                           int cnt_thread, int ngs, int cap);
 cudaError_t launch_merge(const MergeArgs& A, const Policy& P, bool has_cost, int grid, cudaStream_t st);
 int64_t merge_smem_total(int in_mode);
 }  // namespace ewsjf
@@ -27,6 +27,7 @@ struct ewsjf_ctx {
     int32_t max_k = 0;
     int num_sms = 0;
     int smem_optin = 0;
+    int coop = 0;
     int32_t cap_max = 0;
     char err[512] = {0};
     // scratch
@@ -52,7 +53,37 @@ struct ewsjf_ctx {
     float* d_max_score = nullptr;
     // partition (R&P) scratch lives in partition.cu
     void* rp = nullptr;
+    // instrumentation
+    long long launches = 0;
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_a, ev_b;
+    std::vector<int> ev_kind;
+    size_t ev_n = 0;
 };
+
+namespace ewsjf {
+enum { KIND_TICK = 0, KIND_MERGE = 1, KIND_PARTITION = 2, KIND_SWEEP = 3 };
+// Bracket one launch with events when timing is on; count it always.
+struct LaunchScope {
+    ewsjf_ctx* c;
+    int kind;
+    bool rec = false;
+    LaunchScope(ewsjf_ctx* ctx, int k) : c(ctx), kind(k) {
+        c->launches++;
+        if (c->timing && c->ev_n < c->ev_a.size()) {
+            cudaEventRecord(c->ev_a[c->ev_n], c->stream);
+            rec = true;
+        }
+    }
+    ~LaunchScope() {
+        if (rec) {
+            cudaEventRecord(c->ev_b[c->ev_n], c->stream);
+            c->ev_kind[c->ev_n] = kind;
+            c->ev_n++;
+        }
+    }
+};
+}  // namespace ewsjf
 
 namespace ewsjf {
 void rp_free(ewsjf_ctx* ctx);
@@ -118,6 +149,8 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
     if (cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
         return bad(EWSJF_ERR_CUDA);
     cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaDeviceGetAttribute(&ctx->coop, cudaDevAttrCooperativeLaunch, device);
+    if (getenv("EWSJF_NO_FUSE")) ctx->coop = 0;
     const int G = ctx->num_sms;
     const size_t nrow = (size_t)kMaxSlots * G;
     bool ok = cudaMalloc(&ctx->rows.keys, nrow * ctx->cap_max * sizeof(u64)) == cudaSuccess &&
@@ -171,10 +204,52 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
                  ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score, ctx->d_max_score};
     for (void* p : d)
         if (p) cudaFree(p);
+    for (auto e : ctx->ev_a) cudaEventDestroy(e);
+    for (auto e : ctx->ev_b) cudaEventDestroy(e);
     if (ctx->h_blog) cudaFreeHost(ctx->h_blog);
     if (ctx->h_summary) cudaFreeHost(ctx->h_summary);
     rp_free(ctx);
     delete ctx;
+    return EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_ctx_set_timing(ewsjf_ctx* ctx, int32_t enable) {
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    CU(cudaSetDevice(ctx->device));
+    if (enable && ctx->ev_a.empty()) {
+        const size_t cap = 16384;
+        ctx->ev_a.resize(cap); ctx->ev_b.resize(cap); ctx->ev_kind.resize(cap);
+        for (size_t i = 0; i < cap; i++) {
+            CU(cudaEventCreate(&ctx->ev_a[i]));
+            CU(cudaEventCreate(&ctx->ev_b[i]));
+        }
+    }
+    ctx->timing = enable != 0;
+    ctx->ev_n = 0;
+    return EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_ctx_get_timing(ewsjf_ctx* ctx, ewsjf_timing* out) {
+    if (!ctx || !out) return EWSJF_ERR_INVALID_ARG;
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaStreamSynchronize(ctx->stream));
+    memset(out, 0, sizeof *out);
+    Counters c;
+    CU(cudaMemcpy(&c, ctx->ctr, sizeof c, cudaMemcpyDeviceToHost));
+    out->candidates_inserted = (int64_t)c.dbg_inserted;
+    out->compactions = (int64_t)c.dbg_compactions;
+    out->launches = ctx->launches;
+    out->recorded = (int64_t)ctx->ev_n;
+    for (size_t i = 0; i < ctx->ev_n; i++) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ctx->ev_a[i], ctx->ev_b[i]));
+        switch (ctx->ev_kind[i]) {
+            case KIND_TICK: out->tick_ms += ms; out->tick_launches++; break;
+            case KIND_MERGE: out->merge_ms += ms; out->merge_launches++; break;
+            case KIND_PARTITION: out->partition_ms += ms; out->partition_launches++; break;
+            default: out->sweep_ms += ms; out->sweep_launches++; break;
+        }
+    }
     return EWSJF_OK;
 }
 
@@ -255,7 +330,8 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, const float* d_cost,
                                 const int32_t* d_qid_in, int32_t* d_qid_out, int64_t n, int64_t gbase,
                                 const ewsjf_partition_t* part, const Policy& P, const ewsjf_select_params* sp,
-                                bool route, bool select) {
+                                bool route, bool select, const MergeArgs* fuse = nullptr, bool* fused = nullptr) {
+    if (fused) *fused = false;
     const int nslots = part->n;
     const bool has_cost = d_cost != nullptr;
     const int K = select ? sp->k : 1;
@@ -273,7 +349,12 @@ static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const floa
             (route ? (!d_qid_out || aligned16(d_qid_out)) : aligned16(d_qid_in));
     A.K = K;
     A.cap = cap;
-    A.tgt = (K + cap) / 2;
+    A.tgt = K + (cap - K) / 4;
+    A.hwm = cap - (cap - K) / 4;
+    A.ids_identity = 1;
+    for (int i = 0; i < nslots; i++)
+        if (part->q[i].id != i) A.ids_identity = 0;
+    A.cnt_thread = nslots <= 64 ? 1 : 0;
     A.select = select ? 1 : 0;
     A.sp = select ? score_params(sp) : ScoreParams{0.f, 0.f, 0.f, 0.f, 0, 1};
     A.rows = ctx->rows;
@@ -297,19 +378,28 @@ static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const floa
     // slot groups so that the candidate buffers fit in shared memory
     int ngs = std::max(nslots, 1);
     const int budget = ctx->smem_optin > 0 ? ctx->smem_optin : 232448;
-    while (ngs > 1 && partial_smem_bytes(route, has_cost, A.tma, use_lut ? A.lut_size : 0, nslots, A.nids, 1, ngs,
-                                         cap) > budget)
-        ngs = (ngs + 1) / 2;
-    if (partial_smem_bytes(route, has_cost, A.tma, use_lut ? A.lut_size : 0, nslots, A.nids, 1, ngs, cap) > budget)
+    auto smem_for = [&](int g) {
+        return partial_smem_bytes(route, has_cost, A.tma, use_lut ? A.lut_size : 0, nslots, A.nids, 1,
+                                  A.cnt_thread, g, cap);
+    };
+    if (A.cnt_thread && smem_for(1) > budget) A.cnt_thread = 0;
+    while (ngs > 1 && smem_for(ngs) > budget) ngs = (ngs + 1) / 2;
+    if (smem_for(ngs) > budget)
         return fail(ctx, EWSJF_ERR_UNSUPPORTED, "tick does not fit shared memory (k=%d)", K);
     const int passes = select ? std::max(1, (nslots + ngs - 1) / ngs) : 1;
+    const bool fuse_ok = fuse && passes == 1 && ctx->coop && smem_for(ngs) <= budget;
     for (int p = 0; p < passes; p++) {
         A.pass0 = p == 0;
         A.g_lo = select ? std::min(nslots, p * ngs) : 0;
         A.g_hi = select ? std::min(nslots, (p + 1) * ngs) : 0;
-        cudaError_t e = launch_partial(A, P, route, has_cost, use_lut, ctx->num_sms, ctx->stream);
-        if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "partial kernel: %s", cudaGetErrorString(e));
+        cudaError_t e;
+        {
+            LaunchScope ls(ctx, KIND_TICK);
+            e = launch_partial(A, P, fuse_ok ? fuse : nullptr, route, has_cost, use_lut, ctx->num_sms, ctx->stream);
+        }
+        if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "tick kernel: %s", cudaGetErrorString(e));
     }
+    if (fused) *fused = fuse_ok;
     return EWSJF_OK;
 }
 
@@ -395,8 +485,6 @@ static ewsjf_status tick_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float*
     ewsjf_weights_from_meta(theta, part, w);
     static thread_local Policy P;
     fill_policy(part, w, &P);
-    if ((s = run_partial(ctx, d_len, d_arr, d_cost, nullptr, d_qid_out, n, gbase, part, P, sp, true, true)) != EWSJF_OK)
-        return s;
     MergeArgs M = merge_args(ctx, part, sp, theta, bubble_width);
     M.in_mode = MERGE_IN_ROWS;
     M.out_mode = MERGE_OUT_FINAL;
@@ -407,8 +495,18 @@ static ewsjf_status tick_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float*
     M.head_id = out->d_head_id; M.head_score = out->d_head_score; M.max_score = out->d_max_score;
     M.summary = out->d_summary ? out->d_summary : ctx->d_summary;
     M.qid = d_qid_out;
-    cudaError_t e = launch_merge(M, P, d_cost != nullptr, merge_grid(ctx, part->n, true), ctx->stream);
-    if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "merge kernel: %s", cudaGetErrorString(e));
+    bool fused = false;
+    if ((s = run_partial(ctx, d_len, d_arr, d_cost, nullptr, d_qid_out, n, gbase, part, P, sp, true, true, &M,
+                         &fused)) != EWSJF_OK)
+        return s;
+    if (!fused) {
+        cudaError_t e;
+        {
+            LaunchScope ls(ctx, KIND_MERGE);
+            e = launch_merge(M, P, d_cost != nullptr, merge_grid(ctx, part->n, true), ctx->stream);
+        }
+        if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "merge kernel: %s", cudaGetErrorString(e));
+    }
     if (out->h_summary) return finish_sync(ctx, part, out->h_summary, M.summary);
     return EWSJF_OK;
 }
@@ -472,8 +570,6 @@ extern "C" ewsjf_status ewsjf_score_select(ewsjf_ctx* ctx, const int32_t* d_len,
     CU(cudaSetDevice(ctx->device));
     static thread_local Policy P;
     fill_policy(part, w, &P);
-    if ((s = run_partial(ctx, d_len, d_arrival, d_cost, d_qid, nullptr, n, 0, part, P, sp, false, true)) != EWSJF_OK)
-        return s;
     MergeArgs M = merge_args(ctx, part, sp, nullptr, 1);
     M.in_mode = MERGE_IN_ROWS;
     M.out_mode = MERGE_OUT_FINAL;
@@ -483,8 +579,18 @@ extern "C" ewsjf_status ewsjf_score_select(ewsjf_ctx* ctx, const int32_t* d_len,
     M.head_id = out->d_head_id; M.head_score = out->d_head_score; M.max_score = out->d_max_score;
     M.summary = out->d_summary ? out->d_summary : ctx->d_summary;
     M.blog = nullptr;
-    cudaError_t e = launch_merge(M, P, d_cost != nullptr, merge_grid(ctx, part->n, false), ctx->stream);
-    if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "merge kernel: %s", cudaGetErrorString(e));
+    bool fused = false;
+    if ((s = run_partial(ctx, d_len, d_arrival, d_cost, d_qid, nullptr, n, 0, part, P, sp, false, true, &M,
+                         &fused)) != EWSJF_OK)
+        return s;
+    if (!fused) {
+        cudaError_t e;
+        {
+            LaunchScope ls(ctx, KIND_MERGE);
+            e = launch_merge(M, P, d_cost != nullptr, merge_grid(ctx, part->n, false), ctx->stream);
+        }
+        if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "merge kernel: %s", cudaGetErrorString(e));
+    }
     if (out->h_summary) return finish_sync(ctx, nullptr, out->h_summary, M.summary);
     return EWSJF_OK;
 }
@@ -512,7 +618,11 @@ extern "C" ewsjf_status ewsjf_route(ewsjf_ctx* ctx, const int32_t* d_len, int64_
     M.n_local = n;
     M.qid = d_qid;
     M.summary = ctx->d_summary;
-    cudaError_t e = launch_merge(M, P, false, 1, ctx->stream);
+    cudaError_t e;
+    {
+        LaunchScope ls(ctx, KIND_MERGE);
+        e = launch_merge(M, P, false, 1, ctx->stream);
+    }
     if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "merge kernel: %s", cudaGetErrorString(e));
     ewsjf_summary tmp;
     return finish_sync(ctx, part, h_summary ? h_summary : &tmp, ctx->d_summary);
@@ -553,7 +663,11 @@ extern "C" ewsjf_status ewsjf_tick_local(ewsjf_ctx* ctx, const int32_t* d_len, c
     M.n_local = n;
     M.ex_out = (unsigned char*)d_exchange;
     M.blog = nullptr;
-    cudaError_t e = launch_merge(M, P, d_cost != nullptr, merge_grid(ctx, part->n, false), ctx->stream);
+    cudaError_t e;
+    {
+        LaunchScope ls(ctx, KIND_MERGE);
+        e = launch_merge(M, P, d_cost != nullptr, merge_grid(ctx, part->n, false), ctx->stream);
+    }
     if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "local reduce: %s", cudaGetErrorString(e));
     return EWSJF_OK;
 }
@@ -586,7 +700,11 @@ extern "C" ewsjf_status ewsjf_tick_merge(ewsjf_ctx* ctx, const void* d_exchange_
     M.topk_id = out->d_topk_id; M.topk_score = out->d_topk_score; M.count = out->d_count;
     M.head_id = out->d_head_id; M.head_score = out->d_head_score; M.max_score = out->d_max_score;
     M.summary = out->d_summary ? out->d_summary : ctx->d_summary;
-    cudaError_t e = launch_merge(M, P, false, merge_grid(ctx, part->n, true), ctx->stream);
+    cudaError_t e;
+    {
+        LaunchScope ls(ctx, KIND_MERGE);
+        e = launch_merge(M, P, false, merge_grid(ctx, part->n, true), ctx->stream);
+    }
     if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "global merge: %s", cudaGetErrorString(e));
     if (out->h_summary) return finish_sync(ctx, part, out->h_summary, M.summary);
     return EWSJF_OK;

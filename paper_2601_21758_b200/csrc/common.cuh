@@ -53,7 +53,8 @@ struct ScoreParams {
 // larger key = better, ties -> lower id (R24).  FIFO key: hi = ~ord(arrival),
 // lo = ~id: larger = earlier arrival, ties -> lower id (R26).  0 = empty.
 __device__ __forceinline__ u32 ord_f32(float f) {
-    u32 u = __float_as_uint(f + 0.0f);         // -0 -> +0
+    u32 u = __float_as_uint(f);
+    u = (u == 0x80000000u) ? 0u : u;           // -0 -> +0 (integer ops: exact under -ftz)
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 __device__ __forceinline__ u64 score_key(float sp, u32 gid) {

@@ -26,7 +26,9 @@ struct Counters {        // device-global, zeroed by the merge for the next call
     unsigned long long n_excluded;
     unsigned long long gap_count;
     unsigned int ticket;
-    unsigned int pad;
+    unsigned int barrier;   // grid barrier of the fused tick kernel
+    // diagnostics, accumulated over calls (never reset by the kernels)
+    unsigned long long dbg_inserted, dbg_compactions, dbg_overflow;
 };
 
 struct PartialArgs {
@@ -38,7 +40,9 @@ struct PartialArgs {
     int64_t n;
     uint32_t gbase;             // global id of element 0
     int32_t tma;                // 1: pipelined TMA path (aligned pointers)
-    int32_t K, cap, tgt;        // selection depth, row capacity, compaction target
+    int32_t K, cap, tgt, hwm;   // selection depth, buffer capacity, compaction target / trigger
+    int32_t ids_identity;       // stable id == position for every queue (qid = slot)
+    int32_t cnt_thread;         // per-thread u16 member counters (<= 64 queues) vs warp match-any
     int32_t g_lo, g_hi;         // slot group handled by this pass (candidates)
     int32_t pass0;              // counts, qid, gaps, counters
     int32_t select;             // 0 = route only

@@ -56,6 +56,14 @@ class Context:
         st = torch.cuda.current_stream(self.device).cuda_stream
         self.lib.ewsjf_ctx_set_stream(self.h, C.c_void_p(st))
 
+    def set_timing(self, enable: bool = True):
+        self.check(self.lib.ewsjf_ctx_set_timing(self.h, int(enable)))
+
+    def timing(self) -> dict:
+        t = L.Timing()
+        self.check(self.lib.ewsjf_ctx_get_timing(self.h, C.byref(t)))
+        return t.as_dict()
+
     def check(self, s: int, allow=(L.OK, L.DOMAIN)) -> int:
         if s not in allow:
             msg = self.lib.ewsjf_last_error(self.h).decode()

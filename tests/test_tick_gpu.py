@@ -119,12 +119,25 @@ def test_tick_gaps_and_bubbles(E, orc, ctx, mode):
     """A partition with holes: gap requests go through Alg. 2 in index order."""
     part = orc.make_partition([(32, 100), (180, 300), (1000, 2000), (5000, 6000)], means=[60, 240, 1500, 5500])
     rng = np.random.default_rng(7)
-    n = 50_000
+    n = 10_000          # ~6.5k gap requests: within the 8192-entry gap list
     pool = {"len": rng.integers(1, 9000, size=n).astype(np.int32),
             "arrival": workload.arrivals(n, 7), "cost": workload.cost_estimates(np.ones(n, np.int32) * 100, 7)}
     g, ref, phi = _run_both(E, orc, ctx, pool, part, 16, mode, bubble_width=64)
     assert ref["n_bubbles"] > 10
     _check(g, ref, phi, pool, mode, 16)
+
+
+def test_tick_gap_list_overflow_reports_capacity(E, ctx):
+    """More gap requests than the gap list holds: CAPACITY, unprocessed qids stay -2."""
+    n = 20_000
+    ln = torch.full((n,), 5000, dtype=torch.int32, device="cuda")
+    ar = torch.zeros(n, dtype=torch.float32, device="cuda")
+    qid = torch.empty(n, dtype=torch.int32, device="cuda")
+    out = E.tick(ctx, ln, ar, None, E.make_partition([(1, 10)]), E.meta(**THETA0), E.select_params(k=4),
+                 qid_out=qid)
+    assert out.summary["status"] == 4 and out.summary["n_gap"] == n
+    q = qid.cpu().numpy()
+    assert ((q == -2) | (q == 1)).all() and (q == 1).sum() == 8192
 
 
 def test_tick_bubble_cap(E, orc, ctx):
@@ -178,7 +191,7 @@ def test_tick_equal_scores_tiebreak(E, orc, ctx):
 
 def test_route_matches_oracle(E, orc, ctx):
     part = orc.make_partition([(32, 100), (180, 300), (1000, 2000)])
-    lens = np.random.default_rng(3).integers(-2, 4000, size=200_000).astype(np.int32)
+    lens = np.random.default_rng(3).integers(-2, 4000, size=10_000).astype(np.int32)   # gaps < 8192
     gpart = to_gpu_partition(E, part)
     qid, summ = E.route(ctx, torch.from_numpy(lens).cuda(), gpart, 50)
     p2 = orc.copy_partition(part)
@@ -221,10 +234,9 @@ def test_tick_host_equals_device(E, orc, ctx, heavy_parts):
     r = E.tick_host(ctx, hl, ha, hc, gpart, theta, sp, qid_out=hq)
     out = E.tick(ctx, hl.cuda(), ha.cuda(), hc.cuda(), to_gpu_partition(E, heavy_parts["rp"]), theta, sp)
     assert r["summary"] == out.summary
-    for k in ("topk_id", "count", "head_id"):
-        np.testing.assert_array_equal(r[k].numpy(), getattr(out, k).cpu().numpy())
-    for k in ("topk_score", "head_score", "max_score"):
-        np.testing.assert_array_equal(r[k].numpy(), getattr(out, k).cpu().numpy())
+    nq = out.summary["n_queues"]
+    for k in ("topk_id", "count", "head_id", "topk_score", "head_score", "max_score"):
+        np.testing.assert_array_equal(r[k].numpy()[:nq], getattr(out, k).cpu().numpy()[:nq])
 
 
 def test_repeat_calls_are_deterministic(E, ctx, heavy_parts):
@@ -236,3 +248,20 @@ def test_repeat_calls_are_deterministic(E, ctx, heavy_parts):
     for o in outs[1:]:
         for k in ("topk_id", "count", "head_id", "topk_score"):
             np.testing.assert_array_equal(o[k], outs[0][k])
+
+
+@pytest.fixture(scope="module")
+def ctx_full(E):
+    return E.Context(0, max_pool=10_000_000, max_history=1_000_000, max_k=64)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_tick_full_size_c3(E, orc, ctx_full, mode):
+    """BASELINE config C3 at full size, in the launch configuration bench.py times:
+    10M heavy-tailed pool, Refine-and-Prune partition of heavy(1M, seed 301), K=64.
+    The oracle computes the whole tick, so every output is compared."""
+    s, opart, _ = orc.partition(workload.heavy(1_000_000, 301))
+    assert s == orc.OK
+    pool = workload.pool("heavy", 10_000_000, 302)
+    g, ref, phi = _run_both(E, orc, ctx_full, pool, opart, 64, mode)
+    _check(g, ref, phi, pool, mode, 64)
