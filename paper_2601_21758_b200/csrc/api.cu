@@ -33,6 +33,7 @@ struct ewsjf_ctx {
     // scratch
     Rows rows{};
     u64* gthr = nullptr;
+    u64* board = nullptr;
     Counters* ctr = nullptr;
     GapEntry* gap = nullptr;
     int32_t gap_cap = 8192;
@@ -153,11 +154,12 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
     if (getenv("EWSJF_NO_FUSE")) ctx->coop = 0;
     const int G = ctx->num_sms;
     const size_t nrow = (size_t)kMaxSlots * G;
-    bool ok = cudaMalloc(&ctx->rows.keys, nrow * ctx->cap_max * sizeof(u64)) == cudaSuccess &&
+    bool ok = cudaMalloc(&ctx->rows.keys, nrow * max_k * sizeof(u64)) == cudaSuccess &&
               cudaMalloc(&ctx->rows.cnt, nrow * sizeof(int32_t)) == cudaSuccess &&
               cudaMalloc(&ctx->rows.members, nrow * sizeof(int64_t)) == cudaSuccess &&
               cudaMalloc(&ctx->rows.sec, nrow * sizeof(u64)) == cudaSuccess &&
               cudaMalloc(&ctx->gthr, kMaxSlots * sizeof(u64)) == cudaSuccess &&
+              cudaMalloc(&ctx->board, nrow * 2 * sizeof(u64)) == cudaSuccess &&
               cudaMalloc(&ctx->ctr, sizeof(Counters)) == cudaSuccess &&
               cudaMalloc(&ctx->gap, (size_t)ctx->gap_cap * sizeof(GapEntry)) == cudaSuccess &&
               cudaMalloc(&ctx->d_blog, sizeof(BubbleLog)) == cudaSuccess &&
@@ -178,6 +180,7 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
     }
     if (!ok) return bad(EWSJF_ERR_CUDA);
     ok = cudaMemset(ctx->gthr, 0, kMaxSlots * sizeof(u64)) == cudaSuccess &&
+         cudaMemset(ctx->board, 0, nrow * 2 * sizeof(u64)) == cudaSuccess &&
          cudaMemset(ctx->ctr, 0, sizeof(Counters)) == cudaSuccess &&
          cudaMemset(ctx->rows.cnt, 0, nrow * sizeof(int32_t)) == cudaSuccess &&
          cudaMemset(ctx->rows.members, 0, nrow * sizeof(int64_t)) == cudaSuccess &&
@@ -199,7 +202,7 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
     if (!ctx) return EWSJF_OK;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    void* d[] = {ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->ctr, ctx->gap,
+    void* d[] = {ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
                  ctx->d_blog, ctx->d_summary, ctx->d_len, ctx->d_arr, ctx->d_cost, ctx->d_qid, ctx->d_topk_id,
                  ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score, ctx->d_max_score};
     for (void* p : d)
@@ -335,7 +338,7 @@ static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const floa
     const int nslots = part->n;
     const bool has_cost = d_cost != nullptr;
     const int K = select ? sp->k : 1;
-    const int cap = cap_for(K);
+    int cap = cap_for(K);
     PartialArgs A;
     memset(&A, 0, sizeof A);
     A.len = d_len;
@@ -349,8 +352,6 @@ static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const floa
             (route ? (!d_qid_out || aligned16(d_qid_out)) : aligned16(d_qid_in));
     A.K = K;
     A.cap = cap;
-    A.tgt = K + (cap - K) / 4;
-    A.hwm = cap - (cap - K) / 4;
     A.ids_identity = 1;
     for (int i = 0; i < nslots; i++)
         if (part->q[i].id != i) A.ids_identity = 0;
@@ -358,7 +359,7 @@ static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const floa
     A.select = select ? 1 : 0;
     A.sp = select ? score_params(sp) : ScoreParams{0.f, 0.f, 0.f, 0.f, 0, 1};
     A.rows = ctx->rows;
-    A.rows.cap = cap;
+    A.rows.cap = K;
     A.gthr = ctx->gthr;
     A.gap = ctx->gap;
     A.gap_cap = ctx->gap_cap;
@@ -378,16 +379,29 @@ static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const floa
     // slot groups so that the candidate buffers fit in shared memory
     int ngs = std::max(nslots, 1);
     const int budget = ctx->smem_optin > 0 ? ctx->smem_optin : 232448;
-    auto smem_for = [&](int g) {
+    auto smem_for_cap = [&](int g, int c) {
         return partial_smem_bytes(route, has_cost, A.tma, use_lut ? A.lut_size : 0, nslots, A.nids, 1,
-                                  A.cnt_thread, g, cap);
+                                  A.cnt_thread, g, c);
     };
+    auto smem_for = [&](int g) { return smem_for_cap(g, cap); };
     if (A.cnt_thread && smem_for(1) > budget) A.cnt_thread = 0;
     while (ngs > 1 && smem_for(ngs) > budget) ngs = (ngs + 1) / 2;
     if (smem_for(ngs) > budget)
         return fail(ctx, EWSJF_ERR_UNSUPPORTED, "tick does not fit shared memory (k=%d)", K);
+    // grow the candidate buffers into the remaining shared memory (fewer compactions)
+    if (select) {
+        while (cap < 1024 && smem_for_cap(ngs, cap + 32) <= budget - 1024) cap += 32;
+    }
+    A.cap = cap;
+    A.tgt = K + (cap - K) / 8;
+    A.hwm = cap - 16;
     const int passes = select ? std::max(1, (nslots + ngs - 1) / ngs) : 1;
     const bool fuse_ok = fuse && passes == 1 && ctx->coop && smem_for(ngs) <= budget;
+    A.dyn = (fuse_ok && !getenv("EWSJF_NO_DYN")) ? 1 : 0;
+    // threshold board: one key per (queue, CTA) while G >= 2K
+    A.board = ctx->board;
+    A.board_m = 0;
+    if (fuse_ok && select && 2 * K <= ctx->num_sms && ctx->num_sms <= 320 && getenv("EWSJF_BOARD")) A.board_m = 1;
     for (int p = 0; p < passes; p++) {
         A.pass0 = p == 0;
         A.g_lo = select ? std::min(nslots, p * ngs) : 0;
@@ -417,7 +431,7 @@ static MergeArgs merge_args(ewsjf_ctx* ctx, const ewsjf_partition_t* part, const
         M.theta[3] = theta->b_u; M.theta[4] = theta->a_f; M.theta[5] = theta->b_f;
     }
     M.rows = ctx->rows;
-    M.rows.cap = cap_for(M.K);
+    M.rows.cap = M.K;
     M.ctr = ctx->ctr;
     M.gap = ctx->gap;
     M.gap_cap = ctx->gap_cap;

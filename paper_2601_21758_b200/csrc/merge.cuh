@@ -551,6 +551,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
     A.ctr->gap_count = 0;
     A.ctr->ticket = 0;
     A.ctr->barrier = 0;
+    A.ctr->tiles = 0;
 }
 
 }  // namespace ewsjf

@@ -27,6 +27,7 @@ struct Counters {        // device-global, zeroed by the merge for the next call
     unsigned long long gap_count;
     unsigned int ticket;
     unsigned int barrier;   // grid barrier of the fused tick kernel
+    unsigned long long tiles;   // dynamic tile scheduler of the fused tick kernel
     // diagnostics, accumulated over calls (never reset by the kernels)
     unsigned long long dbg_inserted, dbg_compactions, dbg_overflow;
 };
@@ -43,6 +44,9 @@ struct PartialArgs {
     int32_t K, cap, tgt, hwm;   // selection depth, buffer capacity, compaction target / trigger
     int32_t ids_identity;       // stable id == position for every queue (qid = slot)
     int32_t cnt_thread;         // per-thread u16 member counters (<= 64 queues) vs warp match-any
+    int32_t dyn;                // dynamic tile scheduling (fused single-pass kernel)
+    int32_t board_m;            // cross-CTA threshold board: keys per (queue, CTA); 0 = off
+    u64* board;                 // [nslots][G][board_m]
     int32_t g_lo, g_hi;         // slot group handled by this pass (candidates)
     int32_t pass0;              // counts, qid, gaps, counters
     int32_t select;             // 0 = route only
