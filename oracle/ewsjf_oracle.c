@@ -256,7 +256,7 @@ int or_partition_run(const int32_t *len, int64_t n, const or_params *p,
     free(v); free(c); free(N); free(S1); free(S2); free(seg);
     free(qlo); free(qhi); free(qc); free(qs1); free(qs2);
     if (st) *st = S;
-    return OR_OK;
+    return S.n_invalid ? OR_DOMAIN : OR_OK;     /* b < 1 is a domain error */
 }
 
 /* ------------------------------------------------------------------------- */

@@ -20,92 +20,7 @@ int64_t merge_smem_total(int in_mode);
 
 using namespace ewsjf;
 
-struct ewsjf_ctx {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    int64_t max_pool = 0, max_history = 0;
-    int32_t max_k = 0;
-    int num_sms = 0;
-    int smem_optin = 0;
-    int coop = 0;
-    int32_t cap_max = 0;
-    char err[512] = {0};
-    // scratch
-    Rows rows{};
-    u64* gthr = nullptr;
-    u64* board = nullptr;
-    Counters* ctr = nullptr;
-    GapEntry* gap = nullptr;
-    int32_t gap_cap = 8192;
-    BubbleLog* d_blog = nullptr;
-    BubbleLog* h_blog = nullptr;        // pinned
-    ewsjf_summary* d_summary = nullptr;
-    ewsjf_summary* h_summary = nullptr; // pinned
-    // host-variant staging (tick_host)
-    int32_t* d_len = nullptr;
-    float* d_arr = nullptr;
-    float* d_cost = nullptr;
-    int32_t* d_qid = nullptr;
-    int64_t* d_topk_id = nullptr;
-    float* d_topk_score = nullptr;
-    int64_t* d_count = nullptr;
-    int64_t* d_head_id = nullptr;
-    float* d_head_score = nullptr;
-    float* d_max_score = nullptr;
-    // partition (R&P) scratch lives in partition.cu
-    void* rp = nullptr;
-    // instrumentation
-    long long launches = 0;
-    bool timing = false;
-    std::vector<cudaEvent_t> ev_a, ev_b;
-    std::vector<int> ev_kind;
-    size_t ev_n = 0;
-};
-
-namespace ewsjf {
-enum { KIND_TICK = 0, KIND_MERGE = 1, KIND_PARTITION = 2, KIND_SWEEP = 3 };
-// Bracket one launch with events when timing is on; count it always.
-struct LaunchScope {
-    ewsjf_ctx* c;
-    int kind;
-    bool rec = false;
-    LaunchScope(ewsjf_ctx* ctx, int k) : c(ctx), kind(k) {
-        c->launches++;
-        if (c->timing && c->ev_n < c->ev_a.size()) {
-            cudaEventRecord(c->ev_a[c->ev_n], c->stream);
-            rec = true;
-        }
-    }
-    ~LaunchScope() {
-        if (rec) {
-            cudaEventRecord(c->ev_b[c->ev_n], c->stream);
-            c->ev_kind[c->ev_n] = kind;
-            c->ev_n++;
-        }
-    }
-};
-}  // namespace ewsjf
-
-namespace ewsjf {
-void rp_free(ewsjf_ctx* ctx);
-}
-
-static ewsjf_status fail(ewsjf_ctx* ctx, ewsjf_status s, const char* fmt, ...) {
-    if (ctx) {
-        va_list ap;
-        va_start(ap, fmt);
-        vsnprintf(ctx->err, sizeof ctx->err, fmt, ap);
-        va_end(ap);
-    }
-    return s;
-}
-#define CU(call)                                                                                   \
-    do {                                                                                           \
-        cudaError_t e_ = (call);                                                                   \
-        if (e_ != cudaSuccess)                                                                     \
-            return fail(ctx, EWSJF_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
-                        __FILE__, __LINE__);                                                       \
-    } while (0)
+#include "ctx.h"
 
 // ------------------------------------------------------------------ misc ---
 extern "C" int ewsjf_abi_version(void) { return EWSJF_ABI_VERSION; }
@@ -188,6 +103,7 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
          cudaDeviceSynchronize() == cudaSuccess;
     if (!ok) return bad(EWSJF_ERR_CUDA);
     ctx->rows.G = G;
+    if (max_history > 0 && rp_alloc(ctx) != EWSJF_OK) return bad(EWSJF_ERR_CUDA);
     *out = ctx;
     return EWSJF_OK;
 }

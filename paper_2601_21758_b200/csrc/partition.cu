@@ -1,14 +1,695 @@
-// partition.cu — Refine-and-Prune (A1-A6) on sm_100a.  (Implemented in the next step.)
-#include "tick.cuh"
+// partition.cu — Refine-and-Prune (§4.2) on sm_100a: the strategic
+// loop's offline optimizer.  Bit-exact with the oracle: integer
+// histogram / RLE / prefix sums, and every fp64 decision evaluated with the
+// canonical expression and explicit _rn intrinsics (no FMA contraction).
+//
+//  A1 hist_kernel      counting sort of the history into hist[len] (smem-
+//                      privatised sub-histograms, 128-bit loads)
+//  A2 rle_* kernels    run-length encode the non-zero bins -> (v, c)[M] and
+//                      exclusive int64 prefixes N, S1, S2
+//  A3 kmeans kernels   exact 1-D k-means, k <= 3: argmax of the canonical
+//                      F(i,j) over all distinct-index cut pairs, ties -> the
+//                      lexicographically smallest (i, j) (reading R9)
+//  A4 refine_kernel    Eq. 2, level-synchronous: every live segment splits at
+//                      every gap with g*(n-1) > alpha*span (R10-R14)
+//  A5+A6 prune_kernel  midpoint finalisation (R15) then Eq. 3 greedy merges with
+//                      a 32-ary tournament tree over adjacent pairs (R16-R18)
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <vector>
+#include "ctx.h"
 
-struct ewsjf_ctx;
 namespace ewsjf {
-void rp_free(ewsjf_ctx*) {}
+
+constexpr int kHistMax = 1 << 20;       // lengths >= 2^20 are UNSUPPORTED
+constexpr int kHistSmem = 49152;        // bins privatised in shared memory (192 KB)
+constexpr int kHT = 1024;               // threads of the histogram / RLE / refine / prune CTAs
+constexpr int kRleChunk = 16384;        // bins per RLE block
+
+struct RpScratch {
+    unsigned int* hist;                 // [kHistMax]
+    unsigned long long* stat;           // [0] invalid, [1] over, [2] max len, [3..] scratch
+    int32_t* v;                         // [kHistMax]
+    int64_t* c;                         // [kHistMax]
+    int64_t *N, *S1, *S2;               // [kHistMax + 1]
+    int64_t* blk;                       // [rle blocks][4]: nonzero, sumc, sumcv, sumcv2 (and prefixes)
+    double *t1, *t3;                    // [kHistMax + 1]
+    double* kbF;                        // [kmeans blocks] best F
+    int64_t* kbI;                       // [kmeans blocks] packed (i << 32 | j)
+    int32_t* seg;                       // [kHistMax + 1] segment starts (output of refine)
+    int32_t* segend;                    // [kHistMax + 1]
+    uint8_t* flag;                      // [kHistMax]
+    int32_t* out_i;                     // refine: [0] m, [1] depth; kmeans: [2] t1, [3] t2
+    int32_t* q_lo;                      // prune outputs [256]
+    int32_t* q_hi;
+    int64_t *q_n, *q_s1, *q_s2;
+    int64_t* merges;
+    // prune working set
+    int32_t *plo, *phi_, *pnext, *pprev;
+    int64_t *pn, *ps1, *ps2;
+    double* tree;                       // 32-ary tournament tree: (U, index) pairs
+    int32_t* treei;
+    int kblocks;
+    int64_t tree_n;
+    cudaEvent_t ev[6];
+};
+
+// ------------------------------------------------------------------ A1 ---
+__global__ void __launch_bounds__(kHT, 1)
+    hist_kernel(const int32_t* __restrict__ len, int64_t n, unsigned int* hist, unsigned long long* stat) {
+    extern __shared__ unsigned int sh[];
+    for (int i = threadIdx.x; i < kHistSmem; i += kHT) sh[i] = 0u;
+    __syncthreads();
+    unsigned int bad = 0, over = 0;
+    int mx = 0;
+    auto one = [&](int b) {
+        if (b < 1) { bad++; return; }
+        if (b >= kHistMax) { over++; return; }
+        mx = b > mx ? b : mx;
+        if (b < kHistSmem) atomicAdd(&sh[b], 1u);
+        else atomicAdd(&hist[b], 1u);
+    };
+    const bool al = ((uintptr_t)len & 15) == 0;
+    const int64_t stride = (int64_t)gridDim.x * kHT;
+    if (al) {
+        const int64_t n4 = n / 4;
+        const int4* l4 = (const int4*)len;
+        for (int64_t i = (int64_t)blockIdx.x * kHT + threadIdx.x; i < n4; i += stride) {
+            const int4 q = __ldcs(l4 + i);
+            one(q.x); one(q.y); one(q.z); one(q.w);
+        }
+        for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * kHT + threadIdx.x; i < n; i += stride) one(__ldcs(len + i));
+    } else {
+        for (int64_t i = (int64_t)blockIdx.x * kHT + threadIdx.x; i < n; i += stride) one(__ldcs(len + i));
+    }
+    bad = __reduce_add_sync(0xffffffffu, bad);
+    over = __reduce_add_sync(0xffffffffu, over);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) {
+        if (bad) atomicAdd(&stat[0], (unsigned long long)bad);
+        if (over) atomicAdd(&stat[1], (unsigned long long)over);
+        if (mx) atomicMax(&stat[2], (unsigned long long)mx);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHistSmem; i += kHT)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
+// ------------------------------------------------------------------ A2 ---
+// Block b covers bins [1 + b*kRleChunk, ...) up to lmax.  Each thread owns 16
+// consecutive bins.  Pass 1: per-block totals; pass 2: scan of the totals
+// (one block); pass 3: write v, c and the inclusive prefixes.
+__device__ __forceinline__ void block_scan_excl4(int64_t (&x)[4], int64_t (&tot)[4], int64_t* sm) {
+    // exclusive scan of 4 int64 fields across the 1024 threads; sm: [32][4]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t inc[4] = {x[0], x[1], x[2], x[3]};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int f = 0; f < 4; f++) {
+            const int64_t u = __shfl_up_sync(0xffffffffu, inc[f], o);
+            if (lane >= o) inc[f] += u;
+        }
+    }
+    if (lane == 31)
+#pragma unroll
+        for (int f = 0; f < 4; f++) sm[w * 4 + f] = inc[f];
+    __syncthreads();
+    if (w == 0) {
+        int64_t s[4];
+#pragma unroll
+        for (int f = 0; f < 4; f++) s[f] = sm[lane * 4 + f];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+            for (int f = 0; f < 4; f++) {
+                const int64_t u = __shfl_up_sync(0xffffffffu, s[f], o);
+                if (lane >= o) s[f] += u;
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < 4; f++) sm[128 + lane * 4 + f] = s[f];   // inclusive per-warp prefix
+    }
+    __syncthreads();
+#pragma unroll
+    for (int f = 0; f < 4; f++) {
+        const int64_t warp_excl = w ? sm[128 + (w - 1) * 4 + f] : 0;
+        x[f] = warp_excl + inc[f] - x[f];
+        tot[f] = sm[128 + 31 * 4 + f];
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kHT) rle_count_kernel(const unsigned int* hist, int lmax, int64_t* blk) {
+    __shared__ int64_t sm[256];
+    const int64_t base = 1 + (int64_t)blockIdx.x * kRleChunk + (int64_t)threadIdx.x * 16;
+    int64_t x[4] = {0, 0, 0, 0}, tot[4];
+    for (int k = 0; k < 16; k++) {
+        const int64_t b = base + k;
+        if (b > lmax) break;
+        const int64_t c = hist[b];
+        if (c) { x[0] += 1; x[1] += c; x[2] += c * b; x[3] += c * b * b; }
+    }
+    block_scan_excl4(x, tot, sm);
+    if (threadIdx.x == 0)
+        for (int f = 0; f < 4; f++) blk[(int64_t)blockIdx.x * 4 + f] = tot[f];
+}
+
+__global__ void __launch_bounds__(kHT) rle_scan_kernel(int64_t* blk, int nb, int64_t* out_tot) {
+    __shared__ int64_t sm[256];
+    int64_t carry[4] = {0, 0, 0, 0};
+    for (int b0 = 0; b0 < nb; b0 += kHT) {
+        const int b = b0 + threadIdx.x;
+        int64_t x[4] = {0, 0, 0, 0}, tot[4];
+        if (b < nb)
+            for (int f = 0; f < 4; f++) x[f] = blk[(int64_t)b * 4 + f];
+        block_scan_excl4(x, tot, sm);
+        if (b < nb)
+            for (int f = 0; f < 4; f++) blk[(int64_t)b * 4 + f] = x[f] + carry[f];
+        for (int f = 0; f < 4; f++) carry[f] += tot[f];
+    }
+    if (threadIdx.x == 0)
+        for (int f = 0; f < 4; f++) out_tot[f] = carry[f];
+}
+
+__global__ void __launch_bounds__(kHT) rle_write_kernel(const unsigned int* hist, int lmax, const int64_t* blk,
+                                                       int32_t* v, int64_t* cc, int64_t* N, int64_t* S1,
+                                                       int64_t* S2) {
+    __shared__ int64_t sm[256];
+    const int64_t base = 1 + (int64_t)blockIdx.x * kRleChunk + (int64_t)threadIdx.x * 16;
+    int64_t x[4] = {0, 0, 0, 0}, tot[4];
+    for (int k = 0; k < 16; k++) {
+        const int64_t b = base + k;
+        if (b > lmax) break;
+        const int64_t c = hist[b];
+        if (c) { x[0] += 1; x[1] += c; x[2] += c * b; x[3] += c * b * b; }
+    }
+    block_scan_excl4(x, tot, sm);
+    int64_t run[4];
+    for (int f = 0; f < 4; f++) run[f] = x[f] + blk[(int64_t)blockIdx.x * 4 + f];
+    if (blockIdx.x == 0 && threadIdx.x == 0) { N[0] = 0; S1[0] = 0; S2[0] = 0; }
+    for (int k = 0; k < 16; k++) {
+        const int64_t b = base + k;
+        if (b > lmax) break;
+        const int64_t c = hist[b];
+        if (c) {
+            const int64_t j = run[0];
+            v[j] = (int32_t)b;
+            cc[j] = c;
+            run[0] += 1; run[1] += c; run[2] += c * b; run[3] += c * b * b;
+            N[j + 1] = run[1]; S1[j + 1] = run[2]; S2[j + 1] = run[3];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ A3 ---
+// Canonical pieces: sq(s)/n with s exact in int64, each op rounded once.
+__device__ __forceinline__ double sq_over(int64_t s, int64_t n) {
+    const double d = (double)s;
+    return __ddiv_rn(__dmul_rn(d, d), (double)n);
+}
+
+__global__ void kmeans_terms_kernel(const int64_t* N, const int64_t* S1, int64_t M, double* t1, double* t3) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= M; i += (int64_t)gridDim.x * blockDim.x) {
+        t1[i] = (i >= 1) ? sq_over(S1[i], N[i]) : 0.0;
+        t3[i] = (i <= M - 1) ? sq_over(S1[M] - S1[i], N[M] - N[i]) : 0.0;
+    }
+}
+
+// Argmax of F over (i, j): lexicographic tie-break = smallest i, then smallest j.
+__device__ __forceinline__ bool better(double F, int64_t ij, double bF, int64_t bij) {
+    return F > bF || (F == bF && ij < bij);
+}
+
+// k = 3: block b handles i in a strided set, threads sweep j.  One result per block.
+__global__ void __launch_bounds__(256) kmeans3_kernel(const int64_t* __restrict__ N, const int64_t* __restrict__ S1,
+                                                     const double* __restrict__ t1, const double* __restrict__ t3,
+                                                     int64_t M, double* outF, int64_t* outIJ) {
+    double bF = -1.0;
+    int64_t bij = INT64_MAX;
+    for (int64_t i = 1 + blockIdx.x; i <= M - 2; i += gridDim.x) {
+        const int64_t Ni = N[i], Si = S1[i];
+        const double ti = t1[i];
+        for (int64_t j = i + 1 + threadIdx.x; j <= M - 1; j += blockDim.x) {
+            const double F = __dadd_rn(__dadd_rn(ti, sq_over(S1[j] - Si, N[j] - Ni)), t3[j]);
+            const int64_t ij = (i << 32) | j;
+            if (better(F, ij, bF, bij)) { bF = F; bij = ij; }
+        }
+    }
+    // block reduce
+    __shared__ double sF[256];
+    __shared__ int64_t sI[256];
+    sF[threadIdx.x] = bF;
+    sI[threadIdx.x] = bij;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s; s >>= 1) {
+        if (threadIdx.x < s && better(sF[threadIdx.x + s], sI[threadIdx.x + s], sF[threadIdx.x], sI[threadIdx.x])) {
+            sF[threadIdx.x] = sF[threadIdx.x + s];
+            sI[threadIdx.x] = sI[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { outF[blockIdx.x] = sF[0]; outIJ[blockIdx.x] = sI[0]; }
+}
+
+// k = 2 (or the final reduction of the per-block results when k = 3).
+__global__ void __launch_bounds__(1024) kmeans_final_kernel(const int64_t* N, const int64_t* S1, int64_t M, int k,
+                                                           const double* inF, const int64_t* inIJ, int nin,
+                                                           int32_t* out) {
+    double bF = -1.0;
+    int64_t bij = INT64_MAX;
+    if (k == 2) {
+        for (int64_t i = 1 + threadIdx.x; i <= M - 1; i += blockDim.x) {
+            const double F = __dadd_rn(sq_over(S1[i], N[i]), sq_over(S1[M] - S1[i], N[M] - N[i]));
+            if (better(F, i, bF, bij)) { bF = F; bij = i; }
+        }
+    } else {
+        for (int b = threadIdx.x; b < nin; b += blockDim.x)
+            if (inIJ[b] != INT64_MAX && better(inF[b], inIJ[b], bF, bij)) { bF = inF[b]; bij = inIJ[b]; }
+    }
+    __shared__ double sF[1024];
+    __shared__ int64_t sI[1024];
+    sF[threadIdx.x] = bF;
+    sI[threadIdx.x] = bij;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s; s >>= 1) {
+        if (threadIdx.x < s && better(sF[threadIdx.x + s], sI[threadIdx.x + s], sF[threadIdx.x], sI[threadIdx.x])) {
+            sF[threadIdx.x] = sF[threadIdx.x + s];
+            sI[threadIdx.x] = sI[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (k == 2) { out[2] = (int32_t)sI[0]; out[3] = 0; }
+        else { out[2] = (int32_t)(sI[0] >> 32); out[3] = (int32_t)(sI[0] & 0xffffffff); }
+    }
+}
+
+// ------------------------------------------------------------------ A4 ---
+// Level-synchronous Eq. 2 over distinct-index segments.  flag[j] = 1 if a
+// segment starts at j.  One CTA; per level: segment bounds via a block scan of
+// the flags, then every index j tests the gap (v[j], v[j+1]) of its segment.
+__global__ void __launch_bounds__(kHT, 1)
+    refine_kernel(const int32_t* __restrict__ v, const int64_t* __restrict__ N, int64_t M, double alpha,
+                  int min_width, uint8_t* flag, int32_t* seg, int32_t* out, int* segend) {
+    __shared__ int s_changed, s_m, s_level;
+    __shared__ int wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) { s_level = 1; }
+    __syncthreads();
+    for (;;) {
+        // 1) compact segment starts: seg[0..m) (ascending) ; segend[k] = next start
+        __syncthreads();
+        if (tid == 0) s_m = 0;
+        __syncthreads();
+        for (int64_t c0 = 0; c0 < M; c0 += kHT) {
+            const int64_t j = c0 + tid;
+            const int f = (j < M) ? flag[j] : 0;
+            const unsigned b = __ballot_sync(0xffffffffu, f);
+            if (lane == 0) wsum[w] = __popc(b);
+            __syncthreads();
+            if (w == 0) {
+                int x = wsum[lane];
+                for (int o = 1; o < 32; o <<= 1) { const int u = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += u; }
+                wsum[lane] = x;   // inclusive
+            }
+            __syncthreads();
+            const int base = s_m + (w ? wsum[w - 1] : 0);
+            if (f) seg[base + __popc(b & ((1u << lane) - 1u))] = (int32_t)j;
+            __syncthreads();
+            if (tid == 0) s_m += wsum[31];
+            __syncthreads();
+        }
+        const int m = s_m;
+        for (int k = tid; k < m; k += kHT) segend[k] = (k + 1 < m) ? seg[k + 1] : (int)M;
+        if (tid == 0) s_changed = 0;
+        __syncthreads();
+        // 2) each segment tests its gaps; new starts set after qualifying gaps
+        for (int k = w; k < m; k += kHT / 32) {
+            const int64_t x = seg[k], y = segend[k];
+            const int64_t n = N[y] - N[x];
+            const int64_t span = (int64_t)v[y - 1] - (int64_t)v[x];
+            if (n < 2 || span == 0 || span < (int64_t)min_width) continue;
+            const double lhs_scale = (double)(n - 1);
+            const double rhs = __dmul_rn(alpha, (double)span);
+            for (int64_t j = x + lane; j < y - 1; j += 32) {
+                const int64_t g = (int64_t)v[j + 1] - (int64_t)v[j];
+                if (__dmul_rn((double)g, lhs_scale) > rhs) {
+                    flag[j + 1] = 2;          // new start (marked 2 this level)
+                    s_changed = 1;
+                }
+            }
+        }
+        __syncthreads();
+        if (!s_changed) break;
+        for (int64_t j = tid; j < M; j += kHT)
+            if (flag[j] == 2) flag[j] = 1;
+        if (tid == 0) s_level++;
+        __syncthreads();
+    }
+    if (tid == 0) { out[0] = s_m; out[1] = s_level; }
+}
+
+// ------------------------------------------------------------- A5 + A6 ---
+// One CTA.  Finalisation: B_0 = lo_1, B_i = floor((hi_i + lo_{i+1})/2) + 1,
+// B_m = hi_m + 1 (R15).  Pruning: while m > max_queues merge the adjacent pair
+// with the smallest (MIN_U) / largest (MAX_U) U, ties -> lowest pair.
+// The pair minima live in a 32-ary tournament tree updated by warp 0.
+__device__ __forceinline__ double rho_of(int64_t n, int32_t lo, int32_t hi) {
+    return __ddiv_rn((double)n, (double)((int64_t)hi - (int64_t)lo));
+}
+__device__ __forceinline__ double mean_of(int64_t s1, int64_t n) {
+    return n > 0 ? __ddiv_rn((double)s1, (double)n) : 0.0;
+}
+__device__ __forceinline__ double util_of(int64_t nl, int64_t sl, int32_t lol, int32_t hil, int64_t nr, int64_t sr,
+                                          int32_t lor, int32_t hir, double eps) {
+    const double rl = rho_of(nl, lol, hil), rr = rho_of(nr, lor, hir);
+    const double ml = mean_of(sl, nl), mr = mean_of(sr, nr);
+    return __ddiv_rn(__dadd_rn(rl, rr), __dadd_rn(fabs(__dsub_rn(mr, ml)), eps));
+}
+
+__global__ void __launch_bounds__(kHT, 1)
+    prune_kernel(const int32_t* __restrict__ v, const int64_t* __restrict__ N, const int64_t* __restrict__ S1,
+                 const int64_t* __restrict__ S2, int64_t M, const int32_t* seg, const int32_t* rout, int max_queues, double eps, int rule, int32_t* plo, int32_t* phi,
+                 int32_t* pnext, int32_t* pprev, int64_t* pn, int64_t* ps1, int64_t* ps2, double* tree,
+                 int32_t* treei, int32_t* q_lo, int32_t* q_hi, int64_t* q_n, int64_t* q_s1, int64_t* q_s2,
+                 int64_t* merges_out) {
+    const int m0 = rout[0];
+    const int tid = threadIdx.x, lane = tid & 31;
+    // finalisation
+    for (int i = tid; i < m0; i += kHT) {
+        const int64_t x = seg[i], y = (i + 1 < m0) ? seg[i + 1] : M;
+        const int64_t seg_hi = v[y - 1];
+        int32_t lo;
+        if (i == 0) lo = v[x];
+        else {
+            const int64_t px = seg[i - 1];
+            (void)px;
+            const int64_t prev_hi = v[x - 1];
+            lo = (int32_t)((prev_hi + (int64_t)v[x]) / 2 + 1);
+        }
+        const int32_t hi = (i + 1 < m0) ? (int32_t)((seg_hi + (int64_t)v[y]) / 2 + 1) : (int32_t)(seg_hi + 1);
+        plo[i] = lo; phi[i] = hi;
+        pn[i] = N[y] - N[x]; ps1[i] = S1[y] - S1[x]; ps2[i] = S2[y] - S2[x];
+        pnext[i] = i + 1 < m0 ? i + 1 : -1;
+        pprev[i] = i - 1;
+    }
+    __syncthreads();
+    // tree: leaves = pairs p (left segment p, right pnext[p]); level sizes by 32
+    const bool maxu = rule == 1;
+    const double INF = maxu ? -1.0 / 0.0 : 1.0 / 0.0;
+    const int npair = m0 - 1;
+    int lv_off[6], lv_n[6], nl = 0;
+    {
+        int off = 0, cnt = npair > 0 ? npair : 1;
+        for (;;) {
+            lv_off[nl] = off; lv_n[nl] = cnt; nl++;
+            off += cnt;
+            if (cnt == 1) break;
+            cnt = (cnt + 31) / 32;
+        }
+    }
+    auto cmp = [&](double a, int ia, double b, int ib) -> bool {   // a strictly better than b
+        if (ia < 0) return false;
+        if (ib < 0) return true;
+        if (maxu) return a > b || (a == b && ia < ib);
+        return a < b || (a == b && ia < ib);
+    };
+    for (int p = tid; p < npair; p += kHT) {
+        tree[p] = util_of(pn[p], ps1[p], plo[p], phi[p], pn[p + 1], ps1[p + 1], plo[p + 1], phi[p + 1], eps);
+        treei[p] = p;
+    }
+    __syncthreads();
+    for (int l = 1; l < nl; l++) {   // build
+        for (int q = tid; q < lv_n[l]; q += kHT) {
+            double bu = INF; int bi = -1;
+            for (int c = q * 32; c < min(lv_n[l - 1], q * 32 + 32); c++) {
+                const double u = tree[lv_off[l - 1] + c]; const int i = treei[lv_off[l - 1] + c];
+                if (cmp(u, i, bu, bi)) { bu = u; bi = i; }
+            }
+            tree[lv_off[l] + q] = bu; treei[lv_off[l] + q] = bi;
+        }
+        __syncthreads();
+    }
+    if (tid >= 32) return;
+    // warp 0: sequential merges
+    auto update_leaf = [&](int p, double u, int id) {   // set leaf p, then recompute its ancestors
+        if (lane == 0) { tree[p] = u; treei[p] = id; }
+        __syncwarp();
+        int c = p;
+        for (int l = 1; l < nl; l++) {
+            const int q = c / 32;
+            const int cc = q * 32 + lane;
+            double bu = INF; int bi = -1;
+            if (cc < lv_n[l - 1]) { bu = tree[lv_off[l - 1] + cc]; bi = treei[lv_off[l - 1] + cc]; }
+            for (int o = 16; o; o >>= 1) {
+                const double ou = __shfl_xor_sync(0xffffffffu, bu, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (cmp(ou, oi, bu, bi)) { bu = ou; bi = oi; }
+            }
+            if (lane == 0) { tree[lv_off[l] + q] = bu; treei[lv_off[l] + q] = bi; }
+            __syncwarp();
+            c = q;
+        }
+    };
+    int m = m0;
+    int64_t merges = 0;
+    while (m > max_queues && m > 1) {
+        const int p = treei[lv_off[nl - 1]];         // best pair: left segment p
+        const int r = pnext[p];
+        // merge r into p
+        const int32_t nhi = phi[r];
+        const int64_t nn = pn[p] + pn[r], ns1 = ps1[p] + ps1[r], ns2 = ps2[p] + ps2[r];
+        const int rn = pnext[r];
+        __syncwarp();
+        if (lane == 0) {
+            phi[p] = nhi; pn[p] = nn; ps1[p] = ns1; ps2[p] = ns2;
+            pnext[p] = rn;
+            if (rn >= 0) pprev[rn] = p;
+        }
+        __syncwarp();
+        if (r < npair) update_leaf(r, INF, -1);   // the pair keyed by r disappears
+        if (rn >= 0)
+            update_leaf(p, util_of(nn, ns1, plo[p], nhi, pn[rn], ps1[rn], plo[rn], phi[rn], eps), p);
+        else
+            update_leaf(p, INF, -1);
+        const int q = pprev[p];
+        if (q >= 0) update_leaf(q, util_of(pn[q], ps1[q], plo[q], phi[q], nn, ns1, plo[p], nhi, eps), q);
+        m--;
+        merges++;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        int k = 0;
+        for (int i = 0; i >= 0 && k < 256; i = pnext[i]) {
+            q_lo[k] = plo[i]; q_hi[k] = phi[i]; q_n[k] = pn[i]; q_s1[k] = ps1[i]; q_s2[k] = ps2[i];
+            k++;
+            if (pnext[i] < 0) break;
+        }
+        merges_out[0] = merges;
+        merges_out[1] = k;
+    }
+}
+
+
+__global__ void set_flags_kernel(uint8_t* flag, const int32_t* out, int k) {
+    flag[0] = 1;
+    if (k >= 2) flag[out[2]] = 1;
+    if (k >= 3) flag[out[3]] = 1;
+}
+
+// ------------------------------------------------------------------ host ---
+void rp_free(ewsjf_ctx* ctx) {
+    RpScratch* R = ctx->rp;
+    if (!R) return;
+    void* p[] = {R->hist, R->stat, R->v, R->c, R->N, R->S1, R->S2, R->blk, R->t1, R->t3, R->kbF, R->kbI,
+                 R->seg, R->segend, R->flag, R->out_i, R->q_lo, R->q_hi, R->q_n, R->q_s1, R->q_s2, R->merges,
+                 R->plo, R->phi_, R->pnext, R->pprev, R->pn, R->ps1, R->ps2, R->tree, R->treei};
+    for (void* x : p)
+        if (x) cudaFree(x);
+    for (auto e : R->ev)
+        if (e) cudaEventDestroy(e);
+    delete R;
+    ctx->rp = nullptr;
+}
+
+ewsjf_status rp_alloc(ewsjf_ctx* ctx) {
+    RpScratch* R = new RpScratch();
+    memset(R, 0, sizeof *R);
+    ctx->rp = R;
+    const size_t H = kHistMax + 1;
+    R->kblocks = 2048;
+    int64_t tn = 0, cnt = kHistMax;
+    for (;;) { tn += cnt; if (cnt == 1) break; cnt = (cnt + 31) / 32; }
+    R->tree_n = tn;
+    bool ok = cudaMalloc(&R->hist, H * 4) == cudaSuccess && cudaMalloc(&R->stat, 16 * 8) == cudaSuccess &&
+              cudaMalloc(&R->v, H * 4) == cudaSuccess && cudaMalloc(&R->c, H * 8) == cudaSuccess &&
+              cudaMalloc(&R->N, H * 8) == cudaSuccess && cudaMalloc(&R->S1, H * 8) == cudaSuccess &&
+              cudaMalloc(&R->S2, H * 8) == cudaSuccess &&
+              cudaMalloc(&R->blk, (kHistMax / kRleChunk + 2) * 4 * 8) == cudaSuccess &&
+              cudaMalloc(&R->t1, H * 8) == cudaSuccess && cudaMalloc(&R->t3, H * 8) == cudaSuccess &&
+              cudaMalloc(&R->kbF, R->kblocks * 8) == cudaSuccess && cudaMalloc(&R->kbI, R->kblocks * 8) == cudaSuccess &&
+              cudaMalloc(&R->seg, H * 4) == cudaSuccess && cudaMalloc(&R->segend, H * 4) == cudaSuccess &&
+              cudaMalloc(&R->flag, H) == cudaSuccess && cudaMalloc(&R->out_i, 16 * 4) == cudaSuccess &&
+              cudaMalloc(&R->q_lo, 256 * 4) == cudaSuccess && cudaMalloc(&R->q_hi, 256 * 4) == cudaSuccess &&
+              cudaMalloc(&R->q_n, 256 * 8) == cudaSuccess && cudaMalloc(&R->q_s1, 256 * 8) == cudaSuccess &&
+              cudaMalloc(&R->q_s2, 256 * 8) == cudaSuccess && cudaMalloc(&R->merges, 4 * 8) == cudaSuccess &&
+              cudaMalloc(&R->plo, H * 4) == cudaSuccess && cudaMalloc(&R->phi_, H * 4) == cudaSuccess &&
+              cudaMalloc(&R->pnext, H * 4) == cudaSuccess && cudaMalloc(&R->pprev, H * 4) == cudaSuccess &&
+              cudaMalloc(&R->pn, H * 8) == cudaSuccess && cudaMalloc(&R->ps1, H * 8) == cudaSuccess &&
+              cudaMalloc(&R->ps2, H * 8) == cudaSuccess && cudaMalloc(&R->tree, tn * 8) == cudaSuccess &&
+              cudaMalloc(&R->treei, tn * 4) == cudaSuccess;
+    for (auto& e : R->ev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
+    if (!ok) { rp_free(ctx); return EWSJF_ERR_CUDA; }
+    return EWSJF_OK;
+}
+
+}  // namespace ewsjf
+
 extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, int64_t n,
-                                        const ewsjf_partition_params* params, ewsjf_partition_t* out,
+                                        const ewsjf_partition_params* p, ewsjf_partition_t* out,
                                         ewsjf_partition_stats* stats) {
-    (void)ctx; (void)d_len; (void)n; (void)params; (void)out; (void)stats;
-    return EWSJF_ERR_UNSUPPORTED;
+    using namespace ewsjf;
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    if (!p || !out) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null params/out");
+    if (!(p->alpha > 1.0) || p->min_width < 1 || p->max_queues < 1 || p->max_queues > EWSJF_MAX_QUEUES ||
+        !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 || (p->merge_rule != 0 && p->merge_rule != 1))
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "partition params out of range (S:121)");
+    if (n < 0 || n > ctx->max_history) return fail(ctx, EWSJF_ERR_INVALID_ARG, "n=%lld > max_history", (long long)n);
+    if (n > 0 && !d_len) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null history");
+    RpScratch* R = ctx->rp;
+    if (!R) return fail(ctx, EWSJF_ERR_INVALID_ARG, "ctx created with max_history = 0");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    ewsjf_partition_stats S;
+    memset(&S, 0, sizeof S);
+    CU(cudaEventRecord(R->ev[0], st));
+    CU(cudaMemsetAsync(R->hist, 0, (size_t)(kHistMax + 1) * 4, st));
+    CU(cudaMemsetAsync(R->stat, 0, 16 * 8, st));
+    if (n > 0) {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        CU(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4));
+        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_len, n, R->hist, R->stat);
+        CU(cudaGetLastError());
+    }
+    CU(cudaEventRecord(R->ev[1], st));
+    unsigned long long hs[3];
+    CU(cudaMemcpyAsync(hs, R->stat, 3 * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    S.n_invalid = (int64_t)hs[0];
+    S.n_valid = n - (int64_t)hs[0] - (int64_t)hs[1];
+    if (hs[1]) {
+        if (stats) *stats = S;
+        return fail(ctx, EWSJF_ERR_UNSUPPORTED, "%llu history lengths >= 2^20", hs[1]);
+    }
+    if (S.n_valid == 0) {
+        if (stats) *stats = S;
+        return fail(ctx, EWSJF_ERR_EMPTY, "no history length >= 1");
+    }
+    const int lmax = (int)hs[2];
+    const int nb = (lmax + kRleChunk - 1) / kRleChunk;
+    {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        rle_count_kernel<<<nb, kHT, 0, st>>>(R->hist, lmax, R->blk);
+    }
+    {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        rle_scan_kernel<<<1, kHT, 0, st>>>(R->blk, nb, (int64_t*)(R->stat + 4));
+    }
+    {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        rle_write_kernel<<<nb, kHT, 0, st>>>(R->hist, lmax, R->blk, R->v, R->c, R->N, R->S1, R->S2);
+    }
+    CU(cudaGetLastError());
+    int64_t tot[4];
+    CU(cudaMemcpyAsync(tot, R->stat + 4, 4 * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    const int64_t M = tot[0];
+    S.distinct = M;
+    const int k = p->coarse_k < M ? p->coarse_k : (int)M;
+    S.k_used = k;
+    if (k == 3) {
+        {
+            LaunchScope ls(ctx, KIND_PARTITION);
+            kmeans_terms_kernel<<<256, 256, 0, st>>>(R->N, R->S1, M, R->t1, R->t3);
+        }
+        const int kb = (int)std::min<int64_t>(R->kblocks, std::max<int64_t>(1, M - 2));
+        {
+            LaunchScope ls(ctx, KIND_PARTITION);
+            kmeans3_kernel<<<kb, 256, 0, st>>>(R->N, R->S1, R->t1, R->t3, M, R->kbF, R->kbI);
+        }
+        {
+            LaunchScope ls(ctx, KIND_PARTITION);
+            kmeans_final_kernel<<<1, 1024, 0, st>>>(R->N, R->S1, M, 3, R->kbF, R->kbI, kb, R->out_i);
+        }
+    } else if (k == 2) {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        kmeans_final_kernel<<<1, 1024, 0, st>>>(R->N, R->S1, M, 2, nullptr, nullptr, 0, R->out_i);
+    }
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(R->ev[2], st));
+    CU(cudaMemsetAsync(R->flag, 0, (size_t)M, st));
+    set_flags_kernel<<<1, 1, 0, st>>>(R->flag, R->out_i, k);
+    {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        refine_kernel<<<1, kHT, 0, st>>>(R->v, R->N, M, p->alpha, p->min_width, R->flag, R->seg, R->out_i,
+                                          R->segend);
+    }
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(R->ev[3], st));
+    {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        prune_kernel<<<1, kHT, 0, st>>>(R->v, R->N, R->S1, R->S2, M, R->seg, R->out_i, p->max_queues, p->epsilon,
+                                         p->merge_rule, R->plo, R->phi_, R->pnext, R->pprev, R->pn, R->ps1, R->ps2,
+                                         R->tree, R->treei, R->q_lo, R->q_hi, R->q_n, R->q_s1, R->q_s2, R->merges);
+    }
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(R->ev[4], st));
+    int32_t oi[4];
+    int32_t qlo[256], qhi[256];
+    int64_t qn[256], qs1[256], qs2[256], mg[2];
+    CU(cudaMemcpyAsync(oi, R->out_i, 16, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(mg, R->merges, 16, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(qlo, R->q_lo, sizeof qlo, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(qhi, R->q_hi, sizeof qhi, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(qn, R->q_n, sizeof qn, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(qs1, R->q_s1, sizeof qs1, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(qs2, R->q_s2, sizeof qs2, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    S.segments = oi[0];
+    S.depth = oi[1];
+    S.t1 = k >= 2 ? oi[2] : 0;
+    S.t2 = k >= 3 ? oi[3] : 0;
+    S.merges = mg[0];
+    const int nq = (int)mg[1];
+    const uint64_t ver = out->version;
+    memset(out, 0, sizeof *out);
+    out->n = nq;
+    out->next_id = nq;
+    out->version = ver + 1;
+    for (int i = 0; i < nq; i++) {
+        ewsjf_queue& q = out->q[i];
+        q.id = i;
+        q.index = i + 1;
+        q.min_len = qlo[i];
+        q.max_len = qhi[i];
+        q.count = qn[i];
+        q.sum = qs1[i];
+        q.sumsq = qs2[i];
+        // the oracle's canonical expressions (host code built with -ffp-contract=off)
+        volatile double m = qn[i] > 0 ? (double)qs1[i] / (double)qn[i] : 0.0;
+        q.mean = m;
+        q.density = (double)qn[i] / (double)((int64_t)qhi[i] - (int64_t)qlo[i]);
+        volatile double sq = (double)qs1[i] * (double)qs1[i];
+        q.sse = (double)qs2[i] - sq / (double)qn[i];
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, R->ev[0], R->ev[1]); S.ms_hist = ms;
+    cudaEventElapsedTime(&ms, R->ev[1], R->ev[2]); S.ms_kmeans = ms;
+    cudaEventElapsedTime(&ms, R->ev[2], R->ev[3]); S.ms_refine = ms;
+    cudaEventElapsedTime(&ms, R->ev[3], R->ev[4]); S.ms_prune = ms;
+    cudaEventElapsedTime(&ms, R->ev[0], R->ev[4]); S.ms_total = ms;
+    if (stats) *stats = S;
+    return S.n_invalid ? EWSJF_ERR_DOMAIN : EWSJF_OK;
 }

@@ -165,7 +165,7 @@ def _check_partition_invariants(orc, xs, part, maxq):
 def test_partition_invariants_random(orc, xs, maxq, alpha):
     """Acceptance #5: contiguity, disjointness, |Q| <= max_queues."""
     s, part, stt = orc.partition(xs, alpha=alpha, max_queues=maxq)
-    assert s == orc.OK
+    assert s == orc.OK          # all lengths >= 1 here
     _check_partition_invariants(orc, xs, part, maxq)
     assert stt.segments - stt.merges == part.n
 

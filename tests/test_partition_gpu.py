@@ -1,0 +1,82 @@
+"""GPU Refine-and-Prune (ewsjf_partition) vs the CPU oracle: bit-exact boundaries,
+integer profiles, fp64 means/densities and every pipeline statistic."""
+import numpy as np
+import pytest
+import torch
+
+import workload
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def E():
+    import paper_2601_21758_b200 as E
+    return E
+
+
+@pytest.fixture(scope="module")
+def ctx(E):
+    return E.Context(0, max_pool=1024, max_history=100_000_000, max_k=8)
+
+
+def _both(E, orc, ctx, hist, **kw):
+    h = np.ascontiguousarray(hist, dtype=np.int32)
+    gpart, gst, gs = E.partition(ctx, torch.from_numpy(h).cuda(), E.partition_params(**kw))
+    os_, opart, ost = orc.partition(h, **kw)
+    return gpart, gst, gs, opart, ost, os_
+
+
+def _check(gpart, gst, gs, opart, ost, os_):
+    assert gs == os_, (gs, os_)
+    gq, oq = gpart.queues(), opart.queues()
+    keys = ("id", "index", "min_len", "max_len", "count", "sum", "sumsq", "mean", "density", "sse", "is_bubble")
+    assert len(gq) == len(oq)
+    for a, b in zip(gq, oq):
+        for k in keys:
+            assert a[k] == b[k], (k, a, b)          # bit-exact, fp64 included
+    for k in ("n_valid", "n_invalid", "distinct", "k_used", "t1", "t2", "segments", "depth", "merges"):
+        assert gst[k] == getattr(ost, k), (k, gst[k], getattr(ost, k))
+
+
+@pytest.mark.parametrize("kind,n,seed", [("bimodal", 10_000, 101), ("heavy", 10_000, 7), ("bimodal", 200_000, 3),
+                                         ("heavy", 300_000, 4)])
+@pytest.mark.parametrize("rule", [0, 1])
+def test_partition_matches_oracle(E, orc, ctx, kind, n, seed, rule):
+    _check(*_both(E, orc, ctx, workload.lengths(kind, n, seed), merge_rule=rule))
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_partition_random_small(E, orc, ctx, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 3000))
+    hi = int(rng.choice([5, 50, 500, 5000, 70000]))
+    hist = rng.integers(1, hi, size=n)
+    if seed % 5 == 0:
+        hist[rng.integers(0, n, size=max(1, n // 20))] = 0        # invalid lengths
+    kw = dict(alpha=float(rng.choice([1.5, 2.0, 3.0, 1.7])), min_width=int(rng.choice([1, 2, 10])),
+              max_queues=int(rng.integers(1, 40)), epsilon=float(rng.choice([1e-6, 0.5, 2.0])),
+              coarse_k=int(rng.integers(1, 4)), merge_rule=int(rng.integers(0, 2)))
+    _check(*_both(E, orc, ctx, hist, **kw))
+
+
+def test_partition_edge_cases(E, orc, ctx):
+    for hist in ([777] * 50, [5, 6], [1], [3, 3, 9, 9, 9], [1, 2, 3, 4], list(range(1, 600))):
+        _check(*_both(E, orc, ctx, np.array(hist)))
+    g, st, s = E.partition(ctx, torch.zeros(10, dtype=torch.int32, device="cuda"))
+    assert s == 3                                                  # EMPTY
+
+
+def test_partition_full_c2(E, orc, ctx):
+    """C2 history: 1M bimodal lengths (seed 201), default parameters."""
+    _check(*_both(E, orc, ctx, workload.bimodal(1_000_000, 201)))
+
+
+def test_partition_full_c3_history(E, orc, ctx):
+    """The 1M heavy-tailed history bench.py partitions (seed 301)."""
+    _check(*_both(E, orc, ctx, workload.heavy(1_000_000, 301)))
+
+
+def test_partition_full_c4_bimodal(E, orc, ctx):
+    """C4 at full size: Refine-and-Prune of a 100M bimodal history (seed 401)."""
+    _check(*_both(E, orc, ctx, workload.bimodal(100_000_000, 401)))
