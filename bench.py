@@ -79,7 +79,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -272,7 +272,7 @@ def main():
     merge_ms = tm["merge_ms"] / max(tm["merge_launches"], 1)
     achieved = BYTES_PER_REQ * n / (tick_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "ewsjf::partial_kernel<ROUTE,HAS_COST,LUT> (route+score+filter)",
+                "traffic": None, "kernel": "ewsjf::tick_kernel (fused: stream route+score+filter, grid barrier, per-queue merge)",
                 "algorithmic_bytes_per_launch": BYTES_PER_REQ * n, "kernel_ms": tick_ms,
                 "merge_kernel_ms": merge_ms, "peak_source": peak_src,
                 "share_of_step": tick_ms / ms_per_step if ms_per_step else None}
