@@ -123,6 +123,8 @@ def lib():
                                    P(C.c_float), P(SelectParams), P(C.c_double), P(C.c_int8)]
         L.or_tick.argtypes = [P(C.c_int32), P(C.c_float), P(C.c_float), C.c_int64, C.c_int64, P(Partition),
                               C.c_int32, P(Meta), P(SelectParams), P(C.c_int32), P(SelectOut)]
+        L.or_sweep.argtypes = [P(C.c_int32), P(C.c_float), P(C.c_float), P(C.c_int32), C.c_int64, C.c_int64,
+                               P(Partition), P(Meta), C.c_int32, P(SelectParams), P(SelectOut)]
     return _lib
 
 
@@ -304,6 +306,23 @@ def score_select(lengths, arrival, cost, qid, part: Partition, w, sp: SelectPara
                               _p(q, C.c_int32), len(x), global_base, C.byref(part), _p(wf, C.c_float),
                               C.byref(sp), C.byref(o.s))
     return o.result(part.n, sp.k, s, part)
+
+
+def sweep(lengths, arrival, cost, qid, part: Partition, thetas, sp: SelectParams, global_base=0):
+    """O11: O7 -> O9 -> O10 per Θ over one routed snapshot; returns (status, [result per Θ])."""
+    x = _i32(lengths); a = _f32(arrival); q = _i32(qid)
+    cst = _f32(cost) if cost is not None else None
+    outs = [_Outs(part.n, sp.k) for _ in thetas]
+    thetas = [t if isinstance(t, Meta) else meta(**t) for t in thetas]
+    arr = (Meta * max(1, len(thetas)))(*thetas)
+    so = (SelectOut * max(1, len(thetas)))(*[o.s for o in outs])
+    s = lib().or_sweep(_p(x, C.c_int32), _p(a, C.c_float), _p(cst, C.c_float) if cst is not None else None,
+                       _p(q, C.c_int32), len(x), global_base, C.byref(part), arr, len(thetas), C.byref(sp), so)
+    res = []
+    for t, o in enumerate(outs):
+        o.s = so[t]
+        res.append(o.result(part.n, sp.k, s, part))
+    return s, res
 
 
 def score_all(lengths, arrival, cost, qid, part: Partition, theta: Meta, sp: SelectParams):

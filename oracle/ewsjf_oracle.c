@@ -491,3 +491,22 @@ void or_score_all(const int32_t *len, const float *arrival, const float *cost, c
         }
     }
 }
+
+/* O11 (A12): Θ sweep.  The meta-optimizer proposes Θ, evaluates the policy and
+ * keeps the best; its inner loop over one snapshot is,
+ * for every Θ, exactly one tactical scoring pass: O7 weights from Θ and the
+ * queue means, O9 scores (Eq. 4), O10 selection (Alg. 1 + top-K). */
+int or_sweep(const int32_t *len, const float *arrival, const float *cost, const int32_t *qid,
+             int64_t n, int64_t global_base, const or_partition *part,
+             const or_meta *thetas, int32_t n_theta, const or_select_params *sp,
+             or_select_out *outs) {
+    if (n_theta < 0 || sp->mode != OR_SCORE) return OR_INVALID;
+    int status = OR_OK;
+    float w[3 * OR_MAXQ];
+    for (int32_t t = 0; t < n_theta; t++) {
+        for (int32_t p = 0; p < part->n; p++) or_weights(&thetas[t], part->q[p].mean, &w[3 * p]);
+        int s = or_score_select(len, arrival, cost, qid, n, global_base, part, w, sp, &outs[t]);
+        if (status == OR_OK) status = s;
+    }
+    return status;
+}

@@ -164,6 +164,15 @@ int     or_tick(const int32_t *len, const float *arrival, const float *cost, int
                 const or_meta *theta, const or_select_params *sp,
                 int32_t *qid_out, or_select_out *out);
 
+/* O11 (A12): the Θ-batched evaluation of the meta-optimizer's scoring inner
+ * loop (§4.4.2): O7 -> O9 -> O10 for each thetas[t] over
+ * one routed snapshot; outs[t] receives Θ t.  Returns the first non-OK
+ * status of the per-Θ calls (DOMAIN if any request was excluded/invalid). */
+int     or_sweep(const int32_t *len, const float *arrival, const float *cost, const int32_t *qid,
+                 int64_t n, int64_t global_base, const or_partition *part,
+                 const or_meta *thetas, int32_t n_theta, const or_select_params *sp,
+                 or_select_out *outs);
+
 #ifdef __cplusplus
 }
 #endif

@@ -475,3 +475,81 @@ def test_alpha_monotonicity_is_per_node_only(orc):
             cur = {int(j) for j in np.nonzero(g * (n - 1) > a * span)[0]}
             assert prev is None or cur <= prev
             prev = cur
+
+
+# ------------------------------------------------------------ Θ sweep (A12) ---
+_SPECIAL_THETAS = [
+    dict(a_b=0, b_b=1, a_u=0, b_u=0, a_f=0, b_f=0),        # SJF within a queue
+    dict(a_b=0, b_b=0, a_u=0, b_u=1, a_f=0, b_f=0),        # urgency only
+    dict(a_b=0, b_b=0, a_u=0, b_u=0, a_f=0, b_f=1),        # fairness only
+    dict(a_b=-1, b_b=0, a_u=-1, b_u=0, a_f=-1, b_f=0),     # all weights clamp to 0: ids decide
+    dict(a_b=0.01, b_b=0.2, a_u=-0.01, b_u=1.0, a_f=0.02, b_f=0.1),
+]
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_sweep_vs_subset_enumeration(orc, seed):
+    """O11: every Θ of the sweep selects the brute-force optimal top-K subset
+    (pools of <= 20 requests, exact rational Eq. 4 up to the log term)."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(1, 19))
+    lens, arr, cost = _small_pool(rng, n)
+    part = orc.make_partition([(1, 20), (20, 40), (40, 60)])
+    s, qid, *_ = orc.route(lens, orc.copy_partition(part), 64)
+    K = int(rng.integers(1, 6))
+    sp = orc.select_params(k=K, mode=0, now=5.0)
+    thetas = _SPECIAL_THETAS + [dict(zip(("a_b", "b_b", "a_u", "b_u", "a_f", "b_f"),
+                                         rng.uniform([-0.05, 0, -0.05, 0, -0.05, 0], [0.05, 2, 0.05, 2, 0.05, 2])))
+                                for _ in range(3)]
+    st_, res = orc.sweep(lens, arr, cost, qid, part, thetas, sp, global_base=7)
+    assert len(res) == len(thetas)
+    for th, r in zip(thetas, res):
+        ne = []
+        for p in range(3):
+            w = orc.weights(orc.meta(**th), part.q[p].mean)
+            members = [i for i in range(n) if qid[i] == part.q[p].id]
+            exact = {i: brute.score_exact(p + 1, int(lens[i]), F32(5.0) - F32(arr[i]), F32(cost[i]),
+                                          F32(w[0]), F32(w[1]), F32(w[2])) for i in members}
+            assert r["count"][p] == len(members)
+            if not members:
+                assert r["topk_id"][p].tolist() == [-1] * K
+                continue
+            ne.append(p)
+            best = brute.topk_brute([(exact[i], -i) for i in members], K)
+            got = [int(g) - 7 for g in r["topk_id"][p] if g >= 0]
+            assert set(got) == {members[j] for j in best}, th
+            assert got == sorted(got, key=lambda i: (-exact[i], i))
+            for g, sc in zip(got, r["topk_score"][p]):
+                assert sc == pytest.approx(float(exact[g]), rel=1e-12, abs=1e-300)
+        if ne:
+            assert r["primary"] == max(ne, key=lambda p: (r["head_score"][p], -p))
+
+
+def F32(x):
+    return Fr(float(np.float32(x)))
+
+
+def test_sweep_special_cases_reduce_to_sorts(orc):
+    """Θ = (1,0,0) is SJF: per queue, ascending length then id.  All-zero weights:
+    every Φ = 0, so ascending id.  Doubling Θ doubles every weight exactly
+    (fp64 a·mean + b and the fp32 rounding commute with ×2) so ids are
+    unchanged and every score doubles exactly (Eq. 4 is linear in w)."""
+    rng = np.random.default_rng(3)
+    n = 2000
+    lens = rng.integers(1, 600, size=n).astype(np.int32)
+    arr = np.float32(rng.random(n) * 50)
+    part = orc.make_partition([(1, 100), (100, 300), (300, 1000)])
+    s, qid, *_ = orc.route(lens, orc.copy_partition(part), 64)
+    th = [_SPECIAL_THETAS[0], _SPECIAL_THETAS[3], _SPECIAL_THETAS[4],
+          {k: 2 * v for k, v in _SPECIAL_THETAS[4].items()}]
+    st_, res = orc.sweep(lens, arr, None, qid, part, th, orc.select_params(k=50, mode=0, now=60.0))
+    for p in range(3):
+        idx = np.nonzero(qid == part.q[p].id)[0]
+        sjf = idx[np.lexsort((idx, lens[idx]))][:50]
+        np.testing.assert_array_equal(res[0]["topk_id"][p], sjf)
+        np.testing.assert_array_equal(res[1]["topk_id"][p], idx[:50])
+        assert (res[1]["topk_score"][p] == 0).all()
+        np.testing.assert_array_equal(res[3]["topk_id"][p], res[2]["topk_id"][p])
+        np.testing.assert_array_equal(res[3]["topk_score"][p], 2 * res[2]["topk_score"][p])
+        assert res[3]["head_score"][p] == 2 * res[2]["head_score"][p]
+    assert res[1]["primary"] == 0                       # all head scores 0 -> lowest position (R24)
