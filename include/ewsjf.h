@@ -87,6 +87,13 @@ typedef struct {
 } ewsjf_timing;
 ewsjf_status ewsjf_ctx_set_timing(ewsjf_ctx *ctx, int32_t enable);
 ewsjf_status ewsjf_ctx_get_timing(ewsjf_ctx *ctx, ewsjf_timing *out);
+/* Diagnostics: with EWSJF_PHASES set in the environment the streaming tick
+ * records per-CTA phase timestamps (globaltimer ns): row c = out[16c .. 16c+15]
+ * = {start, setup done, streaming done (max over warps), all warps done,
+ * rows written, collectives, ns in collectives (CTA), first tile done, after
+ * the grid barrier, merge done, 0...}.  Copies min(n, num_ctas*16) values.
+ * Synchronises.                                                              */
+ewsjf_status ewsjf_ctx_get_phases(ewsjf_ctx *ctx, uint64_t *out, int32_t n);
 
 /* ------------------------------------------------------------- partition --- */
 /* Refine-and-Prune parameters (§4.2). alpha > 1 (Eq. 2 significance

@@ -93,6 +93,7 @@ SYMBOLS = [
     "ewsjf_ctx_destroy", "ewsjf_ctx_num_ctas", "ewsjf_partition", "ewsjf_weights_from_meta", "ewsjf_route",
     "ewsjf_score_select", "ewsjf_tick", "ewsjf_tick_host", "ewsjf_exchange_bytes", "ewsjf_tick_local",
     "ewsjf_tick_merge", "ewsjf_score_select_sweep", "ewsjf_ctx_set_timing", "ewsjf_ctx_get_timing",
+    "ewsjf_ctx_get_phases",
 ]
 
 _lib = None
@@ -119,6 +120,7 @@ def load() -> C.CDLL:
     L.ewsjf_ctx_num_ctas.restype = I32
     L.ewsjf_ctx_set_timing.argtypes = [V, I32]
     L.ewsjf_ctx_get_timing.argtypes = [V, P(Timing)]
+    L.ewsjf_ctx_get_phases.argtypes = [V, P(C.c_uint64), I32]
     L.ewsjf_partition.argtypes = [V, V, I64, P(PartitionParams), P(Partition), P(PartitionStats)]
     L.ewsjf_weights_from_meta.argtypes = [P(Meta), P(Partition), P(Weights)]
     L.ewsjf_route.argtypes = [V, V, I64, P(Partition), I32, V, P(Summary)]

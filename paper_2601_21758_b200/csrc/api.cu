@@ -16,6 +16,9 @@ int64_t partial_smem_bytes(bool route, bool has_cost, bool tma, int lut_size, in
                            int cnt_thread, int ngs, int cap);
 cudaError_t launch_merge(const MergeArgs& A, const Policy& P, bool has_cost, int grid, cudaStream_t st);
 int64_t merge_smem_total(int in_mode);
+cudaError_t launch_stream(const PartialArgs& A, const Policy& P, const MergeArgs* MA, bool has_cost, int grid,
+                          cudaStream_t st);
+int64_t stream_smem_bytes(bool has_cost, int lut_size, int nslots, int cap, int stages);
 }  // namespace ewsjf
 
 using namespace ewsjf;
@@ -74,8 +77,9 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
               cudaMalloc(&ctx->rows.members, nrow * sizeof(int64_t)) == cudaSuccess &&
               cudaMalloc(&ctx->rows.sec, nrow * sizeof(u64)) == cudaSuccess &&
               cudaMalloc(&ctx->gthr, kMaxSlots * sizeof(u64)) == cudaSuccess &&
-              cudaMalloc(&ctx->board, nrow * 2 * sizeof(u64)) == cudaSuccess &&
+              cudaMalloc(&ctx->board, nrow * 8 * sizeof(u64)) == cudaSuccess &&
               cudaMalloc(&ctx->ctr, sizeof(Counters)) == cudaSuccess &&
+              cudaMalloc(&ctx->dbg, (size_t)G * 16 * 8) == cudaSuccess &&
               cudaMalloc(&ctx->gap, (size_t)ctx->gap_cap * sizeof(GapEntry)) == cudaSuccess &&
               cudaMalloc(&ctx->d_blog, sizeof(BubbleLog)) == cudaSuccess &&
               cudaMallocHost(&ctx->h_blog, sizeof(BubbleLog)) == cudaSuccess &&
@@ -95,7 +99,7 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
     }
     if (!ok) return bad(EWSJF_ERR_CUDA);
     ok = cudaMemset(ctx->gthr, 0, kMaxSlots * sizeof(u64)) == cudaSuccess &&
-         cudaMemset(ctx->board, 0, nrow * 2 * sizeof(u64)) == cudaSuccess &&
+         cudaMemset(ctx->board, 0, nrow * 8 * sizeof(u64)) == cudaSuccess &&
          cudaMemset(ctx->ctr, 0, sizeof(Counters)) == cudaSuccess &&
          cudaMemset(ctx->rows.cnt, 0, nrow * sizeof(int32_t)) == cudaSuccess &&
          cudaMemset(ctx->rows.members, 0, nrow * sizeof(int64_t)) == cudaSuccess &&
@@ -118,7 +122,7 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
     if (!ctx) return EWSJF_OK;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    void* d[] = {ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
+    void* d[] = {ctx->dbg, ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
                  ctx->d_blog, ctx->d_summary, ctx->d_len, ctx->d_arr, ctx->d_cost, ctx->d_qid, ctx->d_topk_id,
                  ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score, ctx->d_max_score};
     for (void* p : d)
@@ -169,6 +173,15 @@ extern "C" ewsjf_status ewsjf_ctx_get_timing(ewsjf_ctx* ctx, ewsjf_timing* out) 
             default: out->sweep_ms += ms; out->sweep_launches++; break;
         }
     }
+    return EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_ctx_get_phases(ewsjf_ctx* ctx, uint64_t* out, int32_t n) {
+    if (!ctx || !out || n < 0) return EWSJF_ERR_INVALID_ARG;
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaStreamSynchronize(ctx->stream));
+    const int64_t m = std::min<int64_t>(n, (int64_t)ctx->num_sms * 16);
+    CU(cudaMemcpy(out, ctx->dbg, (size_t)m * 8, cudaMemcpyDeviceToHost));
     return EWSJF_OK;
 }
 
@@ -292,9 +305,43 @@ static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const floa
         A.nids = nslots;
         for (int i = 0; i < nslots; i++) { A.sorted_ids[i] = ids[i].first; A.sorted_slot[i] = ids[i].second; }
     }
+    const int budget = ctx->smem_optin > 0 ? ctx->smem_optin : 232448;
+    // The barrier-free streaming pass (stream.cu): LUT-routable partitions of
+    // <= 64 queues over a 16-byte aligned pool, all queues in one pass.
+    if (route && select && use_lut && nslots <= 64 && A.tma && !getenv("EWSJF_OLD_TICK")) {
+        // candidate buffer: K + 64 <= cap <= 256 (register selection holds 8 keys per lane)
+        int scap = std::min(256, (std::max(K + 64, 3 * K) + 31) & ~31);
+        int stages = 3;
+        if (const char* e = getenv("EWSJF_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
+        while (scap > K + 64 && stream_smem_bytes(has_cost, A.lut_size, nslots, scap, stages) > budget) scap -= 32;
+        while (stages > 2 && stream_smem_bytes(has_cost, A.lut_size, nslots, scap, stages) > budget) stages--;
+        A.stages = stages;
+        const int a_tma = A.tma;
+        A.tma = getenv("EWSJF_TMA_RING") ? 1 : 0;      // per-warp TMA bulk ring vs per-lane cp.async ring
+        if (scap >= K + 64 && stream_smem_bytes(has_cost, A.lut_size, nslots, scap, stages) <= budget) {
+            A.cap = scap;
+            A.hwm = scap - 32;
+            A.dbg = getenv("EWSJF_PHASES") ? ctx->dbg : nullptr;
+            if (getenv("EWSJF_STREAM_ONLY")) A.pass0 = 7;   // timing experiment only (wrong results)
+            // cross-CTA board: bm keys per (queue, CTA), G*bm <= 320 and >= K
+            A.board = ctx->board;
+            A.board_m = std::min(2, 320 / std::max(ctx->num_sms, 1));
+            if (const char* e = getenv("EWSJF_BOARD_M")) A.board_m = std::min(atoi(e), 320 / std::max(ctx->num_sms, 1));
+            if (ctx->num_sms * A.board_m < K) A.board_m = 0;
+            const bool fuse_s = fuse && ctx->coop && merge_smem_total(MERGE_IN_ROWS) <= budget;
+            cudaError_t e;
+            {
+                LaunchScope ls(ctx, KIND_TICK);
+                e = launch_stream(A, P, fuse_s ? fuse : nullptr, has_cost, ctx->num_sms, ctx->stream);
+            }
+            if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "stream tick kernel: %s", cudaGetErrorString(e));
+            if (fused) *fused = fuse_s;
+            return EWSJF_OK;
+        }
+        A.tma = a_tma;
+    }
     // slot groups so that the candidate buffers fit in shared memory
     int ngs = std::max(nslots, 1);
-    const int budget = ctx->smem_optin > 0 ? ctx->smem_optin : 232448;
     auto smem_for_cap = [&](int g, int c) {
         return partial_smem_bytes(route, has_cost, A.tma, use_lut ? A.lut_size : 0, nslots, A.nids, 1,
                                   A.cnt_thread, g, c);

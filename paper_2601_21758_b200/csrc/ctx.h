@@ -28,6 +28,7 @@ struct ewsjf_ctx {
     u64* board = nullptr;
     Counters* ctr = nullptr;
     GapEntry* gap = nullptr;
+    unsigned long long* dbg = nullptr;   // [num_sms][16] phase timestamps
     int32_t gap_cap = 8192;
     BubbleLog* d_blog = nullptr;
     BubbleLog* h_blog = nullptr;        // pinned

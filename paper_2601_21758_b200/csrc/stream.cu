@@ -1,0 +1,1076 @@
+// stream.cu — the streaming pass of the EWSJF tick on sm_100a (route A8 +
+// Eq. 4 score A10 + per-queue filter A11) and its fusion with the per-queue
+// merge (merge.cuh) behind one grid barrier.
+//
+// The tick is HBM-bound only if nothing makes the warps of an SM wait for each
+// other, so every warp owns a private ring of A.stages 1-D TMA bulk copies
+// (cp.async.bulk + mbarrier; 128 requests x {len, arrival, cost} per stage)
+// and walks its own warp tiles.  Per request the common path is: byte-LUT
+// route, qid store, weights (float4) + Eq. 4 (one MUFU.LG2, one MUFU.RCP), a
+// per-thread u16 member counter and two 32-bit threshold compares.
+//
+// The rare requests that beat their queue's threshold reserve a slot in the
+// queue's shared candidate buffer with one warp-aggregated atomicAdd per
+// distinct queue (no locks); past the buffer they spill into a CTA overflow
+// list.  When a buffer crosses its high-water mark the CTA meets in a
+// collective (named barrier, entered by each warp after its current tile, so
+// it happens a few times per launch, not per tile): one warp per queue cuts
+// buffer + overflow to the exact K-th key (warp quickselect), which raises the
+// queue's filter threshold and is published to the other CTAs (atomicMax on
+// gthr) together with the queue's top keys on a cross-CTA board; a few times
+// per launch each warp turns the board into a valid global threshold (the
+// K-th largest of distinct real keys).
+//
+// Paper: route = Dispatcher, score = Eq. 4, selection =
+// Alg. 1's per-queue scores + ArgMax; readings R1-R27.
+#include <climits>
+#include <cstdlib>
+#include "merge.cuh"
+
+namespace ewsjf {
+
+constexpr int kSThreads = 512;
+constexpr int kSWarps = kSThreads / 32;
+constexpr int kWT = 128;          // requests per warp tile (4 per lane)
+constexpr int kSStagesMax = 8;    // TMA ring depth per warp: runtime A.stages (<= 8)
+constexpr int kSTab = 256;        // per-code tables (codes 0..255 index them unmasked)
+constexpr int kOvfCap = kSWarps * kWT;   // overflow bound: one tile per warp after a flag
+constexpr int kBoardRegs = 10;    // board keys per lane in the board selection (G*m <= 320)
+constexpr int kSCodeGap = 0xFE;
+constexpr int kSCodeBad = 0xFF;
+
+__host__ __device__ inline int64_t sal16(int64_t x) { return (x + 15) & ~(int64_t)15; }
+
+struct SMisc {
+    int flag;       // some buffer crossed its high-water mark: collective wanted
+    int novf;       // overflow list fill
+    int ndone;      // warps done streaming
+    int pad;
+};
+
+struct StreamSmem {
+    int64_t ring, bars, w4, thr64, sec, thrhi, sechi, thrf, secf, sid, bcnt, misc, cnt, buf, ovfk, ovfq, lut, total;
+    int narr;
+};
+__host__ __device__ inline StreamSmem stream_layout(bool has_cost, int lut_size, int nslots, int cap, int stages) {
+    StreamSmem L;
+    L.narr = has_cost ? 3 : 2;
+    int64_t o = 0;
+    L.ring = o;  o += (int64_t)kSWarps * stages * L.narr * kWT * 4;
+    L.bars = o;  o = sal16(o + 8LL * kSWarps * stages);
+    L.w4 = o;    o = sal16(o + 16LL * kSTab);
+    L.thr64 = o; o = sal16(o + 8LL * kSTab);
+    L.sec = o;   o = sal16(o + 8LL * kSTab);
+    L.thrhi = o; o = sal16(o + 4LL * kSTab);
+    L.sechi = o; o = sal16(o + 4LL * kSTab);
+    L.thrf = o;  o = sal16(o + 4LL * kSTab);
+    L.secf = o;  o = sal16(o + 4LL * kSTab);
+    L.sid = o;   o = sal16(o + 12LL * kSTab);   // sid, round-1 counts, round-1 offsets
+    L.bcnt = o;  o = sal16(o + 4LL * kSTab);
+    L.misc = o;  o = sal16(o + sizeof(SMisc));
+    L.cnt = o;   o = sal16(o + 2LL * kSThreads * (nslots + 2));   // + rows: excluded, other
+    L.buf = o;   o = sal16(o + (8LL * nslots * cap > (int64_t)sizeof(Policy) ? 8LL * nslots * cap : (int64_t)sizeof(Policy)));
+    L.ovfk = o;  o = sal16(o + 8LL * kOvfCap);
+    L.ovfq = o;  o = sal16(o + kOvfCap);
+    L.lut = o;   o = sal16(o + lut_size + 1);                      // lut[lut_size] = gap
+    L.total = o;
+    return L;
+}
+
+int64_t stream_smem_bytes(bool has_cost, int lut_size, int nslots, int cap, int stages) {
+    return stream_layout(has_cost, lut_size, nslots, cap, stages).total;
+}
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// phase timestamps (EWSJF_PHASES diagnostics): slot s of this CTA's row
+__device__ __forceinline__ void dbg_max(const PartialArgs& A, int s, unsigned long long v) {
+    if (A.dbg) atomicMax(&A.dbg[blockIdx.x * 16 + s], v);
+}
+
+// cp.async (LDGSTS) of 16 bytes global -> shared, L2 only; groups per thread.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// wait until at most n of this thread's groups are pending (n = ring depth - 1)
+__device__ __forceinline__ void cp_async_wait(int n) {
+    switch (n) {
+        case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+        case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+        case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+        case 6: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
+    }
+}
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Warp sort of one u64 per lane, descending (lane 0 = largest); bitonic network.
+__device__ __forceinline__ u64 warp_sort_desc(u64 v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const u64 o = shfl_xor_u64(v, j);
+            const bool first = (lane & j) == 0;          // lower lane of the pair
+            const bool desc = (lane & k) == 0;           // block direction (last stage: all descending)
+            v = (first == desc) ? (o > v ? o : v) : (o < v ? o : v);
+        }
+    }
+    return v;
+}
+
+// Warp selection over a set of unique nonzero keys given by for_each(f)
+// (f(key) for every key, lane-strided).  Returns t with K <= #(>= t) <= tgt
+// (tgt == K: t is the exact K-th largest key).  Requires #keys >= K.
+// Each round draws one min-hash sample per lane among the keys strictly
+// inside the current bracket (lo, hi) (an unbiased sample whatever the key
+// order), sorts the 32 samples and takes the one whose rank estimates the
+// target count; the bracket shrinks strictly every round.
+template <typename ForEach>
+__device__ __forceinline__ u64 warp_select(ForEach for_each, int K, int tgt) {
+    const int lane = threadIdx.x & 31;
+    u64 lo = 0ull, hi = ~0ull;   // invariant: #(>= lo) >= K, #(>= hi) < K
+    int c_hi = 0;                // #(>= hi)
+    for (unsigned it = 0;; it++) {
+        int m = 0;
+        u64 s = 0ull;
+        u32 best = 0u;
+        const u32 salt = 0x9E3779B9u * (it + 1u);
+        for_each([&](u64 v) {
+            if (v > lo && v < hi) {
+                m++;
+                const u32 h = ((u32)v ^ salt) * 0x85EBCA77u ^ (u32)(v >> 32) * 0xC2B2AE3Du;
+                if (h >= best) { best = h; s = v; }
+            }
+        });
+        m = __reduce_add_sync(0xffffffffu, m);
+        if (m == 0) break;               // lo is a key with #(>= lo) == K (or the only bound left)
+        const int ns = __popc(__ballot_sync(0xffffffffu, s != 0ull));
+        s = warp_sort_desc(s);
+        // sample rank r (0 = largest) estimates #(>= s_r) ~ c_hi + (r + 1) m / ns
+        const int want = (K + tgt) / 2 - c_hi;
+        int r = (int)ceilf((float)want * (float)ns / (float)m) - 1;
+        r = r < 0 ? 0 : (r >= ns ? ns - 1 : r);
+        const u64 piv = ((u64)__shfl_sync(0xffffffffu, (u32)(s >> 32), r) << 32) |
+                        (u64)__shfl_sync(0xffffffffu, (u32)s, r);
+        int c = 0;
+        for_each([&](u64 v) { c += v >= piv; });
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (c >= K) {
+            lo = piv;
+            if (c <= tgt) break;
+        } else {
+            hi = piv;
+            c_hi = c;
+        }
+    }
+    return lo;
+}
+
+// warp_select over a contiguous array a[0..n): samples are drawn by random
+// index (4 probes per lane, the first inside the bracket wins); when fewer than
+// 8 lanes find one, the round falls back to the min-hash scan.  One count scan
+// per round.  Same contract as warp_select.
+__device__ __forceinline__ u64 warp_select_arr(const u64* a, int n, int K, int tgt) {
+    const int lane = threadIdx.x & 31;
+    u64 lo = 0ull, hi = ~0ull;
+    int c_hi = 0, m = n;         // m ~ #keys strictly inside (lo, hi)
+    for (unsigned it = 0;; it++) {
+        u64 s = 0ull;
+        u32 h = (lane * 0x9E3779B9u) ^ (it * 0x85EBCA77u) ^ 0x27D4EB2Fu;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            h = h * 1664525u + 1013904223u;
+            const u64 v = a[(int)(((unsigned long long)(h >> 8) * (unsigned)n) >> 24)];
+            if (s == 0ull && v > lo && v < hi) s = v;
+        }
+        int ns = __popc(__ballot_sync(0xffffffffu, s != 0ull));
+        if (ns < 8) {                  // sparse bracket: min-hash sample over a scan
+            int mm = 0;
+            u32 best = 0u;
+            s = 0ull;
+            const u32 salt = 0x9E3779B9u * (it + 1u);
+            for (int j = lane; j < n; j += 32) {
+                const u64 v = a[j];
+                if (v > lo && v < hi) {
+                    mm++;
+                    const u32 hh = ((u32)v ^ salt) * 0x85EBCA77u ^ (u32)(v >> 32) * 0xC2B2AE3Du;
+                    if (hh >= best) { best = hh; s = v; }
+                }
+            }
+            m = __reduce_add_sync(0xffffffffu, mm);
+            if (m == 0) break;
+            ns = __popc(__ballot_sync(0xffffffffu, s != 0ull));
+        }
+        s = warp_sort_desc(s);
+        const int want = (K + tgt) / 2 - c_hi;
+        int r = (int)ceilf((float)want * (float)ns / (float)max(m, 1)) - 1;
+        r = r < 0 ? 0 : (r >= ns ? ns - 1 : r);
+        const u64 piv = ((u64)__shfl_sync(0xffffffffu, (u32)(s >> 32), r) << 32) |
+                        (u64)__shfl_sync(0xffffffffu, (u32)s, r);
+        int c = 0;
+        for (int j = lane; j < n; j += 32) c += a[j] >= piv;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (c >= K) {
+            m = c - c_hi - 1;          // keys strictly inside (piv, hi)... approx. for the next estimate
+            lo = piv;
+            if (c <= tgt) break;
+        } else {
+            m = m - (c - c_hi);
+            hi = piv;
+            c_hi = c;
+        }
+        if (m < 1) m = 1;
+    }
+    return lo;
+}
+
+// K-th largest of the nonzero keys held in registers (R per lane, 0 = empty;
+// requires #nonzero >= K >= 1).  MSB-first search for the largest t with
+// #(>= t) >= K, one warp reduction per bit, starting below the keys' common
+// prefix.  It stops early, returning t itself, once bits below `stop_bit`
+// are reached with #(>= t) <= limit: a valid bound (K real keys >= t) within
+// 2^(stop_bit-32) relative of the K-th key's high word, not necessarily a key.
+// When #(>= t) hits K exactly the exact K-th key min{key >= t} is returned.
+// stop_bit = 0 (or limit = K) gives the exact K-th key.
+constexpr int kRegSel = 8;
+constexpr int kApproxBit = 40;   // keep 24 bits of the key's high word (s' / ord(arrival))
+template <int R>
+__device__ __forceinline__ u64 warp_kth_regs(const u64 (&v)[R], int K, int stop_bit = 0, int limit = 0) {
+    u64 mx = 0ull, mn = ~0ull;
+    int n = 0;
+#pragma unroll
+    for (int r = 0; r < R; r++)
+        if (v[r]) { mx = v[r] > mx ? v[r] : mx; mn = v[r] < mn ? v[r] : mn; n++; }
+    mx = warp_max_u64(mx);
+    mn = warp_min_u64(mn);
+    n = __reduce_add_sync(0xffffffffu, n);
+    const u64 diff = mx ^ mn;
+    if (!diff) return mx;
+    int bit = 63 - __clzll((long long)diff);
+    u64 t = mn & ~((bit == 63) ? ~0ull : ((2ull << bit) - 1ull));   // common prefix, low bits clear
+    if (t == 0ull) t = 1ull;                                        // keys are nonzero
+    int ct = n;                                                     // #(>= t)
+    bool exact = false;
+    for (; bit >= 0; bit--) {
+        if (bit < stop_bit && ct <= limit) break;
+        const u64 tt = t | (1ull << bit);
+        int c = 0;
+#pragma unroll
+        for (int r = 0; r < R; r++) c += v[r] >= tt;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (c >= K) {
+            t = tt;
+            ct = c;
+            if (c == K) { exact = true; break; }
+        }
+    }
+    if (!exact && bit >= 0) return t;   // early stop: valid bound, ct in [K, limit]
+    u64 m = ~0ull;
+#pragma unroll
+    for (int r = 0; r < R; r++)
+        if (v[r] && v[r] >= t) m = v[r] < m ? v[r] : m;
+    return warp_min_u64(m);
+}
+// K-th largest of a[0..n), n <= 32*kRegSel (a shared-memory array); see warp_kth_regs.
+__device__ __forceinline__ u64 warp_kth_arr(const u64* a, int n, int K, int stop_bit = 0, int limit = 0) {
+    const int lane = threadIdx.x & 31;
+    u64 v[kRegSel];
+#pragma unroll
+    for (int r = 0; r < kRegSel; r++) {
+        const int j = lane + 32 * r;
+        v[r] = j < n ? a[j] : 0ull;
+    }
+    return warp_kth_regs<kRegSel>(v, K, stop_bit, limit);
+}
+
+template <int MODE, bool HAS_COST>
+__device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy& P, unsigned char* smem) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nslots = P.nslots;
+    const int cap = A.cap, K = A.K, hwm = A.hwm;
+    const int lutsz = A.lut_size;
+    const int S = A.stages;
+    const StreamSmem L = stream_layout(HAS_COST, lutsz, nslots, cap, S);
+    constexpr int narr = HAS_COST ? 3 : 2;
+    unsigned char* lut = smem + L.lut;
+    uint16_t* s_cnt16 = (uint16_t*)(smem + L.cnt);
+    int* s_sid = (int*)(smem + L.sid);
+    float4* s_w4 = (float4*)(smem + L.w4);
+    u64* s_thr64 = (u64*)(smem + L.thr64);
+    u32* s_thrhi = (u32*)(smem + L.thrhi);
+    u64* s_sec = (u64*)(smem + L.sec);
+    u32* s_sechi = (u32*)(smem + L.sechi);
+    float* s_thrf = (float*)(smem + L.thrf);   // fast filter: SCORE s' >= thrf, FIFO arrival <= thrf
+    float* s_secf = (float*)(smem + L.secf);   // fast secondary: SCORE arrival <= secf, FIFO s' >= secf
+    int* s_bcnt = (int*)(smem + L.bcnt);
+    u64* s_buf = (u64*)(smem + L.buf);
+    u64* s_ovfk = (u64*)(smem + L.ovfk);
+    unsigned char* s_ovfq = smem + L.ovfq;
+    SMisc* M = (SMisc*)(smem + L.misc);
+    uint64_t* bars = (uint64_t*)(smem + L.bars) + warp * S;
+    unsigned char* ring = smem + L.ring + (int64_t)warp * S * narr * kWT * 4;
+    const uint32_t gbase = A.gbase;
+    const bool identity = A.ids_identity != 0;
+    const bool write_qid = A.qid_out != nullptr;
+    const int G = gridDim.x;
+    const int bm = A.board_m;            // board keys per (queue, CTA); 0 = off
+
+    // ---- warp tiles: tile t covers requests [t*kWT, (t+1)*kWT); warp gw of the
+    // grid takes tiles gw, gw + GW, ...: all warps sweep the pool front to back
+    // together (the oldest requests first, so thresholds settle early).
+    const int64_t nfull = A.n / kWT;
+    const int64_t GW = (int64_t)G * kSWarps;
+    const int64_t gw = (int64_t)blockIdx.x * kSWarps + warp;
+    auto stage = [&](int st, int a) -> unsigned char* { return ring + (st * narr + a) * kWT * 4; };
+    // per-lane ring (A.tma == 0): every lane copies and later reads back its own
+    // 16 bytes per array with cp.async; one commit group per tile (empty past the end)
+    const bool lane_ring = A.tma == 0;
+    auto issue_lane = [&](int64_t t, int st) {
+        if (t < nfull) {
+            const int64_t off = t * kWT + 4 * lane;
+            cp_async16(stage(st, 0) + 16 * lane, A.len + off);
+            cp_async16(stage(st, 1) + 16 * lane, A.arrival + off);
+            if (HAS_COST) cp_async16(stage(st, 2) + 16 * lane, A.cost + off);
+        }
+        cp_async_commit();
+    };
+    auto issue = [&](int64_t t, int st) {   // lane 0
+        mbar_arrive_expect_tx(&bars[st], (uint32_t)(narr * kWT * 4));
+        const int64_t off = t * kWT;
+        tma_load_1d(stage(st, 0), A.len + off, kWT * 4, &bars[st]);
+        tma_load_1d(stage(st, 1), A.arrival + off, kWT * 4, &bars[st]);
+        if (HAS_COST) tma_load_1d(stage(st, 2), A.cost + off, kWT * 4, &bars[st]);
+    };
+    if (tid == 0 && A.dbg) { for (int s = 0; s < 16; s++) A.dbg[blockIdx.x * 16 + s] = 0ull; dbg_max(A, 0, gtime()); }
+    if (lane_ring) {
+        for (int s = 0; s < S; s++) issue_lane(gw + s * GW, s);
+    } else if (lane == 0) {
+        for (int s = 0; s < S; s++) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        for (int s = 0; s < S; s++) {
+            const int64_t t = gw + s * GW;
+            if (t < nfull) issue(t, s);
+        }
+    }
+
+    // ---- policy tables -> smem while the first tiles are in flight.  The
+    // Policy kernel parameter is first copied with one coalesced 16-byte load
+    // per thread into the (still empty) candidate-buffer area, so no thread
+    // makes divergent constant-bank loads.
+    const Policy* Ps = (const Policy*)s_buf;
+    {
+        const int n16 = (int)((sizeof(Policy) + 15) / 16);
+        const int4* src = reinterpret_cast<const int4*>(&P);
+        for (int i = tid; i < n16; i += kSThreads) ((int4*)s_buf)[i] = src[i];
+        uint32_t* c32 = (uint32_t*)s_cnt16;
+        for (int i = tid; i < kSThreads * (nslots + 2) / 2; i += kSThreads) c32[i] = 0u;
+    }
+    if (tid == 0) { M->flag = 0; M->novf = 0; M->ndone = 0; }
+    __syncthreads();
+    for (int i = tid; i < kSTab; i += kSThreads) {
+        const bool v = i < nslots;
+        s_w4[i] = v ? make_float4(Ps->wb[i], Ps->wu[i], Ps->wf[i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        s_thr64[i] = 0ull; s_thrhi[i] = 0u; s_sec[i] = 0ull; s_sechi[i] = 0u; s_bcnt[i] = 0;
+        // codes >= nslots never pass; qid table: gap -> -2, bad/none -> -1
+        const float inf = __int_as_float(0x7f800000);
+        s_thrf[i] = MODE == EWSJF_SELECT_SCORE ? (v ? 0.f : inf) : (v ? inf : -inf);
+        s_secf[i] = MODE == EWSJF_SELECT_SCORE ? (v ? inf : -inf) : (v ? 0.f : inf);
+        s_sid[i] = v ? Ps->sid[i] : (i == kSCodeGap ? -2 : -1);
+    }
+    {
+        // byte LUT length -> queue position, built a word (4 lengths) at a time:
+        // each thread walks a contiguous run of words through the sorted,
+        // disjoint [min_len, max_len) intervals.
+        const int nw = (lutsz + 1 + 3) / 4;   // lut[0..lutsz], lut[lutsz] = gap
+        const int wpt = (nw + kSThreads - 1) / kSThreads;
+        const int w0 = tid * wpt, w1 = min(nw, w0 + wpt);
+        if (w0 < w1) {
+            int qi = 0, hi = nslots;                 // first queue with max_len > 4*w0
+            while (qi < hi) {
+                const int mid = (qi + hi) >> 1;
+                if (Ps->max_len[mid] <= 4 * w0) qi = mid + 1; else hi = mid;
+            }
+            int qmin = qi < nslots ? Ps->min_len[qi] : INT_MAX, qmax = qi < nslots ? Ps->max_len[qi] : INT_MAX;
+            uint32_t* lw = (uint32_t*)lut;
+            for (int w = w0; w < w1; w++) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const int Lk = 4 * w + k;
+                    while (Lk >= qmax) {
+                        qi++;
+                        qmin = qi < nslots ? Ps->min_len[qi] : INT_MAX;
+                        qmax = qi < nslots ? Ps->max_len[qi] : INT_MAX;
+                    }
+                    const uint32_t code = Lk == 0 ? (uint32_t)kSCodeBad
+                                                  : (Lk >= qmin && Lk < lutsz ? (uint32_t)qi : (uint32_t)kSCodeGap);
+                    word |= code << (8 * k);
+                }
+                lw[w] = word;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) dbg_max(A, 1, gtime());
+
+    unsigned exc = 0, nins = 0, ngap = 0, ncomp = 0, ndrop = 0, excl_total = 0;
+    long long cyc_wait = 0, cyc_proc = 0, cyc_loop0 = 0, cyc_ref = 0, cyc_board = 0, cyc_flag = 0, cyc_tile = 0;   // EWSJF_PHASES cycle accounting
+    long long processed = 0;
+
+    // key high word -> the fast-test float (SCORE: s'; FIFO: the arrival a with ~ord(a) == hi)
+    auto hi_to_f = [](u32 hi) -> float {
+        if (MODE == EWSJF_SELECT_SCORE) return __uint_as_float(hi);
+        const u32 u = ~hi;
+        return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+    };
+    auto raise_thr = [&](int q, u64 t) {   // one lane
+        if (t > *(volatile u64*)&s_thr64[q]) {
+            atomicMax(&s_thr64[q], t);
+            const u32 old = atomicMax(&s_thrhi[q], (u32)(t >> 32));
+            const u32 hi = old > (u32)(t >> 32) ? old : (u32)(t >> 32);
+            *(volatile float*)&s_thrf[q] = hi_to_f(hi);
+        }
+    };
+
+    // ---- collective: cut every queue holding more than K candidates to its
+    // exact K-th key (buffer + overflow), publish thresholds and board rows.
+    auto collective = [&]() {
+        const unsigned long long tc0 = A.dbg ? gtime() : 0ull;
+        named_sync(1, kSThreads);            // every warp finished its tile: no insert in flight
+        const int no_all = min(*(volatile int*)&M->novf, kOvfCap);
+        for (int q = warp; q < nslots; q += kSWarps) {
+            u64* bb = s_buf + (size_t)q * cap;
+            int nb = min(s_bcnt[q], cap);
+            int no = 0;
+            for (int j = lane; j < no_all; j += 32) no += s_ovfq[j] == q;
+            no = __reduce_add_sync(0xffffffffu, no);
+            u64 t = 0ull;
+            auto keep_buf = [&](u64 th) {    // keep buffer keys >= th (stable, in place)
+                int outc = 0;
+                for (int j0 = 0; j0 < nb; j0 += 32) {
+                    const int j = j0 + lane;
+                    const u64 v = j < nb ? bb[j] : 0ull;
+                    const bool keep = j < nb && v >= th;
+                    const unsigned m = __ballot_sync(0xffffffffu, keep);
+                    __syncwarp();
+                    if (keep) bb[outc + __popc(m & ((1u << lane) - 1u))] = v;
+                    outc += __popc(m);
+                    __syncwarp();
+                }
+                nb = outc;
+            };
+            if (nb + no > cap) {             // window over buffer + overflow: <= cap-64 survive
+                t = warp_select(
+                    [&](auto f) {
+                        for (int j = lane; j < nb; j += 32) f(bb[j]);
+                        for (int j = lane; j < no_all; j += 32)
+                            if (s_ovfq[j] == q) f(s_ovfk[j]);
+                    },
+                    K, cap - 64);
+                keep_buf(t);
+            }
+            if (no) {                        // append overflow keys >= t
+                for (int j0 = 0; j0 < no_all; j0 += 32) {
+                    const int j = j0 + lane;
+                    const bool keep = j < no_all && s_ovfq[j] == q && s_ovfk[j] >= t;
+                    const unsigned m = __ballot_sync(0xffffffffu, keep);
+                    if (keep) bb[nb + __popc(m & ((1u << lane) - 1u))] = s_ovfk[j];
+                    nb += __popc(m);
+                }
+                __syncwarp();
+            }
+            if (nb > K) {                    // exact K-th of the (<= cap) candidates
+                t = warp_kth_arr(bb, nb, K, kApproxBit, cap - 64);
+                keep_buf(t);
+                ncomp++;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                s_bcnt[q] = nb;
+                if (t) { raise_thr(q, t); atomicMax(&A.gthr[q], t); }
+            }
+            if (bm) {                        // board row: this CTA's top-bm keys of q
+                u64 prev = ~0ull;
+                for (int i = 0; i < bm; i++) {
+                    u64 mx = 0;
+                    for (int j = lane; j < nb; j += 32) {
+                        const u64 v = bb[j];
+                        if (v < prev && v > mx) mx = v;
+                    }
+                    mx = warp_max_u64(mx);
+                    if (lane == 0) A.board[((size_t)q * G + blockIdx.x) * bm + i] = mx;
+                    prev = mx;
+                }
+            }
+        }
+        named_sync(1, kSThreads);
+        if (tid == 0) { M->novf = 0; M->flag = 0; }
+        named_sync(1, kSThreads);
+        if (A.dbg && tid == 0) {
+            atomicAdd(&A.dbg[blockIdx.x * 16 + 5], 1ull);
+            atomicAdd(&A.dbg[blockIdx.x * 16 + 6], gtime() - tc0);
+        }
+    };
+
+    // ---- board -> global threshold of queue q (one warp): the K-th largest of
+    // the published keys (distinct real requests of distinct CTAs) bounds the
+    // global K-th from below.
+    auto board_refresh = [&](int q) {
+        const int nbk = G * bm;
+        const u64* row = A.board + (size_t)q * G * bm;
+        u64 v[kBoardRegs];
+        int nz = 0;
+#pragma unroll
+        for (int r = 0; r < kBoardRegs; r++) {
+            const int j = lane + 32 * r;
+            v[r] = j < nbk ? __ldcg(row + j) : 0ull;
+            nz += v[r] != 0ull;
+        }
+        nz = __reduce_add_sync(0xffffffffu, nz);
+        if (nz < K) return;
+        const u64 t = warp_kth_regs<kBoardRegs>(v, K, kApproxBit, 1 << 30);
+        if (lane == 0 && t) { raise_thr(q, t); atomicMax(&A.gthr[q], t); }
+    };
+
+    // ---- the 4 consecutive requests [idx0, idx0 + nv) of this lane
+    // r1k != nullptr (round 1): no filter; the lane's scored keys go to r1k/r1q
+    auto process4 = [&](int64_t idx0, int nv, const int (&b)[4], const float (&ar)[4], const float (&co)[4],
+                        u64* r1k, int* r1q) {
+        int code[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int c = lut[min(max(b[j], 0), lutsz)];   // lut[0]: bad; lut[lutsz]: gap
+            code[j] = j < nv ? c : 0x1FF;
+        }
+        processed += nv;
+        if (write_qid) {
+            int qo[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) qo[j] = s_sid[code[j] & 0xFF];
+            if (nv == 4) {
+                __stcs((int4*)(A.qid_out + idx0), make_int4(qo[0], qo[1], qo[2], qo[3]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (j < nv) A.qid_out[idx0 + j] = qo[j];
+            }
+        }
+        // gap-falling lengths (rare): append to the gap list for Alg. 2 (App. D)
+        {
+            unsigned gm = 0;
+#pragma unroll
+            for (int j = 0; j < 4; j++) gm |= (unsigned)(code[j] == kSCodeGap) << j;
+            if (__any_sync(0xffffffffu, gm != 0)) {
+                ngap += __popc(gm);
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const bool g = (gm >> j) & 1u;
+                    const unsigned m = __ballot_sync(0xffffffffu, g);
+                    if (m) {
+                        unsigned long long base = 0;
+                        const int leader = __ffs(m) - 1;
+                        if (lane == leader) base = atomicAdd(&A.ctr->gap_count, (unsigned long long)__popc(m));
+                        base = __shfl_sync(0xffffffffu, base, leader);
+                        if (g) {
+                            const unsigned long long p = base + __popc(m & ((1u << lane) - 1u));
+                            if (p < (unsigned long long)A.gap_cap) {
+                                GapEntry e;
+                                e.gid = gbase + (uint32_t)(idx0 + j);
+                                e.len = b[j];
+                                e.arrival = ar[j];
+                                e.cost = HAS_COST ? co[j] : __int_as_float(0x7fc00000);
+                                A.gap[p] = e;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        // Eq. 4 score, member counter (branch-free: rows nslots / nslots+1 take
+        // the excluded / other requests), fast float filter tests
+        float sp[4];
+        unsigned okm = 0, pass1 = 0, pass2 = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int c = code[j];
+            const int ci = c & 0xFF;
+            const float4 w = s_w4[ci];
+            const bool ok0 = score_sp(b[j], ar[j], HAS_COST ? co[j] : 0.0f, HAS_COST, A.sp, w.x, w.y, w.z, &sp[j]);
+            const bool valid = c < kSCodeGap;
+            const bool ok = valid && ok0;
+            const int row = ok ? ci : (valid ? nslots : nslots + 1);
+            s_cnt16[row * kSThreads + tid]++;
+            okm |= (unsigned)ok << j;
+            const float f1 = MODE == EWSJF_SELECT_SCORE ? sp[j] : ar[j];
+            const float f2 = MODE == EWSJF_SELECT_SCORE ? ar[j] : sp[j];
+            const bool p1 = MODE == EWSJF_SELECT_SCORE ? f1 >= s_thrf[ci] : f1 <= s_thrf[ci];
+            const bool p2 = MODE == EWSJF_SELECT_SCORE ? f2 <= s_secf[ci] : f2 >= s_secf[ci];
+            pass1 |= (unsigned)(ok && p1) << j;
+            pass2 |= (unsigned)(ok && p2) << j;
+        }
+        if (A.pass0 == 7) { pass1 = 0; pass2 = 0; }   // timing experiment: streaming only
+        if (r1k) {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const u32 fh = ~ord_f32(ar[j]);
+                const u32 sh = __float_as_uint(sp[j]);
+                r1k[j] = ((u64)(MODE == EWSJF_SELECT_SCORE ? sh : fh) << 32) | ~(gbase + (uint32_t)(idx0 + j));
+                r1q[j] = ((okm >> j) & 1u) ? (code[j] & 0xFF) : -1;
+            }
+            pass1 = 0;
+        }
+        // rare: exact 64-bit keys, slot reservations, secondary max (per lane)
+        if (__any_sync(0xffffffffu, (pass1 | pass2) != 0)) {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                if (!(((pass1 | pass2) >> j) & 1u)) continue;
+                const u32 lo = ~(gbase + (uint32_t)(idx0 + j));
+                const int q = code[j] & 0xFF;
+                const u32 fh = ~ord_f32(ar[j]);
+                const u32 sh = __float_as_uint(sp[j]);
+                const u32 k1h = MODE == EWSJF_SELECT_SCORE ? sh : fh;
+                const u32 k2h = MODE == EWSJF_SELECT_SCORE ? fh : sh;
+                const u64 k1 = ((u64)k1h << 32) | lo;
+                if (((pass1 >> j) & 1u) && k1 >= *(volatile u64*)&s_thr64[q]) {
+                    const int pos = atomicAdd(&s_bcnt[q], 1);
+                    if (pos < cap) {
+                        s_buf[(size_t)q * cap + pos] = k1;
+                    } else {
+                        const int o = atomicAdd(&M->novf, 1);
+                        if (o < kOvfCap) { s_ovfk[o] = k1; s_ovfq[o] = (unsigned char)q; }
+                        else ndrop++;
+                    }
+                    if (pos + 1 >= hwm) *(volatile int*)&M->flag = 1;
+                    nins++;
+                }
+                if ((pass2 >> j) & 1u) {
+                    // native 32-bit max on the high word first; only a lane that
+                    // may hold the maximum runs the 64-bit (CAS) max
+                    const u32 old = atomicMax(&s_sechi[q], k2h);
+                    if (k2h >= old) {
+                        atomicMax(&s_sec[q], ((u64)k2h << 32) | lo);
+                        // the fast copy may lag (looser), never pass a tie by mistake: ties go to the exact max
+                        *(volatile float*)&s_secf[q] = MODE == EWSJF_SELECT_SCORE ? ar[j] : sp[j];
+                    }
+                }
+            }
+        }
+    };
+
+    auto flag_set = [&]() -> bool {
+        int f = 0;
+        if (lane == 0) f = *(volatile int*)&M->flag;
+        return __shfl_sync(0xffffffffu, f, 0) != 0;
+    };
+
+    // ---- one warp tile: index t = gw + i*GW; t < nfull: TMA ring stage; t ==
+    // nfull: the ragged tail (direct loads).  Returns false past the end.
+    const bool has_tail = (A.n % kWT) != 0;
+    auto tile = [&](int64_t t, int st, uint32_t par, u64* r1k, int* r1q) -> bool {
+        if (t < nfull) {
+            long long c0 = A.dbg ? clock64() : 0;
+            if (lane_ring) cp_async_wait(S - 1);
+            else mbar_wait(&bars[st], par);
+            long long c1 = A.dbg ? clock64() : 0;
+            cyc_wait += c1 - c0;
+            const int4 bv = ((const int4*)stage(st, 0))[lane];
+            const float4 av = ((const float4*)stage(st, 1))[lane];
+            float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (HAS_COST) cv = ((const float4*)stage(st, 2))[lane];
+            const int b4[4] = {bv.x, bv.y, bv.z, bv.w};
+            const float a4[4] = {av.x, av.y, av.z, av.w};
+            const float c4[4] = {cv.x, cv.y, cv.z, cv.w};
+            process4(t * kWT + 4 * lane, 4, b4, a4, c4, r1k, r1q);
+                if (A.dbg) cyc_proc += clock64() - c1;
+            // every lane has consumed the stage (its values fed the stores above)
+            if (lane_ring) {
+                issue_lane(t + S * GW, st);
+                return true;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const int64_t tn = t + S * GW;
+                if (tn < nfull) {
+                    if (A.gap_cap < 0) fence_proxy_async();   // (experiment switch; never taken)
+                    issue(tn, st);
+                }
+            }
+            return true;
+        }
+        if (t == nfull && has_tail) {
+            const int64_t i0 = nfull * kWT + 4 * lane;
+            const int nv = (int)max((int64_t)0, min((int64_t)4, A.n - i0));
+            int b4[4];
+            float a4[4], c4[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const bool v = j < nv;
+                b4[j] = v ? __ldg(A.len + i0 + j) : 0;
+                a4[j] = v ? __ldg(A.arrival + i0 + j) : 0.f;
+                c4[j] = (HAS_COST && v) ? __ldg(A.cost + i0 + j) : 0.f;
+            }
+            process4(i0, nv, b4, a4, c4, r1k, r1q);
+        }
+        return false;
+    };
+
+    // ---- round 1 (every warp's first tile), one structured CTA pass: the
+    // scored keys are bucketed by queue into contiguous slices of the overflow
+    // area (per-thread offsets = exclusive prefix of the per-thread member
+    // counters), each queue's exact K-th key becomes its threshold, and only
+    // the keys >= it enter the queue's buffer.  So the stream starts filtered.
+    int* s_r1n = (int*)s_sid + kSTab;      // see layout: r1n / r1off follow sid
+    int* s_r1off = s_r1n + kSTab;
+    {
+        u64 r1k[4] = {0ull, 0ull, 0ull, 0ull};
+        int r1q[4] = {-1, -1, -1, -1};
+        tile(gw, 0, 0u, r1k, r1q);
+        if (A.pass0 == 7) for (int j = 0; j < 4; j++) r1q[j] = -1;
+        __syncthreads();
+        // per-queue totals and per-thread exclusive prefixes (lane l: threads 16l..16l+15)
+        for (int q = warp; q < nslots; q += kSWarps) {
+            uint32_t* col = (uint32_t*)(s_cnt16 + (size_t)q * kSThreads) + 8 * lane;
+            uint32_t w[8];
+            int sum = 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) { w[k] = col[k]; sum += (int)(w[k] & 0xffffu) + (int)(w[k] >> 16); }
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            int run = incl - sum;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const uint32_t a0 = (uint32_t)run; run += (int)(w[k] & 0xffffu);
+                const uint32_t a1 = (uint32_t)run; run += (int)(w[k] >> 16);
+                col[k] = a0 | (a1 << 16);
+            }
+            if (lane == 31) s_r1n[q] = incl;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int carry = 0;
+            for (int q0 = 0; q0 < nslots; q0 += 32) {
+                const int q = q0 + lane;
+                const int v = q < nslots ? s_r1n[q] : 0;
+                int incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += u;
+                }
+                if (q < nslots) s_r1off[q] = carry + incl - v;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int q = r1q[j];
+            if (q >= 0) {
+                int k = 0;
+#pragma unroll
+                for (int jj = 0; jj < j; jj++) k += r1q[jj] == q;
+                s_ovfk[s_r1off[q] + s_cnt16[(size_t)q * kSThreads + tid] + k] = r1k[j];
+            }
+        }
+        __syncthreads();
+        for (int q = warp; q < nslots; q += kSWarps) {
+            const int n = s_r1n[q];
+            const u64* sl = s_ovfk + s_r1off[q];
+            u64 t = 0ull;
+            if (n > 32 * kRegSel) t = warp_select_arr(sl, n, K, cap - 64);   // window: <= cap-64 survive
+            else if (n > K) t = warp_kth_arr(sl, n, K, kApproxBit, cap - 64);
+            u64* bb = s_buf + (size_t)q * cap;
+            int nb = 0;
+            for (int j0 = 0; j0 < n; j0 += 32) {
+                const int j = j0 + lane;
+                const u64 v = j < n ? sl[j] : 0ull;
+                const bool keep = j < n && v >= t;
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                if (keep) bb[nb + __popc(m & ((1u << lane) - 1u))] = v;
+                nb += __popc(m);
+            }
+            __syncwarp();
+            if (nb > K) {                    // window survivors -> exact K-th
+                t = warp_kth_arr(bb, nb, K, kApproxBit, cap - 64);
+                int outc = 0;
+                for (int j0 = 0; j0 < nb; j0 += 32) {
+                    const int j = j0 + lane;
+                    const u64 v = j < nb ? bb[j] : 0ull;
+                    const bool keep = j < nb && v >= t;
+                    const unsigned m = __ballot_sync(0xffffffffu, keep);
+                    __syncwarp();
+                    if (keep) bb[outc + __popc(m & ((1u << lane) - 1u))] = v;
+                    outc += __popc(m);
+                    __syncwarp();
+                }
+                nb = outc;
+            }
+            uint32_t* col = (uint32_t*)(s_cnt16 + (size_t)q * kSThreads) + 8 * lane;
+#pragma unroll
+            for (int k = 0; k < 8; k++) col[k] = 0u;
+            if (lane == 0) {
+                s_bcnt[q] = nb;
+                if (t) { raise_thr(q, t); atomicMax(&A.gthr[q], t); }
+            }
+            if (bm) {                        // board row: this CTA's top-bm keys of q
+                u64 prev = ~0ull;
+                for (int i = 0; i < bm; i++) {
+                    u64 mx = 0;
+                    for (int j = lane; j < nb; j += 32) {
+                        const u64 v = bb[j];
+                        if (v < prev && v > mx) mx = v;
+                    }
+                    mx = warp_max_u64(mx);
+                    if (lane == 0) A.board[((size_t)q * G + blockIdx.x) * bm + i] = mx;
+                    prev = mx;
+                }
+            }
+        }
+        __syncthreads();
+        if (A.dbg && lane == 0 && warp == 0) dbg_max(A, 7, gtime());
+    }
+
+    // ---- main loop: private TMA ring, CTA barriers only in collectives
+    cyc_loop0 = A.dbg ? clock64() : 0;
+    cyc_wait = 0; cyc_proc = 0;
+    u64 g_pre = 0ull;
+    int rq = warp % max(nslots, 1);
+    int st = 1 % S;
+    uint32_t par = S == 1 ? 1u : 0u;
+    int64_t t = gw + GW;
+    for (int i = 1;; ++i) {
+        // cross-CTA threshold refresh every 4th tile, loaded one tile ahead
+        if ((i & 7) == 1 && lane == 0 && nslots > 0) g_pre = __ldcg(&A.gthr[rq]);
+        long long c6 = A.dbg ? clock64() : 0;
+        if (!tile(t, st, par, nullptr, nullptr)) break;
+        if (A.dbg) cyc_tile += clock64() - c6;
+        t += GW;
+        if (++st == S) { st = 0; par ^= 1u; }
+        long long c3 = A.dbg ? clock64() : 0;
+        if ((i & 7) == 6 && lane == 0 && nslots > 0) {
+            if (g_pre) raise_thr(rq, g_pre);
+            rq += kSWarps;
+            if (rq >= nslots) rq -= nslots * (rq / nslots);
+        }
+        __syncwarp();
+        long long c4 = A.dbg ? clock64() : 0;
+        cyc_ref += c4 - c3;
+        if (bm && i == 3)
+            for (int q = warp; q < nslots; q += kSWarps) board_refresh(q);
+        long long c5 = A.dbg ? clock64() : 0;
+        cyc_board += c5 - c4;
+        if (flag_set()) collective();
+        if (A.dbg) cyc_flag += clock64() - c5;
+    }
+    if (lane == 0) dbg_max(A, 2, A.dbg ? gtime() : 0ull);
+    if (lane == 0 && A.dbg) {   // per-CTA sums over warps (cycles): TMA waits, tile processing, loop total
+        atomicAdd(&A.dbg[blockIdx.x * 16 + 10], (unsigned long long)cyc_wait);
+        atomicAdd(&A.dbg[blockIdx.x * 16 + 11], (unsigned long long)cyc_proc);
+        atomicAdd(&A.dbg[blockIdx.x * 16 + 12], (unsigned long long)(clock64() - cyc_loop0));
+        atomicAdd(&A.dbg[blockIdx.x * 16 + 13], (unsigned long long)cyc_tile);
+        atomicAdd(&A.dbg[blockIdx.x * 16 + 14], (unsigned long long)cyc_ref);
+        atomicAdd(&A.dbg[blockIdx.x * 16 + 15], (unsigned long long)(cyc_board * 65536 + cyc_flag / 16));
+    }
+    // done streaming: keep serving collectives until every warp is done.  A
+    // flag raised by this warp is visible before its ndone increment, and
+    // ndone is read before the flag, so no warp leaves while one is pending.
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) atomicAdd(&M->ndone, 1);
+    for (;;) {
+        int f = 0, d = 0;
+        if (lane == 0) {
+            d = *(volatile int*)&M->ndone;
+            __threadfence_block();
+            f = *(volatile int*)&M->flag;
+        }
+        f = __shfl_sync(0xffffffffu, f, 0);
+        d = __shfl_sync(0xffffffffu, d, 0);
+        if (f) { collective(); continue; }
+        if (d == kSWarps) break;
+        __nanosleep(64);
+    }
+    __syncthreads();
+    if (tid == 0) dbg_max(A, 3, A.dbg ? gtime() : 0ull);
+
+    // ---- final trim: every queue keeps exactly its local top-K (no overflow is
+    // pending: an overflow always raised the flag first)
+    for (int q = warp; q < nslots; q += kSWarps) {
+        u64* bb = s_buf + (size_t)q * cap;
+        const int nb = min(s_bcnt[q], cap);
+        if (nb > K) {
+            const u64 t = warp_kth_arr(bb, nb, K);
+            int outc = 0;
+            for (int j0 = 0; j0 < nb; j0 += 32) {
+                const int j = j0 + lane;
+                const u64 v = j < nb ? bb[j] : 0ull;
+                const bool keep = j < nb && v >= t;
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                __syncwarp();
+                if (keep) bb[outc + __popc(m & ((1u << lane) - 1u))] = v;
+                outc += __popc(m);
+                __syncwarp();
+            }
+            ncomp++;
+            if (lane == 0) { s_bcnt[q] = outc; raise_thr(q, t); atomicMax(&A.gthr[q], t); }
+        }
+    }
+    __syncthreads();
+
+    // ---- rows out: keys >= max(local, global) threshold, secondary, members
+    const Rows& R = A.rows;
+    long long counted = 0;
+    for (int q = warp; q < nslots; q += kSWarps) {
+        const int nb = min(s_bcnt[q], cap);
+        u64 tf = s_thr64[q];
+        const u64 gg = __ldcg(&A.gthr[q]);
+        tf = gg > tf ? gg : tf;
+        u64* dst = R.keys + ((size_t)q * G + blockIdx.x) * R.cap;
+        int outc = 0;
+        for (int j0 = 0; j0 < nb; j0 += 32) {
+            const int j = j0 + lane;
+            const u64 v = j < nb ? s_buf[(size_t)q * cap + j] : 0ull;
+            const bool keep = j < nb && v >= tf;
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) dst[outc + __popc(m & ((1u << lane) - 1u))] = v;
+            outc += __popc(m);
+        }
+        long long mm = 0;
+        const uint32_t* c32 = (const uint32_t*)(s_cnt16 + (size_t)q * kSThreads);
+        for (int k = lane; k < kSThreads / 2; k += 32) { const uint32_t v = c32[k]; mm += (v & 0xffffu) + (v >> 16); }
+        for (int o = 16; o; o >>= 1) mm += __shfl_xor_sync(0xffffffffu, mm, o);
+        mm += s_r1n[q];
+        if (lane == 0) {
+            R.cnt[(size_t)q * G + blockIdx.x] = outc;
+            R.sec[(size_t)q * G + blockIdx.x] = s_sec[q];
+            R.members[(size_t)q * G + blockIdx.x] = mm;
+        }
+        counted += mm;   // lane-uniform
+    }
+    if (lane == 0) dbg_max(A, 4, A.dbg ? gtime() : 0ull);
+    // excluded = the dummy row nslots; invalid = processed - counted - excluded - gap
+    {
+        const uint32_t* c32 = (const uint32_t*)(s_cnt16 + (size_t)nslots * kSThreads);
+        unsigned e = 0;
+        if (warp == 0)
+            for (int k = lane; k < kSThreads / 2; k += 32) { const uint32_t v = c32[k]; e += (v & 0xffffu) + (v >> 16); }
+        exc = warp == 0 ? e : 0u;   // reduced below with the other per-lane counters
+        if (warp == 0) {
+            unsigned ee = e;
+            for (int o = 16; o; o >>= 1) ee += __shfl_xor_sync(0xffffffffu, ee, o);
+            excl_total = ee;
+        }
+    }
+    long long invl = processed - (long long)ngap;
+    for (int o = 16; o; o >>= 1) {
+        invl += __shfl_xor_sync(0xffffffffu, invl, o);
+        exc += __shfl_xor_sync(0xffffffffu, exc, o);
+        nins += __shfl_xor_sync(0xffffffffu, nins, o);
+        ndrop += __shfl_xor_sync(0xffffffffu, ndrop, o);
+    }
+    if (lane == 0) {
+        invl -= counted;
+        if (warp == 0) invl -= (long long)excl_total;
+        if (invl) atomicAdd(&A.ctr->n_invalid, (unsigned long long)invl);
+        if (exc) atomicAdd(&A.ctr->n_excluded, (unsigned long long)exc);
+        if (nins) atomicAdd(&A.ctr->dbg_inserted, (unsigned long long)nins);
+        if (ncomp) atomicAdd(&A.ctr->dbg_compactions, (unsigned long long)ncomp);
+        if (ndrop) atomicAdd(&A.ctr->dbg_overflow, (unsigned long long)ndrop);
+    }
+}
+
+// Clear this CTA's board rows (nobody reads them any more).
+__device__ __forceinline__ void board_clear(const PartialArgs& A, int nslots) {
+    if (!A.board_m) return;
+    for (int i = threadIdx.x; i < nslots * A.board_m; i += blockDim.x) {
+        const int s = i / A.board_m, j = i % A.board_m;
+        A.board[((size_t)s * gridDim.x + blockIdx.x) * A.board_m + j] = 0ull;
+    }
+}
+
+// Streaming pass alone (the merge is a separate launch).
+template <int MODE, bool HAS_COST>
+__global__ void __launch_bounds__(kSThreads, 1)
+    stream_kernel(const __grid_constant__ PartialArgs A, const __grid_constant__ Policy P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    stream_phase<MODE, HAS_COST>(A, P, smem);
+    board_clear(A, P.nslots);
+}
+
+__device__ __forceinline__ void sgrid_barrier(unsigned int* ctr, unsigned int target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        unsigned int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v < target) __nanosleep(32);
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+// Fused tick: streaming pass -> grid barrier -> per-queue merge.
+template <int MODE, bool HAS_COST>
+__global__ void __launch_bounds__(kSThreads, 1)
+    stream_tick_kernel(const __grid_constant__ PartialArgs A, const __grid_constant__ Policy P,
+                       const __grid_constant__ MergeArgs MA) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    stream_phase<MODE, HAS_COST>(A, P, smem);
+    sgrid_barrier(&A.ctr->barrier, gridDim.x);
+    if (threadIdx.x == 0) dbg_max(A, 8, A.dbg ? gtime() : 0ull);
+    board_clear(A, P.nslots);
+    merge_phase<MERGE_IN_ROWS, MERGE_OUT_FINAL, HAS_COST>(MA, P, smem);
+    if (threadIdx.x == 0) dbg_max(A, 9, A.dbg ? gtime() : 0ull);
+}
+
+int64_t merge_smem_total(int in_mode);
+
+template <int MO, bool C>
+static cudaError_t launch_s(const PartialArgs& A, const Policy& P, const MergeArgs* MA, int grid, cudaStream_t st) {
+    const int64_t ls = stream_layout(C, A.lut_size, P.nslots, A.cap, A.stages).total;
+    if (!MA) {
+        auto k = stream_kernel<MO, C>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ls);
+        if (e != cudaSuccess) return e;
+        k<<<grid, kSThreads, ls, st>>>(A, P);
+        return cudaGetLastError();
+    }
+    const int64_t lm = merge_smem_total(MERGE_IN_ROWS);
+    const int64_t smem = ls > lm ? ls : lm;
+    auto k = stream_tick_kernel<MO, C>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    void* args[] = {(void*)&A, (void*)&P, (void*)MA};
+    return cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kSThreads), args, (size_t)smem, st);
+}
+
+// Route + score + select over an aligned pool with a LUT-routable partition of
+// <= 64 queues; MA == nullptr: streaming pass only.
+cudaError_t launch_stream(const PartialArgs& A, const Policy& P, const MergeArgs* MA, bool has_cost, int grid,
+                          cudaStream_t st) {
+    if (A.sp.mode == EWSJF_SELECT_FIFO)
+        return has_cost ? launch_s<EWSJF_SELECT_FIFO, true>(A, P, MA, grid, st)
+                        : launch_s<EWSJF_SELECT_FIFO, false>(A, P, MA, grid, st);
+    return has_cost ? launch_s<EWSJF_SELECT_SCORE, true>(A, P, MA, grid, st)
+                    : launch_s<EWSJF_SELECT_SCORE, false>(A, P, MA, grid, st);
+}
+
+}  // namespace ewsjf

@@ -51,9 +51,11 @@ struct PartialArgs {
     int32_t pass0;              // counts, qid, gaps, counters
     int32_t select;             // 0 = route only
     int32_t lut_size;           // LUT covers lengths [0, lut_size); 0 = binary search
+    int32_t stages;             // stream.cu: TMA ring depth per warp
     ScoreParams sp;
     Rows rows;
     u64* gthr;                  // [nslots] cross-CTA filter thresholds
+    unsigned long long* dbg;    // nullable: per-CTA phase timestamps [G][16] (EWSJF_PHASES)
     GapEntry* gap;
     int32_t gap_cap;
     Counters* ctr;

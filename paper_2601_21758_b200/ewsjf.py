@@ -64,6 +64,14 @@ class Context:
         self.check(self.lib.ewsjf_ctx_get_timing(self.h, C.byref(t)))
         return t.as_dict()
 
+    def phases(self):
+        """Per-CTA phase timestamps of the last streaming tick (EWSJF_PHASES), shape [ctas, 16]."""
+        import numpy as np
+        n = self.num_ctas * 16
+        buf = (C.c_uint64 * n)()
+        self.check(self.lib.ewsjf_ctx_get_phases(self.h, buf, n))
+        return np.frombuffer(buf, dtype=np.uint64).reshape(self.num_ctas, 16).copy()
+
     def check(self, s: int, allow=(L.OK, L.DOMAIN)) -> int:
         if s not in allow:
             msg = self.lib.ewsjf_last_error(self.h).decode()
