@@ -282,9 +282,15 @@ ewsjf_status ewsjf_tick_merge(ewsjf_ctx *ctx, const void *d_exchange_all, int32_
                               const ewsjf_select_params *params, ewsjf_select_out *out);
 
 /* ----------------------------------------------- Θ sweep (A12, config C5) --- */
-/* For each of n_theta meta-parameter vectors (§4.4.2): A7 -> A10 ->
- * A11 over one routed snapshot.  outs[t] receives the selection for thetas[t]
- * (device buffers as in ewsjf_select_out; h_summary ignored).  Async.        */
+/* For each of n_theta meta-parameter vectors (§4.4.2):
+ * A7 -> A10 -> A11 over one routed snapshot (d_qid: stable ids of *part).
+ * outs[t] receives the selection for thetas[t] (device buffers as in
+ * ewsjf_select_out; h_summary ignored; each outs[t].d_summary, when non-NULL,
+ * gets that Θ's summary).  Every outs[t] equals what ewsjf_score_select returns
+ * with ewsjf_weights_from_meta(&thetas[t], part).  SCORE mode only (the sweep
+ * ranks scoring policies; FIFO keys do not depend on Θ): params->mode must be
+ * EWSJF_SELECT_SCORE.  Async; returns DOMAIN if any Θ excluded elements,
+ * INVALID_ARG on bad arguments (nothing launched).                          */
 ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx *ctx, const int32_t *d_len, const float *d_arrival,
                                       const float *d_cost, const int32_t *d_qid, int64_t n,
                                       const ewsjf_partition_t *part, const ewsjf_meta *thetas,

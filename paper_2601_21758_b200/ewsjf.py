@@ -157,6 +157,12 @@ class Outputs:
     def nq(self) -> int:
         return self.summary["n_queues"]
 
+    def fetch_summary(self) -> dict:
+        """Copy the device summary of an asynchronous call (e.g. one Θ of a sweep) to the host."""
+        b = bytes(self.summary_dev.cpu().numpy().tobytes())
+        self.summary = L.Summary.from_buffer_copy(b).as_dict()
+        return self.summary
+
 
 def _dev_check(t: torch.Tensor | None, dtype, name):
     if t is None:

@@ -1,0 +1,99 @@
+"""GPU parity of the Θ sweep (A12, config C5; §4.4.2) against the
+CPU oracle's O11, and self-consistency with independent score_select calls.
+
+Snapshot = bimodal pool routed by the Refine-and-Prune partition of a bimodal
+history (C2's partition), Θ uniform in S:500's bounds.
+"""
+import numpy as np
+import pytest
+import torch
+
+import workload
+from tests.parity import compare_selection, gpu_result, to_gpu_partition
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def E():
+    import paper_2601_21758_b200 as E
+    return E
+
+
+@pytest.fixture(scope="module")
+def ctx(E):
+    return E.Context(0, max_pool=1 << 21, max_history=0, max_k=64)
+
+
+@pytest.fixture(scope="module")
+def c2_partition(orc):
+    s, part, _ = orc.partition(workload.bimodal(1_000_000, 201))
+    assert s == orc.OK
+    return part
+
+
+def _snapshot(orc, opart, n, seed):
+    pool = workload.pool("bimodal", n, seed)
+    s, qid, *_ = orc.route(pool["len"], orc.copy_partition(opart), 64)
+    assert s == orc.OK      # the snapshot is routed by the same partition: no bubbles
+    return pool, qid
+
+
+def _run_sweep(E, ctx, pool, qid, opart, thetas, K, mode):
+    dev = [torch.from_numpy(pool[k]).cuda() for k in ("len", "arrival", "cost")] + [torch.from_numpy(qid).cuda()]
+    outs = E.score_select_sweep(ctx, *dev, to_gpu_partition(E, opart), [E.meta(**t) for t in thetas],
+                                E.select_params(k=K, mode=mode))
+    torch.cuda.synchronize()
+    res = []
+    for o in outs:
+        o.fetch_summary()
+        res.append(gpu_result(o))
+    return res, dev
+
+
+def _check_against_oracle(orc, pool, qid, opart, thetas, res, K, mode):
+    sp = orc.select_params(k=K, mode=mode)
+    st, ref = orc.sweep(pool["len"], pool["arrival"], pool["cost"], qid, opart, thetas, sp)
+    assert len(ref) == len(res)
+    for t, (g, r) in enumerate(zip(res, ref)):
+        phi, _ = orc.score_all(pool["len"], pool["arrival"], pool["cost"], qid, opart, orc.meta(**thetas[t]), sp)
+        compare_selection(g, r, phi, pool["arrival"], mode, K)
+
+
+@pytest.mark.parametrize("K", [1, 16, 64])
+def test_sweep_matches_oracle(E, orc, ctx, c2_partition, K):
+    pool, qid = _snapshot(orc, c2_partition, 200_003, 501)
+    thetas = workload.random_thetas(12, 502)
+    res, _ = _run_sweep(E, ctx, pool, qid, c2_partition, thetas, K, 0)
+    _check_against_oracle(orc, pool, qid, c2_partition, thetas, res, K, 0)
+
+
+def test_sweep_rejects_fifo_mode(E, orc, ctx, c2_partition):
+    pool, qid = _snapshot(orc, c2_partition, 1000, 505)
+    with pytest.raises(E.EwsjfError):
+        _run_sweep(E, ctx, pool, qid, c2_partition, workload.random_thetas(2, 1), 4, 1)
+
+
+def test_sweep_equals_independent_score_select(E, orc, ctx, c2_partition):
+    """A12 = n_Θ independent A11 runs (SURVEY §8c pin): identical outputs, bit for bit."""
+    pool, qid = _snapshot(orc, c2_partition, 150_000, 503)
+    thetas = workload.random_thetas(5, 504)
+    res, dev = _run_sweep(E, ctx, pool, qid, c2_partition, thetas, 16, 0)
+    for t, th in enumerate(thetas):
+        gp = to_gpu_partition(E, c2_partition)
+        w = E.weights_from_meta(E.meta(**th), gp)
+        one = gpu_result(E.score_select(ctx, *dev, gp, w, E.select_params(k=16)))
+        nq = one["n_queues"]
+        assert res[t]["n_queues"] == nq and res[t]["primary"] == one["primary"]
+        for k in ("topk_id", "topk_score", "count", "head_id", "head_score", "max_score"):   # rows >= nq unused
+            np.testing.assert_array_equal(res[t][k][:nq], one[k][:nq], err_msg=f"theta {t} {k}")
+
+
+def test_sweep_full_size_c5(E, orc, ctx, c2_partition):
+    """BASELINE C5 at full snapshot size (1M bimodal requests routed by the C2
+    partition), K=16, in bench.py's launch configuration; 24 of the 256 Θ are
+    checked against the oracle (the oracle's full sort per Θ is the slow part)."""
+    pool, qid = _snapshot(orc, c2_partition, 1_000_000, 501)
+    thetas = workload.random_thetas(256, 502)[::11]
+    res, _ = _run_sweep(E, ctx, pool, qid, c2_partition, thetas, 16, 0)
+    _check_against_oracle(orc, pool, qid, c2_partition, thetas, res, 16, 0)
