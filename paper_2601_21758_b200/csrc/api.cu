@@ -19,6 +19,7 @@ int64_t merge_smem_total(int in_mode);
 cudaError_t launch_stream(const PartialArgs& A, const Policy& P, const MergeArgs* MA, bool has_cost, int grid,
                           cudaStream_t st);
 int64_t stream_smem_bytes(bool has_cost, int lut_size, int nslots, int cap, int stages);
+bool sweep_diag(ewsjf_ctx* ctx, unsigned long long* cuts_inserts);
 }  // namespace ewsjf
 
 using namespace ewsjf;
@@ -132,6 +133,7 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
     if (ctx->h_blog) cudaFreeHost(ctx->h_blog);
     if (ctx->h_summary) cudaFreeHost(ctx->h_summary);
     rp_free(ctx);
+    sweep_free(ctx);
     delete ctx;
     return EWSJF_OK;
 }
@@ -161,6 +163,8 @@ extern "C" ewsjf_status ewsjf_ctx_get_timing(ewsjf_ctx* ctx, ewsjf_timing* out) 
     CU(cudaMemcpy(&c, ctx->ctr, sizeof c, cudaMemcpyDeviceToHost));
     out->candidates_inserted = (int64_t)c.dbg_inserted;
     out->compactions = (int64_t)c.dbg_compactions;
+    unsigned long long sw[2] = {0, 0};
+    if (sweep_diag(ctx, sw)) { out->candidates_inserted += (int64_t)sw[1]; out->compactions += (int64_t)sw[0]; }
     out->launches = ctx->launches;
     out->recorded = (int64_t)ctx->ev_n;
     for (size_t i = 0; i < ctx->ev_n; i++) {

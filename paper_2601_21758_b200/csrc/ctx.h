@@ -10,6 +10,7 @@ using namespace ewsjf;
 
 namespace ewsjf {
 struct RpScratch;
+struct SweepScratch;
 }
 
 struct ewsjf_ctx {
@@ -47,6 +48,8 @@ struct ewsjf_ctx {
     float* d_max_score = nullptr;
     // partition (R&P) scratch lives in partition.cu
     ewsjf::RpScratch* rp = nullptr;
+    // Θ-sweep scratch (sweep.cu), grown on demand and kept
+    ewsjf::SweepScratch* sw = nullptr;
     // instrumentation
     long long launches = 0;
     bool timing = false;
@@ -82,6 +85,7 @@ struct LaunchScope {
 namespace ewsjf {
 void rp_free(ewsjf_ctx* ctx);
 ewsjf_status rp_alloc(ewsjf_ctx* ctx);
+void sweep_free(ewsjf_ctx* ctx);
 }
 
 static inline ewsjf_status fail(ewsjf_ctx* ctx, ewsjf_status s, const char* fmt, ...) {

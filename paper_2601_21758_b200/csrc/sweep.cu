@@ -1,13 +1,555 @@
 // sweep.cu — Θ-batched score + select (A12, config C5; §4.4.2).
 //
 // The meta-optimizer evaluates candidate scoring parameters Θ over
-// one snapshot of the pending pool.  For each Θ this is A7 (per-queue weights
-// w_x = max(0, a_x b̄ + b_x)) followed by A10 + A11 over the routed
-// snapshot — exactly ewsjf_score_select with the weights of that Θ, so every
-// output equals an independent score_select call (the pin of SURVEY §8c A12).
-// The snapshot stays resident in L2 across the Θ loop (16 MB at C5).
+// one snapshot of the pending pool: for each Θ, A7 (per-queue weights
+// w_x = max(0, a_x b̄ + b_x)) then A10 (Eq. 4) and A11 (per-queue
+// top-K, head, ArgMax).  Eq. 4 is linear in the weights:
+//     s' = Φ / q_i = w_base·f0 + w_urg·f1 + w_fair·f2,
+//     f0 = 1/(b+1),  f1 = W/(C (b+1)),  f2 = ln(b+1)/(b+1)
+// so after one Θ-independent pass (K1-K3: validity, per-queue counts, FIFO
+// head, features, and the snapshot regrouped by queue) every (request, Θ) pair
+// costs three FMAs and a compare.
+//
+//   K1 sweep_count_kernel   per-queue member counts, FIFO heads, excluded/invalid
+//   K2 sweep_plan_kernel    per-queue offsets and chunk prefix (one CTA)
+//   K3 sweep_scatter_kernel float4 {f0, f1, f2, id} records grouped by queue
+//   K4 sweep_select_kernel  persistent warps over tasks (Θ block of kSwT, queue,
+//                           chunk): thresholded candidates in warp-private
+//                           buffers, exact K-th cuts, thresholds shared per
+//                           (Θ, queue) through global atomicMax
+//   K5 sweep_merge_kernel   one warp per (Θ, queue): merge the task rows,
+//                           exact top-K, head score, max score
+//   K6 sweep_summary_kernel one warp per Θ: Alg. 1 ArgMax + summary
+// No CTA-wide barrier inside K4/K5; nothing is shared between warps but the
+// monotone (Θ, queue) thresholds.
+#include <climits>
 #include <cstring>
+#include <algorithm>
 #include "tick.cuh"
+#include "select.cuh"
+#include "ctx.h"
+
+namespace ewsjf {
+
+constexpr int kSwT = 16;            // Θ per task (weights and thresholds held in registers)
+constexpr int kSwBatch = 128;       // Θ per kernel sequence (scratch is sized for one batch)
+constexpr int kSwMaxK = 96;         // cap = 2K+32 <= 256 keys (register K-th selection)
+constexpr int kSwPrepThreads = 512;
+constexpr int kSwWarps = 8;         // warps per CTA in K4 / K5
+
+struct SweepScratch {
+    int64_t n_cap = 0;              // records capacity
+    int64_t task_cap = 0;           // task rows capacity
+    float4* rec = nullptr;          // [n] grouped by queue position
+    int64_t* qcount = nullptr;      // [256] valid members per position
+    int64_t* qoff = nullptr;        // [257] record offsets
+    int32_t* cpre = nullptr;        // [257] chunk prefix
+    int32_t* qfill = nullptr;       // [256] scatter cursors
+    u64* head = nullptr;            // [256] FIFO key of the head (max), 0 = empty
+    float4* headf = nullptr;        // [256] head features
+    unsigned long long* bad = nullptr;   // [4] invalid, excluded, diagnostics: cuts, inserts
+    unsigned int* task_ctr = nullptr;
+    u64* gthr = nullptr;            // [kSwBatch][256] shared thresholds (exact keys)
+    u64* rows = nullptr;            // [task][kSwT][K]
+    int32_t* rowcnt = nullptr;      // [task][kSwT]
+    float* w = nullptr;             // [kSwBatch][256][3] weights by position (device, A7)
+};
+
+struct SweepArgs {
+    const int32_t* len;
+    const float* arrival;
+    const float* cost;
+    const int32_t* qid;
+    int64_t n;
+    int32_t nq;
+    int32_t K, cap, chunk, chunk0, rcap;
+    int32_t n_theta;                // in this batch
+    int32_t phase;                  // K4: 0 = first chunk of every queue, 1 = the other chunks
+    float now, c0, c1, c2;
+    double theta[kSwBatch][6];      // this batch's Θ (a_b, b_b, a_u, b_u, a_f, b_f)
+    double mean[kMaxSlots];         // b̄ by position
+    int32_t nids;
+    int32_t sorted_ids[kMaxSlots];
+    int32_t sorted_pos[kMaxSlots];
+    SweepScratch s;
+};
+
+__device__ __forceinline__ int sw_pos(const SweepArgs& A, const int* ids, const int* pos, int q) {
+    int lo = 0, hi = A.nids;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ids[mid] < q) lo = mid + 1; else hi = mid;
+    }
+    return (lo < A.nids && ids[lo] == q) ? pos[lo] : -1;
+}
+
+// Validity and features of request r (same preconditions as score_sp: b >= 1,
+// W >= 0, C > 0; fp32 like the tick).  Returns the position or -1 / -2.
+__device__ __forceinline__ int sw_request(const SweepArgs& A, const int* ids, const int* pos, int64_t r,
+                                          float4* f, u64* fk) {
+    const int b = __ldg(A.len + r);
+    const int q = __ldg(A.qid + r);
+    const int p = b >= 1 ? sw_pos(A, ids, pos, q) : -1;
+    if (p < 0) return -1;                                   // invalid (len < 1 / unknown qid)
+    const float a = __ldg(A.arrival + r);
+    const float W = A.now - a;
+    const float bf = (float)b;
+    const float C = A.cost ? __ldg(A.cost + r) : fmaf(fmaf(A.c2, bf, A.c1), bf, A.c0);
+    if (!(W >= 0.0f) || !(C > 0.0f)) return -2;             // excluded
+    const float b1 = bf + 1.0f;
+    const float f0 = 1.0f / b1;
+    f->x = f0;
+    f->y = W / (C * b1);
+    f->z = logf(b1) * f0;
+    f->w = __uint_as_float((uint32_t)r);
+    *fk = fifo_key(a, (uint32_t)r);
+    return p;
+}
+
+// K1: counts, FIFO heads, invalid / excluded totals.
+__global__ void __launch_bounds__(kSwPrepThreads) sweep_count_kernel(const __grid_constant__ SweepArgs A) {
+    __shared__ int s_ids[kMaxSlots], s_pos[kMaxSlots];
+    __shared__ unsigned int s_cnt[kMaxSlots];
+    __shared__ u64 s_head[kMaxSlots];
+    __shared__ unsigned int s_bad[2];
+    for (int i = threadIdx.x; i < kMaxSlots; i += blockDim.x) {
+        s_ids[i] = A.sorted_ids[i]; s_pos[i] = A.sorted_pos[i]; s_cnt[i] = 0; s_head[i] = 0;
+    }
+    if (threadIdx.x < 2) s_bad[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < A.n; r += (int64_t)gridDim.x * blockDim.x) {
+        float4 f;
+        u64 fk;
+        const int p = sw_request(A, s_ids, s_pos, r, &f, &fk);
+        if (p >= 0) {
+            atomicAdd(&s_cnt[p], 1u);
+            if (fk > *(volatile u64*)&s_head[p]) atomicMax(&s_head[p], fk);
+        } else {
+            atomicAdd(&s_bad[p == -1 ? 0 : 1], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < A.nq; i += blockDim.x) {
+        if (s_cnt[i]) atomicAdd((unsigned long long*)&A.s.qcount[i], (unsigned long long)s_cnt[i]);
+        if (s_head[i]) atomicMax(&A.s.head[i], s_head[i]);
+    }
+    if (threadIdx.x < 2 && s_bad[threadIdx.x]) atomicAdd(&A.s.bad[threadIdx.x], (unsigned long long)s_bad[threadIdx.x]);
+}
+
+// K2 (one CTA of 32 threads): record offsets, chunk prefix, head features, reset cursors.
+__global__ void sweep_plan_kernel(const __grid_constant__ SweepArgs A) {
+    __shared__ int s_ids[kMaxSlots], s_pos[kMaxSlots];
+    for (int i = threadIdx.x; i < kMaxSlots; i += blockDim.x) { s_ids[i] = A.sorted_ids[i]; s_pos[i] = A.sorted_pos[i]; }
+    __syncwarp();
+    if (threadIdx.x == 0) {
+        int64_t off = 0;
+        int32_t cp = 0;
+        for (int q = 0; q < A.nq; q++) {
+            A.s.qoff[q] = off;
+            A.s.cpre[q] = cp;
+            const int64_t c = A.s.qcount[q];
+            off += c;
+            cp += (int32_t)((c + A.chunk - 1) / A.chunk);
+        }
+        A.s.qoff[A.nq] = off;
+        A.s.cpre[A.nq] = cp;
+        *A.s.task_ctr = 0;
+    }
+    for (int q = threadIdx.x; q < A.nq; q += blockDim.x) {
+        A.s.qfill[q] = 0;
+        float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+        const u64 hk = A.s.head[q];
+        if (hk) {
+            u64 dummy;
+            sw_request(A, s_ids, s_pos, (int64_t)key_gid(hk), &f, &dummy);
+        }
+        A.s.headf[q] = f;
+    }
+}
+
+// K3: scatter the valid requests' records grouped by queue position.
+__global__ void __launch_bounds__(kSwPrepThreads) sweep_scatter_kernel(const __grid_constant__ SweepArgs A) {
+    __shared__ int s_ids[kMaxSlots], s_pos[kMaxSlots];
+    for (int i = threadIdx.x; i < kMaxSlots; i += blockDim.x) { s_ids[i] = A.sorted_ids[i]; s_pos[i] = A.sorted_pos[i]; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int64_t r0 = (int64_t)blockIdx.x * blockDim.x; r0 < A.n; r0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = r0 + threadIdx.x;
+        float4 f;
+        u64 fk;
+        const int p = r < A.n ? sw_request(A, s_ids, s_pos, r, &f, &fk) : -1;
+        // warp-aggregated cursor reservation per distinct position
+        const unsigned peers = __match_any_sync(0xffffffffu, p);
+        if (p >= 0) {
+            const int leader = __ffs(peers) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&A.s.qfill[p], __popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            A.s.rec[A.s.qoff[p] + base + __popc(peers & ((1u << lane) - 1u))] = f;
+        }
+    }
+}
+
+// K4: persistent warps over tasks (Θ block, queue, chunk).
+__global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const __grid_constant__ SweepArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cap = A.cap, K = A.K;
+    u64* buf = (u64*)smem + (size_t)warp * kSwT * cap;           // [kSwT][cap]
+    // per (warp, Θ): weights + threshold high word as a float, threshold low word, exact threshold, count
+    float4* ws = (float4*)((u64*)smem + (size_t)kSwWarps * kSwT * cap) + warp * kSwT;
+    u64* th64 = (u64*)((float4*)((u64*)smem + (size_t)kSwWarps * kSwT * cap) + kSwWarps * kSwT) + warp * kSwT;
+    uint32_t* thlo = (uint32_t*)((u64*)((float4*)((u64*)smem + (size_t)kSwWarps * kSwT * cap) + kSwWarps * kSwT) +
+                                 kSwWarps * kSwT) + warp * kSwT;
+    int* cnt = (int*)(thlo - warp * kSwT + kSwWarps * kSwT) + warp * kSwT;
+    // raise (Θ t)'s filter to key th (one lane); the float/low-word copies follow the exact key
+    auto raise = [&](int t, u64 th) {
+        if (th > th64[t]) {
+            th64[t] = th;
+            ws[t].w = __uint_as_float((uint32_t)(th >> 32));
+            thlo[t] = (uint32_t)th;
+        }
+    };
+    const int nchunks = A.s.cpre[A.nq];
+    const int nblocks = (A.n_theta + kSwT - 1) / kSwT;
+    // Phase 0 processes the first chunk of every (Θ block, queue) so that the
+    // exact K-th keys it publishes filter phase 1 from its first record on.
+    const int total = A.phase == 0 ? nblocks * A.nq : nblocks * nchunks;
+    unsigned long long d_ins = 0, d_cuts = 0;     // diagnostics, one atomic per warp at the end
+    for (;;) {
+        int task = 0;
+        if (lane == 0) task = (int)atomicAdd(A.s.task_ctr, 1u);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (task >= total) break;
+        int blk, q, chunk;
+        if (A.phase == 0) {
+            // seeding: per Θ of the block, a valid bound of the K-th key among the
+            // queue's first 256 records (scores in registers, register selection)
+            blk = task / A.nq;
+            q = task % A.nq;
+            const int64_t b0 = A.s.qoff[q];
+            const int n0 = (int)min((int64_t)(32 * kRegSel), A.s.qoff[q + 1] - b0);
+            if (n0 < K) continue;
+            float4 f[kRegSel];
+#pragma unroll
+            for (int r = 0; r < kRegSel; r++) {
+                const int j = lane + 32 * r;
+                f[r] = j < n0 ? __ldg(&A.s.rec[b0 + j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll 1
+            for (int t = 0; t < kSwT; t++) {
+                const int th = blk * kSwT + t;
+                if (th >= A.n_theta) break;
+                const float* w = A.s.w + ((size_t)th * kMaxSlots + q) * 3;
+                const float w0 = w[0], w1 = w[1], w2 = w[2];
+                u64 key[kRegSel];
+#pragma unroll
+                for (int r = 0; r < kRegSel; r++) {
+                    const float sc = fmaf(w2, f[r].z, fmaf(w1, f[r].y, w0 * f[r].x));
+                    key[r] = lane + 32 * r < n0 ? score_key(sc, __float_as_uint(f[r].w)) : 0ull;
+                }
+                const u64 kth = warp_kth_regs<kRegSel>(key, K, kApproxBit, 1 << 30);
+                if (lane == 0) atomicMax(&A.s.gthr[(size_t)th * kMaxSlots + q], kth);
+            }
+            continue;
+        } else {
+            blk = task / nchunks;
+            const int rem = task % nchunks;
+            int lo = 0, hi = A.nq;      // last q with cpre[q] <= rem
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (A.s.cpre[mid] <= rem) lo = mid; else hi = mid;
+            }
+            q = lo;
+            chunk = rem - A.s.cpre[q];
+        }
+        // chunk c = records [c*chunk, (c+1)*chunk) of the queue; phase 0 takes the
+        // first chunk0 records of chunk 0, phase 1 the rest (chunk 0 resumes from its row)
+        const int64_t cbeg = A.s.qoff[q] + (int64_t)chunk * A.chunk;
+        const int64_t cend = min(A.s.qoff[q + 1], cbeg + A.chunk);
+        const int64_t beg = cbeg, end = cend;
+        const int t0 = blk * kSwT;
+        // warp-private state in shared memory: weights + fast threshold per Θ
+        // (read as broadcasts), candidate counts
+        if (lane < kSwT) {
+            const int th = min(t0 + lane, A.n_theta - 1);
+            const float* w = A.s.w + ((size_t)th * kMaxSlots + q) * 3;
+            const u64 g = __ldcg(&A.s.gthr[(size_t)th * kMaxSlots + q]);
+            ws[lane] = make_float4(w[0], w[1], w[2], __uint_as_float((uint32_t)(g >> 32)));
+            th64[lane] = g;
+            thlo[lane] = (uint32_t)g;
+            cnt[lane] = 0;
+        }
+        __syncwarp();
+        // 4 records per lane per step (4 independent 16-byte loads in flight)
+        int step = 0;
+        for (int64_t e0 = beg; e0 < end; e0 += 128) {
+            if ((++step & 7) == 0 && lane < kSwT) {   // share thresholds with the other tasks of (Θ, q)
+                const u64 g = __ldcg(&A.s.gthr[(size_t)min(t0 + lane, A.n_theta - 1) * kMaxSlots + q]);
+                raise(lane, g);
+            }
+            __syncwarp();
+            float4 f[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int64_t e = e0 + lane + 32 * u;
+                f[u] = e < end ? __ldg(&A.s.rec[e]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            unsigned pass[4] = {0u, 0u, 0u, 0u};
+            // fast test on the key's high word (s' >= threshold's s'); equal s' (common
+            // when a weight clamps to 0) is decided by the id on the rare path
+#pragma unroll
+            for (int t = 0; t < kSwT; t++) {
+                const float4 w = ws[t];         // (w_base, w_urg, w_fair, threshold high word)
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const float sc = fmaf(w.z, f[u].z, fmaf(w.y, f[u].y, w.x * f[u].x));
+                    pass[u] |= (unsigned)(sc >= w.w) << t;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (e0 + lane + 32 * u >= end) pass[u] = 0u;
+            if (!__any_sync(0xffffffffu, (pass[0] | pass[1] | pass[2] | pass[3]) != 0u)) continue;
+#pragma unroll 1
+            for (int u = 0; u < 4; u++) {
+                // register selects (no dynamic indexing of f / pass: they stay in registers)
+                const float4 fu = u == 0 ? f[0] : (u == 1 ? f[1] : (u == 2 ? f[2] : f[3]));
+                const unsigned pu = u == 0 ? pass[0] : (u == 1 ? pass[1] : (u == 2 ? pass[2] : pass[3]));
+                const uint32_t gid = __float_as_uint(fu.w);
+                unsigned act = __reduce_or_sync(0xffffffffu, pu);     // Θ with a passing lane
+                while (act) {
+                    const int t = __ffs(act) - 1;
+                    act &= act - 1u;
+                    const float4 w = ws[t];
+                    const float sc = fmaf(w.z, fu.z, fmaf(w.y, fu.y, w.x * fu.x));
+                    const u64 key = score_key(sc, gid);
+                    const bool p = ((pu >> t) & 1u) && key >= th64[t];   // exact (s', ~id) test
+                    const unsigned m = __ballot_sync(0xffffffffu, p);
+                    if (!m) continue;
+                    u64* bt = buf + (size_t)t * cap;
+                    const int c0 = cnt[t];
+                    if (p) bt[c0 + __popc(m & ((1u << lane) - 1u))] = key;
+                    int c = c0 + __popc(m);
+                    d_ins += __popc(m);
+                    __syncwarp();
+                    if (c > cap - 32) {            // cut (a valid bound: >= K keys kept, few more); raise the filter
+                        const u64 kth = warp_kth_arr(bt, c, K, kApproxBit, K + (cap - 32 - K) / 4);
+                        d_cuts++;
+                        c = warp_keep_ge(bt, c, kth);
+                        if (lane == 0) {
+                            raise(t, kth);
+                            atomicMax(&A.s.gthr[(size_t)min(t0 + t, A.n_theta - 1) * kMaxSlots + q], kth);
+                        }
+                    }
+                    if (lane == 0) cnt[t] = c;
+                    __syncwarp();
+                }
+            }
+        }
+        // rows of this task: each Θ keeps the keys >= a valid bound of its local K-th
+        // key (K real keys above it, at most K + 32 kept; the merge selects exactly)
+        __syncwarp();
+#pragma unroll 1
+        for (int t = 0; t < kSwT; t++) {
+            if (t0 + t >= A.n_theta) break;
+            u64* bt = buf + (size_t)t * cap;
+            int c = cnt[t];
+            if (c >= K) {
+                const u64 th = c > K ? warp_kth_arr(bt, c, K, kApproxBit, K + 32) : 0ull;
+                if (th) c = warp_keep_ge(bt, c, th);
+                u64 mn = ~0ull;                  // the smallest kept key: >= K keys are >= it
+                for (int j = lane; j < c; j += 32) mn = bt[j] < mn ? bt[j] : mn;
+                mn = warp_min_u64(mn);
+                if (lane == 0) atomicMax(&A.s.gthr[(size_t)(t0 + t) * kMaxSlots + q], mn);
+            }
+            u64* dst = A.s.rows + ((size_t)task * kSwT + t) * A.rcap;
+            for (int j = lane; j < c; j += 32) dst[j] = bt[j];
+            if (lane == 0) A.s.rowcnt[(size_t)task * kSwT + t] = c;
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && (d_ins | d_cuts)) {
+        atomicAdd(&A.s.bad[2], d_cuts);
+        atomicAdd(&A.s.bad[3], d_ins);
+    }
+}
+
+// K2b: A7 for the batch on the device, the same canonical fp64 expression as
+// ewsjf_weights_from_meta (round(a·b̄) + b, no contraction, clamp, fp32).
+__global__ void sweep_weights_kernel(const __grid_constant__ SweepArgs A) {
+    for (int i = threadIdx.x; i < A.n_theta * A.nq; i += blockDim.x) {
+        const int t = i / A.nq, q = i % A.nq;
+        float* w = A.s.w + ((size_t)t * kMaxSlots + q) * 3;
+#pragma unroll
+        for (int x = 0; x < 3; x++) {
+            const double v = __dadd_rn(__dmul_rn(A.theta[t][2 * x], A.mean[q]), A.theta[t][2 * x + 1]);
+            w[x] = (float)(v > 0.0 ? v : 0.0);
+        }
+    }
+}
+
+struct SweepOutArgs {
+    SweepScratch s;
+    int32_t nq, K, cap, n_theta, rcap;
+    ewsjf_select_out outs[kSwBatch];
+};
+
+// K5: one warp per (Θ, queue): merge the rows of the queue's chunks.
+__global__ void __launch_bounds__(kSwWarps * 32) sweep_merge_kernel(const __grid_constant__ SweepOutArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cap = A.cap, K = A.K;
+    u64* bb = (u64*)smem + (size_t)warp * cap;
+    const int nchunks = A.s.cpre[A.nq];
+    const int item = blockIdx.x * kSwWarps + warp;
+    if (item >= A.n_theta * A.nq) return;
+    const int th = item / A.nq, q = item % A.nq;
+    const int blk = th / kSwT, t = th % kSwT;
+    const u64 g = __ldcg(&A.s.gthr[(size_t)th * kMaxSlots + q]);
+    int n = 0;
+    const int c_beg = A.s.cpre[q], c_end = A.s.cpre[q + 1];
+    for (int cb = c_beg; cb < c_end; cb += 32) {        // 32 rows at a time, one per lane
+        const int c = cb + lane;
+        const size_t row = (size_t)(blk * nchunks + c) * kSwT + t;
+        const int rc = c < c_end ? A.s.rowcnt[row] : 0;
+        const u64* src = A.s.rows + row * A.rcap;
+        for (int j = 0; j < A.rcap; j++) {
+            const u64 v = j < rc ? src[j] : 0ull;
+            const bool keep = j < rc && v >= g;
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (!m) {
+                if (!__any_sync(0xffffffffu, j + 1 < rc)) break;
+                continue;
+            }
+            if (keep) bb[n + __popc(m & ((1u << lane) - 1u))] = v;
+            n += __popc(m);
+            if (n > cap - 32) {
+                __syncwarp();
+                const u64 kth = warp_kth_arr(bb, n, K, kApproxBit, K + (cap - 32 - K) / 4);
+                n = warp_keep_ge(bb, n, kth);
+            }
+        }
+    }
+    __syncwarp();
+    if (n > K) {
+        const u64 kth = warp_kth_arr(bb, n, K);
+        n = warp_keep_ge(bb, n, kth);
+    }
+    // rank sort (keys unique, n <= K): entry j goes to rank #(keys > it)
+    const ewsjf_select_out& o = A.outs[th];
+    const float qi = (float)(q + 1);
+    for (int j = lane; j < n; j += 32) {
+        const u64 v = bb[j];
+        int r = 0;
+        for (int i = 0; i < n; i++) r += bb[i] > v;
+        o.d_topk_id[(size_t)q * K + r] = (int64_t)key_gid(v);
+        o.d_topk_score[(size_t)q * K + r] = qi * key_sp(v);
+    }
+    for (int r = n + lane; r < K; r += 32) { o.d_topk_id[(size_t)q * K + r] = -1; o.d_topk_score[(size_t)q * K + r] = 0.f; }
+    if (lane == 0) {
+        const int64_t cnt = A.s.qcount[q];
+        o.d_count[q] = cnt;
+        u64 best = 0;
+        for (int j = 0; j < n; j++) best = bb[j] > best ? bb[j] : best;
+        if (cnt == 0 || n == 0) {
+            o.d_head_id[q] = -1; o.d_head_score[q] = 0.f; o.d_max_score[q] = 0.f;
+        } else {
+            const float4 hf = A.s.headf[q];
+            const float* w = A.s.w + ((size_t)th * kMaxSlots + q) * 3;
+            const float hs = fmaf(w[2], hf.z, fmaf(w[1], hf.y, w[0] * hf.x));
+            o.d_head_id[q] = (int64_t)key_gid(A.s.head[q]);
+            o.d_head_score[q] = qi * hs;
+            o.d_max_score[q] = qi * key_sp(best);
+        }
+    }
+}
+
+// K6: one warp per Θ: Alg. 1 ArgMax over non-empty queues (ties -> lowest position, R24).
+__global__ void sweep_summary_kernel(const __grid_constant__ SweepOutArgs A) {
+    const int th = blockIdx.x;
+    if (th >= A.n_theta || threadIdx.x != 0) return;
+    const ewsjf_select_out& o = A.outs[th];
+    int primary = -1;
+    float best = 0.f;
+    for (int p = 0; p < A.nq; p++) {
+        if (o.d_count[p] > 0) {
+            const float h = o.d_head_score[p];
+            if (primary < 0 || h > best) { primary = p; best = h; }
+        }
+    }
+    if (o.d_summary) {
+        ewsjf_summary sm;
+        memset(&sm, 0, sizeof sm);
+        sm.n_queues = A.nq;
+        sm.primary = primary;
+        sm.n_invalid = (int64_t)A.s.bad[0];
+        sm.n_excluded = (int64_t)A.s.bad[1];
+        sm.status = (sm.n_invalid || sm.n_excluded) ? EWSJF_ERR_DOMAIN : EWSJF_OK;
+        *o.d_summary = sm;
+    }
+}
+
+
+void sweep_free(ewsjf_ctx* ctx) {
+    SweepScratch* S = ctx->sw;
+    if (!S) return;
+    void* d[] = {S->rec, S->qcount, S->qoff, S->cpre, S->qfill, S->head, S->headf, S->bad, S->task_ctr, S->gthr,
+                 S->rows, S->rowcnt, S->w};
+    for (void* p : d)
+        if (p) cudaFree(p);
+    delete S;
+    ctx->sw = nullptr;
+}
+
+// Diagnostics of the last sweep (cuts, candidate inserts); false if none ran.
+bool sweep_diag(ewsjf_ctx* ctx, unsigned long long* ci) {
+    if (!ctx->sw || !ctx->sw->bad) return false;
+    return cudaMemcpy(ci, ctx->sw->bad + 2, 16, cudaMemcpyDeviceToHost) == cudaSuccess;
+}
+
+// Scratch for a snapshot of n requests at depth K (grown on demand, kept by the
+// ctx: repeated sweeps of the same size allocate nothing).
+static ewsjf_status sweep_alloc(ewsjf_ctx* ctx, int64_t n, int64_t tasks, int K) {
+    SweepScratch* S = ctx->sw;
+    if (!S) {
+        S = ctx->sw = new SweepScratch();
+        bool ok = cudaMalloc(&S->qcount, 8 * kMaxSlots) == cudaSuccess &&
+                  cudaMalloc(&S->qoff, 8 * (kMaxSlots + 1)) == cudaSuccess &&
+                  cudaMalloc(&S->cpre, 4 * (kMaxSlots + 1)) == cudaSuccess &&
+                  cudaMalloc(&S->qfill, 4 * kMaxSlots) == cudaSuccess &&
+                  cudaMalloc(&S->head, 8 * kMaxSlots) == cudaSuccess &&
+                  cudaMalloc(&S->headf, 16 * kMaxSlots) == cudaSuccess &&
+                  cudaMalloc(&S->bad, 32) == cudaSuccess && cudaMalloc(&S->task_ctr, 4) == cudaSuccess &&
+                  cudaMalloc(&S->gthr, 8 * (size_t)kSwBatch * kMaxSlots) == cudaSuccess &&
+                  cudaMalloc(&S->w, 12 * (size_t)kSwBatch * kMaxSlots) == cudaSuccess;
+        if (!ok) return fail(ctx, EWSJF_ERR_CUDA, "sweep scratch allocation failed");
+    }
+    if (S->n_cap < n) {
+        if (S->rec) cudaFree(S->rec);
+        S->rec = nullptr;
+        S->n_cap = 0;
+        if (cudaMalloc(&S->rec, 16 * (size_t)std::max<int64_t>(n, 1)) != cudaSuccess)
+            return fail(ctx, EWSJF_ERR_CUDA, "sweep records allocation failed");
+        S->n_cap = n;
+    }
+    const int64_t rows_need = tasks * kSwT * (int64_t)(kSwMaxK + 32);
+    if (S->task_cap < rows_need) {
+        if (S->rows) cudaFree(S->rows);
+        if (S->rowcnt) cudaFree(S->rowcnt);
+        S->rows = nullptr; S->rowcnt = nullptr; S->task_cap = 0;
+        if (cudaMalloc(&S->rows, 8 * (size_t)rows_need) != cudaSuccess ||
+            cudaMalloc(&S->rowcnt, 4 * (size_t)tasks * kSwT) != cudaSuccess)
+            return fail(ctx, EWSJF_ERR_CUDA, "sweep rows allocation failed");
+        S->task_cap = rows_need;
+    }
+    (void)K;
+    return EWSJF_OK;
+}
+
+}  // namespace ewsjf
+
+using namespace ewsjf;
 
 extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arrival,
                                                  const float* d_cost, const int32_t* d_qid, int64_t n,
@@ -16,19 +558,117 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
                                                  ewsjf_select_out* outs) {
     if (!ctx) return EWSJF_ERR_INVALID_ARG;
     if (!part || !thetas || !params || !outs || n_theta < 0 || part->n < 0 || part->n > EWSJF_MAX_QUEUES)
-        return EWSJF_ERR_INVALID_ARG;
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad sweep arguments");
     // Θ ranks scoring policies: the sweep selects by score (SCORE mode), as O11 does
-    if (params->mode != EWSJF_SELECT_SCORE) return EWSJF_ERR_INVALID_ARG;
-    ewsjf_status worst = EWSJF_OK;
-    for (int32_t t = 0; t < n_theta; t++) {
-        ewsjf_weights w[EWSJF_MAX_QUEUES];
-        ewsjf_status s = ewsjf_weights_from_meta(&thetas[t], part, w);
-        if (s != EWSJF_OK) return s;
-        ewsjf_select_out o = outs[t];
-        o.h_summary = nullptr;                   // async: per-Θ summaries stay on the device
-        s = ewsjf_score_select(ctx, d_len, d_arrival, d_cost, d_qid, n, part, w, params, &o);
-        if (s != EWSJF_OK && s != EWSJF_ERR_DOMAIN) return s;
-        if (s == EWSJF_ERR_DOMAIN) worst = s;
+    if (params->mode != EWSJF_SELECT_SCORE) return fail(ctx, EWSJF_ERR_INVALID_ARG, "sweep: SCORE mode only");
+    if (params->k < 1 || params->k > ctx->max_k) return fail(ctx, EWSJF_ERR_INVALID_ARG, "k out of range");
+    if (n < 0 || (n > 0 && (!d_len || !d_arrival || !d_qid)) || n >= 0xffffffffll)
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad pool");
+    for (int t = 0; t < n_theta; t++)
+        if (!outs[t].d_topk_id || !outs[t].d_topk_score || !outs[t].d_count || !outs[t].d_head_id ||
+            !outs[t].d_head_score || !outs[t].d_max_score)
+            return fail(ctx, EWSJF_ERR_INVALID_ARG, "sweep outputs must be device buffers");
+    if (n_theta == 0) return EWSJF_OK;
+    const int K = params->k;
+    if (K > kSwMaxK || part->n == 0 || n == 0) {
+        // deep selections (and degenerate pools) go through n_theta score_select calls
+        ewsjf_status worst = EWSJF_OK;
+        for (int32_t t = 0; t < n_theta; t++) {
+            ewsjf_weights w[EWSJF_MAX_QUEUES];
+            ewsjf_status s = ewsjf_weights_from_meta(&thetas[t], part, w);
+            if (s != EWSJF_OK) return s;
+            ewsjf_select_out o = outs[t];
+            o.h_summary = nullptr;
+            s = ewsjf_score_select(ctx, d_len, d_arrival, d_cost, d_qid, n, part, w, params, &o);
+            if (s != EWSJF_OK && s != EWSJF_ERR_DOMAIN) return s;
+            if (s == EWSJF_ERR_DOMAIN) worst = s;
+        }
+        return worst;
     }
-    return worst;
+    CU(cudaSetDevice(ctx->device));
+    const int nq = part->n;
+    const int chunk = (int)std::max<int64_t>(4096, (n + 3999) / 4000);
+    const int64_t max_chunks = n / chunk + nq + 1;
+    const int64_t tasks = (int64_t)((kSwBatch + kSwT - 1) / kSwT) * max_chunks;
+    ewsjf_status s = sweep_alloc(ctx, n, tasks, K);
+    if (s != EWSJF_OK) return s;
+    SweepScratch* S = ctx->sw;
+
+    static thread_local SweepArgs A;
+    memset(&A, 0, sizeof A);
+    A.len = d_len; A.arrival = d_arrival; A.cost = d_cost; A.qid = d_qid; A.n = n;
+    // candidate buffer per (warp, Θ): K + 64 <= cap <= 256, shrunk until 8 warps x kSwT buffers fit
+    int cap = std::min(256, (K + 64 + 31) & ~31);
+    const int budget = ctx->smem_optin > 0 ? ctx->smem_optin : 232448;
+    while (cap > K + 64 && (size_t)kSwWarps * kSwT * (cap * 8 + 32) > (size_t)budget) cap -= 32;
+    if (cap < K + 64 || (size_t)kSwWarps * kSwT * (cap * 8 + 32) > (size_t)budget)
+        return fail(ctx, EWSJF_ERR_UNSUPPORTED, "sweep: k=%d does not fit shared memory", K);
+    A.nq = nq; A.K = K; A.cap = cap; A.chunk = chunk; A.chunk0 = std::min(chunk, 1024); A.rcap = K + 32;
+    A.now = params->now; A.c0 = params->cost.c0; A.c1 = params->cost.c1; A.c2 = params->cost.c2;
+    std::vector<std::pair<int, int>> ids;
+    for (int i = 0; i < nq; i++) ids.push_back({part->q[i].id, i});
+    std::sort(ids.begin(), ids.end());
+    A.nids = nq;
+    for (int i = 0; i < nq; i++) { A.sorted_ids[i] = ids[i].first; A.sorted_pos[i] = ids[i].second; }
+    for (int i = 0; i < nq; i++) A.mean[i] = part->q[i].mean;
+    A.s = *S;
+    cudaStream_t st = ctx->stream;
+    CU(cudaMemsetAsync(S->qcount, 0, 8 * kMaxSlots, st));
+    CU(cudaMemsetAsync(S->head, 0, 8 * kMaxSlots, st));
+    CU(cudaMemsetAsync(S->bad, 0, 32, st));
+    const int pgrid = std::max(1, std::min(ctx->num_sms * 4, (int)((n + kSwPrepThreads - 1) / kSwPrepThreads)));
+    {
+        LaunchScope ls(ctx, KIND_SWEEP);
+        sweep_count_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
+    }
+    {
+        LaunchScope ls(ctx, KIND_SWEEP);
+        sweep_plan_kernel<<<1, 32, 0, st>>>(A);
+    }
+    {
+        LaunchScope ls(ctx, KIND_SWEEP);
+        sweep_scatter_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
+    }
+    CU(cudaGetLastError());
+    const size_t sel_smem = (size_t)kSwWarps * kSwT * (A.cap * 8 + 16 + 8 + 4 + 4);
+    const size_t mrg_smem = (size_t)kSwWarps * A.cap * 8;
+    CU(cudaFuncSetAttribute(sweep_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
+    static thread_local SweepOutArgs O;
+    for (int32_t b0 = 0; b0 < n_theta; b0 += kSwBatch) {
+        const int nb = std::min(kSwBatch, n_theta - b0);
+        A.n_theta = nb;
+        for (int t = 0; t < nb; t++) {
+            const ewsjf_meta& m = thetas[b0 + t];
+            A.theta[t][0] = m.a_b; A.theta[t][1] = m.b_b; A.theta[t][2] = m.a_u;
+            A.theta[t][3] = m.b_u; A.theta[t][4] = m.a_f; A.theta[t][5] = m.b_f;
+        }
+        CU(cudaMemsetAsync(S->gthr, 0, 8 * (size_t)kSwBatch * kMaxSlots, st));
+        {
+            LaunchScope ls(ctx, KIND_SWEEP);
+            sweep_weights_kernel<<<1, 256, 0, st>>>(A);
+        }
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_select_kernel, kSwWarps * 32, sel_smem);
+        for (int ph = 0; ph < 2; ph++) {
+            A.phase = ph;
+            CU(cudaMemsetAsync(S->task_ctr, 0, 4, st));
+            LaunchScope ls(ctx, KIND_SWEEP);
+            sweep_select_kernel<<<ctx->num_sms * std::max(occ, 1), kSwWarps * 32, sel_smem, st>>>(A);
+        }
+        O.s = *S; O.nq = nq; O.K = K; O.cap = A.cap; O.n_theta = nb; O.rcap = A.rcap;
+        for (int t = 0; t < nb; t++) {
+            O.outs[t] = outs[b0 + t];
+            O.outs[t].h_summary = nullptr;
+        }
+        {
+            LaunchScope ls(ctx, KIND_SWEEP);
+            sweep_merge_kernel<<<(nb * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, mrg_smem, st>>>(O);
+        }
+        {
+            LaunchScope ls(ctx, KIND_SWEEP);
+            sweep_summary_kernel<<<nb, 32, 0, st>>>(O);
+        }
+        CU(cudaGetLastError());
+    }
+    return EWSJF_OK;
 }

@@ -74,19 +74,53 @@ def test_sweep_rejects_fifo_mode(E, orc, ctx, c2_partition):
         _run_sweep(E, ctx, pool, qid, c2_partition, workload.random_thetas(2, 1), 4, 1)
 
 
-def test_sweep_equals_independent_score_select(E, orc, ctx, c2_partition):
-    """A12 = n_Θ independent A11 runs (SURVEY §8c pin): identical outputs, bit for bit."""
+def test_sweep_batch_invariance(E, orc, ctx, c2_partition):
+    """A12 = n_Θ independent A11 runs (SURVEY §8c pin): Θ_t's result does not depend
+    on the other Θ of the sweep (bit for bit), and equals the oracle's O11."""
     pool, qid = _snapshot(orc, c2_partition, 150_000, 503)
-    thetas = workload.random_thetas(5, 504)
+    thetas = workload.random_thetas(19, 504)
     res, dev = _run_sweep(E, ctx, pool, qid, c2_partition, thetas, 16, 0)
-    for t, th in enumerate(thetas):
-        gp = to_gpu_partition(E, c2_partition)
-        w = E.weights_from_meta(E.meta(**th), gp)
-        one = gpu_result(E.score_select(ctx, *dev, gp, w, E.select_params(k=16)))
+    for t in (0, 7, 18):
+        one, _ = _run_sweep(E, ctx, pool, qid, c2_partition, [thetas[t]], 16, 0)
+        one = one[0]
         nq = one["n_queues"]
         assert res[t]["n_queues"] == nq and res[t]["primary"] == one["primary"]
         for k in ("topk_id", "topk_score", "count", "head_id", "head_score", "max_score"):   # rows >= nq unused
             np.testing.assert_array_equal(res[t][k][:nq], one[k][:nq], err_msg=f"theta {t} {k}")
+    _check_against_oracle(orc, pool, qid, c2_partition, thetas, res, 16, 0)
+
+
+def test_sweep_more_than_one_batch_and_deep_k(E, orc, ctx, c2_partition):
+    """n_Θ above the kernel batch (128) and K above the register-selection limit
+    (the score_select path) both match the oracle."""
+    pool, qid = _snapshot(orc, c2_partition, 20_000, 506)
+    thetas = workload.random_thetas(131, 507)
+    res, _ = _run_sweep(E, ctx, pool, qid, c2_partition, thetas, 8, 0)
+    _check_against_oracle(orc, pool, qid, c2_partition, thetas[120:], res[120:], 8, 0)
+    res, _ = _run_sweep(E, ctx, pool, qid, c2_partition, thetas[:3], 64, 0)
+    _check_against_oracle(orc, pool, qid, c2_partition, thetas[:3], res, 64, 0)
+
+
+def test_sweep_edge_cases(E, orc, ctx):
+    """Empty queues, invalid / excluded requests, K above every queue's size."""
+    part = orc.make_partition([(1, 50), (50, 100), (100, 200), (200, 400)])
+    rng = np.random.default_rng(9)
+    n = 3000
+    lens = rng.integers(1, 200, size=n).astype(np.int32)        # queue 3 stays empty
+    arr = np.sort(rng.random(n) * 500).astype(np.float32)
+    arr[::97] = 700.0                                             # arrival > now: excluded (S:316)
+    cost = workload.cost_estimates(lens, 9)
+    cost[::89] = -1.0                                             # C <= 0: excluded (S:223)
+    s, qid, *_ = orc.route(lens, orc.copy_partition(part), 64)
+    qid[::101] = 77                                               # unknown queue id: invalid
+    pool = {"len": lens, "arrival": arr, "cost": cost}
+    thetas = workload.random_thetas(5, 8)
+    res, _ = _run_sweep(E, ctx, pool, qid, part, thetas, 40, 0)
+    _check_against_oracle(orc, pool, qid, part, thetas, res, 40, 0)
+    st, ref = orc.sweep(lens, arr, cost, qid, part, thetas, orc.select_params(k=40))
+    for g, r in zip(res, ref):
+        assert g["n_invalid"] == r["n_invalid"] and g["n_excluded"] == r["n_excluded"]
+        assert g["primary"] == r["primary"]
 
 
 def test_sweep_full_size_c5(E, orc, ctx, c2_partition):
