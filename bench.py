@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--partition", default="rp", choices=["rp", "quantile"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C5 Θ-sweep measurement")
+    ap.add_argument("--sweep-thetas", type=int, default=256)
     return ap.parse_args()
 
 
@@ -170,6 +172,51 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_sweep(E, ctx, dev, args):
+    """C5 (BASELINE configs[4]) on one GPU: 256 Θ x 1M snapshot, K=16, SCORE mode.
+    ALU-bound: each (request, Θ) pair is 3 fp32 FMA-pipe ops (FMUL + 2 FFMA) and one
+    FSETP on the hot path, so the peak is 148 SMs x 128 fp32 lanes x clock / 4."""
+    import torch
+    n = 1_000_000
+    hist = torch.from_numpy(workload.bimodal(1_000_000, 201)).to(dev)
+    c2part, _, _ = E.partition(ctx, hist)
+    pool = workload.pool("bimodal", n, 501)
+    ln, ar, co = (torch.from_numpy(pool[k]).to(dev) for k in ("len", "arrival", "cost"))
+    qid, rsum = E.route(ctx, ln, c2part)
+    thetas = [E.meta(**t) for t in workload.random_thetas(args.sweep_thetas, 502)]
+    sp = E.select_params(k=16, mode=0, now=workload.NOW)
+    sctx = E.Context(dev.index or 0, max_pool=n, max_history=0, max_k=64)
+    outs = E.score_select_sweep(sctx, ln, ar, co, qid, c2part, thetas, sp)
+    for _ in range(2):
+        E.score_select_sweep(sctx, ln, ar, co, qid, c2part, thetas, sp, outs=outs)
+    torch.cuda.synchronize()
+    reps = 10
+    sctx.set_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        E.score_select_sweep(sctx, ln, ar, co, qid, c2part, thetas, sp, outs=outs)
+    e1.record()
+    torch.cuda.synchronize()
+    tm = sctx.timing()
+    ms = e0.elapsed_time(e1) / reps
+    pairs = n * len(thetas)
+    props = torch.cuda.get_device_properties(dev)
+    clk_ghz = 1.965
+    peak = props.multi_processor_count * 128 * clk_ghz * 1e9 / 4
+    achieved = pairs / (ms / 1e3)
+    sctx.close()
+    return {"workload": "C5: 256 Θ uniform in S:500 bounds (seed 502) x 1M bimodal snapshot (seed 501) routed by "
+                        "the GPU Refine-and-Prune partition of bimodal(1M, seed 201); K=16, SCORE",
+            "metric": "(request, Θ) pairs scored+selected/s", "value": achieved, "ms_per_sweep": ms,
+            "thetas": len(thetas), "snapshot": n, "queues": c2part.n,
+            "kernel_ms_per_sweep": tm["sweep_ms"] / reps, "launches_per_sweep": tm["sweep_launches"] / reps,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "pairs/s",
+                         "frac": achieved / peak,
+                         "peak_source": "derived: 148 SMs x 128 fp32 lanes x 1.965 GHz / 4 fp32-pipe ops per pair"},
+            "candidates_inserted_last_sweep": tm["candidates_inserted"]}
+
+
 def config_dict(args, opart_source):
     return {"workload": "C3: 10M pending requests per GPU, heavy-tailed lengths (80% lognormal(ln128,0.6) "
                         "32..2047, 20% Pareto(1.5) 2048..32768), route + score + per-queue top-k",
@@ -272,7 +319,7 @@ def main():
     merge_ms = tm["merge_ms"] / max(tm["merge_launches"], 1)
     achieved = BYTES_PER_REQ * n / (tick_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "ewsjf::tick_kernel (fused: stream route+score+filter, grid barrier, per-queue merge)",
+                "traffic": None, "kernel": "ewsjf::stream_tick_kernel (fused: streaming route+score+filter, grid barrier, per-queue merge)",
                 "algorithmic_bytes_per_launch": BYTES_PER_REQ * n, "kernel_ms": tick_ms,
                 "merge_kernel_ms": merge_ms, "peak_source": peak_src,
                 "share_of_step": tick_ms / ms_per_step if ms_per_step else None}
@@ -311,6 +358,11 @@ def main():
         line["e2e"] = {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": 12 * n,
                        "d2h_bytes_per_step": 4 * n + out_bytes, "ms_per_step": 1e3 * dt, "steps": k_e2e,
                        "path": "ewsjf_tick_host (pinned host SoA in, qid + results out)"}
+
+    # ---- C5: the meta-optimizer's Θ sweep (A12) over a 1M bimodal snapshot routed by
+    # the GPU Refine-and-Prune partition of bimodal(1M, seed 201) (C2's partition)
+    if not args.no_sweep and ws == 1:
+        line["sweep"] = run_sweep(E, ctx, dev, args)
 
     # ---- the oracle beside it (rank 0, N=1 only), bounded sample
     if not args.no_cpu_baseline and ws == 1 and rank == 0:
