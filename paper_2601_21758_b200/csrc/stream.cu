@@ -66,7 +66,7 @@ __host__ __device__ inline StreamSmem stream_layout(bool has_cost, int lut_size,
     L.sechi = o; o = sal16(o + 4LL * kSTab);
     L.thrf = o;  o = sal16(o + 4LL * kSTab);
     L.secf = o;  o = sal16(o + 4LL * kSTab);
-    L.sid = o;   o = sal16(o + 12LL * kSTab);   // sid, round-1 counts, round-1 offsets
+    L.sid = o;   o = sal16(o + 20LL * kSTab);   // sid, round-1 counts, offsets, CTA bounds
     L.bcnt = o;  o = sal16(o + 4LL * kSTab);
     L.misc = o;  o = sal16(o + sizeof(SMisc));
     L.cnt = o;   o = sal16(o + 2LL * kSThreads * (nslots + 2));   // + rows: excluded, other
@@ -297,7 +297,8 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
     };
     if (tid == 0 && A.dbg) { for (int s = 0; s < 16; s++) A.dbg[blockIdx.x * 16 + s] = 0ull; dbg_max(A, 0, gtime()); }
     if (lane_ring) {
-        for (int s = 0; s < S; s++) issue_lane(gw + s * GW, s);
+        if (A.pass0 != 4)
+            for (int s = 0; s < S; s++) issue_lane(gw + s * GW, s);
     } else if (lane == 0) {
         for (int s = 0; s < S; s++) mbar_init(&bars[s], 1);
         fence_mbar_init();
@@ -315,7 +316,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
     {
         const int n16 = (int)((sizeof(Policy) + 15) / 16);
         const int4* src = reinterpret_cast<const int4*>(&P);
-        for (int i = tid; i < n16; i += kSThreads) ((int4*)s_buf)[i] = src[i];
+        for (int i = tid; i < (A.pass0 == 6 ? 0 : n16); i += kSThreads) ((int4*)s_buf)[i] = src[i];
         uint32_t* c32 = (uint32_t*)s_cnt16;
         for (int i = tid; i < kSThreads * (nslots + 2) / 2; i += kSThreads) c32[i] = 0u;
     }
@@ -331,11 +332,12 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
         s_secf[i] = MODE == EWSJF_SELECT_SCORE ? (v ? inf : -inf) : (v ? 0.f : inf);
         s_sid[i] = v ? Ps->sid[i] : (i == kSCodeGap ? -2 : -1);
     }
+    if (tid == 0) dbg_max(A, 12, A.dbg ? gtime() : 0ull);
     {
         // byte LUT length -> queue position, built a word (4 lengths) at a time:
         // each thread walks a contiguous run of words through the sorted,
         // disjoint [min_len, max_len) intervals.
-        const int nw = (lutsz + 1 + 3) / 4;   // lut[0..lutsz], lut[lutsz] = gap
+        const int nw = A.pass0 == 5 ? 0 : (lutsz + 1 + 3) / 4;   // lut[0..lutsz], lut[lutsz] = gap
         const int wpt = (nw + kSThreads - 1) / kSThreads;
         const int w0 = tid * wpt, w1 = min(nw, w0 + wpt);
         if (w0 < w1) {
@@ -347,6 +349,16 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             int qmin = qi < nslots ? Ps->min_len[qi] : INT_MAX, qmax = qi < nslots ? Ps->max_len[qi] : INT_MAX;
             uint32_t* lw = (uint32_t*)lut;
             for (int w = w0; w < w1; w++) {
+                const int L0 = 4 * w;
+                while (L0 >= qmax) {
+                    qi++;
+                    qmin = qi < nslots ? Ps->min_len[qi] : INT_MAX;
+                    qmax = qi < nslots ? Ps->max_len[qi] : INT_MAX;
+                }
+                if (L0 > 0 && L0 >= qmin && L0 + 3 < qmax && L0 + 3 < lutsz) {   // the common case
+                    lw[w] = 0x01010101u * (uint32_t)qi;
+                    continue;
+                }
                 uint32_t word = 0;
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
@@ -364,8 +376,11 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             }
         }
     }
+    if (tid == 0) dbg_max(A, 13, A.dbg ? gtime() : 0ull);
     __syncthreads();
     if (tid == 0) dbg_max(A, 1, gtime());
+    if (lane_ring && A.pass0 == 4)
+        for (int s = 0; s < S; s++) issue_lane(gw + s * GW, s);
 
     unsigned exc = 0, nins = 0, ngap = 0, ncomp = 0, ndrop = 0, excl_total = 0;
     long long cyc_wait = 0, cyc_proc = 0, cyc_loop0 = 0, cyc_ref = 0, cyc_board = 0, cyc_flag = 0, cyc_tile = 0;   // EWSJF_PHASES cycle accounting
@@ -622,11 +637,15 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
     const bool has_tail = (A.n % kWT) != 0;
     auto tile = [&](int64_t t, int st, uint32_t par, u64* r1k, int* r1q) -> bool {
         if (t < nfull) {
+#ifdef EWSJF_CYCLES
             long long c0 = A.dbg ? clock64() : 0;
+#endif
             if (lane_ring) cp_async_wait(S - 1);
             else mbar_wait(&bars[st], par);
+#ifdef EWSJF_CYCLES
             long long c1 = A.dbg ? clock64() : 0;
             cyc_wait += c1 - c0;
+#endif
             const int4 bv = ((const int4*)stage(st, 0))[lane];
             const float4 av = ((const float4*)stage(st, 1))[lane];
             float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -635,7 +654,9 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             const float a4[4] = {av.x, av.y, av.z, av.w};
             const float c4[4] = {cv.x, cv.y, cv.z, cv.w};
             process4(t * kWT + 4 * lane, 4, b4, a4, c4, r1k, r1q);
-                if (A.dbg) cyc_proc += clock64() - c1;
+#ifdef EWSJF_CYCLES
+            if (A.dbg) cyc_proc += clock64() - c1;
+#endif
             // every lane has consumed the stage (its values fed the stores above)
             if (lane_ring) {
                 issue_lane(t + S * GW, st);
@@ -675,12 +696,14 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
     // the keys >= it enter the queue's buffer.  So the stream starts filtered.
     int* s_r1n = (int*)s_sid + kSTab;      // see layout: r1n / r1off follow sid
     int* s_r1off = s_r1n + kSTab;
+    u64* s_r1t = (u64*)(s_r1off + kSTab);   // round-1 CTA-wide bounds (0 = none)
     {
         u64 r1k[4] = {0ull, 0ull, 0ull, 0ull};
         int r1q[4] = {-1, -1, -1, -1};
         tile(gw, 0, 0u, r1k, r1q);
         if (A.pass0 == 7) for (int j = 0; j < 4; j++) r1q[j] = -1;
         __syncthreads();
+        if (tid == 0) dbg_max(A, 13, A.dbg ? gtime() : 0ull);   // all first tiles done
         // per-queue totals and per-thread exclusive prefixes (lane l: threads 16l..16l+15)
         for (int q = warp; q < nslots; q += kSWarps) {
             uint32_t* col = (uint32_t*)(s_cnt16 + (size_t)q * kSThreads) + 8 * lane;
@@ -704,6 +727,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             if (lane == 31) s_r1n[q] = incl;
         }
         __syncthreads();
+        if (tid == 0) dbg_max(A, 14, A.dbg ? gtime() : 0ull);   // prefix done
         if (warp == 0) {
             int carry = 0;
             for (int q0 = 0; q0 < nslots; q0 += 32) {
@@ -731,15 +755,114 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             }
         }
         __syncthreads();
+        if (tid == 0) dbg_max(A, 15, A.dbg ? gtime() : 0ull);   // scatter done
+        // slices larger than a warp's register selection (typically one dominant
+        // queue): one CTA-wide 256-bucket histogram over the keys' high words gives
+        // a valid bound — the lower edge of the highest bucket at which at least K
+        // keys lie above — in four barriers; a bucket too full (ties) falls back to
+        // the warp selection below.
+        {
+            // s_h: [256] buckets, [256] max, [257] min, [258..263] pass state (buffers still empty)
+            unsigned* s_h = (unsigned*)s_buf;
+            for (int q = 0; q < nslots; q++) {
+                const int n = s_r1n[q];
+                if (n <= 32 * kRegSel) continue;
+                const u64* sl = s_ovfk + s_r1off[q];
+                u32 hv[kOvfCap / kSThreads];
+                u32 mx = 0u, mn = 0xffffffffu;
+#pragma unroll
+                for (int r = 0; r < kOvfCap / kSThreads; r++) {
+                    const int j = tid + kSThreads * r;
+                    hv[r] = j < n ? (u32)(sl[j] >> 32) : 0u;
+                    if (j < n) { mx = max(mx, hv[r]); mn = min(mn, hv[r]); }
+                }
+                mx = __reduce_max_sync(0xffffffffu, mx);
+                mn = __reduce_min_sync(0xffffffffu, mn);
+                if (tid == 0) { s_h[256] = 0u; s_h[257] = 0xffffffffu; }
+                __syncthreads();
+                if (lane == 0) { atomicMax(&s_h[256], mx); atomicMin(&s_h[257], mn); }
+                __syncthreads();
+                u32 lo_h = s_h[257], hi_h = s_h[256];    // high-word range still open
+                unsigned above = 0;                      // keys with high word > hi_h
+                u64 res = 0ull;
+                for (int pass = 0; pass < 4; pass++) {
+                    __syncthreads();
+                    if (tid < 256) s_h[tid] = 0u;
+                    __syncthreads();
+                    const unsigned long long R = (unsigned long long)(hi_h - lo_h) + 1ull;
+#pragma unroll
+                    for (int r = 0; r < kOvfCap / kSThreads; r++)
+                        if (tid + kSThreads * r < n && hv[r] >= lo_h && hv[r] <= hi_h)
+                            atomicAdd(&s_h[(unsigned)(((unsigned long long)(hv[r] - lo_h) * 256ull) / R)], 1u);
+                    __syncthreads();
+                    if (warp == 0) {                     // highest bucket b with above + #(>= b) >= K
+                        unsigned c[8], tot = 0;
+#pragma unroll
+                        for (int k = 0; k < 8; k++) { c[k] = s_h[255 - (8 * lane + k)]; tot += c[k]; }
+                        unsigned incl = tot;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= o) incl += u;
+                        }
+                        unsigned run = above + incl - tot;
+                        int bsel = -1;
+                        unsigned csel = 0, cb = 0;
+#pragma unroll
+                        for (int k = 0; k < 8; k++) {
+                            run += c[k];
+                            if (bsel < 0 && run >= (unsigned)K) { bsel = 255 - (8 * lane + k); csel = run; cb = c[k]; }
+                        }
+                        const unsigned hit = __ballot_sync(0xffffffffu, bsel >= 0);
+                        const int src = hit ? __ffs(hit) - 1 : 0;
+                        bsel = __shfl_sync(0xffffffffu, bsel, src);
+                        csel = __shfl_sync(0xffffffffu, csel, src);
+                        cb = __shfl_sync(0xffffffffu, cb, src);
+                        if (lane == 0) {
+                            // bucket b holds high words [e_b, e_{b+1}), e_b = lo + ceil(b R / 256)
+                            const unsigned long long eb = (unsigned long long)lo_h + ((unsigned long long)bsel * R + 255ull) / 256ull;
+                            const unsigned long long eb1 = (unsigned long long)lo_h + ((unsigned long long)(bsel + 1) * R + 255ull) / 256ull;
+                            unsigned st = 0;                  // 0: continue, 1: done, 2: give up
+                            if (bsel < 0) st = 2;
+                            else if (csel <= (unsigned)(cap - 64)) { st = 1; s_h[258] = (unsigned)eb; }
+                            else if (eb1 - eb <= 1) st = 2;   // one high word: ties, the warp path decides
+                            else { s_h[259] = (unsigned)eb; s_h[260] = (unsigned)(eb1 - 1); s_h[261] = csel - cb; }
+                            s_h[262] = st;
+                        }
+                    }
+                    __syncthreads();
+                    const unsigned st = s_h[262];
+                    if (st == 1) { res = (u64)s_h[258] << 32; break; }
+                    if (st == 2) break;
+                    lo_h = s_h[259]; hi_h = s_h[260]; above = s_h[261];
+                }
+                if (tid == 0) s_r1t[q] = res;           // 0: none, the warp selection decides
+                // the CTA copies the keys >= the bound straight into the buffer (<= cap - 64 of them)
+                if (res) {
+#pragma unroll
+                    for (int r = 0; r < kOvfCap / kSThreads; r++) {
+                        const int j = tid + kSThreads * r;
+                        if (j < n && sl[j] >= res) s_buf[(size_t)q * cap + atomicAdd(&s_bcnt[q], 1)] = sl[j];
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        if (tid == 0) dbg_max(A, 12, A.dbg ? gtime() : 0ull);   // CTA histogram bounds done
         for (int q = warp; q < nslots; q += kSWarps) {
             const int n = s_r1n[q];
             const u64* sl = s_ovfk + s_r1off[q];
             u64 t = 0ull;
-            if (n > 32 * kRegSel) t = warp_select_arr(sl, n, K, cap - 64);   // window: <= cap-64 survive
+            const bool copied = n > 32 * kRegSel && s_r1t[q] != 0ull;     // done CTA-wide above
+            if (n > 32 * kRegSel) {
+                t = s_r1t[q];
+                if (!t) t = warp_select_arr(sl, n, K, cap - 64);   // window: <= cap-64 survive
+            }
             else if (n > K) t = warp_kth_arr(sl, n, K, kApproxBit, cap - 64);
+            if (lane == 0) dbg_max(A, 10, A.dbg ? gtime() : 0ull);
             u64* bb = s_buf + (size_t)q * cap;
-            int nb = 0;
-            for (int j0 = 0; j0 < n; j0 += 32) {
+            int nb = copied ? s_bcnt[q] : 0;
+            for (int j0 = 0; j0 < (copied ? 0 : n); j0 += 32) {
                 const int j = j0 + lane;
                 const u64 v = j < n ? sl[j] : 0ull;
                 const bool keep = j < n && v >= t;
@@ -748,7 +871,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
                 nb += __popc(m);
             }
             __syncwarp();
-            if (nb > K) {                    // window survivors -> exact K-th
+            if (nb > K && !copied) {         // window survivors -> a tighter bound
                 t = warp_kth_arr(bb, nb, K, kApproxBit, cap - 64);
                 int outc = 0;
                 for (int j0 = 0; j0 < nb; j0 += 32) {
@@ -763,6 +886,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
                 }
                 nb = outc;
             }
+            if (lane == 0) dbg_max(A, 11, A.dbg ? gtime() : 0ull);
             uint32_t* col = (uint32_t*)(s_cnt16 + (size_t)q * kSThreads) + 8 * lane;
 #pragma unroll
             for (int k = 0; k < 8; k++) col[k] = 0u;
@@ -799,28 +923,20 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
     for (int i = 1;; ++i) {
         // cross-CTA threshold refresh every 4th tile, loaded one tile ahead
         if ((i & 7) == 1 && lane == 0 && nslots > 0) g_pre = __ldcg(&A.gthr[rq]);
-        long long c6 = A.dbg ? clock64() : 0;
         if (!tile(t, st, par, nullptr, nullptr)) break;
-        if (A.dbg) cyc_tile += clock64() - c6;
         t += GW;
         if (++st == S) { st = 0; par ^= 1u; }
-        long long c3 = A.dbg ? clock64() : 0;
         if ((i & 7) == 6 && lane == 0 && nslots > 0) {
             if (g_pre) raise_thr(rq, g_pre);
             rq += kSWarps;
             if (rq >= nslots) rq -= nslots * (rq / nslots);
         }
-        __syncwarp();
-        long long c4 = A.dbg ? clock64() : 0;
-        cyc_ref += c4 - c3;
         if (bm && i == 3)
             for (int q = warp; q < nslots; q += kSWarps) board_refresh(q);
-        long long c5 = A.dbg ? clock64() : 0;
-        cyc_board += c5 - c4;
         if (flag_set()) collective();
-        if (A.dbg) cyc_flag += clock64() - c5;
     }
     if (lane == 0) dbg_max(A, 2, A.dbg ? gtime() : 0ull);
+#ifdef EWSJF_CYCLES
     if (lane == 0 && A.dbg) {   // per-CTA sums over warps (cycles): TMA waits, tile processing, loop total
         atomicAdd(&A.dbg[blockIdx.x * 16 + 10], (unsigned long long)cyc_wait);
         atomicAdd(&A.dbg[blockIdx.x * 16 + 11], (unsigned long long)cyc_proc);
@@ -829,6 +945,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
         atomicAdd(&A.dbg[blockIdx.x * 16 + 14], (unsigned long long)cyc_ref);
         atomicAdd(&A.dbg[blockIdx.x * 16 + 15], (unsigned long long)(cyc_board * 65536 + cyc_flag / 16));
     }
+#endif
     // done streaming: keep serving collectives until every warp is done.  A
     // flag raised by this warp is visible before its ndone increment, and
     // ndone is read before the flag, so no warp leaves while one is pending.
