@@ -405,6 +405,7 @@ static MergeArgs merge_args(ewsjf_ctx* ctx, const ewsjf_partition_t* part, const
     M.gap_cap = ctx->gap_cap;
     M.gthr = ctx->gthr;
     M.blog = ctx->d_blog;
+    M.dbg = getenv("EWSJF_PHASES") ? ctx->dbg : nullptr;
     return M;
 }
 

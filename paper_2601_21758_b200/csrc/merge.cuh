@@ -11,6 +11,15 @@
 #include "tick.cuh"
 
 namespace ewsjf {
+// merge-phase timestamps (EWSJF_PHASES): max over CTAs of slot x of the per-CTA debug row
+#define MDBG(slot_)                                                                                    \
+    do {                                                                                           \
+        if (A.dbg && threadIdx.x == 0) {                                                           \
+            unsigned long long t_;                                                                 \
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                  \
+            atomicMax(&A.dbg[blockIdx.x * 16 + (slot_)], t_);                                        \
+        }                                                                                          \
+    } while (0)
 __host__ __device__ inline int64_t al16m(int64_t x) { return (x + 15) & ~(int64_t)15; }
 
 // ------------------------------------------------------------------ merge ---
@@ -324,6 +333,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             }
         }
         __syncthreads();
+        MDBG(12);
         // ---- members and secondary (rows + this slot's gap requests)
         {
             unsigned long long m = 0;
@@ -372,6 +382,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             __syncthreads();
         }
 
+        MDBG(13);
         // ---- candidate pool: rows entries then this slot's gap requests.  Row keys
         // below the best threshold any CTA published are not in the top-k.
         u64 thr = (IN == MERGE_IN_ROWS && s < nq) ? __ldcg(&A.gthr[s]) : 0ull;
@@ -379,6 +390,35 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         const int total_rows = rowoff[nrows];
         const int total = total_rows + nmine_all;
         int e0 = 0;
+        // fast path (rows input, <= 2 keys per lane per row, <= 12 rows per warp): every
+        // warp loads all keys of its rows in one go (independent loads in flight), then
+        // filters them into the pool; the general loop below then handles only the
+        // gap requests of this slot.
+        constexpr int kMWarps = kMThreads / 32;
+        constexpr int kFR = 12;
+        if (IN == MERGE_IN_ROWS && A.rows.cap <= 64 && nrows <= kFR * kMWarps &&
+            total_rows <= L.esmem - kMThreads) {
+            const int warp_m = tid >> 5;
+            u64 kv[kFR][2];
+#pragma unroll
+            for (int i = 0; i < kFR; i++) {
+                const int r = warp_m + i * kMWarps;
+                const int c = r < nrows ? rowoff[r + 1] - rowoff[r] : 0;
+                const u64* src = A.rows.keys + ((size_t)s * A.rows.G + r) * A.rows.cap;
+                kv[i][0] = lane < c ? __ldcg(src + lane) : 0ull;
+                kv[i][1] = lane + 32 < c ? __ldcg(src + lane + 32) : 0ull;
+            }
+            if (tid == 0) M->pn = 0;
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < kFR; i++)
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                    if (kv[i][h] && kv[i][h] >= thr) uni[atomicAdd(&M->pn, 1)] = kv[i][h];
+            __syncthreads();
+            pn = M->pn;
+            e0 = total_rows;            // rows done; the loop below appends gap requests only
+        }
         while (e0 < total) {
             const int space = L.esmem - pn;
             if (space < kMThreads && pn > kRankMax) {
@@ -388,34 +428,48 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             const int take = min(total - e0, space);
             if (tid == 0) M->pn = pn;
             __syncthreads();
-            for (int i = tid; i < take; i += kMThreads) {
-                const int e = e0 + i;
-                u64 key = 0;
-                float sp = 0.f;
-                bool ok = false;
-                if (e < total_rows) {
-                    int lo = 0, hi = nrows;       // row r with rowoff[r] <= e < rowoff[r+1]
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (rowoff[mid] <= e) lo = mid; else hi = mid;
+            // kU elements per thread per step: their row lookups and loads are issued
+            // together (kU loads in flight instead of one L2 round trip each)
+            constexpr int kU = 8;
+            for (int i0 = tid; i0 < take; i0 += kU * kMThreads) {
+                u64 key[kU];
+                float sp[kU];
+                bool ok[kU];
+#pragma unroll
+                for (int u = 0; u < kU; u++) {
+                    const int i = i0 + u * kMThreads;
+                    const int e = e0 + i;
+                    key[u] = 0ull; sp[u] = 0.f; ok[u] = false;
+                    if (i < take && e < total_rows) {
+                        int lo = 0, hi = nrows;       // row r with rowoff[r] <= e < rowoff[r+1]
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (rowoff[mid] <= e) lo = mid; else hi = mid;
+                        }
+                        const int j = e - rowoff[lo];
+                        if (IN == MERGE_IN_ROWS) {
+                            key[u] = __ldcg(&A.rows.keys[((size_t)s * A.rows.G + lo) * A.rows.cap + j]);
+                        } else {
+                            const unsigned char* rec = A.ex_in + (int64_t)lo * A.ex_bytes;
+                            key[u] = ((const u64*)(rec + X.keys))[(size_t)s * K + j];
+                            sp[u] = ((const float*)(rec + X.sp))[(size_t)s * K + j];
+                        }
+                        ok[u] = true;
                     }
-                    const int j = e - rowoff[lo];
-                    if (IN == MERGE_IN_ROWS) {
-                        key = A.rows.keys[((size_t)s * A.rows.G + lo) * A.rows.cap + j];
-                    } else {
-                        const unsigned char* rec = A.ex_in + (int64_t)lo * A.ex_bytes;
-                        key = ((const u64*)(rec + X.keys))[(size_t)s * K + j];
-                        sp = ((const float*)(rec + X.sp))[(size_t)s * K + j];
-                    }
-                    ok = true;
-                } else if (myslot[e - total_rows] == s) {
-                    u64 k2;
-                    ok = gap_keys(gap_entry(mygap[e - total_rows]), key, k2, sp);
                 }
-                if (ok && key >= thr) {
-                    const int p = atomicAdd(&M->pn, 1);
-                    uni[p] = key;
-                    if (psp) psp[p] = sp;
+#pragma unroll
+                for (int u = 0; u < kU; u++) {
+                    const int i = i0 + u * kMThreads;
+                    const int e = e0 + i;
+                    if (i < take && e >= total_rows && myslot[e - total_rows] == s) {
+                        u64 k2;
+                        ok[u] = gap_keys(gap_entry(mygap[e - total_rows]), key[u], k2, sp[u]);
+                    }
+                    if (ok[u] && key[u] >= thr) {
+                        const int p = atomicAdd(&M->pn, 1);
+                        uni[p] = key[u];
+                        if (psp) psp[p] = sp[u];
+                    }
                 }
             }
             __syncthreads();
@@ -423,6 +477,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             e0 += take;
         }
         if (pn > kRankMax) pool_shrink(uni, psp, pn, thr, K, surv, ssp, M);
+        MDBG(14);
         // rank sort (keys unique) -> surv[0..pn) descending
         for (int i = tid; i < pn; i += kMThreads) {
             const u64 k = uni[i];
@@ -432,6 +487,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             if (psp) ssp[r] = psp[i];
         }
         __syncthreads();
+        MDBG(15);
         const int nout = pn < K ? pn : K;
         auto payload = [&](int r) -> float {     // s' of ranked entry r
             const u64 k = surv[r];
@@ -512,8 +568,23 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         M->is_last = (t == gridDim.x - 1);
     }
     __syncthreads();
-    if (!M->is_last || tid != 0) return;
+    if (!M->is_last || tid >= 32) return;
     __threadfence();
+    // Alg. 1 ArgMax over the non-empty queues by head score, ties -> lowest position
+    // (one warp: all loads in flight at once, then a warp reduction)
+    int primary = -1;
+    if (OUT == MERGE_OUT_FINAL) {
+        u64 best = 0ull;      // (ordered head score << 32) | ~position, 0 = none
+        for (int p = tid; p < nfinal; p += 32) {
+            if (__ldcg(&A.count[p]) > 0) {
+                const u64 k = ((u64)ord_f32(__ldcg(&A.head_score[p])) << 32) | (u64)(~(u32)p);
+                best = k > best ? k : best;
+            }
+        }
+        best = warp_max_u64(best);
+        primary = best ? (int)(~(u32)best) : -1;
+    }
+    if (tid != 0) return;
     long long inv = (long long)__ldcg(&A.ctr->n_invalid) + M->ndrop;
     long long exc = (long long)__ldcg(&A.ctr->n_excluded);
     if (IN == MERGE_IN_EXCHANGE) {
@@ -524,16 +595,6 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         }
     }
     if (OUT != MERGE_OUT_EXCHANGE && A.summary) {
-        int primary = -1;
-        float best = 0.f;
-        if (OUT == MERGE_OUT_FINAL) {
-            for (int p = 0; p < nfinal; p++) {
-                if (__ldcg(&A.count[p]) > 0) {
-                    const float h = __ldcg(&A.head_score[p]);
-                    if (primary < 0 || h > best) { primary = p; best = h; }
-                }
-            }
-        }
         ewsjf_summary sm;
         sm.n_queues = nfinal;
         sm.primary = primary;

@@ -531,7 +531,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             for (int j = 0; j < 4; j++) gm |= (unsigned)(code[j] == kSCodeGap) << j;
             if (__any_sync(0xffffffffu, gm != 0)) {
                 ngap += __popc(gm);
-#pragma unroll
+#pragma unroll 1
                 for (int j = 0; j < 4; j++) {
                     const bool g = (gm >> j) & 1u;
                     const unsigned m = __ballot_sync(0xffffffffu, g);
@@ -545,9 +545,10 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
                             if (p < (unsigned long long)A.gap_cap) {
                                 GapEntry e;
                                 e.gid = gbase + (uint32_t)(idx0 + j);
-                                e.len = b[j];
-                                e.arrival = ar[j];
-                                e.cost = HAS_COST ? co[j] : __int_as_float(0x7fc00000);
+                                e.len = j == 0 ? b[0] : (j == 1 ? b[1] : (j == 2 ? b[2] : b[3]));
+                                e.arrival = j == 0 ? ar[0] : (j == 1 ? ar[1] : (j == 2 ? ar[2] : ar[3]));
+                                e.cost = HAS_COST ? (j == 0 ? co[0] : (j == 1 ? co[1] : (j == 2 ? co[2] : co[3])))
+                                                  : __int_as_float(0x7fc00000);
                                 A.gap[p] = e;
                             }
                         }
@@ -590,13 +591,17 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
         }
         // rare: exact 64-bit keys, slot reservations, secondary max (per lane)
         if (__any_sync(0xffffffffu, (pass1 | pass2) != 0)) {
-#pragma unroll
+#pragma unroll 1
             for (int j = 0; j < 4; j++) {
                 if (!(((pass1 | pass2) >> j) & 1u)) continue;
+                // register selects (a rolled loop must not index the arrays dynamically)
+                const float arj = j == 0 ? ar[0] : (j == 1 ? ar[1] : (j == 2 ? ar[2] : ar[3]));
+                const float spj = j == 0 ? sp[0] : (j == 1 ? sp[1] : (j == 2 ? sp[2] : sp[3]));
+                const int cj = j == 0 ? code[0] : (j == 1 ? code[1] : (j == 2 ? code[2] : code[3]));
                 const u32 lo = ~(gbase + (uint32_t)(idx0 + j));
-                const int q = code[j] & 0xFF;
-                const u32 fh = ~ord_f32(ar[j]);
-                const u32 sh = __float_as_uint(sp[j]);
+                const int q = cj & 0xFF;
+                const u32 fh = ~ord_f32(arj);
+                const u32 sh = __float_as_uint(spj);
                 const u32 k1h = MODE == EWSJF_SELECT_SCORE ? sh : fh;
                 const u32 k2h = MODE == EWSJF_SELECT_SCORE ? fh : sh;
                 const u64 k1 = ((u64)k1h << 32) | lo;
@@ -619,7 +624,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
                     if (k2h >= old) {
                         atomicMax(&s_sec[q], ((u64)k2h << 32) | lo);
                         // the fast copy may lag (looser), never pass a tie by mistake: ties go to the exact max
-                        *(volatile float*)&s_secf[q] = MODE == EWSJF_SELECT_SCORE ? ar[j] : sp[j];
+                        *(volatile float*)&s_secf[q] = MODE == EWSJF_SELECT_SCORE ? arj : spj;
                     }
                 }
             }
@@ -636,47 +641,24 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
     // nfull: the ragged tail (direct loads).  Returns false past the end.
     const bool has_tail = (A.n % kWT) != 0;
     auto tile = [&](int64_t t, int st, uint32_t par, u64* r1k, int* r1q) -> bool {
-        if (t < nfull) {
-#ifdef EWSJF_CYCLES
-            long long c0 = A.dbg ? clock64() : 0;
-#endif
+        const bool full = t < nfull;
+        if (!full && !(t == nfull && has_tail)) return false;
+        int b4[4];
+        float a4[4], c4[4];
+        int nv = 4;
+        const int64_t i0 = t * kWT + 4 * lane;
+        if (full) {
             if (lane_ring) cp_async_wait(S - 1);
             else mbar_wait(&bars[st], par);
-#ifdef EWSJF_CYCLES
-            long long c1 = A.dbg ? clock64() : 0;
-            cyc_wait += c1 - c0;
-#endif
             const int4 bv = ((const int4*)stage(st, 0))[lane];
             const float4 av = ((const float4*)stage(st, 1))[lane];
             float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
             if (HAS_COST) cv = ((const float4*)stage(st, 2))[lane];
-            const int b4[4] = {bv.x, bv.y, bv.z, bv.w};
-            const float a4[4] = {av.x, av.y, av.z, av.w};
-            const float c4[4] = {cv.x, cv.y, cv.z, cv.w};
-            process4(t * kWT + 4 * lane, 4, b4, a4, c4, r1k, r1q);
-#ifdef EWSJF_CYCLES
-            if (A.dbg) cyc_proc += clock64() - c1;
-#endif
-            // every lane has consumed the stage (its values fed the stores above)
-            if (lane_ring) {
-                issue_lane(t + S * GW, st);
-                return true;
-            }
-            __syncwarp();
-            if (lane == 0) {
-                const int64_t tn = t + S * GW;
-                if (tn < nfull) {
-                    if (A.gap_cap < 0) fence_proxy_async();   // (experiment switch; never taken)
-                    issue(tn, st);
-                }
-            }
-            return true;
-        }
-        if (t == nfull && has_tail) {
-            const int64_t i0 = nfull * kWT + 4 * lane;
-            const int nv = (int)max((int64_t)0, min((int64_t)4, A.n - i0));
-            int b4[4];
-            float a4[4], c4[4];
+            b4[0] = bv.x; b4[1] = bv.y; b4[2] = bv.z; b4[3] = bv.w;
+            a4[0] = av.x; a4[1] = av.y; a4[2] = av.z; a4[3] = av.w;
+            c4[0] = cv.x; c4[1] = cv.y; c4[2] = cv.z; c4[3] = cv.w;
+        } else {                                  // the ragged tail: direct loads
+            nv = (int)max((int64_t)0, min((int64_t)4, A.n - i0));
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 const bool v = j < nv;
@@ -684,9 +666,17 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
                 a4[j] = v ? __ldg(A.arrival + i0 + j) : 0.f;
                 c4[j] = (HAS_COST && v) ? __ldg(A.cost + i0 + j) : 0.f;
             }
-            process4(i0, nv, b4, a4, c4, r1k, r1q);
         }
-        return false;
+        process4(i0, nv, b4, a4, c4, r1k, r1q);
+        if (!full) return false;
+        // every lane has consumed the stage (its values fed the stores above)
+        if (lane_ring) {
+            issue_lane(t + S * GW, st);
+        } else {
+            __syncwarp();
+            if (lane == 0 && t + S * GW < nfull) issue(t + S * GW, st);
+        }
+        return true;
     };
 
     // ---- round 1 (every warp's first tile), one structured CTA pass: the
@@ -697,273 +687,270 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
     int* s_r1n = (int*)s_sid + kSTab;      // see layout: r1n / r1off follow sid
     int* s_r1off = s_r1n + kSTab;
     u64* s_r1t = (u64*)(s_r1off + kSTab);   // round-1 CTA-wide bounds (0 = none)
-    {
-        u64 r1k[4] = {0ull, 0ull, 0ull, 0ull};
-        int r1q[4] = {-1, -1, -1, -1};
-        tile(gw, 0, 0u, r1k, r1q);
-        if (A.pass0 == 7) for (int j = 0; j < 4; j++) r1q[j] = -1;
-        __syncthreads();
-        if (tid == 0) dbg_max(A, 13, A.dbg ? gtime() : 0ull);   // all first tiles done
-        // per-queue totals and per-thread exclusive prefixes (lane l: threads 16l..16l+15)
-        for (int q = warp; q < nslots; q += kSWarps) {
-            uint32_t* col = (uint32_t*)(s_cnt16 + (size_t)q * kSThreads) + 8 * lane;
-            uint32_t w[8];
-            int sum = 0;
-#pragma unroll
-            for (int k = 0; k < 8; k++) { w[k] = col[k]; sum += (int)(w[k] & 0xffffu) + (int)(w[k] >> 16); }
-            int incl = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += u;
-            }
-            int run = incl - sum;
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                const uint32_t a0 = (uint32_t)run; run += (int)(w[k] & 0xffffu);
-                const uint32_t a1 = (uint32_t)run; run += (int)(w[k] >> 16);
-                col[k] = a0 | (a1 << 16);
-            }
-            if (lane == 31) s_r1n[q] = incl;
-        }
-        __syncthreads();
-        if (tid == 0) dbg_max(A, 14, A.dbg ? gtime() : 0ull);   // prefix done
-        if (warp == 0) {
-            int carry = 0;
-            for (int q0 = 0; q0 < nslots; q0 += 32) {
-                const int q = q0 + lane;
-                const int v = q < nslots ? s_r1n[q] : 0;
-                int incl = v;
-#pragma unroll
+
+    // ---- one loop: round 1 at i == 0, then the private ring; CTA barriers only
+    // in collectives.  A warp out of tiles keeps serving collectives until every
+    // warp is done (a flag raised by this warp is visible before its ndone
+    // increment, and ndone is read before the flag, so no warp leaves while one
+    // is pending).  One call site each for tile() and collective() (code size:
+    // the cold paths are not duplicated in the instruction stream).
+    u64 r1k[4] = {0ull, 0ull, 0ull, 0ull};
+    int r1q[4] = {-1, -1, -1, -1};
+    u64 g_pre = 0ull;
+    int rq = warp % max(nslots, 1);
+    int st = 0;
+    uint32_t par = 0u;
+    int64_t t = gw;
+    bool streaming = true;
+    for (int i = 0;; ++i) {
+        if (streaming) {
+            if ((i & 7) == 1 && lane == 0 && nslots > 0) g_pre = __ldcg(&A.gthr[rq]);
+            const bool first = i == 0;
+            const bool more = tile(t, st, par, first ? r1k : nullptr, first ? r1q : nullptr);
+            if (first) {
+            if (A.pass0 == 7) for (int j = 0; j < 4; j++) r1q[j] = -1;
+            __syncthreads();
+            if (tid == 0) dbg_max(A, 13, A.dbg ? gtime() : 0ull);   // all first tiles done
+            // per-queue totals and per-thread exclusive prefixes (lane l: threads 16l..16l+15)
+            for (int q = warp; q < nslots; q += kSWarps) {
+                uint32_t* col = (uint32_t*)(s_cnt16 + (size_t)q * kSThreads) + 8 * lane;
+                uint32_t w[8];
+                int sum = 0;
+    #pragma unroll
+                for (int k = 0; k < 8; k++) { w[k] = col[k]; sum += (int)(w[k] & 0xffffu) + (int)(w[k] >> 16); }
+                int incl = sum;
+    #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int u = __shfl_up_sync(0xffffffffu, incl, o);
                     if (lane >= o) incl += u;
                 }
-                if (q < nslots) s_r1off[q] = carry + incl - v;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const int q = r1q[j];
-            if (q >= 0) {
-                int k = 0;
-#pragma unroll
-                for (int jj = 0; jj < j; jj++) k += r1q[jj] == q;
-                s_ovfk[s_r1off[q] + s_cnt16[(size_t)q * kSThreads + tid] + k] = r1k[j];
-            }
-        }
-        __syncthreads();
-        if (tid == 0) dbg_max(A, 15, A.dbg ? gtime() : 0ull);   // scatter done
-        // slices larger than a warp's register selection (typically one dominant
-        // queue): one CTA-wide 256-bucket histogram over the keys' high words gives
-        // a valid bound — the lower edge of the highest bucket at which at least K
-        // keys lie above — in four barriers; a bucket too full (ties) falls back to
-        // the warp selection below.
-        {
-            // s_h: [256] buckets, [256] max, [257] min, [258..263] pass state (buffers still empty)
-            unsigned* s_h = (unsigned*)s_buf;
-            for (int q = 0; q < nslots; q++) {
-                const int n = s_r1n[q];
-                if (n <= 32 * kRegSel) continue;
-                const u64* sl = s_ovfk + s_r1off[q];
-                u32 hv[kOvfCap / kSThreads];
-                u32 mx = 0u, mn = 0xffffffffu;
-#pragma unroll
-                for (int r = 0; r < kOvfCap / kSThreads; r++) {
-                    const int j = tid + kSThreads * r;
-                    hv[r] = j < n ? (u32)(sl[j] >> 32) : 0u;
-                    if (j < n) { mx = max(mx, hv[r]); mn = min(mn, hv[r]); }
+                int run = incl - sum;
+    #pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const uint32_t a0 = (uint32_t)run; run += (int)(w[k] & 0xffffu);
+                    const uint32_t a1 = (uint32_t)run; run += (int)(w[k] >> 16);
+                    col[k] = a0 | (a1 << 16);
                 }
-                mx = __reduce_max_sync(0xffffffffu, mx);
-                mn = __reduce_min_sync(0xffffffffu, mn);
-                if (tid == 0) { s_h[256] = 0u; s_h[257] = 0xffffffffu; }
-                __syncthreads();
-                if (lane == 0) { atomicMax(&s_h[256], mx); atomicMin(&s_h[257], mn); }
-                __syncthreads();
-                u32 lo_h = s_h[257], hi_h = s_h[256];    // high-word range still open
-                unsigned above = 0;                      // keys with high word > hi_h
-                u64 res = 0ull;
-                for (int pass = 0; pass < 4; pass++) {
-                    __syncthreads();
-                    if (tid < 256) s_h[tid] = 0u;
-                    __syncthreads();
-                    const unsigned long long R = (unsigned long long)(hi_h - lo_h) + 1ull;
-#pragma unroll
-                    for (int r = 0; r < kOvfCap / kSThreads; r++)
-                        if (tid + kSThreads * r < n && hv[r] >= lo_h && hv[r] <= hi_h)
-                            atomicAdd(&s_h[(unsigned)(((unsigned long long)(hv[r] - lo_h) * 256ull) / R)], 1u);
-                    __syncthreads();
-                    if (warp == 0) {                     // highest bucket b with above + #(>= b) >= K
-                        unsigned c[8], tot = 0;
-#pragma unroll
-                        for (int k = 0; k < 8; k++) { c[k] = s_h[255 - (8 * lane + k)]; tot += c[k]; }
-                        unsigned incl = tot;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
-                            if (lane >= o) incl += u;
-                        }
-                        unsigned run = above + incl - tot;
-                        int bsel = -1;
-                        unsigned csel = 0, cb = 0;
-#pragma unroll
-                        for (int k = 0; k < 8; k++) {
-                            run += c[k];
-                            if (bsel < 0 && run >= (unsigned)K) { bsel = 255 - (8 * lane + k); csel = run; cb = c[k]; }
-                        }
-                        const unsigned hit = __ballot_sync(0xffffffffu, bsel >= 0);
-                        const int src = hit ? __ffs(hit) - 1 : 0;
-                        bsel = __shfl_sync(0xffffffffu, bsel, src);
-                        csel = __shfl_sync(0xffffffffu, csel, src);
-                        cb = __shfl_sync(0xffffffffu, cb, src);
-                        if (lane == 0) {
-                            // bucket b holds high words [e_b, e_{b+1}), e_b = lo + ceil(b R / 256)
-                            const unsigned long long eb = (unsigned long long)lo_h + ((unsigned long long)bsel * R + 255ull) / 256ull;
-                            const unsigned long long eb1 = (unsigned long long)lo_h + ((unsigned long long)(bsel + 1) * R + 255ull) / 256ull;
-                            unsigned st = 0;                  // 0: continue, 1: done, 2: give up
-                            if (bsel < 0) st = 2;
-                            else if (csel <= (unsigned)(cap - 64)) { st = 1; s_h[258] = (unsigned)eb; }
-                            else if (eb1 - eb <= 1) st = 2;   // one high word: ties, the warp path decides
-                            else { s_h[259] = (unsigned)eb; s_h[260] = (unsigned)(eb1 - 1); s_h[261] = csel - cb; }
-                            s_h[262] = st;
-                        }
+                if (lane == 31) s_r1n[q] = incl;
+            }
+            __syncthreads();
+            if (tid == 0) dbg_max(A, 14, A.dbg ? gtime() : 0ull);   // prefix done
+            if (warp == 0) {
+                int carry = 0;
+                for (int q0 = 0; q0 < nslots; q0 += 32) {
+                    const int q = q0 + lane;
+                    const int v = q < nslots ? s_r1n[q] : 0;
+                    int incl = v;
+    #pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += u;
                     }
-                    __syncthreads();
-                    const unsigned st = s_h[262];
-                    if (st == 1) { res = (u64)s_h[258] << 32; break; }
-                    if (st == 2) break;
-                    lo_h = s_h[259]; hi_h = s_h[260]; above = s_h[261];
+                    if (q < nslots) s_r1off[q] = carry + incl - v;
+                    carry += __shfl_sync(0xffffffffu, incl, 31);
                 }
-                if (tid == 0) s_r1t[q] = res;           // 0: none, the warp selection decides
-                // the CTA copies the keys >= the bound straight into the buffer (<= cap - 64 of them)
-                if (res) {
-#pragma unroll
+            }
+            __syncthreads();
+    #pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int q = r1q[j];
+                if (q >= 0) {
+                    int k = 0;
+    #pragma unroll
+                    for (int jj = 0; jj < j; jj++) k += r1q[jj] == q;
+                    s_ovfk[s_r1off[q] + s_cnt16[(size_t)q * kSThreads + tid] + k] = r1k[j];
+                }
+            }
+            __syncthreads();
+            if (tid == 0) dbg_max(A, 15, A.dbg ? gtime() : 0ull);   // scatter done
+            // slices larger than a warp's register selection (typically one dominant
+            // queue): one CTA-wide 256-bucket histogram over the keys' high words gives
+            // a valid bound — the lower edge of the highest bucket at which at least K
+            // keys lie above — in four barriers; a bucket too full (ties) falls back to
+            // the warp selection below.
+            {
+                // s_h: [256] buckets, [256] max, [257] min, [258..263] pass state (buffers still empty)
+                unsigned* s_h = (unsigned*)s_buf;
+                for (int q = 0; q < nslots; q++) {
+                    const int n = s_r1n[q];
+                    if (n <= 32 * kRegSel) continue;
+                    const u64* sl = s_ovfk + s_r1off[q];
+                    u32 hv[kOvfCap / kSThreads];
+                    u32 mx = 0u, mn = 0xffffffffu;
+    #pragma unroll
                     for (int r = 0; r < kOvfCap / kSThreads; r++) {
                         const int j = tid + kSThreads * r;
-                        if (j < n && sl[j] >= res) s_buf[(size_t)q * cap + atomicAdd(&s_bcnt[q], 1)] = sl[j];
+                        hv[r] = j < n ? (u32)(sl[j] >> 32) : 0u;
+                        if (j < n) { mx = max(mx, hv[r]); mn = min(mn, hv[r]); }
                     }
+                    mx = __reduce_max_sync(0xffffffffu, mx);
+                    mn = __reduce_min_sync(0xffffffffu, mn);
+                    if (tid == 0) { s_h[256] = 0u; s_h[257] = 0xffffffffu; }
+                    __syncthreads();
+                    if (lane == 0) { atomicMax(&s_h[256], mx); atomicMin(&s_h[257], mn); }
+                    __syncthreads();
+                    u32 lo_h = s_h[257], hi_h = s_h[256];    // high-word range still open
+                    unsigned above = 0;                      // keys with high word > hi_h
+                    u64 res = 0ull;
+                    for (int pass = 0; pass < 4; pass++) {
+                        __syncthreads();
+                        if (tid < 256) s_h[tid] = 0u;
+                        __syncthreads();
+                        const unsigned long long R = (unsigned long long)(hi_h - lo_h) + 1ull;
+    #pragma unroll
+                        for (int r = 0; r < kOvfCap / kSThreads; r++)
+                            if (tid + kSThreads * r < n && hv[r] >= lo_h && hv[r] <= hi_h)
+                                atomicAdd(&s_h[(unsigned)(((unsigned long long)(hv[r] - lo_h) * 256ull) / R)], 1u);
+                        __syncthreads();
+                        if (warp == 0) {                     // highest bucket b with above + #(>= b) >= K
+                            unsigned c[8], tot = 0;
+    #pragma unroll
+                            for (int k = 0; k < 8; k++) { c[k] = s_h[255 - (8 * lane + k)]; tot += c[k]; }
+                            unsigned incl = tot;
+    #pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                                if (lane >= o) incl += u;
+                            }
+                            unsigned run = above + incl - tot;
+                            int bsel = -1;
+                            unsigned csel = 0, cb = 0;
+    #pragma unroll
+                            for (int k = 0; k < 8; k++) {
+                                run += c[k];
+                                if (bsel < 0 && run >= (unsigned)K) { bsel = 255 - (8 * lane + k); csel = run; cb = c[k]; }
+                            }
+                            const unsigned hit = __ballot_sync(0xffffffffu, bsel >= 0);
+                            const int src = hit ? __ffs(hit) - 1 : 0;
+                            bsel = __shfl_sync(0xffffffffu, bsel, src);
+                            csel = __shfl_sync(0xffffffffu, csel, src);
+                            cb = __shfl_sync(0xffffffffu, cb, src);
+                            if (lane == 0) {
+                                // bucket b holds high words [e_b, e_{b+1}), e_b = lo + ceil(b R / 256)
+                                const unsigned long long eb = (unsigned long long)lo_h + ((unsigned long long)bsel * R + 255ull) / 256ull;
+                                const unsigned long long eb1 = (unsigned long long)lo_h + ((unsigned long long)(bsel + 1) * R + 255ull) / 256ull;
+                                unsigned st = 0;                  // 0: continue, 1: done, 2: give up
+                                if (bsel < 0) st = 2;
+                                else if (csel <= (unsigned)(cap - 64)) { st = 1; s_h[258] = (unsigned)eb; }
+                                else if (eb1 - eb <= 1) st = 2;   // one high word: ties, the warp path decides
+                                else { s_h[259] = (unsigned)eb; s_h[260] = (unsigned)(eb1 - 1); s_h[261] = csel - cb; }
+                                s_h[262] = st;
+                            }
+                        }
+                        __syncthreads();
+                        const unsigned st = s_h[262];
+                        if (st == 1) { res = (u64)s_h[258] << 32; break; }
+                        if (st == 2) break;
+                        lo_h = s_h[259]; hi_h = s_h[260]; above = s_h[261];
+                    }
+                    if (tid == 0) s_r1t[q] = res;           // 0: none, the warp selection decides
+                    // the CTA copies the keys >= the bound straight into the buffer (<= cap - 64 of them)
+                    if (res) {
+    #pragma unroll
+                        for (int r = 0; r < kOvfCap / kSThreads; r++) {
+                            const int j = tid + kSThreads * r;
+                            if (j < n && sl[j] >= res) s_buf[(size_t)q * cap + atomicAdd(&s_bcnt[q], 1)] = sl[j];
+                        }
+                    }
+                    __syncthreads();
                 }
-                __syncthreads();
             }
-        }
-        if (tid == 0) dbg_max(A, 12, A.dbg ? gtime() : 0ull);   // CTA histogram bounds done
-        for (int q = warp; q < nslots; q += kSWarps) {
-            const int n = s_r1n[q];
-            const u64* sl = s_ovfk + s_r1off[q];
-            u64 t = 0ull;
-            const bool copied = n > 32 * kRegSel && s_r1t[q] != 0ull;     // done CTA-wide above
-            if (n > 32 * kRegSel) {
-                t = s_r1t[q];
-                if (!t) t = warp_select_arr(sl, n, K, cap - 64);   // window: <= cap-64 survive
-            }
-            else if (n > K) t = warp_kth_arr(sl, n, K, kApproxBit, cap - 64);
-            if (lane == 0) dbg_max(A, 10, A.dbg ? gtime() : 0ull);
-            u64* bb = s_buf + (size_t)q * cap;
-            int nb = copied ? s_bcnt[q] : 0;
-            for (int j0 = 0; j0 < (copied ? 0 : n); j0 += 32) {
-                const int j = j0 + lane;
-                const u64 v = j < n ? sl[j] : 0ull;
-                const bool keep = j < n && v >= t;
-                const unsigned m = __ballot_sync(0xffffffffu, keep);
-                if (keep) bb[nb + __popc(m & ((1u << lane) - 1u))] = v;
-                nb += __popc(m);
-            }
-            __syncwarp();
-            if (nb > K && !copied) {         // window survivors -> a tighter bound
-                t = warp_kth_arr(bb, nb, K, kApproxBit, cap - 64);
-                int outc = 0;
-                for (int j0 = 0; j0 < nb; j0 += 32) {
+            if (tid == 0) dbg_max(A, 12, A.dbg ? gtime() : 0ull);   // CTA histogram bounds done
+            for (int q = warp; q < nslots; q += kSWarps) {
+                const int n = s_r1n[q];
+                const u64* sl = s_ovfk + s_r1off[q];
+                u64 t = 0ull;
+                const bool copied = n > 32 * kRegSel && s_r1t[q] != 0ull;     // done CTA-wide above
+                if (n > 32 * kRegSel) {
+                    t = s_r1t[q];
+                    if (!t) t = warp_select_arr(sl, n, K, cap - 64);   // window: <= cap-64 survive
+                }
+                else if (n > K) t = warp_kth_arr(sl, n, K, kApproxBit, cap - 64);
+                if (lane == 0) dbg_max(A, 10, A.dbg ? gtime() : 0ull);
+                u64* bb = s_buf + (size_t)q * cap;
+                int nb = copied ? s_bcnt[q] : 0;
+                for (int j0 = 0; j0 < (copied ? 0 : n); j0 += 32) {
                     const int j = j0 + lane;
-                    const u64 v = j < nb ? bb[j] : 0ull;
-                    const bool keep = j < nb && v >= t;
+                    const u64 v = j < n ? sl[j] : 0ull;
+                    const bool keep = j < n && v >= t;
                     const unsigned m = __ballot_sync(0xffffffffu, keep);
-                    __syncwarp();
-                    if (keep) bb[outc + __popc(m & ((1u << lane) - 1u))] = v;
-                    outc += __popc(m);
-                    __syncwarp();
+                    if (keep) bb[nb + __popc(m & ((1u << lane) - 1u))] = v;
+                    nb += __popc(m);
                 }
-                nb = outc;
-            }
-            if (lane == 0) dbg_max(A, 11, A.dbg ? gtime() : 0ull);
-            uint32_t* col = (uint32_t*)(s_cnt16 + (size_t)q * kSThreads) + 8 * lane;
-#pragma unroll
-            for (int k = 0; k < 8; k++) col[k] = 0u;
-            if (lane == 0) {
-                s_bcnt[q] = nb;
-                if (t) { raise_thr(q, t); atomicMax(&A.gthr[q], t); }
-            }
-            if (bm) {                        // board row: this CTA's top-bm keys of q
-                u64 prev = ~0ull;
-                for (int i = 0; i < bm; i++) {
-                    u64 mx = 0;
-                    for (int j = lane; j < nb; j += 32) {
-                        const u64 v = bb[j];
-                        if (v < prev && v > mx) mx = v;
+                __syncwarp();
+                if (nb > K && !copied) {         // window survivors -> a tighter bound
+                    t = warp_kth_arr(bb, nb, K, kApproxBit, cap - 64);
+                    int outc = 0;
+                    for (int j0 = 0; j0 < nb; j0 += 32) {
+                        const int j = j0 + lane;
+                        const u64 v = j < nb ? bb[j] : 0ull;
+                        const bool keep = j < nb && v >= t;
+                        const unsigned m = __ballot_sync(0xffffffffu, keep);
+                        __syncwarp();
+                        if (keep) bb[outc + __popc(m & ((1u << lane) - 1u))] = v;
+                        outc += __popc(m);
+                        __syncwarp();
                     }
-                    mx = warp_max_u64(mx);
-                    if (lane == 0) A.board[((size_t)q * G + blockIdx.x) * bm + i] = mx;
-                    prev = mx;
+                    nb = outc;
+                }
+                if (lane == 0) dbg_max(A, 11, A.dbg ? gtime() : 0ull);
+                uint32_t* col = (uint32_t*)(s_cnt16 + (size_t)q * kSThreads) + 8 * lane;
+    #pragma unroll
+                for (int k = 0; k < 8; k++) col[k] = 0u;
+                if (lane == 0) {
+                    s_bcnt[q] = nb;
+                    if (t) { raise_thr(q, t); atomicMax(&A.gthr[q], t); }
+                }
+                if (bm) {                        // board row: this CTA's top-bm keys of q
+                    u64 prev = ~0ull;
+                    for (int i = 0; i < bm; i++) {
+                        u64 mx = 0;
+                        for (int j = lane; j < nb; j += 32) {
+                            const u64 v = bb[j];
+                            if (v < prev && v > mx) mx = v;
+                        }
+                        mx = warp_max_u64(mx);
+                        if (lane == 0) A.board[((size_t)q * G + blockIdx.x) * bm + i] = mx;
+                        prev = mx;
+                    }
                 }
             }
+            __syncthreads();
+                if (A.dbg && lane == 0 && warp == 0) dbg_max(A, 7, gtime());
+            }
+            if (more) {
+                t += GW;
+                if (++st == S) { st = 0; par ^= 1u; }
+                if ((i & 7) == 6 && lane == 0 && nslots > 0) {
+                    if (g_pre) raise_thr(rq, g_pre);
+                    rq += kSWarps;
+                    if (rq >= nslots) rq -= nslots * (rq / nslots);
+                }
+                if (bm && i == 3)
+                    for (int q = warp; q < nslots; q += kSWarps) board_refresh(q);
+            } else {
+                streaming = false;
+                if (lane == 0) dbg_max(A, 2, A.dbg ? gtime() : 0ull);
+                __threadfence_block();
+                __syncwarp();
+                if (lane == 0) atomicAdd(&M->ndone, 1);
+            }
+        } else {
+            int f = 0, dn = 0;
+            if (lane == 0) {
+                dn = *(volatile int*)&M->ndone;
+                __threadfence_block();
+                f = *(volatile int*)&M->flag;
+            }
+            f = __shfl_sync(0xffffffffu, f, 0);
+            dn = __shfl_sync(0xffffffffu, dn, 0);
+            if (!f) {
+                if (dn == kSWarps) break;
+                __nanosleep(64);
+                continue;
+            }
         }
-        __syncthreads();
-        if (A.dbg && lane == 0 && warp == 0) dbg_max(A, 7, gtime());
-    }
-
-    // ---- main loop: private TMA ring, CTA barriers only in collectives
-    cyc_loop0 = A.dbg ? clock64() : 0;
-    cyc_wait = 0; cyc_proc = 0;
-    u64 g_pre = 0ull;
-    int rq = warp % max(nslots, 1);
-    int st = 1 % S;
-    uint32_t par = S == 1 ? 1u : 0u;
-    int64_t t = gw + GW;
-    for (int i = 1;; ++i) {
-        // cross-CTA threshold refresh every 4th tile, loaded one tile ahead
-        if ((i & 7) == 1 && lane == 0 && nslots > 0) g_pre = __ldcg(&A.gthr[rq]);
-        if (!tile(t, st, par, nullptr, nullptr)) break;
-        t += GW;
-        if (++st == S) { st = 0; par ^= 1u; }
-        if ((i & 7) == 6 && lane == 0 && nslots > 0) {
-            if (g_pre) raise_thr(rq, g_pre);
-            rq += kSWarps;
-            if (rq >= nslots) rq -= nslots * (rq / nslots);
-        }
-        if (bm && i == 3)
-            for (int q = warp; q < nslots; q += kSWarps) board_refresh(q);
         if (flag_set()) collective();
-    }
-    if (lane == 0) dbg_max(A, 2, A.dbg ? gtime() : 0ull);
-#ifdef EWSJF_CYCLES
-    if (lane == 0 && A.dbg) {   // per-CTA sums over warps (cycles): TMA waits, tile processing, loop total
-        atomicAdd(&A.dbg[blockIdx.x * 16 + 10], (unsigned long long)cyc_wait);
-        atomicAdd(&A.dbg[blockIdx.x * 16 + 11], (unsigned long long)cyc_proc);
-        atomicAdd(&A.dbg[blockIdx.x * 16 + 12], (unsigned long long)(clock64() - cyc_loop0));
-        atomicAdd(&A.dbg[blockIdx.x * 16 + 13], (unsigned long long)cyc_tile);
-        atomicAdd(&A.dbg[blockIdx.x * 16 + 14], (unsigned long long)cyc_ref);
-        atomicAdd(&A.dbg[blockIdx.x * 16 + 15], (unsigned long long)(cyc_board * 65536 + cyc_flag / 16));
-    }
-#endif
-    // done streaming: keep serving collectives until every warp is done.  A
-    // flag raised by this warp is visible before its ndone increment, and
-    // ndone is read before the flag, so no warp leaves while one is pending.
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) atomicAdd(&M->ndone, 1);
-    for (;;) {
-        int f = 0, d = 0;
-        if (lane == 0) {
-            d = *(volatile int*)&M->ndone;
-            __threadfence_block();
-            f = *(volatile int*)&M->flag;
-        }
-        f = __shfl_sync(0xffffffffu, f, 0);
-        d = __shfl_sync(0xffffffffu, d, 0);
-        if (f) { collective(); continue; }
-        if (d == kSWarps) break;
-        __nanosleep(64);
     }
     __syncthreads();
     if (tid == 0) dbg_max(A, 3, A.dbg ? gtime() : 0ull);

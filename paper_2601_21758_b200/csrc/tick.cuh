@@ -137,6 +137,7 @@ struct MergeArgs {
     BubbleLog* blog;
     int32_t* qid;               // gap requests' qid write-back (local pool)
     u64* gthr;                  // zeroed for the next call
+    unsigned long long* dbg;    // nullable: phase timestamps (EWSJF_PHASES)
 };
 
 }  // namespace ewsjf
