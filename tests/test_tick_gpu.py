@@ -265,3 +265,38 @@ def test_tick_full_size_c3(E, orc, ctx_full, mode):
     pool = workload.pool("heavy", 10_000_000, 302)
     g, ref, phi = _run_both(E, orc, ctx_full, pool, opart, 64, mode)
     _check(g, ref, phi, pool, mode, 64)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_sharded_tick_records_on_one_gpu(E, orc, ctx, heavy_parts, world, mode):
+    """The multi-GPU path with the all-gather replaced by a plain
+    concatenation on one device: every shard runs ewsjf_tick_local (route + score
+    + local top-K -> exchange record, global ids), the records of all shards are
+    merged by ewsjf_tick_merge; the result equals the oracle tick over the whole
+    pool (world-size invariance), qids of each shard included."""
+    import torch
+    pool = workload.pool("heavy", 300_001, 311)
+    n = len(pool["len"])
+    opart = heavy_parts["rp"]
+    K = 32
+    theta, sp = E.meta(**THETA0), E.select_params(k=K, mode=mode)
+    dev = {k: torch.from_numpy(pool[k]).cuda() for k in ("len", "arrival", "cost")}
+    qid = torch.full((n,), -7, dtype=torch.int32, device="cuda")
+    recs, bounds = [], []
+    for r in range(world):
+        lo, hi = workload.shard_range(n, r, world)
+        bounds.append((lo, hi))
+        recs.append(E.tick_local(ctx, dev["len"][lo:hi], dev["arrival"][lo:hi], dev["cost"][lo:hi], lo,
+                                 to_gpu_partition(E, opart), theta, sp, qid_out=qid[lo:hi]).clone())
+    allx = torch.cat(recs)
+    ref = orc.tick(pool["len"], pool["arrival"], pool["cost"], opart, orc.meta(**THETA0),
+                   orc.select_params(k=K, mode=mode))
+    phi, _ = orc.score_all(pool["len"], pool["arrival"], pool["cost"], ref["qid"], ref["partition"],
+                           orc.meta(**THETA0), orc.select_params(k=K, mode=mode))
+    for r, (lo, hi) in enumerate(bounds):      # every "rank" merges the same records
+        gp = to_gpu_partition(E, opart)
+        out = E.tick_merge(ctx, allx, world, lo, hi - lo, qid[lo:hi], gp, theta, sp)
+        g = gpu_result(out)
+        compare_selection(g, ref, phi, pool["arrival"], mode, K)
+    np.testing.assert_array_equal(qid.cpu().numpy(), ref["qid"])
