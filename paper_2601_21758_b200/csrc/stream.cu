@@ -59,7 +59,7 @@ __host__ __device__ inline StreamSmem stream_layout(bool has_cost, int lut_size,
     int64_t o = 0;
     L.ring = o;  o += (int64_t)kSWarps * stages * L.narr * kWT * 4;
     L.bars = o;  o = sal16(o + 8LL * kSWarps * stages);
-    L.w4 = o;    o = sal16(o + 16LL * kSTab);
+    L.w4 = o;    o = sal16(o + 32LL * kSTab);    // per-code record {wb, wu, wf, thrf, secf, qid, -, -}
     L.thr64 = o; o = sal16(o + 8LL * kSTab);
     L.sec = o;   o = sal16(o + 8LL * kSTab);
     L.thrhi = o; o = sal16(o + 4LL * kSTab);
@@ -249,13 +249,17 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
     unsigned char* lut = smem + L.lut;
     uint16_t* s_cnt16 = (uint16_t*)(smem + L.cnt);
     int* s_sid = (int*)(smem + L.sid);
-    float4* s_w4 = (float4*)(smem + L.w4);
+    // per-code record read with two 16-byte loads on the common path:
+    // .x/.y/.z = w_base, w_urg, w_fair·ln2; .w = fast filter; [+1].x = fast secondary, [+1].y = qid bits
+    float4* s_rec = (float4*)(smem + L.w4);
     u64* s_thr64 = (u64*)(smem + L.thr64);
     u32* s_thrhi = (u32*)(smem + L.thrhi);
     u64* s_sec = (u64*)(smem + L.sec);
     u32* s_sechi = (u32*)(smem + L.sechi);
-    float* s_thrf = (float*)(smem + L.thrf);   // fast filter: SCORE s' >= thrf, FIFO arrival <= thrf
-    float* s_secf = (float*)(smem + L.secf);   // fast secondary: SCORE arrival <= secf, FIFO s' >= secf
+    // fast filter (SCORE s' >= thrf, FIFO arrival <= thrf) and secondary (SCORE arrival <= secf,
+    // FIFO s' >= secf) live in the per-code record
+    auto thrf_at = [&](int q) -> float* { return (float*)(s_rec + 2 * q) + 3; };
+    auto secf_at = [&](int q) -> float* { return (float*)(s_rec + 2 * q + 1); };
     int* s_bcnt = (int*)(smem + L.bcnt);
     u64* s_buf = (u64*)(smem + L.buf);
     u64* s_ovfk = (u64*)(smem + L.ovfk);
@@ -324,12 +328,14 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
     __syncthreads();
     for (int i = tid; i < kSTab; i += kSThreads) {
         const bool v = i < nslots;
-        s_w4[i] = v ? make_float4(Ps->wb[i], Ps->wu[i], Ps->wf[i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float inf0 = __int_as_float(0x7f800000);
+        s_rec[2 * i] = v ? make_float4(Ps->wb[i], Ps->wu[i], Ps->wf[i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        s_rec[2 * i].w = MODE == EWSJF_SELECT_SCORE ? (v ? 0.f : inf0) : (v ? inf0 : -inf0);
+        s_rec[2 * i + 1] = make_float4(MODE == EWSJF_SELECT_SCORE ? (v ? inf0 : -inf0) : (v ? 0.f : inf0),
+                                       __int_as_float(v ? Ps->sid[i] : (i == kSCodeGap ? -2 : -1)), 0.f, 0.f);
         s_thr64[i] = 0ull; s_thrhi[i] = 0u; s_sec[i] = 0ull; s_sechi[i] = 0u; s_bcnt[i] = 0;
         // codes >= nslots never pass; qid table: gap -> -2, bad/none -> -1
         const float inf = __int_as_float(0x7f800000);
-        s_thrf[i] = MODE == EWSJF_SELECT_SCORE ? (v ? 0.f : inf) : (v ? inf : -inf);
-        s_secf[i] = MODE == EWSJF_SELECT_SCORE ? (v ? inf : -inf) : (v ? 0.f : inf);
         s_sid[i] = v ? Ps->sid[i] : (i == kSCodeGap ? -2 : -1);
     }
     if (tid == 0) dbg_max(A, 12, A.dbg ? gtime() : 0ull);
@@ -397,7 +403,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             atomicMax(&s_thr64[q], t);
             const u32 old = atomicMax(&s_thrhi[q], (u32)(t >> 32));
             const u32 hi = old > (u32)(t >> 32) ? old : (u32)(t >> 32);
-            *(volatile float*)&s_thrf[q] = hi_to_f(hi);
+            *(volatile float*)thrf_at(q) = hi_to_f(hi);
         }
     };
 
@@ -512,10 +518,16 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             code[j] = j < nv ? c : 0x1FF;
         }
         processed += nv;
+        float4 rw[4], rs[4];                      // per-code records (weights+filter, secondary+qid)
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            rw[j] = s_rec[2 * (code[j] & 0xFF)];
+            rs[j] = s_rec[2 * (code[j] & 0xFF) + 1];
+        }
         if (write_qid) {
             int qo[4];
 #pragma unroll
-            for (int j = 0; j < 4; j++) qo[j] = s_sid[code[j] & 0xFF];
+            for (int j = 0; j < 4; j++) qo[j] = __float_as_int(rs[j].y);
             if (nv == 4) {
                 __stcs((int4*)(A.qid_out + idx0), make_int4(qo[0], qo[1], qo[2], qo[3]));
             } else {
@@ -564,7 +576,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
         for (int j = 0; j < 4; j++) {
             const int c = code[j];
             const int ci = c & 0xFF;
-            const float4 w = s_w4[ci];
+            const float4 w = rw[j];
             const bool ok0 = score_sp(b[j], ar[j], HAS_COST ? co[j] : 0.0f, HAS_COST, A.sp, w.x, w.y, w.z, &sp[j]);
             const bool valid = c < kSCodeGap;
             const bool ok = valid && ok0;
@@ -573,8 +585,8 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             okm |= (unsigned)ok << j;
             const float f1 = MODE == EWSJF_SELECT_SCORE ? sp[j] : ar[j];
             const float f2 = MODE == EWSJF_SELECT_SCORE ? ar[j] : sp[j];
-            const bool p1 = MODE == EWSJF_SELECT_SCORE ? f1 >= s_thrf[ci] : f1 <= s_thrf[ci];
-            const bool p2 = MODE == EWSJF_SELECT_SCORE ? f2 <= s_secf[ci] : f2 >= s_secf[ci];
+            const bool p1 = MODE == EWSJF_SELECT_SCORE ? f1 >= w.w : f1 <= w.w;
+            const bool p2 = MODE == EWSJF_SELECT_SCORE ? f2 <= rs[j].x : f2 >= rs[j].x;
             pass1 |= (unsigned)(ok && p1) << j;
             pass2 |= (unsigned)(ok && p2) << j;
         }
@@ -624,7 +636,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
                     if (k2h >= old) {
                         atomicMax(&s_sec[q], ((u64)k2h << 32) | lo);
                         // the fast copy may lag (looser), never pass a tie by mistake: ties go to the exact max
-                        *(volatile float*)&s_secf[q] = MODE == EWSJF_SELECT_SCORE ? arj : spj;
+                        *(volatile float*)secf_at(q) = MODE == EWSJF_SELECT_SCORE ? arj : spj;
                     }
                 }
             }
