@@ -315,34 +315,38 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const __gri
             for (int u = 0; u < 4; u++) {
                 // register selects (no dynamic indexing of f / pass: they stay in registers)
                 const float4 fu = u == 0 ? f[0] : (u == 1 ? f[1] : (u == 2 ? f[2] : f[3]));
-                const unsigned pu = u == 0 ? pass[0] : (u == 1 ? pass[1] : (u == 2 ? pass[2] : pass[3]));
+                unsigned pu = u == 0 ? pass[0] : (u == 1 ? pass[1] : (u == 2 ? pass[2] : pass[3]));
                 const uint32_t gid = __float_as_uint(fu.w);
-                unsigned act = __reduce_or_sync(0xffffffffu, pu);     // Θ with a passing lane
-                while (act) {
-                    const int t = __ffs(act) - 1;
-                    act &= act - 1u;
+                // each lane inserts its own passing Θ (few bits; no warp-wide loop over Θ)
+                while (pu) {
+                    const int t = __ffs(pu) - 1;
+                    pu &= pu - 1u;
                     const float4 w = ws[t];
                     const float sc = fmaf(w.z, fu.z, fmaf(w.y, fu.y, w.x * fu.x));
                     const u64 key = score_key(sc, gid);
-                    const bool p = ((pu >> t) & 1u) && key >= th64[t];   // exact (s', ~id) test
-                    const unsigned m = __ballot_sync(0xffffffffu, p);
-                    if (!m) continue;
-                    u64* bt = buf + (size_t)t * cap;
-                    const int c0 = cnt[t];
-                    if (p) bt[c0 + __popc(m & ((1u << lane) - 1u))] = key;
-                    int c = c0 + __popc(m);
-                    d_ins += __popc(m);
-                    __syncwarp();
-                    if (c > cap - 32) {            // cut (a valid bound: >= K keys kept, few more); raise the filter
-                        const u64 kth = warp_kth_arr(bt, c, K, kApproxBit, K + (cap - 32 - K) / 4);
-                        d_cuts++;
-                        c = warp_keep_ge(bt, c, kth);
-                        if (lane == 0) {
-                            raise(t, kth);
-                            atomicMax(&A.s.gthr[(size_t)min(t0 + t, A.n_theta - 1) * kMaxSlots + q], kth);
-                        }
+                    if (key >= th64[t]) {                                   // exact (s', ~id) test
+                        buf[(size_t)t * cap + atomicAdd(&cnt[t], 1)] = key;  // <= 32 per t per step
+                        d_ins++;
                     }
-                    if (lane == 0) cnt[t] = c;
+                }
+                __syncwarp();
+                // cut the buffers that crossed cap - 32 (warp-uniform)
+                unsigned full = 0;
+                if (lane < kSwT) full = cnt[lane] > cap - 32;
+                full = __ballot_sync(0xffffffffu, full);
+                while (full) {
+                    const int t = __ffs(full) - 1;
+                    full &= full - 1u;
+                    u64* bt = buf + (size_t)t * cap;
+                    int c = cnt[t];
+                    const u64 kth = warp_kth_arr(bt, c, K, kApproxBit, K + (cap - 32 - K) / 4);
+                    d_cuts++;
+                    c = warp_keep_ge(bt, c, kth);
+                    if (lane == 0) {
+                        raise(t, kth);
+                        atomicMax(&A.s.gthr[(size_t)min(t0 + t, A.n_theta - 1) * kMaxSlots + q], kth);
+                        cnt[t] = c;
+                    }
                     __syncwarp();
                 }
             }
@@ -369,6 +373,7 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const __gri
         }
         __syncwarp();
     }
+    d_ins = __reduce_add_sync(0xffffffffu, (unsigned)d_ins);     // inserts are per lane
     if (lane == 0 && (d_ins | d_cuts)) {
         atomicAdd(&A.s.bad[2], d_cuts);
         atomicAdd(&A.s.bad[3], d_ins);
@@ -632,7 +637,14 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
     CU(cudaGetLastError());
     const size_t sel_smem = (size_t)kSwWarps * kSwT * (A.cap * 8 + 16 + 8 + 4 + 4);
     const size_t mrg_smem = (size_t)kSwWarps * A.cap * 8;
-    CU(cudaFuncSetAttribute(sweep_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
+    // kernel attributes and occupancy are queried once per shared-memory size (host calls)
+    static thread_local size_t s_attr_smem = 0;
+    static thread_local int s_occ = 1;
+    if (s_attr_smem != sel_smem) {
+        CU(cudaFuncSetAttribute(sweep_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s_occ, sweep_select_kernel, kSwWarps * 32, sel_smem);
+        s_attr_smem = sel_smem;
+    }
     static thread_local SweepOutArgs O;
     for (int32_t b0 = 0; b0 < n_theta; b0 += kSwBatch) {
         const int nb = std::min(kSwBatch, n_theta - b0);
@@ -647,8 +659,7 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
             LaunchScope ls(ctx, KIND_SWEEP);
             sweep_weights_kernel<<<1, 256, 0, st>>>(A);
         }
-        int occ = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_select_kernel, kSwWarps * 32, sel_smem);
+        const int occ = s_occ;
         for (int ph = 0; ph < 2; ph++) {
             A.phase = ph;
             CU(cudaMemsetAsync(S->task_ctr, 0, 4, st));
