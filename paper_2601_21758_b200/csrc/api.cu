@@ -81,6 +81,9 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
               cudaMalloc(&ctx->board, nrow * 8 * sizeof(u64)) == cudaSuccess &&
               cudaMalloc(&ctx->ctr, sizeof(Counters)) == cudaSuccess &&
               cudaMalloc(&ctx->dbg, (size_t)G * 16 * 8) == cudaSuccess &&
+              cudaMalloc(&ctx->d_lut, kLutCap + 32) == cudaSuccess &&
+              cudaMallocHost(&ctx->h_lut, kLutCap + 32) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->lut_ev, cudaEventDisableTiming) == cudaSuccess &&
               cudaMalloc(&ctx->gap, (size_t)ctx->gap_cap * sizeof(GapEntry)) == cudaSuccess &&
               cudaMalloc(&ctx->d_blog, sizeof(BubbleLog)) == cudaSuccess &&
               cudaMallocHost(&ctx->h_blog, sizeof(BubbleLog)) == cudaSuccess &&
@@ -123,7 +126,9 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
     if (!ctx) return EWSJF_OK;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    void* d[] = {ctx->dbg, ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
+    if (ctx->h_lut) cudaFreeHost(ctx->h_lut);
+    if (ctx->lut_ev) cudaEventDestroy(ctx->lut_ev);
+    void* d[] = {ctx->d_lut, ctx->dbg, ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
                  ctx->d_blog, ctx->d_summary, ctx->d_len, ctx->d_arr, ctx->d_cost, ctx->d_qid, ctx->d_topk_id,
                  ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score, ctx->d_max_score};
     for (void* p : d)
@@ -262,6 +267,31 @@ static ScoreParams score_params(const ewsjf_select_params* sp) {
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
+// The streaming tick's length -> position byte LUT (lut[0] = bad, holes and
+// lut[lutsz] = gap), built on the host and uploaded when the bounds change.
+static ewsjf_status ensure_lut(ewsjf_ctx* ctx, const ewsjf_partition_t* part, int lutsz) {
+    std::vector<int32_t> key;
+    key.reserve(2 * part->n);
+    for (int i = 0; i < part->n; i++) { key.push_back(part->q[i].min_len); key.push_back(part->q[i].max_len); }
+    if (ctx->lut_n == part->n && ctx->lut_size == lutsz && key == ctx->lut_bounds) return EWSJF_OK;
+    CU(cudaEventSynchronize(ctx->lut_ev));          // the staging buffer is free again
+    unsigned char* h = ctx->h_lut;
+    const int padded = (lutsz + 1 + 15) & ~15;
+    memset(h, 0xFE, padded);
+    for (int q = 0; q < part->n; q++) {
+        const int lo = part->q[q].min_len, hi = std::min(part->q[q].max_len, lutsz);
+        for (int b = std::max(lo, 0); b < hi; b++) h[b] = (unsigned char)q;
+    }
+    h[0] = 0xFF;
+    h[lutsz] = 0xFE;
+    CU(cudaMemcpyAsync(ctx->d_lut, h, padded, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaEventRecord(ctx->lut_ev, ctx->stream));
+    ctx->lut_n = part->n;
+    ctx->lut_size = lutsz;
+    ctx->lut_bounds = key;
+    return EWSJF_OK;
+}
+
 // Run the partial pass(es) of a tick / score_select / route over [len, n).
 static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, const float* d_cost,
                                 const int32_t* d_qid_in, int32_t* d_qid_out, int64_t n, int64_t gbase,
@@ -325,6 +355,8 @@ static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const floa
         if (scap >= K + 64 && stream_smem_bytes(has_cost, A.lut_size, nslots, scap, stages) <= budget) {
             A.cap = scap;
             A.hwm = scap - 32;
+            if (ensure_lut(ctx, part, A.lut_size) != EWSJF_OK) return EWSJF_ERR_CUDA;
+            A.lut_dev = ctx->d_lut;
             A.dbg = getenv("EWSJF_PHASES") ? ctx->dbg : nullptr;
             if (getenv("EWSJF_STREAM_ONLY")) A.pass0 = 7;   // timing experiment only (wrong results)
             if (const char* e = getenv("EWSJF_EXP")) A.pass0 = atoi(e);   // timing experiments only (wrong results)

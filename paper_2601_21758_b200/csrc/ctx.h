@@ -30,6 +30,13 @@ struct ewsjf_ctx {
     Counters* ctr = nullptr;
     GapEntry* gap = nullptr;
     unsigned long long* dbg = nullptr;   // [num_sms][16] phase timestamps
+    // length -> queue-position byte LUT of the last partition routed (stream.cu),
+    // rebuilt on the host and uploaded only when the queue bounds change
+    unsigned char* d_lut = nullptr;     // device, kLutCap + 32 bytes
+    unsigned char* h_lut = nullptr;     // pinned staging
+    cudaEvent_t lut_ev = nullptr;       // last upload
+    int32_t lut_n = -1, lut_size = 0;
+    std::vector<int32_t> lut_bounds;    // min/max of the cached partition
     int32_t gap_cap = 8192;
     BubbleLog* d_blog = nullptr;
     BubbleLog* h_blog = nullptr;        // pinned

@@ -339,7 +339,12 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
         s_sid[i] = v ? Ps->sid[i] : (i == kSCodeGap ? -2 : -1);
     }
     if (tid == 0) dbg_max(A, 12, A.dbg ? gtime() : 0ull);
-    {
+    if (A.lut_dev) {
+        // the prebuilt LUT (ctx cache, 16-byte padded): four 16-byte loads per thread
+        const int n16 = (lutsz + 1 + 15) / 16;
+        const int4* src = reinterpret_cast<const int4*>(A.lut_dev);
+        for (int i = tid; i < n16; i += kSThreads) ((int4*)lut)[i] = __ldg(src + i);
+    } else {
         // byte LUT length -> queue position, built a word (4 lengths) at a time:
         // each thread walks a contiguous run of words through the sorted,
         // disjoint [min_len, max_len) intervals.
@@ -382,6 +387,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             }
         }
     }
+
     if (tid == 0) dbg_max(A, 13, A.dbg ? gtime() : 0ull);
     __syncthreads();
     if (tid == 0) dbg_max(A, 1, gtime());

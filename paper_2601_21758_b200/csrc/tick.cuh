@@ -51,6 +51,7 @@ struct PartialArgs {
     int32_t pass0;              // counts, qid, gaps, counters
     int32_t select;             // 0 = route only
     int32_t lut_size;           // LUT covers lengths [0, lut_size); 0 = binary search
+    const unsigned char* lut_dev;   // stream.cu: prebuilt byte LUT (ctx cache, 16-byte padded) or null
     int32_t stages;             // stream.cu: TMA ring depth per warp
     ScoreParams sp;
     Rows rows;
