@@ -312,32 +312,34 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
         }
     }
 
-    // ---- policy tables -> smem while the first tiles are in flight.  The
-    // Policy kernel parameter is first copied with one coalesced 16-byte load
-    // per thread into the (still empty) candidate-buffer area, so no thread
-    // makes divergent constant-bank loads.
+    // ---- policy tables -> smem while the first tiles are in flight.  Only the
+    // fields the stream reads are loaded from the Policy parameter (one code per
+    // thread); the whole Policy is staged in shared memory only when the LUT has
+    // to be built here (no prebuilt LUT).
     const Policy* Ps = (const Policy*)s_buf;
     {
-        const int n16 = (int)((sizeof(Policy) + 15) / 16);
-        const int4* src = reinterpret_cast<const int4*>(&P);
-        for (int i = tid; i < (A.pass0 == 6 ? 0 : n16); i += kSThreads) ((int4*)s_buf)[i] = src[i];
+        if (!A.lut_dev) {
+            const int n16 = (int)((sizeof(Policy) + 15) / 16);
+            const int4* src = reinterpret_cast<const int4*>(&P);
+            for (int i = tid; i < n16; i += kSThreads) ((int4*)s_buf)[i] = src[i];
+        }
         uint32_t* c32 = (uint32_t*)s_cnt16;
         for (int i = tid; i < kSThreads * (nslots + 2) / 2; i += kSThreads) c32[i] = 0u;
     }
     if (tid == 0) { M->flag = 0; M->novf = 0; M->ndone = 0; }
-    __syncthreads();
     for (int i = tid; i < kSTab; i += kSThreads) {
         const bool v = i < nslots;
         const float inf0 = __int_as_float(0x7f800000);
-        s_rec[2 * i] = v ? make_float4(Ps->wb[i], Ps->wu[i], Ps->wf[i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
-        s_rec[2 * i].w = MODE == EWSJF_SELECT_SCORE ? (v ? 0.f : inf0) : (v ? inf0 : -inf0);
+        const int sid = v ? P.sid[i] : (i == kSCodeGap ? -2 : -1);   // qid table: gap -> -2, bad/none -> -1
+        // codes >= nslots never pass the filters
+        s_rec[2 * i] = make_float4(v ? P.wb[i] : 0.f, v ? P.wu[i] : 0.f, v ? P.wf[i] : 0.f,
+                                   MODE == EWSJF_SELECT_SCORE ? (v ? 0.f : inf0) : (v ? inf0 : -inf0));
         s_rec[2 * i + 1] = make_float4(MODE == EWSJF_SELECT_SCORE ? (v ? inf0 : -inf0) : (v ? 0.f : inf0),
-                                       __int_as_float(v ? Ps->sid[i] : (i == kSCodeGap ? -2 : -1)), 0.f, 0.f);
+                                       __int_as_float(sid), 0.f, 0.f);
         s_thr64[i] = 0ull; s_thrhi[i] = 0u; s_sec[i] = 0ull; s_sechi[i] = 0u; s_bcnt[i] = 0;
-        // codes >= nslots never pass; qid table: gap -> -2, bad/none -> -1
-        const float inf = __int_as_float(0x7f800000);
-        s_sid[i] = v ? Ps->sid[i] : (i == kSCodeGap ? -2 : -1);
+        s_sid[i] = sid;
     }
+    __syncthreads();
     if (tid == 0) dbg_max(A, 12, A.dbg ? gtime() : 0ull);
     if (A.lut_dev) {
         // the prebuilt LUT (ctx cache, 16-byte padded): four 16-byte loads per thread
