@@ -358,8 +358,6 @@ static ewsjf_status run_partial(ewsjf_ctx* ctx, const int32_t* d_len, const floa
             if (ensure_lut(ctx, part, A.lut_size) != EWSJF_OK) return EWSJF_ERR_CUDA;
             A.lut_dev = ctx->d_lut;
             A.dbg = getenv("EWSJF_PHASES") ? ctx->dbg : nullptr;
-            if (getenv("EWSJF_STREAM_ONLY")) A.pass0 = 7;   // timing experiment only (wrong results)
-            if (const char* e = getenv("EWSJF_EXP")) A.pass0 = atoi(e);   // timing experiments only (wrong results)
             // cross-CTA board: bm keys per (queue, CTA), G*bm <= 320 and >= K
             A.board = ctx->board;
             A.board_m = std::min(2, 320 / std::max(ctx->num_sms, 1));

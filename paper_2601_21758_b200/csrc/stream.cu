@@ -350,7 +350,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
         // byte LUT length -> queue position, built a word (4 lengths) at a time:
         // each thread walks a contiguous run of words through the sorted,
         // disjoint [min_len, max_len) intervals.
-        const int nw = A.pass0 == 5 ? 0 : (lutsz + 1 + 3) / 4;   // lut[0..lutsz], lut[lutsz] = gap
+        const int nw = (lutsz + 1 + 3) / 4;   // lut[0..lutsz], lut[lutsz] = gap
         const int wpt = (nw + kSThreads - 1) / kSThreads;
         const int w0 = tid * wpt, w1 = min(nw, w0 + wpt);
         if (w0 < w1) {
@@ -393,8 +393,6 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
     if (tid == 0) dbg_max(A, 13, A.dbg ? gtime() : 0ull);
     __syncthreads();
     if (tid == 0) dbg_max(A, 1, gtime());
-    if (lane_ring && A.pass0 == 4)
-        for (int s = 0; s < S; s++) issue_lane(gw + s * GW, s);
 
     unsigned exc = 0, nins = 0, ngap = 0, ncomp = 0, ndrop = 0, excl_total = 0;
     long long cyc_wait = 0, cyc_proc = 0, cyc_loop0 = 0, cyc_ref = 0, cyc_board = 0, cyc_flag = 0, cyc_tile = 0;   // EWSJF_PHASES cycle accounting
@@ -598,7 +596,6 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             pass1 |= (unsigned)(ok && p1) << j;
             pass2 |= (unsigned)(ok && p2) << j;
         }
-        if (A.pass0 == 7) { pass1 = 0; pass2 = 0; }   // timing experiment: streaming only
         if (r1k) {
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -728,7 +725,6 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
             const bool first = i == 0;
             const bool more = tile(t, st, par, first ? r1k : nullptr, first ? r1q : nullptr);
             if (first) {
-            if (A.pass0 == 7) for (int j = 0; j < 4; j++) r1q[j] = -1;
             __syncthreads();
             if (tid == 0) dbg_max(A, 13, A.dbg ? gtime() : 0ull);   // all first tiles done
             // per-queue totals and per-thread exclusive prefixes (lane l: threads 16l..16l+15)
