@@ -93,6 +93,10 @@ class SelectOut(C.Structure):
 _lib = None
 
 
+class Budget(C.Structure):
+    _fields_ = [("max_requests", C.c_int32), ("max_tokens", C.c_int64)]
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -125,6 +129,11 @@ def lib():
                               C.c_int32, P(Meta), P(SelectParams), P(C.c_int32), P(SelectOut)]
         L.or_sweep.argtypes = [P(C.c_int32), P(C.c_float), P(C.c_float), P(C.c_int32), C.c_int64, C.c_int64,
                                P(Partition), P(Meta), C.c_int32, P(SelectParams), P(SelectOut)]
+        L.or_batch.restype = C.c_int64
+        L.or_batch.argtypes = [P(C.c_int32), P(C.c_float), P(C.c_float), P(C.c_int32), C.c_int64, C.c_int64,
+                               P(Partition), P(SelectParams), C.c_int32, P(Budget), P(C.c_int64), P(C.c_int64)]
+        L.or_prune_empty.restype = C.c_int32
+        L.or_prune_empty.argtypes = [P(Partition), P(C.c_int32), P(C.c_int64), C.c_int32]
     return _lib
 
 
@@ -352,3 +361,26 @@ def tick(lengths, arrival, cost, part: Partition, theta: Meta, sp: SelectParams,
     res = o.result(p2.n, sp.k, s, p2)
     res["qid"] = qid[: len(x)]
     return res
+
+
+def batch(lengths, arrival, cost, qid, part: Partition, sp: SelectParams, primary: int, max_requests: int,
+          max_tokens: int, global_base=0):
+    """O12: Alg. 1's Batch Builder (GreedyFill + Backfill) over a routed pool -> (ids, tokens)."""
+    x = _i32(lengths); a = _f32(arrival); q = _i32(qid)
+    cst = _f32(cost) if cost is not None else None
+    ids = np.full(max(max_requests, 1), -1, np.int64)
+    tok = C.c_int64(0)
+    b = Budget(max_requests, max_tokens)
+    nb = lib().or_batch(_p(x, C.c_int32), _p(a, C.c_float), _p(cst, C.c_float) if cst is not None else None,
+                        _p(q, C.c_int32), len(x), global_base, C.byref(part), C.byref(sp), primary, C.byref(b),
+                        _p(ids, C.c_int64), C.byref(tok))
+    return ids[:nb], tok.value
+
+
+def prune_empty(part: Partition, empty_cnt, counts, threshold: int):
+    """Alg. 1 lines 8-12 on a copy of ``part``: (new partition, new empty counters, removed)."""
+    p2 = copy_partition(part)
+    e = np.ascontiguousarray(np.asarray(empty_cnt, np.int32).copy())
+    c = np.ascontiguousarray(np.asarray(counts, np.int64))
+    removed = lib().or_prune_empty(C.byref(p2), _p(e, C.c_int32), _p(c, C.c_int64), threshold)
+    return p2, e[: p2.n], removed

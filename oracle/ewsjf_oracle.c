@@ -510,3 +510,91 @@ int or_sweep(const int32_t *len, const float *arrival, const float *cost, const 
     }
     return status;
 }
+
+/* ---------------------------------------------------------------- O12 --- */
+typedef struct { float arrival; int64_t r; } fkey;
+static int cmp_fkey(const void *a, const void *b) {
+    const fkey *x = (const fkey *)a, *y = (const fkey *)b;
+    if ((double)x->arrival < (double)y->arrival) return -1;
+    if ((double)x->arrival > (double)y->arrival) return 1;
+    return x->r < y->r ? -1 : (x->r > y->r);
+}
+
+/* Pull queue p's members in FIFO order while the budget admits them (Alg. 1
+ * GreedyFill / Backfill body; S:324 (3)-(4); first request of the batch always
+ * admitted). */
+static void pull_fifo(const fkey *mem, int64_t m, const int32_t *len, int64_t global_base, const or_budget *bd,
+                      int64_t *batch_ids, int64_t *nb, int64_t *tok) {
+    for (int64_t t = 0; t < m; t++) {
+        if (*nb >= bd->max_requests) return;
+        const int64_t b = len[mem[t].r];
+        if (*nb > 0 && *tok + b > bd->max_tokens) return;     /* stop at the first that does not fit (R28) */
+        batch_ids[(*nb)++] = global_base + mem[t].r;
+        *tok += b;
+    }
+}
+
+int64_t or_batch(const int32_t *len, const float *arrival, const float *cost, const int32_t *qid,
+                 int64_t n, int64_t global_base, const or_partition *part, const or_select_params *sp,
+                 int32_t primary, const or_budget *budget, int64_t *batch_ids, int64_t *batch_tokens) {
+    int32_t nq = part->n;
+    *batch_tokens = 0;
+    if (primary < 0 || primary >= nq || budget->max_requests < 1) return 0;
+    idpos map[OR_MAXQ];
+    for (int32_t i = 0; i < nq; i++) { map[i].id = part->q[i].id; map[i].pos = i; }
+    qsort(map, (size_t)nq, sizeof(idpos), cmp_idpos);
+    /* members per position: what O9 scores (the weights do not matter for validity) */
+    const float w0[3] = {1.0f, 0.0f, 0.0f};
+    int64_t *cnt = (int64_t *)calloc((size_t)nq + 1, sizeof(int64_t));
+    int32_t *pos = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t r = 0; r < n; r++) {
+        pos[r] = -1;
+        if (qid[r] < 0 || len[r] < 1) continue;
+        int32_t a = 0, b = nq;
+        while (a < b) { int32_t mid = (a + b) / 2; if (map[mid].id < qid[r]) a = mid + 1; else b = mid; }
+        if (a >= nq || map[a].id != qid[r]) continue;
+        double f;
+        if (or_score_one(len[r], arrival[r], cost ? &cost[r] : NULL, 1, w0, sp, &f)) continue;
+        pos[r] = map[a].pos;
+        cnt[pos[r]]++;
+    }
+    int64_t *start = (int64_t *)calloc((size_t)nq + 1, sizeof(int64_t));
+    for (int32_t p = 0; p < nq; p++) start[p + 1] = start[p] + cnt[p];
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * ((size_t)nq + 1));
+    memcpy(fill, start, sizeof(int64_t) * ((size_t)nq + 1));
+    fkey *mem = (fkey *)malloc(sizeof(fkey) * (size_t)(start[nq] > 0 ? start[nq] : 1));
+    for (int64_t r = 0; r < n; r++)
+        if (pos[r] >= 0) { fkey k; k.arrival = arrival[r]; k.r = r; mem[fill[pos[r]]++] = k; }
+    for (int32_t p = 0; p < nq; p++) qsort(mem + start[p], (size_t)cnt[p], sizeof(fkey), cmp_fkey);
+
+    int64_t nb = 0, tok = 0;
+    /* GreedyFill from the primary queue (Alg. 1 line 16) */
+    pull_fifo(mem + start[primary], cnt[primary], len, global_base, budget, batch_ids, &nb, &tok);
+    /* Backfill from adjacent queues, nearest index first, lower neighbour first (lines 17-19) */
+    for (int32_t d = 1; d < nq && nb < budget->max_requests; d++) {
+        const int32_t cand[2] = {primary - d, primary + d};
+        for (int c = 0; c < 2 && nb < budget->max_requests; c++) {
+            const int32_t p = cand[c];
+            if (p < 0 || p >= nq) continue;
+            pull_fifo(mem + start[p], cnt[p], len, global_base, budget, batch_ids, &nb, &tok);
+        }
+    }
+    *batch_tokens = tok;
+    free(cnt); free(pos); free(start); free(fill); free(mem);
+    return nb;
+}
+
+int32_t or_prune_empty(or_partition *part, int32_t *empty_cnt, const int64_t *count, int32_t threshold) {
+    int32_t k = 0, removed = 0;
+    for (int32_t p = 0; p < part->n; p++) {
+        int32_t e = empty_cnt[p];
+        if (count[p] == 0) e++;                          /* Alg. 1 line 9 (no reset, R30) */
+        if (e > threshold) { removed++; continue; }       /* lines 10-11, strict (R25) */
+        part->q[k] = part->q[p];
+        part->q[k].index = k + 1;                         /* renumber */
+        empty_cnt[k] = e;
+        k++;
+    }
+    part->n = k;
+    return removed;
+}

@@ -23,6 +23,7 @@
  *   O9 Eq. 1 / Eq. 4 score                            (R2-R5)
  *   O10 per-queue count, FIFO head, top-K, argmax     (Alg. 1; R1, R24, R26)
  *   O11 Θ sweep: O7 -> O9 -> O10 per Θ                (§4.4.2)
+ *   O12 Alg. 1 Batch Builder + empty-queue pruning    (R28-R30)
  *
  * Parity unpinned (no paper-printed value exists):
  *   the C_prefill quadratic and its defaults (SPEC invention), the
@@ -172,6 +173,28 @@ int     or_sweep(const int32_t *len, const float *arrival, const float *cost, co
                  int64_t n, int64_t global_base, const or_partition *part,
                  const or_meta *thetas, int32_t n_theta, const or_select_params *sp,
                  or_select_out *outs);
+
+/* O12: Alg. 1 lines 14-21, the Batch Builder (P:163,
+ * P:178-193) over a routed pool.  Members of a queue are
+ * the requests O9 scores (valid qid, len >= 1, W >= 0, C > 0), FIFO by
+ * (arrival, id).  GreedyFill: from queue `primary` (position, the O10 ArgMax)
+ * pull members in FIFO order while the budget admits them (count <
+ * max_requests and tokens + len <= max_tokens; the batch's first request is
+ * always admitted), stopping at the first one that does not fit
+ * (R28).  Backfill (if the batch is not full): queues at position distance
+ * 1, 2, ... from the primary, lower neighbour first (R29), each pulled
+ * FIFO while the budget admits.  Writes batch ids (global) in pull order.
+ * Returns the batch size. */
+typedef struct { int32_t max_requests; int64_t max_tokens; } or_budget;
+int64_t or_batch(const int32_t *len, const float *arrival, const float *cost, const int32_t *qid,
+                 int64_t n, int64_t global_base, const or_partition *part, const or_select_params *sp,
+                 int32_t primary, const or_budget *budget, int64_t *batch_ids, int64_t *batch_tokens);
+
+/* Alg. 1 lines 8-12: every queue with count[p] == 0 increments its empty
+ * counter (no reset, R30); a queue whose counter exceeds `threshold` (strict,
+ * R25) is removed and the remaining indices renumbered.  empty_cnt[p] is
+ * in/out by position (compacted like the queues).  Returns queues removed. */
+int32_t or_prune_empty(or_partition *part, int32_t *empty_cnt, const int64_t *count, int32_t threshold);
 
 #ifdef __cplusplus
 }

@@ -553,3 +553,105 @@ def test_sweep_special_cases_reduce_to_sorts(orc):
         np.testing.assert_array_equal(res[3]["topk_score"][p], 2 * res[2]["topk_score"][p])
         assert res[3]["head_score"][p] == 2 * res[2]["head_score"][p]
     assert res[1]["primary"] == 0                       # all head scores 0 -> lowest position (R24)
+
+
+# ------------------------------------------------ O12: Alg. 1 Batch Builder ---
+def _bpool(orc, specs, now=100.0):
+    """specs: [(len, arrival)], routed onto queues [1,100) [100,200) [200,300)."""
+    part = orc.make_partition([(1, 100), (100, 200), (200, 300)])
+    lens = np.array([b for b, _ in specs], np.int32)
+    arr = np.array([a for _, a in specs], np.float32)
+    s, qid, *_ = orc.route(lens, orc.copy_partition(part), 64)
+    return part, lens, arr, qid, orc.select_params(k=8, mode=1, now=now)
+
+
+def test_batch_spec_examples(orc):
+    """all empty -> empty batch; one queue, 3 fitting requests -> those 3
+    in FIFO order; primary's single request uses half the token budget and the
+    neighbour has 2 fitting requests -> 3, neighbour's appended."""
+    part, lens, arr, qid, sp = _bpool(orc, [])
+    ids, tok = orc.batch(lens, arr, None, qid, part, sp, -1, 8, 1000)
+    assert list(ids) == [] and tok == 0
+    p2, e, removed = orc.prune_empty(part, [0, 0, 0], [0, 0, 0], 5)
+    assert list(e) == [1, 1, 1] and removed == 0
+    part, lens, arr, qid, sp = _bpool(orc, [(50, 3.0), (60, 1.0), (70, 2.0)])
+    ids, tok = orc.batch(lens, arr, None, qid, part, sp, 0, 8, 1000)
+    assert list(ids) == [1, 2, 0] and tok == 180          # FIFO by arrival
+    part, lens, arr, qid, sp = _bpool(orc, [(150, 1.0), (40, 2.0), (30, 3.0)])
+    ids, tok = orc.batch(lens, arr, None, qid, part, sp, 1, 8, 300)   # 150 = half of 300
+    assert list(ids) == [0, 1, 2] and tok == 220
+
+
+def test_batch_first_request_always_admitted_and_fifo_stop(orc):
+    """the batch's first request is admitted even above max_tokens; a queue
+    is pulled while the budget admits (R28: stop at the first that does not fit,
+    no skipping ahead in its FIFO)."""
+    part, lens, arr, qid, sp = _bpool(orc, [(250, 1.0), (20, 2.0)])
+    ids, tok = orc.batch(lens, arr, None, qid, part, sp, 2, 8, 100)
+    assert list(ids) == [0] and tok == 250                # oversized first request alone
+    part, lens, arr, qid, sp = _bpool(orc, [(10, 1.0), (90, 2.0), (5, 3.0), (120, 4.0)])
+    ids, tok = orc.batch(lens, arr, None, qid, part, sp, 0, 8, 50)
+    # primary [10, 90, 5]: 10 fits, 90 does not -> stop (5 is not taken); backfill
+    # queue 1 (distance 1, no lower neighbour): 120 does not fit
+    assert list(ids) == [0] and tok == 10
+
+
+def test_batch_backfill_nearest_lower_first_and_caps(orc):
+    """R29: backfill visits index distance 1, 2, ..., lower neighbour
+    first, FIFO within each queue; max_requests caps the batch."""
+    part = orc.make_partition([(1, 10), (10, 20), (20, 30), (30, 40), (40, 50)])
+    specs = [(45, 1.0), (35, 2.0), (25, 3.0), (15, 4.0), (5, 5.0), (26, 6.0), (14, 7.0), (44, 8.0)]
+    lens = np.array([b for b, _ in specs], np.int32)
+    arr = np.array([a for _, a in specs], np.float32)
+    s, qid, *_ = orc.route(lens, orc.copy_partition(part), 64)
+    sp = orc.select_params(k=8, mode=1, now=100.0)
+    ids, tok = orc.batch(lens, arr, None, qid, part, sp, 2, 16, 10_000)
+    # primary 2: [25(r2), 26(r5)]; d=1: queue 1 [15(r3), 14(r6)], queue 3 [35(r1)];
+    # d=2: queue 0 [5(r4)], queue 4 [45(r0), 44(r7)]
+    assert list(ids) == [2, 5, 3, 6, 1, 4, 0, 7]
+    assert tok == int(lens.sum())
+    ids, _ = orc.batch(lens, arr, None, qid, part, sp, 2, 3, 10_000)
+    assert list(ids) == [2, 5, 3]
+
+
+def test_batch_invariants_random(orc):
+    """Every queue contributes a FIFO prefix of its members; count <= max_requests;
+    tokens <= max_tokens unless the batch is one request; the primary's prefix is
+    maximal; members are exactly the scored requests (W >= 0)."""
+    import workload
+    rng = np.random.default_rng(12)
+    part = orc.make_partition(workload.quantile_bounds(workload.heavy(20_000, 3), 8))
+    for trial in range(30):
+        n = int(rng.integers(1, 400))
+        lens = workload.heavy(n, 100 + trial)
+        arr = (rng.random(n) * 120).astype(np.float32)         # some arrive after now: excluded
+        s, qid, *_ = orc.route(lens, orc.copy_partition(part), 64)
+        sp = orc.select_params(k=8, mode=1, now=100.0)
+        mr = int(rng.integers(1, 40)); mt = int(rng.integers(100, 20_000))
+        prim = int(rng.integers(0, part.n))
+        ids, tok = orc.batch(lens, arr, None, qid, part, sp, prim, mr, mt)
+        assert len(ids) <= mr and len(set(ids)) == len(ids)
+        assert tok == int(lens[ids].sum()) if len(ids) else tok == 0
+        assert tok <= mt or len(ids) == 1
+        pos = {part.q[i].id: i for i in range(part.n)}
+        for p in range(part.n):
+            mem = [r for r in range(n) if qid[r] >= 0 and pos[qid[r]] == p and arr[r] <= 100.0]
+            mem.sort(key=lambda r: (float(arr[r]), r))
+            got = [int(r) for r in ids if pos[qid[r]] == p]
+            assert got == mem[:len(got)], (trial, p)
+            if p == prim and len(got) < len(mem) and len(ids) < mr:
+                nxt = mem[len(got)]
+                prim_tok = int(lens[[r for r in ids if pos[qid[r]] == p]].sum())
+                assert prim_tok + int(lens[nxt]) > mt   # the next primary member did not fit
+
+
+def test_prune_empty_threshold_strict_and_renumbers(orc):
+    """Alg. 1 lines 8-12: empty queues count up (no reset, R30); removal when the
+    counter exceeds the threshold (strict, R25); indices renumbered."""
+    part = orc.make_partition([(1, 10), (10, 20), (20, 30), (30, 40)])
+    e = [5, 0, 4, 5]
+    p2, e2, removed = orc.prune_empty(part, e, [0, 0, 0, 7], 5)
+    # queue 0: 5 -> 6 > 5 removed; queue 1: 0 -> 1; queue 2: 4 -> 5 kept; queue 3 non-empty: 5 kept
+    assert removed == 1
+    assert [(q["min_len"], q["index"]) for q in p2.queues()] == [(10, 1), (20, 2), (30, 3)]
+    assert list(e2) == [1, 5, 5]
