@@ -217,6 +217,36 @@ def run_sweep(E, ctx, dev, args):
             "candidates_inserted_last_sweep": tm["candidates_inserted"]}
 
 
+def run_batch(E, ctx, part, theta, copies, dev, n, max_req=256, max_tok=65536, reps=20):
+    """Alg. 1's Batch Builder after a FIFO-mode tick at the C3 size
+    (k = max_requests so every queue's pullable FIFO prefix is in its row)."""
+    import torch
+    sp = E.select_params(k=max_req, mode=1, now=workload.NOW)
+    out = E.Outputs.alloc(max_req, dev)
+    ids = torch.empty(max_req, dtype=torch.int64, device=dev)
+    info = torch.empty(4, dtype=torch.int64, device=dev)
+    ln, ar, co, q = copies[0]
+    s = E.tick(ctx, ln, ar, co, part, theta, sp, qid_out=q, out=out)
+    nq = s.summary["n_queues"]
+    for _ in range(3):
+        E.batch_build(ctx, ln, out, nq, max_req, max_tok, ids_out=ids, info_out=info)
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    for i in range(reps):
+        l2, a2, c2, q2 = copies[i % 3]
+        E.tick(ctx, l2, a2, c2, part, theta, sp, qid_out=q2, out=out, sync=False)
+        E.batch_build(ctx, l2, out, nq, max_req, max_tok, ids_out=ids, info_out=info)
+    torch.cuda.synchronize()
+    tm = ctx.timing()
+    inf = info.cpu().tolist()
+    return {"workload": f"FIFO tick (k={max_req}) over the C3 pool + Alg. 1 batch build "
+                        f"(max_requests={max_req}, max_tokens={max_tok})",
+            "batch_kernel_us": 1e3 * tm["batch_ms"] / max(tm["batch_launches"], 1),
+            "fifo_tick_kernel_ms": tm["tick_ms"] / max(tm["tick_launches"], 1),
+            "fifo_merge_kernel_ms": tm["merge_ms"] / max(tm["merge_launches"], 1),
+            "batch_size": inf[0], "batch_tokens": inf[1], "status": inf[2], "primary": inf[3]}
+
+
 def config_dict(args, opart_source):
     return {"workload": "C3: 10M pending requests per GPU, heavy-tailed lengths (80% lognormal(ln128,0.6) "
                         "32..2047, 20% Pareto(1.5) 2048..32768), route + score + per-queue top-k",
@@ -363,6 +393,10 @@ def main():
     # the GPU Refine-and-Prune partition of bimodal(1M, seed 201) (C2's partition)
     if not args.no_sweep and ws == 1:
         line["sweep"] = run_sweep(E, ctx, dev, args)
+    if ws == 1 and args.k <= 256:
+        bctx = E.Context(local, max_pool=n, max_history=0, max_k=256)
+        line["batch"] = run_batch(E, bctx, part, theta, copies, dev, n)
+        bctx.close()
 
     # ---- the oracle beside it (rank 0, N=1 only), bounded sample
     if not args.no_cpu_baseline and ws == 1 and rank == 0:

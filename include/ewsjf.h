@@ -84,6 +84,8 @@ typedef struct {
     double  tick_ms, merge_ms, partition_ms, sweep_ms;
     int64_t candidates_inserted;   /* diagnostics since ctx creation: keys that passed the  */
     int64_t compactions;           /* per-queue filters, and per-queue buffer compactions   */
+    int64_t batch_launches;        /* ewsjf_batch_build kernels                             */
+    double  batch_ms;
 } ewsjf_timing;
 ewsjf_status ewsjf_ctx_set_timing(ewsjf_ctx *ctx, int32_t enable);
 ewsjf_status ewsjf_ctx_get_timing(ewsjf_ctx *ctx, ewsjf_timing *out);
@@ -296,6 +298,43 @@ ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx *ctx, const int32_t *d_len, cons
                                       const ewsjf_partition_t *part, const ewsjf_meta *thetas,
                                       int32_t n_theta, const ewsjf_select_params *params,
                                       ewsjf_select_out *outs);
+
+/* ------------------------------------ Alg. 1 batch builder --- */
+/* Budget of one forward pass (BatchBudget). */
+typedef struct {
+    int32_t max_requests;  /* >= 1                                         */
+    int32_t pad;
+    int64_t max_tokens;    /* Σ prompt lengths, 0 <= max_tokens < 2^32 - 1  */
+} ewsjf_batch_budget;
+
+/* Alg. 1 lines 13-21: GreedyFill from the primary queue
+ * (sel->d_summary->primary, the ArgMax of the per-queue head scores) in FIFO
+ * order, stopping at the first request that does not fit (R28; the batch's
+ * first request is always admitted), then Backfill from the queues at
+ * index distance 1, 2, …, lower neighbour first, each FIFO under the same rule
+ * (R29), until max_requests or the queues run out.
+ * sel: the device outputs of a FIFO-mode selection (ewsjf_tick / ewsjf_score_select
+ *   with params.mode = EWSJF_SELECT_FIFO) with depth k >= max_requests (so every
+ *   queue's pullable FIFO prefix is in its row) over n_queues queue positions;
+ *   d_summary NULL -> the ctx summary the last selection wrote.
+ * d_len[n]: prompt lengths; the row ids are global_base + index into d_len.
+ * d_batch_id [max_requests] (device, caller-owned): batch request ids in
+ *   admission order, -1 padding.  d_batch_info [4] (device int64): batch size,
+ *   tokens, status (EWSJF_OK, or INVALID_ARG if a row id fell outside d_len),
+ *   primary position.  Async, one kernel on the ctx stream.  INVALID_ARG
+ *   (nothing launched) on null pointers, k < max_requests, max_tokens range. */
+ewsjf_status ewsjf_batch_build(ewsjf_ctx *ctx, const int32_t *d_len, int64_t n, int64_t global_base,
+                               const ewsjf_select_out *sel, int32_t k, int32_t n_queues,
+                               const ewsjf_batch_budget *budget, int64_t *d_batch_id, int64_t *d_batch_info);
+
+/* Alg. 1 lines 8-12: for every queue position p with h_count[p] == 0
+ * increment part->q[p].empty_count (never reset, R30); remove the queues whose
+ * counter exceeds `threshold` (strict, R25), renumber the survivors' index
+ * 1..n and bump part->version if any was removed.  Host-only (the
+ * partition is host state); *removed (nullable) = queues removed.  h_count is
+ * the d_count of the tick, copied to the host.                               */
+ewsjf_status ewsjf_prune_empty(ewsjf_partition_t *part, const int64_t *h_count, int32_t threshold,
+                               int32_t *removed);
 
 #ifdef __cplusplus
 }

@@ -75,10 +75,15 @@ class Timing(C.Structure):
     _fields_ = [("launches", C.c_int64), ("recorded", C.c_int64), ("tick_launches", C.c_int64),
                 ("merge_launches", C.c_int64), ("partition_launches", C.c_int64), ("sweep_launches", C.c_int64),
                 ("tick_ms", C.c_double), ("merge_ms", C.c_double), ("partition_ms", C.c_double),
-                ("sweep_ms", C.c_double), ("candidates_inserted", C.c_int64), ("compactions", C.c_int64)]
+                ("sweep_ms", C.c_double), ("candidates_inserted", C.c_int64), ("compactions", C.c_int64),
+                ("batch_launches", C.c_int64), ("batch_ms", C.c_double)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class Budget(C.Structure):
+    _fields_ = [("max_requests", C.c_int32), ("pad", C.c_int32), ("max_tokens", C.c_int64)]
 
 
 class SelectOut(C.Structure):
@@ -93,7 +98,7 @@ SYMBOLS = [
     "ewsjf_ctx_destroy", "ewsjf_ctx_num_ctas", "ewsjf_partition", "ewsjf_weights_from_meta", "ewsjf_route",
     "ewsjf_score_select", "ewsjf_tick", "ewsjf_tick_host", "ewsjf_exchange_bytes", "ewsjf_tick_local",
     "ewsjf_tick_merge", "ewsjf_score_select_sweep", "ewsjf_ctx_set_timing", "ewsjf_ctx_get_timing",
-    "ewsjf_ctx_get_phases",
+    "ewsjf_ctx_get_phases", "ewsjf_batch_build", "ewsjf_prune_empty",
 ]
 
 _lib = None
@@ -135,6 +140,8 @@ def load() -> C.CDLL:
                                    P(SelectOut)]
     L.ewsjf_score_select_sweep.argtypes = [V, V, V, V, V, I64, P(Partition), P(Meta), I32, P(SelectParams),
                                            P(SelectOut)]
+    L.ewsjf_batch_build.argtypes = [V, V, I64, I64, P(SelectOut), I32, I32, P(Budget), V, V]
+    L.ewsjf_prune_empty.argtypes = [P(Partition), V, I32, P(C.c_int32)]
     for name in SYMBOLS:
         if name not in ("ewsjf_abi_version", "ewsjf_status_str", "ewsjf_last_error", "ewsjf_ctx_num_ctas",
                         "ewsjf_exchange_bytes"):

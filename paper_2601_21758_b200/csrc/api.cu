@@ -139,6 +139,7 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
     if (ctx->h_summary) cudaFreeHost(ctx->h_summary);
     rp_free(ctx);
     sweep_free(ctx);
+    if (ctx->d_bpre) cudaFree(ctx->d_bpre);
     delete ctx;
     return EWSJF_OK;
 }
@@ -179,6 +180,7 @@ extern "C" ewsjf_status ewsjf_ctx_get_timing(ewsjf_ctx* ctx, ewsjf_timing* out) 
             case KIND_TICK: out->tick_ms += ms; out->tick_launches++; break;
             case KIND_MERGE: out->merge_ms += ms; out->merge_launches++; break;
             case KIND_PARTITION: out->partition_ms += ms; out->partition_launches++; break;
+            case KIND_BATCH: out->batch_ms += ms; out->batch_launches++; break;
             default: out->sweep_ms += ms; out->sweep_launches++; break;
         }
     }

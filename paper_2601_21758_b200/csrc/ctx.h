@@ -57,6 +57,9 @@ struct ewsjf_ctx {
     ewsjf::RpScratch* rp = nullptr;
     // Θ-sweep scratch (sweep.cu), grown on demand and kept
     ewsjf::SweepScratch* sw = nullptr;
+    // batch builder prefix scratch (batch.cu)
+    uint32_t* d_bpre = nullptr;
+    int64_t bpre_cap = 0;
     // instrumentation
     long long launches = 0;
     bool timing = false;
@@ -66,7 +69,7 @@ struct ewsjf_ctx {
 };
 
 namespace ewsjf {
-enum { KIND_TICK = 0, KIND_MERGE = 1, KIND_PARTITION = 2, KIND_SWEEP = 3 };
+enum { KIND_TICK = 0, KIND_MERGE = 1, KIND_PARTITION = 2, KIND_SWEEP = 3, KIND_BATCH = 4 };
 // Bracket one launch with events when timing is on; count it always.
 struct LaunchScope {
     ewsjf_ctx* c;

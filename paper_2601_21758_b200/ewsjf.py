@@ -16,7 +16,7 @@ from . import _lib as L
 __all__ = [
     "EwsjfError", "Context", "make_partition", "meta", "select_params", "partition_params", "weights_from_meta",
     "Outputs", "tick", "tick_host", "score_select", "route", "partition", "score_select_sweep",
-    "exchange_bytes", "tick_local", "tick_merge", "tick_sharded",
+    "exchange_bytes", "tick_local", "tick_merge", "tick_sharded", "batch_build", "prune_empty",
 ]
 
 
@@ -265,6 +265,37 @@ def score_select_sweep(ctx: Context, length, arrival, cost, qid, part: L.Partiti
                                          C.byref(part), th, n_theta, C.byref(params), so)
     ctx.check(s, (L.OK, L.DOMAIN))
     return outs
+
+
+# ------------------------------------------------------ Alg. 1 batch ------
+def batch_build(ctx: Context, length, sel: Outputs, n_queues: int, max_requests: int, max_tokens: int,
+                global_base: int = 0, ids_out=None, info_out=None):
+    """ewsjf_batch_build over a FIFO-mode selection ``sel`` (depth >= max_requests).
+
+    Returns (ids [max_requests] int64 device, -1 padded; info [4] int64 device:
+    count, tokens, status, primary).  Asynchronous on the current stream."""
+    _dev_check(length, torch.int32, "len")
+    ids = ids_out if ids_out is not None else torch.empty(max_requests, dtype=torch.int64, device=length.device)
+    info = info_out if info_out is not None else torch.empty(4, dtype=torch.int64, device=length.device)
+    _dev_check(ids, torch.int64, "ids_out"); _dev_check(info, torch.int64, "info_out")
+    so = sel.struct()
+    b = L.Budget(max_requests, 0, max_tokens)
+    ctx.use_current_stream()
+    s = ctx.lib.ewsjf_batch_build(ctx.h, _ptr(length), length.numel(), global_base, C.byref(so), sel.k,
+                                  n_queues, C.byref(b), _ptr(ids), _ptr(info))
+    ctx.check(s, (L.OK,))
+    return ids, info
+
+
+def prune_empty(part: L.Partition, counts, threshold: int) -> int:
+    """ewsjf_prune_empty (host): Alg. 1 lines 8-12 on ``part`` in place; returns queues removed."""
+    import numpy as np
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.int64)[: part.n])
+    rm = C.c_int32(0)
+    s = L.load().ewsjf_prune_empty(C.byref(part), c.ctypes.data, threshold, C.byref(rm))
+    if s != L.OK:
+        raise RuntimeError(f"ewsjf_prune_empty: status {s}")
+    return rm.value
 
 
 # ----------------------------------------------------------- multi-GPU ------

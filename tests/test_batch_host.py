@@ -1,0 +1,36 @@
+"""Host half of Alg. 1 (lines 8-12): ewsjf_prune_empty in libewsjf against the
+oracle's or_prune_empty on random counter states (no GPU needed: the call is
+host bookkeeping over the host partition)."""
+import numpy as np
+import pytest
+
+from tests.parity import to_gpu_partition
+
+
+@pytest.fixture(scope="module")
+def E():
+    import paper_2601_21758_b200 as E
+    return E
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_prune_empty_matches_oracle(E, orc, seed):
+    rng = np.random.default_rng(seed)
+    nq = int(rng.integers(1, 40))
+    edges = np.sort(rng.choice(np.arange(2, 5000), nq - 1, replace=False)) if nq > 1 else np.array([], int)
+    b = [1] + [int(x) for x in edges] + [5001]
+    opart = orc.make_partition([(b[i], b[i + 1]) for i in range(nq)])
+    e0 = rng.integers(0, 6, nq).astype(np.int32)
+    counts = np.where(rng.random(nq) < 0.5, 0, rng.integers(1, 100, nq)).astype(np.int64)
+    thr = int(rng.integers(0, 6))
+    gp = to_gpu_partition(E, opart)
+    for i in range(nq):
+        gp.q[i].empty_count = int(e0[i])
+    v0 = gp.version
+    rm = E.prune_empty(gp, counts, thr)
+    op, oe, orm = orc.prune_empty(opart, e0, counts, thr)
+    assert rm == orm and gp.n == op.n
+    assert [(q["min_len"], q["max_len"], q["id"], q["index"]) for q in gp.queues()] == \
+           [(q["min_len"], q["max_len"], q["id"], q["index"]) for q in op.queues()]
+    assert [gp.q[i].empty_count for i in range(gp.n)] == list(oe)
+    assert gp.version == v0 + (1 if rm else 0)
