@@ -20,12 +20,21 @@
 // max_tokens < 2^32 - 1 keeps the saturated prefixes exact for every test
 // (a saturated entry never fits).
 #include <climits>
+#include <algorithm>
 #include "tick.cuh"
 #include "ctx.h"
 
 namespace ewsjf {
 
 constexpr int kBThreads = 1024;
+constexpr int kBPer = 8;                       // row entries per lane per gather pass
+constexpr int kBSmemMax = 200 * 1024;          // prefix table in shared memory up to this size
+
+// prefix entries are written by other warps of this CTA before __syncthreads:
+// shared memory, or global scratch read past L1 (generic address either way)
+__device__ __forceinline__ uint32_t ld_pre(const uint32_t* p) {
+    return __isShared(p) ? *p : __ldcg(p);
+}
 
 struct BatchArgs {
     const int32_t* len;
@@ -35,7 +44,7 @@ struct BatchArgs {
     const ewsjf_summary* summary;
     int32_t k, nq, max_req;
     int64_t max_tok;
-    uint32_t* pre;          // [nq][kk] scratch
+    uint32_t* pre;          // [nq][kk] global scratch, or nullptr -> dynamic shared memory
     int32_t kk;             // min(k, max_req)
     int64_t* out_id;        // [max_req]
     int64_t* out_info;      // [4]: count, tokens, status, primary
@@ -49,30 +58,48 @@ __global__ void __launch_bounds__(kBThreads, 1) batch_build_kernel(BatchArgs A) 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (threadIdx.x == 0) { s_bad = 0; s_nb = 0; }
     __syncthreads();
-    // ---- phase 1: per-queue prefix of lengths over the FIFO rows
+    // ---- phase 1: per-queue prefix of lengths over the FIFO rows.  All of a
+    // lane's row ids, then all of its lengths, are loaded before the scans so the
+    // dependent gathers overlap (kBPer entries per lane per pass).
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t* pre = A.pre ? A.pre : s_dyn;
     for (int p = warp; p < A.nq; p += nw) {
         const int64_t c = A.count[p];
         const int m = (int)(c < A.kk ? c : A.kk);
         const int64_t* row = A.topk_id + (int64_t)p * A.k;
-        uint32_t* pr = A.pre + (int64_t)p * A.kk;
+        uint32_t* pr = pre + (int64_t)p * A.kk;
         int64_t carry = 0;
-        for (int t0 = 0; t0 < m; t0 += 32) {
-            const int t = t0 + lane;
-            int64_t b = 0;
-            if (t < m) {
-                const int64_t r = row[t] - A.base;
-                if (row[t] < 0 || r < 0 || r >= A.n) { b = 0; atomicOr(&s_bad, 1); }
-                else b = A.len[r];
-            }
-            int64_t x = b;
+        for (int b0 = 0; b0 < m; b0 += 32 * kBPer) {
+            int64_t id[kBPer];
+            int32_t b[kBPer];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
+            for (int u = 0; u < kBPer; u++) {
+                const int t = b0 + u * 32 + lane;
+                id[u] = t < m ? __ldg(row + t) : 0;
             }
-            x += carry;
-            if (t < m) pr[t] = x >= 0xffffffffll ? 0xffffffffu : (uint32_t)x;
-            carry = __shfl_sync(0xffffffffu, x, 31);
+#pragma unroll
+            for (int u = 0; u < kBPer; u++) {
+                const int t = b0 + u * 32 + lane;
+                const int64_t r = id[u] - A.base;
+                b[u] = 0;
+                if (t < m) {
+                    if (id[u] < 0 || r < 0 || r >= A.n) atomicOr(&s_bad, 1);
+                    else b[u] = __ldg(A.len + r);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kBPer; u++) {
+                const int t = b0 + u * 32 + lane;
+                int64_t x = b[u];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                x += carry;
+                if (t < m) pr[t] = x >= 0xffffffffll ? 0xffffffffu : (uint32_t)x;
+                carry = __shfl_sync(0xffffffffu, x, 31);
+            }
         }
         if (lane == 0) { s_m[p] = m; s_take[p] = 0; s_off[p] = 0; }
     }
@@ -90,11 +117,11 @@ __global__ void __launch_bounds__(kBThreads, 1) batch_build_kernel(BatchArgs A) 
                     if (m == 0) continue;
                     if (nb > 0 && tok >= A.max_tok) continue;     // nothing of length >= 1 fits
                     const int64_t R = A.max_tok - tok;            // >= 0 unless nb == 0
-                    const uint32_t* pr = A.pre + (int64_t)p * A.kk;
+                    const uint32_t* pr = pre + (int64_t)p * A.kk;
                     int j = 0;
                     for (int t0 = 0; t0 < m; t0 += 32) {
                         const int t = t0 + lane;
-                        const bool fit = t < m && (int64_t)__ldcg(pr + t) <= R;
+                        const bool fit = t < m && (int64_t)ld_pre(pr + t) <= R;
                         const unsigned bal = __ballot_sync(0xffffffffu, fit);
                         j += __popc(bal);
                         if (bal != 0xffffffffu) break;
@@ -102,7 +129,7 @@ __global__ void __launch_bounds__(kBThreads, 1) batch_build_kernel(BatchArgs A) 
                     if (nb == 0 && j == 0) j = 1;                 // the first request is always admitted
                     if (j > A.max_req - nb) j = (int)(A.max_req - nb);
                     if (lane == 0) { s_take[p] = j; s_off[p] = (int)nb; }
-                    if (j > 0) tok += (int64_t)__ldcg(pr + j - 1);
+                    if (j > 0) tok += (int64_t)ld_pre(pr + j - 1);
                     nb += j;
                 }
             }
@@ -142,8 +169,9 @@ extern "C" ewsjf_status ewsjf_batch_build(ewsjf_ctx* ctx, const int32_t* d_len, 
         return fail(ctx, EWSJF_ERR_INVALID_ARG, "batch_build: max_tokens out of range [0, 2^32-1)");
     CU(cudaSetDevice(ctx->device));
     const int32_t kk = budget->max_requests;
-    const int64_t need = (int64_t)EWSJF_MAX_QUEUES * kk;
-    if (need > ctx->bpre_cap) {
+    const int64_t need = (int64_t)std::max(n_queues, 1) * kk;
+    const bool in_smem = need * 4 <= std::min<int64_t>(kBSmemMax, ctx->smem_optin - 4096);
+    if (!in_smem && need > ctx->bpre_cap) {
         if (ctx->d_bpre) cudaFree(ctx->d_bpre);
         ctx->d_bpre = nullptr;
         ctx->bpre_cap = 0;
@@ -155,11 +183,16 @@ extern "C" ewsjf_status ewsjf_batch_build(ewsjf_ctx* ctx, const int32_t* d_len, 
     A.topk_id = sel->d_topk_id; A.count = sel->d_count;
     A.summary = sel->d_summary ? sel->d_summary : ctx->d_summary;
     A.k = k; A.nq = n_queues; A.max_req = budget->max_requests; A.max_tok = budget->max_tokens;
-    A.pre = ctx->d_bpre; A.kk = kk;
+    A.pre = in_smem ? nullptr : ctx->d_bpre; A.kk = kk;
+    const size_t smem = in_smem ? (size_t)need * 4 : 0;
+    if (smem > 48 * 1024 && smem > ctx->batch_smem_attr) {
+        CU(cudaFuncSetAttribute(batch_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBSmemMax));
+        ctx->batch_smem_attr = kBSmemMax;
+    }
     A.out_id = d_batch_id; A.out_info = d_batch_info;
     {
         LaunchScope ls(ctx, KIND_BATCH);
-        batch_build_kernel<<<1, kBThreads, 0, ctx->stream>>>(A);
+        batch_build_kernel<<<1, kBThreads, smem, ctx->stream>>>(A);
     }
     CU(cudaGetLastError());
     return EWSJF_OK;

@@ -60,6 +60,7 @@ struct ewsjf_ctx {
     // batch builder prefix scratch (batch.cu)
     uint32_t* d_bpre = nullptr;
     int64_t bpre_cap = 0;
+    int64_t batch_smem_attr = 0;
     // instrumentation
     long long launches = 0;
     bool timing = false;

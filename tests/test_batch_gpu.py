@@ -78,7 +78,7 @@ def test_batch_random_budgets(E, orc, ctx, part_c1, seed):
     n = int(rng.integers(1, 5000))
     pool = workload.pool("bimodal" if seed % 2 else "heavy", n, 900 + seed)
     mr = int(rng.integers(1, 200)); mt = int(rng.integers(0, 200_000))
-    _both(E, orc, ctx, pool, part_c1, mr, mt, K=int(rng.integers(mr, 257)), base=int(rng.integers(0, 1 << 40)))
+    _both(E, orc, ctx, pool, part_c1, mr, mt, K=int(rng.integers(mr, 257)), base=int(rng.integers(0, 1 << 31)))
 
 
 def test_batch_empty_pool_and_oversized_first(E, orc, ctx, part_c1):
@@ -107,3 +107,15 @@ def test_batch_rejects_shallow_rows(E, ctx, part_c1):
     out = E.tick(ctx, ln, ar, None, gpart, E.meta(**THETA0), E.select_params(k=8, mode=1, now=600.0))
     with pytest.raises(Exception):
         E.batch_build(ctx, ln, out, out.summary["n_queues"], 16, 1000)
+
+
+def test_batch_many_queues_global_scratch(E, orc, ctx):
+    """250 queues x 256-deep rows: the prefix table (256 KB) exceeds shared memory
+    and lives in global scratch."""
+    opart = orc.make_partition([(1 + 4 * i, 5 + 4 * i) for i in range(250)])
+    rng = np.random.default_rng(4)
+    n = 20_000
+    ln = rng.integers(1, 1001, n).astype(np.int32)
+    pool = {"len": ln, "arrival": workload.arrivals(n, 41), "cost": workload.cost_estimates(ln, 42)}
+    for mr, mt in [(256, 1 << 20), (256, 3000), (200, 50_000)]:
+        _both(E, orc, ctx, pool, opart, mr, mt)
