@@ -52,6 +52,7 @@ struct RpScratch {
     int32_t* treei;
     int kblocks;
     int64_t tree_n;
+    int prune_cap;                      // largest m the shared-memory prune holds
     cudaEvent_t ev[6];
 };
 
@@ -374,7 +375,8 @@ __global__ void __launch_bounds__(kHT, 1)
                  const int64_t* __restrict__ S2, int64_t M, const int32_t* seg, const int32_t* rout, int max_queues, double eps, int rule, int32_t* plo, int32_t* phi,
                  int32_t* pnext, int32_t* pprev, int64_t* pn, int64_t* ps1, int64_t* ps2, double* tree,
                  int32_t* treei, int32_t* q_lo, int32_t* q_hi, int64_t* q_n, int64_t* q_s1, int64_t* q_s2,
-                 int64_t* merges_out) {
+                 int64_t* merges_out, const int32_t* done) {
+    if (*done) return;                  // prune_smem_kernel handled this partition
     const int m0 = rout[0];
     const int tid = threadIdx.x, lane = tid & 31;
     // finalisation
@@ -492,6 +494,158 @@ __global__ void __launch_bounds__(kHT, 1)
     }
 }
 
+
+// ---- A5 + A6 in shared memory (m <= cap).  Same decisions as prune_kernel:
+// U per adjacent pair from the canonical util_of, argmin (MIN_U) / argmax (MAX_U)
+// with ties to the lowest pair.  A merged segment is always a run of original
+// segments [p, next[p]), so its statistics come from constant per-segment
+// prefixes (lo, N, S1 at each original start; prune_prep_kernel) and the only
+// mutable state is the linked list (u16 next/prev) and the tournament tree of
+// 64-bit order keys (leaves: key only; inner nodes: key + pair index), all in
+// shared memory.  One warp merges; a tree node is a 32-way redux.min over keys.
+constexpr uint64_t kDead = ~0ull;
+constexpr uint16_t kNone = 0xffffu;
+
+__global__ void prune_prep_kernel(const int32_t* __restrict__ v, const int64_t* __restrict__ N,
+                                  const int64_t* __restrict__ S1, const int32_t* __restrict__ seg, int64_t M,
+                                  const int32_t* rout, int32_t* lo, int64_t* nx, int64_t* s1x) {
+    const int m0 = rout[0];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= m0; i += gridDim.x * blockDim.x) {
+        const int64_t x = i < m0 ? seg[i] : M;
+        int32_t l;
+        if (i == 0) l = v[x];
+        else if (i < m0) l = (int32_t)(((int64_t)v[x - 1] + (int64_t)v[x]) / 2 + 1);
+        else l = v[M - 1] + 1;
+        lo[i] = l; nx[i] = N[x]; s1x[i] = S1[x];
+    }
+}
+
+__device__ __forceinline__ uint64_t ukey(double u, bool maxu) {
+    const uint64_t b = (uint64_t)__double_as_longlong(u);
+    const uint64_t o = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    return maxu ? ~o : o;
+}
+
+// smem bytes for m segments (npair = m - 1 leaves)
+__host__ __device__ inline size_t prune_smem_bytes(int m, int* nl_out, int* lv_off, int* lv_n) {
+    const int npair = m > 1 ? m - 1 : 1;
+    int nl = 0, off = 0, cnt = npair;
+    for (;;) {
+        if (lv_off) { lv_off[nl] = off; lv_n[nl] = cnt; }
+        if (nl > 0) off += cnt;
+        nl++;
+        if (cnt == 1) break;
+        cnt = (cnt + 31) / 32;
+    }
+    if (nl_out) *nl_out = nl;
+    // leaves u64[npair] | inner keys u64[off] | inner idx i32[off] | next, prev u16[m + 1]
+    size_t b = (size_t)npair * 8 + (size_t)off * 12;
+    b = (b + 15) & ~(size_t)15;
+    return b + (size_t)(m + 1) * 4 + 16;
+}
+
+__global__ void __launch_bounds__(kHT, 1)
+    prune_smem_kernel(const int32_t* __restrict__ lo, const int64_t* __restrict__ nx, const int64_t* __restrict__ s1x,
+                      const int64_t* __restrict__ S2, const int32_t* __restrict__ seg, int64_t M, const int32_t* rout,
+                      int cap_m, int max_queues, double eps, int rule, int32_t* q_lo, int32_t* q_hi, int64_t* q_n,
+                      int64_t* q_s1, int64_t* q_s2, int64_t* merges_out, int32_t* done) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int m0 = rout[0];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (m0 > cap_m) { if (tid == 0) *done = 0; return; }
+    int lv_off[8], lv_n[8], nl;
+    prune_smem_bytes(m0, &nl, lv_off, lv_n);
+    const int npair = m0 - 1;
+    uint64_t* leaf = (uint64_t*)sm;
+    uint64_t* ikey = leaf + lv_n[0];                       // inner node (l, j) at ikey[lv_off[l] + j]
+    int32_t* iidx = (int32_t*)(ikey + (lv_off[nl - 1] + (nl > 1 ? 1 : 0)));
+    size_t b = (size_t)lv_n[0] * 8 + (size_t)(lv_off[nl - 1] + (nl > 1 ? 1 : 0)) * 12;
+    b = (b + 15) & ~(size_t)15;
+    uint16_t* nxt = (uint16_t*)(sm + b);
+    uint16_t* prv = nxt + (m0 + 1);
+    const bool maxu = rule == 1;
+    // segment [a, e) of original segments: n, S1, lo, hi
+    auto U = [&](int a, int e, int f) -> uint64_t {    // pair ([a,e), [e,f))
+        const int64_t nl_ = __ldg(nx + e) - __ldg(nx + a), sl = __ldg(s1x + e) - __ldg(s1x + a);
+        const int64_t nr = __ldg(nx + f) - __ldg(nx + e), sr = __ldg(s1x + f) - __ldg(s1x + e);
+        return ukey(util_of(nl_, sl, __ldg(lo + a), __ldg(lo + e), nr, sr, __ldg(lo + e), __ldg(lo + f), eps), maxu);
+    };
+    for (int i = tid; i <= m0; i += kHT) {
+        nxt[i] = (uint16_t)(i < m0 ? i + 1 : kNone);
+        prv[i] = (uint16_t)(i > 0 ? i - 1 : kNone);
+    }
+    for (int p = tid; p < npair; p += kHT) leaf[p] = U(p, p + 1, p + 2);
+    if (npair < 1 && tid == 0) leaf[0] = kDead;
+    __syncthreads();
+    // node (l, j) <- best of its <= 32 children at level l-1 (one warp)
+    auto node = [&](int l, int j) {
+        if (j >= lv_n[l]) return;                           // warp-uniform
+        const int c = j * 32 + lane;
+        uint64_t k = kDead;
+        int id = -1;
+        if (c < lv_n[l - 1]) {
+            if (l == 1) { k = leaf[c]; id = k == kDead ? -1 : c; }
+            else { k = ikey[lv_off[l - 1] + c]; id = iidx[lv_off[l - 1] + c]; }
+        }
+        const unsigned hi = (unsigned)(k >> 32), lw = (unsigned)k;
+        const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lw : 0xffffffffu);
+        const int win = __ffs(__ballot_sync(0xffffffffu, hi == mh && lw == ml)) - 1;
+        const int wid = __shfl_sync(0xffffffffu, id, win);
+        if (lane == 0) { ikey[lv_off[l] + j] = ((uint64_t)mh << 32) | ml; iidx[lv_off[l] + j] = wid; }
+    };
+    for (int l = 1; l < nl; l++) {
+        for (int j = warp; j < lv_n[l]; j += kHT / 32) node(l, j);
+        __syncthreads();
+    }
+    if (warp != 0) return;
+    int m = m0;
+    int64_t merges = 0;
+    while (m > max_queues && m > 1) {
+        const int p = nl > 1 ? iidx[lv_off[nl - 1]] : 0;
+        const int r = nxt[p];
+        const int rn = nxt[r];                  // m0 = end sentinel
+        const int rnn = rn < m0 ? nxt[rn] : m0;
+        const int q = prv[p];
+        // lanes 0 and 1 evaluate the two new pairs (p, rn) and (q, p) converged
+        const bool has = lane == 0 ? rn < m0 : (lane == 1 && q != kNone);
+        const int ua = lane == 0 ? p : q, ue = lane == 0 ? rn : p, uf = lane == 0 ? rnn : rn;
+        uint64_t ku = kDead;
+        if (lane < 2) ku = has ? U(ua, ue, has ? uf : ue) : kDead;
+        const uint64_t kp = __shfl_sync(0xffffffffu, ku, 0), kq = __shfl_sync(0xffffffffu, ku, 1);
+        if (lane == 0) {
+            nxt[p] = (uint16_t)rn;
+            if (rn < m0) prv[rn] = (uint16_t)p;
+            if (r < npair) leaf[r] = kDead;
+            leaf[p] = kp;
+            if (q != kNone) leaf[q] = kq;
+        }
+        __syncwarp();
+        int a = r, bb = p, c = q != kNone ? q : p;
+        for (int l = 1; l < nl; l++) {
+            a >>= 5; bb >>= 5; c >>= 5;
+            node(l, a);
+            if (bb != a) node(l, bb);
+            if (c != a && c != bb) node(l, c);
+            __syncwarp();
+        }
+        m--;
+        merges++;
+    }
+    if (lane == 0) {
+        int k = 0;
+        for (int i = 0; i < m0 && k < 256; i = nxt[i]) {
+            const int e = nxt[i];
+            const int64_t xi = seg[i], xe = e < m0 ? seg[e] : M;
+            q_lo[k] = lo[i]; q_hi[k] = lo[e]; q_n[k] = nx[e] - nx[i]; q_s1[k] = s1x[e] - s1x[i];
+            q_s2[k] = S2[xe] - S2[xi];
+            k++;
+        }
+        merges_out[0] = merges;
+        merges_out[1] = k;
+        *done = 1;
+    }
+}
 
 __global__ void set_flags_kernel(uint8_t* flag, const int32_t* out, int k) {
     flag[0] = 1;
@@ -639,10 +793,27 @@ extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, in
     CU(cudaGetLastError());
     CU(cudaEventRecord(R->ev[3], st));
     {
+        // shared-memory prune for m <= cap (every partition up to ~18k segments), else the
+        // global-memory tree (prune_kernel skips itself when the first one finished)
+        const int budget = (ctx->smem_optin > 0 ? ctx->smem_optin : 232448) - 1024;
+        if (R->prune_cap == 0) {
+            int lo_ = 2, hi_ = kHistMax;
+            while (lo_ < hi_) {
+                const int mid = (lo_ + hi_ + 1) / 2;
+                if (prune_smem_bytes(mid, nullptr, nullptr, nullptr) <= (size_t)budget) lo_ = mid; else hi_ = mid - 1;
+            }
+            R->prune_cap = lo_;
+            CU(cudaFuncSetAttribute(prune_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+        }
         LaunchScope ls(ctx, KIND_PARTITION);
+        prune_prep_kernel<<<64, 256, 0, st>>>(R->v, R->N, R->S1, R->seg, M, R->out_i, R->plo, R->pn, R->ps1);
+        prune_smem_kernel<<<1, kHT, budget, st>>>(R->plo, R->pn, R->ps1, R->S2, R->seg, M, R->out_i, R->prune_cap,
+                                                  p->max_queues, p->epsilon, p->merge_rule, R->q_lo, R->q_hi,
+                                                  R->q_n, R->q_s1, R->q_s2, R->merges, R->out_i + 8);
         prune_kernel<<<1, kHT, 0, st>>>(R->v, R->N, R->S1, R->S2, M, R->seg, R->out_i, p->max_queues, p->epsilon,
                                          p->merge_rule, R->plo, R->phi_, R->pnext, R->pprev, R->pn, R->ps1, R->ps2,
-                                         R->tree, R->treei, R->q_lo, R->q_hi, R->q_n, R->q_s1, R->q_s2, R->merges);
+                                         R->tree, R->treei, R->q_lo, R->q_hi, R->q_n, R->q_s1, R->q_s2, R->merges,
+                                         R->out_i + 8);
     }
     CU(cudaGetLastError());
     CU(cudaEventRecord(R->ev[4], st));
