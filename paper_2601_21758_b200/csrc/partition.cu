@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(kHT, 1)
 // shared memory.  One warp merges; a tree node is a 32-way redux.min over keys.
 constexpr uint64_t kDead = ~0ull;
 constexpr uint16_t kNone = 0xffffu;
+constexpr int kPL = 5;
 
 __global__ void prune_prep_kernel(const int32_t* __restrict__ v, const int64_t* __restrict__ N,
                                   const int64_t* __restrict__ S1, const int32_t* __restrict__ seg, int64_t M,
@@ -553,13 +554,27 @@ __global__ void __launch_bounds__(kHT, 1)
     const int m0 = rout[0];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (m0 > cap_m) { if (tid == 0) *done = 0; return; }
-    int lv_off[8], lv_n[8], nl;
-    prune_smem_bytes(m0, &nl, lv_off, lv_n);
+    // tree levels (static indices after unrolling: kPL levels cover 32^4 > kHistMax leaves)
+    int lv_off[kPL], lv_n[kPL], nl = kPL;
+    {
+        int off = 0, cnt = m0 > 1 ? m0 - 1 : 1;
+#pragma unroll
+        for (int l = 0; l < kPL; l++) {
+            lv_off[l] = off; lv_n[l] = cnt;
+            if (l > 0) off += cnt;
+            if (cnt == 1 && nl == kPL) nl = l + 1;
+            cnt = (cnt + 31) / 32;
+        }
+    }
     const int npair = m0 - 1;
     uint64_t* leaf = (uint64_t*)sm;
+    int n_inner = 0;
+#pragma unroll
+    for (int l = 1; l < kPL; l++)
+        if (l < nl) n_inner += lv_n[l];
     uint64_t* ikey = leaf + lv_n[0];                       // inner node (l, j) at ikey[lv_off[l] + j]
-    int32_t* iidx = (int32_t*)(ikey + (lv_off[nl - 1] + (nl > 1 ? 1 : 0)));
-    size_t b = (size_t)lv_n[0] * 8 + (size_t)(lv_off[nl - 1] + (nl > 1 ? 1 : 0)) * 12;
+    int32_t* iidx = (int32_t*)(ikey + n_inner);
+    size_t b = (size_t)lv_n[0] * 8 + (size_t)n_inner * 12;
     b = (b + 15) & ~(size_t)15;
     uint16_t* nxt = (uint16_t*)(sm + b);
     uint16_t* prv = nxt + (m0 + 1);
@@ -594,15 +609,21 @@ __global__ void __launch_bounds__(kHT, 1)
         const int wid = __shfl_sync(0xffffffffu, id, win);
         if (lane == 0) { ikey[lv_off[l] + j] = ((uint64_t)mh << 32) | ml; iidx[lv_off[l] + j] = wid; }
     };
-    for (int l = 1; l < nl; l++) {
-        for (int j = warp; j < lv_n[l]; j += kHT / 32) node(l, j);
+#pragma unroll
+    for (int l = 1; l < kPL; l++) {
+        if (l < nl)
+            for (int j = warp; j < lv_n[l]; j += kHT / 32) node(l, j);
         __syncthreads();
     }
     if (warp != 0) return;
+    int off_top = 0;
+#pragma unroll
+    for (int l = 1; l < kPL; l++)
+        if (l == nl - 1) off_top = lv_off[l];
     int m = m0;
     int64_t merges = 0;
     while (m > max_queues && m > 1) {
-        const int p = nl > 1 ? iidx[lv_off[nl - 1]] : 0;
+        const int p = nl > 1 ? iidx[off_top] : 0;
         const int r = nxt[p];
         const int rn = nxt[r];                  // m0 = end sentinel
         const int rnn = rn < m0 ? nxt[rn] : m0;
@@ -622,7 +643,9 @@ __global__ void __launch_bounds__(kHT, 1)
         }
         __syncwarp();
         int a = r, bb = p, c = q != kNone ? q : p;
-        for (int l = 1; l < nl; l++) {
+#pragma unroll
+        for (int l = 1; l < kPL; l++) {
+            if (l >= nl) break;
             a >>= 5; bb >>= 5; c >>= 5;
             node(l, a);
             if (bb != a) node(l, bb);
