@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C5 Θ-sweep measurement")
     ap.add_argument("--sweep-thetas", type=int, default=256)
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 100M-history Refine-and-Prune measurement")
     return ap.parse_args()
 
 
@@ -247,6 +248,30 @@ def run_batch(E, ctx, part, theta, copies, dev, n, max_req=256, max_tok=65536, r
             "batch_size": inf[0], "batch_tokens": inf[1], "status": inf[2], "primary": inf[3]}
 
 
+def run_c4(E, dev, local, reps=3):
+    """C4 (BASELINE configs[3]): Refine-and-Prune over a 100M heavy-tailed history on one GPU."""
+    import torch
+    hist = torch.from_numpy(workload.heavy(100_000_000, 401)).to(dev)
+    cctx = E.Context(local, max_pool=1024, max_history=100_000_000, max_k=8)
+    E.partition(cctx, hist)
+    cctx.set_timing(True)
+    sts = []
+    for _ in range(reps):
+        part, st, _ = E.partition(cctx, hist)
+        sts.append(st)
+    tm = cctx.timing()
+    cctx.close()
+    med = sorted(sts, key=lambda x: x["ms_total"])[len(sts) // 2]
+    peak, src = peaks()
+    hist_gbs = 4e8 / (med["ms_hist"] / 1e3) / 1e9
+    return {"workload": "C4: Refine-and-Prune of heavy(100M, seed 401), alpha=2, max_queues=32, MIN_U",
+            "ms": med["ms_total"], "stages_ms": {k: med[k] for k in ("ms_hist", "ms_kmeans", "ms_refine", "ms_prune")},
+            "kernel_ms_sum": tm["partition_ms"] / reps, "launches": tm["partition_launches"] / reps,
+            "distinct": med["distinct"], "segments": med["segments"], "merges": med["merges"], "queues": part.n,
+            "hist_roofline": {"bound": "hbm", "achieved": hist_gbs, "peak": peak, "unit": "GB/s",
+                              "frac": hist_gbs / peak, "bytes": 4e8, "peak_source": src}}
+
+
 def config_dict(args, opart_source):
     return {"workload": "C3: 10M pending requests per GPU, heavy-tailed lengths (80% lognormal(ln128,0.6) "
                         "32..2047, 20% Pareto(1.5) 2048..32768), route + score + per-queue top-k",
@@ -393,6 +418,8 @@ def main():
     # the GPU Refine-and-Prune partition of bimodal(1M, seed 201) (C2's partition)
     if not args.no_sweep and ws == 1:
         line["sweep"] = run_sweep(E, ctx, dev, args)
+    if ws == 1 and not args.no_c4:
+        line["c4"] = run_c4(E, dev, local)
     if ws == 1 and args.k <= 256:
         bctx = E.Context(local, max_pool=n, max_history=0, max_k=256)
         line["batch"] = run_batch(E, bctx, part, theta, copies, dev, n)

@@ -53,6 +53,7 @@ struct RpScratch {
     int kblocks;
     int64_t tree_n;
     int prune_cap;                      // largest m the shared-memory prune holds
+    int prune_cap_lg;                   // ... with its leaves in global scratch
     cudaEvent_t ev[6];
 };
 
@@ -528,7 +529,7 @@ __device__ __forceinline__ uint64_t ukey(double u, bool maxu) {
 }
 
 // smem bytes for m segments (npair = m - 1 leaves)
-__host__ __device__ inline size_t prune_smem_bytes(int m, int* nl_out, int* lv_off, int* lv_n) {
+__host__ __device__ inline size_t prune_smem_bytes(int m, int* nl_out, int* lv_off, int* lv_n, bool leaf_global) {
     const int npair = m > 1 ? m - 1 : 1;
     int nl = 0, off = 0, cnt = npair;
     for (;;) {
@@ -540,20 +541,28 @@ __host__ __device__ inline size_t prune_smem_bytes(int m, int* nl_out, int* lv_o
     }
     if (nl_out) *nl_out = nl;
     // leaves u64[npair] | inner keys u64[off] | inner idx i32[off] | next, prev u16[m + 1]
-    size_t b = (size_t)npair * 8 + (size_t)off * 12;
+    size_t b = (leaf_global ? 0 : (size_t)npair * 8) + (size_t)off * 12;
     b = (b + 15) & ~(size_t)15;
     return b + (size_t)(m + 1) * 4 + 16;
 }
 
+// LG: leaves in global scratch (read past L1), inner nodes and links in shared
+// memory — partitions up to ~50k segments; otherwise everything in shared memory.
+template <bool LG>
 __global__ void __launch_bounds__(kHT, 1)
-    prune_smem_kernel(const int32_t* __restrict__ lo, const int64_t* __restrict__ nx, const int64_t* __restrict__ s1x,
+    prune_smem_kernel(uint64_t* gleaf, const int32_t* __restrict__ lo, const int64_t* __restrict__ nx, const int64_t* __restrict__ s1x,
                       const int64_t* __restrict__ S2, const int32_t* __restrict__ seg, int64_t M, const int32_t* rout,
                       int cap_m, int max_queues, double eps, int rule, int32_t* q_lo, int32_t* q_hi, int64_t* q_n,
                       int64_t* q_s1, int64_t* q_s2, int64_t* merges_out, int32_t* done) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int m0 = rout[0];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (m0 > cap_m) { if (tid == 0) *done = 0; return; }
+    if (LG) {
+        if (*done || m0 > cap_m) return;
+    } else if (m0 > cap_m) {
+        if (tid == 0) *done = 0;
+        return;
+    }
     // tree levels (static indices after unrolling: kPL levels cover 32^4 > kHistMax leaves)
     int lv_off[kPL], lv_n[kPL], nl = kPL;
     {
@@ -567,14 +576,14 @@ __global__ void __launch_bounds__(kHT, 1)
         }
     }
     const int npair = m0 - 1;
-    uint64_t* leaf = (uint64_t*)sm;
+    uint64_t* leaf = LG ? gleaf : (uint64_t*)sm;
     int n_inner = 0;
 #pragma unroll
     for (int l = 1; l < kPL; l++)
         if (l < nl) n_inner += lv_n[l];
-    uint64_t* ikey = leaf + lv_n[0];                       // inner node (l, j) at ikey[lv_off[l] + j]
+    uint64_t* ikey = LG ? (uint64_t*)sm : leaf + lv_n[0];  // inner node (l, j) at ikey[lv_off[l] + j]
     int32_t* iidx = (int32_t*)(ikey + n_inner);
-    size_t b = (size_t)lv_n[0] * 8 + (size_t)n_inner * 12;
+    size_t b = (LG ? 0 : (size_t)lv_n[0] * 8) + (size_t)n_inner * 12;
     b = (b + 15) & ~(size_t)15;
     uint16_t* nxt = (uint16_t*)(sm + b);
     uint16_t* prv = nxt + (m0 + 1);
@@ -599,7 +608,7 @@ __global__ void __launch_bounds__(kHT, 1)
         uint64_t k = kDead;
         int id = -1;
         if (c < lv_n[l - 1]) {
-            if (l == 1) { k = leaf[c]; id = k == kDead ? -1 : c; }
+            if (l == 1) { k = LG ? __ldcg(leaf + c) : leaf[c]; id = k == kDead ? -1 : c; }
             else { k = ikey[lv_off[l - 1] + c]; id = iidx[lv_off[l - 1] + c]; }
         }
         const unsigned hi = (unsigned)(k >> 32), lw = (unsigned)k;
@@ -820,19 +829,28 @@ extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, in
         // global-memory tree (prune_kernel skips itself when the first one finished)
         const int budget = (ctx->smem_optin > 0 ? ctx->smem_optin : 232448) - 1024;
         if (R->prune_cap == 0) {
-            int lo_ = 2, hi_ = kHistMax;
-            while (lo_ < hi_) {
-                const int mid = (lo_ + hi_ + 1) / 2;
-                if (prune_smem_bytes(mid, nullptr, nullptr, nullptr) <= (size_t)budget) lo_ = mid; else hi_ = mid - 1;
+            for (int g = 0; g < 2; g++) {
+                int lo_ = 2, hi_ = 65534;                   // u16 links
+                while (lo_ < hi_) {
+                    const int mid = (lo_ + hi_ + 1) / 2;
+                    if (prune_smem_bytes(mid, nullptr, nullptr, nullptr, g == 1) <= (size_t)budget) lo_ = mid;
+                    else hi_ = mid - 1;
+                }
+                (g ? R->prune_cap_lg : R->prune_cap) = lo_;
             }
-            R->prune_cap = lo_;
-            CU(cudaFuncSetAttribute(prune_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+            CU(cudaFuncSetAttribute(prune_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+            CU(cudaFuncSetAttribute(prune_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
         }
         LaunchScope ls(ctx, KIND_PARTITION);
         prune_prep_kernel<<<64, 256, 0, st>>>(R->v, R->N, R->S1, R->seg, M, R->out_i, R->plo, R->pn, R->ps1);
-        prune_smem_kernel<<<1, kHT, budget, st>>>(R->plo, R->pn, R->ps1, R->S2, R->seg, M, R->out_i, R->prune_cap,
-                                                  p->max_queues, p->epsilon, p->merge_rule, R->q_lo, R->q_hi,
-                                                  R->q_n, R->q_s1, R->q_s2, R->merges, R->out_i + 8);
+        prune_smem_kernel<false><<<1, kHT, budget, st>>>(nullptr, R->plo, R->pn, R->ps1, R->S2, R->seg, M, R->out_i,
+                                                         R->prune_cap, p->max_queues, p->epsilon, p->merge_rule,
+                                                         R->q_lo, R->q_hi, R->q_n, R->q_s1, R->q_s2, R->merges,
+                                                         R->out_i + 8);
+        prune_smem_kernel<true><<<1, kHT, budget, st>>>((uint64_t*)R->tree, R->plo, R->pn, R->ps1, R->S2, R->seg, M,
+                                                        R->out_i, R->prune_cap_lg, p->max_queues, p->epsilon,
+                                                        p->merge_rule, R->q_lo, R->q_hi, R->q_n, R->q_s1, R->q_s2,
+                                                        R->merges, R->out_i + 8);
         prune_kernel<<<1, kHT, 0, st>>>(R->v, R->N, R->S1, R->S2, M, R->seg, R->out_i, p->max_queues, p->epsilon,
                                          p->merge_rule, R->plo, R->phi_, R->pnext, R->pprev, R->pn, R->ps1, R->ps2,
                                          R->tree, R->treei, R->q_lo, R->q_hi, R->q_n, R->q_s1, R->q_s2, R->merges,

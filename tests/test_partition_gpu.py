@@ -80,3 +80,24 @@ def test_partition_full_c3_history(E, orc, ctx):
 def test_partition_full_c4_bimodal(E, orc, ctx):
     """C4 at full size: Refine-and-Prune of a 100M bimodal history (seed 401)."""
     _check(*_both(E, orc, ctx, workload.bimodal(100_000_000, 401)))
+
+
+@pytest.mark.parametrize("rule", [0, 1])
+@pytest.mark.parametrize("top", [12_000, 18_000, 25_000, 40_000])
+def test_partition_many_segments(E, orc, ctx, rule, top):
+    """Every distinct length twice: each unit gap exceeds alpha * mean(G) ~ 1.0, so
+    Stage 2 leaves `top` segments and Stage 3 merges them down to 32.  12k-18k
+    segments run the all-shared-memory prune, 25k-40k the one with global
+    leaves (C4's 100M heavy history has 32.6k)."""
+    hist = np.repeat(np.arange(1, top + 1, dtype=np.int32), 2)
+    g = _both(E, orc, ctx, hist, merge_rule=rule)
+    assert g[1]["segments"] == top
+    _check(*g)
+
+
+def test_partition_many_segments_global_tree(E, orc, ctx):
+    """56k segments: beyond both shared-memory variants -> global-memory tree."""
+    hist = np.repeat(np.arange(1, 56_001, dtype=np.int32), 2)
+    g = _both(E, orc, ctx, hist)
+    assert g[1]["segments"] == 56_000
+    _check(*g)
