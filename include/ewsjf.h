@@ -159,6 +159,27 @@ ewsjf_status ewsjf_partition(ewsjf_ctx *ctx, const int32_t *d_len, int64_t n,
                              const ewsjf_partition_params *params, ewsjf_partition_t *out,
                              ewsjf_partition_stats *stats);
 
+/* Multi-GPU Refine-and-Prune: A1 is a histogram, so a
+ * history sharded across ranks partitions exactly by summing the ranks'
+ * histograms (integer all-reduce over NCCL) and running A2..A6 from the sum.
+ *
+ * ewsjf_history_hist: A1 counting sort of d_len[n] into d_hist
+ *   (device, caller-owned, EWSJF_HIST_BINS + 1 uint32 entries; bin b = number
+ *   of lengths equal to b; bin 0 unused).  h_info[3] (host): lengths < 1,
+ *   lengths >= EWSJF_HIST_BINS (UNSUPPORTED when > 0), largest valid length.
+ *   Synchronises.
+ * ewsjf_partition_from_hist: A2..A6 of ewsjf_partition from a summed
+ *   histogram; max_len = largest length with a non-zero bin (all-reduce MAX of
+ *   h_info[2]), n_invalid = summed h_info[0] (reported as stats->n_invalid and
+ *   DOMAIN, as ewsjf_partition does).  The result is bit-identical to
+ *   ewsjf_partition over the concatenated history.  Bins are uint32: at most
+ *   2^32 - 1 history lengths per value.  Synchronises.                      */
+#define EWSJF_HIST_BINS (1 << 20)
+ewsjf_status ewsjf_history_hist(ewsjf_ctx *ctx, const int32_t *d_len, int64_t n, uint32_t *d_hist, int64_t *h_info);
+ewsjf_status ewsjf_partition_from_hist(ewsjf_ctx *ctx, const uint32_t *d_hist, int32_t max_len, int64_t n_invalid,
+                                       const ewsjf_partition_params *params, ewsjf_partition_t *out,
+                                       ewsjf_partition_stats *stats);
+
 /* --------------------------------------------------------------- tactical -- */
 /* Scoring part of Θ (§4.4.2): w_x(b̄) = a_x b̄ + b_x. */
 typedef struct { double a_b, b_b, a_u, b_u, a_f, b_f; } ewsjf_meta;

@@ -3,4 +3,4 @@
 include/ewsjf.h); this package is the thin torch binding.  No CPU fallback."""
 from . import _lib  # noqa: F401
 from .ewsjf import *  # noqa: F401,F403
-from ._lib import SELECT_SCORE, SELECT_FIFO, MIN_U, MAX_U, MAX_QUEUES  # noqa: F401
+from ._lib import SELECT_SCORE, SELECT_FIFO, MIN_U, MAX_U, MAX_QUEUES, HIST_BINS  # noqa: F401

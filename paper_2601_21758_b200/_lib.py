@@ -12,6 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libewsjf.so")
 
 MAX_QUEUES = 256
+HIST_BINS = 1 << 20
 MAX_K = 256
 
 OK, INVALID_ARG, DOMAIN, EMPTY, CAPACITY, CUDA_ERR, UNSUPPORTED = range(7)
@@ -99,6 +100,7 @@ SYMBOLS = [
     "ewsjf_score_select", "ewsjf_tick", "ewsjf_tick_host", "ewsjf_exchange_bytes", "ewsjf_tick_local",
     "ewsjf_tick_merge", "ewsjf_score_select_sweep", "ewsjf_ctx_set_timing", "ewsjf_ctx_get_timing",
     "ewsjf_ctx_get_phases", "ewsjf_batch_build", "ewsjf_prune_empty",
+    "ewsjf_history_hist", "ewsjf_partition_from_hist",
 ]
 
 _lib = None
@@ -142,6 +144,8 @@ def load() -> C.CDLL:
                                            P(SelectOut)]
     L.ewsjf_batch_build.argtypes = [V, V, I64, I64, P(SelectOut), I32, I32, P(Budget), V, V]
     L.ewsjf_prune_empty.argtypes = [P(Partition), V, I32, P(C.c_int32)]
+    L.ewsjf_history_hist.argtypes = [V, V, I64, V, P(C.c_int64)]
+    L.ewsjf_partition_from_hist.argtypes = [V, V, I32, I64, P(PartitionParams), P(Partition), P(PartitionStats)]
     for name in SYMBOLS:
         if name not in ("ewsjf_abi_version", "ewsjf_status_str", "ewsjf_last_error", "ewsjf_ctx_num_ctas",
                         "ewsjf_exchange_bytes"):

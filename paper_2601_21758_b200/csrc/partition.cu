@@ -733,51 +733,16 @@ ewsjf_status rp_alloc(ewsjf_ctx* ctx) {
 
 }  // namespace ewsjf
 
-extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, int64_t n,
-                                        const ewsjf_partition_params* p, ewsjf_partition_t* out,
-                                        ewsjf_partition_stats* stats) {
-    using namespace ewsjf;
-    if (!ctx) return EWSJF_ERR_INVALID_ARG;
-    if (!p || !out) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null params/out");
-    if (!(p->alpha > 1.0) || p->min_width < 1 || p->max_queues < 1 || p->max_queues > EWSJF_MAX_QUEUES ||
-        !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 || (p->merge_rule != 0 && p->merge_rule != 1))
-        return fail(ctx, EWSJF_ERR_INVALID_ARG, "partition params out of range (S:121)");
-    if (n < 0 || n > ctx->max_history) return fail(ctx, EWSJF_ERR_INVALID_ARG, "n=%lld > max_history", (long long)n);
-    if (n > 0 && !d_len) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null history");
+namespace ewsjf {
+// A2..A6 from a finished histogram (bins 1..lmax); S carries the A1 statistics.
+static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int lmax, const ewsjf_partition_params* p,
+                                 ewsjf_partition_t* out, ewsjf_partition_stats* stats, ewsjf_partition_stats& S) {
     RpScratch* R = ctx->rp;
-    if (!R) return fail(ctx, EWSJF_ERR_INVALID_ARG, "ctx created with max_history = 0");
-    CU(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
-    ewsjf_partition_stats S;
-    memset(&S, 0, sizeof S);
-    CU(cudaEventRecord(R->ev[0], st));
-    CU(cudaMemsetAsync(R->hist, 0, (size_t)(kHistMax + 1) * 4, st));
-    CU(cudaMemsetAsync(R->stat, 0, 16 * 8, st));
-    if (n > 0) {
-        LaunchScope ls(ctx, KIND_PARTITION);
-        CU(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4));
-        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_len, n, R->hist, R->stat);
-        CU(cudaGetLastError());
-    }
-    CU(cudaEventRecord(R->ev[1], st));
-    unsigned long long hs[3];
-    CU(cudaMemcpyAsync(hs, R->stat, 3 * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    S.n_invalid = (int64_t)hs[0];
-    S.n_valid = n - (int64_t)hs[0] - (int64_t)hs[1];
-    if (hs[1]) {
-        if (stats) *stats = S;
-        return fail(ctx, EWSJF_ERR_UNSUPPORTED, "%llu history lengths >= 2^20", hs[1]);
-    }
-    if (S.n_valid == 0) {
-        if (stats) *stats = S;
-        return fail(ctx, EWSJF_ERR_EMPTY, "no history length >= 1");
-    }
-    const int lmax = (int)hs[2];
     const int nb = (lmax + kRleChunk - 1) / kRleChunk;
     {
         LaunchScope ls(ctx, KIND_PARTITION);
-        rle_count_kernel<<<nb, kHT, 0, st>>>(R->hist, lmax, R->blk);
+        rle_count_kernel<<<nb, kHT, 0, st>>>(hist, lmax, R->blk);
     }
     {
         LaunchScope ls(ctx, KIND_PARTITION);
@@ -785,7 +750,7 @@ extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, in
     }
     {
         LaunchScope ls(ctx, KIND_PARTITION);
-        rle_write_kernel<<<nb, kHT, 0, st>>>(R->hist, lmax, R->blk, R->v, R->c, R->N, R->S1, R->S2);
+        rle_write_kernel<<<nb, kHT, 0, st>>>(hist, lmax, R->blk, R->v, R->c, R->N, R->S1, R->S2);
     }
     CU(cudaGetLastError());
     int64_t tot[4];
@@ -793,6 +758,11 @@ extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, in
     CU(cudaStreamSynchronize(st));
     const int64_t M = tot[0];
     S.distinct = M;
+    S.n_valid = tot[1];
+    if (M == 0) {
+        if (stats) *stats = S;
+        return fail(ctx, EWSJF_ERR_EMPTY, "no history length >= 1");
+    }
     const int k = p->coarse_k < M ? p->coarse_k : (int)M;
     S.k_used = k;
     if (k == 3) {
@@ -904,4 +874,106 @@ extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, in
     cudaEventElapsedTime(&ms, R->ev[0], R->ev[4]); S.ms_total = ms;
     if (stats) *stats = S;
     return S.n_invalid ? EWSJF_ERR_DOMAIN : EWSJF_OK;
+}
+}  // namespace ewsjf
+
+static ewsjf_status check_rp_params(ewsjf_ctx* ctx, const ewsjf_partition_params* p, ewsjf_partition_t* out) {
+    if (!p || !out) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null params/out");
+    if (!(p->alpha > 1.0) || p->min_width < 1 || p->max_queues < 1 || p->max_queues > EWSJF_MAX_QUEUES ||
+        !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 || (p->merge_rule != 0 && p->merge_rule != 1))
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "partition params out of range (S:121)");
+    return EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, int64_t n,
+                                        const ewsjf_partition_params* p, ewsjf_partition_t* out,
+                                        ewsjf_partition_stats* stats) {
+    using namespace ewsjf;
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    if (!p || !out) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null params/out");
+    if (!(p->alpha > 1.0) || p->min_width < 1 || p->max_queues < 1 || p->max_queues > EWSJF_MAX_QUEUES ||
+        !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 || (p->merge_rule != 0 && p->merge_rule != 1))
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "partition params out of range (S:121)");
+    if (n < 0 || n > ctx->max_history) return fail(ctx, EWSJF_ERR_INVALID_ARG, "n=%lld > max_history", (long long)n);
+    if (n > 0 && !d_len) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null history");
+    RpScratch* R = ctx->rp;
+    if (!R) return fail(ctx, EWSJF_ERR_INVALID_ARG, "ctx created with max_history = 0");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    ewsjf_partition_stats S;
+    memset(&S, 0, sizeof S);
+    CU(cudaEventRecord(R->ev[0], st));
+    CU(cudaMemsetAsync(R->hist, 0, (size_t)(kHistMax + 1) * 4, st));
+    CU(cudaMemsetAsync(R->stat, 0, 16 * 8, st));
+    if (n > 0) {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        CU(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4));
+        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_len, n, R->hist, R->stat);
+        CU(cudaGetLastError());
+    }
+    CU(cudaEventRecord(R->ev[1], st));
+    unsigned long long hs[3];
+    CU(cudaMemcpyAsync(hs, R->stat, 3 * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    S.n_invalid = (int64_t)hs[0];
+    S.n_valid = n - (int64_t)hs[0] - (int64_t)hs[1];
+    if (hs[1]) {
+        if (stats) *stats = S;
+        return fail(ctx, EWSJF_ERR_UNSUPPORTED, "%llu history lengths >= 2^20", hs[1]);
+    }
+    if (S.n_valid == 0) {
+        if (stats) *stats = S;
+        return fail(ctx, EWSJF_ERR_EMPTY, "no history length >= 1");
+    }
+    return rp_from_hist(ctx, R->hist, (int)hs[2], p, out, stats, S);
+}
+
+extern "C" ewsjf_status ewsjf_history_hist(ewsjf_ctx* ctx, const int32_t* d_len, int64_t n, uint32_t* d_hist,
+                                           int64_t* h_info) {
+    using namespace ewsjf;
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    if (!d_hist || !h_info || n < 0 || (n > 0 && !d_len)) return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad history_hist arguments");
+    RpScratch* R = ctx->rp;
+    if (!R) return fail(ctx, EWSJF_ERR_INVALID_ARG, "ctx created with max_history = 0");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    CU(cudaMemsetAsync(d_hist, 0, (size_t)(kHistMax + 1) * 4, st));
+    CU(cudaMemsetAsync(R->stat, 0, 16 * 8, st));
+    if (n > 0) {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        CU(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4));
+        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_len, n, (unsigned int*)d_hist, R->stat);
+        CU(cudaGetLastError());
+    }
+    unsigned long long hs[3];
+    CU(cudaMemcpyAsync(hs, R->stat, 3 * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    h_info[0] = (int64_t)hs[0];
+    h_info[1] = (int64_t)hs[1];
+    h_info[2] = (int64_t)hs[2];
+    return hs[1] ? fail(ctx, EWSJF_ERR_UNSUPPORTED, "%llu history lengths >= 2^20", hs[1]) : EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_partition_from_hist(ewsjf_ctx* ctx, const uint32_t* d_hist, int32_t max_len,
+                                                  int64_t n_invalid, const ewsjf_partition_params* p,
+                                                  ewsjf_partition_t* out, ewsjf_partition_stats* stats) {
+    using namespace ewsjf;
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    ewsjf_status c = check_rp_params(ctx, p, out);
+    if (c != EWSJF_OK) return c;
+    if (!d_hist || max_len < 0 || max_len >= kHistMax || n_invalid < 0)
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad histogram arguments");
+    RpScratch* R = ctx->rp;
+    if (!R) return fail(ctx, EWSJF_ERR_INVALID_ARG, "ctx created with max_history = 0");
+    CU(cudaSetDevice(ctx->device));
+    ewsjf_partition_stats S;
+    memset(&S, 0, sizeof S);
+    S.n_invalid = n_invalid;
+    CU(cudaEventRecord(R->ev[0], ctx->stream));
+    CU(cudaEventRecord(R->ev[1], ctx->stream));
+    if (max_len == 0) {
+        if (stats) *stats = S;
+        return fail(ctx, EWSJF_ERR_EMPTY, "no history length >= 1");
+    }
+    return rp_from_hist(ctx, (const unsigned int*)d_hist, max_len, p, out, stats, S);
 }

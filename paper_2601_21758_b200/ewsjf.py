@@ -17,6 +17,7 @@ __all__ = [
     "EwsjfError", "Context", "make_partition", "meta", "select_params", "partition_params", "weights_from_meta",
     "Outputs", "tick", "tick_host", "score_select", "route", "partition", "score_select_sweep",
     "exchange_bytes", "tick_local", "tick_merge", "tick_sharded", "batch_build", "prune_empty",
+    "history_hist", "partition_from_hist", "reduce_hist", "partition_sharded",
 ]
 
 
@@ -251,6 +252,53 @@ def partition(ctx: Context, length, params: L.PartitionParams | None = None):
     s = ctx.lib.ewsjf_partition(ctx.h, _ptr(length), length.numel(), C.byref(params), C.byref(out), C.byref(st))
     ctx.check(s, (L.OK, L.DOMAIN, L.EMPTY))
     return out, {f: getattr(st, f) for f, _ in L.PartitionStats._fields_}, s
+
+
+def history_hist(ctx: Context, length, hist_out=None):
+    """ewsjf_history_hist: A1 histogram of a device history (int32 view of the uint32
+    bins, HIST_BINS + 1 entries).  Returns (hist, {"invalid", "over", "max_len"})."""
+    _dev_check(length, torch.int32, "len")
+    hist = hist_out if hist_out is not None else torch.empty(L.HIST_BINS + 1, dtype=torch.int32, device=length.device)
+    _dev_check(hist, torch.int32, "hist_out")
+    info = (C.c_int64 * 3)()
+    ctx.use_current_stream()
+    s = ctx.lib.ewsjf_history_hist(ctx.h, _ptr(length), length.numel(), _ptr(hist), info)
+    ctx.check(s, (L.OK,))
+    return hist, {"invalid": info[0], "over": info[1], "max_len": info[2]}
+
+
+def partition_from_hist(ctx: Context, hist, max_len: int, n_invalid: int = 0,
+                        params: L.PartitionParams | None = None):
+    """ewsjf_partition_from_hist: A2..A6 from a (summed) histogram -> (Partition, stats, status)."""
+    _dev_check(hist, torch.int32, "hist")
+    params = params or partition_params()
+    ctx.use_current_stream()
+    out = L.Partition()
+    st = L.PartitionStats()
+    s = ctx.lib.ewsjf_partition_from_hist(ctx.h, _ptr(hist), max_len, n_invalid, C.byref(params), C.byref(out),
+                                          C.byref(st))
+    ctx.check(s, (L.OK, L.DOMAIN, L.EMPTY))
+    return out, {f: getattr(st, f) for f, _ in L.PartitionStats._fields_}, s
+
+
+def reduce_hist(hist, info: dict, group=None):
+    """All-reduce of the ranks' histograms (exact integer SUM) and of their A1
+    statistics (invalid: SUM, max_len: MAX) over ``group`` — in place on ``hist``."""
+    import torch.distributed as dist
+    dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+    t = torch.tensor([info["invalid"], info["over"]], dtype=torch.int64, device=hist.device)
+    m = torch.tensor([info["max_len"]], dtype=torch.int64, device=hist.device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    return hist, {"invalid": int(t[0]), "over": int(t[1]), "max_len": int(m[0])}
+
+
+def partition_sharded(ctx: Context, length_shard, params: L.PartitionParams | None = None, group=None):
+    """Refine-and-Prune of a history sharded across the ranks of ``group`` (NCCL):
+    local histogram, all-reduce, A2..A6 on every rank (identical, replicated result)."""
+    hist, info = history_hist(ctx, length_shard)
+    hist, info = reduce_hist(hist, info, group)
+    return partition_from_hist(ctx, hist, info["max_len"], info["invalid"], params)
 
 
 def score_select_sweep(ctx: Context, length, arrival, cost, qid, part: L.Partition, thetas: list[L.Meta],

@@ -101,3 +101,37 @@ def test_partition_many_segments_global_tree(E, orc, ctx):
     g = _both(E, orc, ctx, hist)
     assert g[1]["segments"] == 56_000
     _check(*g)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kind,n,seed", [("heavy", 300_000, 11), ("bimodal", 100_000, 12)])
+def test_partition_from_summed_shard_histograms(E, orc, ctx, world, kind, n, seed):
+    """Sharded history: the per-shard histograms summed (what
+    the NCCL all-reduce computes) give the partition of the whole history, bit for
+    bit, equal to the oracle's."""
+    h = workload.lengths(kind, n, seed).astype(np.int32)
+    h[::997] = 0                                                  # a few invalid lengths
+    dev = torch.from_numpy(h).cuda()
+    tot = None
+    inv, mx = 0, 0
+    for r in range(world):
+        a, b = workload.shard_range(n, r, world)
+        hist, info = E.history_hist(ctx, dev[a:b].contiguous())
+        tot = hist.clone() if tot is None else tot + hist
+        inv += info["invalid"]; mx = max(mx, info["max_len"])
+    gpart, gst, gs = E.partition_from_hist(ctx, tot, mx, inv)
+    fpart, fst, fs = E.partition(ctx, dev)
+    assert gs == fs
+    assert [tuple(q.values()) for q in gpart.queues()] == [tuple(q.values()) for q in fpart.queues()]
+    for k in ("n_valid", "n_invalid", "distinct", "segments", "merges"):
+        assert gst[k] == fst[k], k
+    os_, opart, ost = orc.partition(h)
+    _check(gpart, gst, gs, opart, ost, os_)
+
+
+def test_partition_from_hist_edge_cases(E, ctx):
+    z = torch.zeros(E.HIST_BINS + 1, dtype=torch.int32, device="cuda")
+    _, _, s = E.partition_from_hist(ctx, z, 0)
+    assert s == 3                                                  # EMPTY
+    _, _, s = E.partition_from_hist(ctx, z, 100)                   # max_len given, no mass
+    assert s == 3
