@@ -134,6 +134,8 @@ def lib():
                                P(Partition), P(SelectParams), C.c_int32, P(Budget), P(C.c_int64), P(C.c_int64)]
         L.or_prune_empty.restype = C.c_int32
         L.or_prune_empty.argtypes = [P(Partition), P(C.c_int32), P(C.c_int64), C.c_int32]
+        L.or_online_adjust.restype = C.c_int32
+        L.or_online_adjust.argtypes = [P(C.c_int32), C.c_int64, C.c_double, P(Partition)]
     return _lib
 
 
@@ -384,3 +386,11 @@ def prune_empty(part: Partition, empty_cnt, counts, threshold: int):
     c = np.ascontiguousarray(np.asarray(counts, np.int64))
     removed = lib().or_prune_empty(C.byref(p2), _p(e, C.c_int32), _p(c, C.c_int64), threshold)
     return p2, e[: p2.n], removed
+
+
+def online_adjust(window, part: Partition, max_shift: float = 0.25):
+    """O13: online adjust (R31) on a copy of ``part`` -> (new partition, boundaries moved)."""
+    w = _i32(window)
+    p2 = copy_partition(part)
+    moved = lib().or_online_adjust(_p(w, C.c_int32), len(w), max_shift, C.byref(p2))
+    return p2, moved

@@ -598,3 +598,42 @@ int32_t or_prune_empty(or_partition *part, int32_t *empty_cnt, const int64_t *co
     part->n = k;
     return removed;
 }
+
+/* ---------------------------------------------------------------- O13 ---- */
+int32_t or_online_adjust(const int32_t *window, int64_t n, double max_shift, or_partition *part) {
+    const int32_t nq = part->n;
+    if (nq < 2 || n <= 0) return 0;
+    int32_t newb[OR_MAXQ];
+    int32_t *loc = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    int32_t moved = 0;
+    for (int32_t i = 1; i < nq; i++) {
+        const or_queue *qa = &part->q[i - 1], *qb = &part->q[i];
+        const int32_t B = qb->min_len;
+        newb[i] = B;
+        if (qa->max_len != B) continue;                 /* not a shared boundary */
+        const int32_t L = qa->min_len, U = qb->max_len;
+        const int64_t ca = qa->count, cb = qb->count;
+        if (ca + cb == 0) continue;
+        int64_t m = 0;                                  /* the window's members in [L, U) */
+        for (int64_t r = 0; r < n; r++)
+            if (window[r] >= 1 && window[r] >= L && window[r] < U) loc[m++] = window[r];
+        if (m == 0) continue;
+        qsort(loc, (size_t)m, sizeof(int32_t), cmp_i32);
+        const int64_t k = (m * ca + (ca + cb) - 1) / (ca + cb);     /* ceil(m ca / (ca + cb)) */
+        const int32_t T = k == 0 ? L : loc[k - 1] + 1;
+        int64_t d = (int64_t)T - B;
+        const int64_t left = (int64_t)floor(max_shift * (double)(B - L));
+        const int64_t right = (int64_t)floor(max_shift * (double)(U - B));
+        if (d < -left) d = -left;
+        if (d > right) d = right;
+        newb[i] = (int32_t)(B + d);
+    }
+    for (int32_t i = 1; i < nq; i++) {
+        if (newb[i] == part->q[i].min_len) continue;
+        part->q[i - 1].max_len = newb[i];
+        part->q[i].min_len = newb[i];
+        moved++;
+    }
+    free(loc);
+    return moved;
+}

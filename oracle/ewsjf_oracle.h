@@ -196,6 +196,21 @@ int64_t or_batch(const int32_t *len, const float *arrival, const float *cost, co
  * in/out by position (compacted like the queues).  Returns queues removed. */
 int32_t or_prune_empty(or_partition *part, int32_t *empty_cnt, const int64_t *count, int32_t threshold);
 
+/* O13 — online adjust mode ("lightweight adjustments ... statistical
+ * heuristics on recent data", reading R31).  For every interior
+ * boundary B shared by adjacent queues a = [L, B) and b = [B, U) (only where
+ * a.max_len == b.min_len): with c_a, c_b the queues' history counts and the
+ * window's m members in [L, U) sorted v_0 <= ... <= v_{m-1}, the local
+ * empirical quantile is the smallest x with #(v < x) * (c_a + c_b) >= m * c_a,
+ * i.e. T = L if k = ceil(m c_a / (c_a + c_b)) is 0, else v_{k-1} + 1.  B moves
+ * toward T by at most floor(max_shift * (B - L)) leftwards and
+ * floor(max_shift * (U - B)) rightwards (fp64 products), all boundaries from
+ * the original bounds at once; m = 0 or c_a + c_b = 0 -> no move.  Lengths
+ * < 1 in the window are ignored.  max_shift in [0, 0.5) keeps every queue's
+ * width >= 1.  Profiles (counts, sums) are not re-binned.  Returns the number
+ * of boundaries moved. */
+int32_t or_online_adjust(const int32_t *window, int64_t n, double max_shift, or_partition *part);
+
 #ifdef __cplusplus
 }
 #endif

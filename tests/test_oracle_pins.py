@@ -655,3 +655,85 @@ def test_prune_empty_threshold_strict_and_renumbers(orc):
     assert removed == 1
     assert [(q["min_len"], q["index"]) for q in p2.queues()] == [(10, 1), (20, 2), (30, 3)]
     assert list(e2) == [1, 5, 5]
+
+
+# ------------------------------------------------- O13: online adjust (R31) ---
+def _counted(orc, bounds, counts):
+    p = orc.make_partition(bounds)
+    for i, c in enumerate(counts):
+        p.q[i].count = c
+    return p
+
+
+def test_online_adjust_hand_example(orc):
+    """Window entirely inside queue [10,20): only that queue's two boundaries move
+    (S:178), each clamped to floor(0.25 * adjacent width) = 2: local targets 13
+    (k = ceil(4*10/20) = 2 -> v_1 + 1) for both."""
+    p = _counted(orc, [(1, 10), (10, 20), (20, 30)], [10, 10, 10])
+    p2, moved = orc.online_adjust([12, 12, 12, 12], p, 0.25)
+    assert moved == 2
+    assert [(q["min_len"], q["max_len"]) for q in p2.queues()] == [(1, 12), (12, 18), (18, 30)]
+    p3, moved = orc.online_adjust([15, 16, 17, 18, 25], _counted(orc, [(1, 10), (10, 20), (20, 30)], [0, 10, 10]), 0.25)
+    # boundary 10: c_a = 0 -> k = 0 -> T = L = 1, clamped to 10 - floor(0.25*9) = 8;
+    # boundary 20: members 15..18, 25 -> k = ceil(5*10/20) = 3 -> T = 18, d = -2 (limit 2)
+    assert [(q["min_len"], q["max_len"]) for q in p3.queues()] == [(1, 8), (8, 18), (18, 30)]
+    assert moved == 2
+
+
+def test_online_adjust_identity_cases(orc):
+    p = _counted(orc, [(1, 10), (10, 20), (20, 30)], [10, 10, 10])
+    for w, s in (([], 0.25), ([5, 15, 25] * 10, 0.0), ([0, -3], 0.25)):
+        p2, moved = orc.online_adjust(np.array(w, np.int32), p, s)
+        assert moved == 0 and [(q["min_len"], q["max_len"]) for q in p2.queues()] == [(1, 10), (10, 20), (20, 30)]
+
+
+def _adjust_brute(bounds, counts, window, s):
+    """The definition searched over every x (no order-statistic closed form)."""
+    new = [b[0] for b in bounds] + [bounds[-1][1]]
+    out = list(new)
+    for i in range(1, len(bounds)):
+        L, B, U = bounds[i - 1][0], bounds[i][0], bounds[i][1]
+        if bounds[i - 1][1] != B:
+            continue
+        ca, cb = counts[i - 1], counts[i]
+        loc = [w for w in window if w >= 1 and L <= w < U]
+        m = len(loc)
+        if m == 0 or ca + cb == 0:
+            continue
+        T = next(x for x in range(L, U + 1) if sum(v < x for v in loc) * (ca + cb) >= m * ca)
+        d = max(-math.floor(s * (B - L)), min(math.floor(s * (U - B)), T - B))
+        out[i] = B + d
+    return out
+
+
+@settings(max_examples=150, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(st.lists(st.integers(1, 12), min_size=1, max_size=6), st.lists(st.integers(0, 20), min_size=6, max_size=6),
+       st.lists(st.integers(-2, 80), max_size=40), st.sampled_from([0.0, 0.1, 0.25, 0.4, 0.49]))
+def test_online_adjust_matches_definition_and_invariants(orc, widths, counts, window, s):
+    b, bounds = 1, []
+    for w in widths:
+        bounds.append((b, b + w)); b += w
+    counts = counts[: len(bounds)]
+    p = _counted(orc, bounds, counts)
+    p2, moved = orc.online_adjust(np.array(window, np.int32), p, s)
+    q2 = p2.queues()
+    edges = [q2[0]["min_len"]] + [q["max_len"] for q in q2]
+    assert edges == _adjust_brute(bounds, counts, window, s)
+    assert all(q["max_len"] > q["min_len"] for q in q2)                        # width >= 1, order kept
+    assert all(q2[i]["max_len"] == q2[i + 1]["min_len"] for i in range(len(q2) - 1))
+    assert moved == sum(e != o for e, o in zip(edges, [bb[0] for bb in bounds] + [bounds[-1][1]]))
+
+
+def test_online_adjust_same_distribution_is_near_identity(orc):
+    """a window drawn like the history moves each boundary by little; under
+    quantile matching an interior boundary with mass on both sides moves by at
+    most a few lengths (here the 32-quantile partition of heavy(200k))."""
+    import workload
+    hist = workload.heavy(200_000, 3)
+    bounds = workload.quantile_bounds(hist, 16)
+    counts = [int(((hist >= lo) & (hist < hi)).sum()) for lo, hi in bounds]
+    p = _counted(orc, bounds, counts)
+    p2, _ = orc.online_adjust(workload.heavy(200_000, 4), p, 0.25)
+    for (lo, hi), q in zip(bounds, p2.queues()):
+        w = hi - lo
+        assert abs(q["min_len"] - lo) <= max(2, 0.05 * w)
