@@ -180,6 +180,19 @@ ewsjf_status ewsjf_partition_from_hist(ewsjf_ctx *ctx, const uint32_t *d_hist, i
                                        const ewsjf_partition_params *params, ewsjf_partition_t *out,
                                        ewsjf_partition_stats *stats);
 
+/* Online adjust mode ("lightweight adjustments ... statistical
+ * heuristics on recent data"; reading R31 in DESIGN.md): each
+ * interior boundary B shared by queues [L, B) and [B, U) moves toward the
+ * local empirical quantile of the window d_window[n] (device, prompt lengths;
+ * < 1 ignored) restricted to [L, U) that keeps the history split
+ * q[a].count : q[b].count, by at most floor(max_shift * (B - L)) left /
+ * floor(max_shift * (U - B)) right; all boundaries from the original bounds.
+ * Updates *part in place (bounds only; version bumped if any moved), *moved
+ * (nullable) = boundaries moved.  max_shift in [0, 0.5) (S:191 default 0.25),
+ * else INVALID_ARG; window lengths >= 2^20 -> UNSUPPORTED.  Synchronises.   */
+ewsjf_status ewsjf_online_adjust(ewsjf_ctx *ctx, const int32_t *d_window, int64_t n, double max_shift,
+                                 ewsjf_partition_t *part, int32_t *moved);
+
 /* --------------------------------------------------------------- tactical -- */
 /* Scoring part of Θ (§4.4.2): w_x(b̄) = a_x b̄ + b_x. */
 typedef struct { double a_b, b_b, a_u, b_u, a_f, b_f; } ewsjf_meta;

@@ -100,7 +100,7 @@ SYMBOLS = [
     "ewsjf_score_select", "ewsjf_tick", "ewsjf_tick_host", "ewsjf_exchange_bytes", "ewsjf_tick_local",
     "ewsjf_tick_merge", "ewsjf_score_select_sweep", "ewsjf_ctx_set_timing", "ewsjf_ctx_get_timing",
     "ewsjf_ctx_get_phases", "ewsjf_batch_build", "ewsjf_prune_empty",
-    "ewsjf_history_hist", "ewsjf_partition_from_hist",
+    "ewsjf_history_hist", "ewsjf_partition_from_hist", "ewsjf_online_adjust",
 ]
 
 _lib = None
@@ -145,6 +145,7 @@ def load() -> C.CDLL:
     L.ewsjf_batch_build.argtypes = [V, V, I64, I64, P(SelectOut), I32, I32, P(Budget), V, V]
     L.ewsjf_prune_empty.argtypes = [P(Partition), V, I32, P(C.c_int32)]
     L.ewsjf_history_hist.argtypes = [V, V, I64, V, P(C.c_int64)]
+    L.ewsjf_online_adjust.argtypes = [V, V, I64, C.c_double, P(Partition), P(C.c_int32)]
     L.ewsjf_partition_from_hist.argtypes = [V, V, I32, I64, P(PartitionParams), P(Partition), P(PartitionStats)]
     for name in SYMBOLS:
         if name not in ("ewsjf_abi_version", "ewsjf_status_str", "ewsjf_last_error", "ewsjf_ctx_num_ctas",

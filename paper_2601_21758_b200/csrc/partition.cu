@@ -14,6 +14,7 @@
 //                      every gap with g*(n-1) > alpha*span (R10-R14)
 //  A5+A6 prune_kernel  midpoint finalisation (R15) then Eq. 3 greedy merges with
 //                      a 32-ary tournament tree over adjacent pairs (R16-R18)
+#include <climits>
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
@@ -976,4 +977,142 @@ extern "C" ewsjf_status ewsjf_partition_from_hist(ewsjf_ctx* ctx, const uint32_t
         return fail(ctx, EWSJF_ERR_EMPTY, "no history length >= 1");
     }
     return rp_from_hist(ctx, (const unsigned int*)d_hist, max_len, p, out, stats, S);
+}
+
+// ------------------------------------------- online adjust (R31) ---
+// One CTA per interior boundary B between queues [L, B) and [B, U): the window's
+// histogram over [L, U) is block-scanned in chunks of kHT bins; the target T is
+// the smallest x with (#window < x in [L, U)) * (c_a + c_b) >= m * c_a (m = the
+// window's members in [L, U)), then the move is clamped to floor(max_shift *
+// adjacent width) on each side — the same fp64 product as the oracle.
+namespace ewsjf {
+struct AdjustArgs {
+    int32_t L[EWSJF_MAX_QUEUES], B[EWSJF_MAX_QUEUES], U[EWSJF_MAX_QUEUES];
+    int64_t ca[EWSJF_MAX_QUEUES], cb[EWSJF_MAX_QUEUES];
+    double max_shift;
+};
+
+__device__ __forceinline__ int64_t block_excl_scan(int64_t x, int64_t* sm, int64_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) sm[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = lane < (int)(blockDim.x >> 5) ? sm[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        sm[32 + lane] = w;                    // inclusive warp-sum prefix
+    }
+    __syncthreads();
+    const int64_t before = warp ? sm[32 + warp - 1] : 0;
+    *total = sm[32 + (blockDim.x >> 5) - 1];
+    __syncthreads();
+    return before + v - x;
+}
+
+__global__ void __launch_bounds__(kHT) adjust_kernel(const unsigned int* __restrict__ hist,
+                                                     const __grid_constant__ AdjustArgs A, int32_t* newb) {
+    __shared__ int64_t sm[64];
+    __shared__ int s_hit;
+    const int i = blockIdx.x + 1;                               // boundary index 1..nq-1
+    const int32_t L = A.L[i], B = A.B[i], U = A.U[i];
+    const int64_t ca = A.ca[i], cb = A.cb[i];
+    if (L < 0 || ca + cb == 0) { if (threadIdx.x == 0) newb[i] = B; return; }   // L < 0: not shared
+    // m = window members in [L, U)
+    int64_t part = 0;
+    for (int x = L + (int)threadIdx.x; x < U; x += blockDim.x) part += hist[x];
+    int64_t m;
+    block_excl_scan(part, sm, &m);
+    if (m == 0) { if (threadIdx.x == 0) newb[i] = B; return; }
+    // smallest x in [L, U] with cum(< x) * (ca + cb) >= m * ca
+    const int64_t rhs = m * ca, den = ca + cb;
+    int32_t T = U;
+    int64_t carry = 0;
+    for (int x0 = L; x0 < U; x0 += blockDim.x) {
+        const int x = x0 + (int)threadIdx.x;
+        const int64_t h = x < U ? (int64_t)hist[x] : 0;
+        int64_t tot;
+        const int64_t before = carry + block_excl_scan(h, sm, &tot);   // cum(< x)
+        if (threadIdx.x == 0) s_hit = INT_MAX;
+        __syncthreads();
+        if (x < U && before * den >= rhs) atomicMin(&s_hit, x);
+        __syncthreads();
+        if (s_hit != INT_MAX) { T = s_hit; break; }
+        carry += tot;
+    }
+    if (threadIdx.x == 0) {
+        int64_t d = (int64_t)T - B;
+        const int64_t left = (int64_t)floor(__dmul_rn(A.max_shift, (double)(B - L)));
+        const int64_t right = (int64_t)floor(__dmul_rn(A.max_shift, (double)(U - B)));
+        if (d < -left) d = -left;
+        if (d > right) d = right;
+        newb[i] = (int32_t)(B + d);
+    }
+}
+}  // namespace ewsjf
+
+extern "C" ewsjf_status ewsjf_online_adjust(ewsjf_ctx* ctx, const int32_t* d_window, int64_t n, double max_shift,
+                                            ewsjf_partition_t* part, int32_t* moved) {
+    using namespace ewsjf;
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    if (!part || n < 0 || (n > 0 && !d_window) || !(max_shift >= 0.0 && max_shift < 0.5) || part->n < 0 ||
+        part->n > EWSJF_MAX_QUEUES)
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "bad online_adjust arguments (max_shift in [0, 0.5))");
+    if (moved) *moved = 0;
+    const int nq = part->n;
+    if (nq < 2 || n == 0) return EWSJF_OK;
+    RpScratch* R = ctx->rp;
+    if (!R) return fail(ctx, EWSJF_ERR_INVALID_ARG, "ctx created with max_history = 0");
+    for (int i = 1; i < nq; i++)
+        if (part->q[i].min_len < part->q[i - 1].max_len || part->q[i].max_len > kHistMax)
+            return fail(ctx, EWSJF_ERR_INVALID_ARG, "partition not sorted / bounds above 2^20");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    CU(cudaMemsetAsync(R->hist, 0, (size_t)(kHistMax + 1) * 4, st));
+    CU(cudaMemsetAsync(R->stat, 0, 16 * 8, st));
+    {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        CU(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4));
+        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_window, n, R->hist, R->stat);
+    }
+    static thread_local AdjustArgs A;
+    A.max_shift = max_shift;
+    for (int i = 1; i < nq; i++) {
+        const ewsjf_queue& a = part->q[i - 1];
+        const ewsjf_queue& b = part->q[i];
+        A.L[i] = a.max_len == b.min_len ? a.min_len : -1;      // only shared boundaries move
+        A.B[i] = b.min_len;
+        A.U[i] = b.max_len;
+        A.ca[i] = a.count;
+        A.cb[i] = b.count;
+    }
+    {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        adjust_kernel<<<nq - 1, kHT, 0, st>>>(R->hist, A, R->seg);
+    }
+    CU(cudaGetLastError());
+    int32_t nb[EWSJF_MAX_QUEUES];
+    unsigned long long hs[3];
+    CU(cudaMemcpyAsync(nb, R->seg, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(hs, R->stat, 3 * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (hs[1]) return fail(ctx, EWSJF_ERR_UNSUPPORTED, "%llu window lengths >= 2^20", hs[1]);
+    int32_t mv = 0;
+    for (int i = 1; i < nq; i++) {
+        if (nb[i] == part->q[i].min_len) continue;
+        part->q[i - 1].max_len = nb[i];
+        part->q[i].min_len = nb[i];
+        mv++;
+    }
+    if (mv) part->version++;
+    if (moved) *moved = mv;
+    return EWSJF_OK;
 }

@@ -17,7 +17,7 @@ __all__ = [
     "EwsjfError", "Context", "make_partition", "meta", "select_params", "partition_params", "weights_from_meta",
     "Outputs", "tick", "tick_host", "score_select", "route", "partition", "score_select_sweep",
     "exchange_bytes", "tick_local", "tick_merge", "tick_sharded", "batch_build", "prune_empty",
-    "history_hist", "partition_from_hist", "reduce_hist", "partition_sharded",
+    "history_hist", "partition_from_hist", "reduce_hist", "partition_sharded", "online_adjust",
 ]
 
 
@@ -279,6 +279,17 @@ def partition_from_hist(ctx: Context, hist, max_len: int, n_invalid: int = 0,
                                           C.byref(st))
     ctx.check(s, (L.OK, L.DOMAIN, L.EMPTY))
     return out, {f: getattr(st, f) for f, _ in L.PartitionStats._fields_}, s
+
+
+def online_adjust(ctx: Context, window, part: L.Partition, max_shift: float = 0.25) -> int:
+    """ewsjf_online_adjust: bounded local-quantile boundary shifts from a recent
+    window (device int32 lengths); updates ``part`` in place, returns boundaries moved."""
+    _dev_check(window, torch.int32, "window")
+    ctx.use_current_stream()
+    mv = C.c_int32(0)
+    s = ctx.lib.ewsjf_online_adjust(ctx.h, _ptr(window), window.numel(), max_shift, C.byref(part), C.byref(mv))
+    ctx.check(s, (L.OK,))
+    return mv.value
 
 
 def reduce_hist(hist, info: dict, group=None):
