@@ -318,6 +318,19 @@ def main():
         psrc = "balanced 32-quantile partition of heavy(1M, seed 301)"
     theta = E.meta(**workload.THETA0)
     sp = E.select_params(k=args.k, mode=mode, now=workload.NOW)
+    if args.partition == "rp":
+        # online adjust mode (R31) of that partition from a 1M recent window (on a copy)
+        win = torch.from_numpy(workload.heavy(1_000_000, 303)).to(dev)
+        padj = type(part).from_buffer_copy(part)
+        E.online_adjust(ctx, win, padj)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(5):
+            padj = type(part).from_buffer_copy(part)
+            moved = E.online_adjust(ctx, win, padj)
+        strategic["online_adjust"] = {"window": 1_000_000, "ms_per_call": (time.perf_counter() - t0) * 1e3 / 5,
+                                      "boundaries_moved": moved, "max_shift": 0.25,
+                                      "note": "synchronous call incl. window histogram + one CTA per boundary"}
 
     # ---- pool: this rank's 10M shard, 3 rotating copies in HBM
     pool = workload.pool("heavy", n, 302 + 1000 * rank)
