@@ -56,6 +56,8 @@ __global__ void __launch_bounds__(kBThreads, 1) batch_build_kernel(BatchArgs A) 
     __shared__ int32_t s_off[EWSJF_MAX_QUEUES];
     __shared__ int32_t s_bad, s_nb;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // the primary is needed only in phase 2: issue its load now, ahead of the gathers
+    const int prim0 = warp == 0 ? __ldg(&A.summary->primary) : 0;
     if (threadIdx.x == 0) { s_bad = 0; s_nb = 0; }
     __syncthreads();
     // ---- phase 1: per-queue prefix of lengths over the FIFO rows.  All of a
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(kBThreads, 1) batch_build_kernel(BatchArgs A) 
     __syncthreads();
     // ---- phase 2: GreedyFill from the primary, Backfill nearest-first (lower first)
     if (warp == 0) {
-        const int prim = A.summary->primary;
+        const int prim = prim0;
         int64_t nb = 0, tok = 0;
         if (!s_bad && prim >= 0 && prim < A.nq && A.max_req > 0) {
             for (int d = 0; d < A.nq && nb < A.max_req; d++) {

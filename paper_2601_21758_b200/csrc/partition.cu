@@ -1026,28 +1026,27 @@ __global__ void __launch_bounds__(kHT) adjust_kernel(const unsigned int* __restr
     const int32_t L = A.L[i], B = A.B[i], U = A.U[i];
     const int64_t ca = A.ca[i], cb = A.cb[i];
     if (L < 0 || ca + cb == 0) { if (threadIdx.x == 0) newb[i] = B; return; }   // L < 0: not shared
-    // m = window members in [L, U)
+    // one contiguous slab of bins per thread: slab sums, one block scan (m = total)
+    const int width = U - L;
+    const int slab = (width + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int xs = L + (int)threadIdx.x * slab, xe = min(U, xs + slab);
     int64_t part = 0;
-    for (int x = L + (int)threadIdx.x; x < U; x += blockDim.x) part += hist[x];
+    for (int x = xs; x < xe; x++) part += hist[x];
     int64_t m;
-    block_excl_scan(part, sm, &m);
+    const int64_t before = block_excl_scan(part, sm, &m);       // window members in [L, xs)
     if (m == 0) { if (threadIdx.x == 0) newb[i] = B; return; }
-    // smallest x in [L, U] with cum(< x) * (ca + cb) >= m * ca
+    // smallest x in [L, U] with cum(< x) * (ca + cb) >= m * ca (x = U always qualifies);
+    // cum is monotone in x, so each thread walks its slab until it qualifies
     const int64_t rhs = m * ca, den = ca + cb;
-    int32_t T = U;
-    int64_t carry = 0;
-    for (int x0 = L; x0 < U; x0 += blockDim.x) {
-        const int x = x0 + (int)threadIdx.x;
-        const int64_t h = x < U ? (int64_t)hist[x] : 0;
-        int64_t tot;
-        const int64_t before = carry + block_excl_scan(h, sm, &tot);   // cum(< x)
-        if (threadIdx.x == 0) s_hit = INT_MAX;
-        __syncthreads();
-        if (x < U && before * den >= rhs) atomicMin(&s_hit, x);
-        __syncthreads();
-        if (s_hit != INT_MAX) { T = s_hit; break; }
-        carry += tot;
+    if (threadIdx.x == 0) s_hit = U;
+    __syncthreads();
+    int64_t cum = before;
+    for (int x = xs; x < xe; x++) {
+        if (cum * den >= rhs) { atomicMin(&s_hit, x); break; }
+        cum += hist[x];
     }
+    __syncthreads();
+    const int32_t T = s_hit;
     if (threadIdx.x == 0) {
         int64_t d = (int64_t)T - B;
         const int64_t left = (int64_t)floor(__dmul_rn(A.max_shift, (double)(B - L)));
