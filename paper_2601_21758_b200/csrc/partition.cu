@@ -980,8 +980,9 @@ extern "C" ewsjf_status ewsjf_partition_from_hist(ewsjf_ctx* ctx, const uint32_t
 }
 
 // ------------------------------------------- online adjust (R31) ---
-// One CTA per interior boundary B between queues [L, B) and [B, U): the window's
-// histogram over [L, U) is block-scanned in chunks of kHT bins; the target T is
+// One CTA per interior boundary B between queues [L, B) and [B, U): each thread
+// sums one contiguous slab of the window's histogram over [L, U), one block scan
+// gives every slab's starting count, and each thread walks its slab; the target T is
 // the smallest x with (#window < x in [L, U)) * (c_a + c_b) >= m * c_a (m = the
 // window's members in [L, U)), then the move is clamped to floor(max_shift *
 // adjacent width) on each side — the same fp64 product as the oracle.
