@@ -508,6 +508,9 @@ __global__ void __launch_bounds__(kHT, 1)
 constexpr uint64_t kDead = ~0ull;
 constexpr uint16_t kNone = 0xffffu;
 constexpr int kPL = 5;
+// tree fan-out: 128 (4 children per lane) when the leaves are in shared memory,
+// 32 when they are read from global scratch (fewer bytes per node on the L2 path)
+__host__ __device__ constexpr int prune_fan(bool leaf_global) { return leaf_global ? 32 : 128; }
 
 __global__ void prune_prep_kernel(const int32_t* __restrict__ v, const int64_t* __restrict__ N,
                                   const int64_t* __restrict__ S1, const int32_t* __restrict__ seg, int64_t M,
@@ -538,7 +541,7 @@ __host__ __device__ inline size_t prune_smem_bytes(int m, int* nl_out, int* lv_o
         if (nl > 0) off += cnt;
         nl++;
         if (cnt == 1) break;
-        cnt = (cnt + 31) / 32;
+        cnt = (cnt + prune_fan(leaf_global) - 1) / prune_fan(leaf_global);
     }
     if (nl_out) *nl_out = nl;
     // leaves u64[npair] | inner keys u64[off] | inner idx i32[off] | next, prev u16[m + 1]
@@ -556,6 +559,7 @@ __global__ void __launch_bounds__(kHT, 1)
                       int cap_m, int max_queues, double eps, int rule, int32_t* q_lo, int32_t* q_hi, int64_t* q_n,
                       int64_t* q_s1, int64_t* q_s2, int64_t* merges_out, int32_t* done) {
     extern __shared__ __align__(16) unsigned char sm[];
+    constexpr int kFan = prune_fan(LG), kFanSh = LG ? 5 : 7;
     const int m0 = rout[0];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (LG) {
@@ -573,7 +577,7 @@ __global__ void __launch_bounds__(kHT, 1)
             lv_off[l] = off; lv_n[l] = cnt;
             if (l > 0) off += cnt;
             if (cnt == 1 && nl == kPL) nl = l + 1;
-            cnt = (cnt + 31) / 32;
+            cnt = (cnt + kFan - 1) / kFan;   // kFan = prune_fan(LG)
         }
     }
     const int npair = m0 - 1;
@@ -605,12 +609,20 @@ __global__ void __launch_bounds__(kHT, 1)
     // node (l, j) <- best of its <= 32 children at level l-1 (one warp)
     auto node = [&](int l, int j) {
         if (j >= lv_n[l]) return;                           // warp-uniform
-        const int c = j * 32 + lane;
+        // kFan children: lane holds kFan/32 consecutive ones (lowest index wins ties locally,
+        // then the lowest lane across the warp)
         uint64_t k = kDead;
         int id = -1;
-        if (c < lv_n[l - 1]) {
-            if (l == 1) { k = LG ? __ldcg(leaf + c) : leaf[c]; id = k == kDead ? -1 : c; }
-            else { k = ikey[lv_off[l - 1] + c]; id = iidx[lv_off[l - 1] + c]; }
+#pragma unroll
+        for (int u = 0; u < kFan / 32; u++) {
+            const int c = j * kFan + lane * (kFan / 32) + u;
+            uint64_t kc = kDead;
+            int ic = -1;
+            if (c < lv_n[l - 1]) {
+                if (l == 1) { kc = LG ? __ldcg(leaf + c) : leaf[c]; ic = kc == kDead ? -1 : c; }
+                else { kc = ikey[lv_off[l - 1] + c]; ic = iidx[lv_off[l - 1] + c]; }
+            }
+            if (kc < k) { k = kc; id = ic; }
         }
         const unsigned hi = (unsigned)(k >> 32), lw = (unsigned)k;
         const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
@@ -656,7 +668,7 @@ __global__ void __launch_bounds__(kHT, 1)
 #pragma unroll
         for (int l = 1; l < kPL; l++) {
             if (l >= nl) break;
-            a >>= 5; bb >>= 5; c >>= 5;
+            a >>= kFanSh; bb >>= kFanSh; c >>= kFanSh;
             node(l, a);
             if (bb != a) node(l, bb);
             if (c != a && c != bb) node(l, c);
