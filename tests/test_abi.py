@@ -51,6 +51,24 @@ def test_library_loads_and_host_calls_work(lib):
     # invalid arguments are rejected before any device work
     assert L.ewsjf_ctx_create(0, None, -1, 0, 64, C.byref(C.c_void_p())) == 1
     assert L.ewsjf_ctx_create(0, None, 0, 0, 0, C.byref(C.c_void_p())) == 1
+    # the §8f entry points reject a null context before any device work
+    so = lib.SelectOut()
+    b = lib.Budget(16, 0, 1000)
+    assert L.ewsjf_batch_build(None, None, 0, 0, C.byref(so), 16, 1, C.byref(b), None, None) == 1
+    assert L.ewsjf_online_adjust(None, None, 0, 0.25, C.byref(p), None) == 1
+    assert L.ewsjf_partition_from_hist(None, None, 0, 0, None, C.byref(p), None) == 1
+    assert L.ewsjf_history_hist(None, None, 0, None, None) == 1
+    # Alg. 1 lines 8-12 are host bookkeeping: no GPU needed
+    p2 = lib.Partition()
+    p2.n = 3
+    for i, (lo, hi) in enumerate([(1, 10), (10, 20), (20, 30)]):
+        p2.q[i].id, p2.q[i].index, p2.q[i].min_len, p2.q[i].max_len = i, i + 1, lo, hi
+    p2.q[1].empty_count = 2
+    cnt = (C.c_int64 * 3)(5, 0, 7)
+    rm = C.c_int32(-1)
+    assert L.ewsjf_prune_empty(C.byref(p2), cnt, 2, C.byref(rm)) == 0
+    assert rm.value == 1 and p2.n == 2 and (p2.q[1].min_len, p2.q[1].index) == (20, 2)
+    assert L.ewsjf_prune_empty(C.byref(p2), cnt, -1, None) == 1
 
 
 def test_struct_layouts_match_the_header(lib, tmp_path):
