@@ -110,6 +110,8 @@ typedef struct {
     double  epsilon;
     int32_t coarse_k;
     int32_t merge_rule;
+    int32_t gap_rule;    /* 0: Eq. 2 gaps over the multiset D (R10, default);
+                            1: over the set of distinct lengths (SURVEY ambiguity 10 variant) */
 } ewsjf_partition_params;
 
 /* One queue q_i = [min_len, max_len). */

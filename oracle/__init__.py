@@ -62,7 +62,8 @@ class Partition(C.Structure):
 
 class Params(C.Structure):
     _fields_ = [("alpha", C.c_double), ("min_width", C.c_int32), ("max_queues", C.c_int32),
-                ("epsilon", C.c_double), ("coarse_k", C.c_int32), ("merge_rule", C.c_int32)]
+                ("epsilon", C.c_double), ("coarse_k", C.c_int32), ("merge_rule", C.c_int32),
+                ("gap_rule", C.c_int32)]
 
 
 class PartitionStats(C.Structure):
@@ -212,8 +213,8 @@ def prune(lo, hi, cnt, s1, s2, max_queues, eps, rule=MIN_U):
     return lo[:m], hi[:m], cnt[:m], s1[:m], s2[:m], merges.value
 
 
-def params(alpha=2.0, min_width=1, max_queues=32, epsilon=1e-6, coarse_k=3, merge_rule=MIN_U) -> Params:
-    return Params(alpha, min_width, max_queues, epsilon, coarse_k, merge_rule)
+def params(alpha=2.0, min_width=1, max_queues=32, epsilon=1e-6, coarse_k=3, merge_rule=MIN_U, gap_rule=0) -> Params:
+    return Params(alpha, min_width, max_queues, epsilon, coarse_k, merge_rule, gap_rule)
 
 
 def partition(lengths, **kw):

@@ -180,7 +180,7 @@ int or_partition_run(const int32_t *len, int64_t n, const or_params *p,
     memset(out, 0, sizeof *out);
     if (!(p->alpha > 1.0) || p->min_width < 1 || p->max_queues < 1 || p->max_queues > OR_MAXQ ||
         !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 ||
-        (p->merge_rule != OR_MIN_U && p->merge_rule != OR_MAX_U) || n < 0)
+        (p->merge_rule != OR_MIN_U && p->merge_rule != OR_MAX_U) || (p->gap_rule != 0 && p->gap_rule != 1) || n < 0)
         return OR_INVALID;
     size_t nn = (size_t)(n > 0 ? n : 1);
     int32_t *v = (int32_t *)malloc(sizeof(int32_t) * nn);
@@ -210,8 +210,13 @@ int or_partition_run(const int32_t *len, int64_t n, const or_params *p,
     int64_t *seg = (int64_t *)malloc(sizeof(int64_t) * (size_t)(M + 1));
     int64_t m = 0;
     int32_t depth = 0;
+    /* gap_rule 1 (set reading of G): Eq. 2 counts distinct lengths, i.e. the
+     * prefix of a multiplicity-1 multiset: Nset[i] = i */
+    int64_t *Nset = (int64_t *)malloc(sizeof(int64_t) * (size_t)(M + 1));
+    for (int64_t i = 0; i <= M; i++) Nset[i] = i;
     for (int i = 0; i + 1 < nb; i++)
-        m += or_refine(v, N, bounds[i], bounds[i + 1], p->alpha, p->min_width, seg + m, &depth);
+        m += or_refine(v, p->gap_rule ? Nset : N, bounds[i], bounds[i + 1], p->alpha, p->min_width, seg + m, &depth);
+    free(Nset);
     seg[m] = M;
     S.segments = m;
     S.depth = depth;

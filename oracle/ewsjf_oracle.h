@@ -72,6 +72,7 @@ typedef struct {
     double  epsilon;       /* Eq. 3 ε > 0                        */
     int32_t coarse_k;      /* Stage-1 k, 1..3                    */
     int32_t merge_rule;    /* OR_MIN_U (literal) or OR_MAX_U     */
+    int32_t gap_rule;      /* 0: gaps over the multiset D (R10); 1: over the set of distinct lengths */
 } or_params;
 
 typedef struct {

@@ -22,7 +22,8 @@ MIN_U, MAX_U = 0, 1
 
 class PartitionParams(C.Structure):
     _fields_ = [("alpha", C.c_double), ("min_width", C.c_int32), ("max_queues", C.c_int32),
-                ("epsilon", C.c_double), ("coarse_k", C.c_int32), ("merge_rule", C.c_int32)]
+                ("epsilon", C.c_double), ("coarse_k", C.c_int32), ("merge_rule", C.c_int32),
+                ("gap_rule", C.c_int32)]
 
 
 class Queue(C.Structure):

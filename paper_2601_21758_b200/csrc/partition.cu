@@ -692,6 +692,11 @@ __global__ void __launch_bounds__(kHT, 1)
     }
 }
 
+__global__ void iota_kernel(int64_t* a, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = i;
+}
+
 __global__ void set_flags_kernel(uint8_t* flag, const int32_t* out, int k) {
     flag[0] = 1;
     if (k >= 2) flag[out[2]] = 1;
@@ -802,8 +807,10 @@ static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int l
     set_flags_kernel<<<1, 1, 0, st>>>(R->flag, R->out_i, k);
     {
         LaunchScope ls(ctx, KIND_PARTITION);
-        refine_kernel<<<1, kHT, 0, st>>>(R->v, R->N, M, p->alpha, p->min_width, R->flag, R->seg, R->out_i,
-                                          R->segend);
+        // gap_rule 1 (set reading of G): Eq. 2 counts distinct lengths -> identity prefix
+        if (p->gap_rule) iota_kernel<<<(int)((M + 1 + 255) / 256), 256, 0, st>>>(R->ps2, M + 1);
+        refine_kernel<<<1, kHT, 0, st>>>(R->v, p->gap_rule ? R->ps2 : R->N, M, p->alpha, p->min_width, R->flag,
+                                          R->seg, R->out_i, R->segend);
     }
     CU(cudaGetLastError());
     CU(cudaEventRecord(R->ev[3], st));
@@ -893,7 +900,8 @@ static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int l
 static ewsjf_status check_rp_params(ewsjf_ctx* ctx, const ewsjf_partition_params* p, ewsjf_partition_t* out) {
     if (!p || !out) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null params/out");
     if (!(p->alpha > 1.0) || p->min_width < 1 || p->max_queues < 1 || p->max_queues > EWSJF_MAX_QUEUES ||
-        !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 || (p->merge_rule != 0 && p->merge_rule != 1))
+        !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 || (p->merge_rule != 0 && p->merge_rule != 1) ||
+        (p->gap_rule != 0 && p->gap_rule != 1))
         return fail(ctx, EWSJF_ERR_INVALID_ARG, "partition params out of range (S:121)");
     return EWSJF_OK;
 }
@@ -905,7 +913,8 @@ extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, in
     if (!ctx) return EWSJF_ERR_INVALID_ARG;
     if (!p || !out) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null params/out");
     if (!(p->alpha > 1.0) || p->min_width < 1 || p->max_queues < 1 || p->max_queues > EWSJF_MAX_QUEUES ||
-        !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 || (p->merge_rule != 0 && p->merge_rule != 1))
+        !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 || (p->merge_rule != 0 && p->merge_rule != 1) ||
+        (p->gap_rule != 0 && p->gap_rule != 1))
         return fail(ctx, EWSJF_ERR_INVALID_ARG, "partition params out of range (S:121)");
     if (n < 0 || n > ctx->max_history) return fail(ctx, EWSJF_ERR_INVALID_ARG, "n=%lld > max_history", (long long)n);
     if (n > 0 && !d_len) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null history");

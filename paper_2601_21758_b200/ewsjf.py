@@ -116,8 +116,9 @@ def select_params(k=64, mode=L.SELECT_SCORE, now=600.0, cost=(0.005, 0.0002, 1e-
     return L.SelectParams(k, mode, now, L.CostParams(*cost))
 
 
-def partition_params(alpha=2.0, min_width=1, max_queues=32, epsilon=1e-6, coarse_k=3, merge_rule=L.MIN_U):
-    return L.PartitionParams(alpha, min_width, max_queues, epsilon, coarse_k, merge_rule)
+def partition_params(alpha=2.0, min_width=1, max_queues=32, epsilon=1e-6, coarse_k=3, merge_rule=L.MIN_U,
+                     gap_rule=0):
+    return L.PartitionParams(alpha, min_width, max_queues, epsilon, coarse_k, merge_rule, gap_rule)
 
 
 def weights_from_meta(theta: L.Meta, part: L.Partition):

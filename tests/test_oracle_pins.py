@@ -737,3 +737,23 @@ def test_online_adjust_same_distribution_is_near_identity(orc):
     for (lo, hi), q in zip(bounds, p2.queues()):
         w = hi - lo
         assert abs(q["min_len"] - lo) <= max(2, 0.05 * w)
+
+
+# ---------------------------------- Eq. 2 over the set of distinct lengths ---
+def test_gap_rule_set_reading_example(orc):
+    """SURVEY ambiguity 10: G over the multiset D (R10, default) vs over the set of
+    distinct lengths (gap_rule=1).  [1 x6, 2, 10], alpha = 2: the multiset reading
+    splits twice (mean(G) = 9/7, then 1/6), the set reading {1, 2, 10} not at all
+    (mean(G) = 4.5, gap 8 < 9)."""
+    xs = [1] * 6 + [2, 10]
+    s0, _, st0 = orc.partition(xs, coarse_k=1, max_queues=256)
+    s1, _, st1 = orc.partition(xs, coarse_k=1, max_queues=256, gap_rule=1)
+    assert st0.segments == len(brute.refine_brute(xs, 2.0)) == 3
+    assert st1.segments == len(brute.refine_brute(sorted(set(xs)), 2.0)) == 1
+
+
+@settings(max_examples=80, deadline=None)
+@given(st.lists(st.integers(1, 60), min_size=1, max_size=40), st.sampled_from([1.5, 2.0, 3.0]))
+def test_gap_rule_set_matches_brute_on_distinct_values(orc, xs, alpha):
+    s, _, st_ = orc.partition(xs, coarse_k=1, max_queues=256, alpha=alpha, gap_rule=1)
+    assert st_.segments == len(brute.refine_brute(sorted(set(xs)), alpha))

@@ -56,7 +56,8 @@ def test_partition_random_small(E, orc, ctx, seed):
         hist[rng.integers(0, n, size=max(1, n // 20))] = 0        # invalid lengths
     kw = dict(alpha=float(rng.choice([1.5, 2.0, 3.0, 1.7])), min_width=int(rng.choice([1, 2, 10])),
               max_queues=int(rng.integers(1, 40)), epsilon=float(rng.choice([1e-6, 0.5, 2.0])),
-              coarse_k=int(rng.integers(1, 4)), merge_rule=int(rng.integers(0, 2)))
+              coarse_k=int(rng.integers(1, 4)), merge_rule=int(rng.integers(0, 2)),
+              gap_rule=int(seed % 3 == 2))
     _check(*_both(E, orc, ctx, hist, **kw))
 
 
@@ -135,3 +136,10 @@ def test_partition_from_hist_edge_cases(E, ctx):
     assert s == 3                                                  # EMPTY
     _, _, s = E.partition_from_hist(ctx, z, 100)                   # max_len given, no mass
     assert s == 3
+
+
+@pytest.mark.parametrize("kind,n,seed", [("heavy", 1_000_000, 301), ("bimodal", 200_000, 3)])
+@pytest.mark.parametrize("rule", [0, 1])
+def test_partition_set_gap_reading(E, orc, ctx, kind, n, seed, rule):
+    """gap_rule = 1 (Eq. 2 over the set of distinct lengths, SURVEY ambiguity 10)."""
+    _check(*_both(E, orc, ctx, workload.lengths(kind, n, seed), merge_rule=rule, gap_rule=1))
