@@ -364,7 +364,8 @@ ewsjf_status ewsjf_batch_build(ewsjf_ctx *ctx, const int32_t *d_len, int64_t n, 
                                const ewsjf_batch_budget *budget, int64_t *d_batch_id, int64_t *d_batch_info);
 
 /* Alg. 1 lines 8-12: for every queue position p with h_count[p] == 0
- * increment part->q[p].empty_count (never reset, R30); remove the queues whose
+ * increment part->q[p].empty_count, else reset it to 0 (consecutive empty
+ * tactical steps; R30); remove the queues whose
  * counter exceeds `threshold` (strict, R25), renumber the survivors' index
  * 1..n and bump part->version if any was removed.  Host-only (the
  * partition is host state); *removed (nullable) = queues removed.  h_count is

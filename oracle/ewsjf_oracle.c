@@ -593,7 +593,9 @@ int32_t or_prune_empty(or_partition *part, int32_t *empty_cnt, const int64_t *co
     int32_t k = 0, removed = 0;
     for (int32_t p = 0; p < part->n; p++) {
         int32_t e = empty_cnt[p];
-        if (count[p] == 0) e++;                          /* Alg. 1 line 9 (no reset, R30) */
+        /* Alg. 1 line 9; empty_count counts CONSECUTIVE empty tactical steps
+           (S:107), so a queue with members resets it (R30) */
+        e = count[p] == 0 ? e + 1 : 0;
         if (e > threshold) { removed++; continue; }       /* lines 10-11, strict (R25) */
         part->q[k] = part->q[p];
         part->q[k].index = k + 1;                         /* renumber */

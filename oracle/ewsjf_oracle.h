@@ -192,7 +192,7 @@ int64_t or_batch(const int32_t *len, const float *arrival, const float *cost, co
                  int32_t primary, const or_budget *budget, int64_t *batch_ids, int64_t *batch_tokens);
 
 /* Alg. 1 lines 8-12: every queue with count[p] == 0 increments its empty
- * counter (no reset, R30); a queue whose counter exceeds `threshold` (strict,
+ * counter (reset to 0 when the queue has members: consecutive empty steps, R30); a queue whose counter exceeds `threshold` (strict,
  * R25) is removed and the remaining indices renumbered.  empty_cnt[p] is
  * in/out by position (compacted like the queues).  Returns queues removed. */
 int32_t or_prune_empty(or_partition *part, int32_t *empty_cnt, const int64_t *count, int32_t threshold);

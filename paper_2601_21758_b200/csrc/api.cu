@@ -19,6 +19,9 @@ int64_t merge_smem_total(int in_mode);
 cudaError_t launch_stream(const PartialArgs& A, const Policy& P, const MergeArgs* MA, bool has_cost, int grid,
                           cudaStream_t st);
 int64_t stream_smem_bytes(bool has_cost, int lut_size, int nslots, int cap, int stages);
+cudaError_t launch_ftick(const FArgs& A, const Policy& P, const MergeArgs& MA, bool has_cost, int grid,
+                         cudaStream_t st);
+int64_t ftick_smem_bytes(bool has_cost, int lut_size, int nslots, int stages);
 bool sweep_diag(ewsjf_ctx* ctx, unsigned long long* cuts_inserts);
 }  // namespace ewsjf
 
@@ -95,6 +98,11 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
               cudaMalloc(&ctx->d_head_id, kMaxSlots * 8) == cudaSuccess &&
               cudaMalloc(&ctx->d_head_score, kMaxSlots * 4) == cudaSuccess &&
               cudaMalloc(&ctx->d_max_score, kMaxSlots * 4) == cudaSuccess;
+    // fused tick rows: 64 queues x G CTAs x f_rc keys; overflow lists G x kFOvf
+    ctx->f_rc = std::max(512, 4 * max_k);
+    ok = ok && cudaMalloc(&ctx->f_rows, (size_t)64 * G * ctx->f_rc * sizeof(u64)) == cudaSuccess &&
+         cudaMalloc(&ctx->f_ovf_keys, (size_t)G * kFOvf * sizeof(u64)) == cudaSuccess &&
+         cudaMalloc(&ctx->f_ovf_code, (size_t)G * kFOvf) == cudaSuccess;
     if (ok && max_pool > 0) {
         ok = cudaMalloc(&ctx->d_len, (size_t)max_pool * 4) == cudaSuccess &&
              cudaMalloc(&ctx->d_arr, (size_t)max_pool * 4) == cudaSuccess &&
@@ -128,7 +136,7 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
     cudaDeviceSynchronize();
     if (ctx->h_lut) cudaFreeHost(ctx->h_lut);
     if (ctx->lut_ev) cudaEventDestroy(ctx->lut_ev);
-    void* d[] = {ctx->d_lut, ctx->dbg, ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
+    void* d[] = {ctx->f_rows, ctx->f_ovf_keys, ctx->f_ovf_code, ctx->d_lut, ctx->dbg, ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
                  ctx->d_blog, ctx->d_summary, ctx->d_len, ctx->d_arr, ctx->d_cost, ctx->d_qid, ctx->d_topk_id,
                  ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score, ctx->d_max_score};
     for (void* p : d)
@@ -483,6 +491,73 @@ static ewsjf_status check_out(ewsjf_ctx* ctx, const ewsjf_select_out* out) {
     return EWSJF_OK;
 }
 
+// The fused streaming tick (ftick.cu) when the pool and partition allow it:
+// <= 64 queues, 16-byte aligned pool, cooperative launch.  merge_mode 1 =
+// final outputs (M: OUT_FINAL), 2 = exchange record (M: OUT_EXCHANGE).
+// Returns false (nothing launched) when not eligible.
+static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, const float* d_cost,
+                      int32_t* d_qid_out, int64_t n, int64_t gbase, const ewsjf_partition_t* part, const Policy& P,
+                      const ewsjf_select_params* sp, MergeArgs& M, int merge_mode, ewsjf_status* st) {
+    const int nslots = part->n;
+    const bool has_cost = d_cost != nullptr;
+    if (getenv("EWSJF_OLD_TICK") || !ctx->coop || nslots < 1 || nslots > 64 || ctx->num_sms > 160 ||
+        ctx->num_sms < nslots)
+        return false;
+    if (!aligned16(d_len) || !aligned16(d_arr) || (has_cost && !aligned16(d_cost)) ||
+        (d_qid_out && !aligned16(d_qid_out)))
+        return false;
+    const int K = sp->k;
+    const int lutsz = std::min(part->q[nslots - 1].max_len, kLutCap);
+    int stages = 4;
+    if (const char* e = getenv("EWSJF_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
+    const int budget = ctx->smem_optin > 0 ? ctx->smem_optin : 232448;
+    while (stages > 2 && ftick_smem_bytes(has_cost, lutsz, nslots, stages) > budget) stages--;
+    if (ftick_smem_bytes(has_cost, lutsz, nslots, stages) > budget || merge_smem_total(MERGE_IN_ROWS) > budget)
+        return false;
+    if ((*st = ensure_lut(ctx, part, lutsz)) != EWSJF_OK) return true;
+    FArgs A;
+    memset(&A, 0, sizeof A);
+    A.len = d_len; A.arrival = d_arr; A.cost = d_cost; A.qid_out = d_qid_out;
+    A.n = n;
+    A.gbase = (uint32_t)gbase;
+    A.nslots = nslots;
+    A.K = K;
+    A.RC = ctx->f_rc;
+    A.HWM = ctx->f_rc * 3 / 4;
+    A.lut_size = lutsz;
+    A.stages = stages;
+    const int G = ctx->num_sms;
+    A.board_m = 2;
+    if (const char* e = getenv("EWSJF_BOARD_M")) A.board_m = std::max(0, std::min(2, atoi(e)));
+    if (G * A.board_m < K || G * A.board_m > 320) A.board_m = 0;
+    A.merge = merge_mode;
+    A.lut_dev = ctx->d_lut;
+    A.sp = score_params(sp);
+    A.rows = ctx->rows;
+    A.rows.keys = ctx->f_rows;
+    A.rows.cap = ctx->f_rc;
+    A.gthr = ctx->gthr;
+    A.board = ctx->board;
+    A.ovf_keys = ctx->f_ovf_keys;
+    A.ovf_code = ctx->f_ovf_code;
+    A.gap = ctx->gap;
+    A.gap_cap = ctx->gap_cap;
+    A.ctr = ctx->ctr;
+    A.dbg = getenv("EWSJF_PHASES") ? ctx->dbg : nullptr;
+    A.topk_id = M.topk_id; A.topk_score = M.topk_score; A.count = M.count;
+    A.head_id = M.head_id; A.head_score = M.head_score; A.max_score = M.max_score;
+    A.summary = M.summary;
+    M.rows.keys = ctx->f_rows;
+    M.rows.cap = ctx->f_rc;
+    cudaError_t e;
+    {
+        LaunchScope ls(ctx, KIND_TICK);
+        e = launch_ftick(A, P, M, has_cost, G, ctx->stream);
+    }
+    *st = e == cudaSuccess ? EWSJF_OK : fail(ctx, EWSJF_ERR_CUDA, "fused tick kernel: %s", cudaGetErrorString(e));
+    return true;
+}
+
 static ewsjf_status tick_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, const float* d_cost, int64_t n,
                               int64_t gbase, ewsjf_partition_t* part, int32_t bubble_width, const ewsjf_meta* theta,
                               const ewsjf_select_params* sp, int32_t* d_qid_out, const ewsjf_select_out* out) {
@@ -511,9 +586,13 @@ static ewsjf_status tick_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float*
     M.summary = out->d_summary ? out->d_summary : ctx->d_summary;
     M.qid = d_qid_out;
     bool fused = false;
-    if ((s = run_partial(ctx, d_len, d_arr, d_cost, nullptr, d_qid_out, n, gbase, part, P, sp, true, true, &M,
-                         &fused)) != EWSJF_OK)
+    if (run_ftick(ctx, d_len, d_arr, d_cost, d_qid_out, n, gbase, part, P, sp, M, 1, &s)) {
+        if (s != EWSJF_OK) return s;
+        fused = true;
+    } else if ((s = run_partial(ctx, d_len, d_arr, d_cost, nullptr, d_qid_out, n, gbase, part, P, sp, true, true, &M,
+                                &fused)) != EWSJF_OK) {
         return s;
+    }
     if (!fused) {
         cudaError_t e;
         {

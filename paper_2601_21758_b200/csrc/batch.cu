@@ -201,8 +201,9 @@ extern "C" ewsjf_status ewsjf_batch_build(ewsjf_ctx* ctx, const int32_t* d_len, 
 }
 
 // Alg. 1 lines 8-12: count empty ticks, drop queues whose counter
-// exceeds the threshold (strict, R25), renumber the survivors.  Counters
-// are never reset (R30).  Host bookkeeping over the host partition.
+// exceeds the threshold (strict, R25), renumber the survivors.  The
+// counter counts consecutive empty tactical steps: a queue with members
+// resets it (R30).  Host bookkeeping over the host partition.
 extern "C" ewsjf_status ewsjf_prune_empty(ewsjf_partition_t* part, const int64_t* h_count, int32_t threshold,
                                           int32_t* removed) {
     if (!part || !h_count || part->n < 0 || part->n > EWSJF_MAX_QUEUES || threshold < 0)
@@ -210,7 +211,7 @@ extern "C" ewsjf_status ewsjf_prune_empty(ewsjf_partition_t* part, const int64_t
     int32_t k = 0, rm = 0;
     for (int32_t p = 0; p < part->n; p++) {
         ewsjf_queue q = part->q[p];
-        if (h_count[p] == 0) q.empty_count++;
+        q.empty_count = h_count[p] == 0 ? q.empty_count + 1 : 0;
         if (q.empty_count > threshold) { rm++; continue; }
         q.index = k + 1;
         part->q[k++] = q;

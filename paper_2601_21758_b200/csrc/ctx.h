@@ -57,6 +57,11 @@ struct ewsjf_ctx {
     ewsjf::RpScratch* rp = nullptr;
     // Θ-sweep scratch (sweep.cu), grown on demand and kept
     ewsjf::SweepScratch* sw = nullptr;
+    // fused tick (ftick.cu): rows [64][G][f_rc], per-CTA overflow lists
+    u64* f_rows = nullptr;
+    int32_t f_rc = 0;
+    u64* f_ovf_keys = nullptr;
+    unsigned char* f_ovf_code = nullptr;
     // batch builder prefix scratch (batch.cu)
     uint32_t* d_bpre = nullptr;
     int64_t bpre_cap = 0;

@@ -1,0 +1,940 @@
+// ftick.cu — the fused EWSJF scheduling tick on sm_100a: route (A8) + Eq. 4
+// score (A10) + per-queue count / head / top-k filter (A11) in one HBM pass
+// over the pending pool, then a grid barrier and the per-queue merge + Alg. 1
+// ArgMax.  Paper: Dispatcher P:162, Eq. 4, Alg. 1 P:167-196;
+// readings R1-R27 in DESIGN.md §3.  Gap-falling lengths (App. D, Alg. 2) are
+// collected here and resolved by merge_phase (merge.cuh).
+//
+// Design:
+//  * one 512-thread CTA per SM (cooperative launch).  Warp (b, w) owns the
+//    contiguous tile block w*G + b of the pool (128 requests per tile), so the
+//    first tile of every warp — together the "sample", 16 tiles per CTA spread
+//    over the whole pool — is representative whatever the pool order;
+//  * every warp streams its block through a private ring of 1-D TMA bulk
+//    copies (cp.async.bulk, one elected lane, mbarrier per stage);
+//  * per request: byte-LUT route, one 32-byte per-code record (weights, fast
+//    thresholds, stable id, member-counter offset), Eq. 4 with one MUFU.LG2 +
+//    one MUFU.RCP, a per-thread u16 member counter, two float compares; the
+//    qid goes out as one 16-byte streaming store per 4 requests;
+//  * sample bound: after its sample tile every CTA publishes its top board_m
+//    keys per queue; the last CTA to publish turns the G*board_m keys of each
+//    queue into a valid bound on the queue's K-th key (K-th largest of
+//    distinct real keys) and releases the others; the sample keys are then
+//    filtered against it.  So the stream starts with near-final thresholds
+//    and only ~K*(N/S) keys per queue are ever inserted;
+//  * survivors go to per-(queue, CTA) rows in global memory (L2); a full row
+//    triggers a CTA collective that cuts it to its exact K-th key (CTA radix
+//    select) and raises the queue's thresholds here and in gthr;
+//  * after a grid barrier (monotone ticket) CTA q merges queue q's rows:
+//    candidates >= gthr into shared memory, CTA radix select of the exact
+//    K-th key, rank sort of the K survivors, outputs; the last CTA takes
+//    Alg. 1's ArgMax.
+#include <climits>
+#include <type_traits>
+#include "merge.cuh"
+#include "select.cuh"
+
+namespace ewsjf {
+
+constexpr int kFT = 512;            // threads per CTA
+constexpr int kFW = kFT / 32;       // warps
+constexpr int kFTile = 128;         // requests per warp tile (4 per lane)
+constexpr int kFCodeFar = 0xFD;     // length beyond the LUT: binary search in the rare path
+constexpr int kFCodeGap = 0xFE;     // length between queues (App. D)
+constexpr int kFCodeBad = 0xFF;     // len < 1
+constexpr int kFCodeNone = 0xFC;    // padding of a ragged lane
+constexpr int kFMaxSlots = 64;
+constexpr int kFBoardMax = 2;       // board keys per (queue, CTA); G * m <= 32 * kFBoardRegs
+constexpr int kFBoardRegs = 10;
+
+__host__ __device__ inline int64_t fal(int64_t x) { return (x + 127) & ~(int64_t)127; }
+
+struct FMisc {
+    int flag;           // some row crossed its high-water mark: collective wanted
+    int novf;           // overflow list fill
+    int ndone;          // warps done streaming
+    int last;           // this CTA published the last sample board
+    int ncoll;
+    int sel_d, sel_cd;
+    int pn;             // merge: candidate pool fill
+    unsigned sel_above;
+    int pad;
+    unsigned long long members, sec;
+    unsigned long long tcoll;
+};
+
+struct FSmem {
+    int64_t rec, lut, ring, bars, thr64, sec64, bmax, rcnt, misc, hist, surv, cnt, total;
+};
+// the per-code records and the LUT sit at fixed offsets (immediate addressing on the hot path)
+constexpr int kFRecOff = 0;
+constexpr int kFLutOff = 32 * 256;
+__host__ __device__ inline FSmem fsmem_layout(bool has_cost, int lut_size, int nslots, int stages) {
+    FSmem L;
+    const int narr = has_cost ? 3 : 2;
+    int64_t o = 0;
+    L.rec = kFRecOff;
+    L.lut = kFLutOff;
+    o = fal(kFLutOff + lut_size + 1);
+    L.ring = o;  o = fal(o + (int64_t)kFW * stages * narr * kFTile * 4);
+    L.bars = o;  o = fal(o + 8LL * kFW * stages);
+    L.thr64 = o; o = fal(o + 8LL * kFMaxSlots);
+    L.sec64 = o; o = fal(o + 8LL * kFMaxSlots);
+    L.bmax = o;  o = fal(o + 8LL * kFMaxSlots * kFBoardMax);
+    L.rcnt = o;  o = fal(o + 4LL * kFMaxSlots);
+    L.misc = o;  o = fal(o + sizeof(FMisc));
+    L.hist = o;  o = fal(o + 4LL * 256);
+    L.surv = o;  o = fal(o + 8LL * EWSJF_MAX_K);
+    L.cnt = o;   o = fal(o + 2LL * kFT * (nslots + 2));   // rows: members 0..nslots-1, bad, dummy
+    L.total = o;
+    return L;
+}
+int64_t ftick_smem_bytes(bool has_cost, int lut_size, int nslots, int stages) {
+    return fsmem_layout(has_cost, lut_size, nslots, stages).total;
+}
+
+__device__ __forceinline__ unsigned long long fgtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// wait until at most n of this thread's cp.async groups are pending
+__device__ __forceinline__ void cp_async_wait_n(int n) {
+    switch (n) {
+        case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+        case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+        case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+        case 6: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
+    }
+}
+__device__ __forceinline__ void fbar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kFT) : "memory"); }
+
+// key high word -> fast-test float.  SCORE keys: the bits of s' (>= +0).
+// FIFO keys: hi = ~ord(arrival), inverted here.
+__device__ __forceinline__ float fifo_hi_to_f(u32 hi) {
+    const u32 u = ~hi;
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// CTA-wide exact K-th largest key (512 threads, all must call).  for_each(f)
+// calls f(key) for this thread's share of the candidate keys (0 = none);
+// requires >= K nonzero keys.  MSB-first 8-bit radix select over a 256-bin
+// shared histogram; returns early with a threshold t such that exactly K keys
+// are >= t when the remaining keys of the selected digit are exactly the ones
+// still wanted.
+template <typename ForEach>
+__device__ __forceinline__ u64 block_kth(ForEach for_each, int K, unsigned* hist, FMisc* M) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    u64 prefix = 0ull, pmask = 0ull;
+    int kk = K;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        if (tid < 256) hist[tid] = 0u;
+        fbar(1);
+        for_each([&](u64 k) {
+            if (k && (k & pmask) == prefix) atomicAdd(&hist[(unsigned)(k >> shift) & 255u], 1u);
+        });
+        fbar(1);
+        if (warp == 0) {
+            unsigned c[8], s = 0;
+#pragma unroll
+            for (int i = 0; i < 8; i++) { c[i] = hist[255 - 8 * lane - i]; s += c[i]; }
+            unsigned incl = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            unsigned run = incl - s;
+            int dsel = -1;
+            unsigned above = 0, cd = 0;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                if (dsel < 0 && run + c[i] >= (unsigned)kk) { dsel = 255 - 8 * lane - i; above = run; cd = c[i]; }
+                run += c[i];
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, dsel >= 0);
+            const int src = hit ? __ffs(hit) - 1 : 0;
+            dsel = __shfl_sync(0xffffffffu, dsel, src);
+            above = __shfl_sync(0xffffffffu, above, src);
+            cd = __shfl_sync(0xffffffffu, cd, src);
+            if (lane == 0) { M->sel_d = dsel; M->sel_above = above; M->sel_cd = (int)cd; }
+        }
+        fbar(1);
+        const int d = M->sel_d;
+        const int above = (int)M->sel_above, cd = M->sel_cd;
+        prefix |= (u64)(unsigned)d << shift;
+        pmask |= 0xFFull << shift;
+        kk -= above;
+        if (cd == kk) return prefix;   // exactly K keys >= prefix (lower bits zero)
+    }
+    return prefix;
+}
+
+// CTA-wide: copy the keys >= t given by for_each into out[] (any order), returns the count.
+template <typename ForEach>
+__device__ __forceinline__ int block_collect(ForEach for_each, u64 t, u64* out, int cap, FMisc* M) {
+    if (threadIdx.x == 0) M->pn = 0;
+    fbar(1);
+    for_each([&](u64 k) {
+        if (k && k >= t) {
+            const int p = atomicAdd(&M->pn, 1);
+            if (p < cap) out[p] = k;
+        }
+    });
+    fbar(1);
+    const int n = M->pn;
+    fbar(1);
+    return n < cap ? n : cap;
+}
+
+template <int MODE, bool HAS_COST>
+__global__ void __launch_bounds__(kFT, 1)
+    ftick_kernel(const __grid_constant__ FArgs A, const __grid_constant__ Policy P,
+                 const __grid_constant__ MergeArgs MA) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int nslots = A.nslots, K = A.K, RC = A.RC, HWM = A.HWM;
+    const int lutsz = A.lut_size;
+    const int R = A.stages;
+    constexpr bool SCORE = MODE == EWSJF_SELECT_SCORE;
+    constexpr int narr = HAS_COST ? 3 : 2;
+    const FSmem L = fsmem_layout(HAS_COST, lutsz, nslots, R);
+    unsigned char* lut = smem + kFLutOff;
+    float4* rec = (float4*)(smem + kFRecOff);           // [code][2]: {wb, wu, wf', thrf}, {secf, qid, cntoff, -}
+    u64* thr64 = (u64*)(smem + L.thr64);
+    u64* sec64 = (u64*)(smem + L.sec64);
+    u64* bmax = (u64*)(smem + L.bmax);
+    int* rcnt = (int*)(smem + L.rcnt);
+    FMisc* M = (FMisc*)(smem + L.misc);
+    unsigned* hist = (unsigned*)(smem + L.hist);
+    u64* surv = (u64*)(smem + L.surv);
+    unsigned char* cntb = smem + L.cnt;
+    unsigned char* ring = smem + L.ring + (int64_t)warp * R * narr * kFTile * 4;
+    const bool dbg = A.dbg != nullptr;
+    auto stamp = [&](int s) {
+        if (dbg && tid == 0) A.dbg[cta * 16 + s] = fgtime();
+    };
+    stamp(0);
+
+    // ---- this warp's tile block: warp (cta, warp) -> block warp*G + cta
+    const int64_t ntiles = (A.n + kFTile - 1) / kFTile;
+    const int64_t nfull = A.n / kFTile;
+    const int64_t GW = (int64_t)G * kFW;
+    const int64_t blk = (int64_t)warp * G + cta;
+    const int64_t t0 = blk * ntiles / GW, t1 = (blk + 1) * ntiles / GW;
+    const int nt = (int)(t1 - t0);
+    auto stage = [&](int st, int a) -> unsigned char* { return ring + (st * narr + a) * kFTile * 4; };
+    // Per-lane cp.async (LDGSTS) ring: every lane copies, and later reads back, its
+    // own 16 bytes per array of each tile; one commit group per tile (empty past
+    // the end).  (A per-warp ring of 512-byte cp.async.bulk copies measured ~2.2 TB/s:
+    // the bulk-copy engine costs ~90 cycles per copy, too many copies per SM.)
+    auto issue = [&](int i, int st) {   // all lanes: tile t0 + i into stage st = i % R
+        const int64_t t = t0 + i;
+        if (i < nt && t < nfull) {
+            const int64_t off = t * kFTile + 4 * lane;
+            cp_async16(stage(st, 0) + 16 * lane, A.len + off);
+            cp_async16(stage(st, 1) + 16 * lane, A.arrival + off);
+            if (HAS_COST) cp_async16(stage(st, 2) + 16 * lane, A.cost + off);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int i = 0; i < R; i++) issue(i, i);
+    stamp(10);
+
+    // ---- setup while the first tiles are in flight
+    {
+        const float inf = __int_as_float(0x7f800000), nan = __int_as_float(0x7fffffff);
+        for (int c = tid; c < 256; c += kFT) {
+            float4 a = make_float4(0.f, 0.f, 0.f, nan), b = make_float4(nan, 0.f, 0.f, 0.f);
+            int cnto = nslots + 1, qid = -2;
+            if (c == kFCodeGap || c == kFCodeFar) {
+                // always into the rare path: the arrival compare (a NaN arrival is !ok anyway)
+                if (SCORE) b.x = inf; else a.w = inf;
+            }
+            if (c < nslots) {
+                // sample phase: no primary filter, no secondary filter (the sample block takes both)
+                a = make_float4(P.wb[c], P.wu[c], P.wf[c], nan);
+                cnto = c;
+                qid = P.sid[c];
+            } else if (c == kFCodeBad) {
+                cnto = nslots;
+                qid = -1;
+            }
+            b.y = __int_as_float(qid);
+            b.z = __int_as_float(cnto * kFT * 2);
+            rec[2 * c] = a;
+            rec[2 * c + 1] = b;
+        }
+        for (int q = tid; q < kFMaxSlots; q += kFT) {
+            thr64[q] = 0ull; sec64[q] = 0ull; rcnt[q] = 0;
+            for (int m = 0; m < kFBoardMax; m++) bmax[q * kFBoardMax + m] = 0ull;
+        }
+        if (dbg && tid == 0) A.dbg[cta * 16 + 11] = fgtime();
+        uint4* c4 = (uint4*)cntb;
+        const int n16 = (2 * kFT * (nslots + 2)) / 16;
+        for (int i = tid; i < n16; i += kFT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (dbg && tid == 0) A.dbg[cta * 16 + 12] = fgtime();
+        const int l16 = (lutsz + 1 + 15) / 16;
+        const int4* src = reinterpret_cast<const int4*>(A.lut_dev);
+        for (int i = tid; i < l16; i += kFT) ((int4*)lut)[i] = __ldg(src + i);
+        if (tid == 0) {
+            M->flag = 0; M->novf = 0; M->ndone = 0; M->last = 0; M->ncoll = 0; M->pn = 0;
+            M->members = 0ull; M->sec = 0ull; M->tcoll = 0ull;
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && lutsz >= 0) lut[lutsz] = (unsigned char)kFCodeFar;   // lengths >= lut_size
+    __syncthreads();
+    stamp(1);
+
+    const uint32_t gbase = A.gbase;
+    const bool write_qid = A.qid_out != nullptr;
+    uint16_t* mycnt = (uint16_t*)(cntb + 2 * tid);
+    unsigned n_exc = 0, n_ins = 0, n_gap = 0, n_bad = 0;
+    u64* const rows_cta = A.rows.keys + (size_t)cta * RC;     // row of queue q: rows_cta + q*G*RC
+    const size_t row_stride = (size_t)G * RC;
+
+    auto raise_thr = [&](int q, u64 t) {   // one lane; thr64 + fast float (may lag looser, never tighter)
+        if (t > *(volatile u64*)&thr64[q]) {
+            atomicMax(&thr64[q], t);
+            const u32 hi = (u32)(t >> 32);
+            ((volatile float*)&rec[2 * q])[3] = SCORE ? __uint_as_float(hi) : fifo_hi_to_f(hi);
+        }
+    };
+    auto insert = [&](int q, u64 k) {
+        const int pos = atomicAdd(&rcnt[q], 1);
+        if (pos < RC) {
+            rows_cta[q * row_stride + pos] = k;
+        } else {
+            const int o = atomicAdd(&M->novf, 1);
+            if (o < kFOvf) { A.ovf_keys[(size_t)cta * kFOvf + o] = k; A.ovf_code[(size_t)cta * kFOvf + o] = (unsigned char)q; }
+        }
+        if (pos + 1 >= HWM) *(volatile int*)&M->flag = 1;
+        n_ins++;
+    };
+    auto sec_update = [&](int q, u64 k2) {
+        if (k2 > *(volatile u64*)&sec64[q]) {
+            atomicMax(&sec64[q], k2);
+            const u32 hi = (u32)(k2 >> 32);
+            ((volatile float*)&rec[2 * q + 1])[0] = SCORE ? fifo_hi_to_f(hi) : __uint_as_float(hi);
+        }
+    };
+    // queue position of a length beyond the LUT (binary search over the policy bounds), -1 = gap
+    auto bsearch = [&](int b) -> int {
+        int lo = 0, hi = nslots;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (P.min_len[mid] <= b) lo = mid + 1; else hi = mid;
+        }
+        const int i = lo - 1;
+        return (i >= 0 && b < P.max_len[i]) ? i : -1;
+    };
+
+    // ---- the rare path of one request (lane-divergent)
+    auto rare = [&](int c, int b, float a, float co, float sp, bool ok, int64_t idx) {
+        const uint32_t gid = gbase + (uint32_t)idx;
+        if (c == kFCodeFar) {
+            if (b < 1) {                      // negative length (clamped to the FAR code): invalid
+                n_bad++;
+                if (write_qid) A.qid_out[idx] = -1;
+                return;
+            }
+            const int q = bsearch(b);
+            if (q >= 0) {
+                const float4 w = rec[2 * q];
+                ok = score_sp(b, a, co, HAS_COST, A.sp, w.x, w.y, w.z, &sp);
+                mycnt[q * kFT]++;
+                if (write_qid) A.qid_out[idx] = P.sid[q];
+                c = q;
+            } else {
+                c = kFCodeGap;
+            }
+        }
+        if (c == kFCodeGap) {
+            const unsigned long long p = atomicAdd(&A.ctr->gap_count, 1ull);
+            if (p < (unsigned long long)A.gap_cap) {
+                GapEntry e;
+                e.gid = gid; e.len = b; e.arrival = a;
+                e.cost = HAS_COST ? co : __int_as_float(0x7fc00000);
+                A.gap[p] = e;
+            }
+            n_gap++;
+            return;
+        }
+        if (c >= nslots) return;   // bad length / padding
+        if (!ok) { mycnt[c * kFT]--; n_exc++; return; }
+        const u64 ks = score_key(sp, gid), kf = fifo_key(a, gid);
+        const u64 k1 = SCORE ? ks : kf, k2 = SCORE ? kf : ks;
+        if (k1 >= *(volatile u64*)&thr64[c]) insert(c, k1);
+        sec_update(c, k2);
+    };
+
+    // ---- one tile of 128 requests (4 per lane); sample: keep the keys, fill the sample maxima
+    u64 skey[4] = {0ull, 0ull, 0ull, 0ull};
+    int scode[4] = {kFCodeNone, kFCodeNone, kFCodeNone, kFCodeNone};
+    int cur_st = 0;             // ring stage of the next tile and its mbarrier parity
+    uint32_t cur_par = 0u;
+    auto body = [&](auto full_tag, int i, bool sample) {
+        constexpr bool FULL = decltype(full_tag)::value;
+        const int64_t t = t0 + i;
+        const int64_t i0 = t * kFTile + 4 * lane;
+        int b[4];
+        float a[4], co[4];
+        int nv = 4;
+        const int st = cur_st;            // = i % R
+        const uint32_t par = cur_par;     // = (i / R) & 1
+        if (++cur_st == R) { cur_st = 0; cur_par ^= 1u; }
+        if (FULL) {
+            cp_async_wait_n(R - 1);
+            (void)par;
+            const int4 bv = ((const int4*)stage(st, 0))[lane];
+            const float4 av = ((const float4*)stage(st, 1))[lane];
+            float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (HAS_COST) cv = ((const float4*)stage(st, 2))[lane];
+            b[0] = bv.x; b[1] = bv.y; b[2] = bv.z; b[3] = bv.w;
+            a[0] = av.x; a[1] = av.y; a[2] = av.z; a[3] = av.w;
+            co[0] = cv.x; co[1] = cv.y; co[2] = cv.z; co[3] = cv.w;
+        } else {                              // the ragged last tile: direct loads
+            nv = (int)max((int64_t)0, min((int64_t)4, A.n - i0));
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const bool v = j < nv;
+                b[j] = v ? __ldg(A.len + i0 + j) : 0;
+                a[j] = v ? __ldg(A.arrival + i0 + j) : 0.f;
+                co[j] = (HAS_COST && v) ? __ldg(A.cost + i0 + j) : 0.f;
+            }
+        }
+        int code[4];
+        float sp[4];
+        int qo[4];
+        bool okv[4];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            // lengths < 0 clamp to lut_size (FAR: the rare path sorts them out); lut[0] = bad
+            const int c = (FULL || j < nv) ? (int)lut[min((unsigned)b[j], (unsigned)lutsz)] : kFCodeNone;
+            code[j] = c;
+            const float4 w = rec[2 * c];
+            const float4 r2 = rec[2 * c + 1];
+            const bool ok = score_sp(b[j], a[j], co[j], HAS_COST, A.sp, w.x, w.y, w.z, &sp[j]);
+            okv[j] = ok;
+            qo[j] = __float_as_int(r2.y);
+            uint16_t* cp = (uint16_t*)((unsigned char*)mycnt + __float_as_int(r2.z));
+            *cp = (uint16_t)(*cp + 1);
+            const float f1 = SCORE ? sp[j] : a[j];
+            const float f2 = SCORE ? a[j] : sp[j];
+            const bool p1 = SCORE ? (f1 >= w.w) : (f1 <= w.w);
+            const bool p2 = SCORE ? (f2 <= r2.x) : (f2 >= r2.x);
+            any = any || p1 || p2 || !ok;
+        }
+        if (write_qid) {
+            if (FULL) {
+                __stcs((int4*)(A.qid_out + i0), make_int4(qo[0], qo[1], qo[2], qo[3]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (j < nv) A.qid_out[i0 + j] = qo[j];
+            }
+        }
+        if (sample) {
+            // sample maxima (board) and exact secondary max of every valid member
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int c = code[j];
+                const bool mem = c < nslots && okv[j];
+                const uint32_t gid = gbase + (uint32_t)(i0 + j);
+                const u64 ks = score_key(sp[j], gid), kf = fifo_key(a[j], gid);
+                const u64 k1 = SCORE ? ks : kf, k2 = SCORE ? kf : ks;
+                skey[j] = mem ? k1 : 0ull;
+                scode[j] = mem ? c : kFCodeNone;
+                if (mem) {
+                    if (k1 > *(volatile u64*)&bmax[c * kFBoardMax]) atomicMax(&bmax[c * kFBoardMax], k1);
+                    if (k2 > *(volatile u64*)&sec64[c]) atomicMax(&sec64[c], k2);
+                }
+            }
+        }
+        if (__any_sync(0xffffffffu, any)) {
+#pragma unroll 1
+            for (int j = 0; j < 4; j++) {
+                const int bj = j == 0 ? b[0] : (j == 1 ? b[1] : (j == 2 ? b[2] : b[3]));
+                const float aj = j == 0 ? a[0] : (j == 1 ? a[1] : (j == 2 ? a[2] : a[3]));
+                const float cj = j == 0 ? co[0] : (j == 1 ? co[1] : (j == 2 ? co[2] : co[3]));
+                const float sj = j == 0 ? sp[0] : (j == 1 ? sp[1] : (j == 2 ? sp[2] : sp[3]));
+                const int dj = j == 0 ? code[0] : (j == 1 ? code[1] : (j == 2 ? code[2] : code[3]));
+                const bool oj = j == 0 ? okv[0] : (j == 1 ? okv[1] : (j == 2 ? okv[2] : okv[3]));
+                const float4 w = rec[2 * dj];
+                const float4 r2 = rec[2 * dj + 1];
+                const float f1 = SCORE ? sj : aj, f2 = SCORE ? aj : sj;
+                const bool pj = (SCORE ? (f1 >= w.w) : (f1 <= w.w)) || (SCORE ? (f2 <= r2.x) : (f2 >= r2.x)) || !oj;
+                if (!pj) continue;
+                if (sample && dj < nslots && oj) continue;   // members of the sample: the sample block
+                rare(dj, bj, aj, cj, sj, oj, i0 + j);
+            }
+        }
+        if (FULL) issue(i + R, st);   // refill this lane's slots of the stage with the tile R ahead
+    };
+    auto tile = [&](int i, bool sample) {
+        if (t0 + i < nfull) body(std::integral_constant<bool, true>(), i, sample);
+        else body(std::integral_constant<bool, false>(), i, sample);
+    };
+
+    // ---- collective: cut every row at/over its high-water mark to its exact K-th key
+    auto collective = [&]() {
+        const unsigned long long tc = dbg ? fgtime() : 0ull;
+        fbar(1);
+        const int no = min(*(volatile int*)&M->novf, kFOvf);
+        const u64* ok_ = A.ovf_keys + (size_t)cta * kFOvf;
+        const unsigned char* oc_ = A.ovf_code + (size_t)cta * kFOvf;
+        for (int q = 0; q < nslots; q++) {
+            const int rc = rcnt[q];
+            fbar(1);                          // everyone has read rcnt[q] before it changes
+            if (rc < HWM) continue;
+            const int nr = min(rc, RC);
+            u64* row = rows_cta + q * row_stride;
+            auto fe = [&](auto f) {
+                for (int j = tid; j < nr; j += kFT) f(__ldcg(row + j));
+                for (int j = tid; j < no; j += kFT)
+                    if (oc_[j] == q) f(__ldcg(ok_ + j));
+            };
+            const u64 t = block_kth(fe, K, hist, M);
+            const int nk = block_collect(fe, t, surv, EWSJF_MAX_K, M);
+            for (int j = tid; j < nk; j += kFT) row[j] = surv[j];
+            if (tid == 0) {
+                rcnt[q] = nk;
+                raise_thr(q, t);
+                atomicMax(&A.gthr[q], t);
+            }
+            fbar(1);
+        }
+        if (tid == 0) {
+            M->novf = 0;
+            M->flag = 0;
+            M->ncoll++;
+            if (dbg) M->tcoll += fgtime() - tc;
+        }
+        fbar(1);
+    };
+
+    // ---- sample tile, board, bound
+    if (nt > 0) tile(0, true);
+    __syncthreads();
+    stamp(2);
+    const int bm = A.board_m;
+    if (bm > 0) {
+        // further board rounds (m > 1): the largest key below the previous round's
+        for (int m = 1; m < bm; m++) {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int c = scode[j];
+                if (c < nslots) {
+                    const u64 prev = bmax[c * kFBoardMax + m - 1];
+                    const u64 k = skey[j];
+                    if (k < prev && k > *(volatile u64*)&bmax[c * kFBoardMax + m]) atomicMax(&bmax[c * kFBoardMax + m], k);
+                }
+            }
+            __syncthreads();
+        }
+        for (int i = tid; i < nslots * bm; i += kFT) {
+            const int q = i / bm, m = i % bm;
+            A.board[((size_t)q * G + cta) * bm + m] = bmax[q * kFBoardMax + m];
+        }
+        __threadfence();
+        __syncthreads();
+        unsigned gen = 0;
+        if (tid == 0) {
+            const unsigned tk = atomicAdd(&A.ctr->pub, 1u);
+            gen = tk / (unsigned)G;
+            M->last = (tk % (unsigned)G) == (unsigned)(G - 1);
+            M->sel_d = (int)gen;
+        }
+        __syncthreads();
+        stamp(13);
+        gen = (unsigned)M->sel_d;
+        if (M->last) {
+            // K-th largest high word of the published keys of each queue: every key
+            // >= (t << 32) of >= K distinct real requests, a valid bound on the K-th key.
+            // MSB-first descent over the high words, the warp's queues interleaved.
+            const int nb = G * bm;
+            constexpr int kQW = kFMaxSlots / kFW;      // queues per warp (<= 4)
+            u32 v[kQW][kFBoardRegs];
+            u32 tq[kQW];
+            bool has[kQW];
+#pragma unroll
+            for (int k = 0; k < kQW; k++) {
+                const int q = warp + kFW * k;
+                int nz = 0;
+#pragma unroll
+                for (int r = 0; r < kFBoardRegs; r++) {
+                    const int j = lane + 32 * r;
+                    const u64 x = (q < nslots && j < nb) ? __ldcg(A.board + (size_t)q * nb + j) : 0ull;
+                    v[k][r] = x ? (u32)(x >> 32) : 0u;
+                    nz += x != 0ull;
+                }
+                has[k] = q < nslots && __reduce_add_sync(0xffffffffu, nz) >= K;
+                tq[k] = 0u;
+            }
+            for (int bit = 31; bit >= 0; bit--) {
+#pragma unroll
+                for (int k = 0; k < kQW; k++) {
+                    const u32 cand = tq[k] | (1u << bit);
+                    int c = 0;
+#pragma unroll
+                    for (int r = 0; r < kFBoardRegs; r++) c += v[k][r] >= cand;
+                    c = __reduce_add_sync(0xffffffffu, c);
+                    if (c >= K) tq[k] = cand;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kQW; k++) {
+                const int q = warp + kFW * k;
+                // hi words of absent entries are 0 (and 0 is the weakest bound): t > 0 only counts real keys
+                if (lane == 0 && has[k] && tq[k]) atomicMax(&A.gthr[q], (u64)tq[k] << 32);
+            }
+            stamp(14);
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&A.ctr->ready), "r"(gen + 1u) : "memory");
+        } else if (tid == 0) {
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&A.ctr->ready) : "memory");
+                if ((int)(v - (gen + 1u)) < 0) __nanosleep(64);
+            } while ((int)(v - (gen + 1u)) < 0);
+        }
+        __syncthreads();
+    }
+    // thresholds from the bound, fast secondary from the sample's exact max
+    for (int q = tid; q < nslots; q += kFT) {
+        const u64 g = bm > 0 ? __ldcg(&A.gthr[q]) : 0ull;
+        thr64[q] = g;
+        const u32 hi = (u32)(g >> 32);
+        const float inf = __int_as_float(0x7f800000);
+        rec[2 * q].w = SCORE ? __uint_as_float(hi) : (g ? fifo_hi_to_f(hi) : inf);
+        const u64 s = sec64[q];
+        const u32 sh = (u32)(s >> 32);
+        rec[2 * q + 1].x = SCORE ? (s ? fifo_hi_to_f(sh) : inf) : __uint_as_float(sh);
+    }
+    __syncthreads();
+    stamp(3);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int c = scode[j];
+        if (c < nslots && skey[j] >= thr64[c]) insert(c, skey[j]);
+    }
+    __syncwarp();
+
+    // ---- stream the rest of the block; collectives on demand
+    int rq = warp;
+    for (int i = 1;; i++) {
+        if (*(volatile int*)&M->flag) collective();
+        if (i >= nt) break;
+        tile(i, false);
+        if ((i & 3) == 0 && nslots > 0) {      // pick up a raised global bound (rotating queue)
+            if (rq >= nslots) rq = warp % nslots;
+            if (lane == 0) {
+                const u64 g = __ldcg(&A.gthr[rq]);
+                if (g) raise_thr(rq, g);
+            }
+            rq += kFW;
+        }
+    }
+    // done: keep serving collectives until every warp is done (a flag raised by
+    // this warp is handled before its ndone increment; ndone is read before the flag)
+    __syncwarp();
+    if (lane == 0) { __threadfence_block(); atomicAdd(&M->ndone, 1); }
+    for (;;) {
+        int f = 0, dn = 0;
+        if (lane == 0) {
+            dn = *(volatile int*)&M->ndone;
+            __threadfence_block();
+            f = *(volatile int*)&M->flag;
+        }
+        f = __shfl_sync(0xffffffffu, f, 0);
+        dn = __shfl_sync(0xffffffffu, dn, 0);
+        if (f) { collective(); continue; }
+        if (dn == kFW) break;
+        __nanosleep(32);
+    }
+    __syncthreads();
+    stamp(4);
+
+    // ---- per-CTA rows: count (<= RC, no overflow pending), members, secondary
+    for (int q = warp; q < nslots; q += kFW) {
+        const uint32_t* c32 = (const uint32_t*)(cntb + (size_t)q * kFT * 2);
+        unsigned long long mm = 0;
+#pragma unroll
+        for (int k = 0; k < kFT / 64; k++) { const uint32_t v = c32[lane + 32 * k]; mm += (v & 0xffffu) + (v >> 16); }
+        for (int o = 16; o; o >>= 1) mm += __shfl_xor_sync(0xffffffffu, mm, o);
+        if (lane == 0) {
+            const size_t r = (size_t)q * G + cta;
+            A.rows.cnt[r] = min(rcnt[q], RC);
+            A.rows.members[r] = (int64_t)mm;
+            A.rows.sec[r] = sec64[q];
+        }
+    }
+    {
+        // invalid lengths (counter row nslots) + excluded + diagnostics
+        unsigned long long bad = n_bad;
+        if (warp == 0) {
+            const uint32_t* c32 = (const uint32_t*)(cntb + (size_t)nslots * kFT * 2);
+            for (int k = lane; k < kFT / 2; k += 32) { const uint32_t v = c32[k]; bad += (v & 0xffffu) + (v >> 16); }
+        }
+        unsigned long long ex = n_exc, ins = n_ins;
+        for (int o = 16; o; o >>= 1) {
+            bad += __shfl_xor_sync(0xffffffffu, bad, o);
+            ex += __shfl_xor_sync(0xffffffffu, ex, o);
+            ins += __shfl_xor_sync(0xffffffffu, ins, o);
+        }
+        if (lane == 0) {
+            if (bad) atomicAdd(&A.ctr->n_invalid, bad);
+            if (ex) atomicAdd(&A.ctr->n_excluded, ex);
+            if (ins) atomicAdd(&A.ctr->dbg_inserted, ins);
+        }
+        if (tid == 0 && M->ncoll) atomicAdd(&A.ctr->dbg_compactions, (unsigned long long)M->ncoll);
+        if (dbg && tid == 0) { A.dbg[cta * 16 + 8] = (unsigned long long)M->ncoll; A.dbg[cta * 16 + 9] = M->tcoll; }
+    }
+    (void)n_gap;
+    __threadfence();
+    __syncthreads();
+    stamp(5);
+    if (A.merge == 0) return;
+
+    // ---- grid barrier (monotone ticket: generation = ticket / G)
+    if (tid == 0) {
+        const unsigned tk = atomicAdd(&A.ctr->done, 1u);
+        const unsigned target = (tk / (unsigned)G + 1u) * (unsigned)G;
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&A.ctr->done) : "memory");
+            if ((int)(v - target) < 0) __nanosleep(32);
+        } while ((int)(v - target) < 0);
+    }
+    __syncthreads();
+    stamp(6);
+
+    const unsigned long long graw = __ldcg(&A.ctr->gap_count);
+    if (graw > 0 || A.merge == 2) {
+        // gap requests (App. D, Alg. 2) / exchange record: the general merge
+        if (A.merge == 2) merge_phase<MERGE_IN_ROWS, MERGE_OUT_EXCHANGE, HAS_COST>(MA, P, smem);
+        else merge_phase<MERGE_IN_ROWS, MERGE_OUT_FINAL, HAS_COST>(MA, P, smem);
+        stamp(7);
+        return;
+    }
+
+    // ---- fast merge: CTA q merges queue q (no gap requests in this tick)
+    const int q = cta;
+    if (q < nslots) {
+        u64 thr = __ldcg(&A.gthr[q]);
+        // the whole shared memory is free now: [rowoff | pool]
+        int* rowoff = (int*)(smem + L.cnt);                  // [G + 1]
+        u64* pool = (u64*)(smem + L.ring);
+        const int pcap = (int)((L.cnt - L.ring) / 8);        // ring .. counters (>= 8K keys)
+        constexpr int kChunk = 4096;                          // candidates scanned per round
+        if (tid == 0) { M->pn = 0; M->members = 0ull; M->sec = 0ull; }
+        // row counts, members, secondary (one row per thread)
+        {
+            unsigned long long mm = 0;
+            u64 sk = 0ull;
+            int nc = 0;
+            if (tid < G) {
+                const size_t r = (size_t)q * G + tid;
+                nc = __ldcg(&A.rows.cnt[r]);
+                mm = (unsigned long long)__ldcg(&A.rows.members[r]);
+                sk = __ldcg(&A.rows.sec[r]);
+            }
+            // exclusive prefix of the counts over the G (<= 512) rows
+            int incl = nc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += u;
+            }
+            unsigned* wsum = hist;                           // per-warp totals
+            if (lane == 31) wsum[warp] = (unsigned)incl;
+            for (int o = 16; o; o >>= 1) {
+                mm += __shfl_xor_sync(0xffffffffu, mm, o);
+                const u64 so = shfl_xor_u64(sk, o);
+                sk = so > sk ? so : sk;
+            }
+            __syncthreads();
+            int woff = 0;
+            for (int w = 0; w < warp; w++) woff += (int)wsum[w];
+            if (tid < G) rowoff[tid] = woff + incl - nc;
+            if (tid == G - 1) rowoff[G] = woff + incl;
+            if (lane == 0) {
+                if (mm) atomicAdd(&M->members, mm);
+                if (sk) atomicMax(&M->sec, sk);
+            }
+        }
+        __syncthreads();
+        const int total = rowoff[G];
+        int pn = 0;
+        for (int base = 0; base < total; base += kChunk) {
+            // candidates [base, base + kChunk): 8 per thread, loads in flight together
+            u64 kv[kChunk / kFT];
+#pragma unroll
+            for (int u = 0; u < kChunk / kFT; u++) {
+                const int e = base + tid + kFT * u;
+                kv[u] = 0ull;
+                if (e < total) {
+                    int lo = 0, hi = G;                      // row r: rowoff[r] <= e < rowoff[r + 1]
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (rowoff[mid] <= e) lo = mid; else hi = mid;
+                    }
+                    kv[u] = __ldcg(A.rows.keys + ((size_t)q * G + lo) * RC + (e - rowoff[lo]));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kChunk / kFT; u++)
+                if (kv[u] && kv[u] >= thr) {
+                    const int p = atomicAdd(&M->pn, 1);
+                    pool[p] = kv[u];
+                }
+            __syncthreads();
+            pn = M->pn;
+            __syncthreads();
+            if (pn > pcap - kChunk && base + kChunk < total) {
+                // no room for another round: cut the pool to its exact top-K
+                auto fe = [&](auto f) { for (int j = tid; j < pn; j += kFT) f(pool[j]); };
+                const u64 t = block_kth(fe, K, hist, M);
+                const int nk = block_collect(fe, t, surv, EWSJF_MAX_K, M);
+                for (int j = tid; j < nk; j += kFT) pool[j] = surv[j];
+                if (tid == 0) M->pn = nk;
+                thr = t;
+                __syncthreads();
+                pn = nk;
+            }
+        }
+        {
+            auto fe = [&](auto f) { for (int j = tid; j < pn; j += kFT) f(pool[j]); };
+            u64 t = 0ull;
+            if (pn > K) t = block_kth(fe, K, hist, M);
+            block_collect(fe, t, surv, EWSJF_MAX_K, M);
+        }
+        // surv holds the min(K, #candidates) best keys (any order): rank sort, outputs
+        const int ns = min(pn, K);
+        u64 myk = 0ull;
+        int myr = -1;
+        if (tid < ns) {
+            myk = surv[tid];
+            int r = 0;
+            for (int j = 0; j < ns; j++) r += surv[j] > myk;
+            myr = r;
+        }
+        __syncthreads();
+        if (tid < ns) surv[myr] = myk;
+        __syncthreads();
+        const float qi = (float)(q + 1);
+        const float wb = P.wb[q], wu = P.wu[q], wf = P.wf[q];
+        auto payload = [&](u64 k) -> float {   // s' of the request with key k
+            if (SCORE) return key_sp(k);
+            const int64_t li = (int64_t)key_gid(k) - (int64_t)gbase;
+            float s = 0.f;
+            score_sp(__ldg(A.len + li), __ldg(A.arrival + li), HAS_COST ? __ldg(A.cost + li) : 0.f, HAS_COST, A.sp,
+                     wb, wu, wf, &s);
+            return s;
+        };
+        for (int r = tid; r < K; r += kFT) {
+            const size_t o = (size_t)q * K + r;
+            if (r < ns) {
+                A.topk_id[o] = (int64_t)key_gid(surv[r]);
+                A.topk_score[o] = qi * payload(surv[r]);
+            } else {
+                A.topk_id[o] = -1;
+                A.topk_score[o] = 0.f;
+            }
+        }
+        if (tid == 0) {
+            const unsigned long long members = M->members;
+            const u64 sec = M->sec;
+            A.count[q] = (int64_t)members;
+            if (members == 0 || ns == 0) {
+                A.head_id[q] = -1; A.head_score[q] = 0.f; A.max_score[q] = 0.f;
+            } else if (SCORE) {
+                const int64_t li = (int64_t)key_gid(sec) - (int64_t)gbase;
+                float s = 0.f;
+                score_sp(__ldg(A.len + li), __ldg(A.arrival + li), HAS_COST ? __ldg(A.cost + li) : 0.f, HAS_COST,
+                         A.sp, wb, wu, wf, &s);
+                A.head_id[q] = (int64_t)key_gid(sec);
+                A.head_score[q] = qi * s;
+                A.max_score[q] = qi * key_sp(surv[0]);
+            } else {
+                A.head_id[q] = (int64_t)key_gid(surv[0]);
+                A.head_score[q] = qi * payload(surv[0]);
+                A.max_score[q] = qi * key_sp(sec);
+            }
+            A.gthr[q] = 0ull;
+        }
+    }
+    stamp(7);
+    // ---- last CTA: Alg. 1 ArgMax (ties -> lowest position, R24), summary, counter reset
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const unsigned tk = atomicAdd(&A.ctr->ticket, 1u);
+        M->last = tk == (unsigned)(G - 1);
+    }
+    __syncthreads();
+    if (!M->last || warp != 0) return;
+    __threadfence();
+    u64 best = 0ull;
+    for (int p = lane; p < nslots; p += 32)
+        if (__ldcg(&A.count[p]) > 0) {
+            const u64 k = ((u64)ord_f32(__ldcg(&A.head_score[p])) << 32) | (u64)(~(u32)p);
+            best = k > best ? k : best;
+        }
+    best = warp_max_u64(best);
+    if (lane != 0) return;
+    const long long inv = (long long)__ldcg(&A.ctr->n_invalid), exc = (long long)__ldcg(&A.ctr->n_excluded);
+    if (A.summary) {
+        ewsjf_summary sm;
+        sm.n_queues = nslots;
+        sm.primary = best ? (int)(~(u32)best) : -1;
+        sm.n_invalid = inv;
+        sm.n_excluded = exc;
+        sm.n_gap = 0;
+        sm.n_bubbles = 0;
+        sm.n_dropped = 0;
+        sm.status = (inv || exc) ? EWSJF_ERR_DOMAIN : EWSJF_OK;
+        sm.pad = 0;
+        *A.summary = sm;
+    }
+    A.ctr->n_invalid = 0;
+    A.ctr->n_excluded = 0;
+    A.ctr->gap_count = 0;
+    A.ctr->ticket = 0;
+}
+
+int64_t merge_smem_total(int in_mode);
+
+template <int MO, bool C>
+static cudaError_t launch_f(const FArgs& A, const Policy& P, const MergeArgs& MA, int grid, cudaStream_t st) {
+    const int64_t ls = fsmem_layout(C, A.lut_size, A.nslots, A.stages).total;
+    const int64_t lm = A.merge ? merge_smem_total(MERGE_IN_ROWS) : 0;
+    const int64_t smem = ls > lm ? ls : lm;
+    auto k = ftick_kernel<MO, C>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    void* args[] = {(void*)&A, (void*)&P, (void*)&MA};
+    return cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kFT), args, (size_t)smem, st);
+}
+
+cudaError_t launch_ftick(const FArgs& A, const Policy& P, const MergeArgs& MA, bool has_cost, int grid,
+                         cudaStream_t st) {
+    if (A.sp.mode == EWSJF_SELECT_FIFO)
+        return has_cost ? launch_f<EWSJF_SELECT_FIFO, true>(A, P, MA, grid, st)
+                        : launch_f<EWSJF_SELECT_FIFO, false>(A, P, MA, grid, st);
+    return has_cost ? launch_f<EWSJF_SELECT_SCORE, true>(A, P, MA, grid, st)
+                    : launch_f<EWSJF_SELECT_SCORE, false>(A, P, MA, grid, st);
+}
+
+}  // namespace ewsjf

@@ -30,7 +30,49 @@ struct Counters {        // device-global, zeroed by the merge for the next call
     unsigned long long tiles;   // dynamic tile scheduler of the fused tick kernel
     // diagnostics, accumulated over calls (never reset by the kernels)
     unsigned long long dbg_inserted, dbg_compactions, dbg_overflow;
+    // ftick.cu: monotone tickets (never reset; launch generation = ticket / grid)
+    unsigned int pub;       // sample boards published
+    unsigned int ready;     // generations whose sample bounds are in gthr
+    unsigned int done;      // CTAs past the streaming phase (grid barrier)
+    unsigned int pad0;
 };
+
+// Fused streaming tick (ftick.cu): route + score + filter + rows, sample bound,
+// grid barrier, per-queue merge.
+struct FArgs {
+    const int32_t* len;
+    const float* arrival;
+    const float* cost;          // nullable
+    int32_t* qid_out;           // nullable
+    int64_t n;
+    uint32_t gbase;
+    int32_t nslots;             // <= 64
+    int32_t K;
+    int32_t RC, HWM;            // row capacity per (queue, CTA) / high-water mark
+    int32_t lut_size;           // LUT covers lengths [0, lut_size); longer: binary search (rare path)
+    int32_t stages;             // TMA ring depth per warp
+    int32_t board_m;            // sample board keys per (queue, CTA); 0 = no sample bound
+    int32_t merge;              // 0: rows only; 1: final outputs; 2: exchange record (merge_phase)
+    const unsigned char* lut_dev;
+    ScoreParams sp;
+    Rows rows;                  // keys [64][G][RC]
+    u64* gthr;                  // [nslots]
+    u64* board;                 // [64][G][board_m]
+    u64* ovf_keys;              // [G][kFOvf]
+    unsigned char* ovf_code;    // [G][kFOvf]
+    GapEntry* gap;
+    int32_t gap_cap;
+    Counters* ctr;
+    unsigned long long* dbg;    // nullable: per-CTA phase timestamps [G][16]
+    int64_t* topk_id;
+    float* topk_score;
+    int64_t* count;
+    int64_t* head_id;
+    float* head_score;
+    float* max_score;
+    ewsjf_summary* summary;
+};
+constexpr int kFOvf = 4608;     // per-CTA overflow list: >= 16 warps x 2 tiles x 128 requests
 
 struct PartialArgs {
     const int32_t* len;

@@ -34,3 +34,24 @@ def test_prune_empty_matches_oracle(E, orc, seed):
            [(q["min_len"], q["max_len"], q["id"], q["index"]) for q in op.queues()]
     assert [gp.q[i].empty_count for i in range(gp.n)] == list(oe)
     assert gp.version == v0 + (1 if rm else 0)
+
+
+def test_prune_empty_alternating_queue_is_never_removed(E, orc):
+    """empty_count counts CONSECUTIVE empty tactical steps ("remain empty"):
+    a queue empty on every other tick never exceeds 1 and is never removed, in both the
+    library and the oracle, while a queue that stays empty goes once its counter passes
+    the threshold (strict, R25)."""
+    opart = orc.make_partition([(1, 10), (10, 20), (20, 30)])
+    gp = to_gpu_partition(E, opart)
+    oe = np.zeros(3, dtype=np.int32)
+    op = opart
+    for tick in range(12):
+        counts = np.array([5, 0 if tick % 2 == 0 else 3, 0 if tick < 11 else 0], dtype=np.int64)[: gp.n]
+        if gp.n == 2:
+            counts = counts[:2]
+        E.prune_empty(gp, counts, 2)
+        op, oe, _ = orc.prune_empty(op, oe, counts, 2)
+        assert [q["id"] for q in gp.queues()] == [q["id"] for q in op.queues()]
+        assert [gp.q[i].empty_count for i in range(gp.n)] == list(oe)
+        assert 1 in [q["id"] for q in gp.queues()]          # the alternating queue stays
+    assert [q["id"] for q in gp.queues()] == [0, 1]          # the always-empty queue is gone

@@ -154,9 +154,20 @@ def _check_partition_invariants(orc, xs, part, maxq):
     pos = np.searchsorted(bounds, v, side="right") - 1
     assert (pos >= 0).all()
     cnt = np.bincount(pos, minlength=len(qs))
-    s1 = np.bincount(pos, weights=v.astype(np.float64), minlength=len(qs))
+    s1 = np.zeros(len(qs), dtype=np.int64)
+    s2 = np.zeros(len(qs), dtype=np.int64)
+    np.add.at(s1, pos, v.astype(np.int64))
+    np.add.at(s2, pos, v.astype(np.int64) ** 2)
     assert cnt.tolist() == [q["count"] for q in qs]
-    assert s1.astype(np.int64).tolist() == [q["sum"] for q in qs]
+    assert s1.tolist() == [q["sum"] for q in qs]
+    assert s2.tolist() == [q["sumsq"] for q in qs]                  # S2 = Σ b² (A2, P:285 mean/variance)
+    # profile fields from first principles: b̄ = Σb/n, ρ = n/width (R16), SSE = Σ(b - b̄)²
+    for i, q in enumerate(qs):
+        mem = v[pos == i]
+        assert q["mean"] == pytest.approx(float(Fr(int(mem.sum()), len(mem))), rel=1e-15)
+        assert q["density"] == pytest.approx(len(mem) / (q["max_len"] - q["min_len"]), rel=1e-15)
+        exact = sum((Fr(int(x)) - Fr(int(mem.sum()), len(mem))) ** 2 for x in mem)
+        assert q["sse"] == pytest.approx(float(exact), rel=1e-9, abs=1e-6)
 
 
 @settings(max_examples=200, deadline=None)
@@ -646,15 +657,16 @@ def test_batch_invariants_random(orc):
 
 
 def test_prune_empty_threshold_strict_and_renumbers(orc):
-    """Alg. 1 lines 8-12: empty queues count up (no reset, R30); removal when the
-    counter exceeds the threshold (strict, R25); indices renumbered."""
+    """Alg. 1 lines 8-12: empty queues count up, a queue with members resets its
+    counter (consecutive empty steps, R30); removal when the counter exceeds
+    the threshold (strict, R25); indices renumbered."""
     part = orc.make_partition([(1, 10), (10, 20), (20, 30), (30, 40)])
     e = [5, 0, 4, 5]
     p2, e2, removed = orc.prune_empty(part, e, [0, 0, 0, 7], 5)
-    # queue 0: 5 -> 6 > 5 removed; queue 1: 0 -> 1; queue 2: 4 -> 5 kept; queue 3 non-empty: 5 kept
+    # queue 0: 5 -> 6 > 5 removed; queue 1: 0 -> 1; queue 2: 4 -> 5 kept; queue 3 non-empty: reset to 0
     assert removed == 1
     assert [(q["min_len"], q["index"]) for q in p2.queues()] == [(10, 1), (20, 2), (30, 3)]
-    assert list(e2) == [1, 5, 5]
+    assert list(e2) == [1, 5, 0]
 
 
 # ------------------------------------------------- O13: online adjust (R31) ---
@@ -757,3 +769,50 @@ def test_gap_rule_set_reading_example(orc):
 def test_gap_rule_set_matches_brute_on_distinct_values(orc, xs, alpha):
     s, _, st_ = orc.partition(xs, coarse_k=1, max_queues=256, alpha=alpha, gap_rule=1)
     assert st_.segments == len(brute.refine_brute(sorted(set(xs)), alpha))
+
+
+def _midpoint_bounds(clusters):
+    """A5 finalisation (R15) of Stage-2 clusters given as sorted value lists:
+    B_0 = lo_1, B_i = floor((hi_i + lo_{i+1}) / 2) + 1, B_m = hi_m + 1."""
+    lo = [c[0] for c in clusters]
+    hi = [c[-1] for c in clusters]
+    B = [lo[0]] + [(hi[i] + lo[i + 1]) // 2 + 1 for i in range(len(clusters) - 1)] + [hi[-1] + 1]
+    return list(zip(B[:-1], B[1:]))
+
+
+@settings(max_examples=120, deadline=None)
+@given(st.lists(st.integers(1, 80), min_size=1, max_size=40), st.sampled_from([1.5, 2.0, 3.0]),
+       st.sampled_from([0, 1]))
+def test_refine_cut_positions_match_brute(orc, xs, alpha, gap_rule):
+    """Eq. 2 cut POSITIONS, both gap readings (R10 multiset / SURVEY ambiguity 10
+    set): with one coarse cluster and no pruning (<= 40 items, max_queues = 256) the oracle's
+    queue bounds are the midpoint finalisation of brute.refine_brute's clusters (exact
+    rational Eq. 2 over the explicit gap list — the multiset, or the set of distinct
+    lengths), and every queue holds exactly its cluster's members."""
+    s, part, st_ = orc.partition(xs, coarse_k=1, max_queues=256, alpha=alpha, gap_rule=gap_rule)
+    assert s == orc.OK
+    base = sorted(xs) if gap_rule == 0 else sorted(set(xs))
+    clusters = brute.refine_brute(base, alpha)
+    qs = part.queues()
+    assert [(q["min_len"], q["max_len"]) for q in qs] == _midpoint_bounds(clusters)
+    v = np.asarray(xs)
+    for q, c in zip(qs, clusters):
+        assert q["count"] == int(((v >= c[0]) & (v <= c[-1])).sum())
+
+
+def test_refine_set_reading_cut_positions_example(orc):
+    """[1 x6, 2, 10, 11, 30]: multiset mean(G) = 29/9 splits at 10-2=8 and 30-11=19
+    (> 2 * 29/9 = 6.44); the set {1, 2, 10, 11, 30} has mean(G) = 29/4 and only 19 > 14.5
+    qualifies.  Bounds after the midpoint rule: multiset [1,7) [7,21) [21,31) ... checked
+    against the brute force and by hand."""
+    xs = [1] * 6 + [2, 10, 11, 30]
+    _, p0, _ = orc.partition(xs, coarse_k=1, max_queues=256)
+    _, p1, _ = orc.partition(xs, coarse_k=1, max_queues=256, gap_rule=1)
+    b0 = [(q["min_len"], q["max_len"]) for q in p0.queues()]
+    b1 = [(q["min_len"], q["max_len"]) for q in p1.queues()]
+    # multiset: gaps [0,0,0,0,0,1,8,1,19], mean 29/9, threshold 58/9 = 6.44 -> cuts after 2 and 11;
+    # {1x6, 2} then mean(G) = 1/6 -> split 1 | 2; {10, 11}: mean 1, gap 1 not > 2 -> stays
+    assert b0 == [(1, 2), (2, 7), (7, 21), (21, 31)]
+    # set: gaps [1, 8, 1, 19], mean 29/4, threshold 14.5 -> cut after 11 only; {1,2,10,11}: mean 10/3,
+    # threshold 20/3 -> 8 qualifies -> {1,2} | {10,11}; {1,2}: one gap = mean -> no split
+    assert b1 == [(1, 7), (7, 21), (21, 31)]
