@@ -46,7 +46,8 @@ typedef enum {
     EWSJF_ERR_EMPTY = 3,          /* empty history (no length >= 1)          */
     EWSJF_ERR_CAPACITY = 4,
     EWSJF_ERR_CUDA = 5,
-    EWSJF_ERR_UNSUPPORTED = 6     /* e.g. a history length above the kernel's range */
+    EWSJF_ERR_UNSUPPORTED = 6,    /* e.g. a history length above the kernel's range */
+    EWSJF_ERR_NCCL = 7            /* NCCL unavailable or a collective failed */
 } ewsjf_status;
 
 typedef struct ewsjf_ctx ewsjf_ctx;
@@ -64,8 +65,39 @@ const char  *ewsjf_last_error(const ewsjf_ctx *ctx);
  * later call.  *out receives the ctx.  Not thread-safe; one ctx per stream.  */
 ewsjf_status ewsjf_ctx_create(int device, void *cuda_stream, int64_t max_pool, int64_t max_history,
                               int32_t max_k, ewsjf_ctx **out);
+/* Switch the ctx to another stream.  The ctx's scratch is shared by all its
+ * calls, so the new stream is first made to wait (cudaStreamWaitEvent) for
+ * everything already queued on the old one; no host synchronisation. */
 ewsjf_status ewsjf_ctx_set_stream(ewsjf_ctx *ctx, void *cuda_stream);
 ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx *ctx);
+/* ------------------------------------------------------ NCCL (multi-GPU) ---
+ * The index-sharded tick (R22 "global index order" across ranks):
+ * with a communicator set on the ctx, ewsjf_tick treats d_len/d_arrival/d_cost
+ * as this rank's shard (ids global_base + i), runs the local route + score +
+ * per-queue reduction into a fixed-size exchange record, ncclAllGather's the
+ * records on the ctx stream and runs the same deterministic merge on every
+ * rank, so every rank receives the identical global result (outputs, bubbles
+ * in *part, primary).  All three steps are stream-ordered (CUDA-graph
+ * capturable when no host output is requested).  NCCL is resolved at run time
+ * (dlopen "libnccl.so.2": the process's loaded copy, else the system one);
+ * EWSJF_ERR_NCCL when it is unavailable or a collective fails.
+ *
+ * ewsjf_nccl_get_unique_id: one rank creates the id (128 bytes) and the caller
+ *   broadcasts it (e.g. over torch.distributed).
+ * ewsjf_ctx_init_nccl: ncclCommInitRank on the ctx device; the ctx owns the
+ *   communicator (destroyed by ewsjf_ctx_destroy / _detach_nccl).  Collective:
+ *   every rank calls it.  Allocates the exchange buffers (256 queues x max_k
+ *   per rank) once; no allocation on a later tick.
+ * ewsjf_ctx_attach_nccl: use a caller-created ncclComm_t (caller keeps
+ *   ownership and must outlive the ctx's use of it).
+ * ewsjf_ctx_detach_nccl: synchronise the ctx stream, drop the communicator
+ *   (destroy it if owned) and the exchange buffers; ewsjf_tick is single-GPU again. */
+#define EWSJF_NCCL_ID_BYTES 128
+ewsjf_status ewsjf_nccl_get_unique_id(uint8_t *id_out /* [128] */);
+ewsjf_status ewsjf_ctx_init_nccl(ewsjf_ctx *ctx, const uint8_t *id /* [128] */, int32_t rank, int32_t world);
+ewsjf_status ewsjf_ctx_attach_nccl(ewsjf_ctx *ctx, void *nccl_comm /* ncclComm_t */, int32_t rank, int32_t world);
+ewsjf_status ewsjf_ctx_detach_nccl(ewsjf_ctx *ctx);
+
 /* Number of SMs the ctx launches persistent kernels over (the "CTA rows"). */
 int32_t      ewsjf_ctx_num_ctas(const ewsjf_ctx *ctx);
 

@@ -15,7 +15,8 @@ MAX_QUEUES = 256
 HIST_BINS = 1 << 20
 MAX_K = 256
 
-OK, INVALID_ARG, DOMAIN, EMPTY, CAPACITY, CUDA_ERR, UNSUPPORTED = range(7)
+OK, INVALID_ARG, DOMAIN, EMPTY, CAPACITY, CUDA_ERR, UNSUPPORTED, NCCL_ERR = range(8)
+NCCL_ID_BYTES = 128
 SELECT_SCORE, SELECT_FIFO = 0, 1
 MIN_U, MAX_U = 0, 1
 
@@ -102,6 +103,7 @@ SYMBOLS = [
     "ewsjf_tick_merge", "ewsjf_score_select_sweep", "ewsjf_ctx_set_timing", "ewsjf_ctx_get_timing",
     "ewsjf_ctx_get_phases", "ewsjf_batch_build", "ewsjf_prune_empty",
     "ewsjf_history_hist", "ewsjf_partition_from_hist", "ewsjf_online_adjust",
+    "ewsjf_nccl_get_unique_id", "ewsjf_ctx_init_nccl", "ewsjf_ctx_attach_nccl", "ewsjf_ctx_detach_nccl",
 ]
 
 _lib = None
@@ -148,6 +150,10 @@ def load() -> C.CDLL:
     L.ewsjf_history_hist.argtypes = [V, V, I64, V, P(C.c_int64)]
     L.ewsjf_online_adjust.argtypes = [V, V, I64, C.c_double, P(Partition), P(C.c_int32)]
     L.ewsjf_partition_from_hist.argtypes = [V, V, I32, I64, P(PartitionParams), P(Partition), P(PartitionStats)]
+    L.ewsjf_nccl_get_unique_id.argtypes = [V]
+    L.ewsjf_ctx_init_nccl.argtypes = [V, V, I32, I32]
+    L.ewsjf_ctx_attach_nccl.argtypes = [V, V, I32, I32]
+    L.ewsjf_ctx_detach_nccl.argtypes = [V]
     for name in SYMBOLS:
         if name not in ("ewsjf_abi_version", "ewsjf_status_str", "ewsjf_last_error", "ewsjf_ctx_num_ctas",
                         "ewsjf_exchange_bytes"):

@@ -23,6 +23,8 @@ cudaError_t launch_ftick(const FArgs& A, const Policy& P, const MergeArgs& MA, b
                          cudaStream_t st);
 int64_t ftick_smem_bytes(bool has_cost, int lut_size, int nslots, int stages);
 bool sweep_diag(ewsjf_ctx* ctx, unsigned long long* cuts_inserts);
+ewsjf_status nccl_allgather(ewsjf_ctx* ctx, int64_t bytes);
+void nccl_release(ewsjf_ctx* ctx);
 }  // namespace ewsjf
 
 using namespace ewsjf;
@@ -41,6 +43,7 @@ extern "C" const char* ewsjf_status_str(ewsjf_status s) {
         case EWSJF_ERR_CAPACITY: return "capacity exceeded";
         case EWSJF_ERR_CUDA: return "CUDA error";
         case EWSJF_ERR_UNSUPPORTED: return "unsupported input";
+        case EWSJF_ERR_NCCL: return "NCCL error";
     }
     return "unknown status";
 }
@@ -87,6 +90,7 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
               cudaMalloc(&ctx->d_lut, kLutCap + 32) == cudaSuccess &&
               cudaMallocHost(&ctx->h_lut, kLutCap + 32) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->lut_ev, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->stream_ev, cudaEventDisableTiming) == cudaSuccess &&
               cudaMalloc(&ctx->gap, (size_t)ctx->gap_cap * sizeof(GapEntry)) == cudaSuccess &&
               cudaMalloc(&ctx->d_blog, sizeof(BubbleLog)) == cudaSuccess &&
               cudaMallocHost(&ctx->h_blog, sizeof(BubbleLog)) == cudaSuccess &&
@@ -126,7 +130,15 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
 
 extern "C" ewsjf_status ewsjf_ctx_set_stream(ewsjf_ctx* ctx, void* cuda_stream) {
     if (!ctx) return EWSJF_ERR_INVALID_ARG;
-    ctx->stream = (cudaStream_t)cuda_stream;
+    cudaStream_t ns = (cudaStream_t)cuda_stream;
+    if (ns != ctx->stream) {
+        // all ctx scratch (rows, counters, LUT, gap list) is shared by the ctx's calls:
+        // order the new stream after everything already queued on the old one
+        CU(cudaSetDevice(ctx->device));
+        CU(cudaEventRecord(ctx->stream_ev, ctx->stream));
+        CU(cudaStreamWaitEvent(ns, ctx->stream_ev, 0));
+        ctx->stream = ns;
+    }
     return EWSJF_OK;
 }
 
@@ -136,6 +148,8 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
     cudaDeviceSynchronize();
     if (ctx->h_lut) cudaFreeHost(ctx->h_lut);
     if (ctx->lut_ev) cudaEventDestroy(ctx->lut_ev);
+    if (ctx->stream_ev) cudaEventDestroy(ctx->stream_ev);
+    nccl_release(ctx);
     void* d[] = {ctx->f_rows, ctx->f_ovf_keys, ctx->f_ovf_code, ctx->d_lut, ctx->dbg, ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
                  ctx->d_blog, ctx->d_summary, ctx->d_len, ctx->d_arr, ctx->d_cost, ctx->d_qid, ctx->d_topk_id,
                  ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score, ctx->d_max_score};
@@ -500,7 +514,7 @@ static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, 
                       const ewsjf_select_params* sp, MergeArgs& M, int merge_mode, ewsjf_status* st) {
     const int nslots = part->n;
     const bool has_cost = d_cost != nullptr;
-    if (getenv("EWSJF_OLD_TICK") || !ctx->coop || nslots < 1 || nslots > 64 || ctx->num_sms > 160 ||
+    if (getenv("EWSJF_OLD_TICK") || getenv("EWSJF_NO_FTICK") || !ctx->coop || nslots < 1 || nslots > 64 || ctx->num_sms > 160 ||
         ctx->num_sms < nslots)
         return false;
     if (!aligned16(d_len) || !aligned16(d_arr) || (has_cost && !aligned16(d_cost)) ||
@@ -538,6 +552,8 @@ static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, 
     A.rows.cap = ctx->f_rc;
     A.gthr = ctx->gthr;
     A.board = ctx->board;
+    A.rboard = ctx->board + (size_t)64 * G * 2;      // [64][G] after the sample board [64][G][<=2]
+    A.refresh = (K <= G && G <= 160 && merge_mode != 0 && !getenv("EWSJF_NO_REFRESH")) ? 1 : 0;
     A.ovf_keys = ctx->f_ovf_keys;
     A.ovf_code = ctx->f_ovf_code;
     A.gap = ctx->gap;
@@ -605,10 +621,18 @@ static ewsjf_status tick_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float*
     return EWSJF_OK;
 }
 
+static ewsjf_status sharded_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, const float* d_cost,
+                                 int64_t n, int64_t gbase, ewsjf_partition_t* part, int32_t bubble_width,
+                                 const ewsjf_meta* theta, const ewsjf_select_params* sp, int32_t* d_qid_out,
+                                 const ewsjf_select_out* out);
+
 extern "C" ewsjf_status ewsjf_tick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arrival, const float* d_cost,
                                    int64_t n, int64_t global_base, ewsjf_partition_t* part, int32_t bubble_width,
                                    const ewsjf_meta* theta, const ewsjf_select_params* params, int32_t* d_qid_out,
                                    ewsjf_select_out* out) {
+    if (ctx && ctx->nccl_comm)
+        return sharded_impl(ctx, d_len, d_arrival, d_cost, n, global_base, part, bubble_width, theta, params,
+                            d_qid_out, out);
     return tick_impl(ctx, d_len, d_arrival, d_cost, n, global_base, part, bubble_width, theta, params, d_qid_out, out);
 }
 
@@ -729,10 +753,10 @@ extern "C" int64_t ewsjf_exchange_bytes(const ewsjf_ctx* ctx, int32_t n_queues, 
     return ex_layout(n_queues, k).total;
 }
 
-extern "C" ewsjf_status ewsjf_tick_local(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arrival,
-                                         const float* d_cost, int64_t n, int64_t global_base,
-                                         const ewsjf_partition_t* part, const ewsjf_meta* theta,
-                                         const ewsjf_select_params* sp, int32_t* d_qid_out, void* d_exchange) {
+static ewsjf_status local_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arrival, const float* d_cost,
+                               int64_t n, int64_t global_base, const ewsjf_partition_t* part,
+                               const ewsjf_meta* theta, const ewsjf_select_params* sp, int32_t* d_qid_out,
+                               void* d_exchange) {
     if (!ctx) return EWSJF_ERR_INVALID_ARG;
     ewsjf_status s;
     if ((s = check_partition(ctx, part)) != EWSJF_OK) return s;
@@ -745,9 +769,6 @@ extern "C" ewsjf_status ewsjf_tick_local(ewsjf_ctx* ctx, const int32_t* d_len, c
     ewsjf_weights_from_meta(theta, part, w);
     static thread_local Policy P;
     fill_policy(part, w, &P);
-    if ((s = run_partial(ctx, d_len, d_arrival, d_cost, nullptr, d_qid_out, n, global_base, part, P, sp, true,
-                         true)) != EWSJF_OK)
-        return s;
     CU(cudaMemsetAsync(d_exchange, 0, ex_layout(part->n, sp->k).total, ctx->stream));
     MergeArgs M = merge_args(ctx, part, sp, theta, 1);
     M.in_mode = MERGE_IN_ROWS;
@@ -757,6 +778,11 @@ extern "C" ewsjf_status ewsjf_tick_local(ewsjf_ctx* ctx, const int32_t* d_len, c
     M.n_local = n;
     M.ex_out = (unsigned char*)d_exchange;
     M.blog = nullptr;
+    // the fused kernel writes the exchange record itself (merge_phase after its grid barrier)
+    if (run_ftick(ctx, d_len, d_arrival, d_cost, d_qid_out, n, global_base, part, P, sp, M, 2, &s)) return s;
+    if ((s = run_partial(ctx, d_len, d_arrival, d_cost, nullptr, d_qid_out, n, global_base, part, P, sp, true,
+                         true)) != EWSJF_OK)
+        return s;
     cudaError_t e;
     {
         LaunchScope ls(ctx, KIND_MERGE);
@@ -766,10 +792,16 @@ extern "C" ewsjf_status ewsjf_tick_local(ewsjf_ctx* ctx, const int32_t* d_len, c
     return EWSJF_OK;
 }
 
-extern "C" ewsjf_status ewsjf_tick_merge(ewsjf_ctx* ctx, const void* d_exchange_all, int32_t world,
-                                         int64_t global_base, int64_t n_local, int32_t* d_qid_local,
-                                         ewsjf_partition_t* part, int32_t bubble_width, const ewsjf_meta* theta,
-                                         const ewsjf_select_params* sp, ewsjf_select_out* out) {
+extern "C" ewsjf_status ewsjf_tick_local(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arrival,
+                                         const float* d_cost, int64_t n, int64_t global_base,
+                                         const ewsjf_partition_t* part, const ewsjf_meta* theta,
+                                         const ewsjf_select_params* sp, int32_t* d_qid_out, void* d_exchange) {
+    return local_impl(ctx, d_len, d_arrival, d_cost, n, global_base, part, theta, sp, d_qid_out, d_exchange);
+}
+
+static ewsjf_status merge_impl(ewsjf_ctx* ctx, const void* d_exchange_all, int32_t world, int64_t global_base,
+                               int64_t n_local, int32_t* d_qid_local, ewsjf_partition_t* part, int32_t bubble_width,
+                               const ewsjf_meta* theta, const ewsjf_select_params* sp, const ewsjf_select_out* out) {
     if (!ctx) return EWSJF_ERR_INVALID_ARG;
     ewsjf_status s;
     if ((s = check_partition(ctx, part)) != EWSJF_OK) return s;
@@ -802,4 +834,34 @@ extern "C" ewsjf_status ewsjf_tick_merge(ewsjf_ctx* ctx, const void* d_exchange_
     if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "global merge: %s", cudaGetErrorString(e));
     if (out->h_summary) return finish_sync(ctx, part, out->h_summary, M.summary);
     return EWSJF_OK;
+}
+
+extern "C" ewsjf_status ewsjf_tick_merge(ewsjf_ctx* ctx, const void* d_exchange_all, int32_t world,
+                                         int64_t global_base, int64_t n_local, int32_t* d_qid_local,
+                                         ewsjf_partition_t* part, int32_t bubble_width, const ewsjf_meta* theta,
+                                         const ewsjf_select_params* sp, ewsjf_select_out* out) {
+    return merge_impl(ctx, d_exchange_all, world, global_base, n_local, d_qid_local, part, bubble_width, theta, sp,
+                      out);
+}
+
+// The index-sharded tick through the ctx's NCCL communicator:
+// local route + score + per-queue reduction into a fixed-size exchange record,
+// ncclAllGather of the records on the ctx stream, the same deterministic merge
+// on every rank.  No host synchronisation unless out->h_summary is set.
+static ewsjf_status sharded_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, const float* d_cost,
+                                 int64_t n, int64_t gbase, ewsjf_partition_t* part, int32_t bubble_width,
+                                 const ewsjf_meta* theta, const ewsjf_select_params* sp, int32_t* d_qid_out,
+                                 const ewsjf_select_out* out) {
+    ewsjf_status s;
+    if ((s = check_partition(ctx, part)) != EWSJF_OK) return s;
+    if ((s = check_select(ctx, sp)) != EWSJF_OK) return s;
+    if ((s = check_out(ctx, out)) != EWSJF_OK) return s;
+    if (sp->k > ctx->max_k) return fail(ctx, EWSJF_ERR_INVALID_ARG, "k > ctx max_k");
+    const int64_t bytes = ex_layout(part->n, sp->k).total;
+    if (bytes > ctx->ex_cap) return fail(ctx, EWSJF_ERR_CAPACITY, "exchange record %lld > %lld", (long long)bytes,
+                                         (long long)ctx->ex_cap);
+    if ((s = local_impl(ctx, d_len, d_arr, d_cost, n, gbase, part, theta, sp, d_qid_out, ctx->ex_local)) != EWSJF_OK)
+        return s;
+    if ((s = nccl_allgather(ctx, bytes)) != EWSJF_OK) return s;
+    return merge_impl(ctx, ctx->ex_all, ctx->nccl_world, gbase, n, d_qid_out, part, bubble_width, theta, sp, out);
 }

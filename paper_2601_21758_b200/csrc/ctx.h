@@ -16,6 +16,7 @@ struct SweepScratch;
 struct ewsjf_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaEvent_t stream_ev = nullptr;   // ewsjf_ctx_set_stream: orders the new stream after the old
     int64_t max_pool = 0, max_history = 0;
     int32_t max_k = 0;
     int num_sms = 0;
@@ -62,6 +63,14 @@ struct ewsjf_ctx {
     int32_t f_rc = 0;
     u64* f_ovf_keys = nullptr;
     unsigned char* f_ovf_code = nullptr;
+    // NCCL communicator of the index-sharded tick (nccl.cu); exchange buffers
+    // sized for 256 queues x max_k, allocated when the comm is set
+    void* nccl_comm = nullptr;
+    bool nccl_owned = false;
+    int32_t nccl_rank = 0, nccl_world = 0;
+    unsigned char* ex_local = nullptr;
+    unsigned char* ex_all = nullptr;
+    int64_t ex_cap = 0;
     // batch builder prefix scratch (batch.cu)
     uint32_t* d_bpre = nullptr;
     int64_t bpre_cap = 0;

@@ -177,6 +177,62 @@ __device__ __forceinline__ u64 block_kth(ForEach for_each, int K, unsigned* hist
     return prefix;
 }
 
+// Warp-wide valid bounds for two queues at once from R high words per lane each
+// (0 = absent): t[x] has its low kFLowBit bits zero and #(v[x] >= t[x]) >= K
+// over the real (nonzero) values, or 0 if fewer than K are present.  MSB-first
+// descent started below the common prefix of the real values and stopped at
+// bit kFLowBit (for fp32 bits: within 2^-(23-kFLowBit) relative), so the
+// queue's K-th key is >= (t << 32).  The two descents are interleaved and the
+// per-lane counts are summed as a tree, so a step is a few independent
+// compares + two REDUX (the dependent chain of a sequential count made this
+// ~250 cycles per step).
+constexpr int kFLowBit = 15;
+template <int R>
+__device__ __forceinline__ int tree_count_ge(const u32 (&v)[R], u32 cand) {
+    int c[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) c[r] = v[r] >= cand ? 1 : 0;
+#pragma unroll
+    for (int w = 1; w < R; w <<= 1)
+#pragma unroll
+        for (int r = 0; r + w < R; r += 2 * w) c[r] += c[r + w];
+    return c[0];
+}
+template <int R>
+__device__ __forceinline__ void warp_kth_hi2(const u32 (&v0)[R], const u32 (&v1)[R], int K, u32* t_out) {
+    u32 mx[2] = {0u, 0u}, mn[2] = {0xffffffffu, 0xffffffffu};
+    int nz[2] = {0, 0};
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        mx[0] = max(mx[0], v0[r]); mx[1] = max(mx[1], v1[r]);
+        mn[0] = v0[r] ? min(mn[0], v0[r]) : mn[0]; mn[1] = v1[r] ? min(mn[1], v1[r]) : mn[1];
+        nz[0] += v0[r] != 0u; nz[1] += v1[r] != 0u;
+    }
+    u32 t[2];
+    int hb = -1;
+    bool on[2];
+#pragma unroll
+    for (int x = 0; x < 2; x++) {
+        mx[x] = __reduce_max_sync(0xffffffffu, mx[x]);
+        mn[x] = __reduce_min_sync(0xffffffffu, mn[x]);
+        nz[x] = __reduce_add_sync(0xffffffffu, nz[x]);
+        on[x] = nz[x] >= K && K >= 1;
+        const u32 diff = mx[x] ^ mn[x];
+        const int h = diff ? 31 - __clz(diff) : -1;
+        t[x] = h >= 0 ? (mx[x] & ~((2u << h) - 1u)) : mx[x];   // common prefix: every real value is >= t
+        if (on[x]) hb = max(hb, h);
+    }
+    for (int bit = hb; bit >= kFLowBit; bit--) {
+        const u32 c0 = t[0] | (1u << bit), c1 = t[1] | (1u << bit);
+        const int n0 = __reduce_add_sync(0xffffffffu, tree_count_ge(v0, c0));
+        const int n1 = __reduce_add_sync(0xffffffffu, tree_count_ge(v1, c1));
+        if (n0 >= K) t[0] = c0;
+        if (n1 >= K) t[1] = c1;
+    }
+    t_out[0] = on[0] ? t[0] : 0u;
+    t_out[1] = on[1] ? t[1] : 0u;
+}
+
 // CTA-wide: copy the keys >= t given by for_each into out[] (any order), returns the count.
 template <typename ForEach>
 __device__ __forceinline__ int block_collect(ForEach for_each, u64 t, u64* out, int cap, FMisc* M) {
@@ -211,7 +267,7 @@ __global__ void __launch_bounds__(kFT, 1)
     float4* rec = (float4*)(smem + kFRecOff);           // [code][2]: {wb, wu, wf', thrf}, {secf, qid, cntoff, -}
     u64* thr64 = (u64*)(smem + L.thr64);
     u64* sec64 = (u64*)(smem + L.sec64);
-    u64* bmax = (u64*)(smem + L.bmax);
+    u32* bmax = (u32*)(smem + L.bmax);     // [q][m] high words of the CTA's top keys (native u32 atomics)
     int* rcnt = (int*)(smem + L.rcnt);
     FMisc* M = (FMisc*)(smem + L.misc);
     unsigned* hist = (unsigned*)(smem + L.hist);
@@ -275,7 +331,7 @@ __global__ void __launch_bounds__(kFT, 1)
         }
         for (int q = tid; q < kFMaxSlots; q += kFT) {
             thr64[q] = 0ull; sec64[q] = 0ull; rcnt[q] = 0;
-            for (int m = 0; m < kFBoardMax; m++) bmax[q * kFBoardMax + m] = 0ull;
+            for (int m = 0; m < kFBoardMax; m++) bmax[q * kFBoardMax + m] = 0u;
         }
         if (dbg && tid == 0) A.dbg[cta * 16 + 11] = fgtime();
         uint4* c4 = (uint4*)cntb;
@@ -310,6 +366,8 @@ __global__ void __launch_bounds__(kFT, 1)
         }
     };
     auto insert = [&](int q, u64 k) {
+        const u32 kh = (u32)(k >> 32);       // CTA max high word (refresh board)
+        if (kh > *(volatile u32*)&bmax[q * kFBoardMax]) atomicMax(&bmax[q * kFBoardMax], kh);
         const int pos = atomicAdd(&rcnt[q], 1);
         if (pos < RC) {
             rows_cta[q * row_stride + pos] = k;
@@ -382,8 +440,9 @@ __global__ void __launch_bounds__(kFT, 1)
     int scode[4] = {kFCodeNone, kFCodeNone, kFCodeNone, kFCodeNone};
     int cur_st = 0;             // ring stage of the next tile and its mbarrier parity
     uint32_t cur_par = 0u;
-    auto body = [&](auto full_tag, int i, bool sample) {
+    auto body = [&](auto full_tag, auto sample_tag, int i) {
         constexpr bool FULL = decltype(full_tag)::value;
+        constexpr bool SAMPLE = decltype(sample_tag)::value;
         const int64_t t = t0 + i;
         const int64_t i0 = t * kFTile + 4 * lane;
         int b[4];
@@ -444,7 +503,7 @@ __global__ void __launch_bounds__(kFT, 1)
                     if (j < nv) A.qid_out[i0 + j] = qo[j];
             }
         }
-        if (sample) {
+        if (SAMPLE) {
             // sample maxima (board) and exact secondary max of every valid member
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -455,35 +514,43 @@ __global__ void __launch_bounds__(kFT, 1)
                 const u64 k1 = SCORE ? ks : kf, k2 = SCORE ? kf : ks;
                 skey[j] = mem ? k1 : 0ull;
                 scode[j] = mem ? c : kFCodeNone;
+                // warp-aggregated per queue: one native u32 atomicMax (board) and one
+                // 64-bit CAS (exact secondary) per (warp, queue) instead of per request
+                const unsigned grp = __match_any_sync(0xffffffffu, mem ? c : -1);
                 if (mem) {
-                    if (k1 > *(volatile u64*)&bmax[c * kFBoardMax]) atomicMax(&bmax[c * kFBoardMax], k1);
-                    if (k2 > *(volatile u64*)&sec64[c]) atomicMax(&sec64[c], k2);
+                    const u32 h1 = __reduce_max_sync(grp, (u32)(k1 >> 32));
+                    const u32 h2 = __reduce_max_sync(grp, (u32)(k2 >> 32));
+                    const unsigned top = __ballot_sync(grp, (u32)(k2 >> 32) == h2);
+                    if ((u32)(k2 >> 32) == h2) {
+                        const u32 l2 = __reduce_max_sync(top, (u32)k2);
+                        if ((u32)k2 == l2) {              // the one lane holding the group's max secondary key
+                            if (k2 > *(volatile u64*)&sec64[c]) atomicMax(&sec64[c], k2);
+                        }
+                    }
+                    if (lane == __ffs(grp) - 1 && h1 > *(volatile u32*)&bmax[c * kFBoardMax])
+                        atomicMax(&bmax[c * kFBoardMax], h1);
                 }
             }
         }
         if (__any_sync(0xffffffffu, any)) {
-#pragma unroll 1
+            // the rare path, one warp-uniform test per request slot (no dynamic register indexing)
+#pragma unroll
             for (int j = 0; j < 4; j++) {
-                const int bj = j == 0 ? b[0] : (j == 1 ? b[1] : (j == 2 ? b[2] : b[3]));
-                const float aj = j == 0 ? a[0] : (j == 1 ? a[1] : (j == 2 ? a[2] : a[3]));
-                const float cj = j == 0 ? co[0] : (j == 1 ? co[1] : (j == 2 ? co[2] : co[3]));
-                const float sj = j == 0 ? sp[0] : (j == 1 ? sp[1] : (j == 2 ? sp[2] : sp[3]));
-                const int dj = j == 0 ? code[0] : (j == 1 ? code[1] : (j == 2 ? code[2] : code[3]));
-                const bool oj = j == 0 ? okv[0] : (j == 1 ? okv[1] : (j == 2 ? okv[2] : okv[3]));
-                const float4 w = rec[2 * dj];
-                const float4 r2 = rec[2 * dj + 1];
-                const float f1 = SCORE ? sj : aj, f2 = SCORE ? aj : sj;
-                const bool pj = (SCORE ? (f1 >= w.w) : (f1 <= w.w)) || (SCORE ? (f2 <= r2.x) : (f2 >= r2.x)) || !oj;
-                if (!pj) continue;
-                if (sample && dj < nslots && oj) continue;   // members of the sample: the sample block
-                rare(dj, bj, aj, cj, sj, oj, i0 + j);
+                const float4 w = rec[2 * code[j]];
+                const float4 r2 = rec[2 * code[j] + 1];
+                const float f1 = SCORE ? sp[j] : a[j], f2 = SCORE ? a[j] : sp[j];
+                bool pj = (SCORE ? (f1 >= w.w) : (f1 <= w.w)) || (SCORE ? (f2 <= r2.x) : (f2 >= r2.x)) || !okv[j];
+                if (SAMPLE) pj = pj && !(code[j] < nslots && okv[j]);   // members of the sample: the sample block
+                if (__any_sync(0xffffffffu, pj)) {
+                    if (pj) rare(code[j], b[j], a[j], co[j], sp[j], okv[j], i0 + j);
+                }
             }
         }
         if (FULL) issue(i + R, st);   // refill this lane's slots of the stage with the tile R ahead
     };
-    auto tile = [&](int i, bool sample) {
-        if (t0 + i < nfull) body(std::integral_constant<bool, true>(), i, sample);
-        else body(std::integral_constant<bool, false>(), i, sample);
+    auto tile = [&](auto sample_tag, int i) {
+        if (t0 + i < nfull) body(std::integral_constant<bool, true>(), sample_tag, i);
+        else body(std::integral_constant<bool, false>(), sample_tag, i);
     };
 
     // ---- collective: cut every row at/over its high-water mark to its exact K-th key
@@ -524,7 +591,7 @@ __global__ void __launch_bounds__(kFT, 1)
     };
 
     // ---- sample tile, board, bound
-    if (nt > 0) tile(0, true);
+    if (nt > 0) tile(std::integral_constant<bool, true>(), 0);
     __syncthreads();
     stamp(2);
     const int bm = A.board_m;
@@ -535,86 +602,62 @@ __global__ void __launch_bounds__(kFT, 1)
             for (int j = 0; j < 4; j++) {
                 const int c = scode[j];
                 if (c < nslots) {
-                    const u64 prev = bmax[c * kFBoardMax + m - 1];
-                    const u64 k = skey[j];
-                    if (k < prev && k > *(volatile u64*)&bmax[c * kFBoardMax + m]) atomicMax(&bmax[c * kFBoardMax + m], k);
+                    const u32 prev = bmax[c * kFBoardMax + m - 1];
+                    const u32 k = (u32)(skey[j] >> 32);
+                    if (k < prev && k > *(volatile u32*)&bmax[c * kFBoardMax + m]) atomicMax(&bmax[c * kFBoardMax + m], k);
                 }
             }
             __syncthreads();
         }
         for (int i = tid; i < nslots * bm; i += kFT) {
             const int q = i / bm, m = i % bm;
-            A.board[((size_t)q * G + cta) * bm + m] = bmax[q * kFBoardMax + m];
+            A.board[((size_t)q * G + cta) * bm + m] = (u64)bmax[q * kFBoardMax + m] << 32;
         }
         __threadfence();
         __syncthreads();
-        unsigned gen = 0;
         if (tid == 0) {
+            // publish, then wait until every CTA of this launch has published
+            // (monotone ticket: generation = ticket / G)
             const unsigned tk = atomicAdd(&A.ctr->pub, 1u);
-            gen = tk / (unsigned)G;
-            M->last = (tk % (unsigned)G) == (unsigned)(G - 1);
-            M->sel_d = (int)gen;
-        }
-        __syncthreads();
-        stamp(13);
-        gen = (unsigned)M->sel_d;
-        if (M->last) {
-            // K-th largest high word of the published keys of each queue: every key
-            // >= (t << 32) of >= K distinct real requests, a valid bound on the K-th key.
-            // MSB-first descent over the high words, the warp's queues interleaved.
-            const int nb = G * bm;
-            constexpr int kQW = kFMaxSlots / kFW;      // queues per warp (<= 4)
-            u32 v[kQW][kFBoardRegs];
-            u32 tq[kQW];
-            bool has[kQW];
-#pragma unroll
-            for (int k = 0; k < kQW; k++) {
-                const int q = warp + kFW * k;
-                int nz = 0;
-#pragma unroll
-                for (int r = 0; r < kFBoardRegs; r++) {
-                    const int j = lane + 32 * r;
-                    const u64 x = (q < nslots && j < nb) ? __ldcg(A.board + (size_t)q * nb + j) : 0ull;
-                    v[k][r] = x ? (u32)(x >> 32) : 0u;
-                    nz += x != 0ull;
-                }
-                has[k] = q < nslots && __reduce_add_sync(0xffffffffu, nz) >= K;
-                tq[k] = 0u;
-            }
-            for (int bit = 31; bit >= 0; bit--) {
-#pragma unroll
-                for (int k = 0; k < kQW; k++) {
-                    const u32 cand = tq[k] | (1u << bit);
-                    int c = 0;
-#pragma unroll
-                    for (int r = 0; r < kFBoardRegs; r++) c += v[k][r] >= cand;
-                    c = __reduce_add_sync(0xffffffffu, c);
-                    if (c >= K) tq[k] = cand;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < kQW; k++) {
-                const int q = warp + kFW * k;
-                // hi words of absent entries are 0 (and 0 is the weakest bound): t > 0 only counts real keys
-                if (lane == 0 && has[k] && tq[k]) atomicMax(&A.gthr[q], (u64)tq[k] << 32);
-            }
-            stamp(14);
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&A.ctr->ready), "r"(gen + 1u) : "memory");
-        } else if (tid == 0) {
+            const unsigned target = (tk / (unsigned)G + 1u) * (unsigned)G;
+            if (dbg) A.dbg[cta * 16 + 13] = fgtime();
             unsigned v;
             do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&A.ctr->ready) : "memory");
-                if ((int)(v - (gen + 1u)) < 0) __nanosleep(64);
-            } while ((int)(v - (gen + 1u)) < 0);
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&A.ctr->pub) : "memory");
+                if ((int)(v - target) < 0) __nanosleep(32);
+            } while ((int)(v - target) < 0);
         }
+        __syncthreads();
+        // every CTA turns the complete board into the same bounds (one warp per
+        // queue): the K-th largest high word t of the G*bm published keys, so
+        // >= K distinct real requests have keys >= (t << 32) -- a valid bound
+        const int nb = G * bm;
+        for (int q = warp; q < nslots; q += 2 * kFW) {
+            const int q1 = q + kFW;
+            u32 v0[kFBoardRegs], v1[kFBoardRegs];
+#pragma unroll
+            for (int r = 0; r < kFBoardRegs; r++) {
+                const int j = lane + 32 * r;
+                v0[r] = j < nb ? (u32)(__ldcg(A.board + (size_t)q * nb + j) >> 32) : 0u;
+                v1[r] = (j < nb && q1 < nslots) ? (u32)(__ldcg(A.board + (size_t)q1 * nb + j) >> 32) : 0u;
+            }
+            u32 t[2];
+            warp_kth_hi2<kFBoardRegs>(v0, v1, K, t);
+            if (lane == 0) {
+                thr64[q] = (u64)t[0] << 32;
+                if (cta == 0 && t[0]) atomicMax(&A.gthr[q], (u64)t[0] << 32);
+                if (q1 < nslots) {
+                    thr64[q1] = (u64)t[1] << 32;
+                    if (cta == 0 && t[1]) atomicMax(&A.gthr[q1], (u64)t[1] << 32);
+                }
+            }
+        }
+        stamp(14);
         __syncthreads();
     }
     // thresholds from the bound, fast secondary from the sample's exact max
     for (int q = tid; q < nslots; q += kFT) {
-        const u64 g = bm > 0 ? __ldcg(&A.gthr[q]) : 0ull;
-        thr64[q] = g;
+        const u64 g = thr64[q];
         const u32 hi = (u32)(g >> 32);
         const float inf = __int_as_float(0x7f800000);
         rec[2 * q].w = SCORE ? __uint_as_float(hi) : (g ? fifo_hi_to_f(hi) : inf);
@@ -632,18 +675,53 @@ __global__ void __launch_bounds__(kFT, 1)
     __syncwarp();
 
     // ---- stream the rest of the block; collectives on demand
-    int rq = warp;
+    // Progressive bound: at its checkpoint tile (1/16 .. 3/4 of the block) warp
+    // w < 6 publishes the CTA's running max key of every queue to the refresh
+    // board and turns the board's current content into a bound for one queue
+    // (K-th largest high word of the CTA maxima present: K distinct real keys
+    // lie above it, so it is valid however incomplete the board is).  No CTA
+    // waits; the bounds reach the others through gthr.
+    int chk = -1;
+    if (A.refresh && warp < 6) {
+        const int num = warp == 0 ? 1 : warp == 1 ? 2 : warp == 2 ? 4 : warp == 3 ? 6 : warp == 4 ? 8 : 12;
+        chk = (nt * num) >> 4;
+        if (chk < 1) chk = -1;
+    }
+    auto refresh = [&]() {
+        u64* rb = A.rboard;
+        for (int q = lane; q < nslots; q += 32) rb[(size_t)q * G + cta] = (u64)(*(volatile u32*)&bmax[q * kFBoardMax]) << 32;
+        __syncwarp();
+        const int qa = (cta * 12 + warp * 2) % nslots, qb = (qa + 1) % nslots;
+        u32 va[5], vb[5];
+#pragma unroll
+        for (int r = 0; r < 5; r++) {
+            const int j = lane + 32 * r;
+            va[r] = j < G ? (u32)(__ldcg(rb + (size_t)qa * G + j) >> 32) : 0u;
+            vb[r] = j < G ? (u32)(__ldcg(rb + (size_t)qb * G + j) >> 32) : 0u;
+        }
+        u32 t[2];
+        warp_kth_hi2<5>(va, vb, K, t);
+        if (lane == 0) {
+            if (t[0]) { atomicMax(&A.gthr[qa], (u64)t[0] << 32); raise_thr(qa, (u64)t[0] << 32); }
+            if (t[1]) { atomicMax(&A.gthr[qb], (u64)t[1] << 32); raise_thr(qb, (u64)t[1] << 32); }
+        }
+    };
+    // pick up raised global bounds: one queue per warp every other tile, the L2
+    // load issued one poll ahead so the warp never waits for it
+    int rq = warp % max(nslots, 1);
+    u64 gpoll = (lane == 0 && nslots > 0) ? __ldcg(&A.gthr[rq]) : 0ull;
     for (int i = 1;; i++) {
         if (*(volatile int*)&M->flag) collective();
         if (i >= nt) break;
-        tile(i, false);
-        if ((i & 3) == 0 && nslots > 0) {      // pick up a raised global bound (rotating queue)
-            if (rq >= nslots) rq = warp % nslots;
+        tile(std::integral_constant<bool, false>(), i);
+        if (i == chk) refresh();
+        if ((i & 1) == 0 && nslots > 0) {
             if (lane == 0) {
-                const u64 g = __ldcg(&A.gthr[rq]);
-                if (g) raise_thr(rq, g);
+                if (gpoll) raise_thr(rq, gpoll);
+                rq += kFW;
+                if (rq >= nslots) rq = (rq - nslots) % nslots;
+                gpoll = __ldcg(&A.gthr[rq]);
             }
-            rq += kFW;
         }
     }
     // done: keep serving collectives until every warp is done (a flag raised by
@@ -719,6 +797,8 @@ __global__ void __launch_bounds__(kFT, 1)
     }
     __syncthreads();
     stamp(6);
+    if (A.refresh)   // nobody reads the refresh board past the barrier: clear this CTA's column for the next tick
+        for (int q = tid; q < nslots; q += kFT) A.rboard[(size_t)q * G + cta] = 0ull;
 
     const unsigned long long graw = __ldcg(&A.ctr->gap_count);
     if (graw > 0 || A.merge == 2) {

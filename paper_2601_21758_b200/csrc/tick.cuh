@@ -58,6 +58,8 @@ struct FArgs {
     Rows rows;                  // keys [64][G][RC]
     u64* gthr;                  // [nslots]
     u64* board;                 // [64][G][board_m]
+    u64* rboard;                // [64][G] refresh board: CTA max key per queue (zero between ticks)
+    int32_t refresh;            // progressive bound refresh on (needs K <= G)
     u64* ovf_keys;              // [G][kFOvf]
     unsigned char* ovf_code;    // [G][kFOvf]
     GapEntry* gap;

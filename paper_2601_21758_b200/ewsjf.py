@@ -17,7 +17,7 @@ __all__ = [
     "EwsjfError", "Context", "make_partition", "meta", "select_params", "partition_params", "weights_from_meta",
     "Outputs", "tick", "tick_host", "score_select", "route", "partition", "score_select_sweep",
     "exchange_bytes", "tick_local", "tick_merge", "tick_sharded", "batch_build", "prune_empty",
-    "history_hist", "partition_from_hist", "reduce_hist", "partition_sharded", "online_adjust",
+    "history_hist", "partition_from_hist", "reduce_hist", "check_reduced", "partition_sharded", "online_adjust",
 ]
 
 
@@ -72,6 +72,29 @@ class Context:
         buf = (C.c_uint64 * n)()
         self.check(self.lib.ewsjf_ctx_get_phases(self.h, buf, n))
         return np.frombuffer(buf, dtype=np.uint64).reshape(self.num_ctas, 16).copy()
+
+    def init_nccl(self, rank: int = 0, world: int = 1, group=None):
+        """Give the ctx its own NCCL communicator (ewsjf_ctx_init_nccl): rank 0 creates
+        the unique id in the library and it is broadcast over ``group`` (any
+        torch.distributed backend; not needed at world 1).  From then on
+        ``tick`` is the index-sharded tick of SURVEY §8e (NCCL all-gather inside
+        the library)."""
+        buf = (C.c_uint8 * L.NCCL_ID_BYTES)()
+        if rank == 0:
+            s = self.lib.ewsjf_nccl_get_unique_id(buf)
+            if s != L.OK:
+                raise EwsjfError(s, "ewsjf_nccl_get_unique_id (NCCL unavailable?)")
+        if world > 1:
+            import torch.distributed as dist
+            obj = [bytes(buf) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            C.memmove(buf, obj[0], L.NCCL_ID_BYTES)
+        self.check(self.lib.ewsjf_ctx_init_nccl(self.h, buf, rank, world), (L.OK,))
+        self.nccl_world = world
+
+    def detach_nccl(self):
+        self.check(self.lib.ewsjf_ctx_detach_nccl(self.h), (L.OK,))
+        self.nccl_world = 0
 
     def check(self, s: int, allow=(L.OK, L.DOMAIN)) -> int:
         if s not in allow:
@@ -257,15 +280,26 @@ def partition(ctx: Context, length, params: L.PartitionParams | None = None):
 
 def history_hist(ctx: Context, length, hist_out=None):
     """ewsjf_history_hist: A1 histogram of a device history (int32 view of the uint32
-    bins, HIST_BINS + 1 entries).  Returns (hist, {"invalid", "over", "max_len"})."""
+    bins, HIST_BINS + 1 entries).  Returns (hist, {"invalid", "over", "max_len"}).
+
+    Lengths >= HIST_BINS do not raise here (status UNSUPPORTED, counted in
+    "over"): in a sharded run every rank must still enter the all-reduce, and
+    all of them then refuse together (``check_reduced``)."""
     _dev_check(length, torch.int32, "len")
     hist = hist_out if hist_out is not None else torch.empty(L.HIST_BINS + 1, dtype=torch.int32, device=length.device)
     _dev_check(hist, torch.int32, "hist_out")
     info = (C.c_int64 * 3)()
     ctx.use_current_stream()
     s = ctx.lib.ewsjf_history_hist(ctx.h, _ptr(length), length.numel(), _ptr(hist), info)
-    ctx.check(s, (L.OK,))
+    ctx.check(s, (L.OK, L.UNSUPPORTED))
     return hist, {"invalid": info[0], "over": info[1], "max_len": info[2]}
+
+
+def check_reduced(info: dict):
+    """After reduce_hist: every rank raises together if any shard held a length
+    the histogram cannot bin (the summed "over" count is identical on all ranks)."""
+    if info["over"] > 0:
+        raise EwsjfError(L.UNSUPPORTED, f"{info['over']} history lengths >= {L.HIST_BINS} across the shards")
 
 
 def partition_from_hist(ctx: Context, hist, max_len: int, n_invalid: int = 0,
@@ -309,7 +343,8 @@ def partition_sharded(ctx: Context, length_shard, params: L.PartitionParams | No
     """Refine-and-Prune of a history sharded across the ranks of ``group`` (NCCL):
     local histogram, all-reduce, A2..A6 on every rank (identical, replicated result)."""
     hist, info = history_hist(ctx, length_shard)
-    hist, info = reduce_hist(hist, info, group)
+    hist, info = reduce_hist(hist, info, group)      # every rank, even one that saw an over-long length
+    check_reduced(info)
     return partition_from_hist(ctx, hist, info["max_len"], info["invalid"], params)
 
 
