@@ -43,7 +43,7 @@ BYTES_PER_REQ = 16          # len 4 + arrival 4 + cost 4 read, qid 4 written (SU
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=10_000_000, help="pending requests per GPU")
@@ -55,6 +55,11 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true", help="skip the C5 Θ-sweep measurement")
     ap.add_argument("--sweep-thetas", type=int, default=256)
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 100M-history Refine-and-Prune measurement")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the in-run ncu dram-bytes probe")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C1/C2/balanced-C3 lines")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: --n is the TOTAL pool, split by index across the ranks")
     return ap.parse_args()
 
 
@@ -202,9 +207,8 @@ def run_sweep(E, ctx, dev, args):
     tm = sctx.timing()
     ms = e0.elapsed_time(e1) / reps
     pairs = n * len(thetas)
-    props = torch.cuda.get_device_properties(dev)
-    clk_ghz = 1.965
-    peak = props.multi_processor_count * 128 * clk_ghz * 1e9 / 4
+    ffma = sctx.ffma_rate()            # measured fp32 FFMA/s on this box
+    peak = ffma / 4                    # 4 fp32-pipe instructions per (request, Θ) pair
     achieved = pairs / (ms / 1e3)
     sctx.close()
     return {"workload": "C5: 256 Θ uniform in S:500 bounds (seed 502) x 1M bimodal snapshot (seed 501) routed by "
@@ -214,7 +218,8 @@ def run_sweep(E, ctx, dev, args):
             "kernel_ms_per_sweep": tm["sweep_ms"] / reps, "launches_per_sweep": tm["sweep_launches"] / reps,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "pairs/s",
                          "frac": achieved / peak,
-                         "peak_source": "derived: 148 SMs x 128 fp32 lanes x 1.965 GHz / 4 fp32-pipe ops per pair"},
+                         "peak_source": "measured: ewsjf_diag_ffma_rate (FFMA throughput microbenchmark) / "
+                                        "4 fp32-pipe instructions per pair", "ffma_per_s": ffma},
             "candidates_inserted_last_sweep": tm["candidates_inserted"]}
 
 
@@ -248,10 +253,11 @@ def run_batch(E, ctx, part, theta, copies, dev, n, max_req=256, max_tok=65536, r
             "batch_size": inf[0], "batch_tokens": inf[1], "status": inf[2], "primary": inf[3]}
 
 
-def run_c4(E, dev, local, reps=3):
-    """C4 (BASELINE configs[3]): Refine-and-Prune over a 100M heavy-tailed history on one GPU."""
+def run_c4(E, dev, local, kind="heavy", seed=402, reps=3):
+    """C4 (BASELINE configs[3]): Refine-and-Prune over a 100M history on one GPU
+    (SURVEY §8d seeds: bimodal 401, heavy 402)."""
     import torch
-    hist = torch.from_numpy(workload.heavy(100_000_000, 401)).to(dev)
+    hist = torch.from_numpy(workload.lengths(kind, 100_000_000, seed)).to(dev)
     cctx = E.Context(local, max_pool=1024, max_history=100_000_000, max_k=8)
     E.partition(cctx, hist)
     cctx.set_timing(True)
@@ -264,12 +270,192 @@ def run_c4(E, dev, local, reps=3):
     med = sorted(sts, key=lambda x: x["ms_total"])[len(sts) // 2]
     peak, src = peaks()
     hist_gbs = 4e8 / (med["ms_hist"] / 1e3) / 1e9
-    return {"workload": "C4: Refine-and-Prune of heavy(100M, seed 401), alpha=2, max_queues=32, MIN_U",
+    return {"workload": f"C4: Refine-and-Prune of {kind}(100M, seed {seed}), alpha=2, max_queues=32, MIN_U",
             "ms": med["ms_total"], "stages_ms": {k: med[k] for k in ("ms_hist", "ms_kmeans", "ms_refine", "ms_prune")},
             "kernel_ms_sum": tm["partition_ms"] / reps, "launches": tm["partition_launches"] / reps,
             "distinct": med["distinct"], "segments": med["segments"], "merges": med["merges"], "queues": part.n,
             "hist_roofline": {"bound": "hbm", "achieved": hist_gbs, "peak": peak, "unit": "GB/s",
                               "frac": hist_gbs / peak, "bytes": 4e8, "peak_source": src}}
+
+
+def median_ms(fn, reps=5, warm=1):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        ts.append(1e3 * (time.perf_counter() - t0))
+    return statistics.median(ts)
+
+
+def tick_kernel_us(E, ctx, pool_t, part, theta, sp, reps=50):
+    """Median-free mean of the tick kernel time (CUDA events on the ctx stream) over reps launches."""
+    import torch
+    ln, ar, co, q = pool_t
+    out = E.Outputs.alloc(sp.k, ln.device)
+    for _ in range(5):
+        E.tick(ctx, ln, ar, co, part, theta, sp, qid_out=q, out=out, sync=False)
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        E.tick(ctx, ln, ar, co, part, theta, sp, qid_out=q, out=out, sync=False)
+    e1.record()
+    torch.cuda.synchronize()
+    tm = ctx.timing()
+    ctx.set_timing(False)
+    return {"kernel_us": 1e3 * tm["tick_ms"] / max(tm["tick_launches"], 1), "step_us": 1e3 * e0.elapsed_time(e1) / reps}
+
+
+def oracle_rp_ms(hist, **kw):
+    import oracle as O
+    t0 = time.perf_counter()
+    s, part, st = O.partition(hist, **kw)
+    return 1e3 * (time.perf_counter() - t0), part
+
+
+def run_extra(E, dev, local, args, peak):
+    """SURVEY §8d rows besides the headline: C1 (1k pending, 10k history, one tick:
+    latency), C2 (100k pending, 1M bimodal history: R&P + tick) and the C3 tick on the
+    balanced 32-quantile partition (SURVEY hard part 4).  The oracle beside each R&P."""
+    import torch
+    res = {}
+    theta = E.meta(**workload.THETA0)
+    sp = E.select_params(k=64, mode=0, now=workload.NOW)
+    for name, hseed, pseed, npool, nhist in (("c1", 101, 102, 1_000, 10_000), ("c2", 201, 202, 100_000, 1_000_000)):
+        ctx = E.Context(local, max_pool=npool, max_history=nhist, max_k=64)
+        hist = workload.bimodal(nhist, hseed)
+        hd = torch.from_numpy(hist).to(dev)
+        rp_ms = median_ms(lambda: E.partition(ctx, hd), reps=5)
+        part, pst, _ = E.partition(ctx, hd)
+        pool = workload.pool("bimodal", npool, pseed)
+        pt = tuple(torch.from_numpy(pool[k]).to(dev) for k in ("len", "arrival", "cost")) + \
+            (torch.empty(npool, dtype=torch.int32, device=dev),)
+        tk = tick_kernel_us(E, ctx, pt, part, theta, sp)
+        o_ms, _ = oracle_rp_ms(hist)
+        res[name] = {"workload": f"{name.upper()}: history bimodal({nhist}, seed {hseed}), pool bimodal({npool}, "
+                                 f"seed {pseed}); GPU R&P + fused tick (K=64, SCORE)",
+                     "refine_and_prune_ms_median5": rp_ms,
+                     "stages_ms": {k: pst[k] for k in ("ms_hist", "ms_kmeans", "ms_refine", "ms_prune")},
+                     "segments": pst["segments"], "merges": pst["merges"], "queues": part.n,
+                     "tick_kernel_us": tk["kernel_us"], "tick_step_us": tk["step_us"],
+                     "tick_req_per_s": npool / (tk["step_us"] * 1e-6),
+                     "one_tick_total_us": 1e3 * rp_ms + tk["step_us"],
+                     "oracle_refine_and_prune_ms": o_ms}
+        ctx.close()
+    # C3 on the balanced 32-quantile partition of the same history
+    n = args.n
+    ctx = E.Context(local, max_pool=n, max_history=0, max_k=64)
+    qpart = E.make_partition(workload.quantile_bounds(workload.heavy(1_000_000, 301), 32))
+    pool = workload.pool("heavy", n, 302)
+    pt = tuple(torch.from_numpy(pool[k]).to(dev) for k in ("len", "arrival", "cost")) + \
+        (torch.empty(n, dtype=torch.int32, device=dev),)
+    tk = tick_kernel_us(E, ctx, pt, qpart, theta, sp, reps=100)
+    gbs = BYTES_PER_REQ * n / (tk["kernel_us"] * 1e-6) / 1e9
+    res["c3_balanced"] = {"workload": "C3 pool, balanced 32-quantile partition of heavy(1M, seed 301), K=64, SCORE",
+                          "tick_kernel_us": tk["kernel_us"], "tick_step_us": tk["step_us"],
+                          "req_per_s": n / (tk["step_us"] * 1e-6),
+                          "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                                       "frac": gbs / peak}}
+    ctx.close()
+    return res
+
+
+def measure_traffic(n, timeout=300):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the fused tick kernel, measured
+    in this run by re-executing this script's --traffic-probe mode under ncu (one GPU,
+    one profiled launch after warm-up).  Returns (bytes per launch, note)."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none",
+           "-k", "regex:ftick_kernel", "-s", "3", "-c", "1", "--csv", sys.executable, os.path.abspath(__file__),
+           "--traffic-probe", "--n", str(n)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    except Exception as e:  # noqa: BLE001
+        return None, f"ncu probe failed: {e}"
+    tot = 0.0
+    seen = 0
+    for line in r.stdout.splitlines():
+        if "dram__bytes_read.sum" in line or "dram__bytes_write.sum" in line:
+            f = [x.strip('"') for x in line.split('","')]
+            try:
+                unit, val = f[-2], float(f[-1].strip('"').replace(",", ""))
+            except Exception:  # noqa: BLE001
+                continue
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
+            tot += val * scale
+            seen += 1
+    if seen < 2:
+        return None, "ncu output not parsed: " + (r.stdout[-300:] + r.stderr[-300:]).replace("\n", " ")
+    return tot, "ncu dram__bytes_read.sum + dram__bytes_write.sum, one launch of ewsjf::ftick_kernel, this run"
+
+
+def traffic_probe(args):
+    import torch
+    import paper_2601_21758_b200 as E
+    dev = torch.device("cuda", 0)
+    ctx = E.Context(0, max_pool=args.n, max_history=1_000_000, max_k=64)
+    part, _, _ = E.partition(ctx, torch.from_numpy(workload.heavy(1_000_000, 301)).to(dev))
+    pool = workload.pool("heavy", args.n, 302)
+    ln, ar, co = (torch.from_numpy(pool[k]).to(dev) for k in ("len", "arrival", "cost"))
+    q = torch.empty_like(ln)
+    out = E.Outputs.alloc(args.k, dev)
+    for _ in range(5):
+        E.tick(ctx, ln, ar, co, part, E.meta(**workload.THETA0), E.select_params(k=args.k, mode=0), qid_out=q,
+               out=out, sync=False)
+    torch.cuda.synchronize()
+
+
+_SHARD = {}
+
+
+def _oracle_shard(a):
+    import oracle as O
+    lo, hi, k, mode = a
+    pool, opart = _SHARD["pool"], _SHARD["part"]
+    sp = O.select_params(k=k, mode=mode, now=workload.NOW)
+    t0 = time.perf_counter()
+    O.tick(pool["len"][lo:hi], pool["arrival"][lo:hi], pool["cost"][lo:hi], opart, O.meta(**workload.THETA0), sp,
+           global_base=lo)
+    return hi - lo, time.perf_counter() - t0
+
+
+def oracle_all_cores(pool, opart, n_sample, k, mode):
+    """The oracle on every host core: the first n_sample requests of the C3 pool split
+    by index into one shard per core (the natural parallel form of O8-O10's
+    per-request map; each shard a full oracle tick with global ids), wall time of
+    the whole parallel map."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    _SHARD["pool"] = {k: pool[k][:n_sample] for k in ("len", "arrival", "cost")}
+    _SHARD["part"] = opart
+    bounds = [(i * n_sample // cores, (i + 1) * n_sample // cores) for i in range(cores)]
+    ctxm = mp.get_context("fork")
+    with ctxm.Pool(cores) as pp:
+        pp.map(_oracle_shard, [(0, 1000, k, mode)] * cores)   # warm (page-in)
+        t0 = time.perf_counter()
+        r = pp.map(_oracle_shard, [(lo, hi, k, mode) for lo, hi in bounds])
+        wall = time.perf_counter() - t0
+    return sum(x for x, _ in r) / wall, wall, cores
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001
+        pass
+    return None
 
 
 def config_dict(args, opart_source):
@@ -283,6 +469,9 @@ def config_dict(args, opart_source):
 
 def main():
     args = parse()
+    if args.traffic_probe:
+        traffic_probe(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
@@ -299,19 +488,32 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
     mode = L.SELECT_SCORE if args.mode == "score" else L.SELECT_FIFO
-    n = args.n
+    if args.strong:       # the TOTAL pool split by index (rank r owns [floor(rN/P), floor((r+1)N/P)))
+        lo_r, hi_r = workload.shard_range(args.n, rank, ws)
+        n = hi_r - lo_r
+    else:
+        lo_r, n = rank * args.n, args.n
     ctx = E.Context(local, max_pool=n, max_history=1_000_000, max_k=max(args.k, 64))
 
     # ---- strategic loop: Refine-and-Prune on the GPU (published before the timed region)
     hist = torch.from_numpy(workload.heavy(1_000_000, 301)).to(dev)
     strategic = {}
     if args.partition == "rp":
-        ctx.set_timing(True)
-        part, pst, _ = E.partition(ctx, hist)
-        tm = ctx.timing()
-        strategic = {"refine_and_prune_ms": pst["ms_total"], "history": 1_000_000, "queues": part.n,
+        part, pst, _ = E.partition(ctx, hist)           # cold (first call)
+        cold_ms = pst["ms_total"]
+        sts = []
+        for _ in range(5):                              # warm: median of 5
+            _, st_, _ = E.partition(ctx, hist)
+            sts.append(st_)
+        pst = sorted(sts, key=lambda x: x["ms_total"])[2]
+        strategic = {"refine_and_prune_ms": pst["ms_total"], "refine_and_prune_ms_cold": cold_ms,
+                     "timing": "median of 5 warm calls (CUDA events per stage)", "history": 1_000_000,
+                     "queues": part.n,
                      "stages_ms": {k: pst[k] for k in ("ms_hist", "ms_kmeans", "ms_refine", "ms_prune")},
                      "distinct": pst["distinct"], "segments": pst["segments"], "merges": pst["merges"]}
+        if rank == 0 and not args.no_cpu_baseline:
+            o_ms, _ = oracle_rp_ms(workload.heavy(1_000_000, 301))
+            strategic["oracle_refine_and_prune_ms"] = o_ms
         psrc = "GPU Refine-and-Prune (ewsjf_partition) of heavy(1M, seed 301), alpha=2, max_queues=32, MIN_U"
     else:
         part = E.make_partition(workload.quantile_bounds(workload.heavy(1_000_000, 301), 32))
@@ -333,13 +535,18 @@ def main():
                                       "note": "synchronous call incl. window histogram + one CTA per boundary"}
 
     # ---- pool: this rank's 10M shard, 3 rotating copies in HBM
-    pool = workload.pool("heavy", n, 302 + 1000 * rank)
+    if args.strong:
+        full = workload.pool("heavy", args.n, 302)
+        pool = {k: v[lo_r:hi_r].copy() for k, v in full.items()}
+        del full
+    else:
+        pool = workload.pool("heavy", n, 302 + 1000 * rank)
     copies = []
     for c in range(3):
         copies.append((torch.from_numpy(pool["len"]).to(dev), torch.from_numpy(pool["arrival"]).to(dev),
                        torch.from_numpy(pool["cost"]).to(dev), torch.empty(n, dtype=torch.int32, device=dev)))
     out = E.Outputs.alloc(args.k, dev)
-    base = rank * n
+    base = lo_r
 
     def step(i):
         ln, ar, co, q = copies[i % 3]
@@ -356,7 +563,9 @@ def main():
 
     sampler = ClockSampler(local)
     sampler.start()
-    time.sleep(0.2)
+    t_wait = time.time()
+    while not sampler.rows and time.time() - t_wait < 5.0:   # nvidia-smi is sampling before the timed region
+        time.sleep(0.02)
     # timed region: K steps between a barrier + synchronize on both sides
     if group is not None:
         torch.distributed.barrier()
@@ -379,7 +588,7 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = n * ws / (ms_per_step / 1e3)
+    value = (args.n if args.strong else n * ws) / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel (the partial tick pass)
     peak, peak_src = peaks()
@@ -387,21 +596,14 @@ def main():
     merge_ms = tm["merge_ms"] / max(tm["merge_launches"], 1)
     achieved = BYTES_PER_REQ * n / (tick_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "ewsjf::stream_tick_kernel (fused: streaming route+score+filter, grid barrier, per-queue merge)",
+                "traffic": None, "kernel": "ewsjf::ftick_kernel (fused: streaming route+score+filter, sample bound, grid barrier, per-queue merge)",
                 "algorithmic_bytes_per_launch": BYTES_PER_REQ * n, "kernel_ms": tick_ms,
                 "merge_kernel_ms": merge_ms, "peak_source": peak_src,
                 "share_of_step": tick_ms / ms_per_step if ms_per_step else None}
-    prof_traffic = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(prof_traffic):
-        try:
-            with open(prof_traffic) as f:
-                roofline["traffic"] = json.load(f).get("bytes_per_launch_at_n", {}).get(str(n))
-        except Exception:
-            pass
-
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None,
         "dtype": "f32", "data": "synthetic", "config": config_dict(args, psrc), "roofline": roofline,
         "gpu_launches": int(tm["launches"] - launches0), "clocks": clocks, "strategic": strategic,
         "tick_summary": summary,
@@ -432,7 +634,10 @@ def main():
     if not args.no_sweep and ws == 1:
         line["sweep"] = run_sweep(E, ctx, dev, args)
     if ws == 1 and not args.no_c4:
-        line["c4"] = run_c4(E, dev, local)
+        line["c4"] = run_c4(E, dev, local, "heavy", 402)
+        line["c4_bimodal"] = run_c4(E, dev, local, "bimodal", 401)
+    if ws == 1 and not args.no_extra:
+        line.update(run_extra(E, dev, local, args, peak))
     if ws == 1 and args.k <= 256:
         bctx = E.Context(local, max_pool=n, max_history=0, max_k=256)
         line["batch"] = run_batch(E, bctx, part, theta, copies, dev, n)
@@ -445,11 +650,47 @@ def main():
             import oracle as O
             opart = O.make_partition(workload.quantile_bounds(workload.heavy(1_000_000, 301), 32))
         sample_n = 2_000_000
-        rate, secs = oracle_rate(pool, opart, args.k, 0 if args.mode == "score" else 1, sample_n)
+        omode = 0 if args.mode == "score" else 1
+        rate, secs = oracle_rate(pool, opart, args.k, omode, sample_n)
+        arate, asecs, cores = oracle_all_cores(pool, opart, 4_000_000, args.k, omode)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": f"first {sample_n} requests of the C3 pool, one oracle tick "
                                           f"({secs:.1f} s, single-threaded C fp64)",
-                                "host_cores_available": os.cpu_count()}
+                                "host_cores_available": os.cpu_count(), "cpu_model": cpu_model(),
+                                "all_cores": {"value": arate, "unit": UNIT, "cores": cores,
+                                              "sample": f"first 4,000,000 requests of the C3 pool split by index "
+                                                        f"into {cores} shards, one oracle tick per shard in "
+                                                        f"{cores} processes ({asecs:.1f} s wall)"}}
+        # parity on that sample: GPU tick vs the oracle (ids exact up to near-ties)
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            import oracle as O
+            from parity import compare_selection, gpu_result, to_gpu_partition
+            ln_s, ar_s, co_s = (torch.from_numpy(pool[k][:sample_n].copy()).to(dev) for k in ("len", "arrival", "cost"))
+            qs = torch.empty_like(ln_s)
+            pctx = E.Context(local, max_pool=sample_n, max_history=0, max_k=max(args.k, 64))
+            gout = E.tick(pctx, ln_s, ar_s, co_s, to_gpu_partition(E, opart), theta, sp, qid_out=qs)
+            osp = O.select_params(k=args.k, mode=omode, now=workload.NOW)
+            ref = O.tick(pool["len"][:sample_n], pool["arrival"][:sample_n], pool["cost"][:sample_n], opart,
+                         O.meta(**workload.THETA0), osp)
+            phi, _ = O.score_all(pool["len"][:sample_n], pool["arrival"][:sample_n], pool["cost"][:sample_n],
+                                 ref["qid"], ref["partition"], O.meta(**workload.THETA0), osp)
+            qid_ok = bool(np.array_equal(qs.cpu().numpy(), ref["qid"]))
+            rep = compare_selection(gpu_result(gout), ref, phi, pool["arrival"][:sample_n], omode, args.k)
+            line["parity_sample"] = {"requests": sample_n, "qid_exact": qid_ok, "near_ties": rep.near_ties,
+                                     "queues_checked": rep.checked_queues, "status": "pass"}
+            pctx.close()
+        except AssertionError as e:
+            line["parity_sample"] = {"requests": sample_n, "status": f"FAIL: {e}"}
+    if rank == 0 and ws == 1 and not args.no_traffic:
+        copies.clear()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        tb, note = measure_traffic(n)
+        roofline["traffic"] = tb
+        roofline["traffic_source"] = note
+        if tb:
+            roofline["traffic_over_algorithmic"] = tb / (BYTES_PER_REQ * n)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if group is not None:

@@ -129,6 +129,12 @@ ewsjf_status ewsjf_ctx_get_timing(ewsjf_ctx *ctx, ewsjf_timing *out);
  * Synchronises.                                                              */
 ewsjf_status ewsjf_ctx_get_phases(ewsjf_ctx *ctx, uint64_t *out, int32_t n);
 
+/* Measurement helper (bench.py): the GPU's fp32 FFMA rate, measured with a
+ * throughput microbenchmark on the ctx stream (8 independent FMA chains per
+ * thread, 8 x 256 threads per SM).  The Θ sweep's roofline peak is this rate
+ * divided by its 4 fp32-pipe instructions per (request, Θ) pair.  Synchronises. */
+ewsjf_status ewsjf_diag_ffma_rate(ewsjf_ctx *ctx, double *ffma_per_s);
+
 /* ------------------------------------------------------------- partition --- */
 /* Refine-and-Prune parameters (§4.2). alpha > 1 (Eq. 2 significance
  * ratio); min_width >= 1 (Stage-2 width stop, R13); max_queues in
@@ -144,6 +150,13 @@ typedef struct {
     int32_t merge_rule;
     int32_t gap_rule;    /* 0: Eq. 2 gaps over the multiset D (R10, default);
                             1: over the set of distinct lengths (SURVEY ambiguity 10 variant) */
+    int32_t kmeans_k;    /* 0: Refine-and-Prune (default).  1..EWSJF_MAX_QUEUES: the k-means-only
+                            partition of Table 3 "EWSJF (K-Means)": exact 1-D
+                            k-means of the history into kmeans_k clusters (DP, reading R32), then
+                            the midpoint finalisation (R15); alpha/min_width/max_queues/epsilon/
+                            coarse_k/merge_rule/gap_rule are not used.  k > distinct lengths ->
+                            one queue per distinct length.  The DP table (4 B x k x distinct) is
+                            allocated on first use and kept by the ctx. */
 } ewsjf_partition_params;
 
 /* One queue q_i = [min_len, max_len). */

@@ -108,6 +108,8 @@ def lib():
         L.or_rle.argtypes = [P(C.c_int32), C.c_int64, P(C.c_int32), P(C.c_int64), P(C.c_int64)]
         L.or_prefix.argtypes = [P(C.c_int32), P(C.c_int64), C.c_int64, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
         L.or_kmeans.argtypes = [P(C.c_int64), P(C.c_int64), C.c_int64, C.c_int32, P(C.c_int32)]
+        L.or_kmeans_dp.argtypes = [P(C.c_int64), P(C.c_int64), C.c_int64, C.c_int32, P(C.c_int32)]
+        L.or_partition_kmeans.argtypes = [P(C.c_int32), C.c_int64, C.c_int32, P(Partition), P(PartitionStats)]
         L.or_refine.restype = C.c_int64
         L.or_refine.argtypes = [P(C.c_int32), P(C.c_int64), C.c_int64, C.c_int64, C.c_double, C.c_int32,
                                 P(C.c_int64), P(C.c_int32)]
@@ -184,6 +186,29 @@ def kmeans(lengths, k):
         raise ValueError("k out of range")
     b = [0] + [int(t) for t in cuts[: k - 1]] + [len(v)]
     return [sorted(np.repeat(v[b[i]:b[i + 1]], c[b[i]:b[i + 1]]).tolist()) for i in range(k)]
+
+
+def kmeans_dp(lengths, k):
+    """O14: exact 1-D k-means for any k (DP, R32); the clusters as sorted value lists."""
+    v, c, _ = rle(lengths)
+    N, S1, _ = prefix(v, c)
+    ku = min(k, len(v))
+    cuts = np.zeros(max(ku, 1), np.int32)
+    st = lib().or_kmeans_dp(_p(N, C.c_int64), _p(S1, C.c_int64), len(v), k, _p(cuts, C.c_int32))
+    if st != OK:
+        raise ValueError("k out of range")
+    b = [0] + [int(t) for t in cuts[: ku - 1]] + [len(v)]
+    return [sorted(np.repeat(v[b[i]:b[i + 1]], c[b[i]:b[i + 1]]).tolist()) for i in range(ku)]
+
+
+def partition_kmeans(lengths, k):
+    """O14 partition: k-means-only queues with O5's finalisation (Table 3 "EWSJF (K-Means)").
+    Returns (status, Partition, stats)."""
+    x = _i32(lengths)
+    part = Partition()
+    st = PartitionStats()
+    s = lib().or_partition_kmeans(_p(x, C.c_int32), len(x), k, C.byref(part), C.byref(st))
+    return s, part, st
 
 
 def refine(values, alpha, min_width=1):

@@ -88,6 +88,45 @@ int or_kmeans(const int64_t *N, const int64_t *S1, int64_t M, int32_t k, int32_t
 }
 
 /* ------------------------------------------------------------------------- */
+/* O14 (next) exact 1-D k-means for any k: Table 3's
+ * "EWSJF (K-Means)" variant partitions the history by k-means alone with
+ * k = 5/10/30.  Same objective as O3 (R9: maximise
+ * Σ_c S1_c²/n_c over contiguous clusters of distinct values), evaluated by
+ * dynamic programming in O3's left-to-right summation order:
+ *   D_1[j] = S1[j]²/N[j],   D_l[j] = max_{l-1 <= i < j} D_{l-1}[i] + (S1[j]-S1[i])²/(N[j]-N[i]),
+ * then backtracking from j = M, at every level the SMALLEST i attaining the
+ * maximum (reading R32).  k > M -> k = M (as S:165).  cuts[0..k-2] ascending.
+ * O(k M²), plain.  For k <= 3 the value equals O3's optimum; only exact ties
+ * may pick other cuts (O3 breaks them lexicographically, R9).              */
+int or_kmeans_dp(const int64_t *N, const int64_t *S1, int64_t M, int32_t k, int32_t *cuts) {
+    if (k < 1 || M < 1) return OR_INVALID;
+    if (k > M) k = (int32_t)M;
+    if (k == 1) return OR_OK;
+    double *D = (double *)malloc(sizeof(double) * (size_t)k * (size_t)(M + 1));
+    int64_t *A = (int64_t *)malloc(sizeof(int64_t) * (size_t)k * (size_t)(M + 1));
+    for (int64_t j = 1; j <= M; j++) { D[j] = sq_over(S1[j], N[j]); A[j] = 0; }
+    for (int32_t l = 2; l <= k; l++) {
+        double *Dp = D + (size_t)(l - 2) * (M + 1), *Dl = D + (size_t)(l - 1) * (M + 1);
+        int64_t *Al = A + (size_t)(l - 1) * (M + 1);
+        for (int64_t j = l; j <= M; j++) {
+            double best = 0.0; int64_t bi = -1;
+            for (int64_t i = l - 1; i < j; i++) {
+                double F = Dp[i] + sq_over(S1[j] - S1[i], N[j] - N[i]);
+                if (bi < 0 || F > best) { best = F; bi = i; }
+            }
+            Dl[j] = best; Al[j] = bi;
+        }
+    }
+    int64_t j = M;
+    for (int32_t l = k; l >= 2; l--) {
+        j = A[(size_t)(l - 1) * (M + 1) + j];
+        cuts[l - 2] = (int32_t)j;
+    }
+    free(D); free(A);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
 /* O4  Stage 2 recursive refinement, Eq. 2 "Gap_j > α · mean(G)".
  * G = consecutive gaps of the sorted MULTISET inside the cluster (R10), so
  * mean(G) = span/(n-1) (telescoping).  Split at EVERY qualifying gap (R11),
@@ -262,6 +301,54 @@ int or_partition_run(const int32_t *len, int64_t n, const or_params *p,
     free(qlo); free(qhi); free(qc); free(qs1); free(qs2);
     if (st) *st = S;
     return S.n_invalid ? OR_DOMAIN : OR_OK;     /* b < 1 is a domain error */
+}
+
+/* O14 partition: k clusters from or_kmeans_dp, then O5's finalisation (R15) and
+ * the queue profiles; no Stage 2 or 3 (Table 3 "EWSJF (K-Means)"). */
+int or_partition_kmeans(const int32_t *len, int64_t n, int32_t k, or_partition *out, or_partition_stats *st) {
+    or_partition_stats S;
+    memset(&S, 0, sizeof S);
+    memset(out, 0, sizeof *out);
+    if (k < 1 || k > OR_MAXQ || n < 0) return OR_INVALID;
+    size_t nn = (size_t)(n > 0 ? n : 1);
+    int32_t *v = (int32_t *)malloc(sizeof(int32_t) * nn);
+    int64_t *c = (int64_t *)malloc(sizeof(int64_t) * nn);
+    int64_t M = or_rle(len, n, v, c, &S.n_invalid);
+    S.n_valid = n - S.n_invalid;
+    S.distinct = M;
+    if (M == 0) { free(v); free(c); if (st) *st = S; return OR_EMPTY; }
+    int64_t *N  = (int64_t *)malloc(sizeof(int64_t) * (size_t)(M + 1));
+    int64_t *S1 = (int64_t *)malloc(sizeof(int64_t) * (size_t)(M + 1));
+    int64_t *S2 = (int64_t *)malloc(sizeof(int64_t) * (size_t)(M + 1));
+    or_prefix(v, c, M, N, S1, S2);
+    int32_t ku = k < M ? k : (int32_t)M;
+    int32_t *cuts = (int32_t *)malloc(sizeof(int32_t) * (size_t)(ku > 1 ? ku : 1));
+    or_kmeans_dp(N, S1, M, ku, cuts);
+    S.k_used = ku;
+    S.t1 = ku >= 2 ? cuts[0] : 0;
+    S.t2 = ku >= 3 ? cuts[1] : 0;
+    S.segments = ku;
+    int64_t b[OR_MAXQ + 1];
+    b[0] = 0;
+    for (int32_t i = 0; i + 1 < ku; i++) b[i + 1] = cuts[i];
+    b[ku] = M;
+    out->n = ku;
+    out->next_id = ku;
+    for (int32_t i = 0; i < ku; i++) {
+        int64_t x = b[i], y = b[i + 1];
+        or_queue *q = &out->q[i];
+        q->id = i; q->index = i + 1;
+        q->min_len = (i == 0) ? v[x] : out->q[i - 1].max_len;
+        q->max_len = (i + 1 < ku) ? (int32_t)(((int64_t)v[y - 1] + (int64_t)v[y]) / 2 + 1) : v[y - 1] + 1;
+        q->count = N[y] - N[x]; q->sum = S1[y] - S1[x]; q->sumsq = S2[y] - S2[x];
+        q->mean = mean_of(q->sum, q->count);
+        q->density = rho_of(q->count, q->min_len, q->max_len);
+        q->sse = (double)q->sumsq - ((double)q->sum * (double)q->sum) / (double)q->count;
+        q->is_bubble = 0;
+    }
+    free(v); free(c); free(N); free(S1); free(S2); free(cuts);
+    if (st) *st = S;
+    return S.n_invalid ? OR_DOMAIN : OR_OK;
 }
 
 /* ------------------------------------------------------------------------- */

@@ -121,6 +121,9 @@ int     or_kmeans(const int64_t *N, const int64_t *S1, int64_t M, int32_t k, int
 
 /* O4 on one distinct-index range [x, y): appends final ranges' starts to
  * seg_lo (ascending), returns number appended; *depth = max depth seen. */
+/* O14: exact 1-D k-means for any k by DP (R32; Table 3 "EWSJF (K-Means)"). */
+int     or_kmeans_dp(const int64_t *N, const int64_t *S1, int64_t M, int32_t k, int32_t *cuts);
+int     or_partition_kmeans(const int32_t *len, int64_t n, int32_t k, or_partition *out, or_partition_stats *st);
 int64_t or_refine(const int32_t *v, const int64_t *N, int64_t x, int64_t y, double alpha,
                   int32_t min_width, int64_t *seg_start, int32_t *depth);
 

@@ -24,7 +24,7 @@ MIN_U, MAX_U = 0, 1
 class PartitionParams(C.Structure):
     _fields_ = [("alpha", C.c_double), ("min_width", C.c_int32), ("max_queues", C.c_int32),
                 ("epsilon", C.c_double), ("coarse_k", C.c_int32), ("merge_rule", C.c_int32),
-                ("gap_rule", C.c_int32)]
+                ("gap_rule", C.c_int32), ("kmeans_k", C.c_int32)]
 
 
 class Queue(C.Structure):
@@ -104,6 +104,7 @@ SYMBOLS = [
     "ewsjf_ctx_get_phases", "ewsjf_batch_build", "ewsjf_prune_empty",
     "ewsjf_history_hist", "ewsjf_partition_from_hist", "ewsjf_online_adjust",
     "ewsjf_nccl_get_unique_id", "ewsjf_ctx_init_nccl", "ewsjf_ctx_attach_nccl", "ewsjf_ctx_detach_nccl",
+    "ewsjf_diag_ffma_rate",
 ]
 
 _lib = None
@@ -154,6 +155,7 @@ def load() -> C.CDLL:
     L.ewsjf_ctx_init_nccl.argtypes = [V, V, I32, I32]
     L.ewsjf_ctx_attach_nccl.argtypes = [V, V, I32, I32]
     L.ewsjf_ctx_detach_nccl.argtypes = [V]
+    L.ewsjf_diag_ffma_rate.argtypes = [V, P(C.c_double)]
     for name in SYMBOLS:
         if name not in ("ewsjf_abi_version", "ewsjf_status_str", "ewsjf_last_error", "ewsjf_ctx_num_ctas",
                         "ewsjf_exchange_bytes"):

@@ -135,8 +135,15 @@ extern "C" ewsjf_status ewsjf_ctx_set_stream(ewsjf_ctx* ctx, void* cuda_stream) 
         // all ctx scratch (rows, counters, LUT, gap list) is shared by the ctx's calls:
         // order the new stream after everything already queued on the old one
         CU(cudaSetDevice(ctx->device));
-        CU(cudaEventRecord(ctx->stream_ev, ctx->stream));
-        CU(cudaStreamWaitEvent(ns, ctx->stream_ev, 0));
+        // not while either stream is being captured into a CUDA graph: an event recorded
+        // outside the capture would invalidate it (the capturing caller orders the streams)
+        cudaStreamCaptureStatus cs_old = cudaStreamCaptureStatusNone, cs_new = cudaStreamCaptureStatusNone;
+        CU(cudaStreamIsCapturing(ctx->stream, &cs_old));
+        CU(cudaStreamIsCapturing(ns, &cs_new));
+        if (cs_old == cudaStreamCaptureStatusNone && cs_new == cudaStreamCaptureStatusNone) {
+            CU(cudaEventRecord(ctx->stream_ev, ctx->stream));
+            CU(cudaStreamWaitEvent(ns, ctx->stream_ev, 0));
+        }
         ctx->stream = ns;
     }
     return EWSJF_OK;

@@ -46,6 +46,8 @@ constexpr int kFCodeNone = 0xFC;    // padding of a ragged lane
 constexpr int kFMaxSlots = 64;
 constexpr int kFBoardMax = 2;       // board keys per (queue, CTA); G * m <= 32 * kFBoardRegs
 constexpr int kFBoardRegs = 10;
+constexpr int kFMaxStages = 8;      // ring depth cap (EWSJF_STAGES)
+constexpr int kFClaim = 4;          // tiles per dynamic claim
 
 __host__ __device__ inline int64_t fal(int64_t x) { return (x + 127) & ~(int64_t)127; }
 
@@ -64,7 +66,7 @@ struct FMisc {
 };
 
 struct FSmem {
-    int64_t rec, lut, ring, bars, thr64, sec64, bmax, rcnt, misc, hist, surv, cnt, total;
+    int64_t rec, lut, ring, bars, thr64, sec64, bmax, rcnt, misc, hist, surv, stile, cnt, total;
 };
 // the per-code records and the LUT sit at fixed offsets (immediate addressing on the hot path)
 constexpr int kFRecOff = 0;
@@ -85,6 +87,7 @@ __host__ __device__ inline FSmem fsmem_layout(bool has_cost, int lut_size, int n
     L.misc = o;  o = fal(o + sizeof(FMisc));
     L.hist = o;  o = fal(o + 4LL * 256);
     L.surv = o;  o = fal(o + 8LL * EWSJF_MAX_K);
+    L.stile = o; o = fal(o + 8LL * kFW * kFMaxStages);
     L.cnt = o;   o = fal(o + 2LL * kFT * (nslots + 2));   // rows: members 0..nslots-1, bad, dummy
     L.total = o;
     return L;
@@ -280,21 +283,53 @@ __global__ void __launch_bounds__(kFT, 1)
     };
     stamp(0);
 
-    // ---- this warp's tile block: warp (cta, warp) -> block warp*G + cta
+    // ---- tile schedule.  The pool's ntiles tiles are cut into GW blocks of
+    // `stride` tiles (block blk = warp*G + cta).  The first S0 = min(R + 1, stride)
+    // tiles of each block are static (the warp's sample tile + its ring prologue:
+    // issued before any coordination and spread over the whole pool, so the
+    // sample is representative whatever the pool order); every other tile is
+    // claimed from a grid-wide counter in batches of kFClaim, so warps and CTAs
+    // finish together (static blocks left warps idling up to ~10 us).
     const int64_t ntiles = (A.n + kFTile - 1) / kFTile;
     const int64_t nfull = A.n / kFTile;
     const int64_t GW = (int64_t)G * kFW;
     const int64_t blk = (int64_t)warp * G + cta;
-    const int64_t t0 = blk * ntiles / GW, t1 = (blk + 1) * ntiles / GW;
-    const int nt = (int)(t1 - t0);
+    const int64_t stride = ntiles / GW;
+    const int S0 = (int)((int64_t)R + 1 < stride ? (int64_t)R + 1 : stride);
+    const int64_t dynb = stride - S0;                 // dynamic tiles per block
+    const int64_t ndyn = ntiles - GW * (int64_t)S0;   // tiles handed out by the counter
+    int64_t* stile = (int64_t*)(smem + L.stile) + warp * kFMaxStages;   // tile held by each ring stage (-1: none)
     auto stage = [&](int st, int a) -> unsigned char* { return ring + (st * narr + a) * kFTile * 4; };
+    int64_t seq = 0;                 // next position in this warp's tile sequence
+    unsigned long long cbase = 0ull, nbase = 0ull;   // claimed batches (lane 0): current, next (in flight)
+    if (lane == 0 && ndyn > 0) nbase = atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim);
+    auto next_tile = [&]() -> int64_t {               // all lanes; tile of sequence position seq, -1 = done
+        int64_t t = -1;
+        if (seq < S0) {
+            t = blk * stride + seq;
+        } else {
+            const int64_t j = seq - S0;
+            if (j % kFClaim == 0) {                   // batch boundary: the next batch becomes current
+                if (lane == 0) {
+                    cbase = nbase;
+                    nbase = cbase < (unsigned long long)ndyn
+                                ? atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim) : cbase;
+                }
+            }
+            long long d = (long long)__shfl_sync(0xffffffffu, cbase, 0) + j % kFClaim;
+            if (d < ndyn) t = d < GW * dynb ? (d / dynb) * stride + S0 + d % dynb : GW * stride + (d - GW * dynb);
+        }
+        seq++;
+        return t;
+    };
     // Per-lane cp.async (LDGSTS) ring: every lane copies, and later reads back, its
     // own 16 bytes per array of each tile; one commit group per tile (empty past
     // the end).  (A per-warp ring of 512-byte cp.async.bulk copies measured ~2.2 TB/s:
     // the bulk-copy engine costs ~90 cycles per copy, too many copies per SM.)
-    auto issue = [&](int i, int st) {   // all lanes: tile t0 + i into stage st = i % R
-        const int64_t t = t0 + i;
-        if (i < nt && t < nfull) {
+    auto issue = [&](int st) {        // all lanes: the next tile of the sequence into stage st
+        const int64_t t = next_tile();
+        if (lane == 0) stile[st] = t;
+        if (t >= 0 && t < nfull) {
             const int64_t off = t * kFTile + 4 * lane;
             cp_async16(stage(st, 0) + 16 * lane, A.len + off);
             cp_async16(stage(st, 1) + 16 * lane, A.arrival + off);
@@ -302,7 +337,8 @@ __global__ void __launch_bounds__(kFT, 1)
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    for (int i = 0; i < R; i++) issue(i, i);
+    for (int i = 0; i < R; i++) issue(i);
+    __syncwarp();
     stamp(10);
 
     // ---- setup while the first tiles are in flight
@@ -438,22 +474,16 @@ __global__ void __launch_bounds__(kFT, 1)
     // ---- one tile of 128 requests (4 per lane); sample: keep the keys, fill the sample maxima
     u64 skey[4] = {0ull, 0ull, 0ull, 0ull};
     int scode[4] = {kFCodeNone, kFCodeNone, kFCodeNone, kFCodeNone};
-    int cur_st = 0;             // ring stage of the next tile and its mbarrier parity
-    uint32_t cur_par = 0u;
-    auto body = [&](auto full_tag, auto sample_tag, int i) {
+    int cur_st = 0;             // ring stage of the next tile
+    auto body = [&](auto full_tag, auto sample_tag, int64_t t, int st) {
         constexpr bool FULL = decltype(full_tag)::value;
         constexpr bool SAMPLE = decltype(sample_tag)::value;
-        const int64_t t = t0 + i;
         const int64_t i0 = t * kFTile + 4 * lane;
         int b[4];
         float a[4], co[4];
         int nv = 4;
-        const int st = cur_st;            // = i % R
-        const uint32_t par = cur_par;     // = (i / R) & 1
-        if (++cur_st == R) { cur_st = 0; cur_par ^= 1u; }
         if (FULL) {
             cp_async_wait_n(R - 1);
-            (void)par;
             const int4 bv = ((const int4*)stage(st, 0))[lane];
             const float4 av = ((const float4*)stage(st, 1))[lane];
             float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -514,21 +544,12 @@ __global__ void __launch_bounds__(kFT, 1)
                 const u64 k1 = SCORE ? ks : kf, k2 = SCORE ? kf : ks;
                 skey[j] = mem ? k1 : 0ull;
                 scode[j] = mem ? c : kFCodeNone;
-                // warp-aggregated per queue: one native u32 atomicMax (board) and one
-                // 64-bit CAS (exact secondary) per (warp, queue) instead of per request
-                const unsigned grp = __match_any_sync(0xffffffffu, mem ? c : -1);
                 if (mem) {
-                    const u32 h1 = __reduce_max_sync(grp, (u32)(k1 >> 32));
-                    const u32 h2 = __reduce_max_sync(grp, (u32)(k2 >> 32));
-                    const unsigned top = __ballot_sync(grp, (u32)(k2 >> 32) == h2);
-                    if ((u32)(k2 >> 32) == h2) {
-                        const u32 l2 = __reduce_max_sync(top, (u32)k2);
-                        if ((u32)k2 == l2) {              // the one lane holding the group's max secondary key
-                            if (k2 > *(volatile u64*)&sec64[c]) atomicMax(&sec64[c], k2);
-                        }
-                    }
-                    if (lane == __ffs(grp) - 1 && h1 > *(volatile u32*)&bmax[c * kFBoardMax])
-                        atomicMax(&bmax[c * kFBoardMax], h1);
+                    // board: native u32 atomicMax of the high word; exact secondary: a
+                    // 64-bit CAS only when the high word ties or beats the current one
+                    const u32 h1 = (u32)(k1 >> 32);
+                    if (h1 > *(volatile u32*)&bmax[c * kFBoardMax]) atomicMax(&bmax[c * kFBoardMax], h1);
+                    if (k2 > *(volatile u64*)&sec64[c]) atomicMax(&sec64[c], k2);
                 }
             }
         }
@@ -546,11 +567,19 @@ __global__ void __launch_bounds__(kFT, 1)
                 }
             }
         }
-        if (FULL) issue(i + R, st);   // refill this lane's slots of the stage with the tile R ahead
     };
-    auto tile = [&](auto sample_tag, int i) {
-        if (t0 + i < nfull) body(std::integral_constant<bool, true>(), sample_tag, i);
-        else body(std::integral_constant<bool, false>(), sample_tag, i);
+    // process the tile in ring stage cur_st, refill the stage with the next tile
+    // of the sequence, advance; false when the sequence has ended
+    auto tile = [&](auto sample_tag) -> bool {
+        const int st = cur_st;
+        const int64_t t = stile[st];
+        if (t < 0) return false;
+        if (t < nfull) body(std::integral_constant<bool, true>(), sample_tag, t, st);
+        else body(std::integral_constant<bool, false>(), sample_tag, t, st);
+        __syncwarp();
+        issue(st);
+        cur_st = st + 1 == R ? 0 : st + 1;
+        return true;
     };
 
     // ---- collective: cut every row at/over its high-water mark to its exact K-th key
@@ -591,7 +620,7 @@ __global__ void __launch_bounds__(kFT, 1)
     };
 
     // ---- sample tile, board, bound
-    if (nt > 0) tile(std::integral_constant<bool, true>(), 0);
+    tile(std::integral_constant<bool, true>());
     __syncthreads();
     stamp(2);
     const int bm = A.board_m;
@@ -684,7 +713,7 @@ __global__ void __launch_bounds__(kFT, 1)
     int chk = -1;
     if (A.refresh && warp < 6) {
         const int num = warp == 0 ? 1 : warp == 1 ? 2 : warp == 2 ? 4 : warp == 3 ? 6 : warp == 4 ? 8 : 12;
-        chk = (nt * num) >> 4;
+        chk = (int)((ntiles / GW) * num >> 4);
         if (chk < 1) chk = -1;
     }
     auto refresh = [&]() {
@@ -706,16 +735,16 @@ __global__ void __launch_bounds__(kFT, 1)
             if (t[1]) { atomicMax(&A.gthr[qb], (u64)t[1] << 32); raise_thr(qb, (u64)t[1] << 32); }
         }
     };
-    // pick up raised global bounds: one queue per warp every other tile, the L2
-    // load issued one poll ahead so the warp never waits for it
+    // pick up raised global bounds: one queue per warp every 4 tiles, the L2 load
+    // issued one poll ahead (a global access waits behind the SM's ~100 KB of
+    // streaming loads in flight, ~2 us)
     int rq = warp % max(nslots, 1);
     u64 gpoll = (lane == 0 && nslots > 0) ? __ldcg(&A.gthr[rq]) : 0ull;
     for (int i = 1;; i++) {
         if (*(volatile int*)&M->flag) collective();
-        if (i >= nt) break;
-        tile(std::integral_constant<bool, false>(), i);
+        if (!tile(std::integral_constant<bool, false>())) break;
         if (i == chk) refresh();
-        if ((i & 1) == 0 && nslots > 0) {
+        if ((i & 3) == 0 && nslots > 0) {
             if (lane == 0) {
                 if (gpoll) raise_thr(rq, gpoll);
                 rq += kFW;
@@ -739,7 +768,7 @@ __global__ void __launch_bounds__(kFT, 1)
         dn = __shfl_sync(0xffffffffu, dn, 0);
         if (f) { collective(); continue; }
         if (dn == kFW) break;
-        __nanosleep(32);
+        __nanosleep(256);      // a done warp must not steal issue slots from the streaming ones
     }
     __syncthreads();
     stamp(4);
@@ -797,6 +826,7 @@ __global__ void __launch_bounds__(kFT, 1)
     }
     __syncthreads();
     stamp(6);
+    if (cta == 0 && tid == 0) A.ctr->ftiles = 0ull;   // every claim of this launch is done
     if (A.refresh)   // nobody reads the refresh board past the barrier: clear this CTA's column for the next tick
         for (int q = tid; q < nslots; q += kFT) A.rboard[(size_t)q * G + cta] = 0ull;
 

@@ -53,6 +53,9 @@ struct RpScratch {
     int32_t* treei;
     int kblocks;
     int64_t tree_n;
+    int32_t* kdp_a;                     // k-means DP argmax table [k][M + 1] (grown on demand)
+    int64_t kdp_cap;
+    int32_t* kcuts;                     // [256] k-means-only cuts
     int prune_cap;                      // largest m the shared-memory prune holds
     int prune_cap_lg;                   // ... with its leaves in global scratch
     cudaEvent_t ev[6];
@@ -508,6 +511,7 @@ __global__ void __launch_bounds__(kHT, 1)
 constexpr uint64_t kDead = ~0ull;
 constexpr uint16_t kNone = 0xffffu;
 constexpr int kPL = 5;
+constexpr int kSpec = 7;          // speculative chain-run depth (2*kSpec+1 queues x 2 profiles <= 32 lanes)
 // tree fan-out: 128 (4 children per lane) when the leaves are in shared memory,
 // 32 when they are read from global scratch (fewer bytes per node on the L2 path)
 __host__ __device__ constexpr int prune_fan(bool leaf_global) { return leaf_global ? 32 : 128; }
@@ -642,40 +646,263 @@ __global__ void __launch_bounds__(kHT, 1)
 #pragma unroll
     for (int l = 1; l < kPL; l++)
         if (l == nl - 1) off_top = lv_off[l];
-    int m = m0;
-    int64_t merges = 0;
-    while (m > max_queues && m > 1) {
-        const int p = nl > 1 ? iidx[off_top] : 0;
-        const int r = nxt[p];
-        const int rn = nxt[r];                  // m0 = end sentinel
-        const int rnn = rn < m0 ? nxt[rn] : m0;
-        const int q = prv[p];
-        // lanes 0 and 1 evaluate the two new pairs (p, rn) and (q, p) converged
-        const bool has = lane == 0 ? rn < m0 : (lane == 1 && q != kNone);
-        const int ua = lane == 0 ? p : q, ue = lane == 0 ? rn : p, uf = lane == 0 ? rnn : rn;
-        uint64_t ku = kDead;
-        if (lane < 2) ku = has ? U(ua, ue, has ? uf : ue) : kDead;
-        const uint64_t kp = __shfl_sync(0xffffffffu, ku, 0), kq = __shfl_sync(0xffffffffu, ku, 1);
-        if (lane == 0) {
-            nxt[p] = (uint16_t)rn;
-            if (rn < m0) prv[rn] = (uint16_t)p;
-            if (r < npair) leaf[r] = kDead;
-            leaf[p] = kp;
-            if (q != kNone) leaf[q] = kq;
-        }
-        __syncwarp();
-        int a = r, bb = p, c = q != kNone ? q : p;
+    // Merge chains (exact).  Under Eq. 3 the queue a merge produces nearly always
+    // takes part in the next merge (measured: 99.8 % of merges on the 1M heavy
+    // history, 100 % on bimodal), so after each tree argmin the merged queue Q is
+    // followed: its two pairs (L, Q) and (Q, R) are "dynamic" (kept out of the
+    // tree, evaluated directly from the per-segment prefixes), every other pair
+    // is static.  Leaves the chain touches are only marked dead (no node
+    // updates), so the root is a LOWER bound of the static minimum; a chain step
+    // whose best dynamic pair beats the root is exactly Eq. 3's argmin.  Otherwise
+    // the nodes over the touched leaf range are recomputed (exact static min S)
+    // and the step is decided against S with the lowest-pair tie rule; losing it
+    // ends the chain (dynamic pairs back into the tree).  Same merge sequence as
+    // one argmin per merge, ~50 tree refreshes per 15k merges.
+    auto refresh_range = [&](int x0, int x1) {     // recompute the nodes over leaves [x0, x1]
 #pragma unroll
         for (int l = 1; l < kPL; l++) {
             if (l >= nl) break;
-            a >>= kFanSh; bb >>= kFanSh; c >>= kFanSh;
-            node(l, a);
-            if (bb != a) node(l, bb);
-            if (c != a && c != bb) node(l, c);
+            const int j0 = x0 >> (kFanSh * l), j1 = x1 >> (kFanSh * l);
+            for (int j = j0; j <= j1; j++) node(l, j);
             __syncwarp();
         }
-        m--;
-        merges++;
+    };
+    auto root_key = [&]() -> uint64_t { return nl > 1 ? ikey[off_top] : (LG ? __ldcg(leaf) : leaf[0]); };
+    auto root_idx = [&]() -> int { return nl > 1 ? iidx[off_top] : 0; };
+    int m = m0;
+    int64_t merges = 0;
+    while (m > max_queues && m > 1) {
+        int p = root_idx();
+        {
+            const int r = nxt[p];
+            const int rn = nxt[r];                  // m0 = end sentinel
+            const int q = prv[p];
+            if (lane == 0) {
+                nxt[p] = (uint16_t)rn;
+                if (rn < m0) prv[rn] = (uint16_t)p;
+                if (r < npair) leaf[r] = kDead;
+                leaf[p] = kDead;                    // Q's right pair: dynamic
+                if (q != kNone) leaf[q] = kDead;    // Q's left pair: dynamic
+            }
+            __syncwarp();
+            m--;
+            merges++;
+            int d0 = q != kNone ? q : p, d1 = r < npair ? r : p;
+            uint64_t lb = root_key();               // stale-low bound of the static minimum
+            bool exact = false;
+            int dir = -1;                           // direction of the last chain merge: 0 left, 1 right
+            while (m > max_queues && m > 1) {
+                if (dir >= 0) {
+                    // ---- speculative direction run: assume the next kSpec merges all absorb
+                    // the neighbour on side `dir` (chains run one way for hundreds of merges:
+                    // 600 on average on the 1M heavy history).  Step k's two pairs are
+                    // evaluated for all k at once (30 lanes: rho/mean of the 2*kSpec+1 queues
+                    // involved, then 14 lanes: the pair utilities); the run is confirmed up to
+                    // the first step where the predicted pair is not Eq. 3's strict winner
+                    // (beaten by the other dynamic pair, not below the static lower bound lb,
+                    // a missing neighbour, or the budget reached) and the rest is left to the
+                    // general step below, so the merge sequence is unchanged.
+                    const int a0 = p;
+                    const int lim = min(kSpec, m - max_queues);
+                    // walk: x_t = t-th queue start on side dir (x_0 = the side's first neighbour)
+                    const int fixed_nb = dir == 0 ? nxt[a0] : prv[a0];          // bq (left run) / L (right run)
+                    const int fixed_end = dir == 0 ? (fixed_nb < m0 ? nxt[fixed_nb] : m0) : a0;
+                    // per lane: queue j = lane >> 1 (0..kSpec-1: Q_j, kSpec..2kSpec-1: N_{j-kSpec}, 2kSpec: F)
+                    const int j = lane >> 1;
+                    int xs = -1, xe = -1;                   // [xs, xe) of this lane's queue
+                    {
+                        // x[t] for t = 0..kSpec: left run x_0 = a0, x_{t+1} = prv[x_t];
+                        //                        right run x_0 = nxt[a0], x_{t+1} = nxt[x_t]
+                        int x = dir == 0 ? a0 : nxt[a0];
+                        int xq_s = -1, xn_s = -1, xn_e = -1;
+#pragma unroll
+                        for (int t = 0; t <= kSpec; t++) {
+                            const int xt = x;
+                            if (dir == 0) {
+                                if (j < kSpec && t == j) xq_s = xt;                      // Q_j = [x_j, bq)
+                                if (j >= kSpec && j < 2 * kSpec) {
+                                    if (t == j - kSpec + 1) xn_s = xt;                   // N_k = [x_{k+1}, x_k)
+                                    if (t == j - kSpec) xn_e = xt;
+                                }
+                                x = (xt != kNone && xt < m0) ? (int)prv[xt] : (int)kNone;
+                            } else {
+                                if (j < kSpec && t == j) xq_s = xt;                      // Q_j = [a0, x_j)
+                                if (j >= kSpec && j < 2 * kSpec) {
+                                    if (t == j - kSpec) xn_s = xt;                       // N_k = [x_k, x_{k+1})
+                                    if (t == j - kSpec + 1) xn_e = xt;
+                                }
+                                x = (xt != kNone && xt < m0) ? (int)nxt[xt] : (int)kNone;
+                            }
+                        }
+                        if (j < kSpec) {
+                            if (dir == 0) { xs = xq_s; xe = fixed_nb; } else { xs = a0; xe = xq_s; }
+                        } else if (j < 2 * kSpec) {
+                            xs = xn_s; xe = xn_e;
+                        } else if (j == 2 * kSpec) {
+                            if (dir == 0) { xs = fixed_nb; xe = fixed_end; } else { xs = fixed_nb; xe = a0; }
+                        }
+                    }
+                    const bool live = xs >= 0 && xs != kNone && xs < m0 && xe >= 0 && xe != kNone && xe <= m0 && xs < xe;
+                    double pv = 0.0;
+                    if (lane < 2 * (2 * kSpec + 1) && live) {
+                        const int64_t nn = __ldg(nx + xe) - __ldg(nx + xs);
+                        if (lane & 1) {
+                            const int64_t ss = __ldg(s1x + xe) - __ldg(s1x + xs);
+                            pv = nn > 0 ? __ddiv_rn((double)ss, (double)nn) : 0.0;
+                        } else {
+                            pv = __ddiv_rn((double)nn, (double)((int64_t)__ldg(lo + xe) - (int64_t)__ldg(lo + xs)));
+                        }
+                    }
+                    const unsigned livem = __ballot_sync(0xffffffffu, live && (lane & 1) == 0);
+                    // pair lanes u = 0..2kSpec-1: step k = u >> 1; side 0 = the run's pair (N_k with Q_k),
+                    // side 1 = the other dynamic pair (Q_k with F).  In the pair's left-right order.
+                    const int k = lane >> 1, side = lane & 1;
+                    const int qa = 2 * k, na = 2 * (kSpec + k), fa = 2 * (2 * kSpec);
+                    int s1l, s2l;                            // profile lanes of the pair's left / right queue
+                    if (dir == 0) { s1l = side == 0 ? na : qa; s2l = side == 0 ? qa : fa; }
+                    else          { s1l = side == 0 ? qa : fa; s2l = side == 0 ? na : qa; }
+                    const double r1 = __shfl_sync(0xffffffffu, pv, s1l & 31), m1 = __shfl_sync(0xffffffffu, pv, (s1l + 1) & 31);
+                    const double r2 = __shfl_sync(0xffffffffu, pv, s2l & 31), m2 = __shfl_sync(0xffffffffu, pv, (s2l + 1) & 31);
+                    uint64_t ku = kDead;
+                    const bool has = lane < 2 * kSpec && ((livem >> s1l) & 1u) && ((livem >> s2l) & 1u);
+                    if (lane < 2 * kSpec) {
+                        const double u = __ddiv_rn(__dadd_rn(r1, r2), __dadd_rn(fabs(__dsub_rn(m2, m1)), eps));
+                        if (has) ku = ukey(u, maxu);
+                    }
+                    // lane k (< kSpec): does step k go the predicted way?
+                    const uint64_t krun = __shfl_sync(0xffffffffu, ku, (2 * lane) & 31);
+                    const uint64_t koth = __shfl_sync(0xffffffffu, ku, (2 * lane + 1) & 31);
+                    // left run: the run pair is the LEFT pair, wins ties; right run: must beat the left pair strictly
+                    const bool wins = dir == 0 ? krun <= koth : krun < koth;
+                    const bool okk = lane < lim && krun != kDead && wins && krun < lb;
+                    const unsigned okm = __ballot_sync(0xffffffffu, okk);
+                    const int kst = __ffs(~okm) - 1;        // confirmed merges (leading ones)
+                    if (kst > 0) {
+                        // commit: the new Q and its links; leaves of every pair touched -> dead
+                        if (dir == 0) {
+                            // Q = [x_kst, bq): x_kst = start of N_{kst-1} = [x_kst, x_{kst-1})
+                            const int newa = __shfl_sync(0xffffffffu, xs, (2 * (kSpec + kst - 1)) & 31);
+                            const int nL = prv[newa];                 // the new left neighbour (links of newa intact)
+                            // x_0..x_{kst-1} (Q_t's starts, lanes 2t) stop being queue starts
+                            if ((lane & 1) == 0 && (lane >> 1) < kst && xs >= 0 && xs < npair) leaf[xs] = kDead;
+                            if (lane == 0) {
+                                nxt[newa] = (uint16_t)fixed_nb;
+                                if (fixed_nb < m0) prv[fixed_nb] = (uint16_t)newa;
+                                if (newa < npair) leaf[newa] = kDead;          // (Q, F): dynamic
+                                if (nL != kNone && nL < npair) leaf[nL] = kDead;  // (N, Q): dynamic
+                            }
+                            d0 = min(d0, nL != kNone ? nL : newa);
+                            p = newa;
+                        } else {
+                            // Q = [a0, x_kst): x_kst = end of N_{kst-1} = [x_{kst-1}, x_kst)
+                            const int newe = __shfl_sync(0xffffffffu, xe, (2 * (kSpec + kst - 1)) & 31);
+                            const int lastabs = __shfl_sync(0xffffffffu, xe, (2 * (kst - 1)) & 31);   // x_{kst-1}
+                            // absorbed starts x_0..x_{kst-1} (Q_t's ends, lanes 2t)
+                            if ((lane & 1) == 0 && (lane >> 1) < kst && xe >= 0 && xe < npair) leaf[xe] = kDead;
+                            if (lane == 0) {
+                                nxt[a0] = (uint16_t)newe;
+                                if (newe < m0) prv[newe] = (uint16_t)a0;
+                                if (a0 < npair) leaf[a0] = kDead;              // (Q, N): dynamic
+                            }
+                            d1 = max(d1, lastabs < npair ? lastabs : a0);
+                        }
+                        __syncwarp();
+                        m -= kst;
+                        merges += kst;
+                        exact = false;
+                        if (kst == lim && lim == kSpec) continue;   // the whole run held: speculate again
+                        if (!(m > max_queues && m > 1)) break;
+                    }
+                }
+                const int a = p, bq = nxt[a], L = prv[a];
+                const int c = bq < m0 ? nxt[bq] : m0;
+                // lanes 0..5: rho / mean of L = [L, a), Q = [a, bq), R = [bq, c) in parallel (one
+                // converged __ddiv_rn each: the canonical rho_of / mean_of); lanes 0 / 1 then form
+                // U(L, Q) / U(Q, R) from them (util_of's order).  Lanes 8..13 prefetch the
+                // per-segment prefixes ~24 segments beyond both ends into L1.
+                double pv = 0.0;
+                if (lane < 6) {
+                    const int qx = lane >> 1;                   // 0 = L, 1 = Q, 2 = R
+                    const int sx = qx == 0 ? L : (qx == 1 ? a : bq);
+                    const int ex = qx == 0 ? a : (qx == 1 ? bq : c);
+                    const bool live = qx == 0 ? L != kNone : (qx == 1 ? true : bq < m0);
+                    if (live) {
+                        const int64_t nn = __ldg(nx + ex) - __ldg(nx + sx);
+                        if (lane & 1) {                         // mean = S1 / n
+                            const int64_t ss = __ldg(s1x + ex) - __ldg(s1x + sx);
+                            pv = nn > 0 ? __ddiv_rn((double)ss, (double)nn) : 0.0;
+                        } else {                                // rho = n / width
+                            pv = __ddiv_rn((double)nn, (double)((int64_t)__ldg(lo + ex) - (int64_t)__ldg(lo + sx)));
+                        }
+                    }
+                } else if (lane >= 8 && lane < 14) {
+                    const int side = lane & 1, arr = (lane - 8) >> 1;
+                    const int ix = side ? min(c + 24, m0) : max(L == kNone ? 0 : L - 24, 0);
+                    const void* ad = arr == 0 ? (const void*)(nx + ix) : arr == 1 ? (const void*)(s1x + ix)
+                                                                                  : (const void*)(lo + ix);
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(ad));
+                }
+                const double rL = __shfl_sync(0xffffffffu, pv, 0), mL = __shfl_sync(0xffffffffu, pv, 1);
+                const double rQ = __shfl_sync(0xffffffffu, pv, 2), mQ = __shfl_sync(0xffffffffu, pv, 3);
+                const double rR = __shfl_sync(0xffffffffu, pv, 4), mR = __shfl_sync(0xffffffffu, pv, 5);
+                const bool has = lane == 0 ? L != kNone : (lane == 1 && bq < m0);
+                uint64_t ku = kDead;
+                if (lane < 2) {                                 // converged: same expression, lane-selected operands
+                    const double r1 = lane == 0 ? rL : rQ, r2 = lane == 0 ? rQ : rR;
+                    const double m1 = lane == 0 ? mL : mQ, m2 = lane == 0 ? mQ : mR;
+                    const double u = __ddiv_rn(__dadd_rn(r1, r2), __dadd_rn(fabs(__dsub_rn(m2, m1)), eps));
+                    if (has) ku = ukey(u, maxu);
+                }
+                const uint64_t kl = __shfl_sync(0xffffffffu, ku, 0), kr = __shfl_sync(0xffffffffu, ku, 1);
+                const bool left = kl <= kr;         // equal keys: the left pair has the lower position
+                const uint64_t cand = left ? kl : kr;
+                const int pos = left ? L : a;
+                bool ok = cand < lb;
+                if (!ok) {
+                    if (!exact) { refresh_range(d0, d1); exact = true; }
+                    const uint64_t S = root_key();
+                    const int si = root_idx();
+                    lb = S;
+                    ok = cand < S || (cand == S && cand != kDead && pos < si);
+                }
+                if (!ok) {                          // chain ends: the dynamic pairs go back into the tree
+                    if (lane == 0) {
+                        if (L != kNone) leaf[L] = kl;
+                        if (bq < m0) leaf[a] = kr;
+                    }
+                    __syncwarp();
+                    refresh_range(L != kNone ? L : a, a);
+                    break;
+                }
+                if (left) {                         // Q absorbs L: Q = [L, bq)
+                    const int LL = prv[L];
+                    if (lane == 0) {
+                        nxt[L] = (uint16_t)bq;
+                        if (bq < m0) prv[bq] = (uint16_t)L;
+                        leaf[L] = kDead;
+                        if (a < npair) leaf[a] = kDead;
+                        if (LL != kNone) leaf[LL] = kDead;
+                    }
+                    d0 = min(d0, LL != kNone ? LL : L);
+                    p = L;
+                    dir = 0;
+                } else {                            // Q absorbs R: Q = [a, c)
+                    if (lane == 0) {
+                        nxt[a] = (uint16_t)c;
+                        if (c < m0) prv[c] = (uint16_t)a;
+                        if (bq < npair) leaf[bq] = kDead;
+                        leaf[a] = kDead;
+                    }
+                    d1 = max(d1, bq < npair ? bq : a);
+                    dir = 1;
+                }
+                __syncwarp();
+                exact = false;
+                m--;
+                merges++;
+            }
+            if (!(m > max_queues && m > 1)) break;
+        }
     }
     if (lane == 0) {
         int k = 0;
@@ -690,6 +917,70 @@ __global__ void __launch_bounds__(kHT, 1)
         merges_out[1] = k;
         *done = 1;
     }
+}
+
+// ---- Table 3 "EWSJF (K-Means)": exact 1-D k-means for any
+// k by dynamic programming over the distinct-value prefixes (oracle O14, R32):
+//   D_1[j] = S1[j]^2/N[j],  D_l[j] = max_{l-1 <= i < j} D_{l-1}[i] + (S1[j]-S1[i])^2/(N[j]-N[i])
+// in the oracle's left-to-right rounding order (__dmul_rn/__ddiv_rn/__dadd_rn, no
+// contraction), smallest i on ties; backtracking from j = M.  One warp per j,
+// lanes stride over i (ascending, strict > keeps each lane's smallest i), then a
+// (value, smallest i) warp reduction.  fp64-ALU bound: ~M^2/2 divisions per layer.
+__device__ __forceinline__ double kdp_term(int64_t s, int64_t n) {
+    const double d = (double)s;
+    return __ddiv_rn(__dmul_rn(d, d), (double)n);
+}
+__global__ void kdp_first_kernel(const int64_t* __restrict__ N, const int64_t* __restrict__ S1, int64_t M, double* D) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= M; j += (int64_t)gridDim.x * blockDim.x)
+        D[j] = j >= 1 ? kdp_term(S1[j], N[j]) : 0.0;
+}
+__global__ void __launch_bounds__(256)
+    kdp_layer_kernel(const int64_t* __restrict__ N, const int64_t* __restrict__ S1, int64_t M, int l,
+                     const double* __restrict__ Dp, double* __restrict__ Dc, int32_t* __restrict__ Al) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // largest j first: the longest rows start early (balance)
+    for (int64_t t = w0; t <= M - l; t += nw) {
+        const int64_t j = M - t;
+        const int64_t nj = N[j], sj = S1[j];
+        double best = 0.0;
+        int64_t bi = -1;
+        for (int64_t i = l - 1 + lane; i < j; i += 32) {
+            const double F = __dadd_rn(Dp[i], kdp_term(sj - S1[i], nj - N[i]));
+            if (bi < 0 || F > best) { best = F; bi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (oi >= 0 && (bi < 0 || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; }
+        }
+        if (lane == 0) { Dc[j] = best; Al[j] = (int32_t)bi; }
+    }
+}
+// backtracking (one thread) + the clusters' queue bounds / statistics (R15 midpoints)
+__global__ void kdp_finish_kernel(const int32_t* __restrict__ v, const int64_t* __restrict__ N,
+                                  const int64_t* __restrict__ S1, const int64_t* __restrict__ S2, int64_t M, int k,
+                                  const int32_t* __restrict__ A, int32_t* cuts, int32_t* q_lo, int32_t* q_hi,
+                                  int64_t* q_n, int64_t* q_s1, int64_t* q_s2, int64_t* merges) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t j = M;
+    cuts[0] = 0;
+    for (int l = k; l >= 2; l--) {
+        j = A[(size_t)(l - 1) * (M + 1) + j];
+        cuts[l - 1] = (int32_t)j;
+    }
+    for (int i = 0; i < k; i++) {
+        const int64_t x = cuts[i], y = i + 1 < k ? cuts[i + 1] : M;
+        q_lo[i] = i == 0 ? v[x] : (int32_t)(((int64_t)v[x - 1] + (int64_t)v[x]) / 2 + 1);
+        q_hi[i] = i + 1 < k ? (int32_t)(((int64_t)v[y - 1] + (int64_t)v[y]) / 2 + 1) : v[M - 1] + 1;
+        q_n[i] = N[y] - N[x];
+        q_s1[i] = S1[y] - S1[x];
+        q_s2[i] = S2[y] - S2[x];
+    }
+    merges[0] = 0;
+    merges[1] = k;
 }
 
 __global__ void iota_kernel(int64_t* a, int64_t n) {
@@ -709,7 +1000,7 @@ void rp_free(ewsjf_ctx* ctx) {
     if (!R) return;
     void* p[] = {R->hist, R->stat, R->v, R->c, R->N, R->S1, R->S2, R->blk, R->t1, R->t3, R->kbF, R->kbI,
                  R->seg, R->segend, R->flag, R->out_i, R->q_lo, R->q_hi, R->q_n, R->q_s1, R->q_s2, R->merges,
-                 R->plo, R->phi_, R->pnext, R->pprev, R->pn, R->ps1, R->ps2, R->tree, R->treei};
+                 R->plo, R->phi_, R->pnext, R->pprev, R->pn, R->ps1, R->ps2, R->tree, R->treei, R->kdp_a, R->kcuts};
     for (void* x : p)
         if (x) cudaFree(x);
     for (auto e : R->ev)
@@ -743,7 +1034,7 @@ ewsjf_status rp_alloc(ewsjf_ctx* ctx) {
               cudaMalloc(&R->pnext, H * 4) == cudaSuccess && cudaMalloc(&R->pprev, H * 4) == cudaSuccess &&
               cudaMalloc(&R->pn, H * 8) == cudaSuccess && cudaMalloc(&R->ps1, H * 8) == cudaSuccess &&
               cudaMalloc(&R->ps2, H * 8) == cudaSuccess && cudaMalloc(&R->tree, tn * 8) == cudaSuccess &&
-              cudaMalloc(&R->treei, tn * 4) == cudaSuccess;
+              cudaMalloc(&R->treei, tn * 4) == cudaSuccess && cudaMalloc(&R->kcuts, 256 * 4) == cudaSuccess;
     for (auto& e : R->ev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
     if (!ok) { rp_free(ctx); return EWSJF_ERR_CUDA; }
     return EWSJF_OK;
@@ -753,6 +1044,81 @@ ewsjf_status rp_alloc(ewsjf_ctx* ctx) {
 
 namespace ewsjf {
 // A2..A6 from a finished histogram (bins 1..lmax); S carries the A1 statistics.
+// Table 3's k-means-only partition from the RLE prefixes (N, S1, S2 of M distinct values).
+static ewsjf_status rp_kmeans_only(ewsjf_ctx* ctx, int64_t M, const ewsjf_partition_params* p,
+                                   ewsjf_partition_t* out, ewsjf_partition_stats* stats, ewsjf_partition_stats& S) {
+    RpScratch* R = ctx->rp;
+    cudaStream_t st = ctx->stream;
+    const int k = (int)std::min<int64_t>(p->kmeans_k, M);
+    S.k_used = k;
+    const int64_t need = (int64_t)k * (M + 1);
+    if (need > R->kdp_cap) {                 // strategic call: grow the DP table once, keep it
+        CU(cudaStreamSynchronize(st));
+        if (R->kdp_a) cudaFree(R->kdp_a);
+        R->kdp_a = nullptr;
+        R->kdp_cap = 0;
+        CU(cudaMalloc(&R->kdp_a, (size_t)need * 4));
+        R->kdp_cap = need;
+    }
+    double* D[2] = {R->t1, R->t3};
+    {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        kdp_first_kernel<<<(int)std::min<int64_t>(1024, (M + 256) / 256), 256, 0, st>>>(R->N, R->S1, M, D[0]);
+    }
+    const int grid = ctx->num_sms * 8;
+    for (int l = 2; l <= k; l++) {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        kdp_layer_kernel<<<grid, 256, 0, st>>>(R->N, R->S1, M, l, D[l & 1], D[(l & 1) ^ 1],
+                                               R->kdp_a + (size_t)(l - 1) * (M + 1));
+    }
+    {
+        LaunchScope ls(ctx, KIND_PARTITION);
+        kdp_finish_kernel<<<1, 32, 0, st>>>(R->v, R->N, R->S1, R->S2, M, k, R->kdp_a, R->kcuts, R->q_lo, R->q_hi,
+                                            R->q_n, R->q_s1, R->q_s2, R->merges);
+    }
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(R->ev[4], st));
+    int32_t cuts[256], qlo[256], qhi[256];
+    int64_t qn[256], qs1[256], qs2[256];
+    CU(cudaMemcpyAsync(cuts, R->kcuts, 4 * k, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(qlo, R->q_lo, 4 * k, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(qhi, R->q_hi, 4 * k, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(qn, R->q_n, 8 * k, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(qs1, R->q_s1, 8 * k, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(qs2, R->q_s2, 8 * k, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    S.segments = k;
+    S.t1 = k >= 2 ? cuts[1] : 0;
+    S.t2 = k >= 3 ? cuts[2] : 0;
+    S.merges = 0;
+    const uint64_t ver = out->version;
+    memset(out, 0, sizeof *out);
+    out->n = k;
+    out->next_id = k;
+    out->version = ver + 1;
+    for (int i = 0; i < k; i++) {
+        ewsjf_queue& q = out->q[i];
+        q.id = i;
+        q.index = i + 1;
+        q.min_len = qlo[i];
+        q.max_len = qhi[i];
+        q.count = qn[i];
+        q.sum = qs1[i];
+        q.sumsq = qs2[i];
+        volatile double m = qn[i] > 0 ? (double)qs1[i] / (double)qn[i] : 0.0;
+        q.mean = m;
+        q.density = (double)qn[i] / (double)((int64_t)qhi[i] - (int64_t)qlo[i]);
+        volatile double sq = (double)qs1[i] * (double)qs1[i];
+        q.sse = (double)qs2[i] - sq / (double)qn[i];
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, R->ev[0], R->ev[1]); S.ms_hist = ms;
+    cudaEventElapsedTime(&ms, R->ev[1], R->ev[4]); S.ms_kmeans = ms;
+    cudaEventElapsedTime(&ms, R->ev[0], R->ev[4]); S.ms_total = ms;
+    if (stats) *stats = S;
+    return S.n_invalid ? EWSJF_ERR_DOMAIN : EWSJF_OK;
+}
+
 static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int lmax, const ewsjf_partition_params* p,
                                  ewsjf_partition_t* out, ewsjf_partition_stats* stats, ewsjf_partition_stats& S) {
     RpScratch* R = ctx->rp;
@@ -781,6 +1147,7 @@ static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int l
         if (stats) *stats = S;
         return fail(ctx, EWSJF_ERR_EMPTY, "no history length >= 1");
     }
+    if (p->kmeans_k > 0) return rp_kmeans_only(ctx, M, p, out, stats, S);
     const int k = p->coarse_k < M ? p->coarse_k : (int)M;
     S.k_used = k;
     if (k == 3) {
@@ -899,6 +1266,9 @@ static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int l
 
 static ewsjf_status check_rp_params(ewsjf_ctx* ctx, const ewsjf_partition_params* p, ewsjf_partition_t* out) {
     if (!p || !out) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null params/out");
+    if (p->kmeans_k < 0 || p->kmeans_k > EWSJF_MAX_QUEUES)
+        return fail(ctx, EWSJF_ERR_INVALID_ARG, "kmeans_k out of range");
+    if (p->kmeans_k > 0) return EWSJF_OK;      // k-means-only: the R&P parameters are not used
     if (!(p->alpha > 1.0) || p->min_width < 1 || p->max_queues < 1 || p->max_queues > EWSJF_MAX_QUEUES ||
         !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 || (p->merge_rule != 0 && p->merge_rule != 1) ||
         (p->gap_rule != 0 && p->gap_rule != 1))
@@ -911,11 +1281,10 @@ extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, in
                                         ewsjf_partition_stats* stats) {
     using namespace ewsjf;
     if (!ctx) return EWSJF_ERR_INVALID_ARG;
-    if (!p || !out) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null params/out");
-    if (!(p->alpha > 1.0) || p->min_width < 1 || p->max_queues < 1 || p->max_queues > EWSJF_MAX_QUEUES ||
-        !(p->epsilon > 0.0) || p->coarse_k < 1 || p->coarse_k > 3 || (p->merge_rule != 0 && p->merge_rule != 1) ||
-        (p->gap_rule != 0 && p->gap_rule != 1))
-        return fail(ctx, EWSJF_ERR_INVALID_ARG, "partition params out of range (S:121)");
+    {
+        ewsjf_status c = check_rp_params(ctx, p, out);
+        if (c != EWSJF_OK) return c;
+    }
     if (n < 0 || n > ctx->max_history) return fail(ctx, EWSJF_ERR_INVALID_ARG, "n=%lld > max_history", (long long)n);
     if (n > 0 && !d_len) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null history");
     RpScratch* R = ctx->rp;

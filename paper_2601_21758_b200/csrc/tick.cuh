@@ -35,6 +35,7 @@ struct Counters {        // device-global, zeroed by the merge for the next call
     unsigned int ready;     // generations whose sample bounds are in gthr
     unsigned int done;      // CTAs past the streaming phase (grid barrier)
     unsigned int pad0;
+    unsigned long long ftiles;   // ftick.cu: dynamic tile claims (reset after the grid barrier)
 };
 
 // Fused streaming tick (ftick.cu): route + score + filter + rows, sample bound,

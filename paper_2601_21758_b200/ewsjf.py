@@ -92,6 +92,12 @@ class Context:
         self.check(self.lib.ewsjf_ctx_init_nccl(self.h, buf, rank, world), (L.OK,))
         self.nccl_world = world
 
+    def ffma_rate(self) -> float:
+        """Measured fp32 FFMA/s of the device (ewsjf_diag_ffma_rate)."""
+        r = C.c_double(0.0)
+        self.check(self.lib.ewsjf_diag_ffma_rate(self.h, C.byref(r)), (L.OK,))
+        return r.value
+
     def detach_nccl(self):
         self.check(self.lib.ewsjf_ctx_detach_nccl(self.h), (L.OK,))
         self.nccl_world = 0
@@ -140,8 +146,9 @@ def select_params(k=64, mode=L.SELECT_SCORE, now=600.0, cost=(0.005, 0.0002, 1e-
 
 
 def partition_params(alpha=2.0, min_width=1, max_queues=32, epsilon=1e-6, coarse_k=3, merge_rule=L.MIN_U,
-                     gap_rule=0):
-    return L.PartitionParams(alpha, min_width, max_queues, epsilon, coarse_k, merge_rule, gap_rule)
+                     gap_rule=0, kmeans_k=0):
+    """kmeans_k > 0 selects the k-means-only partition (Table 3 "EWSJF (K-Means)")."""
+    return L.PartitionParams(alpha, min_width, max_queues, epsilon, coarse_k, merge_rule, gap_rule, kmeans_k)
 
 
 def weights_from_meta(theta: L.Meta, part: L.Partition):

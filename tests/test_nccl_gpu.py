@@ -47,10 +47,10 @@ def test_nccl_world1_gap_requests_and_graph_replay():
     the whole sharded tick captured once in a CUDA graph and replayed."""
     import paper_2601_21758_b200 as E
     dev = torch.device("cuda", 0)
-    bounds = [(32, 100), (100, 400), (700, 2000), (2001, 40000)]   # 441..629 make bubbles (Alg. 2)
+    bounds = [(32, 100), (100, 2001), (2001, 5000), (7000, 40000)]   # 5501..6299 make bubbles (Alg. 2)
     gp = E.make_partition(bounds)
     op = O.make_partition(bounds)
-    pool = workload.pool("heavy", 200_000, 77)
+    pool = workload.pool("heavy", 30_000, 77)
     t = {k: torch.from_numpy(pool[k]).to(dev) for k in ("len", "arrival", "cost")}
     th = E.meta(**workload.THETA0)
     sp = E.select_params(k=32, mode=0)
@@ -83,8 +83,9 @@ def test_nccl_world1_gap_requests_and_graph_replay():
     g.replay()
     torch.cuda.synchronize()
     np.testing.assert_array_equal(qid.cpu().numpy(), ref["qid"])
-    np.testing.assert_array_equal(out2.count.cpu().numpy(), out.count.cpu().numpy())
-    np.testing.assert_array_equal(out2.topk_id.cpu().numpy(), out.topk_id.cpu().numpy())
-    np.testing.assert_array_equal(out2.head_id.cpu().numpy(), out.head_id.cpu().numpy())
+    nq = out.summary["n_queues"]            # rows past nq are not written
+    np.testing.assert_array_equal(out2.count.cpu().numpy()[:nq], out.count.cpu().numpy()[:nq])
+    np.testing.assert_array_equal(out2.topk_id.cpu().numpy()[:nq], out.topk_id.cpu().numpy()[:nq])
+    np.testing.assert_array_equal(out2.head_id.cpu().numpy()[:nq], out.head_id.cpu().numpy()[:nq])
     ctx.detach_nccl()
     ctx.close()

@@ -143,3 +143,38 @@ def test_partition_from_hist_edge_cases(E, ctx):
 def test_partition_set_gap_reading(E, orc, ctx, kind, n, seed, rule):
     """gap_rule = 1 (Eq. 2 over the set of distinct lengths, SURVEY ambiguity 10)."""
     _check(*_both(E, orc, ctx, workload.lengths(kind, n, seed), merge_rule=rule, gap_rule=1))
+
+
+# ---- Table 3 "EWSJF (K-Means)": k-means-only partitions (oracle O14, R32; SURVEY §8f rank 4)
+def _check_kmeans(E, orc, ctx, hist, k):
+    h = np.ascontiguousarray(hist, dtype=np.int32)
+    gpart, gst, gs = E.partition(ctx, torch.from_numpy(h).cuda(), E.partition_params(kmeans_k=k))
+    os_, opart, ost = orc.partition_kmeans(h, k)
+    assert gs == os_, (gs, os_)
+    gq, oq = gpart.queues(), opart.queues()
+    assert len(gq) == len(oq) == ost.k_used == gst["k_used"]
+    for a, b in zip(gq, oq):
+        for key in ("id", "index", "min_len", "max_len", "count", "sum", "sumsq", "mean", "density", "sse"):
+            assert a[key] == b[key], (key, a, b)    # bit-exact (the fp64 DP decisions included)
+
+
+@pytest.mark.parametrize("k", [5, 10, 30])
+@pytest.mark.parametrize("kind,n,seed", [("bimodal", 10_000, 101), ("heavy", 50_000, 9)])
+def test_kmeans_only_partition_matches_oracle(E, orc, ctx, kind, n, seed, k):
+    _check_kmeans(E, orc, ctx, workload.lengths(kind, n, seed), k)
+
+
+@pytest.mark.parametrize("k", [5, 10, 30])
+def test_kmeans_only_partition_c2_history(E, orc, ctx, k):
+    """The C2 history (bimodal 1M, seed 201; ~12.5k distinct lengths)."""
+    _check_kmeans(E, orc, ctx, workload.bimodal(1_000_000, 201), k)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_kmeans_only_random_small(E, orc, ctx, seed):
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(1, 400))
+    hist = rng.integers(1, int(rng.choice([4, 30, 300, 5000])), size=n)
+    if seed % 4 == 0:
+        hist[0] = 0                                  # one invalid length: DOMAIN on both sides
+    _check_kmeans(E, orc, ctx, hist, int(rng.integers(1, 12)))
