@@ -191,7 +191,7 @@ def run_sweep(E, ctx, dev, args):
     qid, rsum = E.route(ctx, ln, c2part)
     thetas = [E.meta(**t) for t in workload.random_thetas(args.sweep_thetas, 502)]
     sp = E.select_params(k=16, mode=0, now=workload.NOW)
-    sctx = E.Context(dev.index or 0, max_pool=n, max_history=0, max_k=64)
+    sctx = E.Context(dev.index or 0, max_pool=n, max_history=0, max_k=64, max_sweep=n)
     outs = E.score_select_sweep(sctx, ln, ar, co, qid, c2part, thetas, sp)
     for _ in range(2):
         E.score_select_sweep(sctx, ln, ar, co, qid, c2part, thetas, sp, outs=outs)

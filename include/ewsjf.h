@@ -134,6 +134,10 @@ ewsjf_status ewsjf_ctx_get_phases(ewsjf_ctx *ctx, uint64_t *out, int32_t n);
  * thread, 8 x 256 threads per SM).  The Θ sweep's roofline peak is this rate
  * divided by its 4 fp32-pipe instructions per (request, Θ) pair.  Synchronises. */
 ewsjf_status ewsjf_diag_ffma_rate(ewsjf_ctx *ctx, double *ffma_per_s);
+/* Process-wide number of cudaMalloc / cudaMallocHost / cudaFree calls the
+ * library has made (contract check: hot calls -- tick, score_select, route,
+ * sweep, batch_build -- never change it once the ctx exists). */
+int64_t      ewsjf_alloc_count(void);
 
 /* ------------------------------------------------------------- partition --- */
 /* Refine-and-Prune parameters (§4.2). alpha > 1 (Eq. 2 significance
@@ -374,6 +378,11 @@ ewsjf_status ewsjf_tick_merge(ewsjf_ctx *ctx, const void *d_exchange_all, int32_
  * ranks scoring policies; FIFO keys do not depend on Θ): params->mode must be
  * EWSJF_SELECT_SCORE.  Async; returns DOMAIN if any Θ excluded elements,
  * INVALID_ARG on bad arguments (nothing launched).                          */
+/* Reserve the sweep's scratch (records + candidate rows) for snapshots of up
+ * to max_n requests; a strategic (setup) call that allocates and synchronises.
+ * ewsjf_score_select_sweep itself never allocates: it returns CAPACITY for a
+ * snapshot larger than the reservation (none made -> CAPACITY). */
+ewsjf_status ewsjf_ctx_reserve_sweep(ewsjf_ctx *ctx, int64_t max_n);
 ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx *ctx, const int32_t *d_len, const float *d_arrival,
                                       const float *d_cost, const int32_t *d_qid, int64_t n,
                                       const ewsjf_partition_t *part, const ewsjf_meta *thetas,

@@ -79,6 +79,9 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
     if (getenv("EWSJF_NO_FUSE")) ctx->coop = 0;
     const int G = ctx->num_sms;
     const size_t nrow = (size_t)kMaxSlots * G;
+    // gap list sized for the whole pool: App. D's Alg. 2 must stay exact however many
+    // pending requests fall between the queues (a stale partition)
+    ctx->gap_cap = (int32_t)std::max<int64_t>(8192, std::min<int64_t>(max_pool, 0x7fffffffLL));
     bool ok = cudaMalloc(&ctx->rows.keys, nrow * max_k * sizeof(u64)) == cudaSuccess &&
               cudaMalloc(&ctx->rows.cnt, nrow * sizeof(int32_t)) == cudaSuccess &&
               cudaMalloc(&ctx->rows.members, nrow * sizeof(int64_t)) == cudaSuccess &&
@@ -86,12 +89,17 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
               cudaMalloc(&ctx->gthr, kMaxSlots * sizeof(u64)) == cudaSuccess &&
               cudaMalloc(&ctx->board, nrow * 8 * sizeof(u64)) == cudaSuccess &&
               cudaMalloc(&ctx->ctr, sizeof(Counters)) == cudaSuccess &&
-              cudaMalloc(&ctx->dbg, (size_t)G * 16 * 8) == cudaSuccess &&
+              cudaMalloc(&ctx->dbg, (size_t)G * kDbgStride * 8) == cudaSuccess &&
               cudaMalloc(&ctx->d_lut, kLutCap + 32) == cudaSuccess &&
               cudaMallocHost(&ctx->h_lut, kLutCap + 32) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->lut_ev, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->stream_ev, cudaEventDisableTiming) == cudaSuccess &&
               cudaMalloc(&ctx->gap, (size_t)ctx->gap_cap * sizeof(GapEntry)) == cudaSuccess &&
+              cudaMalloc(&ctx->g_slot, (size_t)ctx->gap_cap * 4) == cudaSuccess &&
+              cudaMalloc(&ctx->g_res, (size_t)ctx->gap_cap * 4) == cudaSuccess &&
+              cudaMalloc(&ctx->g_u0, (size_t)ctx->gap_cap * 4) == cudaSuccess &&
+              cudaMalloc(&ctx->g_u1, (size_t)ctx->gap_cap * 4) == cudaSuccess &&
+              cudaMalloc(&ctx->g_tab, (3 + 5 * kMaxSlots) * 4) == cudaSuccess &&
               cudaMalloc(&ctx->d_blog, sizeof(BubbleLog)) == cudaSuccess &&
               cudaMallocHost(&ctx->h_blog, sizeof(BubbleLog)) == cudaSuccess &&
               cudaMalloc(&ctx->d_summary, sizeof(ewsjf_summary)) == cudaSuccess &&
@@ -104,6 +112,8 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
               cudaMalloc(&ctx->d_max_score, kMaxSlots * 4) == cudaSuccess;
     // fused tick rows: 64 queues x G CTAs x f_rc keys; overflow lists G x kFOvf
     ctx->f_rc = std::max(512, 4 * max_k);
+    ctx->bpre_cap = (int64_t)kMaxSlots * max_k;      // batch builder prefixes (global fallback)
+    ok = ok && cudaMalloc(&ctx->d_bpre, (size_t)ctx->bpre_cap * sizeof(uint32_t)) == cudaSuccess;
     ok = ok && cudaMalloc(&ctx->f_rows, (size_t)64 * G * ctx->f_rc * sizeof(u64)) == cudaSuccess &&
          cudaMalloc(&ctx->f_ovf_keys, (size_t)G * kFOvf * sizeof(u64)) == cudaSuccess &&
          cudaMalloc(&ctx->f_ovf_code, (size_t)G * kFOvf) == cudaSuccess;
@@ -157,7 +167,7 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
     if (ctx->lut_ev) cudaEventDestroy(ctx->lut_ev);
     if (ctx->stream_ev) cudaEventDestroy(ctx->stream_ev);
     nccl_release(ctx);
-    void* d[] = {ctx->f_rows, ctx->f_ovf_keys, ctx->f_ovf_code, ctx->d_lut, ctx->dbg, ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
+    void* d[] = {ctx->g_slot, ctx->g_res, ctx->g_u0, ctx->g_u1, ctx->g_tab, ctx->f_rows, ctx->f_ovf_keys, ctx->f_ovf_code, ctx->d_lut, ctx->dbg, ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
                  ctx->d_blog, ctx->d_summary, ctx->d_len, ctx->d_arr, ctx->d_cost, ctx->d_qid, ctx->d_topk_id,
                  ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score, ctx->d_max_score};
     for (void* p : d)
@@ -220,7 +230,7 @@ extern "C" ewsjf_status ewsjf_ctx_get_phases(ewsjf_ctx* ctx, uint64_t* out, int3
     if (!ctx || !out || n < 0) return EWSJF_ERR_INVALID_ARG;
     CU(cudaSetDevice(ctx->device));
     CU(cudaStreamSynchronize(ctx->stream));
-    const int64_t m = std::min<int64_t>(n, (int64_t)ctx->num_sms * 16);
+    const int64_t m = std::min<int64_t>(n, (int64_t)ctx->num_sms * kDbgStride);
     CU(cudaMemcpy(out, ctx->dbg, (size_t)m * 8, cudaMemcpyDeviceToHost));
     return EWSJF_OK;
 }
@@ -464,6 +474,8 @@ static MergeArgs merge_args(ewsjf_ctx* ctx, const ewsjf_partition_t* part, const
     M.ctr = ctx->ctr;
     M.gap = ctx->gap;
     M.gap_cap = ctx->gap_cap;
+    M.g_slot = ctx->g_slot; M.g_res = ctx->g_res; M.g_u0 = ctx->g_u0; M.g_u1 = ctx->g_u1; M.g_tab = ctx->g_tab;
+    M.seq = ++ctx->merge_seq;
     M.gthr = ctx->gthr;
     M.blog = ctx->d_blog;
     M.dbg = getenv("EWSJF_PHASES") ? ctx->dbg : nullptr;
@@ -548,7 +560,9 @@ static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, 
     A.lut_size = lutsz;
     A.stages = stages;
     const int G = ctx->num_sms;
-    A.board_m = 2;
+    // sample board: each CTA's top key per queue when G >= 2K (the bound's descent then runs
+    // over G keys per queue instead of 2G), its top two otherwise
+    A.board_m = 2 * K <= G ? 1 : 2;
     if (const char* e = getenv("EWSJF_BOARD_M")) A.board_m = std::max(0, std::min(2, atoi(e)));
     if (G * A.board_m < K || G * A.board_m > 320) A.board_m = 0;
     A.merge = merge_mode;

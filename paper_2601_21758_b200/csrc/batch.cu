@@ -173,13 +173,9 @@ extern "C" ewsjf_status ewsjf_batch_build(ewsjf_ctx* ctx, const int32_t* d_len, 
     const int32_t kk = budget->max_requests;
     const int64_t need = (int64_t)std::max(n_queues, 1) * kk;
     const bool in_smem = need * 4 <= std::min<int64_t>(kBSmemMax, ctx->smem_optin - 4096);
-    if (!in_smem && need > ctx->bpre_cap) {
-        if (ctx->d_bpre) cudaFree(ctx->d_bpre);
-        ctx->d_bpre = nullptr;
-        ctx->bpre_cap = 0;
-        CU(cudaMalloc(&ctx->d_bpre, need * sizeof(uint32_t)));
-        ctx->bpre_cap = need;
-    }
+    if (!in_smem && need > ctx->bpre_cap)      // preallocated by ewsjf_ctx_create for 256 queues x max_k
+        return fail(ctx, EWSJF_ERR_CAPACITY, "batch_build: %lld prefix entries > ctx capacity %lld (max_k)",
+                    (long long)need, (long long)ctx->bpre_cap);
     BatchArgs A;
     A.len = d_len; A.n = n; A.base = global_base;
     A.topk_id = sel->d_topk_id; A.count = sel->d_count;

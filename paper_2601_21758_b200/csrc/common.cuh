@@ -12,6 +12,16 @@
 #error "libewsjf targets sm_100a (B200) only"
 #endif
 
+// Every device / pinned allocation and free of the library goes through these
+// counters (ewsjf_alloc_count): the tests check that no hot call allocates.
+extern "C" void ewsjf_count_alloc_(void);
+static inline cudaError_t ewsjf_counted_malloc_(void** p, size_t n) { ewsjf_count_alloc_(); return cudaMalloc(p, n); }
+static inline cudaError_t ewsjf_counted_malloc_host_(void** p, size_t n) { ewsjf_count_alloc_(); return cudaMallocHost(p, n); }
+static inline cudaError_t ewsjf_counted_free_(void* p) { ewsjf_count_alloc_(); return cudaFree(p); }
+#define cudaMalloc(p, n) ewsjf_counted_malloc_((void**)(p), (n))
+#define cudaMallocHost(p, n) ewsjf_counted_malloc_host_((void**)(p), (n))
+#define cudaFree(p) ewsjf_counted_free_((void*)(p))
+
 namespace ewsjf {
 
 typedef unsigned long long u64;

@@ -38,7 +38,9 @@ struct ewsjf_ctx {
     cudaEvent_t lut_ev = nullptr;       // last upload
     int32_t lut_n = -1, lut_size = 0;
     std::vector<int32_t> lut_bounds;    // min/max of the cached partition
-    int32_t gap_cap = 8192;
+    int32_t gap_cap = 8192;             // gap list entries (max(8192, max_pool))
+    int32_t *g_slot = nullptr, *g_res = nullptr, *g_u0 = nullptr, *g_u1 = nullptr, *g_tab = nullptr;
+    uint32_t merge_seq = 0;             // launches of merge_phase (Alg. 2 table publication)
     BubbleLog* d_blog = nullptr;
     BubbleLog* h_blog = nullptr;        // pinned
     ewsjf_summary* d_summary = nullptr;

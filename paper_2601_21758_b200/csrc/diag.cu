@@ -30,6 +30,11 @@ __global__ void __launch_bounds__(256) ffma_probe_kernel(float* out, int iters, 
 
 using namespace ewsjf;
 
+#include <atomic>
+static std::atomic<long long> g_allocs{0};
+extern "C" void ewsjf_count_alloc_(void) { g_allocs.fetch_add(1, std::memory_order_relaxed); }
+extern "C" int64_t ewsjf_alloc_count(void) { return (int64_t)g_allocs.load(std::memory_order_relaxed); }
+
 extern "C" ewsjf_status ewsjf_diag_ffma_rate(ewsjf_ctx* ctx, double* ffma_per_s) {
     if (!ctx || !ffma_per_s) return EWSJF_ERR_INVALID_ARG;
     CU(cudaSetDevice(ctx->device));

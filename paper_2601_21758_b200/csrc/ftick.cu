@@ -60,7 +60,7 @@ struct FMisc {
     int sel_d, sel_cd;
     int pn;             // merge: candidate pool fill
     unsigned sel_above;
-    int pad;
+    int maxnc;          // merge: longest candidate row
     unsigned long long members, sec;
     unsigned long long tcoll;
 };
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kFT, 1)
     unsigned char* ring = smem + L.ring + (int64_t)warp * R * narr * kFTile * 4;
     const bool dbg = A.dbg != nullptr;
     auto stamp = [&](int s) {
-        if (dbg && tid == 0) A.dbg[cta * 16 + s] = fgtime();
+        if (dbg && tid == 0) A.dbg[cta * kDbgStride + s] = fgtime();
     };
     stamp(0);
 
@@ -302,7 +302,10 @@ __global__ void __launch_bounds__(kFT, 1)
     auto stage = [&](int st, int a) -> unsigned char* { return ring + (st * narr + a) * kFTile * 4; };
     int64_t seq = 0;                 // next position in this warp's tile sequence
     unsigned long long cbase = 0ull, nbase = 0ull;   // claimed batches (lane 0): current, next (in flight)
-    if (lane == 0 && ndyn > 0) nbase = atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim);
+    // the first claim: right away if the ring prologue already needs dynamic tiles, else
+    // after the sample tile (it then completes during the sample-bound wait; 2368 warps
+    // claiming at launch serialised on the counter for ~1.5 us)
+    if (lane == 0 && ndyn > 0 && S0 <= R) nbase = atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim);
     auto next_tile = [&]() -> int64_t {               // all lanes; tile of sequence position seq, -1 = done
         int64_t t = -1;
         if (seq < S0) {
@@ -337,6 +340,12 @@ __global__ void __launch_bounds__(kFT, 1)
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    {   // the LUT first (its own commit group, ahead of the ring in the SM's load queue)
+        const int l16 = (lutsz + 1 + 15) / 16;
+        const int4* src = reinterpret_cast<const int4*>(A.lut_dev);
+        for (int i = tid; i < l16; i += kFT) cp_async16(smem + kFLutOff + 16 * i, src + i);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     for (int i = 0; i < R; i++) issue(i);
     __syncwarp();
     stamp(10);
@@ -369,14 +378,12 @@ __global__ void __launch_bounds__(kFT, 1)
             thr64[q] = 0ull; sec64[q] = 0ull; rcnt[q] = 0;
             for (int m = 0; m < kFBoardMax; m++) bmax[q * kFBoardMax + m] = 0u;
         }
-        if (dbg && tid == 0) A.dbg[cta * 16 + 11] = fgtime();
+        if (dbg && tid == 0) A.dbg[cta * kDbgStride + 11] = fgtime();
         uint4* c4 = (uint4*)cntb;
         const int n16 = (2 * kFT * (nslots + 2)) / 16;
         for (int i = tid; i < n16; i += kFT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
-        if (dbg && tid == 0) A.dbg[cta * 16 + 12] = fgtime();
-        const int l16 = (lutsz + 1 + 15) / 16;
-        const int4* src = reinterpret_cast<const int4*>(A.lut_dev);
-        for (int i = tid; i < l16; i += kFT) ((int4*)lut)[i] = __ldg(src + i);
+        if (dbg && tid == 0) A.dbg[cta * kDbgStride + 12] = fgtime();
+        cp_async_wait_n(R);            // this thread's LUT chunks (the oldest group) have landed
         if (tid == 0) {
             M->flag = 0; M->novf = 0; M->ndone = 0; M->last = 0; M->ncoll = 0; M->pn = 0;
             M->members = 0ull; M->sec = 0ull; M->tcoll = 0ull;
@@ -505,24 +512,29 @@ __global__ void __launch_bounds__(kFT, 1)
         float sp[4];
         int qo[4];
         bool okv[4];
-        bool any = false;
+        unsigned pm = 0u;             // request slots j of this lane that need the rare path
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             // lengths < 0 clamp to lut_size (FAR: the rare path sorts them out); lut[0] = bad
             const int c = (FULL || j < nv) ? (int)lut[min((unsigned)b[j], (unsigned)lutsz)] : kFCodeNone;
             code[j] = c;
+            // member counter row straight from the code (no wait on the record load):
+            // rows 0..nslots-1 members, nslots invalid length, nslots+1 dummy
+            const int crow = c < nslots ? c : (c == kFCodeBad ? nslots : nslots + 1);
+            uint16_t* cp = mycnt + crow * kFT;
+            *cp = (uint16_t)(*cp + 1);
             const float4 w = rec[2 * c];
             const float4 r2 = rec[2 * c + 1];
             const bool ok = score_sp(b[j], a[j], co[j], HAS_COST, A.sp, w.x, w.y, w.z, &sp[j]);
             okv[j] = ok;
             qo[j] = __float_as_int(r2.y);
-            uint16_t* cp = (uint16_t*)((unsigned char*)mycnt + __float_as_int(r2.z));
-            *cp = (uint16_t)(*cp + 1);
             const float f1 = SCORE ? sp[j] : a[j];
             const float f2 = SCORE ? a[j] : sp[j];
             const bool p1 = SCORE ? (f1 >= w.w) : (f1 <= w.w);
             const bool p2 = SCORE ? (f2 <= r2.x) : (f2 >= r2.x);
-            any = any || p1 || p2 || !ok;
+            bool pj = p1 || p2 || !ok;
+            if (SAMPLE) pj = pj && !(c < nslots && ok);    // members of the sample: the sample block
+            pm |= pj ? (1u << j) : 0u;
         }
         if (write_qid) {
             if (FULL) {
@@ -553,18 +565,20 @@ __global__ void __launch_bounds__(kFT, 1)
                 }
             }
         }
-        if (__any_sync(0xffffffffu, any)) {
-            // the rare path, one warp-uniform test per request slot (no dynamic register indexing)
-#pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const float4 w = rec[2 * code[j]];
-                const float4 r2 = rec[2 * code[j] + 1];
-                const float f1 = SCORE ? sp[j] : a[j], f2 = SCORE ? a[j] : sp[j];
-                bool pj = (SCORE ? (f1 >= w.w) : (f1 <= w.w)) || (SCORE ? (f2 <= r2.x) : (f2 >= r2.x)) || !okv[j];
-                if (SAMPLE) pj = pj && !(code[j] < nslots && okv[j]);   // members of the sample: the sample block
-                if (__any_sync(0xffffffffu, pj)) {
-                    if (pj) rare(code[j], b[j], a[j], co[j], sp[j], okv[j], i0 + j);
-                }
+        // the rare path: one inline copy, each lane walks its own flagged slots (the
+        // operands of slot j picked by selects; 4 inlined copies made the loop body too
+        // large for the instruction cache)
+        while (__any_sync(0xffffffffu, pm != 0u)) {
+            if (pm) {
+                const int j = __ffs(pm) - 1;
+                pm &= pm - 1u;
+                const int bj = j == 0 ? b[0] : (j == 1 ? b[1] : (j == 2 ? b[2] : b[3]));
+                const float aj = j == 0 ? a[0] : (j == 1 ? a[1] : (j == 2 ? a[2] : a[3]));
+                const float cj = j == 0 ? co[0] : (j == 1 ? co[1] : (j == 2 ? co[2] : co[3]));
+                const float sj = j == 0 ? sp[0] : (j == 1 ? sp[1] : (j == 2 ? sp[2] : sp[3]));
+                const int dj = j == 0 ? code[0] : (j == 1 ? code[1] : (j == 2 ? code[2] : code[3]));
+                const bool oj = j == 0 ? okv[0] : (j == 1 ? okv[1] : (j == 2 ? okv[2] : okv[3]));
+                rare(dj, bj, aj, cj, sj, oj, i0 + j);
             }
         }
     };
@@ -621,6 +635,7 @@ __global__ void __launch_bounds__(kFT, 1)
 
     // ---- sample tile, board, bound
     tile(std::integral_constant<bool, true>());
+    if (lane == 0 && ndyn > 0 && S0 > R) nbase = atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim);
     __syncthreads();
     stamp(2);
     const int bm = A.board_m;
@@ -649,7 +664,7 @@ __global__ void __launch_bounds__(kFT, 1)
             // (monotone ticket: generation = ticket / G)
             const unsigned tk = atomicAdd(&A.ctr->pub, 1u);
             const unsigned target = (tk / (unsigned)G + 1u) * (unsigned)G;
-            if (dbg) A.dbg[cta * 16 + 13] = fgtime();
+            if (dbg) A.dbg[cta * kDbgStride + 13] = fgtime();
             unsigned v;
             do {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&A.ctr->pub) : "memory");
@@ -661,26 +676,31 @@ __global__ void __launch_bounds__(kFT, 1)
         // queue): the K-th largest high word t of the G*bm published keys, so
         // >= K distinct real requests have keys >= (t << 32) -- a valid bound
         const int nb = G * bm;
-        for (int q = warp; q < nslots; q += 2 * kFW) {
-            const int q1 = q + kFW;
-            u32 v0[kFBoardRegs], v1[kFBoardRegs];
+        auto bounds = [&](auto regs_tag) {
+            constexpr int RR = decltype(regs_tag)::value;
+            for (int q = warp; q < nslots; q += 2 * kFW) {
+                const int q1 = q + kFW;
+                u32 v0[RR], v1[RR];
 #pragma unroll
-            for (int r = 0; r < kFBoardRegs; r++) {
-                const int j = lane + 32 * r;
-                v0[r] = j < nb ? (u32)(__ldcg(A.board + (size_t)q * nb + j) >> 32) : 0u;
-                v1[r] = (j < nb && q1 < nslots) ? (u32)(__ldcg(A.board + (size_t)q1 * nb + j) >> 32) : 0u;
-            }
-            u32 t[2];
-            warp_kth_hi2<kFBoardRegs>(v0, v1, K, t);
-            if (lane == 0) {
-                thr64[q] = (u64)t[0] << 32;
-                if (cta == 0 && t[0]) atomicMax(&A.gthr[q], (u64)t[0] << 32);
-                if (q1 < nslots) {
-                    thr64[q1] = (u64)t[1] << 32;
-                    if (cta == 0 && t[1]) atomicMax(&A.gthr[q1], (u64)t[1] << 32);
+                for (int r = 0; r < RR; r++) {
+                    const int j = lane + 32 * r;
+                    v0[r] = j < nb ? (u32)(__ldcg(A.board + (size_t)q * nb + j) >> 32) : 0u;
+                    v1[r] = (j < nb && q1 < nslots) ? (u32)(__ldcg(A.board + (size_t)q1 * nb + j) >> 32) : 0u;
+                }
+                u32 t[2];
+                warp_kth_hi2<RR>(v0, v1, K, t);
+                if (lane == 0) {
+                    thr64[q] = (u64)t[0] << 32;
+                    if (cta == 0 && t[0]) atomicMax(&A.gthr[q], (u64)t[0] << 32);
+                    if (q1 < nslots) {
+                        thr64[q1] = (u64)t[1] << 32;
+                        if (cta == 0 && t[1]) atomicMax(&A.gthr[q1], (u64)t[1] << 32);
+                    }
                 }
             }
-        }
+        };
+        if (nb <= 160) bounds(std::integral_constant<int, 5>());
+        else bounds(std::integral_constant<int, kFBoardRegs>());
         stamp(14);
         __syncthreads();
     }
@@ -773,6 +793,36 @@ __global__ void __launch_bounds__(kFT, 1)
     __syncthreads();
     stamp(4);
 
+    // ---- per-CTA rows cut to the best bound known now (this CTA's threshold or the
+    // global one, max of the two): the merge then reads a few keys per row instead
+    // of every insert (the dominant queue's merge read ~400 per CTA, ~10 us).
+    for (int q = warp; q < nslots; q += kFW) {
+        const int nr = min(rcnt[q], RC);
+        if (nr == 0) continue;
+        u64 g = __ldcg(&A.gthr[q]);
+        const u64 tl = thr64[q];
+        g = g > tl ? g : tl;
+        u64* row = rows_cta + q * row_stride;
+        int wpos = 0;
+        for (int base = 0; base < nr; base += 32 * 16) {
+            u64 kv[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                const int j = base + u * 32 + lane;
+                kv[u] = j < nr ? __ldcg(row + j) : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                const bool keep = kv[u] != 0ull && kv[u] >= g;
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (keep) row[wpos + __popc(bal & ((1u << lane) - 1u))] = kv[u];
+                wpos += __popc(bal);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) rcnt[q] = wpos;
+    }
+    __syncthreads();
     // ---- per-CTA rows: count (<= RC, no overflow pending), members, secondary
     for (int q = warp; q < nslots; q += kFW) {
         const uint32_t* c32 = (const uint32_t*)(cntb + (size_t)q * kFT * 2);
@@ -806,7 +856,7 @@ __global__ void __launch_bounds__(kFT, 1)
             if (ins) atomicAdd(&A.ctr->dbg_inserted, ins);
         }
         if (tid == 0 && M->ncoll) atomicAdd(&A.ctr->dbg_compactions, (unsigned long long)M->ncoll);
-        if (dbg && tid == 0) { A.dbg[cta * 16 + 8] = (unsigned long long)M->ncoll; A.dbg[cta * 16 + 9] = M->tcoll; }
+        if (dbg && tid == 0) { A.dbg[cta * kDbgStride + 8] = (unsigned long long)M->ncoll; A.dbg[cta * kDbgStride + 9] = M->tcoll; }
     }
     (void)n_gap;
     __threadfence();
@@ -846,103 +896,144 @@ __global__ void __launch_bounds__(kFT, 1)
         // the whole shared memory is free now: [rowoff | pool]
         int* rowoff = (int*)(smem + L.cnt);                  // [G + 1]
         u64* pool = (u64*)(smem + L.ring);
-        const int pcap = (int)((L.cnt - L.ring) / 8);        // ring .. counters (>= 8K keys)
-        constexpr int kChunk = 4096;                          // candidates scanned per round
-        if (tid == 0) { M->pn = 0; M->members = 0ull; M->sec = 0ull; }
-        // row counts, members, secondary (one row per thread)
+        // the candidate pool takes the ring region only (the control block M, hist and
+        // surv that follow it are still in use): >= 2 stages x 2 arrays x 16 warps x 512 B
+        const int pcap = (int)((L.bars - L.ring) / 8);
+        constexpr int kChunk = 2048;                          // candidates scanned per round
+        if (tid == 0) { M->pn = 0; M->members = 0ull; M->sec = 0ull; M->ncoll = 0; M->maxnc = 0; }
+        __syncthreads();
+        // one round trip: 3 threads per row load its count, members and secondary and,
+        // speculatively, its first 24 keys (masked by the count afterwards; the rows
+        // were cut to the end-of-stream bound, so most hold far fewer)
+        const int rrow = tid % G, rpart = tid / G;
+        const bool ract = tid < 3 * G;
+        const size_t rr = (size_t)q * G + rrow;
+        const u64* rk = A.rows.keys + rr * RC;
+        int nc = 0;
+        u64 kv[8];
         {
             unsigned long long mm = 0;
             u64 sk = 0ull;
-            int nc = 0;
-            if (tid < G) {
-                const size_t r = (size_t)q * G + tid;
-                nc = __ldcg(&A.rows.cnt[r]);
-                mm = (unsigned long long)__ldcg(&A.rows.members[r]);
-                sk = __ldcg(&A.rows.sec[r]);
-            }
-            // exclusive prefix of the counts over the G (<= 512) rows
-            int incl = nc;
+            if (ract) {
+                nc = __ldcg(&A.rows.cnt[rr]);
+                if (rpart == 0) { mm = (unsigned long long)__ldcg(&A.rows.members[rr]); sk = __ldcg(&A.rows.sec[rr]); }
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += u;
+                for (int u = 0; u < 8; u++) kv[u] = __ldcg(rk + rpart * 8 + u);
             }
-            unsigned* wsum = hist;                           // per-warp totals
-            if (lane == 31) wsum[warp] = (unsigned)incl;
             for (int o = 16; o; o >>= 1) {
                 mm += __shfl_xor_sync(0xffffffffu, mm, o);
                 const u64 so = shfl_xor_u64(sk, o);
                 sk = so > sk ? so : sk;
             }
-            __syncthreads();
-            int woff = 0;
-            for (int w = 0; w < warp; w++) woff += (int)wsum[w];
-            if (tid < G) rowoff[tid] = woff + incl - nc;
-            if (tid == G - 1) rowoff[G] = woff + incl;
             if (lane == 0) {
                 if (mm) atomicAdd(&M->members, mm);
                 if (sk) atomicMax(&M->sec, sk);
             }
+            if (ract && rpart == 0 && nc) {
+                atomicAdd(&M->ncoll, nc);      // total candidates (ncoll reused)
+                atomicMax(&M->maxnc, nc);
+                rowoff[rrow + 1] = nc;         // counts for the prefix of the chunked path
+            }
+            if (ract && rpart == 0 && !nc) rowoff[rrow + 1] = 0;
         }
         __syncthreads();
-        const int total = rowoff[G];
+        if (dbg && tid == 0) A.dbg[cta * kDbgStride + 20] = fgtime();
+        const int total = M->ncoll;
         int pn = 0;
-        for (int base = 0; base < total; base += kChunk) {
-            // candidates [base, base + kChunk): 8 per thread, loads in flight together
-            u64 kv[kChunk / kFT];
+        if (M->maxnc <= 24) {                  // every row fully loaded already
+            if (ract) {
 #pragma unroll
-            for (int u = 0; u < kChunk / kFT; u++) {
-                const int e = base + tid + kFT * u;
-                kv[u] = 0ull;
-                if (e < total) {
-                    int lo = 0, hi = G;                      // row r: rowoff[r] <= e < rowoff[r + 1]
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (rowoff[mid] <= e) lo = mid; else hi = mid;
-                    }
-                    kv[u] = __ldcg(A.rows.keys + ((size_t)q * G + lo) * RC + (e - rowoff[lo]));
+                for (int u = 0; u < 8; u++) {
+                    const int j = rpart * 8 + u;
+                    if (j < nc && kv[u] && kv[u] >= thr) pool[atomicAdd(&M->pn, 1)] = kv[u];
                 }
             }
-#pragma unroll
-            for (int u = 0; u < kChunk / kFT; u++)
-                if (kv[u] && kv[u] >= thr) {
-                    const int p = atomicAdd(&M->pn, 1);
-                    pool[p] = kv[u];
-                }
             __syncthreads();
             pn = M->pn;
             __syncthreads();
-            if (pn > pcap - kChunk && base + kChunk < total) {
-                // no room for another round: cut the pool to its exact top-K
-                auto fe = [&](auto f) { for (int j = tid; j < pn; j += kFT) f(pool[j]); };
-                const u64 t = block_kth(fe, K, hist, M);
-                const int nk = block_collect(fe, t, surv, EWSJF_MAX_K, M);
-                for (int j = tid; j < nk; j += kFT) pool[j] = surv[j];
-                if (tid == 0) M->pn = nk;
-                thr = t;
+        } else {
+            // long rows: prefix of the counts (already in rowoff[1..G]), then rounds of
+            // kChunk candidates over all threads with cuts to the top K
+            {
+                const int c = tid < G ? rowoff[tid + 1] : 0;
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += u;
+                }
+                if (lane == 31) hist[warp] = (unsigned)incl;
                 __syncthreads();
-                pn = nk;
+                int woff = 0;
+                for (int w = 0; w < warp; w++) woff += (int)hist[w];
+                __syncthreads();
+                if (tid < G) rowoff[tid + 1] = woff + incl;
+                if (tid == 0) rowoff[0] = 0;
+            }
+            __syncthreads();
+            for (int base = 0; base < total; base += kChunk) {
+                u64 kx[kChunk / kFT];
+#pragma unroll
+                for (int u = 0; u < kChunk / kFT; u++) {
+                    const int e = base + tid + kFT * u;
+                    kx[u] = 0ull;
+                    if (e < total) {
+                        int lo = 0, hi = G;                      // row r: rowoff[r] <= e < rowoff[r + 1]
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (rowoff[mid] <= e) lo = mid; else hi = mid;
+                        }
+                        kx[u] = __ldcg(A.rows.keys + ((size_t)q * G + lo) * RC + (e - rowoff[lo]));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kChunk / kFT; u++)
+                    if (kx[u] && kx[u] >= thr) pool[atomicAdd(&M->pn, 1)] = kx[u];
+                __syncthreads();
+                pn = M->pn;
+                __syncthreads();
+                if (pn > pcap - kChunk && base + kChunk < total) {
+                    auto fe = [&](auto f) { for (int j = tid; j < pn; j += kFT) f(pool[j]); };
+                    const u64 t = block_kth(fe, K, hist, M);
+                    const int nk = block_collect(fe, t, surv, EWSJF_MAX_K, M);
+                    for (int j = tid; j < nk; j += kFT) pool[j] = surv[j];
+                    if (tid == 0) M->pn = nk;
+                    thr = t;
+                    __syncthreads();
+                    pn = nk;
+                }
             }
         }
-        {
-            auto fe = [&](auto f) { for (int j = tid; j < pn; j += kFT) f(pool[j]); };
-            u64 t = 0ull;
-            if (pn > K) t = block_kth(fe, K, hist, M);
-            block_collect(fe, t, surv, EWSJF_MAX_K, M);
-        }
-        // surv holds the min(K, #candidates) best keys (any order): rank sort, outputs
+        if (dbg && tid == 0) { A.dbg[cta * kDbgStride + 16] = fgtime(); A.dbg[cta * kDbgStride + 17] = (unsigned long long)pn; }
         const int ns = min(pn, K);
-        u64 myk = 0ull;
-        int myr = -1;
-        if (tid < ns) {
-            myk = surv[tid];
-            int r = 0;
-            for (int j = 0; j < ns; j++) r += surv[j] > myk;
-            myr = r;
+        if (pn <= 128) {
+            // small pool: one counting pass ranks every candidate (keys are unique),
+            // rank < K are the top K already in order -- no radix select, no sort
+            const u64 k0 = tid < pn ? pool[tid] : 0ull;
+            int r0 = 0;
+            if (tid < pn)
+                for (int j = 0; j < pn; j++) r0 += pool[j] > k0;
+            __syncthreads();
+            if (tid < pn && r0 < K) surv[r0] = k0;
+            __syncthreads();
+        } else {
+            auto fe = [&](auto f) { for (int j = tid; j < pn; j += kFT) f(pool[j]); };
+            const u64 t = block_kth(fe, K, hist, M);
+            block_collect(fe, t, surv, EWSJF_MAX_K, M);
+            // surv holds the K best keys (any order): rank sort
+            u64 myk = 0ull;
+            int myr = -1;
+            if (tid < ns) {
+                myk = surv[tid];
+                int r = 0;
+                for (int j = 0; j < ns; j++) r += surv[j] > myk;
+                myr = r;
+            }
+            __syncthreads();
+            if (tid < ns) surv[myr] = myk;
+            __syncthreads();
         }
-        __syncthreads();
-        if (tid < ns) surv[myr] = myk;
-        __syncthreads();
+        if (dbg && tid == 0) A.dbg[cta * kDbgStride + 18] = fgtime();
         const float qi = (float)(q + 1);
         const float wb = P.wb[q], wu = P.wu[q], wf = P.wf[q];
         auto payload = [&](u64 k) -> float {   // s' of the request with key k
@@ -984,6 +1075,7 @@ __global__ void __launch_bounds__(kFT, 1)
             }
             A.gthr[q] = 0ull;
         }
+        if (dbg && tid == 0) A.dbg[cta * kDbgStride + 19] = fgtime();
     }
     stamp(7);
     // ---- last CTA: Alg. 1 ArgMax (ties -> lowest position, R24), summary, counter reset

@@ -17,18 +17,17 @@ namespace ewsjf {
         if (A.dbg && threadIdx.x == 0) {                                                           \
             unsigned long long t_;                                                                 \
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                  \
-            atomicMax(&A.dbg[blockIdx.x * 16 + (slot_)], t_);                                        \
+            atomicMax(&A.dbg[blockIdx.x * kDbgStride + (slot_)], t_);                                        \
         }                                                                                          \
     } while (0)
 __host__ __device__ inline int64_t al16m(int64_t x) { return (x + 15) & ~(int64_t)15; }
 
 // ------------------------------------------------------------------ merge ---
 constexpr int kMThreads = 512;
-constexpr int kGapSort = 8192;        // gap entries handled by Alg. 2 per call
 constexpr int kRankMax = 512;         // survivors rank-sorted at the end
 
 struct MergeSmem {
-    int64_t uni, psp, gslot, mygap, myslot, tables, rowoff, surv, ssp, misc, total;
+    int64_t uni, psp, tables, rowoff, surv, ssp, misc, total;
     int esmem;
 };
 __host__ __device__ inline MergeSmem merge_layout(int in_mode) {
@@ -38,9 +37,6 @@ __host__ __device__ inline MergeSmem merge_layout(int in_mode) {
     int64_t o = 0;
     L.uni = o;    o += uni_bytes;
     L.psp = in_mode == MERGE_IN_ROWS ? 0 : 8 * (int64_t)L.esmem;   // payloads after the keys (exchange)
-    L.gslot = o;  o = al16m(o + 2 * kGapSort);
-    L.mygap = o;  o = al16m(o + 4 * kGapSort);
-    L.myslot = o; o = al16m(o + 2 * kGapSort);
     L.tables = o; o = al16m(o + 4 * 6 * kMaxSlots);
     L.rowoff = o; o = al16m(o + 4 * 1025);
     L.surv = o;   o = al16m(o + 8 * kRankMax);
@@ -57,6 +53,9 @@ struct MMisc {
     int cnt[3];
     int nfinal, nbub, ndrop, nmine, pn, nsurv, is_last, gexc;
     float sec_sp;
+    unsigned cmin;      // Alg. 2 epoch: lowest creator gid
+    int vcre;           // ... its gap-list index
+    int nkeep;          // ... requests classified again next epoch
 };
 
 // A7 for a bubble (device side, same canonical fp64 expression as the host).
@@ -128,9 +127,6 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
     const int tid = threadIdx.x, lane = tid & 31;
     u64* uni = (u64*)(smem + L.uni);
     float* psp = IN == MERGE_IN_EXCHANGE ? (float*)(smem + L.uni + L.psp) : nullptr;
-    int16_t* gslot = (int16_t*)(smem + L.gslot);
-    uint32_t* mygap = (uint32_t*)(smem + L.mygap);
-    int16_t* myslot = (int16_t*)(smem + L.myslot);
     int* t_lo = (int*)(smem + L.tables);
     int* t_hi = t_lo + kMaxSlots;
     int* t_slot = t_hi + kMaxSlots;   // position -> internal slot
@@ -145,7 +141,8 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
     const ExLayout X = ex_layout(nq, K);
     const bool is_score = A.sp.mode == EWSJF_SELECT_SCORE;
 
-    // ---------------- gap list size
+    // ---------------- gap list size (virtual index v = position in the concatenation
+    // of the gap lists: the single list, or rank 0's entries then rank 1's ...)
     long long graw = 0, gcount = 0;
     if (IN == MERGE_IN_ROWS) {
         graw = (long long)__ldcg(&A.ctr->gap_count);
@@ -157,14 +154,31 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             gcount += c < kExGap ? c : kExGap;
         }
     }
-    if (gcount > kGapSort) gcount = kGapSort;
+    if (gcount > A.gap_cap) gcount = A.gap_cap;
     const bool gap_overflow = graw > gcount;
-    auto gap_entry = [&](uint32_t src) -> GapEntry {
-        if (IN == MERGE_IN_ROWS) return A.gap[src];
-        return ((const GapEntry*)(A.ex_in + (int64_t)(src / kExGap) * A.ex_bytes + X.gaps))[src % kExGap];
+    auto gap_entry = [&](uint32_t v) -> GapEntry {
+        if (IN == MERGE_IN_ROWS) return A.gap[v];
+        long long acc = 0;
+        int r = 0;
+        for (; r < A.world; r++) {
+            long long c = ((const ExHeader*)(A.ex_in + (int64_t)r * A.ex_bytes))->gap_count;
+            c = c < kExGap ? c : kExGap;
+            if ((long long)v < acc + c) break;
+            acc += c;
+        }
+        return ((const GapEntry*)(A.ex_in + (int64_t)r * A.ex_bytes + X.gaps))[v - acc];
     };
 
-    // ---------------- final partition: Alg. 2 over the gap list in global index order (R22)
+    // ---------------- final partition: App. D Alg. 2 over the gap requests in global
+    // index order (R22), epoch-parallel and exact.  Requests in index order see the
+    // partition unchanged until the first one that creates a bubble; so in each
+    // epoch every unresolved request is classified against the current table in
+    // parallel (inside a queue / tolerated by a neighbour, R19 / would create a
+    // bubble), the lowest-index creator c inserts its bubble (R20), every request
+    // before c is final, and after c only those in c's gap and the other pending
+    // creators are classified again (a bubble changes nothing outside its gap; a
+    // request inside a queue stays there).  At most 256 - nq epochs.  CTA 0 runs it
+    // and publishes the table; the other CTAs wait for it.
     for (int i = tid; i < nq; i += kMThreads) {
         t_lo[i] = P.min_len[i]; t_hi[i] = P.max_len[i];
         t_slot[i] = i; t_pos[i] = i; t_id[i] = P.sid[i];
@@ -172,45 +186,23 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
     if (tid == 0) { M->nfinal = nq; M->nbub = 0; M->ndrop = 0; M->nmine = 0; M->gexc = 0; }
     __syncthreads();
     const bool do_gaps = gcount > 0 && OUT != MERGE_OUT_EXCHANGE;
-    if (do_gaps) {
-        int np2 = 1;
-        while (np2 < gcount) np2 <<= 1;
-        for (int i = tid; i < np2; i += kMThreads) {
-            u64 k = ~0ull;
-            if (i < gcount) {
-                uint32_t src = (uint32_t)i;
-                if (IN == MERGE_IN_EXCHANGE) {
-                    long long acc = 0;
-                    int r = 0;
-                    for (; r < A.world; r++) {
-                        long long c = ((const ExHeader*)(A.ex_in + (int64_t)r * A.ex_bytes))->gap_count;
-                        c = c < kExGap ? c : kExGap;
-                        if (i < acc + c) break;
-                        acc += c;
-                    }
-                    src = (uint32_t)(r * kExGap + (i - acc));
-                }
-                k = ((u64)gap_entry(src).gid << 32) | src;
-            }
-            uni[i] = k;
-        }
-        __syncthreads();
-        for (int k2 = 2; k2 <= np2; k2 <<= 1) {           // bitonic sort, ascending
-            for (int j = k2 >> 1; j > 0; j >>= 1) {
-                for (int i = tid; i < np2; i += kMThreads) {
-                    const int ixj = i ^ j;
-                    if (ixj > i) {
-                        const u64 a = uni[i], b = uni[ixj];
-                        if ((a > b) == ((i & k2) == 0)) { uni[i] = b; uni[ixj] = a; }
-                    }
-                }
-                __syncthreads();
-            }
-        }
-        if (tid == 0) {   // Alg. 2 with the integer tests of R19/R20
-            int n = nq, nb = 0, nd = 0;
-            for (int e = 0; e < gcount; e++) {
-                const GapEntry g = gap_entry((uint32_t)(uni[e] & 0xffffffffu));
+    if (do_gaps && blockIdx.x == 0) {
+        unsigned* cmin_s = (unsigned*)&M->cmin;
+        int n = nq, nb = 0, nd = 0;
+        long long nu = gcount;
+        bool first = true;
+        int32_t* ucur = A.g_u0;
+        int32_t* unext = A.g_u1;
+        // classification word: slot (10 bits, 1023 = drop) | class << 10 | gap << 12
+        constexpr int kClsIn = 0, kClsTol = 1, kClsNew = 2, kClsDrop = 3;
+        unsigned* mincre = (unsigned*)uni;       // [gap index 0..n]: lowest creator gid in that gap (uni is free here)
+        for (;;) {
+            if (tid == 0) { *cmin_s = 0xffffffffu; M->nkeep = 0; }
+            for (int i = tid; i <= n; i += kMThreads) mincre[i] = 0xffffffffu;
+            __syncthreads();
+            for (long long idx = tid; idx < nu; idx += kMThreads) {
+                const uint32_t v = first ? (uint32_t)idx : (uint32_t)ucur[idx];
+                const GapEntry g = gap_entry(v);
                 const int Lq = g.len;
                 int lo = 0, hi = n;
                 while (lo < hi) {
@@ -218,71 +210,148 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
                     if (t_lo[mid] <= Lq) lo = mid + 1; else hi = mid;
                 }
                 const int i = lo - 1;
-                int as;
+                int cls, slot = 1023;
                 if (i >= 0 && Lq < t_hi[i]) {
-                    as = t_slot[i];
+                    cls = kClsIn; slot = t_slot[i];
                 } else {
                     const bool hl = i >= 0, hr = i + 1 < n;
                     const long long L64 = Lq;
-                    if (hl && 10 * L64 <= 11 * (long long)t_hi[i]) {
-                        as = t_slot[i];
-                    } else if (hr && 10 * L64 >= 9 * (long long)t_lo[i + 1]) {
-                        as = t_slot[i + 1];
-                    } else if (n >= kMaxSlots) {
-                        as = -1;
-                        nd++;
-                    } else {
-                        const long long lb = hl ? t_hi[i] : 1;
-                        const long long rb = hr ? t_lo[i + 1] : (1ll << 40);
-                        const long long avail = rb - lb;
-                        const long long rg = (long long)A.bubble_width < avail ? (long long)A.bubble_width : avail;
-                        long long nlo = L64 - rg / 2;
-                        if (nlo < lb) nlo = lb;
-                        long long nhi = L64 + (rg + 1) / 2;
-                        if (nhi > rb) nhi = rb;
-                        if (nhi > INT_MAX) nhi = INT_MAX;
-                        for (int p = n; p > i + 1; p--) {
-                            t_lo[p] = t_lo[p - 1]; t_hi[p] = t_hi[p - 1]; t_slot[p] = t_slot[p - 1];
-                        }
-                        const int ns = nq + nb;
-                        t_lo[i + 1] = (int)nlo; t_hi[i + 1] = (int)nhi; t_slot[i + 1] = ns;
-                        t_L[ns] = Lq;
-                        t_id[ns] = A.next_id + nb;
-                        if (A.blog && blockIdx.x == 0) {
-                            A.blog->pos[nb] = i + 1; A.blog->lo[nb] = (int)nlo;
-                            A.blog->hi[nb] = (int)nhi; A.blog->L[nb] = Lq;
-                        }
-                        n++; nb++;
-                        as = ns;
-                    }
+                    if (hl && 10 * L64 <= 11 * (long long)t_hi[i]) { cls = kClsTol; slot = t_slot[i]; }
+                    else if (hr && 10 * L64 >= 9 * (long long)t_lo[i + 1]) { cls = kClsTol; slot = t_slot[i + 1]; }
+                    else if (n >= kMaxSlots) cls = kClsDrop;
+                    else { cls = kClsNew; atomicMin(cmin_s, g.gid); atomicMin(&mincre[i + 1], g.gid); }
                 }
-                gslot[e] = (int16_t)as;
+                A.g_res[v] = slot | (cls << 10) | ((i + 1) << 12);
             }
-            M->nfinal = n; M->nbub = nb; M->ndrop = nd;
+            __syncthreads();
+            const unsigned cmin = *cmin_s;
+            if (cmin == 0xffffffffu) {            // no creator left: every pending request is final
+                for (long long idx = tid; idx < nu; idx += kMThreads) {
+                    const uint32_t v = first ? (uint32_t)idx : (uint32_t)ucur[idx];
+                    const int r = A.g_res[v];
+                    const int slot = r & 1023;
+                    A.g_slot[v] = slot == 1023 ? -1 : slot;
+                    if (slot == 1023) atomicAdd(&M->ndrop, 1);
+                }
+                __syncthreads();
+                break;
+            }
+            // the creator (unique gid) inserts its bubble
+            for (long long idx = tid; idx < nu; idx += kMThreads) {
+                const uint32_t v = first ? (uint32_t)idx : (uint32_t)ucur[idx];
+                if (((A.g_res[v] >> 10) & 3) == kClsNew && gap_entry(v).gid == cmin) M->vcre = (int)v;
+            }
+            __syncthreads();
+            const int vc = M->vcre;
+            const int cgap = A.g_res[vc] >> 12;       // gap index: between positions cgap-1 and cgap
+            if (tid == 0) {
+                const int i = cgap - 1;
+                const int Lq = gap_entry((uint32_t)vc).len;
+                const bool hl = i >= 0, hr = i + 1 < n;
+                const long long L64 = Lq;
+                const long long lb = hl ? t_hi[i] : 1;
+                const long long rb = hr ? t_lo[i + 1] : (1ll << 40);
+                const long long avail = rb - lb;
+                const long long rg = (long long)A.bubble_width < avail ? (long long)A.bubble_width : avail;
+                long long nlo = L64 - rg / 2;
+                if (nlo < lb) nlo = lb;
+                long long nhi = L64 + (rg + 1) / 2;
+                if (nhi > rb) nhi = rb;
+                if (nhi > INT_MAX) nhi = INT_MAX;
+                for (int p = n; p > i + 1; p--) {
+                    t_lo[p] = t_lo[p - 1]; t_hi[p] = t_hi[p - 1]; t_slot[p] = t_slot[p - 1];
+                }
+                const int ns = nq + nb;
+                t_lo[i + 1] = (int)nlo; t_hi[i + 1] = (int)nhi; t_slot[i + 1] = ns;
+                t_L[ns] = Lq;
+                t_id[ns] = A.next_id + nb;
+                if (A.blog) {
+                    A.blog->pos[nb] = i + 1; A.blog->lo[nb] = (int)nlo;
+                    A.blog->hi[nb] = (int)nhi; A.blog->L[nb] = Lq;
+                }
+                A.g_slot[vc] = ns;
+                M->nfinal = n + 1;
+            }
+            __syncthreads();
+            const int ns = nq + nb;
+            n++; nb++;
+            // settle: a request before c is final; after c, one inside a queue is final,
+            // a creator goes again, and a tolerated one goes again only if some creator
+            // precedes it in its own gap (that bubble may become its neighbour)
+            for (long long idx = tid; idx < nu; idx += kMThreads) {
+                const uint32_t v = first ? (uint32_t)idx : (uint32_t)ucur[idx];
+                if ((int)v == vc) continue;
+                const int r = A.g_res[v];
+                const int cls = (r >> 10) & 3, slot = r & 1023, gp = r >> 12;
+                const unsigned gid = gap_entry(v).gid;
+                bool keep;
+                if (cls == kClsIn || cls == kClsDrop || gid < cmin) keep = false;
+                else keep = cls == kClsNew || gid > mincre[gp];
+                if (keep) {
+                    unext[atomicAdd(&M->nkeep, 1)] = (int32_t)v;
+                } else {
+                    A.g_slot[v] = slot == 1023 ? -1 : slot;
+                    if (slot == 1023) atomicAdd(&M->ndrop, 1);
+                }
+            }
+            __syncthreads();
+            nu = M->nkeep;
+            first = false;
+            int32_t* t = ucur; ucur = unext; unext = t;
+            (void)ns;
+            if (nu == 0) break;
+            __syncthreads();
+        }
+        nd = M->ndrop;
+        if (tid == 0) {
+            M->nfinal = n; M->nbub = nb;
+            A.g_tab[0] = n; A.g_tab[1] = nb; A.g_tab[2] = nd;
         }
         __syncthreads();
-        for (int p = tid; p < M->nfinal; p += kMThreads) t_pos[t_slot[p]] = p;
-        if (blockIdx.x == 0 && A.qid) {   // qid write-back of this rank's gap requests
-            for (int e = tid; e < gcount; e += kMThreads) {
-                const GapEntry g = gap_entry((uint32_t)(uni[e] & 0xffffffffu));
+        for (int i = tid; i < n; i += kMThreads) {
+            A.g_tab[3 + i] = t_lo[i]; A.g_tab[3 + kMaxSlots + i] = t_hi[i]; A.g_tab[3 + 2 * kMaxSlots + i] = t_slot[i];
+        }
+        for (int i = tid; i < nq + nb; i += kMThreads) {
+            A.g_tab[3 + 3 * kMaxSlots + i] = t_L[i]; A.g_tab[3 + 4 * kMaxSlots + i] = t_id[i];
+        }
+        // qid write-back of this rank's gap requests (stable ids)
+        if (A.qid) {
+            for (long long e = tid; e < gcount; e += kMThreads) {
+                const GapEntry g = gap_entry((uint32_t)e);
                 const long long li = (long long)g.gid - (long long)A.gbase;
-                if (li >= 0 && li < A.n_local) { const int as = gslot[e]; A.qid[li] = as >= 0 ? t_id[as] : -1; }
+                if (li >= 0 && li < A.n_local) { const int as = A.g_slot[e]; A.qid[li] = as >= 0 ? t_id[as] : -1; }
             }
         }
-        // keep the gap requests of the slots this CTA will merge (uni is reused below)
-        for (int e = tid; e < gcount; e += kMThreads) {
-            const int as = gslot[e];
-            if (as >= 0 && as % (int)gridDim.x == (int)blockIdx.x) {
-                const int p = atomicAdd(&M->nmine, 1);
-                mygap[p] = (uint32_t)(uni[e] & 0xffffffffu);
-                myslot[p] = (int16_t)as;
-            }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&A.ctr->gap_done), "r"(A.seq) : "memory");
+    } else if (do_gaps) {
+        if (tid == 0) {
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&A.ctr->gap_done) : "memory");
+                if (v != A.seq) __nanosleep(200);
+            } while (v != A.seq);
         }
+        __syncthreads();
+        const int n = __ldcg(&A.g_tab[0]), nb = __ldcg(&A.g_tab[1]);
+        for (int i = tid; i < n; i += kMThreads) {
+            t_lo[i] = __ldcg(&A.g_tab[3 + i]); t_hi[i] = __ldcg(&A.g_tab[3 + kMaxSlots + i]);
+            t_slot[i] = __ldcg(&A.g_tab[3 + 2 * kMaxSlots + i]);
+        }
+        for (int i = tid; i < nq + nb; i += kMThreads) {
+            t_L[i] = __ldcg(&A.g_tab[3 + 3 * kMaxSlots + i]); t_id[i] = __ldcg(&A.g_tab[3 + 4 * kMaxSlots + i]);
+        }
+        if (tid == 0) { M->nfinal = n; M->nbub = nb; M->ndrop = __ldcg(&A.g_tab[2]); }
+        __syncthreads();
+    }
+    if (do_gaps) {
+        for (int p = tid; p < M->nfinal; p += kMThreads) t_pos[t_slot[p]] = p;
         __syncthreads();
     }
     if (blockIdx.x == 0 && A.blog && tid == 0) A.blog->n = M->nbub;
     const int nfinal = M->nfinal;
-    const int nmine_all = M->nmine;
+    const long long ngap_all = do_gaps ? gcount : 0;   // every gap entry is checked against the slot
     const int nloop = OUT == MERGE_OUT_ROUTE ? 0 : (OUT == MERGE_OUT_EXCHANGE ? nq : nfinal);
 
     for (int s = blockIdx.x; s < nloop; s += gridDim.x) {
@@ -356,11 +425,11 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
                     if (k > sk) { sk = k; ssk = kp; }
                 }
             }
-            for (int e = tid; e < nmine_all; e += kMThreads) {
-                if (myslot[e] != s) continue;
+            for (long long e = tid; e < ngap_all; e += kMThreads) {
+                if (__ldcg(&A.g_slot[e]) != s) continue;
                 u64 k1, k2;
                 float sp;
-                if (gap_keys(gap_entry(mygap[e]), k1, k2, sp)) {
+                if (gap_keys(gap_entry((uint32_t)e), k1, k2, sp)) {
                     m++;
                     if (k2 > sk) { sk = k2; ssk = sp; }
                 } else {
@@ -388,8 +457,8 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         u64 thr = (IN == MERGE_IN_ROWS && s < nq) ? __ldcg(&A.gthr[s]) : 0ull;
         int pn = 0;
         const int total_rows = rowoff[nrows];
-        const int total = total_rows + nmine_all;
-        int e0 = 0;
+        const long long total = total_rows + ngap_all;
+        long long e0 = 0;
         // fast path (rows input, <= 2 keys per lane per row, <= 12 rows per warp): every
         // warp loads all keys of its rows in one go (independent loads in flight), then
         // filters them into the pool; the general loop below then handles only the
@@ -425,7 +494,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
                 pool_shrink(uni, psp, pn, thr, K, surv, ssp, M);
                 continue;
             }
-            const int take = min(total - e0, space);
+            const int take = (int)(total - e0 < (long long)space ? total - e0 : (long long)space);
             if (tid == 0) M->pn = pn;
             __syncthreads();
             // kU elements per thread per step: their row lookups and loads are issued
@@ -438,7 +507,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
 #pragma unroll
                 for (int u = 0; u < kU; u++) {
                     const int i = i0 + u * kMThreads;
-                    const int e = e0 + i;
+                    const long long e = e0 + i;
                     key[u] = 0ull; sp[u] = 0.f; ok[u] = false;
                     if (i < take && e < total_rows) {
                         int lo = 0, hi = nrows;       // row r with rowoff[r] <= e < rowoff[r+1]
@@ -446,7 +515,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
                             const int mid = (lo + hi) >> 1;
                             if (rowoff[mid] <= e) lo = mid; else hi = mid;
                         }
-                        const int j = e - rowoff[lo];
+                        const int j = (int)(e - rowoff[lo]);
                         if (IN == MERGE_IN_ROWS) {
                             key[u] = __ldcg(&A.rows.keys[((size_t)s * A.rows.G + lo) * A.rows.cap + j]);
                         } else {
@@ -460,10 +529,10 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
 #pragma unroll
                 for (int u = 0; u < kU; u++) {
                     const int i = i0 + u * kMThreads;
-                    const int e = e0 + i;
-                    if (i < take && e >= total_rows && myslot[e - total_rows] == s) {
+                    const long long e = e0 + i;
+                    if (i < take && e >= total_rows && __ldcg(&A.g_slot[e - total_rows]) == s) {
                         u64 k2;
-                        ok[u] = gap_keys(gap_entry(mygap[e - total_rows]), key[u], k2, sp[u]);
+                        ok[u] = gap_keys(gap_entry((uint32_t)(e - total_rows)), key[u], k2, sp[u]);
                     }
                     if (ok[u] && key[u] >= thr) {
                         const int p = atomicAdd(&M->pn, 1);

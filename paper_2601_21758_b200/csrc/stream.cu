@@ -89,7 +89,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 // phase timestamps (EWSJF_PHASES diagnostics): slot s of this CTA's row
 __device__ __forceinline__ void dbg_max(const PartialArgs& A, int s, unsigned long long v) {
-    if (A.dbg) atomicMax(&A.dbg[blockIdx.x * 16 + s], v);
+    if (A.dbg) atomicMax(&A.dbg[blockIdx.x * kDbgStride + s], v);
 }
 
 // cp.async (LDGSTS) of 16 bytes global -> shared, L2 only; groups per thread.
@@ -299,7 +299,7 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
         tma_load_1d(stage(st, 1), A.arrival + off, kWT * 4, &bars[st]);
         if (HAS_COST) tma_load_1d(stage(st, 2), A.cost + off, kWT * 4, &bars[st]);
     };
-    if (tid == 0 && A.dbg) { for (int s = 0; s < 16; s++) A.dbg[blockIdx.x * 16 + s] = 0ull; dbg_max(A, 0, gtime()); }
+    if (tid == 0 && A.dbg) { for (int s = 0; s < kDbgStride; s++) A.dbg[blockIdx.x * kDbgStride + s] = 0ull; dbg_max(A, 0, gtime()); }
     if (lane_ring) {
         if (A.pass0 != 4)
             for (int s = 0; s < S; s++) issue_lane(gw + s * GW, s);
@@ -488,8 +488,8 @@ __device__ __forceinline__ void stream_phase(const PartialArgs& A, const Policy&
         if (tid == 0) { M->novf = 0; M->flag = 0; }
         named_sync(1, kSThreads);
         if (A.dbg && tid == 0) {
-            atomicAdd(&A.dbg[blockIdx.x * 16 + 5], 1ull);
-            atomicAdd(&A.dbg[blockIdx.x * 16 + 6], gtime() - tc0);
+            atomicAdd(&A.dbg[blockIdx.x * kDbgStride + 5], 1ull);
+            atomicAdd(&A.dbg[blockIdx.x * kDbgStride + 6], gtime() - tc0);
         }
     };
 

@@ -53,6 +53,8 @@ struct SweepScratch {
     u64* rows = nullptr;            // [task][kSwT][K]
     int32_t* rowcnt = nullptr;      // [task][kSwT]
     float* w = nullptr;             // [kSwBatch][256][3] weights by position (device, A7)
+    size_t attr_smem = 0;           // select kernel: dynamic smem attribute set for this ctx's device
+    int occ = 1;
 };
 
 struct SweepArgs {
@@ -515,7 +517,7 @@ bool sweep_diag(ewsjf_ctx* ctx, unsigned long long* ci) {
 
 // Scratch for a snapshot of n requests at depth K (grown on demand, kept by the
 // ctx: repeated sweeps of the same size allocate nothing).
-static ewsjf_status sweep_alloc(ewsjf_ctx* ctx, int64_t n, int64_t tasks, int K) {
+ewsjf_status sweep_alloc(ewsjf_ctx* ctx, int64_t n, int64_t tasks, int K) {
     SweepScratch* S = ctx->sw;
     if (!S) {
         S = ctx->sw = new SweepScratch();
@@ -595,9 +597,11 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
     const int chunk = (int)std::max<int64_t>(4096, (n + 3999) / 4000);
     const int64_t max_chunks = n / chunk + nq + 1;
     const int64_t tasks = (int64_t)((kSwBatch + kSwT - 1) / kSwT) * max_chunks;
-    ewsjf_status s = sweep_alloc(ctx, n, tasks, K);
-    if (s != EWSJF_OK) return s;
+    // scratch is reserved up front (ewsjf_ctx_reserve_sweep): no allocation on this call
     SweepScratch* S = ctx->sw;
+    if (!S || S->n_cap < n || S->task_cap < tasks * kSwT * (int64_t)(kSwMaxK + 32))
+        return fail(ctx, EWSJF_ERR_CAPACITY, "sweep: snapshot of %lld requests exceeds the ctx reservation "
+                    "(ewsjf_ctx_reserve_sweep)", (long long)n);
 
     static thread_local SweepArgs A;
     memset(&A, 0, sizeof A);
@@ -638,12 +642,10 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
     const size_t sel_smem = (size_t)kSwWarps * kSwT * (A.cap * 8 + 16 + 8 + 4 + 4);
     const size_t mrg_smem = (size_t)kSwWarps * A.cap * 8;
     // kernel attributes and occupancy are queried once per shared-memory size (host calls)
-    static thread_local size_t s_attr_smem = 0;
-    static thread_local int s_occ = 1;
-    if (s_attr_smem != sel_smem) {
+    if (S->attr_smem != sel_smem) {   // per ctx (its device), not per host thread
         CU(cudaFuncSetAttribute(sweep_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s_occ, sweep_select_kernel, kSwWarps * 32, sel_smem);
-        s_attr_smem = sel_smem;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&S->occ, sweep_select_kernel, kSwWarps * 32, sel_smem);
+        S->attr_smem = sel_smem;
     }
     static thread_local SweepOutArgs O;
     for (int32_t b0 = 0; b0 < n_theta; b0 += kSwBatch) {
@@ -659,7 +661,7 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
             LaunchScope ls(ctx, KIND_SWEEP);
             sweep_weights_kernel<<<1, 256, 0, st>>>(A);
         }
-        const int occ = s_occ;
+        const int occ = S->occ;
         for (int ph = 0; ph < 2; ph++) {
             A.phase = ph;
             CU(cudaMemsetAsync(S->task_ctr, 0, 4, st));
@@ -682,4 +684,17 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
         CU(cudaGetLastError());
     }
     return EWSJF_OK;
+}
+
+// Reserve the sweep's scratch for snapshots of up to max_n requests (records,
+// per-task candidate rows; sizes as the call computes them for nq <= 256).
+extern "C" ewsjf_status ewsjf_ctx_reserve_sweep(ewsjf_ctx* ctx, int64_t max_n) {
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    if (max_n < 0 || max_n >= 0xffffffffll) return fail(ctx, EWSJF_ERR_INVALID_ARG, "reserve_sweep: bad size");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaStreamSynchronize(ctx->stream));
+    const int chunk = (int)std::max<int64_t>(4096, (max_n + 3999) / 4000);
+    const int64_t max_chunks = max_n / chunk + kMaxSlots + 1;
+    const int64_t tasks = (int64_t)((kSwBatch + kSwT - 1) / kSwT) * max_chunks;
+    return sweep_alloc(ctx, max_n, tasks, kSwMaxK);
 }

@@ -21,6 +21,8 @@ struct Rows {
     int32_t G, cap;
 };
 
+constexpr int kDbgStride = 32;   // EWSJF_PHASES: per-CTA timestamp slots
+
 struct Counters {        // device-global, zeroed by the merge for the next call
     unsigned long long n_invalid;
     unsigned long long n_excluded;
@@ -36,6 +38,8 @@ struct Counters {        // device-global, zeroed by the merge for the next call
     unsigned int done;      // CTAs past the streaming phase (grid barrier)
     unsigned int pad0;
     unsigned long long ftiles;   // ftick.cu: dynamic tile claims (reset after the grid barrier)
+    unsigned int gap_done;       // merge.cuh: launch sequence whose Alg. 2 table is published
+    unsigned int pad1;
 };
 
 // Fused streaming tick (ftick.cu): route + score + filter + rows, sample bound,
@@ -167,6 +171,15 @@ struct MergeArgs {
     const GapEntry* gap;        // single gap list
     Counters* ctr;
     int32_t gap_cap;
+    // epoch-parallel Alg. 2 (merge.cuh): per gap entry its final internal slot, a
+    // classification scratch and two ping-pong lists of unresolved entries
+    // [gap capacity each]; the final queue table; launch sequence of this merge
+    int32_t* g_slot;
+    int32_t* g_res;
+    int32_t* g_u0;
+    int32_t* g_u1;
+    int32_t* g_tab;             // [0] n, [1] nb, [2] nd, then lo/hi/slot/L/id [256] each
+    uint32_t seq;
     // --- exchange input (in_mode EXCHANGE)
     const unsigned char* ex_in; // world records
     int32_t world;

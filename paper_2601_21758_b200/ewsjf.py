@@ -17,7 +17,7 @@ __all__ = [
     "EwsjfError", "Context", "make_partition", "meta", "select_params", "partition_params", "weights_from_meta",
     "Outputs", "tick", "tick_host", "score_select", "route", "partition", "score_select_sweep",
     "exchange_bytes", "tick_local", "tick_merge", "tick_sharded", "batch_build", "prune_empty",
-    "history_hist", "partition_from_hist", "reduce_hist", "check_reduced", "partition_sharded", "online_adjust",
+    "alloc_count", "history_hist", "partition_from_hist", "reduce_hist", "check_reduced", "partition_sharded", "online_adjust",
 ]
 
 
@@ -36,7 +36,8 @@ def _ptr(t) -> int | None:
 class Context:
     """Owns an ``ewsjf_ctx`` (all scratch preallocated for max_pool / max_history / max_k)."""
 
-    def __init__(self, device: int = 0, max_pool: int = 0, max_history: int = 0, max_k: int = 64):
+    def __init__(self, device: int = 0, max_pool: int = 0, max_history: int = 0, max_k: int = 64,
+                 max_sweep: int = 0):
         self.lib = L.load()
         self.device = device
         self.max_k = max_k
@@ -48,6 +49,8 @@ class Context:
         if s != L.OK:
             raise EwsjfError(s, "ewsjf_ctx_create failed")
         self.h = h
+        if max_sweep > 0:      # Θ-sweep scratch reserved up front (the sweep call never allocates)
+            self.check(self.lib.ewsjf_ctx_reserve_sweep(h, max_sweep), (L.OK,))
 
     @property
     def num_ctas(self) -> int:
@@ -68,10 +71,10 @@ class Context:
     def phases(self):
         """Per-CTA phase timestamps of the last streaming tick (EWSJF_PHASES), shape [ctas, 16]."""
         import numpy as np
-        n = self.num_ctas * 16
+        n = self.num_ctas * 32
         buf = (C.c_uint64 * n)()
         self.check(self.lib.ewsjf_ctx_get_phases(self.h, buf, n))
-        return np.frombuffer(buf, dtype=np.uint64).reshape(self.num_ctas, 16).copy()
+        return np.frombuffer(buf, dtype=np.uint64).reshape(self.num_ctas, 32).copy()
 
     def init_nccl(self, rank: int = 0, world: int = 1, group=None):
         """Give the ctx its own NCCL communicator (ewsjf_ctx_init_nccl): rank 0 creates
@@ -149,6 +152,11 @@ def partition_params(alpha=2.0, min_width=1, max_queues=32, epsilon=1e-6, coarse
                      gap_rule=0, kmeans_k=0):
     """kmeans_k > 0 selects the k-means-only partition (Table 3 "EWSJF (K-Means)")."""
     return L.PartitionParams(alpha, min_width, max_queues, epsilon, coarse_k, merge_rule, gap_rule, kmeans_k)
+
+
+def alloc_count() -> int:
+    """Process-wide count of the library's device/pinned allocations and frees."""
+    return int(L.load().ewsjf_alloc_count())
 
 
 def weights_from_meta(theta: L.Meta, part: L.Partition):

@@ -18,3 +18,15 @@ def orc():
     import oracle
     oracle.build()
     return oracle
+
+
+def pytest_terminal_summary(terminalreporter):
+    try:
+        from tests.parity import SESSION, NEAR_TIE_BOUND
+    except Exception:  # noqa: BLE001
+        return
+    if SESSION["calls"]:
+        terminalreporter.write_line(
+            f"parity: {SESSION['calls']} selections, {SESSION['queues']} queues compared, "
+            f"{SESSION['near_ties']} near-tie id swaps in total (max {SESSION['max_per_call']} per selection, "
+            f"bound {NEAR_TIE_BOUND})")

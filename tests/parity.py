@@ -41,6 +41,15 @@ class Report:
         self.checked_queues = 0
 
 
+# Session totals (near-tie counts are reported, not silently
+# tolerated): every compare_selection adds to these; conftest prints them.
+SESSION = {"calls": 0, "queues": 0, "near_ties": 0, "max_per_call": 0}
+# Bound per call: swapped ids are allowed only at the K-th boundary between keys
+# whose fp64 scores differ by <= 1e-5 relative; more than this many in one call
+# means a systematic error, not rounding.
+NEAR_TIE_BOUND = 8
+
+
 def compare_selection(gpu: dict, ref: dict, phi: np.ndarray, arrival: np.ndarray, mode: int, K: int,
                       base: int = 0, report: Report | None = None):
     """gpu: dict of numpy arrays (rows = positions); ref: oracle tick/score_select result;
@@ -92,6 +101,11 @@ def compare_selection(gpu: dict, ref: dict, phi: np.ndarray, arrival: np.ndarray
             assert gpu["primary"] in cands
     else:
         assert gpu["primary"] == -1
+    SESSION["calls"] += 1
+    SESSION["queues"] += rep.checked_queues
+    SESSION["near_ties"] += rep.near_ties
+    SESSION["max_per_call"] = max(SESSION["max_per_call"], rep.near_ties)
+    assert rep.near_ties <= NEAR_TIE_BOUND, f"{rep.near_ties} near-tie swaps in one selection (> {NEAR_TIE_BOUND})"
     return rep
 
 

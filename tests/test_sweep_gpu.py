@@ -22,7 +22,7 @@ def E():
 
 @pytest.fixture(scope="module")
 def ctx(E):
-    return E.Context(0, max_pool=1 << 21, max_history=0, max_k=64)
+    return E.Context(0, max_pool=1 << 21, max_history=0, max_k=64, max_sweep=1 << 21)
 
 
 @pytest.fixture(scope="module")

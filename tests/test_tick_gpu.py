@@ -119,7 +119,7 @@ def test_tick_gaps_and_bubbles(E, orc, ctx, mode):
     """A partition with holes: gap requests go through Alg. 2 in index order."""
     part = orc.make_partition([(32, 100), (180, 300), (1000, 2000), (5000, 6000)], means=[60, 240, 1500, 5500])
     rng = np.random.default_rng(7)
-    n = 10_000          # ~6.5k gap requests: within the 8192-entry gap list
+    n = 200_000         # ~130k gap requests through the epoch-parallel Alg. 2
     pool = {"len": rng.integers(1, 9000, size=n).astype(np.int32),
             "arrival": workload.arrivals(n, 7), "cost": workload.cost_estimates(np.ones(n, np.int32) * 100, 7)}
     g, ref, phi = _run_both(E, orc, ctx, pool, part, 16, mode, bubble_width=64)
@@ -127,17 +127,19 @@ def test_tick_gaps_and_bubbles(E, orc, ctx, mode):
     _check(g, ref, phi, pool, mode, 16)
 
 
-def test_tick_gap_list_overflow_reports_capacity(E, ctx):
-    """More gap requests than the gap list holds: CAPACITY, unprocessed qids stay -2."""
+def test_tick_all_pool_in_one_hole(E, ctx):
+    """Every request falls in one hole (20k gap requests, far more than the old
+    8192-entry list): the first creates the bubble [L - 32, L + 32), all the others
+    land inside it (App. D Alg. 2 in index order) -- nothing is refused."""
     n = 20_000
     ln = torch.full((n,), 5000, dtype=torch.int32, device="cuda")
     ar = torch.zeros(n, dtype=torch.float32, device="cuda")
     qid = torch.empty(n, dtype=torch.int32, device="cuda")
-    out = E.tick(ctx, ln, ar, None, E.make_partition([(1, 10)]), E.meta(**THETA0), E.select_params(k=4),
-                 qid_out=qid)
-    assert out.summary["status"] == 4 and out.summary["n_gap"] == n
-    q = qid.cpu().numpy()
-    assert ((q == -2) | (q == 1)).all() and (q == 1).sum() == 8192
+    part = E.make_partition([(1, 10)])
+    out = E.tick(ctx, ln, ar, None, part, E.meta(**THETA0), E.select_params(k=4), qid_out=qid)
+    assert out.summary["status"] == 0 and out.summary["n_gap"] == n and out.summary["n_bubbles"] == 1
+    assert (qid.cpu().numpy() == 1).all()
+    assert [(q["min_len"], q["max_len"]) for q in part.queues()] == [(1, 10), (4968, 5032)]
 
 
 def test_tick_bubble_cap(E, orc, ctx):
@@ -300,3 +302,19 @@ def test_sharded_tick_records_on_one_gpu(E, orc, ctx, heavy_parts, world, mode):
         g = gpu_result(out)
         compare_selection(g, ref, phi, pool["arrival"], mode, K)
     np.testing.assert_array_equal(qid.cpu().numpy(), ref["qid"])
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_tick_full_size_with_holes(E, orc, ctx_full, mode):
+    """App. D at pool scale: the C3 pool routed by the R&P partition with three of
+    its queues removed (five ranges become holes holding >= 1% of the 10M
+    requests).  Alg. 2 runs over every gap request in index order; qids, bubbles
+    and every selection output equal the oracle's."""
+    s, opart, _ = orc.partition(workload.heavy(1_000_000, 301))
+    qs = opart.queues()
+    keep = [q for i, q in enumerate(qs) if i not in (5, 11, 17, 23, len(qs) - 3)]
+    hole = orc.make_partition([(q["min_len"], q["max_len"]) for q in keep], means=[q["mean"] for q in keep])
+    pool = workload.pool("heavy", 10_000_000, 302)
+    g, ref, phi = _run_both(E, orc, ctx_full, pool, hole, 64, mode)
+    assert g["n_gap"] >= 100_000, g["n_gap"]
+    _check(g, ref, phi, pool, mode, 64)
