@@ -178,8 +178,10 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def run_sweep(E, ctx, dev, args):
-    """C5 (BASELINE configs[4]) on one GPU: 256 Θ x 1M snapshot, K=16, SCORE mode.
+def run_sweep(E, ctx, dev, args, rank=0, ws=1, group=None):
+    """C5 (BASELINE configs[4]): 256 Θ x 1M snapshot, K=16, SCORE mode; at N GPUs the
+    Θ are split by rank (32 per GPU at 8) and each rank sweeps its share
+    over the same (replicated) snapshot, no exchange; time = max over ranks.
     ALU-bound: each (request, Θ) pair is 3 fp32 FMA-pipe ops (FMUL + 2 FFMA) and one
     FSETP on the hot path, so the peak is 148 SMs x 128 fp32 lanes x clock / 4."""
     import torch
@@ -189,7 +191,9 @@ def run_sweep(E, ctx, dev, args):
     pool = workload.pool("bimodal", n, 501)
     ln, ar, co = (torch.from_numpy(pool[k]).to(dev) for k in ("len", "arrival", "cost"))
     qid, rsum = E.route(ctx, ln, c2part)
-    thetas = [E.meta(**t) for t in workload.random_thetas(args.sweep_thetas, 502)]
+    all_t = workload.random_thetas(args.sweep_thetas, 502)
+    lo_t, hi_t = workload.shard_range(len(all_t), rank, ws)
+    thetas = [E.meta(**t) for t in all_t[lo_t:hi_t]]
     sp = E.select_params(k=16, mode=0, now=workload.NOW)
     sctx = E.Context(dev.index or 0, max_pool=n, max_history=0, max_k=64, max_sweep=n)
     outs = E.score_select_sweep(sctx, ln, ar, co, qid, c2part, thetas, sp)
@@ -198,6 +202,9 @@ def run_sweep(E, ctx, dev, args):
     torch.cuda.synchronize()
     reps = 10
     sctx.set_timing(True)
+    if group is not None:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
@@ -206,15 +213,19 @@ def run_sweep(E, ctx, dev, args):
     torch.cuda.synchronize()
     tm = sctx.timing()
     ms = e0.elapsed_time(e1) / reps
-    pairs = n * len(thetas)
+    if group is not None:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    pairs = n * len(all_t)                      # all ranks together
     ffma = sctx.ffma_rate()            # measured fp32 FFMA/s on this box
-    peak = ffma / 4                    # 4 fp32-pipe instructions per (request, Θ) pair
+    peak = ffma / 4 * ws               # 4 fp32-pipe instructions per (request, Θ) pair, all ranks
     achieved = pairs / (ms / 1e3)
     sctx.close()
     return {"workload": "C5: 256 Θ uniform in S:500 bounds (seed 502) x 1M bimodal snapshot (seed 501) routed by "
                         "the GPU Refine-and-Prune partition of bimodal(1M, seed 201); K=16, SCORE",
             "metric": "(request, Θ) pairs scored+selected/s", "value": achieved, "ms_per_sweep": ms,
-            "thetas": len(thetas), "snapshot": n, "queues": c2part.n,
+            "thetas": len(all_t), "thetas_per_rank": len(thetas), "ranks": ws, "snapshot": n, "queues": c2part.n,
             "kernel_ms_per_sweep": tm["sweep_ms"] / reps, "launches_per_sweep": tm["sweep_launches"] / reps,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "pairs/s",
                          "frac": achieved / peak,
@@ -631,8 +642,8 @@ def main():
 
     # ---- C5: the meta-optimizer's Θ sweep (A12) over a 1M bimodal snapshot routed by
     # the GPU Refine-and-Prune partition of bimodal(1M, seed 201) (C2's partition)
-    if not args.no_sweep and ws == 1:
-        line["sweep"] = run_sweep(E, ctx, dev, args)
+    if not args.no_sweep:
+        line["sweep"] = run_sweep(E, ctx, dev, args, rank, ws, group)
     if ws == 1 and not args.no_c4:
         line["c4"] = run_c4(E, dev, local, "heavy", 402)
         line["c4_bimodal"] = run_c4(E, dev, local, "bimodal", 401)
