@@ -19,7 +19,7 @@ int64_t merge_smem_total(int in_mode);
 cudaError_t launch_stream(const PartialArgs& A, const Policy& P, const MergeArgs* MA, bool has_cost, int grid,
                           cudaStream_t st);
 int64_t stream_smem_bytes(bool has_cost, int lut_size, int nslots, int cap, int stages);
-cudaError_t launch_ftick(const FArgs& A, const Policy& P, const MergeArgs& MA, bool has_cost, int grid,
+cudaError_t launch_ftick(const FArgs& A, const Policy* P, const MergeArgs& MA, bool has_cost, int grid,
                          cudaStream_t st);
 int64_t ftick_smem_bytes(bool has_cost, int lut_size, int nslots, int stages);
 bool sweep_diag(ewsjf_ctx* ctx, unsigned long long* cuts_inserts);
@@ -94,6 +94,9 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
               cudaMallocHost(&ctx->h_lut, kLutCap + 32) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->lut_ev, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->stream_ev, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->policy_ev, cudaEventDisableTiming) == cudaSuccess &&
+              cudaMalloc(&ctx->d_policy, sizeof(Policy)) == cudaSuccess &&
+              cudaMallocHost(&ctx->h_policy, sizeof(Policy)) == cudaSuccess &&
               cudaMalloc(&ctx->gap, (size_t)ctx->gap_cap * sizeof(GapEntry)) == cudaSuccess &&
               cudaMalloc(&ctx->g_slot, (size_t)ctx->gap_cap * 4) == cudaSuccess &&
               cudaMalloc(&ctx->g_res, (size_t)ctx->gap_cap * 4) == cudaSuccess &&
@@ -112,6 +115,7 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
               cudaMalloc(&ctx->d_max_score, kMaxSlots * 4) == cudaSuccess;
     // fused tick rows: 64 queues x G CTAs x f_rc keys; overflow lists G x kFOvf
     ctx->f_rc = std::max(512, 4 * max_k);
+    ctx->h_policy_shadow = new unsigned char[sizeof(Policy)];
     ctx->bpre_cap = (int64_t)kMaxSlots * max_k;      // batch builder prefixes (global fallback)
     ok = ok && cudaMalloc(&ctx->d_bpre, (size_t)ctx->bpre_cap * sizeof(uint32_t)) == cudaSuccess;
     ok = ok && cudaMalloc(&ctx->f_rows, (size_t)64 * G * ctx->f_rc * sizeof(u64)) == cudaSuccess &&
@@ -166,6 +170,10 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
     if (ctx->h_lut) cudaFreeHost(ctx->h_lut);
     if (ctx->lut_ev) cudaEventDestroy(ctx->lut_ev);
     if (ctx->stream_ev) cudaEventDestroy(ctx->stream_ev);
+    if (ctx->policy_ev) cudaEventDestroy(ctx->policy_ev);
+    if (ctx->h_policy) cudaFreeHost(ctx->h_policy);
+    if (ctx->d_policy) cudaFree(ctx->d_policy);
+    delete[] (unsigned char*)ctx->h_policy_shadow;
     nccl_release(ctx);
     void* d[] = {ctx->g_slot, ctx->g_res, ctx->g_u0, ctx->g_u1, ctx->g_tab, ctx->f_rows, ctx->f_ovf_keys, ctx->f_ovf_code, ctx->d_lut, ctx->dbg, ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
                  ctx->d_blog, ctx->d_summary, ctx->d_len, ctx->d_arr, ctx->d_cost, ctx->d_qid, ctx->d_topk_id,
@@ -330,6 +338,19 @@ static ewsjf_status ensure_lut(ewsjf_ctx* ctx, const ewsjf_partition_t* part, in
     ctx->lut_n = part->n;
     ctx->lut_size = lutsz;
     ctx->lut_bounds = key;
+    return EWSJF_OK;
+}
+
+// The policy tables of the fused tick in device memory: uploaded (through a pinned
+// staging copy) only when they differ from the last upload.
+static ewsjf_status ensure_policy(ewsjf_ctx* ctx, const Policy& P) {
+    if (ctx->policy_valid && memcmp(ctx->h_policy_shadow, &P, sizeof(Policy)) == 0) return EWSJF_OK;
+    CU(cudaEventSynchronize(ctx->policy_ev));       // the staging buffer is free again
+    memcpy(ctx->h_policy, &P, sizeof(Policy));
+    memcpy(ctx->h_policy_shadow, &P, sizeof(Policy));
+    CU(cudaMemcpyAsync(ctx->d_policy, ctx->h_policy, sizeof(Policy), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaEventRecord(ctx->policy_ev, ctx->stream));
+    ctx->policy_valid = true;
     return EWSJF_OK;
 }
 
@@ -548,6 +569,7 @@ static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, 
     if (ftick_smem_bytes(has_cost, lutsz, nslots, stages) > budget || merge_smem_total(MERGE_IN_ROWS) > budget)
         return false;
     if ((*st = ensure_lut(ctx, part, lutsz)) != EWSJF_OK) return true;
+    if ((*st = ensure_policy(ctx, P)) != EWSJF_OK) return true;
     FArgs A;
     memset(&A, 0, sizeof A);
     A.len = d_len; A.arrival = d_arr; A.cost = d_cost; A.qid_out = d_qid_out;
@@ -589,7 +611,7 @@ static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, 
     cudaError_t e;
     {
         LaunchScope ls(ctx, KIND_TICK);
-        e = launch_ftick(A, P, M, has_cost, G, ctx->stream);
+        e = launch_ftick(A, (const Policy*)ctx->d_policy, M, has_cost, G, ctx->stream);
     }
     *st = e == cudaSuccess ? EWSJF_OK : fail(ctx, EWSJF_ERR_CUDA, "fused tick kernel: %s", cudaGetErrorString(e));
     return true;

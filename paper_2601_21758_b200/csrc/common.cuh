@@ -42,7 +42,7 @@ constexpr uint32_t kBadSlot = 0xFFFFu;        // invalid (len < 1 / unknown qid)
 // as a __grid_constant__ kernel parameter (≈6 KB).  Index = queue position.
 struct Policy {
     int32_t nslots;
-    int32_t pad;
+    int32_t pad[3];                // every table 16-byte aligned (the fused tick stages them with cp.async)
     int32_t min_len[kMaxSlots];
     int32_t max_len[kMaxSlots];
     int32_t sid[kMaxSlots];        // stable id

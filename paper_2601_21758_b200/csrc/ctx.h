@@ -17,6 +17,12 @@ struct ewsjf_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t stream_ev = nullptr;   // ewsjf_ctx_set_stream: orders the new stream after the old
+    // fused tick policy tables in device memory (ftick.cu), cached by content
+    void* d_policy = nullptr;
+    void* h_policy = nullptr;          // pinned staging
+    void* h_policy_shadow = nullptr;   // last uploaded content
+    cudaEvent_t policy_ev = nullptr;
+    bool policy_valid = false;
     int64_t max_pool = 0, max_history = 0;
     int32_t max_k = 0;
     int num_sms = 0;

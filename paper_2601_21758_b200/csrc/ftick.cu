@@ -36,7 +36,7 @@
 
 namespace ewsjf {
 
-constexpr int kFT = 512;            // threads per CTA
+constexpr int kFT = 768;            // threads per CTA (24 warps: latency hiding for the smem/MUFU chains)
 constexpr int kFW = kFT / 32;       // warps
 constexpr int kFTile = 128;         // requests per warp tile (4 per lane)
 constexpr int kFCodeFar = 0xFD;     // length beyond the LUT: binary search in the rare path
@@ -88,7 +88,7 @@ __host__ __device__ inline FSmem fsmem_layout(bool has_cost, int lut_size, int n
     L.hist = o;  o = fal(o + 4LL * 256);
     L.surv = o;  o = fal(o + 8LL * EWSJF_MAX_K);
     L.stile = o; o = fal(o + 8LL * kFW * kFMaxStages);
-    L.cnt = o;   o = fal(o + 2LL * kFT * (nslots + 2));   // rows: members 0..nslots-1, bad, dummy
+    L.cnt = o;   o = fal(o + 2LL * kFT * (nslots + 2));   // u16 rows: members 0..nslots-1, bad, dummy
     L.total = o;
     return L;
 }
@@ -117,7 +117,9 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {
         default: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
     }
 }
-__device__ __forceinline__ void fbar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kFT) : "memory"); }
+// non-aligned barrier: warps arrive from different call sites (the collective is entered from the
+// streaming loop and from the idle loop), which the .aligned form (bar.sync) does not allow
+__device__ __forceinline__ void fbar(int id) { asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(kFT) : "memory"); }
 
 // key high word -> fast-test float.  SCORE keys: the bits of s' (>= +0).
 // FIFO keys: hi = ~ord(arrival), inverted here.
@@ -255,8 +257,12 @@ __device__ __forceinline__ int block_collect(ForEach for_each, u64 t, u64* out, 
 
 template <int MODE, bool HAS_COST>
 __global__ void __launch_bounds__(kFT, 1)
-    ftick_kernel(const __grid_constant__ FArgs A, const __grid_constant__ Policy P,
+    ftick_kernel(const __grid_constant__ FArgs A, const Policy* __restrict__ Pd,
                  const __grid_constant__ MergeArgs MA) {
+    // the policy tables (6 KB) live in device memory, uploaded only when they change:
+    // as a kernel parameter they added ~4.5 us to every launch (measured); only the
+    // setup, the rare path and the merge read them
+    const Policy& P = *Pd;
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
@@ -344,6 +350,14 @@ __global__ void __launch_bounds__(kFT, 1)
         const int l16 = (lutsz + 1 + 15) / 16;
         const int4* src = reinterpret_cast<const int4*>(A.lut_dev);
         for (int i = tid; i < l16; i += kFT) cp_async16(smem + kFLutOff + 16 * i, src + i);
+        // and the per-queue weights / stable ids of the first 64 positions (the setup's
+        // only policy reads) into the surv region, 16 chunks of 16 B per array
+        if (tid < 64) {
+            const int arr = tid >> 4, ch = tid & 15;
+            const int32_t* srcp = arr == 0 ? (const int32_t*)Pd->wb : arr == 1 ? (const int32_t*)Pd->wu
+                                : arr == 2 ? (const int32_t*)Pd->wf : Pd->sid;
+            cp_async16(smem + L.surv + arr * 256 + ch * 16, srcp + ch * 4);
+        }
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     for (int i = 0; i < R; i++) issue(i);
@@ -352,28 +366,6 @@ __global__ void __launch_bounds__(kFT, 1)
 
     // ---- setup while the first tiles are in flight
     {
-        const float inf = __int_as_float(0x7f800000), nan = __int_as_float(0x7fffffff);
-        for (int c = tid; c < 256; c += kFT) {
-            float4 a = make_float4(0.f, 0.f, 0.f, nan), b = make_float4(nan, 0.f, 0.f, 0.f);
-            int cnto = nslots + 1, qid = -2;
-            if (c == kFCodeGap || c == kFCodeFar) {
-                // always into the rare path: the arrival compare (a NaN arrival is !ok anyway)
-                if (SCORE) b.x = inf; else a.w = inf;
-            }
-            if (c < nslots) {
-                // sample phase: no primary filter, no secondary filter (the sample block takes both)
-                a = make_float4(P.wb[c], P.wu[c], P.wf[c], nan);
-                cnto = c;
-                qid = P.sid[c];
-            } else if (c == kFCodeBad) {
-                cnto = nslots;
-                qid = -1;
-            }
-            b.y = __int_as_float(qid);
-            b.z = __int_as_float(cnto * kFT * 2);
-            rec[2 * c] = a;
-            rec[2 * c + 1] = b;
-        }
         for (int q = tid; q < kFMaxSlots; q += kFT) {
             thr64[q] = 0ull; sec64[q] = 0ull; rcnt[q] = 0;
             for (int m = 0; m < kFBoardMax; m++) bmax[q * kFBoardMax + m] = 0u;
@@ -383,20 +375,50 @@ __global__ void __launch_bounds__(kFT, 1)
         const int n16 = (2 * kFT * (nslots + 2)) / 16;
         for (int i = tid; i < n16; i += kFT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + 12] = fgtime();
-        cp_async_wait_n(R);            // this thread's LUT chunks (the oldest group) have landed
         if (tid == 0) {
             M->flag = 0; M->novf = 0; M->ndone = 0; M->last = 0; M->ncoll = 0; M->pn = 0;
             M->members = 0ull; M->sec = 0ull; M->tcoll = 0ull;
         }
+        cp_async_wait_n(R);            // this thread's LUT / policy chunks (the oldest group) have landed
     }
     __syncthreads();
-    if (tid == 0 && lutsz >= 0) lut[lutsz] = (unsigned char)kFCodeFar;   // lengths >= lut_size
+    {
+        // per-code records from the staged policy
+        const float inf = __int_as_float(0x7f800000), nan = __int_as_float(0x7fffffff);
+        const float* pw = (const float*)(smem + L.surv);        // staged {wb, wu, wf, sid}[64]
+        for (int c = tid; c < 256; c += kFT) {
+            float4 a = make_float4(0.f, 0.f, 0.f, nan), b = make_float4(nan, 0.f, 0.f, 0.f);
+            int cnto = nslots + 1, qid = -2;
+            if (c == kFCodeGap || c == kFCodeFar) {
+                // always into the rare path: the arrival compare (a NaN arrival is !ok anyway)
+                if (SCORE) b.x = inf; else a.w = inf;
+            }
+            if (c < nslots) {
+                // sample phase: no primary filter, no secondary filter (the sample block takes both)
+                a = make_float4(pw[c], pw[64 + c], pw[128 + c], nan);
+                cnto = c;
+                qid = ((const int*)pw)[192 + c];
+            } else if (c == kFCodeBad) {
+                cnto = nslots;
+                qid = -1;
+            }
+            b.y = __int_as_float(qid);
+            b.z = __int_as_float(cnto * kFT * 2);
+            rec[2 * c] = a;
+            rec[2 * c + 1] = b;
+        }
+        if (tid == 0 && lutsz >= 0) lut[lutsz] = (unsigned char)kFCodeFar;   // lengths >= lut_size
+    }
     __syncthreads();
     stamp(1);
 
     const uint32_t gbase = A.gbase;
     const bool write_qid = A.qid_out != nullptr;
-    uint16_t* mycnt = (uint16_t*)(cntb + 2 * tid);
+    // per-thread u16 member counters (row r of thread t at halfword r*kFT + t), bumped
+    // with no-return atomics on the containing word (ATOMS.ADD of 1 or 1 << 16): no
+    // load-add-store dependency on the hot path; <= 65535 requests per thread per tick
+    uint32_t* cntw = (uint32_t*)cntb + (tid >> 1);
+    const uint32_t cinc = (tid & 1) ? 0x10000u : 1u;
     unsigned n_exc = 0, n_ins = 0, n_gap = 0, n_bad = 0;
     u64* const rows_cta = A.rows.keys + (size_t)cta * RC;     // row of queue q: rows_cta + q*G*RC
     const size_t row_stride = (size_t)G * RC;
@@ -452,7 +474,7 @@ __global__ void __launch_bounds__(kFT, 1)
             if (q >= 0) {
                 const float4 w = rec[2 * q];
                 ok = score_sp(b, a, co, HAS_COST, A.sp, w.x, w.y, w.z, &sp);
-                mycnt[q * kFT]++;
+                atomicAdd(cntw + q * (kFT / 2), cinc);
                 if (write_qid) A.qid_out[idx] = P.sid[q];
                 c = q;
             } else {
@@ -471,7 +493,7 @@ __global__ void __launch_bounds__(kFT, 1)
             return;
         }
         if (c >= nslots) return;   // bad length / padding
-        if (!ok) { mycnt[c * kFT]--; n_exc++; return; }
+        if (!ok) { atomicSub(cntw + c * (kFT / 2), cinc); n_exc++; return; }
         const u64 ks = score_key(sp, gid), kf = fifo_key(a, gid);
         const u64 k1 = SCORE ? ks : kf, k2 = SCORE ? kf : ks;
         if (k1 >= *(volatile u64*)&thr64[c]) insert(c, k1);
@@ -521,8 +543,7 @@ __global__ void __launch_bounds__(kFT, 1)
             // member counter row straight from the code (no wait on the record load):
             // rows 0..nslots-1 members, nslots invalid length, nslots+1 dummy
             const int crow = c < nslots ? c : (c == kFCodeBad ? nslots : nslots + 1);
-            uint16_t* cp = mycnt + crow * kFT;
-            *cp = (uint16_t)(*cp + 1);
+            atomicAdd(cntw + crow * (kFT / 2), cinc);
             const float4 w = rec[2 * c];
             const float4 r2 = rec[2 * c + 1];
             const bool ok = score_sp(b[j], a[j], co[j], HAS_COST, A.sp, w.x, w.y, w.z, &sp[j]);
@@ -859,8 +880,8 @@ __global__ void __launch_bounds__(kFT, 1)
         if (dbg && tid == 0) { A.dbg[cta * kDbgStride + 8] = (unsigned long long)M->ncoll; A.dbg[cta * kDbgStride + 9] = M->tcoll; }
     }
     (void)n_gap;
-    __threadfence();
     __syncthreads();
+    if (tid == 0) __threadfence();   // cumulative over the CTA's writes ordered by the bar.sync (as a grid sync)
     stamp(5);
     if (A.merge == 0) return;
 
@@ -880,46 +901,48 @@ __global__ void __launch_bounds__(kFT, 1)
     if (A.refresh)   // nobody reads the refresh board past the barrier: clear this CTA's column for the next tick
         for (int q = tid; q < nslots; q += kFT) A.rboard[(size_t)q * G + cta] = 0ull;
 
+    // The fast merge's loads (this queue's rows, its bound) are issued together with
+    // the gap-count check, so the common case pays one round trip, not two.
+    const int q = cta;
+    const int rrow = tid % G, rpart = tid / G;
+    const bool ract = q < nslots && tid < 3 * G;     // 3 threads per row
+    const size_t rr = (size_t)q * G + rrow;
+    const u64* rk = A.rows.keys + rr * RC;
+    int nc = 0;
+    u64 kv[8];
+    unsigned long long mm = 0;
+    u64 sk = 0ull;
+    if (ract) {
+        // one round trip: count, members and secondary and, speculatively, the first 24
+        // keys (masked by the count below; the rows were cut to the end-of-stream bound)
+        nc = __ldcg(&A.rows.cnt[rr]);
+        if (rpart == 0) { mm = (unsigned long long)__ldcg(&A.rows.members[rr]); sk = __ldcg(&A.rows.sec[rr]); }
+#pragma unroll
+        for (int u = 0; u < 8; u++) kv[u] = __ldcg(rk + rpart * 8 + u);
+    }
+    u64 thr = q < nslots ? __ldcg(&A.gthr[q]) : 0ull;
     const unsigned long long graw = __ldcg(&A.ctr->gap_count);
     if (graw > 0 || A.merge == 2) {
         // gap requests (App. D, Alg. 2) / exchange record: the general merge
-        if (A.merge == 2) merge_phase<MERGE_IN_ROWS, MERGE_OUT_EXCHANGE, HAS_COST>(MA, P, smem);
-        else merge_phase<MERGE_IN_ROWS, MERGE_OUT_FINAL, HAS_COST>(MA, P, smem);
+        if (A.merge == 2) merge_phase<MERGE_IN_ROWS, MERGE_OUT_EXCHANGE, HAS_COST, kFT>(MA, P, smem);
+        else merge_phase<MERGE_IN_ROWS, MERGE_OUT_FINAL, HAS_COST, kFT>(MA, P, smem);
         stamp(7);
         return;
     }
 
     // ---- fast merge: CTA q merges queue q (no gap requests in this tick)
-    const int q = cta;
     if (q < nslots) {
-        u64 thr = __ldcg(&A.gthr[q]);
         // the whole shared memory is free now: [rowoff | pool]
         int* rowoff = (int*)(smem + L.cnt);                  // [G + 1]
         u64* pool = (u64*)(smem + L.ring);
         // the candidate pool takes the ring region only (the control block M, hist and
         // surv that follow it are still in use): >= 2 stages x 2 arrays x 16 warps x 512 B
         const int pcap = (int)((L.bars - L.ring) / 8);
-        constexpr int kChunk = 2048;                          // candidates scanned per round
+        constexpr int kChunk = 3 * kFT;                       // candidates scanned per round
         if (tid == 0) { M->pn = 0; M->members = 0ull; M->sec = 0ull; M->ncoll = 0; M->maxnc = 0; }
         __syncthreads();
-        // one round trip: 3 threads per row load its count, members and secondary and,
-        // speculatively, its first 24 keys (masked by the count afterwards; the rows
-        // were cut to the end-of-stream bound, so most hold far fewer)
-        const int rrow = tid % G, rpart = tid / G;
-        const bool ract = tid < 3 * G;
-        const size_t rr = (size_t)q * G + rrow;
-        const u64* rk = A.rows.keys + rr * RC;
-        int nc = 0;
-        u64 kv[8];
+        if (dbg && tid == 0) A.dbg[cta * kDbgStride + 21] = fgtime();
         {
-            unsigned long long mm = 0;
-            u64 sk = 0ull;
-            if (ract) {
-                nc = __ldcg(&A.rows.cnt[rr]);
-                if (rpart == 0) { mm = (unsigned long long)__ldcg(&A.rows.members[rr]); sk = __ldcg(&A.rows.sec[rr]); }
-#pragma unroll
-                for (int u = 0; u < 8; u++) kv[u] = __ldcg(rk + rpart * 8 + u);
-            }
             for (int o = 16; o; o >>= 1) {
                 mm += __shfl_xor_sync(0xffffffffu, mm, o);
                 const u64 so = shfl_xor_u64(sk, o);
@@ -935,6 +958,7 @@ __global__ void __launch_bounds__(kFT, 1)
                 rowoff[rrow + 1] = nc;         // counts for the prefix of the chunked path
             }
             if (ract && rpart == 0 && !nc) rowoff[rrow + 1] = 0;
+            if (dbg && tid == 0) A.dbg[cta * kDbgStride + 22] = fgtime();
         }
         __syncthreads();
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + 20] = fgtime();
@@ -1119,18 +1143,18 @@ __global__ void __launch_bounds__(kFT, 1)
 int64_t merge_smem_total(int in_mode);
 
 template <int MO, bool C>
-static cudaError_t launch_f(const FArgs& A, const Policy& P, const MergeArgs& MA, int grid, cudaStream_t st) {
+static cudaError_t launch_f(const FArgs& A, const Policy* P, const MergeArgs& MA, int grid, cudaStream_t st) {
     const int64_t ls = fsmem_layout(C, A.lut_size, A.nslots, A.stages).total;
     const int64_t lm = A.merge ? merge_smem_total(MERGE_IN_ROWS) : 0;
     const int64_t smem = ls > lm ? ls : lm;
     auto k = ftick_kernel<MO, C>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    void* args[] = {(void*)&A, (void*)&P, (void*)&MA};
+    void* args[] = {(void*)&A, (void*)&P, (void*)&MA};   // &P: address of the device pointer
     return cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kFT), args, (size_t)smem, st);
 }
 
-cudaError_t launch_ftick(const FArgs& A, const Policy& P, const MergeArgs& MA, bool has_cost, int grid,
+cudaError_t launch_ftick(const FArgs& A, const Policy* P, const MergeArgs& MA, bool has_cost, int grid,
                          cudaStream_t st) {
     if (A.sp.mode == EWSJF_SELECT_FIFO)
         return has_cost ? launch_f<EWSJF_SELECT_FIFO, true>(A, P, MA, grid, st)

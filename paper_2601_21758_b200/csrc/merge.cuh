@@ -70,9 +70,10 @@ static __device__ __forceinline__ void bubble_weights(const double* th, double L
 }
 
 // CTA-wide count of pool keys >= t (one barrier; rotating counters).
+template <int NT>
 static __device__ __forceinline__ int pool_count_ge(const u64* pool, int n, u64 t, MMisc* M, int it) {
     int c = 0;
-    for (int i = threadIdx.x; i < n; i += kMThreads) c += pool[i] >= t;
+    for (int i = threadIdx.x; i < n; i += NT) c += pool[i] >= t;
     c = __reduce_add_sync(0xffffffffu, c);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(&M->cnt[it % 3], c);
     __syncthreads();
@@ -83,10 +84,11 @@ static __device__ __forceinline__ int pool_count_ge(const u64* pool, int n, u64 
 
 // Shrink the pool to the keys >= t where K <= #(>= t) <= kRankMax (bisection,
 // requires #(>= lo) >= K); survivors are moved to the front.
+template <int NT>
 static __device__ void pool_shrink(u64* pool, float* psp, int& pn, u64& lo, int K, u64* surv, float* ssp, MMisc* M) {
     const int tid = threadIdx.x;
     u64 mx = 0;
-    for (int i = tid; i < pn; i += kMThreads) mx = pool[i] > mx ? pool[i] : mx;
+    for (int i = tid; i < pn; i += NT) mx = pool[i] > mx ? pool[i] : mx;
     mx = warp_max_u64(mx);
     __syncthreads();
     if (tid == 0) { M->maxk = 0; M->cnt[0] = M->cnt[1] = M->cnt[2] = 0; M->nsurv = 0; }
@@ -97,7 +99,7 @@ static __device__ void pool_shrink(u64* pool, float* psp, int& pn, u64& lo, int 
     int it = 0;
     while (hi - lo > 1ull) {
         const u64 mid = lo + (hi - lo) / 2ull;
-        const int c = pool_count_ge(pool, pn, mid, M, it++);
+        const int c = pool_count_ge<NT>(pool, pn, mid, M, it++);
         if (c >= K) {
             lo = mid;
             if (c <= kRankMax) break;
@@ -105,7 +107,7 @@ static __device__ void pool_shrink(u64* pool, float* psp, int& pn, u64& lo, int 
             hi = mid;
         }
     }
-    for (int i = tid; i < pn; i += kMThreads) {
+    for (int i = tid; i < pn; i += NT) {
         if (pool[i] >= lo) {
             const int p = atomicAdd(&M->nsurv, 1);
             surv[p] = pool[i];
@@ -114,14 +116,14 @@ static __device__ void pool_shrink(u64* pool, float* psp, int& pn, u64& lo, int 
     }
     __syncthreads();
     pn = M->nsurv;
-    for (int i = tid; i < pn; i += kMThreads) {
+    for (int i = tid; i < pn; i += NT) {
         pool[i] = surv[i];
         if (psp) psp[i] = ssp[i];
     }
     __syncthreads();
 }
 
-template <int IN, int OUT, bool HAS_COST>
+template <int IN, int OUT, bool HAS_COST, int NT = kMThreads>
 __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P, unsigned char* smem) {
     const MergeSmem L = merge_layout(IN);
     const int tid = threadIdx.x, lane = tid & 31;
@@ -179,7 +181,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
     // creators are classified again (a bubble changes nothing outside its gap; a
     // request inside a queue stays there).  At most 256 - nq epochs.  CTA 0 runs it
     // and publishes the table; the other CTAs wait for it.
-    for (int i = tid; i < nq; i += kMThreads) {
+    for (int i = tid; i < nq; i += NT) {
         t_lo[i] = P.min_len[i]; t_hi[i] = P.max_len[i];
         t_slot[i] = i; t_pos[i] = i; t_id[i] = P.sid[i];
     }
@@ -198,9 +200,9 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         unsigned* mincre = (unsigned*)uni;       // [gap index 0..n]: lowest creator gid in that gap (uni is free here)
         for (;;) {
             if (tid == 0) { *cmin_s = 0xffffffffu; M->nkeep = 0; }
-            for (int i = tid; i <= n; i += kMThreads) mincre[i] = 0xffffffffu;
+            for (int i = tid; i <= n; i += NT) mincre[i] = 0xffffffffu;
             __syncthreads();
-            for (long long idx = tid; idx < nu; idx += kMThreads) {
+            for (long long idx = tid; idx < nu; idx += NT) {
                 const uint32_t v = first ? (uint32_t)idx : (uint32_t)ucur[idx];
                 const GapEntry g = gap_entry(v);
                 const int Lq = g.len;
@@ -226,7 +228,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             __syncthreads();
             const unsigned cmin = *cmin_s;
             if (cmin == 0xffffffffu) {            // no creator left: every pending request is final
-                for (long long idx = tid; idx < nu; idx += kMThreads) {
+                for (long long idx = tid; idx < nu; idx += NT) {
                     const uint32_t v = first ? (uint32_t)idx : (uint32_t)ucur[idx];
                     const int r = A.g_res[v];
                     const int slot = r & 1023;
@@ -237,7 +239,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
                 break;
             }
             // the creator (unique gid) inserts its bubble
-            for (long long idx = tid; idx < nu; idx += kMThreads) {
+            for (long long idx = tid; idx < nu; idx += NT) {
                 const uint32_t v = first ? (uint32_t)idx : (uint32_t)ucur[idx];
                 if (((A.g_res[v] >> 10) & 3) == kClsNew && gap_entry(v).gid == cmin) M->vcre = (int)v;
             }
@@ -278,7 +280,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             // settle: a request before c is final; after c, one inside a queue is final,
             // a creator goes again, and a tolerated one goes again only if some creator
             // precedes it in its own gap (that bubble may become its neighbour)
-            for (long long idx = tid; idx < nu; idx += kMThreads) {
+            for (long long idx = tid; idx < nu; idx += NT) {
                 const uint32_t v = first ? (uint32_t)idx : (uint32_t)ucur[idx];
                 if ((int)v == vc) continue;
                 const int r = A.g_res[v];
@@ -308,15 +310,15 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             A.g_tab[0] = n; A.g_tab[1] = nb; A.g_tab[2] = nd;
         }
         __syncthreads();
-        for (int i = tid; i < n; i += kMThreads) {
+        for (int i = tid; i < n; i += NT) {
             A.g_tab[3 + i] = t_lo[i]; A.g_tab[3 + kMaxSlots + i] = t_hi[i]; A.g_tab[3 + 2 * kMaxSlots + i] = t_slot[i];
         }
-        for (int i = tid; i < nq + nb; i += kMThreads) {
+        for (int i = tid; i < nq + nb; i += NT) {
             A.g_tab[3 + 3 * kMaxSlots + i] = t_L[i]; A.g_tab[3 + 4 * kMaxSlots + i] = t_id[i];
         }
         // qid write-back of this rank's gap requests (stable ids)
         if (A.qid) {
-            for (long long e = tid; e < gcount; e += kMThreads) {
+            for (long long e = tid; e < gcount; e += NT) {
                 const GapEntry g = gap_entry((uint32_t)e);
                 const long long li = (long long)g.gid - (long long)A.gbase;
                 if (li >= 0 && li < A.n_local) { const int as = A.g_slot[e]; A.qid[li] = as >= 0 ? t_id[as] : -1; }
@@ -335,18 +337,18 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         }
         __syncthreads();
         const int n = __ldcg(&A.g_tab[0]), nb = __ldcg(&A.g_tab[1]);
-        for (int i = tid; i < n; i += kMThreads) {
+        for (int i = tid; i < n; i += NT) {
             t_lo[i] = __ldcg(&A.g_tab[3 + i]); t_hi[i] = __ldcg(&A.g_tab[3 + kMaxSlots + i]);
             t_slot[i] = __ldcg(&A.g_tab[3 + 2 * kMaxSlots + i]);
         }
-        for (int i = tid; i < nq + nb; i += kMThreads) {
+        for (int i = tid; i < nq + nb; i += NT) {
             t_L[i] = __ldcg(&A.g_tab[3 + 3 * kMaxSlots + i]); t_id[i] = __ldcg(&A.g_tab[3 + 4 * kMaxSlots + i]);
         }
         if (tid == 0) { M->nfinal = n; M->nbub = nb; M->ndrop = __ldcg(&A.g_tab[2]); }
         __syncthreads();
     }
     if (do_gaps) {
-        for (int p = tid; p < M->nfinal; p += kMThreads) t_pos[t_slot[p]] = p;
+        for (int p = tid; p < M->nfinal; p += NT) t_pos[t_slot[p]] = p;
         __syncthreads();
     }
     if (blockIdx.x == 0 && A.blog && tid == 0) A.blog->n = M->nbub;
@@ -379,7 +381,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         if (tid == 0) { M->members = 0; M->sec = 0; M->sec_sp = 0.f; M->gexc = 0; M->pn = 0; }
         // ---- rows: exclusive prefix of the row counts (parallel load + block scan)
         const int nrows = IN == MERGE_IN_ROWS ? A.rows.G : A.world;
-        for (int r = tid; r < nrows; r += kMThreads) {
+        for (int r = tid; r < nrows; r += NT) {
             int c = 0;
             if (s < nq)
                 c = IN == MERGE_IN_ROWS ? A.rows.cnt[(size_t)s * A.rows.G + r]
@@ -410,7 +412,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             float ssk = 0.f;
             int gex = 0;
             if (s < nq) {
-                for (int r = tid; r < nrows; r += kMThreads) {
+                for (int r = tid; r < nrows; r += NT) {
                     u64 k;
                     float kp = 0.f;
                     if (IN == MERGE_IN_ROWS) {
@@ -425,7 +427,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
                     if (k > sk) { sk = k; ssk = kp; }
                 }
             }
-            for (long long e = tid; e < ngap_all; e += kMThreads) {
+            for (long long e = tid; e < ngap_all; e += NT) {
                 if (__ldcg(&A.g_slot[e]) != s) continue;
                 u64 k1, k2;
                 float sp;
@@ -463,10 +465,10 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         // warp loads all keys of its rows in one go (independent loads in flight), then
         // filters them into the pool; the general loop below then handles only the
         // gap requests of this slot.
-        constexpr int kMWarps = kMThreads / 32;
+        constexpr int kMWarps = NT / 32;
         constexpr int kFR = 12;
         if (IN == MERGE_IN_ROWS && A.rows.cap <= 64 && nrows <= kFR * kMWarps &&
-            total_rows <= L.esmem - kMThreads) {
+            total_rows <= L.esmem - NT) {
             const int warp_m = tid >> 5;
             u64 kv[kFR][2];
 #pragma unroll
@@ -490,8 +492,8 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         }
         while (e0 < total) {
             const int space = L.esmem - pn;
-            if (space < kMThreads && pn > kRankMax) {
-                pool_shrink(uni, psp, pn, thr, K, surv, ssp, M);
+            if (space < NT && pn > kRankMax) {
+                pool_shrink<NT>(uni, psp, pn, thr, K, surv, ssp, M);
                 continue;
             }
             const int take = (int)(total - e0 < (long long)space ? total - e0 : (long long)space);
@@ -500,13 +502,13 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             // kU elements per thread per step: their row lookups and loads are issued
             // together (kU loads in flight instead of one L2 round trip each)
             constexpr int kU = 8;
-            for (int i0 = tid; i0 < take; i0 += kU * kMThreads) {
+            for (int i0 = tid; i0 < take; i0 += kU * NT) {
                 u64 key[kU];
                 float sp[kU];
                 bool ok[kU];
 #pragma unroll
                 for (int u = 0; u < kU; u++) {
-                    const int i = i0 + u * kMThreads;
+                    const int i = i0 + u * NT;
                     const long long e = e0 + i;
                     key[u] = 0ull; sp[u] = 0.f; ok[u] = false;
                     if (i < take && e < total_rows) {
@@ -528,7 +530,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
                 }
 #pragma unroll
                 for (int u = 0; u < kU; u++) {
-                    const int i = i0 + u * kMThreads;
+                    const int i = i0 + u * NT;
                     const long long e = e0 + i;
                     if (i < take && e >= total_rows && __ldcg(&A.g_slot[e - total_rows]) == s) {
                         u64 k2;
@@ -545,10 +547,10 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             pn = M->pn;
             e0 += take;
         }
-        if (pn > kRankMax) pool_shrink(uni, psp, pn, thr, K, surv, ssp, M);
+        if (pn > kRankMax) pool_shrink<NT>(uni, psp, pn, thr, K, surv, ssp, M);
         MDBG(14);
         // rank sort (keys unique) -> surv[0..pn) descending
-        for (int i = tid; i < pn; i += kMThreads) {
+        for (int i = tid; i < pn; i += NT) {
             const u64 k = uni[i];
             int r = 0;
             for (int j = 0; j < pn; j++) r += uni[j] > k;
@@ -576,7 +578,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         if (OUT == MERGE_OUT_FINAL) {
             const int pos = t_pos[s];
             const float qi = (float)(pos + 1);
-            for (int r = tid; r < K; r += kMThreads) {
+            for (int r = tid; r < K; r += NT) {
                 const size_t o = (size_t)pos * K + r;
                 if (r < nout) {
                     A.topk_id[o] = (int64_t)key_gid(surv[r]);
@@ -602,7 +604,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             }
         } else {   // MERGE_OUT_EXCHANGE: this rank's record
             unsigned char* rec = A.ex_out;
-            for (int r = tid; r < nout; r += kMThreads) {
+            for (int r = tid; r < nout; r += NT) {
                 ((u64*)(rec + X.keys))[(size_t)s * K + r] = surv[r];
                 ((float*)(rec + X.sp))[(size_t)s * K + r] = payload(r);
             }
@@ -617,10 +619,10 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         if (tid == 0 && M->gexc) atomicAdd(&A.ctr->n_excluded, (unsigned long long)M->gexc);
     }
     if (IN == MERGE_IN_ROWS && OUT == MERGE_OUT_ROUTE)
-        for (int i = blockIdx.x * kMThreads + tid; i < nq; i += gridDim.x * kMThreads) A.gthr[i] = 0ull;
+        for (int i = blockIdx.x * NT + tid; i < nq; i += gridDim.x * NT) A.gthr[i] = 0ull;
     if (OUT == MERGE_OUT_EXCHANGE && blockIdx.x == 0) {   // header + gap entries of this rank
         const int ng = (int)(graw < kExGap ? graw : kExGap);
-        for (int i = tid; i < ng; i += kMThreads) ((GapEntry*)(A.ex_out + X.gaps))[i] = A.gap[i];
+        for (int i = tid; i < ng; i += NT) ((GapEntry*)(A.ex_out + X.gaps))[i] = A.gap[i];
         if (tid == 0) {
             ExHeader* h = (ExHeader*)(A.ex_out + X.hdr);
             h->gap_count = graw;

@@ -677,6 +677,7 @@ __global__ void __launch_bounds__(kHT, 1)
             const int r = nxt[p];
             const int rn = nxt[r];                  // m0 = end sentinel
             const int q = prv[p];
+            __syncwarp();                           // every lane has read the links before lane 0 writes
             if (lane == 0) {
                 nxt[p] = (uint16_t)rn;
                 if (rn < m0) prv[rn] = (uint16_t)p;
@@ -778,6 +779,7 @@ __global__ void __launch_bounds__(kHT, 1)
                     const unsigned okm = __ballot_sync(0xffffffffu, okk);
                     const int kst = __ffs(~okm) - 1;        // confirmed merges (leading ones)
                     if (kst > 0) {
+                        __syncwarp();                       // the walk's reads before the commit's writes
                         // commit: the new Q and its links; leaves of every pair touched -> dead
                         if (dir == 0) {
                             // Q = [x_kst, bq): x_kst = start of N_{kst-1} = [x_kst, x_{kst-1})
@@ -866,6 +868,7 @@ __global__ void __launch_bounds__(kHT, 1)
                     ok = cand < S || (cand == S && cand != kDead && pos < si);
                 }
                 if (!ok) {                          // chain ends: the dynamic pairs go back into the tree
+                    __syncwarp();
                     if (lane == 0) {
                         if (L != kNone) leaf[L] = kl;
                         if (bq < m0) leaf[a] = kr;
@@ -876,6 +879,7 @@ __global__ void __launch_bounds__(kHT, 1)
                 }
                 if (left) {                         // Q absorbs L: Q = [L, bq)
                     const int LL = prv[L];
+                    __syncwarp();
                     if (lane == 0) {
                         nxt[L] = (uint16_t)bq;
                         if (bq < m0) prv[bq] = (uint16_t)L;
@@ -887,6 +891,7 @@ __global__ void __launch_bounds__(kHT, 1)
                     p = L;
                     dir = 0;
                 } else {                            // Q absorbs R: Q = [a, c)
+                    __syncwarp();
                     if (lane == 0) {
                         nxt[a] = (uint16_t)c;
                         if (c < m0) prv[c] = (uint16_t)a;

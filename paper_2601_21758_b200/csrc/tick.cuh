@@ -79,7 +79,7 @@ struct FArgs {
     float* max_score;
     ewsjf_summary* summary;
 };
-constexpr int kFOvf = 4608;     // per-CTA overflow list: >= 16 warps x 2 tiles x 128 requests
+constexpr int kFOvf = 6144;     // per-CTA overflow list: >= 24 warps x 2 tiles x 128 requests
 
 struct PartialArgs {
     const int32_t* len;
