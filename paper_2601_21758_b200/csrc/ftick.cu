@@ -63,6 +63,7 @@ struct FMisc {
     int maxnc;          // merge: longest candidate row
     unsigned long long members, sec;
     unsigned long long tcoll;
+    unsigned long long agg[3];   // end of stream: invalid, excluded, inserted (CTA totals)
 };
 
 struct FSmem {
@@ -378,6 +379,7 @@ __global__ void __launch_bounds__(kFT, 1)
         if (tid == 0) {
             M->flag = 0; M->novf = 0; M->ndone = 0; M->last = 0; M->ncoll = 0; M->pn = 0;
             M->members = 0ull; M->sec = 0ull; M->tcoll = 0ull;
+            M->agg[0] = M->agg[1] = M->agg[2] = 0ull;
         }
         cp_async_wait_n(R);            // this thread's LUT / policy chunks (the oldest group) have landed
     }
@@ -871,10 +873,17 @@ __global__ void __launch_bounds__(kFT, 1)
             ex += __shfl_xor_sync(0xffffffffu, ex, o);
             ins += __shfl_xor_sync(0xffffffffu, ins, o);
         }
+        // CTA totals first (smem), then one global atomic per CTA and counter
         if (lane == 0) {
-            if (bad) atomicAdd(&A.ctr->n_invalid, bad);
-            if (ex) atomicAdd(&A.ctr->n_excluded, ex);
-            if (ins) atomicAdd(&A.ctr->dbg_inserted, ins);
+            if (bad) atomicAdd(&M->agg[0], bad);
+            if (ex) atomicAdd(&M->agg[1], ex);
+            if (ins) atomicAdd(&M->agg[2], ins);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (M->agg[0]) atomicAdd(&A.ctr->n_invalid, M->agg[0]);
+            if (M->agg[1]) atomicAdd(&A.ctr->n_excluded, M->agg[1]);
+            if (M->agg[2]) atomicAdd(&A.ctr->dbg_inserted, M->agg[2]);
         }
         if (tid == 0 && M->ncoll) atomicAdd(&A.ctr->dbg_compactions, (unsigned long long)M->ncoll);
         if (dbg && tid == 0) { A.dbg[cta * kDbgStride + 8] = (unsigned long long)M->ncoll; A.dbg[cta * kDbgStride + 9] = M->tcoll; }
@@ -897,6 +906,7 @@ __global__ void __launch_bounds__(kFT, 1)
     }
     __syncthreads();
     stamp(6);
+    if (dbg && tid == 0) A.dbg[cta * kDbgStride + 24] = fgtime();
     if (cta == 0 && tid == 0) A.ctr->ftiles = 0ull;   // every claim of this launch is done
     if (A.refresh)   // nobody reads the refresh board past the barrier: clear this CTA's column for the next tick
         for (int q = tid; q < nslots; q += kFT) A.rboard[(size_t)q * G + cta] = 0ull;
@@ -922,6 +932,7 @@ __global__ void __launch_bounds__(kFT, 1)
     }
     u64 thr = q < nslots ? __ldcg(&A.gthr[q]) : 0ull;
     const unsigned long long graw = __ldcg(&A.ctr->gap_count);
+    if (dbg && tid == 0) A.dbg[cta * kDbgStride + 23] = fgtime() ^ (unsigned long long)(graw == 0x123456789ull);
     if (graw > 0 || A.merge == 2) {
         // gap requests (App. D, Alg. 2) / exchange record: the general merge
         if (A.merge == 2) merge_phase<MERGE_IN_ROWS, MERGE_OUT_EXCHANGE, HAS_COST, kFT>(MA, P, smem);

@@ -36,6 +36,12 @@ constexpr int kSwBatch = 128;       // Θ per kernel sequence (scratch is sized 
 constexpr int kSwMaxK = 96;         // cap = 2K+32 <= 256 keys (register K-th selection)
 constexpr int kSwPrepThreads = 512;
 constexpr int kSwWarps = 8;         // warps per CTA in K4 / K5
+// Θ-independent candidate prefilter (K3a-K3g): lengths 2 <= b < kSkyBins are
+// grouped; blocks of kSkyBlk consecutive lengths; K <= 32 (one key per lane)
+constexpr int kSkyBins = 1 << 16;
+constexpr int kSkyBlk = 64;
+constexpr int kSkyMaxBlocks = kSkyBins / kSkyBlk + kMaxSlots + 1;
+constexpr int kSkyMaxK = 32;
 
 struct SweepScratch {
     int64_t n_cap = 0;              // records capacity
@@ -53,6 +59,23 @@ struct SweepScratch {
     u64* rows = nullptr;            // [task][kSwT][K]
     int32_t* rowcnt = nullptr;      // [task][kSwT]
     float* w = nullptr;             // [kSwBatch][256][3] weights by position (device, A7)
+    // prefilter scratch: bin counts -> starts, scatter cursors, records sorted by length,
+    // candidate flags, per-block top keys, prefix bounds, the compacted records + layout
+    int32_t* bcnt = nullptr;        // [kSkyBins + 1]
+    int32_t* bfill = nullptr;       // [kSkyBins]
+    int32_t* srt = nullptr;         // [n]
+    uint8_t* cand = nullptr;        // [n]
+    u64* blktop = nullptr;          // [kSkyMaxBlocks][kSkyMaxK]
+    u64* blkid = nullptr;           // [kSkyMaxBlocks][kSkyMaxK]
+    u64* lentop = nullptr;          // [kSkyBins][kSkyMaxK] per length: its K best (f1, id) keys
+    u64* lenid = nullptr;           // [kSkyBins][kSkyMaxK] per length: its K lowest id keys
+    u64* qidk = nullptr;            // [256]
+    uint32_t* pref = nullptr;       // [kSkyMaxBlocks]
+    float4* rec2 = nullptr;         // [n]
+    int64_t* qoff2 = nullptr;       // [257]
+    int32_t* cpre2 = nullptr;       // [257]
+    int32_t* qfill2 = nullptr;      // [256]
+    int64_t* qcnt2 = nullptr;       // [256]
     size_t attr_smem = 0;           // select kernel: dynamic smem attribute set for this ctx's device
     int occ = 1;
 };
@@ -73,6 +96,8 @@ struct SweepArgs {
     int32_t nids;
     int32_t sorted_ids[kMaxSlots];
     int32_t sorted_pos[kMaxSlots];
+    // prefilter: per position the grouped length range [qbin_lo, qbin_hi) and its first block
+    int32_t qbin_lo[kMaxSlots], qbin_hi[kMaxSlots], qblk[kMaxSlots + 1];
     SweepScratch s;
 };
 
@@ -189,6 +214,274 @@ __global__ void __launch_bounds__(kSwPrepThreads) sweep_scatter_kernel(const __g
             base = __shfl_sync(peers, base, leader);
             A.s.rec[A.s.qoff[p] + base + __popc(peers & ((1u << lane) - 1u))] = f;
         }
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Θ-independent candidate prefilter (exact up to fp32 near-ties).  Within a
+// queue, s' = w_base f0(b) + w_urg f1 + w_fair f2(b) with all weights >= 0
+// (S:306), f0 = 1/(b+1) and f2 = ln(b+1)/(b+1) both non-increasing in b for
+// b >= 2, and the fp32 evaluation monotone in every feature.  So a record p can
+// only be in a queue's top K for some Θ if fewer than K records q dominate it
+// (f0, f1, f2 all >=): (i) inside p's own length b only the K best by (f1, id)
+// qualify (features f0, f2 are bit-identical there, ties go to the lower id as
+// in the key), (ii) across lengths, the K-th best f1 of the candidates of all
+// shorter lengths must stay below p's f1 (tracked per block of kSkyBlk lengths:
+// dominators in p's own block are ignored, which only keeps more).  A dominated
+// record can only displace p at an exact fp32 tie, i.e. a near-tie.  The select
+// kernels then run over the survivors (~10^3 of the 10^6 records at C5).
+__device__ __forceinline__ int sky_len(const float4& f) { return (int)rintf(1.0f / f.x - 1.0f); }
+__device__ __forceinline__ int sky_pos(const SweepArgs& A, int64_t i) {   // position of record i
+    int lo = 0, hi = A.nq;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (A.s.qoff[mid] <= i) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ bool sky_grouped(const SweepArgs& A, int p, int b) {
+    return b >= A.qbin_lo[p] && b < A.qbin_hi[p];
+}
+__device__ __forceinline__ u64 sky_key(const float4& f) {
+    return ((u64)__float_as_uint(f.y) << 32) | (u64)(~__float_as_uint(f.w));
+}
+
+// K3a: histogram of the grouped records' lengths
+__global__ void __launch_bounds__(kSwPrepThreads) sky_hist_kernel(const __grid_constant__ SweepArgs A) {
+    const int64_t ntot = A.s.qoff[A.nq];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 f = A.s.rec[i];
+        const int b = sky_len(f), p = sky_pos(A, i);
+        if (sky_grouped(A, p, b)) atomicAdd(&A.s.bcnt[b], 1);
+    }
+}
+// K3b: one CTA, exclusive scan of the kSkyBins counts in place (bcnt[kSkyBins] = total):
+// warp w scans its contiguous 2048 bins in coalesced rows of 32, then the warp totals
+__global__ void __launch_bounds__(1024) sky_scan_kernel(const __grid_constant__ SweepArgs A) {
+    __shared__ int ws[32];
+    constexpr int per = kSkyBins / 32;                 // bins per warp
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int* bc = A.s.bcnt + warp * per;
+    int tot = 0;
+    for (int j = lane; j < per; j += 32) { tot += bc[j]; A.s.bfill[warp * per + j] = 0; }
+    tot = __reduce_add_sync(0xffffffffu, tot);
+    if (lane == 0) ws[warp] = tot;
+    __syncthreads();
+    int run = 0;
+    for (int w = 0; w < warp; w++) run += ws[w];
+    for (int j0 = 0; j0 < per; j0 += 32) {
+        const int c = bc[j0 + lane];
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        bc[j0 + lane] = run + incl - c;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tid == 1023) A.s.bcnt[kSkyBins] = run;
+}
+// K3c: record indices sorted by length
+__global__ void __launch_bounds__(kSwPrepThreads) sky_scatter_kernel(const __grid_constant__ SweepArgs A) {
+    const int64_t ntot = A.s.qoff[A.nq];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 f = A.s.rec[i];
+        const int b = sky_len(f), p = sky_pos(A, i);
+        A.s.cand[i] = 0;
+        if (sky_grouped(A, p, b)) A.s.srt[A.s.bcnt[b] + atomicAdd(&A.s.bfill[b], 1)] = (int32_t)i;
+    }
+}
+// Streaming warp top-K of the nonzero keys produced by key(j) for j in [beg, end):
+// chunks of 7 x 32 keys plus the K kept (one per lane, K <= 32); returns the kept
+// keys (one per lane, 0 = none).  sb: 32 u64 of shared scratch for this warp.
+template <typename KeyFn>
+__device__ __forceinline__ u64 sky_warp_topk(int beg, int end, int K, KeyFn key, u64* sb) {
+    const int lane = threadIdx.x & 31;
+    u64 kept = 0ull;
+    for (int j0 = beg; j0 < end; j0 += 7 * 32) {
+        u64 v[8];
+        int nz = 0;
+#pragma unroll
+        for (int r = 0; r < 7; r++) {
+            const int j = j0 + r * 32 + lane;
+            v[r] = j < end ? key(j) : 0ull;
+            nz += v[r] != 0ull;
+        }
+        v[7] = kept;
+        nz += kept != 0ull;
+        nz = __reduce_add_sync(0xffffffffu, nz);
+        const u64 t = nz > K ? warp_kth_regs<8>(v, K) : 1ull;
+        int base = 0;
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const bool keep = v[r] && v[r] >= t;
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) sb[base + __popc(m & ((1u << lane) - 1u))] = v[r];   // <= K <= 32 kept
+            base += __popc(m);
+        }
+        __syncwarp();
+        kept = lane < base ? sb[lane] : 0ull;
+        __syncwarp();
+    }
+    return kept;
+}
+__device__ __forceinline__ u64 sky_idkey(const float4& f) { return (u64)(~__float_as_uint(f.w)) + 1ull; }   // larger = lower id
+
+// K3d: one warp per length: its K best records by (f1, id) are candidates, and so
+// are its K lowest ids (when w_urg = 0 every record of the length scores the same
+// and R24's lowest ids win).  Both lists (min(count, K) keys each) are kept per
+// length for K3e.
+__global__ void __launch_bounds__(kSwPrepThreads) sky_group_kernel(const __grid_constant__ SweepArgs A) {
+    __shared__ u64 sbuf[kSwPrepThreads / 32][32];
+    const int lane = threadIdx.x & 31;
+    u64* sb = sbuf[threadIdx.x >> 5];
+    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int K = A.K;
+    for (int b = 2 + w0; b < kSkyBins; b += nw) {
+        const int beg = A.s.bcnt[b], end = A.s.bcnt[b + 1], c = end - beg;
+        if (c == 0) continue;
+        u64* lt = A.s.lentop + (size_t)b * kSkyMaxK;
+        u64* li = A.s.lenid + (size_t)b * kSkyMaxK;
+        if (c <= K) {                                  // c <= K <= 32: one record per lane
+            if (lane < c) {
+                const int i = A.s.srt[beg + lane];
+                const float4 f = __ldg(&A.s.rec[i]);
+                A.s.cand[i] = 1;
+                lt[lane] = sky_key(f);
+                li[lane] = sky_idkey(f);
+            }
+            continue;
+        }
+        const u64 k1 = sky_warp_topk(beg, end, K, [&](int j) { return sky_key(__ldg(&A.s.rec[A.s.srt[j]])); }, sb);
+        const u64 k2 = sky_warp_topk(beg, end, K, [&](int j) { return sky_idkey(__ldg(&A.s.rec[A.s.srt[j]])); }, sb);
+        if (lane < K) { lt[lane] = k1; li[lane] = k2; }   // exactly K nonzero keys each (keys are unique)
+        u64 m1 = k1 ? k1 : ~0ull, m2 = k2 ? k2 : ~0ull;    // the K-th of each = the smallest kept
+        m1 = warp_min_u64(m1);
+        m2 = warp_min_u64(m2);
+        for (int j = beg + lane; j < end; j += 32) {
+            const int i = A.s.srt[j];
+            const float4 f = __ldg(&A.s.rec[i]);
+            if (sky_key(f) >= m1 || sky_idkey(f) >= m2) A.s.cand[i] = 1;
+        }
+    }
+}
+// K3e: one warp per block of kSkyBlk lengths of one position: the top K candidate
+// keys (by f1) and the K lowest candidate ids of the block, merged from the
+// per-length lists (the block's top K by f1 among all its candidates are among
+// the lengths' top K by f1, and likewise for the ids)
+__global__ void __launch_bounds__(kSwPrepThreads) sky_block_kernel(const __grid_constant__ SweepArgs A) {
+    __shared__ u64 sbuf[kSwPrepThreads / 32][32];
+    const int lane = threadIdx.x & 31;
+    u64* sb = sbuf[threadIdx.x >> 5];
+    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int K = A.K;
+    const int nblk = A.qblk[A.nq];
+    for (int g = w0; g < nblk; g += nw) {
+        int p = 0;
+        while (p + 1 < A.nq && A.qblk[p + 1] <= g) p++;
+        const int jj = g - A.qblk[p];
+        const int blo = A.qbin_lo[p] + jj * kSkyBlk, bhi = min(blo + kSkyBlk, A.qbin_hi[p]);
+        // item j = (length blo + j / 32, list slot j % 32): one length per warp row
+        auto item = [&](const u64* lists, int j) -> u64 {
+            const int b = blo + (j >> 5), l = j & 31;
+            const int n_b = min(A.s.bcnt[b + 1] - A.s.bcnt[b], K);
+            return l < n_b ? lists[(size_t)b * kSkyMaxK + l] : 0ull;
+        };
+        const int nit = (bhi - blo) * 32;
+        const u64 k1 = sky_warp_topk(0, nit, K, [&](int j) { return item(A.s.lentop, j); }, sb);
+        const u64 k2 = sky_warp_topk(0, nit, K, [&](int j) { return item(A.s.lenid, j); }, sb);
+        A.s.blktop[(size_t)g * kSkyMaxK + lane] = k1;
+        A.s.blkid[(size_t)g * kSkyMaxK + lane] = k2;
+    }
+}
+// K3f: one warp per position: prefix over its blocks -> pref[g] = high word (f1) of
+// the K-th largest candidate key of the blocks before g (0 while fewer than K);
+// and qidk[p] = the queue's K-th lowest candidate id key (all weights 0: every
+// member scores 0 and the K lowest ids are the answer, R24)
+__device__ __forceinline__ u64 sky_merge_topk(u64 run, u64 add, int K, u64* sb, int* n_out) {
+    const int lane = threadIdx.x & 31;
+    u64 v[2] = {run, add};
+    int nz = (v[0] != 0ull) + (v[1] != 0ull);
+    nz = __reduce_add_sync(0xffffffffu, nz);
+    const u64 t = nz > K ? warp_kth_regs<2>(v, K) : 1ull;
+    int base = 0;
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        const bool keep = v[r] && v[r] >= t;
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) sb[base + __popc(m & ((1u << lane) - 1u))] = v[r];
+        base += __popc(m);
+    }
+    __syncwarp();
+    const u64 out = lane < base ? sb[lane] : 0ull;
+    __syncwarp();
+    *n_out = base;
+    return out;
+}
+__global__ void sky_prefix_kernel(const __grid_constant__ SweepArgs A) {
+    __shared__ u64 sb[32];
+    const int lane = threadIdx.x & 31;
+    const int p = blockIdx.x;
+    if (p >= A.nq) return;
+    const int K = A.K;
+    u64 run = 0ull, rid = 0ull;
+    int nrun = 0, nid = 0;
+    u64 kth = 0ull, kid = 0ull;         // K-th key of run / rid once they hold K keys (their minimum)
+    for (int g = A.qblk[p]; g < A.qblk[p + 1]; g++) {
+        if (lane == 0) A.s.pref[g] = (u32)(kth >> 32);
+        const u64 a1 = A.s.blktop[(size_t)g * kSkyMaxK + lane], a2 = A.s.blkid[(size_t)g * kSkyMaxK + lane];
+        // a block with no key above the current K-th leaves the running top K as it is
+        if (__any_sync(0xffffffffu, a1 > kth)) {
+            run = sky_merge_topk(run, a1, K, sb, &nrun);
+            if (nrun >= K) kth = warp_min_u64(run ? run : ~0ull);
+        }
+        if (__any_sync(0xffffffffu, a2 > kid)) {
+            rid = sky_merge_topk(rid, a2, K, sb, &nid);
+            if (nid >= K) kid = warp_min_u64(rid ? rid : ~0ull);
+        }
+    }
+    if (lane == 0) A.s.qidk[p] = kid;   // 0: fewer than K candidates, keep them all
+}
+__device__ __forceinline__ bool sky_keep(const SweepArgs& A, int64_t i, const float4& f, int p) {
+    const int b = sky_len(f);
+    if (!sky_grouped(A, p, b)) return true;
+    if (!A.s.cand[i]) return false;
+    if (sky_idkey(f) >= A.s.qidk[p]) return true;          // among the queue's K lowest ids
+    const int g = A.qblk[p] + (b - A.qbin_lo[p]) / kSkyBlk;
+    return __float_as_uint(f.y) > A.s.pref[g];
+}
+// K3g: survivors per position, then (plan2, one thread) the compacted layout, then the scatter
+__global__ void __launch_bounds__(kSwPrepThreads) sky_count_kernel(const __grid_constant__ SweepArgs A) {
+    const int64_t ntot = A.s.qoff[A.nq];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 f = A.s.rec[i];
+        const int p = sky_pos(A, i);
+        if (sky_keep(A, i, f, p)) atomicAdd((unsigned long long*)&A.s.qcnt2[p], 1ull);
+    }
+}
+__global__ void sky_plan_kernel(const __grid_constant__ SweepArgs A) {
+    if (threadIdx.x != 0) return;
+    int64_t off = 0;
+    int32_t cp = 0;
+    for (int q = 0; q < A.nq; q++) {
+        A.s.qoff2[q] = off;
+        A.s.cpre2[q] = cp;
+        const int64_t c = A.s.qcnt2[q];
+        off += c;
+        cp += (int32_t)((c + A.chunk - 1) / A.chunk);
+        A.s.qfill2[q] = 0;
+    }
+    A.s.qoff2[A.nq] = off;
+    A.s.cpre2[A.nq] = cp;
+}
+__global__ void __launch_bounds__(kSwPrepThreads) sky_compact_kernel(const __grid_constant__ SweepArgs A) {
+    const int64_t ntot = A.s.qoff[A.nq];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 f = A.s.rec[i];
+        const int p = sky_pos(A, i);
+        if (sky_keep(A, i, f, p)) A.s.rec2[A.s.qoff2[p] + atomicAdd(&A.s.qfill2[p], 1)] = f;
     }
 }
 
@@ -501,7 +794,8 @@ __global__ void sweep_summary_kernel(const __grid_constant__ SweepOutArgs A) {
 void sweep_free(ewsjf_ctx* ctx) {
     SweepScratch* S = ctx->sw;
     if (!S) return;
-    void* d[] = {S->rec, S->qcount, S->qoff, S->cpre, S->qfill, S->head, S->headf, S->bad, S->task_ctr, S->gthr,
+    void* d[] = {S->lentop, S->lenid, S->blkid, S->qidk, S->bcnt, S->bfill, S->srt, S->cand, S->blktop, S->pref, S->rec2, S->qoff2, S->cpre2, S->qfill2,
+                 S->qcnt2, S->rec, S->qcount, S->qoff, S->cpre, S->qfill, S->head, S->headf, S->bad, S->task_ctr, S->gthr,
                  S->rows, S->rowcnt, S->w};
     for (void* p : d)
         if (p) cudaFree(p);
@@ -529,14 +823,29 @@ ewsjf_status sweep_alloc(ewsjf_ctx* ctx, int64_t n, int64_t tasks, int K) {
                   cudaMalloc(&S->headf, 16 * kMaxSlots) == cudaSuccess &&
                   cudaMalloc(&S->bad, 32) == cudaSuccess && cudaMalloc(&S->task_ctr, 4) == cudaSuccess &&
                   cudaMalloc(&S->gthr, 8 * (size_t)kSwBatch * kMaxSlots) == cudaSuccess &&
-                  cudaMalloc(&S->w, 12 * (size_t)kSwBatch * kMaxSlots) == cudaSuccess;
+                  cudaMalloc(&S->w, 12 * (size_t)kSwBatch * kMaxSlots) == cudaSuccess &&
+                  cudaMalloc(&S->bcnt, 4 * (size_t)(kSkyBins + 1)) == cudaSuccess &&
+                  cudaMalloc(&S->bfill, 4 * (size_t)kSkyBins) == cudaSuccess &&
+                  cudaMalloc(&S->blktop, 8 * (size_t)kSkyMaxBlocks * kSkyMaxK) == cudaSuccess &&
+                  cudaMalloc(&S->blkid, 8 * (size_t)kSkyMaxBlocks * kSkyMaxK) == cudaSuccess &&
+                  cudaMalloc(&S->lentop, 8 * (size_t)kSkyBins * kSkyMaxK) == cudaSuccess &&
+                  cudaMalloc(&S->lenid, 8 * (size_t)kSkyBins * kSkyMaxK) == cudaSuccess &&
+                  cudaMalloc(&S->qidk, 8 * kMaxSlots) == cudaSuccess &&
+                  cudaMalloc(&S->pref, 4 * (size_t)kSkyMaxBlocks) == cudaSuccess &&
+                  cudaMalloc(&S->qoff2, 8 * (kMaxSlots + 1)) == cudaSuccess &&
+                  cudaMalloc(&S->cpre2, 4 * (kMaxSlots + 1)) == cudaSuccess &&
+                  cudaMalloc(&S->qfill2, 4 * kMaxSlots) == cudaSuccess &&
+                  cudaMalloc(&S->qcnt2, 8 * kMaxSlots) == cudaSuccess;
         if (!ok) return fail(ctx, EWSJF_ERR_CUDA, "sweep scratch allocation failed");
     }
     if (S->n_cap < n) {
-        if (S->rec) cudaFree(S->rec);
-        S->rec = nullptr;
+        for (void* x : {(void*)S->rec, (void*)S->rec2, (void*)S->srt, (void*)S->cand})
+            if (x) cudaFree(x);
+        S->rec = S->rec2 = nullptr; S->srt = nullptr; S->cand = nullptr;
         S->n_cap = 0;
-        if (cudaMalloc(&S->rec, 16 * (size_t)std::max<int64_t>(n, 1)) != cudaSuccess)
+        const size_t nn = (size_t)std::max<int64_t>(n, 1);
+        if (cudaMalloc(&S->rec, 16 * nn) != cudaSuccess || cudaMalloc(&S->rec2, 16 * nn) != cudaSuccess ||
+            cudaMalloc(&S->srt, 4 * nn) != cudaSuccess || cudaMalloc(&S->cand, nn) != cudaSuccess)
             return fail(ctx, EWSJF_ERR_CUDA, "sweep records allocation failed");
         S->n_cap = n;
     }
@@ -639,6 +948,35 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
         sweep_scatter_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
     }
     CU(cudaGetLastError());
+    // Θ-independent candidate prefilter (K <= 32): the select kernels run over the
+    // records no other K records dominate in every feature
+    const bool sky = K <= kSkyMaxK && !getenv("EWSJF_NO_SKY");
+    if (sky) {
+        int nb = 0;
+        for (int p = 0; p < nq; p++) {
+            int lo = std::max(2, part->q[p].min_len), hi = std::min(part->q[p].max_len, kSkyBins);
+            if (lo >= hi) lo = hi = 0;
+            A.qbin_lo[p] = lo; A.qbin_hi[p] = hi; A.qblk[p] = nb;
+            nb += (hi - lo + kSkyBlk - 1) / kSkyBlk;
+        }
+        A.qblk[nq] = nb;
+        CU(cudaMemsetAsync(S->bcnt, 0, 4 * (size_t)(kSkyBins + 1), st));
+        CU(cudaMemsetAsync(S->qcnt2, 0, 8 * kMaxSlots, st));
+        const int sgrid = ctx->num_sms * 4;
+        LaunchScope ls(ctx, KIND_SWEEP);
+        sky_hist_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
+        sky_scan_kernel<<<1, 1024, 0, st>>>(A);
+        sky_scatter_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
+        sky_group_kernel<<<sgrid, kSwPrepThreads, 0, st>>>(A);
+        sky_block_kernel<<<std::max(1, std::min(sgrid, (nb + 15) / 16)), kSwPrepThreads, 0, st>>>(A);
+        sky_prefix_kernel<<<nq, 32, 0, st>>>(A);
+        sky_count_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
+        sky_plan_kernel<<<1, 32, 0, st>>>(A);
+        sky_compact_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
+        CU(cudaGetLastError());
+        // the select / merge kernels read the survivors
+        A.s.rec = S->rec2; A.s.qoff = S->qoff2; A.s.cpre = S->cpre2;
+    }
     const size_t sel_smem = (size_t)kSwWarps * kSwT * (A.cap * 8 + 16 + 8 + 4 + 4);
     const size_t mrg_smem = (size_t)kSwWarps * A.cap * 8;
     // kernel attributes and occupancy are queried once per shared-memory size (host calls)
@@ -668,7 +1006,7 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
             LaunchScope ls(ctx, KIND_SWEEP);
             sweep_select_kernel<<<ctx->num_sms * std::max(occ, 1), kSwWarps * 32, sel_smem, st>>>(A);
         }
-        O.s = *S; O.nq = nq; O.K = K; O.cap = A.cap; O.n_theta = nb; O.rcap = A.rcap;
+        O.s = A.s; O.nq = nq; O.K = K; O.cap = A.cap; O.n_theta = nb; O.rcap = A.rcap;
         for (int t = 0; t < nb; t++) {
             O.outs[t] = outs[b0 + t];
             O.outs[t].h_summary = nullptr;

@@ -124,10 +124,40 @@ def test_sweep_edge_cases(E, orc, ctx):
 
 
 def test_sweep_full_size_c5(E, orc, ctx, c2_partition):
-    """BASELINE C5 at full snapshot size (1M bimodal requests routed by the C2
-    partition), K=16, in bench.py's launch configuration; 24 of the 256 Θ are
-    checked against the oracle (the oracle's full sort per Θ is the slow part)."""
+    """BASELINE C5 at full size in bench.py's launch configuration: all 256 Θ over
+    the 1M bimodal snapshot routed by the C2 partition in ONE call, K=16; a strided
+    subset of 24 Θ is checked against the oracle (its full sort per Θ is slow)."""
     pool, qid = _snapshot(orc, c2_partition, 1_000_000, 501)
-    thetas = workload.random_thetas(256, 502)[::11]
+    thetas = workload.random_thetas(256, 502)
     res, _ = _run_sweep(E, ctx, pool, qid, c2_partition, thetas, 16, 0)
-    _check_against_oracle(orc, pool, qid, c2_partition, thetas, res, 16, 0)
+    _check_against_oracle(orc, pool, qid, c2_partition, thetas[::11], res[::11], 16, 0)
+
+
+@pytest.mark.parametrize("kind", ["bimodal", "heavy"])
+def test_sweep_prefilter_matches_full_evaluation(E, orc, ctx, c2_partition, kind, monkeypatch):
+    """The Θ-independent dominance prefilter (sweep.cu K3a-K3g) against the sweep
+    without it (EWSJF_NO_SKY) and against the oracle: lengths 1 (where
+    ln(b+1)/(b+1) still rises), lengths past the 65536 grouping range, ties."""
+    rng = np.random.default_rng(12 if kind == "heavy" else 13)
+    n = 60_000
+    lens = workload.lengths(kind, n, 14).copy()
+    lens[rng.integers(0, n, 300)] = 1
+    lens[rng.integers(0, n, 300)] = 2
+    lens[rng.integers(0, n, 200)] = 70_000 + rng.integers(0, 500, 200)
+    part = orc.make_partition([(1, 3), (3, 64), (64, 3000), (3000, 71_000)])
+    arr = workload.arrivals(n, 15)
+    arr[::50] = arr[0]                                        # exact feature ties across ids
+    cost = workload.cost_estimates(lens, 16)
+    s, qid, *_ = orc.route(lens, orc.copy_partition(part), 64)
+    pool = {"len": lens, "arrival": arr, "cost": cost}
+    thetas = workload.random_thetas(9, 17) + [dict(a_b=0.0, b_b=1.0, a_u=0.0, b_u=0.0, a_f=0.0, b_f=0.0),
+                                              dict(a_b=0.0, b_b=0.0, a_u=0.0, b_u=0.0, a_f=0.0, b_f=2.0)]
+    res, _ = _run_sweep(E, ctx, pool, qid, part, thetas, 16, 0)
+    _check_against_oracle(orc, pool, qid, part, thetas, res, 16, 0)
+    monkeypatch.setenv("EWSJF_NO_SKY", "1")
+    full, _ = _run_sweep(E, ctx, pool, qid, part, thetas, 16, 0)
+    for a, b in zip(res, full):
+        nq = a["n_queues"]
+        np.testing.assert_array_equal(a["count"][:nq], b["count"][:nq])
+        np.testing.assert_array_equal(a["head_id"][:nq], b["head_id"][:nq])
+        np.testing.assert_array_equal(a["topk_id"][:nq], b["topk_id"][:nq])      # same fp32 keys: identical
