@@ -555,7 +555,7 @@ static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, 
     const int nslots = part->n;
     const bool has_cost = d_cost != nullptr;
     if (getenv("EWSJF_OLD_TICK") || getenv("EWSJF_NO_FTICK") || !ctx->coop || nslots < 1 || nslots > 64 || ctx->num_sms > 160 ||
-        ctx->num_sms < nslots)
+        ctx->num_sms < nslots || n >= (1ll << 37))   // tile indices are 32-bit in the fused kernel
         return false;
     if (!aligned16(d_len) || !aligned16(d_arr) || (has_cost && !aligned16(d_cost)) ||
         (d_qid_out && !aligned16(d_qid_out)))
@@ -563,7 +563,7 @@ static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, 
     const int K = sp->k;
     const int lutsz = std::min(part->q[nslots - 1].max_len, kLutCap);
     int stages = 4;
-    if (const char* e = getenv("EWSJF_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
+    if (const char* e = getenv("EWSJF_STAGES")) stages = std::max(2, std::min(4, atoi(e)));
     const int budget = ctx->smem_optin > 0 ? ctx->smem_optin : 232448;
     while (stages > 2 && ftick_smem_bytes(has_cost, lutsz, nslots, stages) > budget) stages--;
     if (ftick_smem_bytes(has_cost, lutsz, nslots, stages) > budget || merge_smem_total(MERGE_IN_ROWS) > budget)

@@ -89,7 +89,7 @@ __host__ __device__ inline FSmem fsmem_layout(bool has_cost, int lut_size, int n
     L.hist = o;  o = fal(o + 4LL * 256);
     L.surv = o;  o = fal(o + 8LL * EWSJF_MAX_K);
     L.stile = o; o = fal(o + 8LL * kFW * kFMaxStages);
-    L.cnt = o;   o = fal(o + 2LL * kFT * (nslots + 2));   // u16 rows: members 0..nslots-1, bad, dummy
+    L.cnt = o;   o = fal(o + 2LL * kFT * (nslots + 1));   // u16 rows: members 0..nslots-1, other codes
     L.total = o;
     return L;
 }
@@ -305,47 +305,65 @@ __global__ void __launch_bounds__(kFT, 1)
     const int S0 = (int)((int64_t)R + 1 < stride ? (int64_t)R + 1 : stride);
     const int64_t dynb = stride - S0;                 // dynamic tiles per block
     const int64_t ndyn = ntiles - GW * (int64_t)S0;   // tiles handed out by the counter
-    int64_t* stile = (int64_t*)(smem + L.stile) + warp * kFMaxStages;   // tile held by each ring stage (-1: none)
+    int* stile = (int*)(smem + L.stile) + warp * kFMaxStages;   // tile held by each ring stage (-1: none)
     auto stage = [&](int st, int a) -> unsigned char* { return ring + (st * narr + a) * kFTile * 4; };
-    int64_t seq = 0;                 // next position in this warp's tile sequence
+    int64_t seq = 0;                 // next position in this warp's static tiles
     unsigned long long cbase = 0ull, nbase = 0ull;   // claimed batches (lane 0): current, next (in flight)
+    // dynamic tiles, warp-uniform: position dcur of the current batch [.., dend), its
+    // tile tn and the dynamic tiles left in tn's block (one division per batch)
+    int dcur = 0, dend = 0, tn = 0, rb = 0;
+    const int ndyn32 = (int)ndyn, dynb32 = (int)dynb, GWdynb = (int)(GW * dynb), GWstride = (int)(GW * stride);
     // the first claim: right away if the ring prologue already needs dynamic tiles, else
     // after the sample tile (it then completes during the sample-bound wait; 2368 warps
     // claiming at launch serialised on the counter for ~1.5 us)
     if (lane == 0 && ndyn > 0 && S0 <= R) nbase = atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim);
-    auto next_tile = [&]() -> int64_t {               // all lanes; tile of sequence position seq, -1 = done
-        int64_t t = -1;
-        if (seq < S0) {
-            t = blk * stride + seq;
-        } else {
-            const int64_t j = seq - S0;
-            if (j % kFClaim == 0) {                   // batch boundary: the next batch becomes current
-                if (lane == 0) {
-                    cbase = nbase;
-                    nbase = cbase < (unsigned long long)ndyn
-                                ? atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim) : cbase;
-                }
+    auto next_tile = [&]() -> int {                   // all lanes; the warp's next tile, -1 = done
+        if (seq < S0) return (int)(blk * stride + seq++);
+        if (dcur >= dend) {                           // batch boundary: the next batch becomes current
+            if (lane == 0) {
+                cbase = nbase;
+                nbase = cbase < (unsigned long long)ndyn
+                            ? atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim) : cbase;
             }
-            long long d = (long long)__shfl_sync(0xffffffffu, cbase, 0) + j % kFClaim;
-            if (d < ndyn) t = d < GW * dynb ? (d / dynb) * stride + S0 + d % dynb : GW * stride + (d - GW * dynb);
+            const unsigned long long d64 = __shfl_sync(0xffffffffu, cbase, 0);
+            if (d64 >= (unsigned long long)ndyn) return -1;
+            const int d = (int)d64;
+            dcur = d;
+            dend = min(d + kFClaim, ndyn32);
+            if (d < GWdynb) {
+                const unsigned qq = (unsigned)d / (unsigned)dynb32, r = (unsigned)d - qq * (unsigned)dynb32;
+                tn = (int)(qq * (unsigned)stride) + S0 + (int)r;
+                rb = dynb32 - (int)r;
+            } else {
+                tn = GWstride + (d - GWdynb);
+                rb = INT_MAX;
+            }
         }
-        seq++;
+        const int t = tn;
+        dcur++;
+        tn++;
+        if (--rb == 0) {                              // past the block's last dynamic tile
+            if (tn < GWstride) { tn += S0; rb = dynb32; } else rb = INT_MAX;
+        }
         return t;
     };
     // Per-lane cp.async (LDGSTS) ring: every lane copies, and later reads back, its
     // own 16 bytes per array of each tile; one commit group per tile (empty past
     // the end).  (A per-warp ring of 512-byte cp.async.bulk copies measured ~2.2 TB/s:
     // the bulk-copy engine costs ~90 cycles per copy, too many copies per SM.)
-    auto issue = [&](int st) {        // all lanes: the next tile of the sequence into stage st
-        const int64_t t = next_tile();
-        if (lane == 0) stile[st] = t;
+    auto issue_t = [&](int st, int t) {   // all lanes: tile t (-1: none) into stage st
         if (t >= 0 && t < nfull) {
-            const int64_t off = t * kFTile + 4 * lane;
+            const int64_t off = (int64_t)t * kFTile + 4 * lane;
             cp_async16(stage(st, 0) + 16 * lane, A.len + off);
             cp_async16(stage(st, 1) + 16 * lane, A.arrival + off);
             if (HAS_COST) cp_async16(stage(st, 2) + 16 * lane, A.cost + off);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto issue = [&](int st) {        // all lanes: the next tile of the sequence into stage st
+        const int t = next_tile();
+        if (lane == 0) stile[st] = t;
+        issue_t(st, t);
     };
     {   // the LUT first (its own commit group, ahead of the ring in the SM's load queue)
         const int l16 = (lutsz + 1 + 15) / 16;
@@ -373,7 +391,7 @@ __global__ void __launch_bounds__(kFT, 1)
         }
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + 11] = fgtime();
         uint4* c4 = (uint4*)cntb;
-        const int n16 = (2 * kFT * (nslots + 2)) / 16;
+        const int n16 = (2 * kFT * (nslots + 1)) / 16;
         for (int i = tid; i < n16; i += kFT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + 12] = fgtime();
         if (tid == 0) {
@@ -467,11 +485,11 @@ __global__ void __launch_bounds__(kFT, 1)
     auto rare = [&](int c, int b, float a, float co, float sp, bool ok, int64_t idx) {
         const uint32_t gid = gbase + (uint32_t)idx;
         if (c == kFCodeFar) {
-            if (b < 1) {                      // negative length (clamped to the FAR code): invalid
-                n_bad++;
-                if (write_qid) A.qid_out[idx] = -1;
+            if (b < 1) {                      // negative length (clamped to the FAR code): invalid,
+                if (write_qid) A.qid_out[idx] = -1;   // already counted in the invalid row
                 return;
             }
+            atomicSub(cntw + nslots * (kFT / 2), cinc);      // not invalid after all
             const int q = bsearch(b);
             if (q >= 0) {
                 const float4 w = rec[2 * q];
@@ -482,6 +500,8 @@ __global__ void __launch_bounds__(kFT, 1)
             } else {
                 c = kFCodeGap;
             }
+        } else if (c == kFCodeGap) {
+            atomicSub(cntw + nslots * (kFT / 2), cinc);      // counted in the invalid row by the body
         }
         if (c == kFCodeGap) {
             const unsigned long long p = atomicAdd(&A.ctr->gap_count, 1ull);
@@ -506,15 +526,16 @@ __global__ void __launch_bounds__(kFT, 1)
     u64 skey[4] = {0ull, 0ull, 0ull, 0ull};
     int scode[4] = {kFCodeNone, kFCodeNone, kFCodeNone, kFCodeNone};
     int cur_st = 0;             // ring stage of the next tile
-    auto body = [&](auto full_tag, auto sample_tag, int64_t t, int st) {
+    auto body = [&](auto full_tag, auto sample_tag, auto wait_tag, int64_t t, int st) {
         constexpr bool FULL = decltype(full_tag)::value;
         constexpr bool SAMPLE = decltype(sample_tag)::value;
+        constexpr int WAIT = decltype(wait_tag)::value;          // pending groups allowed, -1: R - 1
         const int64_t i0 = t * kFTile + 4 * lane;
         int b[4];
         float a[4], co[4];
         int nv = 4;
         if (FULL) {
-            cp_async_wait_n(R - 1);
+            if (WAIT >= 0) cp_async_wait_n(WAIT); else cp_async_wait_n(R - 1);
             const int4 bv = ((const int4*)stage(st, 0))[lane];
             const float4 av = ((const float4*)stage(st, 1))[lane];
             float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -543,9 +564,10 @@ __global__ void __launch_bounds__(kFT, 1)
             const int c = (FULL || j < nv) ? (int)lut[min((unsigned)b[j], (unsigned)lutsz)] : kFCodeNone;
             code[j] = c;
             // member counter row straight from the code (no wait on the record load):
-            // rows 0..nslots-1 members, nslots invalid length, nslots+1 dummy
-            const int crow = c < nslots ? c : (c == kFCodeBad ? nslots : nslots + 1);
-            atomicAdd(cntw + crow * (kFT / 2), cinc);
+            // rows 0..nslots-1 members, nslots every other code (invalid length, and the
+            // FAR / GAP codes, which the rare path takes back out); padding uncounted
+            const int crow = min(c, nslots);
+            if (FULL || j < nv) atomicAdd(cntw + crow * (kFT / 2), cinc);
             const float4 w = rec[2 * c];
             const float4 r2 = rec[2 * c + 1];
             const bool ok = score_sp(b[j], a[j], co[j], HAS_COST, A.sp, w.x, w.y, w.z, &sp[j]);
@@ -606,13 +628,13 @@ __global__ void __launch_bounds__(kFT, 1)
         }
     };
     // process the tile in ring stage cur_st, refill the stage with the next tile
-    // of the sequence, advance; false when the sequence has ended
+    // of the sequence, advance; false when the sequence has ended (the sample tile)
     auto tile = [&](auto sample_tag) -> bool {
         const int st = cur_st;
-        const int64_t t = stile[st];
+        const int t = stile[st];
         if (t < 0) return false;
-        if (t < nfull) body(std::integral_constant<bool, true>(), sample_tag, t, st);
-        else body(std::integral_constant<bool, false>(), sample_tag, t, st);
+        if (t < nfull) body(std::true_type(), sample_tag, std::integral_constant<int, -1>(), t, st);
+        else body(std::false_type(), sample_tag, std::integral_constant<int, -1>(), t, st);
         __syncwarp();
         issue(st);
         cur_st = st + 1 == R ? 0 : st + 1;
@@ -783,19 +805,41 @@ __global__ void __launch_bounds__(kFT, 1)
     // streaming loads in flight, ~2 us)
     int rq = warp % max(nslots, 1);
     u64 gpoll = (lane == 0 && nslots > 0) ? __ldcg(&A.gthr[rq]) : 0ull;
-    for (int i = 1;; i++) {
-        if (*(volatile int*)&M->flag) collective();
-        if (!tile(std::integral_constant<bool, false>())) break;
-        if (i == chk) refresh();
-        if ((i & 3) == 0 && nslots > 0) {
-            if (lane == 0) {
-                if (gpoll) raise_thr(rq, gpoll);
-                rq += kFW;
-                if (rq >= nslots) rq = (rq - nslots) % nslots;
-                gpoll = __ldcg(&A.gthr[rq]);
+    // the streaming loop with the ring depth fixed at compile time: the tiles of the
+    // RR stages in registers (tq[0] = next), the cp.async wait an immediate
+    auto stream = [&](auto r_tag) {
+        constexpr int RR = decltype(r_tag)::value;
+        __syncwarp();
+        int tq[RR];
+#pragma unroll
+        for (int j = 0; j < RR; j++) tq[j] = stile[(cur_st + j) % RR];
+        int st = cur_st;
+        for (int i = 1;; i++) {
+            if (*(volatile int*)&M->flag) collective();
+            const int t = tq[0];
+            if (t < 0) break;
+            if (t < nfull) body(std::true_type(), std::false_type(), std::integral_constant<int, RR - 1>(), t, st);
+            else body(std::false_type(), std::false_type(), std::integral_constant<int, RR - 1>(), t, st);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j + 1 < RR; j++) tq[j] = tq[j + 1];
+            tq[RR - 1] = next_tile();
+            issue_t(st, tq[RR - 1]);
+            st = st + 1 == RR ? 0 : st + 1;
+            if (i == chk) refresh();
+            if ((i & 3) == 0 && nslots > 0) {
+                if (lane == 0) {
+                    if (gpoll) raise_thr(rq, gpoll);
+                    rq += kFW;
+                    if (rq >= nslots) rq = (rq - nslots) % nslots;
+                    gpoll = __ldcg(&A.gthr[rq]);
+                }
             }
         }
-    }
+    };
+    if (R == 2) stream(std::integral_constant<int, 2>());
+    else if (R == 3) stream(std::integral_constant<int, 3>());
+    else stream(std::integral_constant<int, 4>());
     // done: keep serving collectives until every warp is done (a flag raised by
     // this warp is handled before its ndone increment; ndone is read before the flag)
     __syncwarp();
