@@ -958,21 +958,33 @@ __global__ void __launch_bounds__(kFT, 1)
     // The fast merge's loads (this queue's rows, its bound) are issued together with
     // the gap-count check, so the common case pays one round trip, not two.
     const int q = cta;
-    const int rrow = tid % G, rpart = tid / G;
-    const bool ract = q < nslots && tid < 3 * G;     // 3 threads per row
-    const size_t rr = (size_t)q * G + rrow;
-    const u64* rk = A.rows.keys + rr * RC;
-    int nc = 0;
+    // 8 threads per row, 16 bytes each per load: a row's first 32 keys are two
+    // coalesced 128-byte segments (rows kFT/8 apart in two passes, G <= 2 * kFT/8)
+    constexpr int kRowT = 8, kRowsPass = kFT / kRowT;
+    const int t8 = tid & (kRowT - 1), rg = tid / kRowT;
+    int ncv[2] = {0, 0};
     u64 kv[8];
     unsigned long long mm = 0;
     u64 sk = 0ull;
-    if (ract) {
-        // one round trip: count, members and secondary and, speculatively, the first 24
-        // keys (masked by the count below; the rows were cut to the end-of-stream bound)
-        nc = __ldcg(&A.rows.cnt[rr]);
-        if (rpart == 0) { mm = (unsigned long long)__ldcg(&A.rows.members[rr]); sk = __ldcg(&A.rows.sec[rr]); }
 #pragma unroll
-        for (int u = 0; u < 8; u++) kv[u] = __ldcg(rk + rpart * 8 + u);
+    for (int ps = 0; ps < 2; ps++) {
+        const int rrow = rg + ps * kRowsPass;
+#pragma unroll
+        for (int u = 0; u < 4; u++) kv[4 * ps + u] = 0ull;
+        if (q < nslots && rrow < G) {
+            // one round trip: count, members and secondary and, speculatively, the first 32
+            // keys (masked by the count below; the rows were cut to the end-of-stream bound)
+            const size_t rr = (size_t)q * G + rrow;
+            ncv[ps] = __ldcg(&A.rows.cnt[rr]);
+            if (t8 == 0) { mm += (unsigned long long)__ldcg(&A.rows.members[rr]); const u64 s2 = __ldcg(&A.rows.sec[rr]); sk = s2 > sk ? s2 : sk; }
+            const ulonglong2* rk2 = (const ulonglong2*)(A.rows.keys + rr * RC);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const ulonglong2 v = __ldcg(rk2 + t8 + kRowT * h);
+                kv[4 * ps + 2 * h] = v.x;
+                kv[4 * ps + 2 * h + 1] = v.y;
+            }
+        }
     }
     u64 thr = q < nslots ? __ldcg(&A.gthr[q]) : 0ull;
     const unsigned long long graw = __ldcg(&A.ctr->gap_count);
@@ -1007,25 +1019,38 @@ __global__ void __launch_bounds__(kFT, 1)
                 if (mm) atomicAdd(&M->members, mm);
                 if (sk) atomicMax(&M->sec, sk);
             }
-            if (ract && rpart == 0 && nc) {
-                atomicAdd(&M->ncoll, nc);      // total candidates (ncoll reused)
-                atomicMax(&M->maxnc, nc);
-                rowoff[rrow + 1] = nc;         // counts for the prefix of the chunked path
+            if (t8 == 0) {
+#pragma unroll
+                for (int ps = 0; ps < 2; ps++) {
+                    const int rrow = rg + ps * kRowsPass, nc = ncv[ps];
+                    if (rrow >= G) continue;
+                    if (nc) {
+                        atomicAdd(&M->ncoll, nc);      // total candidates (ncoll reused)
+                        atomicMax(&M->maxnc, nc);
+                    }
+                    rowoff[rrow + 1] = nc;             // counts for the prefix of the chunked path
+                }
             }
-            if (ract && rpart == 0 && !nc) rowoff[rrow + 1] = 0;
             if (dbg && tid == 0) A.dbg[cta * kDbgStride + 22] = fgtime();
         }
         __syncthreads();
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + 20] = fgtime();
+        // SCORE head (the FIFO key's max): its request's fields, loaded now and used at the end
+        int h_len = 0;
+        float h_arr = 0.f, h_cost = 0.f;
+        if (SCORE && tid == 0 && M->sec) {
+            const int64_t li = (int64_t)key_gid(M->sec) - (int64_t)gbase;
+            h_len = __ldg(A.len + li);
+            h_arr = __ldg(A.arrival + li);
+            if (HAS_COST) h_cost = __ldg(A.cost + li);
+        }
         const int total = M->ncoll;
         int pn = 0;
-        if (M->maxnc <= 24) {                  // every row fully loaded already
-            if (ract) {
+        if (M->maxnc <= 2 * 2 * kRowT) {       // every row fully loaded already
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int j = rpart * 8 + u;
-                    if (j < nc && kv[u] && kv[u] >= thr) pool[atomicAdd(&M->pn, 1)] = kv[u];
-                }
+            for (int u = 0; u < 8; u++) {
+                const int ps = u >> 2, j = 2 * t8 + 2 * kRowT * ((u >> 1) & 1) + (u & 1);
+                if (j < ncv[ps] && kv[u] && kv[u] >= thr) pool[atomicAdd(&M->pn, 1)] = kv[u];
             }
             __syncthreads();
             pn = M->pn;
@@ -1088,10 +1113,20 @@ __global__ void __launch_bounds__(kFT, 1)
         if (pn <= 128) {
             // small pool: one counting pass ranks every candidate (keys are unique),
             // rank < K are the top K already in order -- no radix select, no sort
+            const int pn4 = (pn + 3) & ~3;
+            if (tid >= pn && tid < pn4) pool[tid] = 0ull;     // pad to a multiple of 4 with zeros
+            __syncthreads();
             const u64 k0 = tid < pn ? pool[tid] : 0ull;
             int r0 = 0;
-            if (tid < pn)
-                for (int j = 0; j < pn; j++) r0 += pool[j] > k0;
+            if (tid < pn) {
+                // 4 independent compare chains (broadcast 16-byte loads)
+                int r1 = 0, r2 = 0, r3 = 0;
+                for (int j = 0; j < pn4; j += 4) {
+                    const ulonglong2 x = *(const ulonglong2*)(pool + j), y = *(const ulonglong2*)(pool + j + 2);
+                    r0 += x.x > k0; r1 += x.y > k0; r2 += y.x > k0; r3 += y.y > k0;
+                }
+                r0 += r1 + r2 + r3;
+            }
             __syncthreads();
             if (tid < pn && r0 < K) surv[r0] = k0;
             __syncthreads();
@@ -1114,7 +1149,8 @@ __global__ void __launch_bounds__(kFT, 1)
         }
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + 18] = fgtime();
         const float qi = (float)(q + 1);
-        const float wb = P.wb[q], wu = P.wu[q], wf = P.wf[q];
+        const float4 wq = rec[2 * q];        // the staged weights (rec is untouched by the merge)
+        const float wb = wq.x, wu = wq.y, wf = wq.z;
         auto payload = [&](u64 k) -> float {   // s' of the request with key k
             if (SCORE) return key_sp(k);
             const int64_t li = (int64_t)key_gid(k) - (int64_t)gbase;
@@ -1140,10 +1176,8 @@ __global__ void __launch_bounds__(kFT, 1)
             if (members == 0 || ns == 0) {
                 A.head_id[q] = -1; A.head_score[q] = 0.f; A.max_score[q] = 0.f;
             } else if (SCORE) {
-                const int64_t li = (int64_t)key_gid(sec) - (int64_t)gbase;
                 float s = 0.f;
-                score_sp(__ldg(A.len + li), __ldg(A.arrival + li), HAS_COST ? __ldg(A.cost + li) : 0.f, HAS_COST,
-                         A.sp, wb, wu, wf, &s);
+                score_sp(h_len, h_arr, h_cost, HAS_COST, A.sp, wb, wu, wf, &s);
                 A.head_id[q] = (int64_t)key_gid(sec);
                 A.head_score[q] = qi * s;
                 A.max_score[q] = qi * key_sp(surv[0]);
