@@ -890,6 +890,7 @@ __global__ void __launch_bounds__(kFT, 1)
         if (lane == 0) rcnt[q] = wpos;
     }
     __syncthreads();
+    if (dbg && tid == 0) A.dbg[cta * kDbgStride + 28] = fgtime();
     // ---- per-CTA rows: count (<= RC, no overflow pending), members, secondary
     for (int q = warp; q < nslots; q += kFW) {
         const uint32_t* c32 = (const uint32_t*)(cntb + (size_t)q * kFT * 2);
@@ -904,6 +905,7 @@ __global__ void __launch_bounds__(kFT, 1)
             A.rows.sec[r] = sec64[q];
         }
     }
+    if (dbg && tid == 0) A.dbg[cta * kDbgStride + 29] = fgtime();
     {
         // invalid lengths (counter row nslots) + excluded + diagnostics
         unsigned long long bad = n_bad;
@@ -934,6 +936,7 @@ __global__ void __launch_bounds__(kFT, 1)
     }
     (void)n_gap;
     __syncthreads();
+    if (dbg && tid == 0) A.dbg[cta * kDbgStride + 30] = fgtime();
     if (tid == 0) __threadfence();   // cumulative over the CTA's writes ordered by the bar.sync (as a grid sync)
     stamp(5);
     if (A.merge == 0) return;
@@ -1047,11 +1050,28 @@ __global__ void __launch_bounds__(kFT, 1)
         const int total = M->ncoll;
         int pn = 0;
         if (M->maxnc <= 2 * 2 * kRowT) {       // every row fully loaded already
+            // one shared atomic per warp (a single counter hit by every passing key
+            // serialised ~100 atomics, ~1 us)
+            unsigned pmask = 0u;
 #pragma unroll
             for (int u = 0; u < 8; u++) {
                 const int ps = u >> 2, j = 2 * t8 + 2 * kRowT * ((u >> 1) & 1) + (u & 1);
-                if (j < ncv[ps] && kv[u] && kv[u] >= thr) pool[atomicAdd(&M->pn, 1)] = kv[u];
+                pmask |= (j < ncv[ps] && kv[u] && kv[u] >= thr) ? (1u << u) : 0u;
             }
+            const int c = __popc(pmask);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int wbase = 0;
+            if (lane == 31 && incl) wbase = atomicAdd(&M->pn, incl);
+            wbase = __shfl_sync(0xffffffffu, wbase, 31);
+            int o = wbase + incl - c;
+#pragma unroll
+            for (int u = 0; u < 8; u++)
+                if (pmask & (1u << u)) pool[o++] = kv[u];
             __syncthreads();
             pn = M->pn;
             __syncthreads();
@@ -1113,22 +1133,28 @@ __global__ void __launch_bounds__(kFT, 1)
         if (pn <= 128) {
             // small pool: one counting pass ranks every candidate (keys are unique),
             // rank < K are the top K already in order -- no radix select, no sort
-            const int pn4 = (pn + 3) & ~3;
-            if (tid >= pn && tid < pn4) pool[tid] = 0ull;     // pad to a multiple of 4 with zeros
+            // 4 threads per candidate (768 threads: up to 192), each counting the keys
+            // above it in every 4th 16-byte pair, 2 loads in flight; pool padded with zeros
+            const int pn8 = (pn + 7) & ~7;
+            if (tid >= pn && tid < pn8) pool[tid] = 0ull;
             __syncthreads();
-            const u64 k0 = tid < pn ? pool[tid] : 0ull;
+            const int ci = tid >> 2, part = tid & 3;
+            const u64 k0 = ci < pn ? pool[ci] : 0ull;
             int r0 = 0;
-            if (tid < pn) {
-                // 4 independent compare chains (broadcast 16-byte loads)
-                int r1 = 0, r2 = 0, r3 = 0;
-                for (int j = 0; j < pn4; j += 4) {
-                    const ulonglong2 x = *(const ulonglong2*)(pool + j), y = *(const ulonglong2*)(pool + j + 2);
-                    r0 += x.x > k0; r1 += x.y > k0; r2 += y.x > k0; r3 += y.y > k0;
+            if (ci < pn) {
+                int r1 = 0;
+                for (int j = 2 * part; j < pn8; j += 16) {
+                    const ulonglong2 x = *(const ulonglong2*)(pool + j);
+                    const ulonglong2 y = *(const ulonglong2*)(pool + j + 8);
+                    r0 += (x.x > k0) + (x.y > k0);
+                    r1 += (j + 8 < pn8) ? (y.x > k0) + (y.y > k0) : 0;
                 }
-                r0 += r1 + r2 + r3;
+                r0 += r1;
             }
+            r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
+            r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
             __syncthreads();
-            if (tid < pn && r0 < K) surv[r0] = k0;
+            if (ci < pn && part == 0 && r0 < K) surv[r0] = k0;
             __syncthreads();
         } else {
             auto fe = [&](auto f) { for (int j = tid; j < pn; j += kFT) f(pool[j]); };
