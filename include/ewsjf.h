@@ -354,6 +354,16 @@ ewsjf_status ewsjf_tick_host(ewsjf_ctx *ctx, const int32_t *h_len, const float *
  * shard's gap requests (capacity-bounded).  The caller all-gathers the
  * records of all ranks (NCCL over NVLink) and calls ewsjf_tick_merge.       */
 int64_t      ewsjf_exchange_bytes(const ewsjf_ctx *ctx, int32_t n_queues, int32_t k);
+/* Capacity of the gap-request section of this ctx's exchange records (App. D:
+ * the requests of a shard whose length falls between queues, P:322-325 and
+ * P:788-808).  Each record carries the shard's gap count plus up to gap_cap
+ * entries (default 1024); ewsjf_exchange_bytes grows by 16 bytes per entry.
+ * Size it for the expected novel lengths per shard (a shard of n requests
+ * needs at most n).  A merge whose shards held more gap requests than the
+ * capacity returns CAPACITY (the overflowing requests keep qid -2).
+ * Strategic call: synchronises the ctx stream and, with a communicator
+ * attached, reallocates the exchange buffers.  INVALID_ARG outside [1, 2^26]. */
+ewsjf_status ewsjf_ctx_set_exchange_gap_cap(ewsjf_ctx *ctx, int32_t gap_cap);
 ewsjf_status ewsjf_tick_local(ewsjf_ctx *ctx, const int32_t *d_len, const float *d_arrival, const float *d_cost,
                               int64_t n, int64_t global_base, const ewsjf_partition_t *part,
                               const ewsjf_meta *theta, const ewsjf_select_params *params,

@@ -104,7 +104,7 @@ SYMBOLS = [
     "ewsjf_ctx_get_phases", "ewsjf_batch_build", "ewsjf_prune_empty",
     "ewsjf_history_hist", "ewsjf_partition_from_hist", "ewsjf_online_adjust",
     "ewsjf_nccl_get_unique_id", "ewsjf_ctx_init_nccl", "ewsjf_ctx_attach_nccl", "ewsjf_ctx_detach_nccl",
-    "ewsjf_diag_ffma_rate", "ewsjf_ctx_reserve_sweep", "ewsjf_alloc_count",
+    "ewsjf_diag_ffma_rate", "ewsjf_ctx_reserve_sweep", "ewsjf_alloc_count", "ewsjf_ctx_set_exchange_gap_cap",
 ]
 
 _lib = None
@@ -157,6 +157,7 @@ def load() -> C.CDLL:
     L.ewsjf_ctx_detach_nccl.argtypes = [V]
     L.ewsjf_diag_ffma_rate.argtypes = [V, P(C.c_double)]
     L.ewsjf_ctx_reserve_sweep.argtypes = [V, I64]
+    L.ewsjf_ctx_set_exchange_gap_cap.argtypes = [V, I32]
     L.ewsjf_alloc_count.argtypes = []
     L.ewsjf_alloc_count.restype = I64
     for name in SYMBOLS:

@@ -485,6 +485,7 @@ static MergeArgs merge_args(ewsjf_ctx* ctx, const ewsjf_partition_t* part, const
     M.nq = part->n;
     M.next_id = part->next_id;
     M.bubble_width = bubble_width;
+    M.ex_gap = ctx->ex_gap;
     M.sp = sp ? score_params(sp) : ScoreParams{0.f, 0.f, 0.f, 0.f, 0, 1};
     if (theta) {
         M.theta[0] = theta->a_b; M.theta[1] = theta->b_b; M.theta[2] = theta->a_u;
@@ -791,9 +792,8 @@ extern "C" ewsjf_status ewsjf_route(ewsjf_ctx* ctx, const int32_t* d_len, int64_
 
 // ---------------------------------------------------------- sharded tick ---
 extern "C" int64_t ewsjf_exchange_bytes(const ewsjf_ctx* ctx, int32_t n_queues, int32_t k) {
-    (void)ctx;
     if (n_queues < 0 || n_queues > EWSJF_MAX_QUEUES || k < 1 || k > EWSJF_MAX_K) return -1;
-    return ex_layout(n_queues, k).total;
+    return ex_layout(n_queues, k, ctx ? ctx->ex_gap : kExGapDefault).total;
 }
 
 static ewsjf_status local_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arrival, const float* d_cost,
@@ -812,7 +812,7 @@ static ewsjf_status local_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float
     ewsjf_weights_from_meta(theta, part, w);
     static thread_local Policy P;
     fill_policy(part, w, &P);
-    CU(cudaMemsetAsync(d_exchange, 0, ex_layout(part->n, sp->k).total, ctx->stream));
+    CU(cudaMemsetAsync(d_exchange, 0, ex_layout(part->n, sp->k, ctx->ex_gap).total, ctx->stream));
     MergeArgs M = merge_args(ctx, part, sp, theta, 1);
     M.in_mode = MERGE_IN_ROWS;
     M.out_mode = MERGE_OUT_EXCHANGE;
@@ -862,7 +862,7 @@ static ewsjf_status merge_impl(ewsjf_ctx* ctx, const void* d_exchange_all, int32
     M.out_mode = MERGE_OUT_FINAL;
     M.ex_in = (const unsigned char*)d_exchange_all;
     M.world = world;
-    M.ex_bytes = ex_layout(part->n, sp->k).total;
+    M.ex_bytes = ex_layout(part->n, sp->k, ctx->ex_gap).total;
     M.gbase = (uint32_t)global_base;
     M.n_local = n_local;
     M.qid = d_qid_local;
@@ -900,7 +900,7 @@ static ewsjf_status sharded_impl(ewsjf_ctx* ctx, const int32_t* d_len, const flo
     if ((s = check_select(ctx, sp)) != EWSJF_OK) return s;
     if ((s = check_out(ctx, out)) != EWSJF_OK) return s;
     if (sp->k > ctx->max_k) return fail(ctx, EWSJF_ERR_INVALID_ARG, "k > ctx max_k");
-    const int64_t bytes = ex_layout(part->n, sp->k).total;
+    const int64_t bytes = ex_layout(part->n, sp->k, ctx->ex_gap).total;
     if (bytes > ctx->ex_cap) return fail(ctx, EWSJF_ERR_CAPACITY, "exchange record %lld > %lld", (long long)bytes,
                                          (long long)ctx->ex_cap);
     if ((s = local_impl(ctx, d_len, d_arr, d_cost, n, gbase, part, theta, sp, d_qid_out, ctx->ex_local)) != EWSJF_OK)

@@ -79,6 +79,7 @@ struct ewsjf_ctx {
     unsigned char* ex_local = nullptr;
     unsigned char* ex_all = nullptr;
     int64_t ex_cap = 0;
+    int32_t ex_gap = 1024;              // gap entries per exchange record (ewsjf_ctx_set_exchange_gap_cap)
     // batch builder prefix scratch (batch.cu)
     uint32_t* d_bpre = nullptr;
     int64_t bpre_cap = 0;

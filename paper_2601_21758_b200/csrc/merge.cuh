@@ -140,7 +140,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
     float* ssp = (float*)(smem + L.ssp);
     MMisc* M = (MMisc*)(smem + L.misc);
     const int nq = A.nq, K = A.K;
-    const ExLayout X = ex_layout(nq, K);
+    const ExLayout X = ex_layout(nq, K, A.ex_gap);
     const bool is_score = A.sp.mode == EWSJF_SELECT_SCORE;
 
     // ---------------- gap list size (virtual index v = position in the concatenation
@@ -153,7 +153,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         for (int r = 0; r < A.world; r++) {
             const long long c = ((const ExHeader*)(A.ex_in + (int64_t)r * A.ex_bytes))->gap_count;
             graw += c;
-            gcount += c < kExGap ? c : kExGap;
+            gcount += c < X.gap_cap ? c : X.gap_cap;
         }
     }
     if (gcount > A.gap_cap) gcount = A.gap_cap;
@@ -164,7 +164,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
         int r = 0;
         for (; r < A.world; r++) {
             long long c = ((const ExHeader*)(A.ex_in + (int64_t)r * A.ex_bytes))->gap_count;
-            c = c < kExGap ? c : kExGap;
+            c = c < X.gap_cap ? c : X.gap_cap;
             if ((long long)v < acc + c) break;
             acc += c;
         }
@@ -621,7 +621,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
     if (IN == MERGE_IN_ROWS && OUT == MERGE_OUT_ROUTE)
         for (int i = blockIdx.x * NT + tid; i < nq; i += gridDim.x * NT) A.gthr[i] = 0ull;
     if (OUT == MERGE_OUT_EXCHANGE && blockIdx.x == 0) {   // header + gap entries of this rank
-        const int ng = (int)(graw < kExGap ? graw : kExGap);
+        const int ng = (int)(graw < X.gap_cap ? graw : X.gap_cap);
         for (int i = tid; i < ng; i += NT) ((GapEntry*)(A.ex_out + X.gaps))[i] = A.gap[i];
         if (tid == 0) {
             ExHeader* h = (ExHeader*)(A.ex_out + X.hdr);

@@ -50,7 +50,7 @@ static NcclApi& nccl_api() {
 
 // Exchange buffers for the largest record this ctx can produce (256 queues x max_k).
 static ewsjf_status alloc_exchange(ewsjf_ctx* ctx, int world) {
-    const int64_t per = ex_layout(kMaxSlots, ctx->max_k).total;
+    const int64_t per = ex_layout(kMaxSlots, ctx->max_k, ctx->ex_gap).total;
     if (cudaMalloc(&ctx->ex_local, per) != cudaSuccess ||
         cudaMalloc(&ctx->ex_all, per * world) != cudaSuccess)
         return fail(ctx, EWSJF_ERR_CUDA, "exchange buffers (%lld x %d bytes)", (long long)per, world);
@@ -124,6 +124,22 @@ extern "C" ewsjf_status ewsjf_ctx_attach_nccl(ewsjf_ctx* ctx, void* nccl_comm, i
     ewsjf_status s = alloc_exchange(ctx, world);
     if (s != EWSJF_OK) nccl_release(ctx);
     return s;
+}
+
+extern "C" ewsjf_status ewsjf_ctx_set_exchange_gap_cap(ewsjf_ctx* ctx, int32_t gap_cap) {
+    if (!ctx) return EWSJF_ERR_INVALID_ARG;
+    if (gap_cap < 1 || gap_cap > (1 << 26)) return fail(ctx, EWSJF_ERR_INVALID_ARG, "gap_cap out of [1, 2^26]");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ctx->ex_gap = gap_cap;
+    if (ctx->ex_local) {               // an attached communicator: its buffers follow the new record size
+        cudaFree(ctx->ex_local);
+        cudaFree(ctx->ex_all);
+        ctx->ex_local = ctx->ex_all = nullptr;
+        ctx->ex_cap = 0;
+        return alloc_exchange(ctx, ctx->nccl_world);
+    }
+    return EWSJF_OK;
 }
 
 extern "C" ewsjf_status ewsjf_ctx_detach_nccl(ewsjf_ctx* ctx) {

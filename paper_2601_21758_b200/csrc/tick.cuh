@@ -133,11 +133,11 @@ struct ExLayout {
     int64_t hdr, members, sec, sec_sp, cnt, keys, sp, gaps, total;
     int32_t nq, k, gap_cap;
 };
-constexpr int kExGap = 1024;
-__host__ __device__ inline ExLayout ex_layout(int nq, int k) {
+constexpr int kExGapDefault = 1024;   // gap entries per record unless the ctx sets another capacity
+__host__ __device__ inline ExLayout ex_layout(int nq, int k, int gap_cap) {
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
     ExLayout L;
-    L.nq = nq; L.k = k; L.gap_cap = kExGap;
+    L.nq = nq; L.k = k; L.gap_cap = gap_cap;
     int64_t o = 0;
     L.hdr = o;      o = al(o + 64);
     L.members = o;  o = al(o + 8 * (int64_t)nq);
@@ -146,7 +146,7 @@ __host__ __device__ inline ExLayout ex_layout(int nq, int k) {
     L.cnt = o;      o = al(o + 4 * (int64_t)nq);
     L.keys = o;     o = al(o + 8 * (int64_t)nq * k);
     L.sp = o;       o = al(o + 4 * (int64_t)nq * k);
-    L.gaps = o;     o = al(o + (int64_t)sizeof(GapEntry) * kExGap);
+    L.gaps = o;     o = al(o + (int64_t)sizeof(GapEntry) * gap_cap);
     L.total = o;
     return L;
 }
@@ -189,6 +189,7 @@ struct MergeArgs {
     const unsigned char* ex_in; // world records
     int32_t world;
     int64_t ex_bytes;
+    int32_t ex_gap;             // gap entries per exchange record (ctx->ex_gap)
     // --- outputs
     unsigned char* ex_out;      // out_mode EXCHANGE: this rank's record
     int64_t* topk_id;

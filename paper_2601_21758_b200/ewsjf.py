@@ -101,6 +101,10 @@ class Context:
         self.check(self.lib.ewsjf_diag_ffma_rate(self.h, C.byref(r)), (L.OK,))
         return r.value
 
+    def set_exchange_gap_cap(self, gap_cap: int):
+        """Gap entries per exchange record (ewsjf_ctx_set_exchange_gap_cap; default 1024)."""
+        self.check(self.lib.ewsjf_ctx_set_exchange_gap_cap(self.h, int(gap_cap)), (L.OK,))
+
     def detach_nccl(self):
         self.check(self.lib.ewsjf_ctx_detach_nccl(self.h), (L.OK,))
         self.nccl_world = 0

@@ -39,6 +39,7 @@ def test_library_loads_and_host_calls_work(lib):
     assert L.ewsjf_status_str(4) == b"capacity exceeded"
     assert L.ewsjf_exchange_bytes(None, 33, 64) > 0
     assert L.ewsjf_exchange_bytes(None, 300, 64) == -1
+    assert L.ewsjf_ctx_set_exchange_gap_cap(None, 4096) == 1          # INVALID_ARG without a ctx
     # A7 on the host (no GPU): w = fp32(max(0, a*mean + b))
     p = lib.Partition()
     p.n = 2

@@ -318,3 +318,50 @@ def test_tick_full_size_with_holes(E, orc, ctx_full, mode):
     g, ref, phi = _run_both(E, orc, ctx_full, pool, hole, 64, mode)
     assert g["n_gap"] >= 100_000, g["n_gap"]
     _check(g, ref, phi, pool, mode, 64)
+
+
+def test_sharded_tick_with_holes_at_pool_scale(E, orc, ctx_full):
+    """App. D across shards: the 10M C3 pool with five hole
+    ranges (>= 1% of the requests fall between queues), split over 2 simulated
+    ranks whose exchange records carry all of their gap requests (the record's
+    gap capacity raised with ewsjf_ctx_set_exchange_gap_cap).  The merge runs
+    Alg. 2 over the union in global index order: qids, bubbles and selections
+    equal the oracle's single-pool tick."""
+    s, opart, _ = orc.partition(workload.heavy(1_000_000, 301))
+    qs = opart.queues()
+    keep = [q for i, q in enumerate(qs) if i not in (5, 11, 17, 23, len(qs) - 3)]
+    hole = orc.make_partition([(q["min_len"], q["max_len"]) for q in keep], means=[q["mean"] for q in keep])
+    pool = workload.pool("heavy", 10_000_000, 302)
+    n, world, K, mode = len(pool["len"]), 2, 64, 0
+    theta, sp = E.meta(**THETA0), E.select_params(k=K, mode=mode)
+    dev = {k: torch.from_numpy(pool[k]).cuda() for k in ("len", "arrival", "cost")}
+    qid = torch.full((n,), -7, dtype=torch.int32, device="cuda")
+    small = E.exchange_bytes(ctx_full, hole.n, K)
+    ctx_full.set_exchange_gap_cap(n // world + 1)
+    try:
+        assert E.exchange_bytes(ctx_full, hole.n, K) > small
+        recs, bounds = [], []
+        for r in range(world):
+            lo, hi = workload.shard_range(n, r, world)
+            bounds.append((lo, hi))
+            recs.append(E.tick_local(ctx_full, dev["len"][lo:hi], dev["arrival"][lo:hi], dev["cost"][lo:hi], lo,
+                                     to_gpu_partition(E, hole), theta, sp, qid_out=qid[lo:hi]).clone())
+        allx = torch.cat(recs)
+        ref = orc.tick(pool["len"], pool["arrival"], pool["cost"], hole, orc.meta(**THETA0),
+                       orc.select_params(k=K, mode=mode))
+        phi, _ = orc.score_all(pool["len"], pool["arrival"], pool["cost"], ref["qid"], ref["partition"],
+                               orc.meta(**THETA0), orc.select_params(k=K, mode=mode))
+        gs = []
+        for r, (lo, hi) in enumerate(bounds):      # each rank finalises its own shard's gap qids
+            gp = to_gpu_partition(E, hole)
+            out = E.tick_merge(ctx_full, allx, world, lo, hi - lo, qid[lo:hi], gp, theta, sp)
+            g = gpu_result(out)
+            g["part"] = gp
+            gs.append(g)
+        full = qid.cpu().numpy()
+        for g in gs:
+            g["qid"] = full
+            assert g["n_gap"] >= 100_000, g["n_gap"]
+            _check(g, ref, phi, pool, mode, K)
+    finally:
+        ctx_full.set_exchange_gap_cap(1024)
