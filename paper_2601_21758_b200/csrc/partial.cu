@@ -357,6 +357,7 @@ __device__ __forceinline__ void partial_phase(const PartialArgs& A, const Policy
                     const unsigned v = ok[j] ? (unsigned)c : 0xffffffffu;
                     const unsigned peers = __match_any_sync(0xffffffffu, v);
                     if (ok[j] && lane == __ffs(peers) - 1) s_cntw[warp * nslots + c] += __popc(peers);
+                    __syncwarp();      // the next slot's leader may update the same counter
                 }
             }
         }
