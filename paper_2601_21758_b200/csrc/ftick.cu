@@ -379,9 +379,7 @@ __global__ void __launch_bounds__(kFT, 1)
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    // the sample tile alone first: the critical path (sample -> board -> bound) waits
-    // on it, the rest of the ring prologue is not needed before the bound
-    issue(0);
+    for (int i = 0; i < R; i++) issue(i);
     __syncwarp();
     stamp(10);
 
@@ -401,7 +399,7 @@ __global__ void __launch_bounds__(kFT, 1)
             M->members = 0ull; M->sec = 0ull; M->tcoll = 0ull;
             M->agg[0] = M->agg[1] = M->agg[2] = 0ull;
         }
-        cp_async_wait_n(1);            // this thread's LUT / policy chunks (the oldest group) have landed
+        cp_async_wait_n(R);            // this thread's LUT / policy chunks (the oldest group) have landed
     }
     __syncthreads();
     {
@@ -681,9 +679,7 @@ __global__ void __launch_bounds__(kFT, 1)
     };
 
     // ---- sample tile, board, bound
-    cp_async_wait_n(0);                // the sample tile has landed: now the rest of the prologue
     if (dbg && tid == 0) A.dbg[cta * kDbgStride + 25] = fgtime();
-    for (int i = 1; i < R; i++) issue(i);
     tile(std::integral_constant<bool, true>());
     if (dbg && tid == 0) A.dbg[cta * kDbgStride + 26] = fgtime();
     if (lane == 0 && ndyn > 0 && S0 > R) nbase = atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim);
