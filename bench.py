@@ -231,7 +231,8 @@ def run_sweep(E, ctx, dev, args, rank=0, ws=1, group=None):
                          "frac": achieved / peak,
                          "peak_source": "measured: ewsjf_diag_ffma_rate (FFMA throughput microbenchmark) / "
                                         "4 fp32-pipe instructions per pair", "ffma_per_s": ffma},
-            "candidates_inserted_last_sweep": tm["candidates_inserted"]}
+            "candidates_inserted_last_sweep": tm["candidates_inserted"],
+            "records_after_prefilter": tm["sweep_records"]}
 
 
 def run_batch(E, ctx, part, theta, copies, dev, n, max_req=256, max_tok=65536, reps=20):

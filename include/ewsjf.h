@@ -118,6 +118,8 @@ typedef struct {
     int64_t compactions;           /* per-queue filters, and per-queue buffer compactions   */
     int64_t batch_launches;        /* ewsjf_batch_build kernels                             */
     double  batch_ms;
+    int64_t sweep_records;         /* records the last sweep's select passes read (after the
+                                      Θ-independent prefilter when it ran), 0 if none ran  */
 } ewsjf_timing;
 ewsjf_status ewsjf_ctx_set_timing(ewsjf_ctx *ctx, int32_t enable);
 ewsjf_status ewsjf_ctx_get_timing(ewsjf_ctx *ctx, ewsjf_timing *out);

@@ -79,7 +79,7 @@ class Timing(C.Structure):
                 ("merge_launches", C.c_int64), ("partition_launches", C.c_int64), ("sweep_launches", C.c_int64),
                 ("tick_ms", C.c_double), ("merge_ms", C.c_double), ("partition_ms", C.c_double),
                 ("sweep_ms", C.c_double), ("candidates_inserted", C.c_int64), ("compactions", C.c_int64),
-                ("batch_launches", C.c_int64), ("batch_ms", C.c_double)]
+                ("batch_launches", C.c_int64), ("batch_ms", C.c_double), ("sweep_records", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}

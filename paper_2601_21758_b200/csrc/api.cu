@@ -22,7 +22,7 @@ int64_t stream_smem_bytes(bool has_cost, int lut_size, int nslots, int cap, int 
 cudaError_t launch_ftick(const FArgs& A, const Policy* P, const MergeArgs& MA, bool has_cost, int grid,
                          cudaStream_t st);
 int64_t ftick_smem_bytes(bool has_cost, int lut_size, int nslots, int stages);
-bool sweep_diag(ewsjf_ctx* ctx, unsigned long long* cuts_inserts);
+bool sweep_diag(ewsjf_ctx* ctx, unsigned long long* cuts_inserts, long long* records);
 ewsjf_status nccl_allgather(ewsjf_ctx* ctx, int64_t bytes);
 void nccl_release(ewsjf_ctx* ctx);
 }  // namespace ewsjf
@@ -217,7 +217,12 @@ extern "C" ewsjf_status ewsjf_ctx_get_timing(ewsjf_ctx* ctx, ewsjf_timing* out) 
     out->candidates_inserted = (int64_t)c.dbg_inserted;
     out->compactions = (int64_t)c.dbg_compactions;
     unsigned long long sw[2] = {0, 0};
-    if (sweep_diag(ctx, sw)) { out->candidates_inserted += (int64_t)sw[1]; out->compactions += (int64_t)sw[0]; }
+    long long recs = 0;
+    if (sweep_diag(ctx, sw, &recs)) {
+        out->candidates_inserted += (int64_t)sw[1];
+        out->compactions += (int64_t)sw[0];
+        out->sweep_records = recs;
+    }
     out->launches = ctx->launches;
     out->recorded = (int64_t)ctx->ev_n;
     for (size_t i = 0; i < ctx->ev_n; i++) {

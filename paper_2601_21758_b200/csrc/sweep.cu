@@ -42,6 +42,7 @@ constexpr int kSkyBins = 1 << 16;
 constexpr int kSkyBlk = 64;
 constexpr int kSkyMaxBlocks = kSkyBins / kSkyBlk + kMaxSlots + 1;
 constexpr int kSkyMaxK = 32;
+constexpr int kSwDirectMax = 4096;  // K5d: one warp per (Θ, queue) scans its queue's survivors directly
 
 struct SweepScratch {
     int64_t n_cap = 0;              // records capacity
@@ -76,8 +77,11 @@ struct SweepScratch {
     int32_t* cpre2 = nullptr;       // [257]
     int32_t* qfill2 = nullptr;      // [256]
     int64_t* qcnt2 = nullptr;       // [256]
+    int32_t* direct = nullptr;      // [1] 1: the prefilter left <= kSwDirectMax records per queue (K5d path)
     size_t attr_smem = 0;           // select kernel: dynamic smem attribute set for this ctx's device
     int occ = 1;
+    int last_nq = 0;                // diagnostics: the last sweep's queue count and record offsets used
+    bool last_sky = false;
 };
 
 struct SweepArgs {
@@ -475,6 +479,9 @@ __global__ void sky_plan_kernel(const __grid_constant__ SweepArgs A) {
     }
     A.s.qoff2[A.nq] = off;
     A.s.cpre2[A.nq] = cp;
+    int64_t mx = 0;
+    for (int q = 0; q < A.nq; q++) mx = A.s.qcnt2[q] > mx ? A.s.qcnt2[q] : mx;
+    *A.s.direct = mx <= kSwDirectMax;
 }
 __global__ void __launch_bounds__(kSwPrepThreads) sky_compact_kernel(const __grid_constant__ SweepArgs A) {
     const int64_t ntot = A.s.qoff[A.nq];
@@ -488,6 +495,7 @@ __global__ void __launch_bounds__(kSwPrepThreads) sky_compact_kernel(const __gri
 // K4: persistent warps over tasks (Θ block, queue, chunk).
 __global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const __grid_constant__ SweepArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
+    if (*A.s.direct) return;                      // K5d handles this sweep
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int cap = A.cap, K = A.K;
     u64* buf = (u64*)smem + (size_t)warp * kSwT * cap;           // [kSwT][cap]
@@ -698,6 +706,7 @@ struct SweepOutArgs {
 // K5: one warp per (Θ, queue): merge the rows of the queue's chunks.
 __global__ void __launch_bounds__(kSwWarps * 32) sweep_merge_kernel(const __grid_constant__ SweepOutArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
+    if (*A.s.direct) return;                      // K5d handles this sweep
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int cap = A.cap, K = A.K;
     u64* bb = (u64*)smem + (size_t)warp * cap;
@@ -765,6 +774,68 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_merge_kernel(const __grid
     }
 }
 
+// K5d (after the prefilter, <= kSwDirectMax survivors per queue, K <= 32): one warp
+// per (Θ, queue) scores the queue's survivors 32 at a time, bitonic-sorts each
+// chunk across the lanes and merges it into the running top 32 (one key per lane,
+// descending: the elementwise max of the list and the reversed chunk is bitonic,
+// a 5-step merge sorts it).  Same keys and outputs as K4 + K5.
+__device__ __forceinline__ u64 sw_bitonic_step(u64 v, int lane, int j, bool up) {
+    const u64 o = shfl_xor_u64(v, j);
+    const bool keep_max = ((lane & j) == 0) == up;
+    return keep_max ? (o > v ? o : v) : (o < v ? o : v);
+}
+__global__ void __launch_bounds__(kSwWarps * 32) sweep_direct_kernel(const __grid_constant__ SweepOutArgs A) {
+    if (!*A.s.direct) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int item = blockIdx.x * kSwWarps + warp;
+    if (item >= A.n_theta * A.nq) return;
+    const int th = item / A.nq, q = item % A.nq;
+    const int K = A.K;
+    const float* w = A.s.w + ((size_t)th * kMaxSlots + q) * 3;
+    const float w0 = w[0], w1 = w[1], w2 = w[2];
+    const int64_t b0 = A.s.qoff[q], b1 = A.s.qoff[q + 1];
+    u64 top = 0ull;                                   // lane i: the (i+1)-th best key so far
+    for (int64_t e0 = b0; e0 < b1; e0 += 32) {
+        const int64_t e = e0 + lane;
+        u64 v = 0ull;
+        if (e < b1) {
+            const float4 f = __ldg(&A.s.rec[e]);
+            v = score_key(fmaf(w2, f.z, fmaf(w1, f.y, w0 * f.x)), __float_as_uint(f.w));
+        }
+        const u64 kth = __shfl_sync(0xffffffffu, top, K - 1);
+        if (!__any_sync(0xffffffffu, v > kth)) continue;
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) v = sw_bitonic_step(v, lane, j, (lane & k) == 0 || k == 32);
+        const u64 r = shfl_xor_u64(v, 31);            // the chunk reversed (ascending)
+        top = r > top ? r : top;                      // bitonic: the best 32 of both
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) top = sw_bitonic_step(top, lane, j, true);
+    }
+    const ewsjf_select_out& o = A.outs[th];
+    const float qi = (float)(q + 1);
+    const int n = __popc(__ballot_sync(0xffffffffu, top != 0ull));
+    if (lane < K) {
+        const bool has = lane < n;
+        o.d_topk_id[(size_t)q * K + lane] = has ? (int64_t)key_gid(top) : -1;
+        o.d_topk_score[(size_t)q * K + lane] = has ? qi * key_sp(top) : 0.f;
+    }
+    if (lane == 0) {
+        const int64_t cnt = A.s.qcount[q];
+        o.d_count[q] = cnt;
+        if (cnt == 0 || n == 0) {
+            o.d_head_id[q] = -1; o.d_head_score[q] = 0.f; o.d_max_score[q] = 0.f;
+        } else {
+            const float4 hf = A.s.headf[q];
+            const float hs = fmaf(w2, hf.z, fmaf(w1, hf.y, w0 * hf.x));
+            o.d_head_id[q] = (int64_t)key_gid(A.s.head[q]);
+            o.d_head_score[q] = qi * hs;
+            o.d_max_score[q] = qi * key_sp(top);
+        }
+    }
+}
+
 // K6: one warp per Θ: Alg. 1 ArgMax over non-empty queues (ties -> lowest position, R24).
 __global__ void sweep_summary_kernel(const __grid_constant__ SweepOutArgs A) {
     const int th = blockIdx.x;
@@ -794,7 +865,7 @@ __global__ void sweep_summary_kernel(const __grid_constant__ SweepOutArgs A) {
 void sweep_free(ewsjf_ctx* ctx) {
     SweepScratch* S = ctx->sw;
     if (!S) return;
-    void* d[] = {S->lentop, S->lenid, S->blkid, S->qidk, S->bcnt, S->bfill, S->srt, S->cand, S->blktop, S->pref, S->rec2, S->qoff2, S->cpre2, S->qfill2,
+    void* d[] = {S->direct, S->lentop, S->lenid, S->blkid, S->qidk, S->bcnt, S->bfill, S->srt, S->cand, S->blktop, S->pref, S->rec2, S->qoff2, S->cpre2, S->qfill2,
                  S->qcnt2, S->rec, S->qcount, S->qoff, S->cpre, S->qfill, S->head, S->headf, S->bad, S->task_ctr, S->gthr,
                  S->rows, S->rowcnt, S->w};
     for (void* p : d)
@@ -804,8 +875,13 @@ void sweep_free(ewsjf_ctx* ctx) {
 }
 
 // Diagnostics of the last sweep (cuts, candidate inserts); false if none ran.
-bool sweep_diag(ewsjf_ctx* ctx, unsigned long long* ci) {
+bool sweep_diag(ewsjf_ctx* ctx, unsigned long long* ci, long long* records) {
     if (!ctx->sw || !ctx->sw->bad) return false;
+    SweepScratch* S = ctx->sw;
+    *records = 0;
+    if (S->last_nq > 0 &&
+        cudaMemcpy(records, (S->last_sky ? S->qoff2 : S->qoff) + S->last_nq, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return false;
     return cudaMemcpy(ci, ctx->sw->bad + 2, 16, cudaMemcpyDeviceToHost) == cudaSuccess;
 }
 
@@ -835,7 +911,8 @@ ewsjf_status sweep_alloc(ewsjf_ctx* ctx, int64_t n, int64_t tasks, int K) {
                   cudaMalloc(&S->qoff2, 8 * (kMaxSlots + 1)) == cudaSuccess &&
                   cudaMalloc(&S->cpre2, 4 * (kMaxSlots + 1)) == cudaSuccess &&
                   cudaMalloc(&S->qfill2, 4 * kMaxSlots) == cudaSuccess &&
-                  cudaMalloc(&S->qcnt2, 8 * kMaxSlots) == cudaSuccess;
+                  cudaMalloc(&S->qcnt2, 8 * kMaxSlots) == cudaSuccess &&
+                  cudaMalloc(&S->direct, 4) == cudaSuccess;
         if (!ok) return fail(ctx, EWSJF_ERR_CUDA, "sweep scratch allocation failed");
     }
     if (S->n_cap < n) {
@@ -951,6 +1028,9 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
     // Θ-independent candidate prefilter (K <= 32): the select kernels run over the
     // records no other K records dominate in every feature
     const bool sky = K <= kSkyMaxK && !getenv("EWSJF_NO_SKY");
+    S->last_nq = nq;
+    S->last_sky = sky;
+    CU(cudaMemsetAsync(S->direct, 0, 4, st));      // sky_plan sets it when the survivors are few
     if (sky) {
         int nb = 0;
         for (int p = 0; p < nq; p++) {
@@ -1014,6 +1094,10 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
         {
             LaunchScope ls(ctx, KIND_SWEEP);
             sweep_merge_kernel<<<(nb * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, mrg_smem, st>>>(O);
+        }
+        if (sky) {
+            LaunchScope ls(ctx, KIND_SWEEP);
+            sweep_direct_kernel<<<(nb * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, 0, st>>>(O);
         }
         {
             LaunchScope ls(ctx, KIND_SWEEP);
