@@ -587,6 +587,11 @@ static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, 
     A.HWM = ctx->f_rc * 3 / 4;
     A.lut_size = lutsz;
     A.stages = stages;
+    A.l2_prefetch = 0;    // measured: no gain at C3 (EWSJF_L2PF)
+    if (const char* e = getenv("EWSJF_L2PF")) A.l2_prefetch = std::max(0, atoi(e));
+    A.diag = getenv("EWSJF_DIAG") ? atoi(getenv("EWSJF_DIAG")) : 0;
+    A.cnt_flush = 62;     // a u8 counter gains <= 4 per iteration: (1 + 62) * 4 <= 255
+    if (const char* e = getenv("EWSJF_CNT_FLUSH")) A.cnt_flush = std::max(1, std::min(62, atoi(e)));
     const int G = ctx->num_sms;
     // sample board: each CTA's top key per queue when G >= 2K (the bound's descent then runs
     // over G keys per queue instead of 2G), its top two otherwise

@@ -47,7 +47,7 @@ constexpr int kFMaxSlots = 64;
 constexpr int kFBoardMax = 2;       // board keys per (queue, CTA); G * m <= 32 * kFBoardRegs
 constexpr int kFBoardRegs = 10;
 constexpr int kFMaxStages = 8;      // ring depth cap (EWSJF_STAGES)
-constexpr int kFClaim = 4;          // tiles per dynamic claim
+constexpr int kFCntRow = kFT / 4;   // words per u8 counter row
 
 __host__ __device__ inline int64_t fal(int64_t x) { return (x + 127) & ~(int64_t)127; }
 
@@ -67,7 +67,7 @@ struct FMisc {
 };
 
 struct FSmem {
-    int64_t rec, lut, ring, bars, thr64, sec64, bmax, rcnt, misc, hist, surv, stile, cnt, total;
+    int64_t rec, lut, ring, bars, thr64, sec64, bmax, rcnt, misc, hist, surv, ctot, cnt, total;
 };
 // the per-code records and the LUT sit at fixed offsets (immediate addressing on the hot path)
 constexpr int kFRecOff = 0;
@@ -80,7 +80,7 @@ __host__ __device__ inline FSmem fsmem_layout(bool has_cost, int lut_size, int n
     L.lut = kFLutOff;
     o = fal(kFLutOff + lut_size + 1);
     L.ring = o;  o = fal(o + (int64_t)kFW * stages * narr * kFTile * 4);
-    L.bars = o;  o = fal(o + 8LL * kFW * stages);
+    L.bars = o;  o = fal(o + 12LL * kFMaxStages);   // mbarriers + release counters
     L.thr64 = o; o = fal(o + 8LL * kFMaxSlots);
     L.sec64 = o; o = fal(o + 8LL * kFMaxSlots);
     L.bmax = o;  o = fal(o + 8LL * kFMaxSlots * kFBoardMax);
@@ -88,8 +88,8 @@ __host__ __device__ inline FSmem fsmem_layout(bool has_cost, int lut_size, int n
     L.misc = o;  o = fal(o + sizeof(FMisc));
     L.hist = o;  o = fal(o + 4LL * 256);
     L.surv = o;  o = fal(o + 8LL * EWSJF_MAX_K);
-    L.stile = o; o = fal(o + 8LL * kFW * kFMaxStages);
-    L.cnt = o;   o = fal(o + 2LL * kFT * (nslots + 1));   // u16 rows: members 0..nslots-1, other codes
+    L.ctot = o;  o = fal(o + 4LL * (kFMaxSlots + 1));     // flushed member counts per row
+    L.cnt = o;   o = fal(o + 1LL * kFT * (nslots + 1));   // u8 rows: members 0..nslots-1, other codes
     L.total = o;
     return L;
 }
@@ -283,89 +283,46 @@ __global__ void __launch_bounds__(kFT, 1)
     unsigned* hist = (unsigned*)(smem + L.hist);
     u64* surv = (u64*)(smem + L.surv);
     unsigned char* cntb = smem + L.cnt;
-    unsigned char* ring = smem + L.ring + (int64_t)warp * R * narr * kFTile * 4;
+    unsigned* ctot = (unsigned*)(smem + L.ctot);
     const bool dbg = A.dbg != nullptr;
     auto stamp = [&](int s) {
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + s] = fgtime();
     };
     stamp(0);
 
-    // ---- tile schedule.  The pool's ntiles tiles are cut into GW blocks of
-    // `stride` tiles (block blk = warp*G + cta).  The first S0 = min(R + 1, stride)
-    // tiles of each block are static (the warp's sample tile + its ring prologue:
-    // issued before any coordination and spread over the whole pool, so the
-    // sample is representative whatever the pool order); every other tile is
-    // claimed from a grid-wide counter in batches of kFClaim, so warps and CTAs
-    // finish together (static blocks left warps idling up to ~10 us).
-    const int64_t ntiles = (A.n + kFTile - 1) / kFTile;
+    // ---- chunk schedule.  The pool is cut into chunks of CH = kFW * kFTile requests;
+    // CTA cta takes chunks cta, cta + G, cta + 2G, ... (iteration i: chunk cta + G*i), so at
+    // any time the grid sweeps one contiguous window of the pool.  Warp w owns tile w of every
+    // chunk (global tile (cta + G*i)*kFW + w).  Full chunks are staged into shared memory by
+    // a CTA-level ring of R stages of 1-D TMA bulk copies (one CH*4-byte copy per array, one
+    // mbarrier per stage); the last warp to release a stage refills it with iteration i + R.
+    // (Measured, tools/mb_stream.cu: this pipeline streams the 16 B/request pattern at
+    // 5.6 TB/s; the per-warp cp.async ring reached 4.3 TB/s and dynamic per-warp tile
+    // claims from a grid-wide counter cost another ~9 us.)  A ragged last chunk is read
+    // with direct loads.  Iteration 0 is each CTA's sample chunk.
+    constexpr int CH = kFW * kFTile;
+    const int64_t nchunks = (A.n + CH - 1) / CH;
+    const int64_t nfullc = A.n / CH;
     const int64_t nfull = A.n / kFTile;
-    const int64_t GW = (int64_t)G * kFW;
-    const int64_t blk = (int64_t)warp * G + cta;
-    const int64_t stride = ntiles / GW;
-    const int S0 = (int)((int64_t)R + 1 < stride ? (int64_t)R + 1 : stride);
-    const int64_t dynb = stride - S0;                 // dynamic tiles per block
-    const int64_t ndyn = ntiles - GW * (int64_t)S0;   // tiles handed out by the counter
-    int* stile = (int*)(smem + L.stile) + warp * kFMaxStages;   // tile held by each ring stage (-1: none)
-    auto stage = [&](int st, int a) -> unsigned char* { return ring + (st * narr + a) * kFTile * 4; };
-    int64_t seq = 0;                 // next position in this warp's static tiles
-    unsigned long long cbase = 0ull, nbase = 0ull;   // claimed batches (lane 0): current, next (in flight)
-    // dynamic tiles, warp-uniform: position dcur of the current batch [.., dend), its
-    // tile tn and the dynamic tiles left in tn's block (one division per batch)
-    int dcur = 0, dend = 0, tn = 0, rb = 0;
-    const int ndyn32 = (int)ndyn, dynb32 = (int)dynb, GWdynb = (int)(GW * dynb), GWstride = (int)(GW * stride);
-    // the first claim: right away if the ring prologue already needs dynamic tiles, else
-    // after the sample tile (it then completes during the sample-bound wait; 2368 warps
-    // claiming at launch serialised on the counter for ~1.5 us)
-    if (lane == 0 && ndyn > 0 && S0 <= R) nbase = atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim);
-    auto next_tile = [&]() -> int {                   // all lanes; the warp's next tile, -1 = done
-        if (seq < S0) return (int)(blk * stride + seq++);
-        if (dcur >= dend) {                           // batch boundary: the next batch becomes current
-            if (lane == 0) {
-                cbase = nbase;
-                nbase = cbase < (unsigned long long)ndyn
-                            ? atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim) : cbase;
-            }
-            const unsigned long long d64 = __shfl_sync(0xffffffffu, cbase, 0);
-            if (d64 >= (unsigned long long)ndyn) return -1;
-            const int d = (int)d64;
-            dcur = d;
-            dend = min(d + kFClaim, ndyn32);
-            if (d < GWdynb) {
-                const unsigned qq = (unsigned)d / (unsigned)dynb32, r = (unsigned)d - qq * (unsigned)dynb32;
-                tn = (int)(qq * (unsigned)stride) + S0 + (int)r;
-                rb = dynb32 - (int)r;
-            } else {
-                tn = GWstride + (d - GWdynb);
-                rb = INT_MAX;
-            }
-        }
-        const int t = tn;
-        dcur++;
-        tn++;
-        if (--rb == 0) {                              // past the block's last dynamic tile
-            if (tn < GWstride) { tn += S0; rb = dynb32; } else rb = INT_MAX;
-        }
-        return t;
+    const int my_iters = cta < nchunks ? (int)((nchunks - 1 - cta) / G + 1) : 0;
+    unsigned char* ringc = smem + L.ring;
+    uint64_t* fullb = (uint64_t*)(smem + L.bars);                       // [R] stage landed
+    unsigned* relc = (unsigned*)(smem + L.bars + 8 * kFMaxStages);      // [R] warp releases (monotone)
+    auto stage = [&](int st, int a) -> unsigned char* { return ringc + (st * narr + a) * (CH * 4) + warp * (kFTile * 4); };
+    auto chunk_of = [&](int i) -> int64_t { return (int64_t)cta + (int64_t)G * i; };
+    auto issue_chunk = [&](int i) {   // one thread: iteration i's full chunk into stage i % R
+        if (i >= my_iters) return;
+        const int64_t c = chunk_of(i);
+        if (c >= nfullc) return;
+        const int s = i % R;
+        uint64_t* b = &fullb[s];
+        mbar_arrive_expect_tx(b, (uint32_t)(narr * CH * 4));
+        unsigned char* d = ringc + s * narr * (CH * 4);
+        tma_load_1d(d, A.len + c * CH, CH * 4, b);
+        tma_load_1d(d + CH * 4, A.arrival + c * CH, CH * 4, b);
+        if (HAS_COST) tma_load_1d(d + 2 * CH * 4, A.cost + c * CH, CH * 4, b);
     };
-    // Per-lane cp.async (LDGSTS) ring: every lane copies, and later reads back, its
-    // own 16 bytes per array of each tile; one commit group per tile (empty past
-    // the end).  (A per-warp ring of 512-byte cp.async.bulk copies measured ~2.2 TB/s:
-    // the bulk-copy engine costs ~90 cycles per copy, too many copies per SM.)
-    auto issue_t = [&](int st, int t) {   // all lanes: tile t (-1: none) into stage st
-        if (t >= 0 && t < nfull) {
-            const int64_t off = (int64_t)t * kFTile + 4 * lane;
-            cp_async16(stage(st, 0) + 16 * lane, A.len + off);
-            cp_async16(stage(st, 1) + 16 * lane, A.arrival + off);
-            if (HAS_COST) cp_async16(stage(st, 2) + 16 * lane, A.cost + off);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    auto issue = [&](int st) {        // all lanes: the next tile of the sequence into stage st
-        const int t = next_tile();
-        if (lane == 0) stile[st] = t;
-        issue_t(st, t);
-    };
-    {   // the LUT first (its own commit group, ahead of the ring in the SM's load queue)
+    {   // the LUT first (its own commit group, issued before the ring's bulk copies)
         const int l16 = (lutsz + 1 + 15) / 16;
         const int4* src = reinterpret_cast<const int4*>(A.lut_dev);
         for (int i = tid; i < l16; i += kFT) cp_async16(smem + kFLutOff + 16 * i, src + i);
@@ -379,8 +336,21 @@ __global__ void __launch_bounds__(kFT, 1)
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    for (int i = 0; i < R; i++) issue(i);
-    __syncwarp();
+    if (tid == 0) {   // after the LUT: its 32 KB (L2 hits) must not queue behind the ring's HBM reads
+        for (int s = 0; s < R; s++) { mbar_init(&fullb[s], 1); relc[s] = 0u; }
+        fence_mbar_init();
+        for (int i = 0; i < R; i++) issue_chunk(i);
+        // the chunks after the ring go to L2 while the CTAs agree on the sample bound
+        // (the HBM would otherwise idle for ~6 us)
+        for (int i = R; i < R + A.l2_prefetch && i < my_iters; i++) {
+            const int64_t c = chunk_of(i);
+            if (c >= nfullc) break;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.len + c * CH), "r"(CH * 4) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.arrival + c * CH), "r"(CH * 4) : "memory");
+            if (HAS_COST)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.cost + c * CH), "r"(CH * 4) : "memory");
+        }
+    }
     stamp(10);
 
     // ---- setup while the first tiles are in flight
@@ -391,7 +361,8 @@ __global__ void __launch_bounds__(kFT, 1)
         }
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + 11] = fgtime();
         uint4* c4 = (uint4*)cntb;
-        const int n16 = (2 * kFT * (nslots + 1)) / 16;
+        const int n16 = (kFT * (nslots + 1)) / 16;
+        for (int q = tid; q <= kFMaxSlots; q += kFT) ctot[q] = 0u;
         for (int i = tid; i < n16; i += kFT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + 12] = fgtime();
         if (tid == 0) {
@@ -399,7 +370,7 @@ __global__ void __launch_bounds__(kFT, 1)
             M->members = 0ull; M->sec = 0ull; M->tcoll = 0ull;
             M->agg[0] = M->agg[1] = M->agg[2] = 0ull;
         }
-        cp_async_wait_n(R);            // this thread's LUT / policy chunks (the oldest group) have landed
+        asm volatile("cp.async.wait_group 0;" ::: "memory");   // this thread's LUT / policy chunks have landed
     }
     __syncthreads();
     {
@@ -423,7 +394,7 @@ __global__ void __launch_bounds__(kFT, 1)
                 qid = -1;
             }
             b.y = __int_as_float(qid);
-            b.z = __int_as_float(cnto * kFT * 2);
+            b.z = __int_as_float(cnto * kFT);
             rec[2 * c] = a;
             rec[2 * c + 1] = b;
         }
@@ -434,11 +405,22 @@ __global__ void __launch_bounds__(kFT, 1)
 
     const uint32_t gbase = A.gbase;
     const bool write_qid = A.qid_out != nullptr;
-    // per-thread u16 member counters (row r of thread t at halfword r*kFT + t), bumped
-    // with no-return atomics on the containing word (ATOMS.ADD of 1 or 1 << 16): no
-    // load-add-store dependency on the hot path; <= 65535 requests per thread per tick
-    uint32_t* cntw = (uint32_t*)cntb + (tid >> 1);
-    const uint32_t cinc = (tid & 1) ? 0x10000u : 1u;
+    // per-thread u8 member counters, bumped with no-return atomics on the containing word
+    // (ATOMS.ADD of 1 << 8*(warp & 3)): thread (warp, lane) of row r is byte warp & 3 of
+    // word r*kFCntRow + (warp >> 2)*32 + lane, so the 32 lanes of a warp hit 32 distinct
+    // words (no same-word serialisation) and a row is kFT bytes (the u16 rows it replaces
+    // took 25 KB more shared memory: a fourth ring stage).  A byte gains <= 4 per
+    // iteration; every warp moves its bytes into ctot[] every A.cnt_flush iterations.
+    uint32_t* cntw = (uint32_t*)cntb + (warp >> 2) * 32 + lane;
+    const int cshift = 8 * (warp & 3);
+    const uint32_t cinc = 1u << cshift;
+    auto flush_counters = [&]() {       // all lanes of the warp
+        for (int r = 0; r <= nslots; r++) {
+            const uint32_t old = atomicAnd(cntw + r * kFCntRow, ~(0xFFu << cshift));
+            const unsigned v = __reduce_add_sync(0xffffffffu, (old >> cshift) & 0xFFu);
+            if (lane == 0 && v) atomicAdd(&ctot[r], v);
+        }
+    };
     unsigned n_exc = 0, n_ins = 0, n_gap = 0, n_bad = 0;
     u64* const rows_cta = A.rows.keys + (size_t)cta * RC;     // row of queue q: rows_cta + q*G*RC
     const size_t row_stride = (size_t)G * RC;
@@ -489,19 +471,19 @@ __global__ void __launch_bounds__(kFT, 1)
                 if (write_qid) A.qid_out[idx] = -1;   // already counted in the invalid row
                 return;
             }
-            atomicSub(cntw + nslots * (kFT / 2), cinc);      // not invalid after all
+            atomicSub(cntw + nslots * kFCntRow, cinc);      // not invalid after all
             const int q = bsearch(b);
             if (q >= 0) {
                 const float4 w = rec[2 * q];
                 ok = score_sp(b, a, co, HAS_COST, A.sp, w.x, w.y, w.z, &sp);
-                atomicAdd(cntw + q * (kFT / 2), cinc);
+                atomicAdd(cntw + q * kFCntRow, cinc);
                 if (write_qid) A.qid_out[idx] = P.sid[q];
                 c = q;
             } else {
                 c = kFCodeGap;
             }
         } else if (c == kFCodeGap) {
-            atomicSub(cntw + nslots * (kFT / 2), cinc);      // counted in the invalid row by the body
+            atomicSub(cntw + nslots * kFCntRow, cinc);      // counted in the invalid row by the body
         }
         if (c == kFCodeGap) {
             const unsigned long long p = atomicAdd(&A.ctr->gap_count, 1ull);
@@ -515,7 +497,7 @@ __global__ void __launch_bounds__(kFT, 1)
             return;
         }
         if (c >= nslots) return;   // bad length / padding
-        if (!ok) { atomicSub(cntw + c * (kFT / 2), cinc); n_exc++; return; }
+        if (!ok) { atomicSub(cntw + c * kFCntRow, cinc); n_exc++; return; }
         const u64 ks = score_key(sp, gid), kf = fifo_key(a, gid);
         const u64 k1 = SCORE ? ks : kf, k2 = SCORE ? kf : ks;
         if (k1 >= *(volatile u64*)&thr64[c]) insert(c, k1);
@@ -525,21 +507,22 @@ __global__ void __launch_bounds__(kFT, 1)
     // ---- one tile of 128 requests (4 per lane); sample: keep the keys, fill the sample maxima
     u64 skey[4] = {0ull, 0ull, 0ull, 0ull};
     int scode[4] = {kFCodeNone, kFCodeNone, kFCodeNone, kFCodeNone};
-    int cur_st = 0;             // ring stage of the next tile
     auto body = [&](auto full_tag, auto sample_tag, auto wait_tag, int64_t t, int st) {
         constexpr bool FULL = decltype(full_tag)::value;
         constexpr bool SAMPLE = decltype(sample_tag)::value;
-        constexpr int WAIT = decltype(wait_tag)::value;          // pending groups allowed, -1: R - 1
         const int64_t i0 = t * kFTile + 4 * lane;
         int b[4];
         float a[4], co[4];
         int nv = 4;
-        if (FULL) {
-            if (WAIT >= 0) cp_async_wait_n(WAIT); else cp_async_wait_n(R - 1);
+        if (FULL) {            // the caller has waited for the stage
             const int4 bv = ((const int4*)stage(st, 0))[lane];
             const float4 av = ((const float4*)stage(st, 1))[lane];
             float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
             if (HAS_COST) cv = ((const float4*)stage(st, 2))[lane];
+            if (!SAMPLE && (A.diag & 2)) {   // timing diagnostic (EWSJF_DIAG=2): stream only
+                if (write_qid) __stcs((int4*)(A.qid_out + i0), make_int4(bv.x ^ __float_as_int(av.x), bv.y, bv.z, __float_as_int(cv.w)));
+                return;
+            }
             b[0] = bv.x; b[1] = bv.y; b[2] = bv.z; b[3] = bv.w;
             a[0] = av.x; a[1] = av.y; a[2] = av.z; a[3] = av.w;
             co[0] = cv.x; co[1] = cv.y; co[2] = cv.z; co[3] = cv.w;
@@ -567,7 +550,7 @@ __global__ void __launch_bounds__(kFT, 1)
             // rows 0..nslots-1 members, nslots every other code (invalid length, and the
             // FAR / GAP codes, which the rare path takes back out); padding uncounted
             const int crow = min(c, nslots);
-            if (FULL || j < nv) atomicAdd(cntw + crow * (kFT / 2), cinc);
+            if (FULL || j < nv) atomicAdd(cntw + crow * kFCntRow, cinc);
             const float4 w = rec[2 * c];
             const float4 r2 = rec[2 * c + 1];
             const bool ok = score_sp(b[j], a[j], co[j], HAS_COST, A.sp, w.x, w.y, w.z, &sp[j]);
@@ -627,20 +610,15 @@ __global__ void __launch_bounds__(kFT, 1)
             }
         }
     };
-    // process the tile in ring stage cur_st, refill the stage with the next tile
-    // of the sequence, advance; false when the sequence has ended (the sample tile)
-    auto tile = [&](auto sample_tag) -> bool {
-        const int st = cur_st;
-        const int t = stile[st];
-        if (t < 0) return false;
-        if (t < nfull) body(std::true_type(), sample_tag, std::integral_constant<int, -1>(), t, st);
-        else body(std::false_type(), sample_tag, std::integral_constant<int, -1>(), t, st);
+    // release stage st of iteration i (lane 0, after the warp's last read of it): the
+    // last of the kFW warps refills it with iteration i + R
+    auto release = [&](int st, int i) {
         __syncwarp();
-        issue(st);
-        cur_st = st + 1 == R ? 0 : st + 1;
-        return true;
+        if (lane == 0) {
+            const unsigned o = atomicAdd(&relc[st], 1u);
+            if (o % kFW == kFW - 1) issue_chunk(i + R);
+        }
     };
-
     // ---- collective: cut every row at/over its high-water mark to its exact K-th key
     auto collective = [&]() {
         const unsigned long long tc = dbg ? fgtime() : 0ull;
@@ -680,9 +658,17 @@ __global__ void __launch_bounds__(kFT, 1)
 
     // ---- sample tile, board, bound
     if (dbg && tid == 0) A.dbg[cta * kDbgStride + 25] = fgtime();
-    tile(std::integral_constant<bool, true>());
+    if (my_iters > 0) {
+        const int64_t c = chunk_of(0);
+        if (c < nfullc) {
+            mbar_wait(&fullb[0], 0u);
+            body(std::true_type(), std::true_type(), std::integral_constant<int, 0>(), c * kFW + warp, 0);
+            release(0, 0);
+        } else {
+            body(std::false_type(), std::true_type(), std::integral_constant<int, 0>(), c * kFW + warp, 0);
+        }
+    }
     if (dbg && tid == 0) A.dbg[cta * kDbgStride + 26] = fgtime();
-    if (lane == 0 && ndyn > 0 && S0 > R) nbase = atomicAdd(&A.ctr->ftiles, (unsigned long long)kFClaim);
     __syncthreads();
     stamp(2);
     const int bm = A.board_m;
@@ -760,6 +746,12 @@ __global__ void __launch_bounds__(kFT, 1)
         const u64 s = sec64[q];
         const u32 sh = (u32)(s >> 32);
         rec[2 * q + 1].x = SCORE ? (s ? fifo_hi_to_f(sh) : inf) : __uint_as_float(sh);
+        if (A.diag & 1) {   // timing diagnostic only (EWSJF_DIAG=1): no candidate ever passes (wrong outputs)
+            rec[2 * q].w = SCORE ? inf : -inf;
+            rec[2 * q + 1].x = SCORE ? -inf : inf;
+            thr64[q] = ~0ull;
+            sec64[q] = ~0ull;
+        }
     }
     __syncthreads();
     stamp(3);
@@ -780,7 +772,7 @@ __global__ void __launch_bounds__(kFT, 1)
     int chk = -1;
     if (A.refresh && warp < 6) {
         const int num = warp == 0 ? 1 : warp == 1 ? 2 : warp == 2 ? 4 : warp == 3 ? 6 : warp == 4 ? 8 : 12;
-        chk = (int)((ntiles / GW) * num >> 4);
+        chk = (my_iters * num) >> 4;
         if (chk < 1) chk = -1;
     }
     auto refresh = [&]() {
@@ -807,27 +799,27 @@ __global__ void __launch_bounds__(kFT, 1)
     // streaming loads in flight, ~2 us)
     int rq = warp % max(nslots, 1);
     u64 gpoll = (lane == 0 && nslots > 0) ? __ldcg(&A.gthr[rq]) : 0ull;
-    // the streaming loop with the ring depth fixed at compile time: the tiles of the
-    // RR stages in registers (tq[0] = next), the cp.async wait an immediate
+    // the streaming loop with the ring depth fixed at compile time (stage / phase counters
+    // without divisions)
     auto stream = [&](auto r_tag) {
         constexpr int RR = decltype(r_tag)::value;
         __syncwarp();
-        int tq[RR];
-#pragma unroll
-        for (int j = 0; j < RR; j++) tq[j] = stile[(cur_st + j) % RR];
-        int st = cur_st;
-        for (int i = 1;; i++) {
+        int st = 1 % RR;
+        uint32_t ph = (1 / RR) & 1;
+        int since_flush = 1;            // the sample iteration
+        for (int i = 1; i < my_iters; i++) {
             if (*(volatile int*)&M->flag) collective();
-            const int t = tq[0];
-            if (t < 0) break;
-            if (t < nfull) body(std::true_type(), std::false_type(), std::integral_constant<int, RR - 1>(), t, st);
-            else body(std::false_type(), std::false_type(), std::integral_constant<int, RR - 1>(), t, st);
-            __syncwarp();
-#pragma unroll
-            for (int j = 0; j + 1 < RR; j++) tq[j] = tq[j + 1];
-            tq[RR - 1] = next_tile();
-            issue_t(st, tq[RR - 1]);
-            st = st + 1 == RR ? 0 : st + 1;
+            const int64_t c = chunk_of(i);
+            const int64_t t = c * kFW + warp;
+            if (c < nfullc) {
+                mbar_wait(&fullb[st], ph);
+                body(std::true_type(), std::false_type(), std::integral_constant<int, 0>(), t, st);
+                release(st, i);
+            } else {
+                body(std::false_type(), std::false_type(), std::integral_constant<int, 0>(), t, st);
+            }
+            if (++st == RR) { st = 0; ph ^= 1u; }
+            if (++since_flush == A.cnt_flush) { flush_counters(); since_flush = 0; }
             if (i == chk) refresh();
             if ((i & 3) == 0 && nslots > 0) {
                 if (lane == 0) {
@@ -860,60 +852,62 @@ __global__ void __launch_bounds__(kFT, 1)
         __nanosleep(256);      // a done warp must not steal issue slots from the streaming ones
     }
     __syncthreads();
+    if (tid == 0)      // the ring's shared memory is reused by the merge
+        for (int st = 0; st < R; st++)
+            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&fullb[st])) : "memory");
     stamp(4);
 
-    // ---- per-CTA rows cut to the best bound known now (this CTA's threshold or the
-    // global one, max of the two): the merge then reads a few keys per row instead
-    // of every insert (the dominant queue's merge read ~400 per CTA, ~10 us).
+    // ---- per-CTA rows: cut to the best bound known now (this CTA's threshold or the
+    // global one, max of the two) -- the merge then reads a few keys per row instead of
+    // every insert (the dominant queue's merge read ~400 per CTA, ~10 us); rows of <= 32
+    // keys are left as they are (the merge loads those whole and filters them itself) --
+    // then count (<= RC, no overflow pending), members, secondary, in one pass per queue
     for (int q = warp; q < nslots; q += kFW) {
         const int nr = min(rcnt[q], RC);
-        if (nr == 0) continue;
-        u64 g = __ldcg(&A.gthr[q]);
-        const u64 tl = thr64[q];
-        g = g > tl ? g : tl;
-        u64* row = rows_cta + q * row_stride;
-        int wpos = 0;
-        for (int base = 0; base < nr; base += 32 * 16) {
-            u64 kv[16];
+        int wpos = nr;
+        if (nr > 32) {
+            u64 g = __ldcg(&A.gthr[q]);
+            const u64 tl = thr64[q];
+            g = g > tl ? g : tl;
+            u64* row = rows_cta + q * row_stride;
+            wpos = 0;
+            for (int base = 0; base < nr; base += 32 * 16) {
+                u64 kv[16];
 #pragma unroll
-            for (int u = 0; u < 16; u++) {
-                const int j = base + u * 32 + lane;
-                kv[u] = j < nr ? __ldcg(row + j) : 0ull;
-            }
+                for (int u = 0; u < 16; u++) {
+                    const int j = base + u * 32 + lane;
+                    kv[u] = j < nr ? __ldcg(row + j) : 0ull;
+                }
 #pragma unroll
-            for (int u = 0; u < 16; u++) {
-                const bool keep = kv[u] != 0ull && kv[u] >= g;
-                const unsigned bal = __ballot_sync(0xffffffffu, keep);
-                if (keep) row[wpos + __popc(bal & ((1u << lane) - 1u))] = kv[u];
-                wpos += __popc(bal);
+                for (int u = 0; u < 16; u++) {
+                    const bool keep = kv[u] != 0ull && kv[u] >= g;
+                    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                    if (keep) row[wpos + __popc(bal & ((1u << lane) - 1u))] = kv[u];
+                    wpos += __popc(bal);
+                }
             }
         }
-        __syncwarp();
-        if (lane == 0) rcnt[q] = wpos;
-    }
-    __syncthreads();
-    if (dbg && tid == 0) A.dbg[cta * kDbgStride + 28] = fgtime();
-    // ---- per-CTA rows: count (<= RC, no overflow pending), members, secondary
-    for (int q = warp; q < nslots; q += kFW) {
-        const uint32_t* c32 = (const uint32_t*)(cntb + (size_t)q * kFT * 2);
-        unsigned long long mm = 0;
+        const uint32_t* c32 = (const uint32_t*)(cntb + (size_t)q * kFT);
+        unsigned long long mm = lane == 0 ? ctot[q] : 0u;
 #pragma unroll
-        for (int k = 0; k < kFT / 64; k++) { const uint32_t v = c32[lane + 32 * k]; mm += (v & 0xffffu) + (v >> 16); }
+        for (int k = 0; k < kFCntRow / 32; k++) mm += __dp4a(c32[lane + 32 * k], 0x01010101u, 0u);
         for (int o = 16; o; o >>= 1) mm += __shfl_xor_sync(0xffffffffu, mm, o);
         if (lane == 0) {
             const size_t r = (size_t)q * G + cta;
-            A.rows.cnt[r] = min(rcnt[q], RC);
+            A.rows.cnt[r] = wpos;
             A.rows.members[r] = (int64_t)mm;
             A.rows.sec[r] = sec64[q];
         }
     }
+    if (dbg && tid == 0) A.dbg[cta * kDbgStride + 28] = fgtime();
     if (dbg && tid == 0) A.dbg[cta * kDbgStride + 29] = fgtime();
     {
         // invalid lengths (counter row nslots) + excluded + diagnostics
         unsigned long long bad = n_bad;
         if (warp == 0) {
-            const uint32_t* c32 = (const uint32_t*)(cntb + (size_t)nslots * kFT * 2);
-            for (int k = lane; k < kFT / 2; k += 32) { const uint32_t v = c32[k]; bad += (v & 0xffffu) + (v >> 16); }
+            const uint32_t* c32 = (const uint32_t*)(cntb + (size_t)nslots * kFT);
+            if (lane == 0) bad += ctot[nslots];
+            for (int k = lane; k < kFCntRow; k += 32) bad += __dp4a(c32[k], 0x01010101u, 0u);
         }
         unsigned long long ex = n_exc, ins = n_ins;
         for (int o = 16; o; o >>= 1) {
@@ -956,7 +950,6 @@ __global__ void __launch_bounds__(kFT, 1)
     __syncthreads();
     stamp(6);
     if (dbg && tid == 0) A.dbg[cta * kDbgStride + 24] = fgtime();
-    if (cta == 0 && tid == 0) A.ctr->ftiles = 0ull;   // every claim of this launch is done
     if (A.refresh)   // nobody reads the refresh board past the barrier: clear this CTA's column for the next tick
         for (int q = tid; q < nslots; q += kFT) A.rboard[(size_t)q * G + cta] = 0ull;
 

@@ -60,9 +60,12 @@ struct FArgs {
     int32_t K;
     int32_t RC, HWM;            // row capacity per (queue, CTA) / high-water mark
     int32_t lut_size;           // LUT covers lengths [0, lut_size); longer: binary search (rare path)
-    int32_t stages;             // TMA ring depth per warp
+    int32_t stages;             // TMA ring depth (CTA-level chunk stages)
+    int32_t l2_prefetch;        // chunks after the ring prefetched into L2 at launch
+    int32_t cnt_flush;          // iterations between u8 member-counter flushes (<= 62)
     int32_t board_m;            // sample board keys per (queue, CTA); 0 = no sample bound
     int32_t merge;              // 0: rows only; 1: final outputs; 2: exchange record (merge_phase)
+    int32_t diag;               // timing diagnostics (EWSJF_DIAG bits); 0 in normal use
     const unsigned char* lut_dev;
     ScoreParams sp;
     Rows rows;                  // keys [64][G][RC]
