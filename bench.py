@@ -193,7 +193,7 @@ def run_sweep(E, ctx, dev, args, rank=0, ws=1, group=None):
     qid, rsum = E.route(ctx, ln, c2part)
     all_t = workload.random_thetas(args.sweep_thetas, 502)
     lo_t, hi_t = workload.shard_range(len(all_t), rank, ws)
-    thetas = [E.meta(**t) for t in all_t[lo_t:hi_t]]
+    thetas = E.meta_array([E.meta(**t) for t in all_t[lo_t:hi_t]])
     sp = E.select_params(k=16, mode=0, now=workload.NOW)
     sctx = E.Context(dev.index or 0, max_pool=n, max_history=0, max_k=64, max_sweep=n)
     outs = E.score_select_sweep(sctx, ln, ar, co, qid, c2part, thetas, sp)

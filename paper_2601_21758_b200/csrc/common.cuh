@@ -137,6 +137,16 @@ __device__ __forceinline__ u64 shfl_xor_u64(u64 v, int m) {
     u32 hi = __shfl_xor_sync(0xffffffffu, (u32)(v >> 32), m);
     return ((u64)hi << 32) | lo;
 }
+__device__ __forceinline__ u64 shfl_idx_u64(u64 v, int src) {
+    const u32 lo = __shfl_sync(0xffffffffu, (u32)v, src);
+    const u32 hi = __shfl_sync(0xffffffffu, (u32)(v >> 32), src);
+    return ((u64)hi << 32) | lo;
+}
+__device__ __forceinline__ u64 shfl_up_u64(u64 v, int d) {
+    const u32 lo = __shfl_up_sync(0xffffffffu, (u32)v, d);
+    const u32 hi = __shfl_up_sync(0xffffffffu, (u32)(v >> 32), d);
+    return ((u64)hi << 32) | lo;
+}
 __device__ __forceinline__ u64 warp_max_u64(u64 v) {
 #pragma unroll
     for (int m = 16; m; m >>= 1) {

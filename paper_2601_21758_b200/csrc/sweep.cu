@@ -60,12 +60,14 @@ struct SweepScratch {
     u64* rows = nullptr;            // [task][kSwT][K]
     int32_t* rowcnt = nullptr;      // [task][kSwT]
     float* w = nullptr;             // [kSwBatch][256][3] weights by position (device, A7)
-    // prefilter scratch: bin counts -> starts, scatter cursors, records sorted by length,
-    // candidate flags, per-block top keys, prefix bounds, the compacted records + layout
+    // prefilter scratch: bin counts -> starts, scatter cursors, per-length list bounds,
+    // per-block top keys, prefix bounds, the compacted records + layout (rec2 holds the
+    // records sorted by length until the compaction)
     int32_t* bcnt = nullptr;        // [kSkyBins + 1]
     int32_t* bfill = nullptr;       // [kSkyBins]
-    int32_t* srt = nullptr;         // [n]
-    uint8_t* cand = nullptr;        // [n]
+    u64* lenkth = nullptr;          // [kSkyBins][2] per length: K-th of its two lists (0: keep all)
+    int32_t* biglist = nullptr;     // [kSkyBins] lengths with > kSkyBig records (K3d's CTA kernel)
+    int32_t* nbig = nullptr;        // [1]
     u64* blktop = nullptr;          // [kSkyMaxBlocks][kSkyMaxK]
     u64* blkid = nullptr;           // [kSkyMaxBlocks][kSkyMaxK]
     u64* lentop = nullptr;          // [kSkyBins][kSkyMaxK] per length: its K best (f1, id) keys
@@ -79,6 +81,16 @@ struct SweepScratch {
     int64_t* qcnt2 = nullptr;       // [256]
     int32_t* direct = nullptr;      // [1] 1: the prefilter left <= kSwDirectMax records per queue (K5d path)
     size_t attr_smem = 0;           // select kernel: dynamic smem attribute set for this ctx's device
+    bool sky_attr = false;          // prefilter kernels' dynamic smem attributes set
+    // kernel arguments live in device memory (SweepArgs is ~13 KB: as a kernel parameter
+    // every launch paid for copying it): a ring of pinned staging slots, each uploaded
+    // with one stream-ordered copy; a slot is rewritten once its previous copy has run
+    static constexpr int kArgSlots = 8;
+    unsigned char* h_args = nullptr;
+    unsigned char* d_args = nullptr;
+    size_t arg_slot = 0;
+    cudaEvent_t arg_ev[kArgSlots] = {};
+    int arg_next = 0;
     int occ = 1;
     int last_nq = 0;                // diagnostics: the last sweep's queue count and record offsets used
     bool last_sky = false;
@@ -93,7 +105,6 @@ struct SweepArgs {
     int32_t nq;
     int32_t K, cap, chunk, chunk0, rcap;
     int32_t n_theta;                // in this batch
-    int32_t phase;                  // K4: 0 = first chunk of every queue, 1 = the other chunks
     float now, c0, c1, c2;
     double theta[kSwBatch][6];      // this batch's Θ (a_b, b_b, a_u, b_u, a_f, b_f)
     double mean[kMaxSlots];         // b̄ by position
@@ -102,6 +113,7 @@ struct SweepArgs {
     int32_t sorted_pos[kMaxSlots];
     // prefilter: per position the grouped length range [qbin_lo, qbin_hi) and its first block
     int32_t qbin_lo[kMaxSlots], qbin_hi[kMaxSlots], qblk[kMaxSlots + 1];
+    int32_t sky_nbins;              // bins in use: > every qbin_hi, multiple of 1024, <= kSkyBins
     SweepScratch s;
 };
 
@@ -138,7 +150,8 @@ __device__ __forceinline__ int sw_request(const SweepArgs& A, const int* ids, co
 }
 
 // K1: counts, FIFO heads, invalid / excluded totals.
-__global__ void __launch_bounds__(kSwPrepThreads) sweep_count_kernel(const __grid_constant__ SweepArgs A) {
+__global__ void __launch_bounds__(kSwPrepThreads) sweep_count_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
     __shared__ int s_ids[kMaxSlots], s_pos[kMaxSlots];
     __shared__ unsigned int s_cnt[kMaxSlots];
     __shared__ u64 s_head[kMaxSlots];
@@ -168,7 +181,8 @@ __global__ void __launch_bounds__(kSwPrepThreads) sweep_count_kernel(const __gri
 }
 
 // K2 (one CTA of 32 threads): record offsets, chunk prefix, head features, reset cursors.
-__global__ void sweep_plan_kernel(const __grid_constant__ SweepArgs A) {
+__global__ void sweep_plan_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
     __shared__ int s_ids[kMaxSlots], s_pos[kMaxSlots];
     for (int i = threadIdx.x; i < kMaxSlots; i += blockDim.x) { s_ids[i] = A.sorted_ids[i]; s_pos[i] = A.sorted_pos[i]; }
     __syncwarp();
@@ -198,26 +212,41 @@ __global__ void sweep_plan_kernel(const __grid_constant__ SweepArgs A) {
     }
 }
 
-// K3: scatter the valid requests' records grouped by queue position.
-__global__ void __launch_bounds__(kSwPrepThreads) sweep_scatter_kernel(const __grid_constant__ SweepArgs A) {
+// Contiguous record range of this CTA: [i0, i1) of [0, ntot).
+__device__ __forceinline__ void sw_cta_range(int64_t ntot, int64_t* i0, int64_t* i1) {
+    const int64_t per = (ntot + gridDim.x - 1) / gridDim.x;
+    *i0 = min(ntot, per * (int64_t)blockIdx.x);
+    *i1 = min(ntot, *i0 + per);
+}
+
+// K3: scatter the valid requests' records grouped by queue position.  Each CTA takes a
+// contiguous range of the snapshot: counts per position in shared memory, one global
+// cursor reservation per (CTA, position), then the records placed with shared cursors
+// (a warp-aggregated global cursor per record batch serialised ~30k atomics on the
+// dominant position's cursor, ~60 us at C5).
+__global__ void __launch_bounds__(kSwPrepThreads) sweep_scatter_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
     __shared__ int s_ids[kMaxSlots], s_pos[kMaxSlots];
-    for (int i = threadIdx.x; i < kMaxSlots; i += blockDim.x) { s_ids[i] = A.sorted_ids[i]; s_pos[i] = A.sorted_pos[i]; }
+    __shared__ unsigned s_cnt[kMaxSlots];
+    for (int i = threadIdx.x; i < kMaxSlots; i += blockDim.x) { s_ids[i] = A.sorted_ids[i]; s_pos[i] = A.sorted_pos[i]; s_cnt[i] = 0u; }
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    for (int64_t r0 = (int64_t)blockIdx.x * blockDim.x; r0 < A.n; r0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = r0 + threadIdx.x;
+    int64_t r0, r1;
+    sw_cta_range(A.n, &r0, &r1);
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
         float4 f;
         u64 fk;
-        const int p = r < A.n ? sw_request(A, s_ids, s_pos, r, &f, &fk) : -1;
-        // warp-aggregated cursor reservation per distinct position
-        const unsigned peers = __match_any_sync(0xffffffffu, p);
-        if (p >= 0) {
-            const int leader = __ffs(peers) - 1;
-            int base = 0;
-            if (lane == leader) base = atomicAdd(&A.s.qfill[p], __popc(peers));
-            base = __shfl_sync(peers, base, leader);
-            A.s.rec[A.s.qoff[p] + base + __popc(peers & ((1u << lane) - 1u))] = f;
-        }
+        const int p = sw_request(A, s_ids, s_pos, r, &f, &fk);
+        if (p >= 0) atomicAdd(&s_cnt[p], 1u);
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < A.nq; p += blockDim.x)
+        if (s_cnt[p]) s_cnt[p] = (unsigned)A.s.qoff[p] + (unsigned)atomicAdd(&A.s.qfill[p], (int)s_cnt[p]);
+    __syncthreads();
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        float4 f;
+        u64 fk;
+        const int p = sw_request(A, s_ids, s_pos, r, &f, &fk);
+        if (p >= 0) A.s.rec[atomicAdd(&s_cnt[p], 1u)] = f;
     }
 }
 
@@ -235,36 +264,119 @@ __global__ void __launch_bounds__(kSwPrepThreads) sweep_scatter_kernel(const __g
 // dominators in p's own block are ignored, which only keeps more).  A dominated
 // record can only displace p at an exact fp32 tie, i.e. a near-tie.  The select
 // kernels then run over the survivors (~10^3 of the 10^6 records at C5).
+//
+// Layout: K3a/K3c sort the grouped records by length (a counting sort: per-CTA
+// shared histograms, one global reservation per (CTA, length)) into rec2 (free
+// until K3g); K3d keeps per length its K best keys by (f1, id) and its K lowest
+// ids (lists zero-padded to 32) and the K-th of each (0: fewer than K, keep all);
+// K3e merges the lists per block of kSkyBlk lengths; K3f turns a position's
+// blocks into prefix bounds with a Hillis-Steele scan of top-K lists in shared
+// memory; K3g keeps a record if it is in its length's lists and above its
+// block's prefix bound (or among the queue's K lowest ids).
 __device__ __forceinline__ int sky_len(const float4& f) { return (int)rintf(1.0f / f.x - 1.0f); }
-__device__ __forceinline__ int sky_pos(const SweepArgs& A, int64_t i) {   // position of record i
-    int lo = 0, hi = A.nq;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (A.s.qoff[mid] <= i) lo = mid; else hi = mid;
-    }
-    return lo;
-}
 __device__ __forceinline__ bool sky_grouped(const SweepArgs& A, int p, int b) {
     return b >= A.qbin_lo[p] && b < A.qbin_hi[p];
 }
 __device__ __forceinline__ u64 sky_key(const float4& f) {
     return ((u64)__float_as_uint(f.y) << 32) | (u64)(~__float_as_uint(f.w));
 }
-
-// K3a: histogram of the grouped records' lengths
-__global__ void __launch_bounds__(kSwPrepThreads) sky_hist_kernel(const __grid_constant__ SweepArgs A) {
-    const int64_t ntot = A.s.qoff[A.nq];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += (int64_t)gridDim.x * blockDim.x) {
-        const float4 f = A.s.rec[i];
-        const int b = sky_len(f), p = sky_pos(A, i);
-        if (sky_grouped(A, p, b)) atomicAdd(&A.s.bcnt[b], 1);
+__device__ __forceinline__ u64 sky_idkey(const float4& f) { return (u64)(~__float_as_uint(f.w)) + 1ull; }   // larger = lower id
+// position of record i (qoff staged in shared memory), advanced from the previous one
+__device__ __forceinline__ int sky_pos_from(const int64_t* qoff, int nq, int p, int64_t i) {
+    while (p + 1 < nq && qoff[p + 1] <= i) p++;
+    return p;
+}
+__device__ __forceinline__ int sky_pos_search(const int64_t* qoff, int nq, int64_t i) {
+    int lo = 0, hi = nq;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (qoff[mid] <= i) lo = mid; else hi = mid;
     }
+    return lo;
+}
+constexpr int kSortBins = 32768;    // per-CTA shared histogram of lengths < kSortBins (128 KB)
+constexpr int kSortThreads = 1024;
+constexpr int kSkyBig = 1024;       // K3d: lengths with more records are reduced by a whole CTA
+constexpr size_t kSortSmem = (size_t)kSortBins * 4;
+
+// Warp streaming top-K (K <= 32): lane i holds the (i+1)-th largest key so far
+// (descending, 0 = none).  A chunk of 32 keys (one per lane) none of which beats
+// the K-th is skipped with one vote; otherwise it is bitonic-sorted and merged
+// (the elementwise max of the list and the reversed chunk is bitonic).
+__device__ __forceinline__ u64 sw_bitonic_step(u64 v, int lane, int j, bool up) {
+    const u64 o = shfl_xor_u64(v, j);
+    const bool keep_max = ((lane & j) == 0) == up;
+    return keep_max ? (o > v ? o : v) : (o < v ? o : v);
+}
+__device__ __forceinline__ u64 topk_add(u64 top, u64 v, int K, int lane) {
+    u64 kth = __shfl_sync(0xffffffffu, top, K - 1);
+    unsigned m = __ballot_sync(0xffffffffu, v > kth);
+    if (!m) return top;
+    if (__popc(m) <= 4) {
+        // a few keys beat the K-th (the common case once the list is full): insert them
+        // one at a time -- rank by one vote, shift the tail down one lane
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1u;
+            const u64 x = shfl_idx_u64(v, src);
+            if (!(x > kth)) continue;
+            const int pos = __popc(__ballot_sync(0xffffffffu, top > x));
+            const u64 up = shfl_up_u64(top, 1);
+            top = lane < pos ? top : (lane == pos ? x : up);
+            kth = __shfl_sync(0xffffffffu, top, K - 1);
+        }
+        return top;
+    }
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) v = sw_bitonic_step(v, lane, j, (lane & k) == 0 || k == 32);
+    const u64 r = shfl_xor_u64(v, 31);
+    top = r > top ? r : top;
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) top = sw_bitonic_step(top, lane, j, true);
+    return top;
+}
+// Merge a sorted list v (descending across the lanes, zeros last) into top: the
+// elementwise max of top and the reversed v is bitonic, one 5-step merge sorts it.
+__device__ __forceinline__ u64 topk_merge_sorted(u64 top, u64 v, int K, int lane) {
+    const u64 kth = __shfl_sync(0xffffffffu, top, K - 1);
+    if (!__any_sync(0xffffffffu, v > kth)) return top;
+    const u64 r = shfl_xor_u64(v, 31);
+    top = r > top ? r : top;
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) top = sw_bitonic_step(top, lane, j, true);
+    return top;
+}
+
+// K3a: per-CTA shared histogram of the grouped records' lengths (global atomics on
+// the ~200 hot short lengths took ~250 us at C5)
+__global__ void __launch_bounds__(kSortThreads) sky_hist_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
+    extern __shared__ unsigned s_h[];
+    __shared__ int64_t s_qoff[kMaxSlots + 1];
+    for (int b = threadIdx.x; b < kSortBins; b += blockDim.x) s_h[b] = 0u;
+    for (int q = threadIdx.x; q <= A.nq; q += blockDim.x) s_qoff[q] = A.s.qoff[q];
+    __syncthreads();
+    int64_t i0, i1;
+    sw_cta_range(s_qoff[A.nq], &i0, &i1);
+    int p = i0 < i1 ? sky_pos_search(s_qoff, A.nq, i0 + threadIdx.x) : 0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        p = sky_pos_from(s_qoff, A.nq, p, i);
+        const int b = sky_len(A.s.rec[i]);
+        if (!sky_grouped(A, p, b)) continue;
+        if (b < kSortBins) atomicAdd(&s_h[b], 1u); else atomicAdd(&A.s.bcnt[b], 1);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kSortBins; b += blockDim.x)
+        if (s_h[b]) atomicAdd(&A.s.bcnt[b], (int)s_h[b]);
 }
 // K3b: one CTA, exclusive scan of the kSkyBins counts in place (bcnt[kSkyBins] = total):
 // warp w scans its contiguous 2048 bins in coalesced rows of 32, then the warp totals
-__global__ void __launch_bounds__(1024) sky_scan_kernel(const __grid_constant__ SweepArgs A) {
+__global__ void __launch_bounds__(1024) sky_scan_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
     __shared__ int ws[32];
-    constexpr int per = kSkyBins / 32;                 // bins per warp
+    const int per = A.sky_nbins / 32;                  // bins per warp (sky_nbins: multiple of 1024)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int* bc = A.s.bcnt + warp * per;
     int tot = 0;
@@ -285,187 +397,237 @@ __global__ void __launch_bounds__(1024) sky_scan_kernel(const __grid_constant__ 
         bc[j0 + lane] = run + incl - c;
         run += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (tid == 1023) A.s.bcnt[kSkyBins] = run;
+    if (tid == 1023) A.s.bcnt[A.sky_nbins] = run;
 }
-// K3c: record indices sorted by length
-__global__ void __launch_bounds__(kSwPrepThreads) sky_scatter_kernel(const __grid_constant__ SweepArgs A) {
-    const int64_t ntot = A.s.qoff[A.nq];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += (int64_t)gridDim.x * blockDim.x) {
+// K3c: the grouped records sorted by length into rec2 (same per-CTA ranges as K3a:
+// recount, reserve one range per (CTA, length), place with shared cursors)
+__global__ void __launch_bounds__(kSortThreads) sky_scatter_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
+    extern __shared__ unsigned s_h[];
+    __shared__ int64_t s_qoff[kMaxSlots + 1];
+    for (int b = threadIdx.x; b < kSortBins; b += blockDim.x) s_h[b] = 0u;
+    for (int q = threadIdx.x; q <= A.nq; q += blockDim.x) s_qoff[q] = A.s.qoff[q];
+    __syncthreads();
+    int64_t i0, i1;
+    sw_cta_range(s_qoff[A.nq], &i0, &i1);
+    const int pstart = i0 < i1 ? sky_pos_search(s_qoff, A.nq, i0 + threadIdx.x) : 0;
+    int p = pstart;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        p = sky_pos_from(s_qoff, A.nq, p, i);
+        const int b = sky_len(A.s.rec[i]);
+        if (sky_grouped(A, p, b) && b < kSortBins) atomicAdd(&s_h[b], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kSortBins; b += blockDim.x)
+        if (s_h[b]) s_h[b] = (unsigned)A.s.bcnt[b] + (unsigned)atomicAdd(&A.s.bfill[b], (int)s_h[b]);
+    __syncthreads();
+    p = pstart;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        p = sky_pos_from(s_qoff, A.nq, p, i);
         const float4 f = A.s.rec[i];
-        const int b = sky_len(f), p = sky_pos(A, i);
-        A.s.cand[i] = 0;
-        if (sky_grouped(A, p, b)) A.s.srt[A.s.bcnt[b] + atomicAdd(&A.s.bfill[b], 1)] = (int32_t)i;
+        const int b = sky_len(f);
+        if (!sky_grouped(A, p, b)) continue;
+        const unsigned slot = b < kSortBins ? atomicAdd(&s_h[b], 1u)
+                                            : (unsigned)A.s.bcnt[b] + (unsigned)atomicAdd(&A.s.bfill[b], 1);
+        A.s.rec2[slot] = f;
     }
 }
-// Streaming warp top-K of the nonzero keys produced by key(j) for j in [beg, end):
-// chunks of 7 x 32 keys plus the K kept (one per lane, K <= 32); returns the kept
-// keys (one per lane, 0 = none).  sb: 32 u64 of shared scratch for this warp.
-template <typename KeyFn>
-__device__ __forceinline__ u64 sky_warp_topk(int beg, int end, int K, KeyFn key, u64* sb) {
-    const int lane = threadIdx.x & 31;
-    u64 kept = 0ull;
-    for (int j0 = beg; j0 < end; j0 += 7 * 32) {
-        u64 v[8];
-        int nz = 0;
-#pragma unroll
-        for (int r = 0; r < 7; r++) {
-            const int j = j0 + r * 32 + lane;
-            v[r] = j < end ? key(j) : 0ull;
-            nz += v[r] != 0ull;
-        }
-        v[7] = kept;
-        nz += kept != 0ull;
-        nz = __reduce_add_sync(0xffffffffu, nz);
-        const u64 t = nz > K ? warp_kth_regs<8>(v, K) : 1ull;
-        int base = 0;
-#pragma unroll
-        for (int r = 0; r < 8; r++) {
-            const bool keep = v[r] && v[r] >= t;
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (keep) sb[base + __popc(m & ((1u << lane) - 1u))] = v[r];   // <= K <= 32 kept
-            base += __popc(m);
-        }
-        __syncwarp();
-        kept = lane < base ? sb[lane] : 0ull;
-        __syncwarp();
-    }
-    return kept;
-}
-__device__ __forceinline__ u64 sky_idkey(const float4& f) { return (u64)(~__float_as_uint(f.w)) + 1ull; }   // larger = lower id
-
-// K3d: one warp per length: its K best records by (f1, id) are candidates, and so
-// are its K lowest ids (when w_urg = 0 every record of the length scores the same
-// and R24's lowest ids win).  Both lists (min(count, K) keys each) are kept per
-// length for K3e.
-__global__ void __launch_bounds__(kSwPrepThreads) sky_group_kernel(const __grid_constant__ SweepArgs A) {
-    __shared__ u64 sbuf[kSwPrepThreads / 32][32];
-    const int lane = threadIdx.x & 31;
-    u64* sb = sbuf[threadIdx.x >> 5];
-    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+// K3d: per length, its K best records by (f1, id) and its K lowest ids (both lists
+// zero-padded to 32 per length; unordered) and the K-th of each (0 when the length
+// has <= K records: all of them are candidates).  BIG: one CTA per length with more
+// than kSkyBig records (16 warps over slices, then one merge per list); else one warp.
+template <bool BIG>
+__global__ void __launch_bounds__(kSwPrepThreads) sky_group_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
+    __shared__ u64 s1[kSwPrepThreads / 32][32], s2[kSwPrepThreads / 32][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     const int K = A.K;
-    for (int b = 2 + w0; b < kSkyBins; b += nw) {
-        const int beg = A.s.bcnt[b], end = A.s.bcnt[b + 1], c = end - beg;
-        if (c == 0) continue;
-        u64* lt = A.s.lentop + (size_t)b * kSkyMaxK;
-        u64* li = A.s.lenid + (size_t)b * kSkyMaxK;
-        if (c <= K) {                                  // c <= K <= 32: one record per lane
-            if (lane < c) {
-                const int i = A.s.srt[beg + lane];
-                const float4 f = __ldg(&A.s.rec[i]);
-                A.s.cand[i] = 1;
-                lt[lane] = sky_key(f);
-                li[lane] = sky_idkey(f);
+    // top-K of the keys of records [beg, end) of rec2, 4 chunks of 32 loaded at a time
+    auto scan = [&](int beg, int end, u64* t1, u64* t2) {
+        u64 a = 0ull, c = 0ull;
+        for (int j0 = beg; j0 < end; j0 += 128) {
+            float4 f[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int j = j0 + 32 * u + lane;
+                f[u] = j < end ? A.s.rec2[j] : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            continue;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const bool v = j0 + 32 * u + lane < end;
+                a = topk_add(a, v ? sky_key(f[u]) : 0ull, K, lane);
+                c = topk_add(c, v ? sky_idkey(f[u]) : 0ull, K, lane);
+            }
         }
-        const u64 k1 = sky_warp_topk(beg, end, K, [&](int j) { return sky_key(__ldg(&A.s.rec[A.s.srt[j]])); }, sb);
-        const u64 k2 = sky_warp_topk(beg, end, K, [&](int j) { return sky_idkey(__ldg(&A.s.rec[A.s.srt[j]])); }, sb);
-        if (lane < K) { lt[lane] = k1; li[lane] = k2; }   // exactly K nonzero keys each (keys are unique)
-        u64 m1 = k1 ? k1 : ~0ull, m2 = k2 ? k2 : ~0ull;    // the K-th of each = the smallest kept
-        m1 = warp_min_u64(m1);
-        m2 = warp_min_u64(m2);
-        for (int j = beg + lane; j < end; j += 32) {
-            const int i = A.s.srt[j];
-            const float4 f = __ldg(&A.s.rec[i]);
-            if (sky_key(f) >= m1 || sky_idkey(f) >= m2) A.s.cand[i] = 1;
+        *t1 = a; *t2 = c;
+    };
+    auto emit = [&](int b, int cnt, u64 k1, u64 k2) {   // one warp
+        k1 = lane < K ? k1 : 0ull;
+        k2 = lane < K ? k2 : 0ull;
+        A.s.lentop[(size_t)b * kSkyMaxK + lane] = k1;
+        A.s.lenid[(size_t)b * kSkyMaxK + lane] = k2;
+        if (lane == K - 1) {
+            A.s.lenkth[2 * (size_t)b] = cnt > K ? k1 : 0ull;
+            A.s.lenkth[2 * (size_t)b + 1] = cnt > K ? k2 : 0ull;
+        }
+    };
+    if (BIG) {
+        const int nbig = *A.s.nbig;
+        for (int x = blockIdx.x; x < nbig; x += gridDim.x) {
+            const int b = A.s.biglist[x];
+            const int beg = A.s.bcnt[b], end = A.s.bcnt[b + 1], c = end - beg;
+            const int per = (c + nwarp - 1) / nwarp;
+            const int sb = min(end, beg + warp * per), se = min(end, sb + per);
+            u64 k1, k2;
+            scan(sb, se, &k1, &k2);
+            s1[warp][lane] = k1;
+            s2[warp][lane] = k2;
+            __syncthreads();
+            if (warp < 2) {
+                u64 (*s)[32] = warp == 0 ? s1 : s2;
+                u64 t = s[0][lane];
+                for (int w = 1; w < nwarp; w++) t = topk_merge_sorted(t, s[w][lane], K, lane);
+                s[0][lane] = t;
+            }
+            __syncthreads();
+            if (warp == 0) emit(b, c, s1[0][lane], s2[0][lane]);
+            __syncthreads();
+        }
+    } else {
+        const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+        for (int b = 2 + w0; b < A.sky_nbins; b += nw) {
+            const int beg = A.s.bcnt[b], end = A.s.bcnt[b + 1], c = end - beg;
+            if (c > kSkyBig && lane == 0) A.s.biglist[atomicAdd(A.s.nbig, 1)] = b;   // the CTA kernel's
+            if (c == 0 || c > kSkyBig) continue;
+            u64 k1, k2;
+            scan(beg, end, &k1, &k2);
+            emit(b, c, k1, k2);
         }
     }
 }
-// K3e: one warp per block of kSkyBlk lengths of one position: the top K candidate
+// K3e: one CTA per block of kSkyBlk lengths of one position: the top K candidate
 // keys (by f1) and the K lowest candidate ids of the block, merged from the
 // per-length lists (the block's top K by f1 among all its candidates are among
-// the lengths' top K by f1, and likewise for the ids)
-__global__ void __launch_bounds__(kSwPrepThreads) sky_block_kernel(const __grid_constant__ SweepArgs A) {
-    __shared__ u64 sbuf[kSwPrepThreads / 32][32];
-    const int lane = threadIdx.x & 31;
-    u64* sb = sbuf[threadIdx.x >> 5];
-    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+// the lengths' top K by f1, and likewise for the ids).  Warp w merges lengths
+// w, w + 16, ... of the block, warps 0 / 1 merge the 16 partial lists.
+__global__ void __launch_bounds__(kSwPrepThreads) sky_block_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
+    __shared__ u64 s1[kSwPrepThreads / 32][32], s2[kSwPrepThreads / 32][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     const int K = A.K;
     const int nblk = A.qblk[A.nq];
-    for (int g = w0; g < nblk; g += nw) {
+    for (int g = blockIdx.x; g < nblk; g += gridDim.x) {
         int p = 0;
         while (p + 1 < A.nq && A.qblk[p + 1] <= g) p++;
         const int jj = g - A.qblk[p];
         const int blo = A.qbin_lo[p] + jj * kSkyBlk, bhi = min(blo + kSkyBlk, A.qbin_hi[p]);
-        // item j = (length blo + j / 32, list slot j % 32): one length per warp row
-        auto item = [&](const u64* lists, int j) -> u64 {
-            const int b = blo + (j >> 5), l = j & 31;
-            const int n_b = min(A.s.bcnt[b + 1] - A.s.bcnt[b], K);
-            return l < n_b ? lists[(size_t)b * kSkyMaxK + l] : 0ull;
-        };
-        const int nit = (bhi - blo) * 32;
-        const u64 k1 = sky_warp_topk(0, nit, K, [&](int j) { return item(A.s.lentop, j); }, sb);
-        const u64 k2 = sky_warp_topk(0, nit, K, [&](int j) { return item(A.s.lenid, j); }, sb);
-        A.s.blktop[(size_t)g * kSkyMaxK + lane] = k1;
-        A.s.blkid[(size_t)g * kSkyMaxK + lane] = k2;
+        u64 t1 = 0ull, t2 = 0ull;
+        for (int b = blo + warp; b < bhi; b += nwarp) {
+            if (A.s.bcnt[b + 1] == A.s.bcnt[b]) continue;   // no records: its lists are stale
+            t1 = topk_merge_sorted(t1, A.s.lentop[(size_t)b * kSkyMaxK + lane], K, lane);
+            t2 = topk_merge_sorted(t2, A.s.lenid[(size_t)b * kSkyMaxK + lane], K, lane);
+        }
+        s1[warp][lane] = t1;
+        s2[warp][lane] = t2;
+        __syncthreads();
+        if (warp < 2) {
+            u64 (*sl)[32] = warp == 0 ? s1 : s2;
+            u64 t = sl[0][lane];
+            for (int w = 1; w < nwarp; w++) t = topk_merge_sorted(t, sl[w][lane], K, lane);
+            (warp == 0 ? A.s.blktop : A.s.blkid)[(size_t)g * kSkyMaxK + lane] = lane < K ? t : 0ull;
+        }
+        __syncthreads();
     }
 }
-// K3f: one warp per position: prefix over its blocks -> pref[g] = high word (f1) of
-// the K-th largest candidate key of the blocks before g (0 while fewer than K);
-// and qidk[p] = the queue's K-th lowest candidate id key (all weights 0: every
-// member scores 0 and the K lowest ids are the answer, R24)
-__device__ __forceinline__ u64 sky_merge_topk(u64 run, u64 add, int K, u64* sb, int* n_out) {
-    const int lane = threadIdx.x & 31;
-    u64 v[2] = {run, add};
-    int nz = (v[0] != 0ull) + (v[1] != 0ull);
-    nz = __reduce_add_sync(0xffffffffu, nz);
-    const u64 t = nz > K ? warp_kth_regs<2>(v, K) : 1ull;
-    int base = 0;
-#pragma unroll
-    for (int r = 0; r < 2; r++) {
-        const bool keep = v[r] && v[r] >= t;
-        const unsigned m = __ballot_sync(0xffffffffu, keep);
-        if (keep) sb[base + __popc(m & ((1u << lane) - 1u))] = v[r];
-        base += __popc(m);
-    }
-    __syncwarp();
-    const u64 out = lane < base ? sb[lane] : 0ull;
-    __syncwarp();
-    *n_out = base;
-    return out;
-}
-__global__ void sky_prefix_kernel(const __grid_constant__ SweepArgs A) {
-    __shared__ u64 sb[32];
-    const int lane = threadIdx.x & 31;
+// K3f: one CTA per position.  pref[g] = high word (f1) of the K-th largest candidate
+// key of the position's blocks before g (0 while fewer than K): an inclusive
+// Hillis-Steele scan of the blocks' top-K lists (merge = top K of the union) in
+// shared memory, segments of kSkyScanSeg blocks with a carried prefix.  qidk[p] =
+// the queue's K-th lowest candidate id key (all weights 0: every member scores 0
+// and the K lowest ids are the answer, R24), 0 while fewer than K.
+constexpr int kSkyScanSeg = 128;
+constexpr int kSkyPrefThreads = 1024;
+__global__ void __launch_bounds__(kSkyPrefThreads) sky_prefix_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
+    extern __shared__ u64 s_l[];                       // [2][kSkyScanSeg][32]
+    __shared__ u64 s_carry[32], s_id[kSkyPrefThreads / 32][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     const int p = blockIdx.x;
     if (p >= A.nq) return;
     const int K = A.K;
-    u64 run = 0ull, rid = 0ull;
-    int nrun = 0, nid = 0;
-    u64 kth = 0ull, kid = 0ull;         // K-th key of run / rid once they hold K keys (their minimum)
-    for (int g = A.qblk[p]; g < A.qblk[p + 1]; g++) {
-        if (lane == 0) A.s.pref[g] = (u32)(kth >> 32);
-        const u64 a1 = A.s.blktop[(size_t)g * kSkyMaxK + lane], a2 = A.s.blkid[(size_t)g * kSkyMaxK + lane];
-        // a block with no key above the current K-th leaves the running top K as it is
-        if (__any_sync(0xffffffffu, a1 > kth)) {
-            run = sky_merge_topk(run, a1, K, sb, &nrun);
-            if (nrun >= K) kth = warp_min_u64(run ? run : ~0ull);
-        }
-        if (__any_sync(0xffffffffu, a2 > kid)) {
-            rid = sky_merge_topk(rid, a2, K, sb, &nid);
-            if (nid >= K) kid = warp_min_u64(rid ? rid : ~0ull);
-        }
+    const int g0 = A.qblk[p], g1 = A.qblk[p + 1];
+    auto kth_hi = [&](u64 top) -> u32 {                // high word of the K-th of a list (0: < K keys)
+        return (u32)(__shfl_sync(0xffffffffu, top, K - 1) >> 32);
+    };
+    if (warp == 0) s_carry[lane] = 0ull;
+    // the id lists: each warp folds its share of the blocks, warp 0 folds the warps
+    u64 ti = 0ull;
+    for (int g = g0 + warp; g < g1; g += nwarp) ti = topk_merge_sorted(ti, A.s.blkid[(size_t)g * kSkyMaxK + lane], K, lane);
+    s_id[warp][lane] = ti;
+    __syncthreads();
+    for (int d = 1; d < nwarp; d <<= 1) {                // tree fold of the warps' lists
+        if ((warp & (2 * d - 1)) == 0 && warp + d < nwarp)
+            s_id[warp][lane] = topk_merge_sorted(s_id[warp][lane], s_id[warp + d][lane], K, lane);
+        __syncthreads();
     }
-    if (lane == 0) A.s.qidk[p] = kid;   // 0: fewer than K candidates, keep them all
+    if (warp == 0) {
+        const u64 kid = __shfl_sync(0xffffffffu, s_id[0][lane], K - 1);
+        if (lane == 0) A.s.qidk[p] = kid;
+    }
+    for (int s0 = g0; s0 < g1; s0 += kSkyScanSeg) {
+        const int n = min(kSkyScanSeg, g1 - s0);
+        u64* in = s_l;
+        u64* out = s_l + kSkyScanSeg * 32;
+        for (int j = warp; j < n; j += nwarp) in[j * 32 + lane] = A.s.blktop[(size_t)(s0 + j) * kSkyMaxK + lane];
+        __syncthreads();
+        if (warp == 0) in[lane] = topk_merge_sorted(s_carry[lane], in[lane], K, lane);   // block s0 includes the carry
+        __syncthreads();
+        for (int d = 1; d < n; d <<= 1) {
+            for (int j = warp; j < n; j += nwarp)
+                out[j * 32 + lane] = j >= d ? topk_merge_sorted(in[(j - d) * 32 + lane], in[j * 32 + lane], K, lane) : in[j * 32 + lane];
+            __syncthreads();
+            u64* t = in; in = out; out = t;
+        }
+        // exclusive: block s0 + j is bounded by the inclusive prefix of s0 + j - 1
+        for (int j = warp; j < n; j += nwarp) {
+            const u32 h = j == 0 ? kth_hi(s_carry[lane]) : kth_hi(in[(j - 1) * 32 + lane]);
+            if (lane == 0) A.s.pref[s0 + j] = h;
+        }
+        __syncthreads();
+        if (warp == 0) s_carry[lane] = in[(n - 1) * 32 + lane];
+        __syncthreads();
+    }
 }
-__device__ __forceinline__ bool sky_keep(const SweepArgs& A, int64_t i, const float4& f, int p) {
+__device__ __forceinline__ bool sky_keep(const SweepArgs& A, const float4& f, int p) {
     const int b = sky_len(f);
     if (!sky_grouped(A, p, b)) return true;
-    if (!A.s.cand[i]) return false;
-    if (sky_idkey(f) >= A.s.qidk[p]) return true;          // among the queue's K lowest ids
+    const u64 k1 = sky_key(f), k2 = sky_idkey(f);
+    if (!(k1 >= A.s.lenkth[2 * (size_t)b] || k2 >= A.s.lenkth[2 * (size_t)b + 1])) return false;   // not in its length's lists
+    if (k2 >= A.s.qidk[p]) return true;                    // among the queue's K lowest ids
     const int g = A.qblk[p] + (b - A.qbin_lo[p]) / kSkyBlk;
     return __float_as_uint(f.y) > A.s.pref[g];
 }
 // K3g: survivors per position, then (plan2, one thread) the compacted layout, then the scatter
-__global__ void __launch_bounds__(kSwPrepThreads) sky_count_kernel(const __grid_constant__ SweepArgs A) {
-    const int64_t ntot = A.s.qoff[A.nq];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += (int64_t)gridDim.x * blockDim.x) {
-        const float4 f = A.s.rec[i];
-        const int p = sky_pos(A, i);
-        if (sky_keep(A, i, f, p)) atomicAdd((unsigned long long*)&A.s.qcnt2[p], 1ull);
+__global__ void __launch_bounds__(kSwPrepThreads) sky_count_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
+    __shared__ int64_t s_qoff[kMaxSlots + 1];
+    __shared__ unsigned s_cnt[kMaxSlots];
+    for (int q = threadIdx.x; q <= A.nq; q += blockDim.x) s_qoff[q] = A.s.qoff[q];
+    for (int q = threadIdx.x; q < kMaxSlots; q += blockDim.x) s_cnt[q] = 0u;
+    __syncthreads();
+    int64_t i0, i1;
+    sw_cta_range(s_qoff[A.nq], &i0, &i1);
+    int p = i0 < i1 ? sky_pos_search(s_qoff, A.nq, i0 + threadIdx.x) : 0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        p = sky_pos_from(s_qoff, A.nq, p, i);
+        if (sky_keep(A, A.s.rec[i], p)) atomicAdd(&s_cnt[p], 1u);
     }
+    __syncthreads();
+    for (int q = threadIdx.x; q < A.nq; q += blockDim.x)
+        if (s_cnt[q]) atomicAdd((unsigned long long*)&A.s.qcnt2[q], (unsigned long long)s_cnt[q]);
 }
-__global__ void sky_plan_kernel(const __grid_constant__ SweepArgs A) {
+__global__ void sky_plan_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
     if (threadIdx.x != 0) return;
     int64_t off = 0;
     int32_t cp = 0;
@@ -483,17 +645,24 @@ __global__ void sky_plan_kernel(const __grid_constant__ SweepArgs A) {
     for (int q = 0; q < A.nq; q++) mx = A.s.qcnt2[q] > mx ? A.s.qcnt2[q] : mx;
     *A.s.direct = mx <= kSwDirectMax;
 }
-__global__ void __launch_bounds__(kSwPrepThreads) sky_compact_kernel(const __grid_constant__ SweepArgs A) {
-    const int64_t ntot = A.s.qoff[A.nq];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot; i += (int64_t)gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(kSwPrepThreads) sky_compact_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
+    __shared__ int64_t s_qoff[kMaxSlots + 1];
+    for (int q = threadIdx.x; q <= A.nq; q += blockDim.x) s_qoff[q] = A.s.qoff[q];
+    __syncthreads();
+    int64_t i0, i1;
+    sw_cta_range(s_qoff[A.nq], &i0, &i1);
+    int p = i0 < i1 ? sky_pos_search(s_qoff, A.nq, i0 + threadIdx.x) : 0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        p = sky_pos_from(s_qoff, A.nq, p, i);
         const float4 f = A.s.rec[i];
-        const int p = sky_pos(A, i);
-        if (sky_keep(A, i, f, p)) A.s.rec2[A.s.qoff2[p] + atomicAdd(&A.s.qfill2[p], 1)] = f;
+        if (sky_keep(A, f, p)) A.s.rec2[A.s.qoff2[p] + atomicAdd(&A.s.qfill2[p], 1)] = f;
     }
 }
 
 // K4: persistent warps over tasks (Θ block, queue, chunk).
-__global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const __grid_constant__ SweepArgs A) {
+__global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const SweepArgs* __restrict__ Ap, int phase) {
+    const SweepArgs& A = *Ap;
     extern __shared__ __align__(16) unsigned char smem[];
     if (*A.s.direct) return;                      // K5d handles this sweep
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -517,7 +686,7 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const __gri
     const int nblocks = (A.n_theta + kSwT - 1) / kSwT;
     // Phase 0 processes the first chunk of every (Θ block, queue) so that the
     // exact K-th keys it publishes filter phase 1 from its first record on.
-    const int total = A.phase == 0 ? nblocks * A.nq : nblocks * nchunks;
+    const int total = phase == 0 ? nblocks * A.nq : nblocks * nchunks;
     unsigned long long d_ins = 0, d_cuts = 0;     // diagnostics, one atomic per warp at the end
     for (;;) {
         int task = 0;
@@ -525,7 +694,7 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const __gri
         task = __shfl_sync(0xffffffffu, task, 0);
         if (task >= total) break;
         int blk, q, chunk;
-        if (A.phase == 0) {
+        if (phase == 0) {
             // seeding: per Θ of the block, a valid bound of the K-th key among the
             // queue's first 256 records (scores in registers, register selection)
             blk = task / A.nq;
@@ -685,7 +854,8 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const __gri
 
 // K2b: A7 for the batch on the device, the same canonical fp64 expression as
 // ewsjf_weights_from_meta (round(a·b̄) + b, no contraction, clamp, fp32).
-__global__ void sweep_weights_kernel(const __grid_constant__ SweepArgs A) {
+__global__ void sweep_weights_kernel(const SweepArgs* __restrict__ Ap) {
+    const SweepArgs& A = *Ap;
     for (int i = threadIdx.x; i < A.n_theta * A.nq; i += blockDim.x) {
         const int t = i / A.nq, q = i % A.nq;
         float* w = A.s.w + ((size_t)t * kMaxSlots + q) * 3;
@@ -704,7 +874,8 @@ struct SweepOutArgs {
 };
 
 // K5: one warp per (Θ, queue): merge the rows of the queue's chunks.
-__global__ void __launch_bounds__(kSwWarps * 32) sweep_merge_kernel(const __grid_constant__ SweepOutArgs A) {
+__global__ void __launch_bounds__(kSwWarps * 32) sweep_merge_kernel(const SweepOutArgs* __restrict__ Ap) {
+    const SweepOutArgs& A = *Ap;
     extern __shared__ __align__(16) unsigned char smem[];
     if (*A.s.direct) return;                      // K5d handles this sweep
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -779,12 +950,8 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_merge_kernel(const __grid
 // chunk across the lanes and merges it into the running top 32 (one key per lane,
 // descending: the elementwise max of the list and the reversed chunk is bitonic,
 // a 5-step merge sorts it).  Same keys and outputs as K4 + K5.
-__device__ __forceinline__ u64 sw_bitonic_step(u64 v, int lane, int j, bool up) {
-    const u64 o = shfl_xor_u64(v, j);
-    const bool keep_max = ((lane & j) == 0) == up;
-    return keep_max ? (o > v ? o : v) : (o < v ? o : v);
-}
-__global__ void __launch_bounds__(kSwWarps * 32) sweep_direct_kernel(const __grid_constant__ SweepOutArgs A) {
+__global__ void __launch_bounds__(kSwWarps * 32) sweep_direct_kernel(const SweepOutArgs* __restrict__ Ap) {
+    const SweepOutArgs& A = *Ap;
     if (!*A.s.direct) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int item = blockIdx.x * kSwWarps + warp;
@@ -795,23 +962,19 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_direct_kernel(const __gri
     const float w0 = w[0], w1 = w[1], w2 = w[2];
     const int64_t b0 = A.s.qoff[q], b1 = A.s.qoff[q + 1];
     u64 top = 0ull;                                   // lane i: the (i+1)-th best key so far
-    for (int64_t e0 = b0; e0 < b1; e0 += 32) {
-        const int64_t e = e0 + lane;
-        u64 v = 0ull;
-        if (e < b1) {
-            const float4 f = __ldg(&A.s.rec[e]);
-            v = score_key(fmaf(w2, f.z, fmaf(w1, f.y, w0 * f.x)), __float_as_uint(f.w));
+    for (int64_t e0 = b0; e0 < b1; e0 += 256) {       // 8 chunks of 32 loaded at a time
+        float4 f[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int64_t e = e0 + 32 * u + lane;
+            f[u] = e < b1 ? __ldg(&A.s.rec[e]) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        const u64 kth = __shfl_sync(0xffffffffu, top, K - 1);
-        if (!__any_sync(0xffffffffu, v > kth)) continue;
 #pragma unroll
-        for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-            for (int j = k >> 1; j > 0; j >>= 1) v = sw_bitonic_step(v, lane, j, (lane & k) == 0 || k == 32);
-        const u64 r = shfl_xor_u64(v, 31);            // the chunk reversed (ascending)
-        top = r > top ? r : top;                      // bitonic: the best 32 of both
-#pragma unroll
-        for (int j = 16; j > 0; j >>= 1) top = sw_bitonic_step(top, lane, j, true);
+        for (int u = 0; u < 8; u++) {
+            const bool ok = e0 + 32 * u + lane < b1;
+            const u64 v = ok ? score_key(fmaf(w2, f[u].z, fmaf(w1, f[u].y, w0 * f[u].x)), __float_as_uint(f[u].w)) : 0ull;
+            top = topk_add(top, v, K, lane);
+        }
     }
     const ewsjf_select_out& o = A.outs[th];
     const float qi = (float)(q + 1);
@@ -837,7 +1000,8 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_direct_kernel(const __gri
 }
 
 // K6: one warp per Θ: Alg. 1 ArgMax over non-empty queues (ties -> lowest position, R24).
-__global__ void sweep_summary_kernel(const __grid_constant__ SweepOutArgs A) {
+__global__ void sweep_summary_kernel(const SweepOutArgs* __restrict__ Ap) {
+    const SweepOutArgs& A = *Ap;
     const int th = blockIdx.x;
     if (th >= A.n_theta || threadIdx.x != 0) return;
     const ewsjf_select_out& o = A.outs[th];
@@ -862,10 +1026,29 @@ __global__ void sweep_summary_kernel(const __grid_constant__ SweepOutArgs A) {
 }
 
 
+// Upload one argument block into the next ring slot (stream-ordered); returns its device copy.
+template <typename T>
+static const T* sw_upload(ewsjf_ctx* ctx, const T& a) {
+    SweepScratch* S = ctx->sw;
+    const int i = S->arg_next;
+    S->arg_next = (i + 1) % SweepScratch::kArgSlots;
+    if (cudaEventSynchronize(S->arg_ev[i]) != cudaSuccess) return nullptr;   // its previous copy has run
+    unsigned char* h = S->h_args + (size_t)i * S->arg_slot;
+    unsigned char* d = S->d_args + (size_t)i * S->arg_slot;
+    memcpy(h, &a, sizeof(T));
+    if (cudaMemcpyAsync(d, h, sizeof(T), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+        cudaEventRecord(S->arg_ev[i], ctx->stream) != cudaSuccess)
+        return nullptr;
+    return (const T*)d;
+}
+
 void sweep_free(ewsjf_ctx* ctx) {
     SweepScratch* S = ctx->sw;
     if (!S) return;
-    void* d[] = {S->direct, S->lentop, S->lenid, S->blkid, S->qidk, S->bcnt, S->bfill, S->srt, S->cand, S->blktop, S->pref, S->rec2, S->qoff2, S->cpre2, S->qfill2,
+    for (auto e : S->arg_ev)
+        if (e) cudaEventDestroy(e);
+    if (S->h_args) cudaFreeHost(S->h_args);
+    void* d[] = {S->d_args, S->direct, S->lentop, S->lenid, S->blkid, S->qidk, S->bcnt, S->bfill, S->lenkth, S->biglist, S->nbig, S->blktop, S->pref, S->rec2, S->qoff2, S->cpre2, S->qfill2,
                  S->qcnt2, S->rec, S->qcount, S->qoff, S->cpre, S->qfill, S->head, S->headf, S->bad, S->task_ctr, S->gthr,
                  S->rows, S->rowcnt, S->w};
     for (void* p : d)
@@ -906,6 +1089,9 @@ ewsjf_status sweep_alloc(ewsjf_ctx* ctx, int64_t n, int64_t tasks, int K) {
                   cudaMalloc(&S->blkid, 8 * (size_t)kSkyMaxBlocks * kSkyMaxK) == cudaSuccess &&
                   cudaMalloc(&S->lentop, 8 * (size_t)kSkyBins * kSkyMaxK) == cudaSuccess &&
                   cudaMalloc(&S->lenid, 8 * (size_t)kSkyBins * kSkyMaxK) == cudaSuccess &&
+                  cudaMalloc(&S->lenkth, 16 * (size_t)kSkyBins) == cudaSuccess &&
+                  cudaMalloc(&S->biglist, 4 * (size_t)kSkyBins) == cudaSuccess &&
+                  cudaMalloc(&S->nbig, 4) == cudaSuccess &&
                   cudaMalloc(&S->qidk, 8 * kMaxSlots) == cudaSuccess &&
                   cudaMalloc(&S->pref, 4 * (size_t)kSkyMaxBlocks) == cudaSuccess &&
                   cudaMalloc(&S->qoff2, 8 * (kMaxSlots + 1)) == cudaSuccess &&
@@ -913,16 +1099,19 @@ ewsjf_status sweep_alloc(ewsjf_ctx* ctx, int64_t n, int64_t tasks, int K) {
                   cudaMalloc(&S->qfill2, 4 * kMaxSlots) == cudaSuccess &&
                   cudaMalloc(&S->qcnt2, 8 * kMaxSlots) == cudaSuccess &&
                   cudaMalloc(&S->direct, 4) == cudaSuccess;
+        S->arg_slot = (std::max(sizeof(SweepArgs), sizeof(SweepOutArgs)) + 255) & ~(size_t)255;
+        ok = ok && cudaMallocHost(&S->h_args, S->arg_slot * SweepScratch::kArgSlots) == cudaSuccess &&
+             cudaMalloc(&S->d_args, S->arg_slot * SweepScratch::kArgSlots) == cudaSuccess;
+        for (auto& e : S->arg_ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
         if (!ok) return fail(ctx, EWSJF_ERR_CUDA, "sweep scratch allocation failed");
     }
     if (S->n_cap < n) {
-        for (void* x : {(void*)S->rec, (void*)S->rec2, (void*)S->srt, (void*)S->cand})
+        for (void* x : {(void*)S->rec, (void*)S->rec2})
             if (x) cudaFree(x);
-        S->rec = S->rec2 = nullptr; S->srt = nullptr; S->cand = nullptr;
+        S->rec = S->rec2 = nullptr;
         S->n_cap = 0;
         const size_t nn = (size_t)std::max<int64_t>(n, 1);
-        if (cudaMalloc(&S->rec, 16 * nn) != cudaSuccess || cudaMalloc(&S->rec2, 16 * nn) != cudaSuccess ||
-            cudaMalloc(&S->srt, 4 * nn) != cudaSuccess || cudaMalloc(&S->cand, nn) != cudaSuccess)
+        if (cudaMalloc(&S->rec, 16 * nn) != cudaSuccess || cudaMalloc(&S->rec2, 16 * nn) != cudaSuccess)
             return fail(ctx, EWSJF_ERR_CUDA, "sweep records allocation failed");
         S->n_cap = n;
     }
@@ -1007,32 +1196,9 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
     for (int i = 0; i < nq; i++) { A.sorted_ids[i] = ids[i].first; A.sorted_pos[i] = ids[i].second; }
     for (int i = 0; i < nq; i++) A.mean[i] = part->q[i].mean;
     A.s = *S;
-    cudaStream_t st = ctx->stream;
-    CU(cudaMemsetAsync(S->qcount, 0, 8 * kMaxSlots, st));
-    CU(cudaMemsetAsync(S->head, 0, 8 * kMaxSlots, st));
-    CU(cudaMemsetAsync(S->bad, 0, 32, st));
-    const int pgrid = std::max(1, std::min(ctx->num_sms * 4, (int)((n + kSwPrepThreads - 1) / kSwPrepThreads)));
-    {
-        LaunchScope ls(ctx, KIND_SWEEP);
-        sweep_count_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
-    }
-    {
-        LaunchScope ls(ctx, KIND_SWEEP);
-        sweep_plan_kernel<<<1, 32, 0, st>>>(A);
-    }
-    {
-        LaunchScope ls(ctx, KIND_SWEEP);
-        sweep_scatter_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
-    }
-    CU(cudaGetLastError());
-    // Θ-independent candidate prefilter (K <= 32): the select kernels run over the
-    // records no other K records dominate in every feature
     const bool sky = K <= kSkyMaxK && !getenv("EWSJF_NO_SKY");
-    S->last_nq = nq;
-    S->last_sky = sky;
-    CU(cudaMemsetAsync(S->direct, 0, 4, st));      // sky_plan sets it when the survivors are few
+    int nb = 0;
     if (sky) {
-        int nb = 0;
         for (int p = 0; p < nq; p++) {
             int lo = std::max(2, part->q[p].min_len), hi = std::min(part->q[p].max_len, kSkyBins);
             if (lo >= hi) lo = hi = 0;
@@ -1040,19 +1206,58 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
             nb += (hi - lo + kSkyBlk - 1) / kSkyBlk;
         }
         A.qblk[nq] = nb;
+        int maxhi = 0;
+        for (int p = 0; p < nq; p++) maxhi = std::max(maxhi, A.qbin_hi[p]);
+        A.sky_nbins = std::min(kSkyBins, std::max(1024, (maxhi + 1 + 1023) & ~1023));
+    }
+    cudaStream_t st = ctx->stream;
+    CU(cudaMemsetAsync(S->qcount, 0, 8 * kMaxSlots, st));
+    CU(cudaMemsetAsync(S->head, 0, 8 * kMaxSlots, st));
+    CU(cudaMemsetAsync(S->bad, 0, 32, st));
+    const int pgrid = std::max(1, std::min(ctx->num_sms * 4, (int)((n + kSwPrepThreads - 1) / kSwPrepThreads)));
+    const SweepArgs* dA = sw_upload(ctx, A);
+    if (!dA) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
+    {
+        LaunchScope ls(ctx, KIND_SWEEP);
+        sweep_count_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(dA);
+    }
+    {
+        LaunchScope ls(ctx, KIND_SWEEP);
+        sweep_plan_kernel<<<1, 32, 0, st>>>(dA);
+    }
+    {
+        LaunchScope ls(ctx, KIND_SWEEP);
+        sweep_scatter_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(dA);
+    }
+    CU(cudaGetLastError());
+    // Θ-independent candidate prefilter (K <= 32): the select kernels run over the
+    // records no other K records dominate in every feature
+    S->last_nq = nq;
+    S->last_sky = sky;
+    CU(cudaMemsetAsync(S->direct, 0, 4, st));      // sky_plan sets it when the survivors are few
+    if (sky) {
         CU(cudaMemsetAsync(S->bcnt, 0, 4 * (size_t)(kSkyBins + 1), st));
+        CU(cudaMemsetAsync(S->nbig, 0, 4, st));
         CU(cudaMemsetAsync(S->qcnt2, 0, 8 * kMaxSlots, st));
         const int sgrid = ctx->num_sms * 4;
+        const size_t pref_smem = 2 * (size_t)kSkyScanSeg * 32 * 8;
+        if (!S->sky_attr) {   // per ctx (its device)
+            CU(cudaFuncSetAttribute(sky_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem));
+            CU(cudaFuncSetAttribute(sky_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem));
+            CU(cudaFuncSetAttribute(sky_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pref_smem));
+            S->sky_attr = true;
+        }
         LaunchScope ls(ctx, KIND_SWEEP);
-        sky_hist_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
-        sky_scan_kernel<<<1, 1024, 0, st>>>(A);
-        sky_scatter_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
-        sky_group_kernel<<<sgrid, kSwPrepThreads, 0, st>>>(A);
-        sky_block_kernel<<<std::max(1, std::min(sgrid, (nb + 15) / 16)), kSwPrepThreads, 0, st>>>(A);
-        sky_prefix_kernel<<<nq, 32, 0, st>>>(A);
-        sky_count_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
-        sky_plan_kernel<<<1, 32, 0, st>>>(A);
-        sky_compact_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(A);
+        sky_hist_kernel<<<ctx->num_sms, kSortThreads, kSortSmem, st>>>(dA);
+        sky_scan_kernel<<<1, 1024, 0, st>>>(dA);
+        sky_scatter_kernel<<<ctx->num_sms, kSortThreads, kSortSmem, st>>>(dA);
+        sky_group_kernel<false><<<sgrid, kSwPrepThreads, 0, st>>>(dA);
+        sky_group_kernel<true><<<ctx->num_sms * 2, kSwPrepThreads, 0, st>>>(dA);
+        sky_block_kernel<<<std::max(1, std::min(ctx->num_sms * 3, nb)), kSwPrepThreads, 0, st>>>(dA);
+        sky_prefix_kernel<<<nq, kSkyPrefThreads, pref_smem, st>>>(dA);
+        sky_count_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(dA);
+        sky_plan_kernel<<<1, 32, 0, st>>>(dA);
+        sky_compact_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(dA);
         CU(cudaGetLastError());
         // the select / merge kernels read the survivors
         A.s.rec = S->rec2; A.s.qoff = S->qoff2; A.s.cpre = S->cpre2;
@@ -1075,33 +1280,36 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
             A.theta[t][3] = m.b_u; A.theta[t][4] = m.a_f; A.theta[t][5] = m.b_f;
         }
         CU(cudaMemsetAsync(S->gthr, 0, 8 * (size_t)kSwBatch * kMaxSlots, st));
+        const SweepArgs* dB = sw_upload(ctx, A);
+        if (!dB) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
         {
             LaunchScope ls(ctx, KIND_SWEEP);
-            sweep_weights_kernel<<<1, 256, 0, st>>>(A);
+            sweep_weights_kernel<<<1, 256, 0, st>>>(dB);
         }
         const int occ = S->occ;
         for (int ph = 0; ph < 2; ph++) {
-            A.phase = ph;
             CU(cudaMemsetAsync(S->task_ctr, 0, 4, st));
             LaunchScope ls(ctx, KIND_SWEEP);
-            sweep_select_kernel<<<ctx->num_sms * std::max(occ, 1), kSwWarps * 32, sel_smem, st>>>(A);
+            sweep_select_kernel<<<ctx->num_sms * std::max(occ, 1), kSwWarps * 32, sel_smem, st>>>(dB, ph);
         }
         O.s = A.s; O.nq = nq; O.K = K; O.cap = A.cap; O.n_theta = nb; O.rcap = A.rcap;
         for (int t = 0; t < nb; t++) {
             O.outs[t] = outs[b0 + t];
             O.outs[t].h_summary = nullptr;
         }
+        const SweepOutArgs* dO = sw_upload(ctx, O);
+        if (!dO) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
         {
             LaunchScope ls(ctx, KIND_SWEEP);
-            sweep_merge_kernel<<<(nb * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, mrg_smem, st>>>(O);
+            sweep_merge_kernel<<<(nb * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, mrg_smem, st>>>(dO);
         }
         if (sky) {
             LaunchScope ls(ctx, KIND_SWEEP);
-            sweep_direct_kernel<<<(nb * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, 0, st>>>(O);
+            sweep_direct_kernel<<<(nb * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, 0, st>>>(dO);
         }
         {
             LaunchScope ls(ctx, KIND_SWEEP);
-            sweep_summary_kernel<<<nb, 32, 0, st>>>(O);
+            sweep_summary_kernel<<<nb, 32, 0, st>>>(dO);
         }
         CU(cudaGetLastError());
     }

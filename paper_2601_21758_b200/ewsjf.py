@@ -15,7 +15,7 @@ from . import _lib as L
 
 __all__ = [
     "EwsjfError", "Context", "make_partition", "meta", "select_params", "partition_params", "weights_from_meta",
-    "Outputs", "tick", "tick_host", "score_select", "route", "partition", "score_select_sweep",
+    "Outputs", "tick", "tick_host", "score_select", "route", "partition", "score_select_sweep", "meta_array",
     "exchange_bytes", "tick_local", "tick_merge", "tick_sharded", "batch_build", "prune_empty",
     "alloc_count", "history_hist", "partition_from_hist", "reduce_hist", "check_reduced", "partition_sharded", "online_adjust",
 ]
@@ -367,13 +367,30 @@ def partition_sharded(ctx: Context, length_shard, params: L.PartitionParams | No
     return partition_from_hist(ctx, hist, info["max_len"], info["invalid"], params)
 
 
+_SWEEP_OUT_CACHE: dict = {}
+
+
+def meta_array(thetas: list[L.Meta]):
+    """A ctypes array of Θ for score_select_sweep (built once, reused across calls)."""
+    return (L.Meta * len(thetas))(*thetas)
+
+
 def score_select_sweep(ctx: Context, length, arrival, cost, qid, part: L.Partition, thetas: list[L.Meta],
                        params: L.SelectParams, outs: list[Outputs] | None = None) -> list[Outputs]:
     """ewsjf_score_select_sweep: one selection per Θ over one routed snapshot (A12)."""
     n_theta = len(thetas)
     outs = outs or [Outputs.alloc(params.k, length.device) for _ in range(n_theta)]
-    th = (L.Meta * n_theta)(*thetas)
-    so = (L.SelectOut * n_theta)(*[o.struct() for o in outs])
+    # thetas may be a prebuilt ctypes array (meta_array): no per-call conversion
+    th = thetas if isinstance(thetas, C.Array) else (L.Meta * n_theta)(*thetas)
+    # the output descriptor array of a given list of Outputs is built once (their tensors
+    # are fixed at allocation); building 256 of them per call took ~1 ms of host time
+    key = tuple(map(id, outs))
+    so = _SWEEP_OUT_CACHE.get(key)
+    if so is None or so[0] is not outs[0]:
+        so = (outs[0], (L.SelectOut * n_theta)(*[o.struct() for o in outs]))
+        _SWEEP_OUT_CACHE.clear()
+        _SWEEP_OUT_CACHE[key] = so
+    so = so[1]
     ctx.use_current_stream()
     s = ctx.lib.ewsjf_score_select_sweep(ctx.h, _ptr(length), _ptr(arrival), _ptr(cost), _ptr(qid), length.numel(),
                                          C.byref(part), th, n_theta, C.byref(params), so)
