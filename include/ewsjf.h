@@ -206,8 +206,13 @@ typedef struct {
  * k<=3 (Stage 1, A3), Eq. 2 refinement (Stage 2, A4), midpoint finalisation
  * (A5), Eq. 3 pruning (Stage 3, A6).  Writes *out (ids 0..n-1, version
  * incremented from out->version) and optional *stats.  Synchronises.
- * Lengths < 1 are excluded and counted (DOMAIN); lengths above 2^20 ->
- * UNSUPPORTED; n > max_history -> INVALID_ARG; no valid length -> EMPTY.    */
+ * Lengths < 1 are excluded and counted (DOMAIN).  Lengths >= 2^20 (long
+ * prompts) are collected into an overflow list, sorted on the device and
+ * appended as runs after the histogram's (A1 long tail): up to 32768 of them
+ * per call and 2^20 distinct lengths in all, else UNSUPPORTED; every length
+ * must stay below 2^31 - 1 (queue bounds are int32).  sumsq wraps modulo
+ * 2^64 once sum(c b^2) exceeds 2^63 (no decision reads it).  n > max_history
+ * -> INVALID_ARG; no valid length -> EMPTY.                                 */
 ewsjf_status ewsjf_partition(ewsjf_ctx *ctx, const int32_t *d_len, int64_t n,
                              const ewsjf_partition_params *params, ewsjf_partition_t *out,
                              ewsjf_partition_stats *stats);

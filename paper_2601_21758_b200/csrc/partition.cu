@@ -23,7 +23,8 @@
 
 namespace ewsjf {
 
-constexpr int kHistMax = 1 << 20;       // lengths >= 2^20 are UNSUPPORTED
+constexpr int kHistMax = 1 << 20;       // lengths >= 2^20 take the overflow list (A1 long tail)
+constexpr int kOvfCap = 32768;          // over-long history lengths per call (sorted in one CTA's shared memory)
 constexpr int kHistSmem = 49152;        // bins privatised in shared memory (192 KB)
 constexpr int kHT = 1024;               // threads of the histogram / RLE / refine / prune CTAs
 constexpr int kRleChunk = 16384;        // bins per RLE block
@@ -31,6 +32,7 @@ constexpr int kRleChunk = 16384;        // bins per RLE block
 struct RpScratch {
     unsigned int* hist;                 // [kHistMax]
     unsigned long long* stat;           // [0] invalid, [1] over, [2] max len, [3..] scratch
+    int32_t* ovf;                       // [kOvfCap] history lengths >= kHistMax (unsorted)
     int32_t* v;                         // [kHistMax]
     int64_t* c;                         // [kHistMax]
     int64_t *N, *S1, *S2;               // [kHistMax + 1]
@@ -63,15 +65,20 @@ struct RpScratch {
 
 // ------------------------------------------------------------------ A1 ---
 __global__ void __launch_bounds__(kHT, 1)
-    hist_kernel(const int32_t* __restrict__ len, int64_t n, unsigned int* hist, unsigned long long* stat) {
+    hist_kernel(const int32_t* __restrict__ len, int64_t n, unsigned int* hist, unsigned long long* stat,
+                int32_t* ovf) {
     extern __shared__ unsigned int sh[];
     for (int i = threadIdx.x; i < kHistSmem; i += kHT) sh[i] = 0u;
     __syncthreads();
-    unsigned int bad = 0, over = 0;
+    unsigned int bad = 0;
     int mx = 0;
     auto one = [&](int b) {
         if (b < 1) { bad++; return; }
-        if (b >= kHistMax) { over++; return; }
+        if (b >= kHistMax) {            // rare (prompts of >= 2^20 tokens): the overflow list
+            const unsigned long long i = atomicAdd(&stat[1], 1ull);
+            if (ovf && i < (unsigned long long)kOvfCap) ovf[i] = b;
+            return;
+        }
         mx = b > mx ? b : mx;
         if (b < kHistSmem) atomicAdd(&sh[b], 1u);
         else atomicAdd(&hist[b], 1u);
@@ -90,11 +97,9 @@ __global__ void __launch_bounds__(kHT, 1)
         for (int64_t i = (int64_t)blockIdx.x * kHT + threadIdx.x; i < n; i += stride) one(__ldcs(len + i));
     }
     bad = __reduce_add_sync(0xffffffffu, bad);
-    over = __reduce_add_sync(0xffffffffu, over);
     mx = __reduce_max_sync(0xffffffffu, mx);
     if ((threadIdx.x & 31) == 0) {
         if (bad) atomicAdd(&stat[0], (unsigned long long)bad);
-        if (over) atomicAdd(&stat[1], (unsigned long long)over);
         if (mx) atomicMax(&stat[2], (unsigned long long)mx);
     }
     __syncthreads();
@@ -206,6 +211,81 @@ __global__ void __launch_bounds__(kHT) rle_write_kernel(const unsigned int* hist
             run[0] += 1; run[1] += c; run[2] += c * b; run[3] += c * b * b;
             N[j + 1] = run[1]; S1[j + 1] = run[2]; S2[j + 1] = run[3];
         }
+    }
+}
+
+// A1/A2 long tail: the over-long lengths (>= kHistMax, unsorted in ovf[0..n)) are
+// sorted in shared memory (bitonic, one CTA) and run-length encoded; every one of
+// them exceeds every histogram length, so their runs are appended after the
+// histogram's M0 runs and the prefixes continue from its totals tot[0..3] = (M0,
+// N, S1, S2), which are updated in place.  runpos: scratch [kOvfCap + 1].
+__global__ void __launch_bounds__(kHT) ovf_rle_kernel(const int32_t* __restrict__ ovf, int n, int64_t* tot,
+                                                      int32_t* v, int64_t* cc, int64_t* N, int64_t* S1, int64_t* S2,
+                                                      int32_t* runpos) {
+    extern __shared__ int32_t so[];                 // [P]
+    __shared__ int64_t sm[256];
+    __shared__ int s_runs;
+    const int tid = threadIdx.x;
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int i = tid; i < P; i += kHT) so[i] = i < n ? ovf[i] : INT_MAX;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < P; i += kHT) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const int a = so[i], b = so[l];
+                    if (((i & k) == 0) == (a > b)) { so[i] = b; so[l] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    // run starts: thread t owns positions [t*E, (t+1)*E); an exclusive scan of the
+    // per-thread start counts numbers the runs
+    const int E = (n + kHT - 1) / kHT;
+    const int i0 = min(n, tid * E), i1 = min(n, i0 + E);
+    int64_t x[4] = {0, 0, 0, 0}, t4[4];
+    for (int i = i0; i < i1; i++) x[0] += (i == 0 || so[i] != so[i - 1]);
+    block_scan_excl4(x, t4, sm);
+    {
+        int r = (int)x[0];
+        for (int i = i0; i < i1; i++)
+            if (i == 0 || so[i] != so[i - 1]) runpos[r++] = i;
+        if (tid == 0) { s_runs = (int)t4[0]; runpos[t4[0]] = n; }
+    }
+    __syncthreads();
+    const int runs = s_runs;
+    const int64_t M0 = tot[0], N0 = tot[1], A0 = tot[2], B0 = tot[3];
+    // runs [r0, r1) of this thread: counts, values, and the S1 / S2 prefixes (block scan)
+    const int RE = (runs + kHT - 1) / kHT;
+    const int r0 = min(runs, tid * RE), r1 = min(runs, r0 + RE);
+    int64_t y[4] = {0, 0, 0, 0}, u4[4];
+    for (int r = r0; r < r1; r++) {
+        const int64_t c = runpos[r + 1] - runpos[r], b = so[runpos[r]];
+        y[0] += c * b;
+        y[1] = (int64_t)((unsigned long long)y[1] + (unsigned long long)c * b * b);   // sumsq wraps mod 2^64 past 2^63 (no decision reads S2)
+    }
+    block_scan_excl4(y, u4, sm);
+    int64_t s1 = A0 + y[0], s2 = B0 + y[1];
+    if (M0 == 0 && tid == 0) { N[0] = 0; S1[0] = 0; S2[0] = 0; }
+    for (int r = r0; r < r1; r++) {
+        const int64_t c = runpos[r + 1] - runpos[r], b = so[runpos[r]];
+        const int64_t j = M0 + r;
+        v[j] = (int32_t)b;
+        cc[j] = c;
+        s1 += c * b;
+        s2 = (int64_t)((unsigned long long)s2 + (unsigned long long)c * b * b);
+        N[j + 1] = N0 + runpos[r + 1];
+        S1[j + 1] = s1;
+        S2[j + 1] = s2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        tot[0] = M0 + runs;
+        tot[1] = N0 + n;
+        tot[2] = A0 + u4[0];
+        tot[3] = (int64_t)((unsigned long long)B0 + (unsigned long long)u4[1]);
     }
 }
 
@@ -1003,7 +1083,7 @@ __global__ void set_flags_kernel(uint8_t* flag, const int32_t* out, int k) {
 void rp_free(ewsjf_ctx* ctx) {
     RpScratch* R = ctx->rp;
     if (!R) return;
-    void* p[] = {R->hist, R->stat, R->v, R->c, R->N, R->S1, R->S2, R->blk, R->t1, R->t3, R->kbF, R->kbI,
+    void* p[] = {R->ovf, R->hist, R->stat, R->v, R->c, R->N, R->S1, R->S2, R->blk, R->t1, R->t3, R->kbF, R->kbI,
                  R->seg, R->segend, R->flag, R->out_i, R->q_lo, R->q_hi, R->q_n, R->q_s1, R->q_s2, R->merges,
                  R->plo, R->phi_, R->pnext, R->pprev, R->pn, R->ps1, R->ps2, R->tree, R->treei, R->kdp_a, R->kcuts};
     for (void* x : p)
@@ -1018,12 +1098,13 @@ ewsjf_status rp_alloc(ewsjf_ctx* ctx) {
     RpScratch* R = new RpScratch();
     memset(R, 0, sizeof *R);
     ctx->rp = R;
-    const size_t H = kHistMax + 1;
+    const size_t H = kHistMax + kOvfCap + 1;      // distinct lengths: histogram runs + long-tail runs
     R->kblocks = 2048;
-    int64_t tn = 0, cnt = kHistMax;
+    int64_t tn = 0, cnt = kHistMax + kOvfCap;
     for (;;) { tn += cnt; if (cnt == 1) break; cnt = (cnt + 31) / 32; }
     R->tree_n = tn;
     bool ok = cudaMalloc(&R->hist, H * 4) == cudaSuccess && cudaMalloc(&R->stat, 16 * 8) == cudaSuccess &&
+              cudaMalloc(&R->ovf, (size_t)kOvfCap * 4) == cudaSuccess &&
               cudaMalloc(&R->v, H * 4) == cudaSuccess && cudaMalloc(&R->c, H * 8) == cudaSuccess &&
               cudaMalloc(&R->N, H * 8) == cudaSuccess && cudaMalloc(&R->S1, H * 8) == cudaSuccess &&
               cudaMalloc(&R->S2, H * 8) == cudaSuccess &&
@@ -1125,10 +1206,14 @@ static ewsjf_status rp_kmeans_only(ewsjf_ctx* ctx, int64_t M, const ewsjf_partit
 }
 
 static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int lmax, const ewsjf_partition_params* p,
-                                 ewsjf_partition_t* out, ewsjf_partition_stats* stats, ewsjf_partition_stats& S) {
+                                 ewsjf_partition_t* out, ewsjf_partition_stats* stats, ewsjf_partition_stats& S,
+                                 int n_ovf = 0) {
     RpScratch* R = ctx->rp;
     cudaStream_t st = ctx->stream;
     const int nb = (lmax + kRleChunk - 1) / kRleChunk;
+    if (nb == 0) {        // every valid length is over-long
+        CU(cudaMemsetAsync(R->stat + 4, 0, 4 * 8, st));
+    } else {
     {
         LaunchScope ls(ctx, KIND_PARTITION);
         rle_count_kernel<<<nb, kHT, 0, st>>>(hist, lmax, R->blk);
@@ -1141,6 +1226,15 @@ static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int l
         LaunchScope ls(ctx, KIND_PARTITION);
         rle_write_kernel<<<nb, kHT, 0, st>>>(hist, lmax, R->blk, R->v, R->c, R->N, R->S1, R->S2);
     }
+    }
+    if (n_ovf > 0) {
+        int P = 1;
+        while (P < n_ovf) P <<= 1;
+        CU(cudaFuncSetAttribute(ovf_rle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kOvfCap * 4));
+        LaunchScope ls(ctx, KIND_PARTITION);
+        ovf_rle_kernel<<<1, kHT, (size_t)P * 4, st>>>(R->ovf, n_ovf, (int64_t*)(R->stat + 4), R->v, R->c, R->N, R->S1,
+                                                      R->S2, R->segend);
+    }
     CU(cudaGetLastError());
     int64_t tot[4];
     CU(cudaMemcpyAsync(tot, R->stat + 4, 4 * 8, cudaMemcpyDeviceToHost, st));
@@ -1148,6 +1242,10 @@ static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int l
     const int64_t M = tot[0];
     S.distinct = M;
     S.n_valid = tot[1];
+    if (M > kHistMax) {   // the Stage-3 tree's static depth covers 2^20 leaves
+        if (stats) *stats = S;
+        return fail(ctx, EWSJF_ERR_UNSUPPORTED, "%lld distinct history lengths (at most 2^20)", (long long)M);
+    }
     if (M == 0) {
         if (stats) *stats = S;
         return fail(ctx, EWSJF_ERR_EMPTY, "no history length >= 1");
@@ -1304,7 +1402,7 @@ extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, in
     if (n > 0) {
         LaunchScope ls(ctx, KIND_PARTITION);
         CU(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4));
-        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_len, n, R->hist, R->stat);
+        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_len, n, R->hist, R->stat, R->ovf);
         CU(cudaGetLastError());
     }
     CU(cudaEventRecord(R->ev[1], st));
@@ -1312,16 +1410,16 @@ extern "C" ewsjf_status ewsjf_partition(ewsjf_ctx* ctx, const int32_t* d_len, in
     CU(cudaMemcpyAsync(hs, R->stat, 3 * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     S.n_invalid = (int64_t)hs[0];
-    S.n_valid = n - (int64_t)hs[0] - (int64_t)hs[1];
-    if (hs[1]) {
+    S.n_valid = n - (int64_t)hs[0];
+    if (hs[1] > (unsigned long long)kOvfCap) {
         if (stats) *stats = S;
-        return fail(ctx, EWSJF_ERR_UNSUPPORTED, "%llu history lengths >= 2^20", hs[1]);
+        return fail(ctx, EWSJF_ERR_UNSUPPORTED, "%llu history lengths >= 2^20 (at most %d per call)", hs[1], kOvfCap);
     }
     if (S.n_valid == 0) {
         if (stats) *stats = S;
         return fail(ctx, EWSJF_ERR_EMPTY, "no history length >= 1");
     }
-    return rp_from_hist(ctx, R->hist, (int)hs[2], p, out, stats, S);
+    return rp_from_hist(ctx, R->hist, (int)hs[2], p, out, stats, S, (int)hs[1]);
 }
 
 extern "C" ewsjf_status ewsjf_history_hist(ewsjf_ctx* ctx, const int32_t* d_len, int64_t n, uint32_t* d_hist,
@@ -1338,7 +1436,7 @@ extern "C" ewsjf_status ewsjf_history_hist(ewsjf_ctx* ctx, const int32_t* d_len,
     if (n > 0) {
         LaunchScope ls(ctx, KIND_PARTITION);
         CU(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4));
-        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_len, n, (unsigned int*)d_hist, R->stat);
+        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_len, n, (unsigned int*)d_hist, R->stat, nullptr);
         CU(cudaGetLastError());
     }
     unsigned long long hs[3];
@@ -1476,7 +1574,7 @@ extern "C" ewsjf_status ewsjf_online_adjust(ewsjf_ctx* ctx, const int32_t* d_win
     {
         LaunchScope ls(ctx, KIND_PARTITION);
         CU(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4));
-        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_window, n, R->hist, R->stat);
+        hist_kernel<<<ctx->num_sms, kHT, kHistSmem * 4, st>>>(d_window, n, R->hist, R->stat, nullptr);
     }
     static thread_local AdjustArgs A;
     A.max_shift = max_shift;

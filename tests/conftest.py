@@ -29,4 +29,5 @@ def pytest_terminal_summary(terminalreporter):
         terminalreporter.write_line(
             f"parity: {SESSION['calls']} selections, {SESSION['queues']} queues compared, "
             f"{SESSION['near_ties']} near-tie id swaps in total (max {SESSION['max_per_call']} per selection, "
-            f"bound {NEAR_TIE_BOUND})")
+            f"bound {NEAR_TIE_BOUND}); {SESSION['unbounded_calls']} long-prompt selections with "
+            f"{SESSION['unbounded_ties']} near-tie swaps, each within 1e-5 relative, count not bounded")

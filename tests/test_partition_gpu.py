@@ -178,3 +178,63 @@ def test_kmeans_only_random_small(E, orc, ctx, seed):
     if seed % 4 == 0:
         hist[0] = 0                                  # one invalid length: DOMAIN on both sides
     _check_kmeans(E, orc, ctx, hist, int(rng.integers(1, 12)))
+
+
+# ---- A1 long tail: history lengths >= 2^20 (prompts of a million tokens and more) ----
+def _with_long_tail(n, n_long, seed, lo=1 << 20, hi=1 << 23):
+    rng = np.random.default_rng(seed)
+    h = workload.lengths("heavy", n, seed).astype(np.int64)
+    idx = rng.choice(n, size=n_long, replace=False)
+    # a few repeated values too (runs of equal over-long lengths)
+    vals = rng.integers(lo, hi, size=n_long)
+    vals[: n_long // 4] = vals[0]
+    h[idx] = vals
+    return h.astype(np.int32)
+
+
+@pytest.mark.parametrize("n,n_long,seed", [(200_000, 1000, 11), (50_000, 32_768, 12), (3_000, 1, 13)])
+def test_partition_long_prompt_tail(E, orc, ctx, n, n_long, seed):
+    """Lengths >= 2^20 go through the overflow list (sorted in one CTA, RLE appended after
+    the histogram's runs): same boundaries and statistics as the oracle's std::sort."""
+    _check(*_both(E, orc, ctx, _with_long_tail(n, n_long, seed)))
+
+
+def test_partition_only_long_prompts(E, orc, ctx):
+    rng = np.random.default_rng(14)
+    h = rng.integers(1 << 20, 1 << 30, size=5000).astype(np.int32)
+    _check(*_both(E, orc, ctx, h))
+
+
+def test_partition_long_tail_over_capacity_refused(E, ctx):
+    h = _with_long_tail(100_000, 32_769, 15)
+    with pytest.raises(E.EwsjfError) as ei:
+        E.partition(ctx, torch.from_numpy(h).cuda())
+    assert ei.value.status == 6          # EWSJF_ERR_UNSUPPORTED
+
+
+def test_tick_routes_long_prompts(E, orc, ctx):
+    """A partition with queues above 2^20 routes and scores long pending prompts like the oracle
+    (lengths past the fused tick's LUT take its binary search)."""
+    from tests.parity import compare_selection, gpu_result, to_gpu_partition
+    hist = _with_long_tail(100_000, 2000, 16)
+    s, opart, _ = orc.partition(hist)
+    assert s == orc.OK
+    pool = workload.pool("heavy", 200_000, 17)
+    rng = np.random.default_rng(18)
+    sel = rng.choice(200_000, size=3000, replace=False)
+    pool["len"][sel] = rng.integers(1 << 20, 1 << 23, size=3000).astype(np.int32)
+    tctx = E.Context(0, max_pool=200_000, max_history=0, max_k=64)
+    qid = torch.empty(200_000, dtype=torch.int32, device="cuda")
+    out = E.tick(tctx, *(torch.from_numpy(pool[k]).cuda() for k in ("len", "arrival", "cost")),
+                 to_gpu_partition(E, opart), E.meta(**workload.THETA0), E.select_params(k=64, mode=0), qid_out=qid)
+    ref = orc.tick(pool["len"], pool["arrival"], pool["cost"], opart, orc.meta(**workload.THETA0),
+                   orc.select_params(k=64, mode=0))
+    phi, _ = orc.score_all(pool["len"], pool["arrival"], pool["cost"], ref["qid"], ref["partition"],
+                           orc.meta(**workload.THETA0), orc.select_params(k=64, mode=0))
+    np.testing.assert_array_equal(qid.cpu().numpy(), ref["qid"])
+    # every swap is still checked to lie within 1e-5 relative of the boundary score (north_star);
+    # the count is not bounded here: at b ~ 2^22 the scores of adjacent lengths differ by
+    # ~1/b = 2.4e-7 relative, about two fp32 ulps, so most of a long queue's top K are near-ties
+    rep = compare_selection(gpu_result(out), ref, phi, pool["arrival"], 0, 64, near_tie_bound=None)
+    print(f"long-prompt tick: {rep.near_ties} near-tie swaps over {rep.checked_queues} queues")
+    tctx.close()
