@@ -57,6 +57,9 @@ static int32_t cap_for(int32_t K) {
     return (c + 31) & ~31;
 }
 
+// ewsjf_tick_host pipelines pools of at least this size (chunks of >= 1M requests)
+constexpr int64_t kPipeMinPool = 2000000;
+
 // --------------------------------------------------------------- context ---
 extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t max_pool, int64_t max_history,
                                          int32_t max_k, ewsjf_ctx** out) {
@@ -127,6 +130,17 @@ extern "C" ewsjf_status ewsjf_ctx_create(int device, void* cuda_stream, int64_t 
              cudaMalloc(&ctx->d_cost, (size_t)max_pool * 4) == cudaSuccess &&
              cudaMalloc(&ctx->d_qid, (size_t)max_pool * 4) == cudaSuccess;
     }
+    if (ok && max_pool >= kPipeMinPool) {   // ewsjf_tick_host pipeline (streams, events, exchange records)
+        ctx->ex_pipe_per = ex_layout(kMaxSlots, max_k, ctx->ex_gap).total;
+        ok = cudaStreamCreateWithFlags(&ctx->h2d_st, cudaStreamNonBlocking) == cudaSuccess &&
+             cudaStreamCreateWithFlags(&ctx->d2h_st, cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ctx->pipe_start, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ctx->pipe_d2h, cudaEventDisableTiming) == cudaSuccess &&
+             cudaMalloc(&ctx->ex_pipe, (size_t)ctx->ex_pipe_per * ewsjf_ctx::kPipeMax) == cudaSuccess;
+        for (int i = 0; ok && i < ewsjf_ctx::kPipeMax; i++)
+            ok = cudaEventCreateWithFlags(&ctx->pipe_h2d[i], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&ctx->pipe_cmp[i], cudaEventDisableTiming) == cudaSuccess;
+    }
     if (!ok) return bad(EWSJF_ERR_CUDA);
     ok = cudaMemset(ctx->gthr, 0, kMaxSlots * sizeof(u64)) == cudaSuccess &&
          cudaMemset(ctx->board, 0, nrow * 8 * sizeof(u64)) == cudaSuccess &&
@@ -175,6 +189,15 @@ extern "C" ewsjf_status ewsjf_ctx_destroy(ewsjf_ctx* ctx) {
     if (ctx->d_policy) cudaFree(ctx->d_policy);
     delete[] (unsigned char*)ctx->h_policy_shadow;
     nccl_release(ctx);
+    for (int i = 0; i < ewsjf_ctx::kPipeMax; i++) {
+        if (ctx->pipe_h2d[i]) cudaEventDestroy(ctx->pipe_h2d[i]);
+        if (ctx->pipe_cmp[i]) cudaEventDestroy(ctx->pipe_cmp[i]);
+    }
+    if (ctx->pipe_start) cudaEventDestroy(ctx->pipe_start);
+    if (ctx->pipe_d2h) cudaEventDestroy(ctx->pipe_d2h);
+    if (ctx->h2d_st) cudaStreamDestroy(ctx->h2d_st);
+    if (ctx->d2h_st) cudaStreamDestroy(ctx->d2h_st);
+    if (ctx->ex_pipe) cudaFree(ctx->ex_pipe);
     void* d[] = {ctx->g_slot, ctx->g_res, ctx->g_u0, ctx->g_u1, ctx->g_tab, ctx->f_rows, ctx->f_ovf_keys, ctx->f_ovf_code, ctx->d_lut, ctx->dbg, ctx->rows.keys, ctx->rows.cnt, ctx->rows.members, ctx->rows.sec, ctx->gthr, ctx->board, ctx->ctr, ctx->gap,
                  ctx->d_blog, ctx->d_summary, ctx->d_len, ctx->d_arr, ctx->d_cost, ctx->d_qid, ctx->d_topk_id,
                  ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score, ctx->d_max_score};
@@ -691,6 +714,77 @@ extern "C" ewsjf_status ewsjf_tick(ewsjf_ctx* ctx, const int32_t* d_len, const f
     return tick_impl(ctx, d_len, d_arrival, d_cost, n, global_base, part, bubble_width, theta, params, d_qid_out, out);
 }
 
+static ewsjf_status local_impl(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arrival, const float* d_cost,
+                               int64_t n, int64_t global_base, const ewsjf_partition_t* part,
+                               const ewsjf_meta* theta, const ewsjf_select_params* sp, int32_t* d_qid_out,
+                               void* d_exchange);
+static ewsjf_status merge_impl(ewsjf_ctx* ctx, const void* d_exchange_all, int32_t world, int64_t global_base,
+                               int64_t n_local, int32_t* d_qid_local, ewsjf_partition_t* part, int32_t bubble_width,
+                               const ewsjf_meta* theta, const ewsjf_select_params* sp, const ewsjf_select_out* out);
+
+// Host-buffer tick, pipelined (pools >= kPipeMinPool): the pool goes up in P chunks on
+// h2d_st; chunk i's local tick (route + score + per-queue reduction into exchange
+// record i, the sharded tick's record) runs on the ctx stream as soon as its copy has
+// landed, and its qid slice goes back on d2h_st while the next chunk is in flight; one
+// merge of the P records gives the tick's result.  The PCIe copies of the two directions
+// overlap each other and the kernels (serial: H2D, kernel, D2H back to back).  A result
+// the exchange records cannot carry (more gap requests than their capacity) is redone
+// by the single-pass tick over the pool now resident on the device.
+static ewsjf_status tick_host_pipelined(ewsjf_ctx* ctx, const int32_t* h_len, const float* h_arrival,
+                                        const float* h_cost, int64_t n, int64_t global_base, ewsjf_partition_t* part,
+                                        int32_t bubble_width, const ewsjf_meta* theta,
+                                        const ewsjf_select_params* params, int32_t* h_qid_out, bool* done,
+                                        bool* on_device) {
+    *done = false;
+    *on_device = false;
+    if (n < kPipeMinPool || !ctx->ex_pipe || part->n < 1 || part->n > 64 || getenv("EWSJF_NO_PIPE")) return EWSJF_OK;
+    const int64_t per = ex_layout(part->n, params->k, ctx->ex_gap).total;
+    if (per > ctx->ex_pipe_per) return EWSJF_OK;
+    const int P = (int)std::min<int64_t>(ewsjf_ctx::kPipeMax, n / (kPipeMinPool / 2));
+    const int64_t step = ((n + P - 1) / P + 4095) & ~(int64_t)4095;     // 16-byte aligned chunk starts
+    cudaStream_t st = ctx->stream;
+    CU(cudaEventRecord(ctx->pipe_start, st));                     // earlier work on the ctx buffers
+    CU(cudaStreamWaitEvent(ctx->h2d_st, ctx->pipe_start, 0));
+    CU(cudaStreamWaitEvent(ctx->d2h_st, ctx->pipe_start, 0));
+    int nc = 0;
+    for (int i = 0; i < P; i++) {
+        const int64_t off = (int64_t)i * step, m = std::min<int64_t>(step, n - off);
+        if (m <= 0) break;
+        nc++;
+        CU(cudaMemcpyAsync(ctx->d_len + off, h_len + off, (size_t)m * 4, cudaMemcpyHostToDevice, ctx->h2d_st));
+        CU(cudaMemcpyAsync(ctx->d_arr + off, h_arrival + off, (size_t)m * 4, cudaMemcpyHostToDevice, ctx->h2d_st));
+        if (h_cost) CU(cudaMemcpyAsync(ctx->d_cost + off, h_cost + off, (size_t)m * 4, cudaMemcpyHostToDevice, ctx->h2d_st));
+        CU(cudaEventRecord(ctx->pipe_h2d[i], ctx->h2d_st));
+        CU(cudaStreamWaitEvent(st, ctx->pipe_h2d[i], 0));
+        ewsjf_status s = local_impl(ctx, ctx->d_len + off, ctx->d_arr + off, h_cost ? ctx->d_cost + off : nullptr, m,
+                                    global_base + off, part, theta, params, ctx->d_qid + off,
+                                    ctx->ex_pipe + (size_t)i * per);
+        if (s != EWSJF_OK) return s;
+        CU(cudaEventRecord(ctx->pipe_cmp[i], st));
+        if (h_qid_out) {
+            CU(cudaStreamWaitEvent(ctx->d2h_st, ctx->pipe_cmp[i], 0));
+            CU(cudaMemcpyAsync(h_qid_out + off, ctx->d_qid + off, (size_t)m * 4, cudaMemcpyDeviceToHost, ctx->d2h_st));
+        }
+    }
+    ewsjf_select_out out{ctx->d_topk_id, ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score,
+                         ctx->d_max_score, ctx->d_summary, nullptr};
+    ewsjf_status s = merge_impl(ctx, ctx->ex_pipe, nc, global_base, n, ctx->d_qid, part, bubble_width, theta, params,
+                                &out);
+    if (s != EWSJF_OK) return s;
+    CU(cudaEventRecord(ctx->pipe_d2h, ctx->d2h_st));
+    CU(cudaStreamWaitEvent(st, ctx->pipe_d2h, 0));                // the qid slices are back before the ctx stream moves on
+    // peek at the summary: a capacity overflow of the records -> redo in one pass
+    CU(cudaMemcpyAsync(ctx->h_summary, ctx->d_summary, sizeof(ewsjf_summary), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    *on_device = true;
+    if (ctx->h_summary->status == EWSJF_ERR_CAPACITY) return EWSJF_OK;   // *done stays false: the caller's
+                                                                         // single pass runs (pool on the device)
+    if (ctx->h_summary->n_gap > 0 && h_qid_out)                   // Alg. 2 rewrote gap requests' qid after the copies
+        CU(cudaMemcpyAsync(h_qid_out, ctx->d_qid, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    *done = true;
+    return EWSJF_OK;
+}
+
 extern "C" ewsjf_status ewsjf_tick_host(ewsjf_ctx* ctx, const int32_t* h_len, const float* h_arrival,
                                         const float* h_cost, int64_t n, int64_t global_base, ewsjf_partition_t* part,
                                         int32_t bubble_width, const ewsjf_meta* theta,
@@ -703,18 +797,26 @@ extern "C" ewsjf_status ewsjf_tick_host(ewsjf_ctx* ctx, const int32_t* h_len, co
     if (n > 0 && (!h_len || !h_arrival)) return fail(ctx, EWSJF_ERR_INVALID_ARG, "null host pool");
     CU(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
-    if (n > 0) {
-        CU(cudaMemcpyAsync(ctx->d_len, h_len, (size_t)n * 4, cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(ctx->d_arr, h_arrival, (size_t)n * 4, cudaMemcpyHostToDevice, st));
-        if (h_cost) CU(cudaMemcpyAsync(ctx->d_cost, h_cost, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    bool piped = false, on_device = false;
+    {
+        ewsjf_status ps = tick_host_pipelined(ctx, h_len, h_arrival, h_cost, n, global_base, part, bubble_width, theta,
+                                              params, h_qid_out, &piped, &on_device);
+        if (ps != EWSJF_OK) return ps;
     }
-    ewsjf_select_out out{ctx->d_topk_id, ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score,
-                         ctx->d_max_score, ctx->d_summary, nullptr};
-    ewsjf_status s = tick_impl(ctx, ctx->d_len, ctx->d_arr, h_cost ? ctx->d_cost : nullptr, n, global_base, part,
-                               bubble_width, theta, params, ctx->d_qid, &out);
-    if (s != EWSJF_OK) return s;
+    if (!piped) {
+        if (n > 0 && !on_device) {
+            CU(cudaMemcpyAsync(ctx->d_len, h_len, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(ctx->d_arr, h_arrival, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+            if (h_cost) CU(cudaMemcpyAsync(ctx->d_cost, h_cost, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+        }
+        ewsjf_select_out out{ctx->d_topk_id, ctx->d_topk_score, ctx->d_count, ctx->d_head_id, ctx->d_head_score,
+                             ctx->d_max_score, ctx->d_summary, nullptr};
+        ewsjf_status s = tick_impl(ctx, ctx->d_len, ctx->d_arr, h_cost ? ctx->d_cost : nullptr, n, global_base, part,
+                                   bubble_width, theta, params, ctx->d_qid, &out);
+        if (s != EWSJF_OK) return s;
+        if (h_qid_out && n > 0) CU(cudaMemcpyAsync(h_qid_out, ctx->d_qid, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    }
     const int K = params->k;
-    if (h_qid_out && n > 0) CU(cudaMemcpyAsync(h_qid_out, ctx->d_qid, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
     if (h_topk_id) CU(cudaMemcpyAsync(h_topk_id, ctx->d_topk_id, (size_t)kMaxSlots * K * 8, cudaMemcpyDeviceToHost, st));
     if (h_topk_score)
         CU(cudaMemcpyAsync(h_topk_score, ctx->d_topk_score, (size_t)kMaxSlots * K * 4, cudaMemcpyDeviceToHost, st));

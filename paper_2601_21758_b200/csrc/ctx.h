@@ -80,6 +80,14 @@ struct ewsjf_ctx {
     unsigned char* ex_all = nullptr;
     int64_t ex_cap = 0;
     int32_t ex_gap = 1024;              // gap entries per exchange record (ewsjf_ctx_set_exchange_gap_cap)
+    // ewsjf_tick_host pipeline: chunks copied on h2d_st, reduced by local ticks into
+    // exchange records on the ctx stream, qid slices copied back on d2h_st
+    static constexpr int kPipeMax = 8;
+    cudaStream_t h2d_st = nullptr, d2h_st = nullptr;
+    cudaEvent_t pipe_h2d[kPipeMax] = {}, pipe_cmp[kPipeMax] = {};
+    cudaEvent_t pipe_start = nullptr, pipe_d2h = nullptr;
+    unsigned char* ex_pipe = nullptr;
+    int64_t ex_pipe_per = 0;
     // batch builder prefix scratch (batch.cu)
     uint32_t* d_bpre = nullptr;
     int64_t bpre_cap = 0;

@@ -365,3 +365,55 @@ def test_sharded_tick_with_holes_at_pool_scale(E, orc, ctx_full):
             _check(g, ref, phi, pool, mode, K)
     finally:
         ctx_full.set_exchange_gap_cap(1024)
+
+
+@pytest.mark.parametrize("case", ["plain", "few_gaps", "many_gaps"])
+def test_tick_host_pipelined_equals_device(E, orc, ctx_full, heavy_parts, case):
+    """ewsjf_tick_host pipelines pools >= 2M (chunked H2D on one stream, per-chunk local
+    ticks into exchange records, qid slices back on another stream, one merge): its
+    results equal the single-pass device tick's.  few_gaps: a partition with one hole
+    (Alg. 2 in the merge, the gap requests' qids re-read after it); many_gaps: holes
+    holding more gap requests than an exchange record carries (the call redoes the tick
+    in one pass over the pool already on the device)."""
+    n = 3_000_000
+    pool = workload.pool("heavy", n, 309)
+    if case == "plain":
+        part_o = heavy_parts["rp"]
+    else:
+        s, opart, _ = orc.partition(workload.heavy(1_000_000, 301))
+        qs = opart.queues()
+        bounds = [(q["min_len"], q["max_len"]) for q in qs]
+        means = [q["mean"] for q in qs]
+        if case == "few_gaps":
+            # the last (long-prompt) queue split around a hole [20000, 20000 + w) holding a few
+            # hundred of the pool's requests (Pareto tail: ~1.5 requests per length there)
+            lo, hi = bounds[-1]
+            w = 1
+            while ((pool["len"] >= 20000) & (pool["len"] < 20000 + 2 * w)).sum() <= 600:
+                w *= 2
+            bounds[-1] = (lo, 20000)
+            bounds.append((20000 + w, hi))
+            means.append(means[-1])
+        else:
+            drop = (5, 11, 17, 23, len(qs) - 3)
+            bounds = [b for i, b in enumerate(bounds) if i not in drop]
+            means = [m for i, m in enumerate(means) if i not in drop]
+        part_o = orc.make_partition(bounds, means=means)
+    theta, sp = E.meta(**THETA0), E.select_params(k=64)
+    hl, ha, hc = (torch.from_numpy(pool[k]).pin_memory() for k in ("len", "arrival", "cost"))
+    hq = torch.full((n,), -7, dtype=torch.int32).pin_memory()
+    gp_host, gp_dev = to_gpu_partition(E, part_o), to_gpu_partition(E, part_o)
+    r = E.tick_host(ctx_full, hl, ha, hc, gp_host, theta, sp, qid_out=hq)
+    dq = torch.empty(n, dtype=torch.int32, device="cuda")
+    out = E.tick(ctx_full, hl.cuda(), ha.cuda(), hc.cuda(), gp_dev, theta, sp, qid_out=dq)
+    if case == "few_gaps":
+        assert 0 < out.summary["n_gap"] <= 1024, out.summary["n_gap"]
+    if case == "many_gaps":
+        assert out.summary["n_gap"] > 3 * 1024, out.summary["n_gap"]
+    assert r["summary"] == out.summary
+    np.testing.assert_array_equal(hq.numpy(), dq.cpu().numpy())
+    assert [(q.min_len, q.max_len, q.id) for q in gp_host.q[: gp_host.n]] == \
+           [(q.min_len, q.max_len, q.id) for q in gp_dev.q[: gp_dev.n]]
+    nq = out.summary["n_queues"]
+    for k in ("topk_id", "count", "head_id", "topk_score", "head_score", "max_score"):
+        np.testing.assert_array_equal(r[k].numpy()[:nq], getattr(out, k).cpu().numpy()[:nq])
