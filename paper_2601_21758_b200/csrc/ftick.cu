@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(kFT, 1)
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + s] = fgtime();
     };
     stamp(0);
+    if (A.diag & 4) return;   // timing diagnostic (EWSJF_DIAG=4): launch + teardown of this configuration only
 
     // ---- chunk schedule.  The pool is cut into chunks of CH = kFW * kFTile requests;
     // CTA cta takes chunks cta, cta + G, cta + 2G, ... (iteration i: chunk cta + G*i), so at
@@ -1262,8 +1263,16 @@ static cudaError_t launch_f(const FArgs& A, const Policy* P, const MergeArgs& MA
     const int64_t lm = A.merge ? merge_smem_total(MERGE_IN_ROWS) : 0;
     const int64_t smem = ls > lm ? ls : lm;
     auto k = ftick_kernel<MO, C>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the attribute only grows per device (a host call per launch otherwise)
+    static int64_t attr[32] = {0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 32 || attr[dev] < smem) {
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        if (dev >= 0 && dev < 32) attr[dev] = smem;
+    }
     void* args[] = {(void*)&A, (void*)&P, (void*)&MA};   // &P: address of the device pointer
     return cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kFT), args, (size_t)smem, st);
 }

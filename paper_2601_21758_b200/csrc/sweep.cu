@@ -59,7 +59,10 @@ struct SweepScratch {
     u64* gthr = nullptr;            // [kSwBatch][256] shared thresholds (exact keys)
     u64* rows = nullptr;            // [task][kSwT][K]
     int32_t* rowcnt = nullptr;      // [task][kSwT]
-    float* w = nullptr;             // [kSwBatch][256][3] weights by position (device, A7)
+    float* w = nullptr;             // [kSwBatch][nq][3] weights by position (device, A7, uploaded per batch)
+    float* h_w = nullptr;           // pinned staging [2][kSwBatch][256][3] (ring of two, w_ev)
+    cudaEvent_t w_ev[2] = {};
+    int w_next = 0;
     // prefilter scratch: bin counts -> starts, scatter cursors, per-length list bounds,
     // per-block top keys, prefix bounds, the compacted records + layout (rec2 holds the
     // records sorted by length until the compaction)
@@ -540,17 +543,18 @@ __global__ void __launch_bounds__(kSwPrepThreads) sky_block_kernel(const SweepAr
     }
 }
 // K3f: one CTA per position.  pref[g] = high word (f1) of the K-th largest candidate
-// key of the position's blocks before g (0 while fewer than K): an inclusive
-// Hillis-Steele scan of the blocks' top-K lists (merge = top K of the union) in
-// shared memory, segments of kSkyScanSeg blocks with a carried prefix.  qidk[p] =
+// key of the position's blocks before g (0 while fewer than K): an exclusive scan
+// of the blocks' top-K lists (merge = top K of the union) in shared memory --
+// per-warp runs, a Hillis-Steele scan over the 32 run totals, a per-block fix-up --
+// segments of kSkyScanSeg blocks with a carried prefix.  qidk[p] =
 // the queue's K-th lowest candidate id key (all weights 0: every member scores 0
 // and the K lowest ids are the answer, R24), 0 while fewer than K.
-constexpr int kSkyScanSeg = 128;
+constexpr int kSkyScanSeg = 256;
 constexpr int kSkyPrefThreads = 1024;
 __global__ void __launch_bounds__(kSkyPrefThreads) sky_prefix_kernel(const SweepArgs* __restrict__ Ap) {
     const SweepArgs& A = *Ap;
-    extern __shared__ u64 s_l[];                       // [2][kSkyScanSeg][32]
-    __shared__ u64 s_carry[32], s_id[kSkyPrefThreads / 32][32];
+    extern __shared__ u64 s_l[];                       // [kSkyScanSeg][32] per-warp inclusive prefixes
+    __shared__ u64 s_carry[32], s_id[kSkyPrefThreads / 32][32], s_w[kSkyPrefThreads / 32][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     const int p = blockIdx.x;
     if (p >= A.nq) return;
@@ -560,12 +564,12 @@ __global__ void __launch_bounds__(kSkyPrefThreads) sky_prefix_kernel(const Sweep
         return (u32)(__shfl_sync(0xffffffffu, top, K - 1) >> 32);
     };
     if (warp == 0) s_carry[lane] = 0ull;
-    // the id lists: each warp folds its share of the blocks, warp 0 folds the warps
+    // the id lists: each warp folds its share of the blocks, then a tree over the warps
     u64 ti = 0ull;
     for (int g = g0 + warp; g < g1; g += nwarp) ti = topk_merge_sorted(ti, A.s.blkid[(size_t)g * kSkyMaxK + lane], K, lane);
     s_id[warp][lane] = ti;
     __syncthreads();
-    for (int d = 1; d < nwarp; d <<= 1) {                // tree fold of the warps' lists
+    for (int d = 1; d < nwarp; d <<= 1) {
         if ((warp & (2 * d - 1)) == 0 && warp + d < nwarp)
             s_id[warp][lane] = topk_merge_sorted(s_id[warp][lane], s_id[warp + d][lane], K, lane);
         __syncthreads();
@@ -574,27 +578,35 @@ __global__ void __launch_bounds__(kSkyPrefThreads) sky_prefix_kernel(const Sweep
         const u64 kid = __shfl_sync(0xffffffffu, s_id[0][lane], K - 1);
         if (lane == 0) A.s.qidk[p] = kid;
     }
+    // the block lists' exclusive prefix, per segment: (1) each warp scans its contiguous
+    // run of blocks, (2) a Hillis-Steele scan over the 32 run totals, (3) each block's
+    // bound = K-th of (carry ∪ earlier runs ∪ its run's blocks before it)
     for (int s0 = g0; s0 < g1; s0 += kSkyScanSeg) {
         const int n = min(kSkyScanSeg, g1 - s0);
-        u64* in = s_l;
-        u64* out = s_l + kSkyScanSeg * 32;
-        for (int j = warp; j < n; j += nwarp) in[j * 32 + lane] = A.s.blktop[(size_t)(s0 + j) * kSkyMaxK + lane];
-        __syncthreads();
-        if (warp == 0) in[lane] = topk_merge_sorted(s_carry[lane], in[lane], K, lane);   // block s0 includes the carry
-        __syncthreads();
-        for (int d = 1; d < n; d <<= 1) {
-            for (int j = warp; j < n; j += nwarp)
-                out[j * 32 + lane] = j >= d ? topk_merge_sorted(in[(j - d) * 32 + lane], in[j * 32 + lane], K, lane) : in[j * 32 + lane];
-            __syncthreads();
-            u64* t = in; in = out; out = t;
+        const int per = (n + nwarp - 1) / nwarp;
+        const int j0 = min(n, warp * per), j1 = min(n, j0 + per);
+        u64 t = 0ull;
+        for (int j = j0; j < j1; j++) {
+            t = topk_merge_sorted(t, A.s.blktop[(size_t)(s0 + j) * kSkyMaxK + lane], K, lane);
+            s_l[j * 32 + lane] = t;
         }
-        // exclusive: block s0 + j is bounded by the inclusive prefix of s0 + j - 1
-        for (int j = warp; j < n; j += nwarp) {
-            const u32 h = j == 0 ? kth_hi(s_carry[lane]) : kth_hi(in[(j - 1) * 32 + lane]);
+        s_w[warp][lane] = t;
+        __syncthreads();
+        for (int d = 1; d < nwarp; d <<= 1) {
+            const u64 mine = s_w[warp][lane], other = warp >= d ? s_w[warp - d][lane] : 0ull;
+            __syncthreads();
+            if (warp >= d) s_w[warp][lane] = topk_merge_sorted(other, mine, K, lane);
+            __syncthreads();
+        }
+        u64 ex = s_carry[lane];
+        if (warp > 0) ex = topk_merge_sorted(ex, s_w[warp - 1][lane], K, lane);
+        for (int j = j0; j < j1; j++) {
+            const u64 before = j == j0 ? ex : topk_merge_sorted(ex, s_l[(j - 1) * 32 + lane], K, lane);
+            const u32 h = kth_hi(before);
             if (lane == 0) A.s.pref[s0 + j] = h;
         }
         __syncthreads();
-        if (warp == 0) s_carry[lane] = in[(n - 1) * 32 + lane];
+        if (warp == 0) s_carry[lane] = topk_merge_sorted(s_carry[lane], s_w[nwarp - 1][lane], K, lane);
         __syncthreads();
     }
 }
@@ -712,7 +724,7 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const Sweep
             for (int t = 0; t < kSwT; t++) {
                 const int th = blk * kSwT + t;
                 if (th >= A.n_theta) break;
-                const float* w = A.s.w + ((size_t)th * kMaxSlots + q) * 3;
+                const float* w = A.s.w + ((size_t)th * A.nq + q) * 3;
                 const float w0 = w[0], w1 = w[1], w2 = w[2];
                 u64 key[kRegSel];
 #pragma unroll
@@ -745,7 +757,7 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const Sweep
         // (read as broadcasts), candidate counts
         if (lane < kSwT) {
             const int th = min(t0 + lane, A.n_theta - 1);
-            const float* w = A.s.w + ((size_t)th * kMaxSlots + q) * 3;
+            const float* w = A.s.w + ((size_t)th * A.nq + q) * 3;
             const u64 g = __ldcg(&A.s.gthr[(size_t)th * kMaxSlots + q]);
             ws[lane] = make_float4(w[0], w[1], w[2], __uint_as_float((uint32_t)(g >> 32)));
             th64[lane] = g;
@@ -852,21 +864,6 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_select_kernel(const Sweep
     }
 }
 
-// K2b: A7 for the batch on the device, the same canonical fp64 expression as
-// ewsjf_weights_from_meta (round(a·b̄) + b, no contraction, clamp, fp32).
-__global__ void sweep_weights_kernel(const SweepArgs* __restrict__ Ap) {
-    const SweepArgs& A = *Ap;
-    for (int i = threadIdx.x; i < A.n_theta * A.nq; i += blockDim.x) {
-        const int t = i / A.nq, q = i % A.nq;
-        float* w = A.s.w + ((size_t)t * kMaxSlots + q) * 3;
-#pragma unroll
-        for (int x = 0; x < 3; x++) {
-            const double v = __dadd_rn(__dmul_rn(A.theta[t][2 * x], A.mean[q]), A.theta[t][2 * x + 1]);
-            w[x] = (float)(v > 0.0 ? v : 0.0);
-        }
-    }
-}
-
 struct SweepOutArgs {
     SweepScratch s;
     int32_t nq, K, cap, n_theta, rcap;
@@ -936,7 +933,7 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_merge_kernel(const SweepO
             o.d_head_id[q] = -1; o.d_head_score[q] = 0.f; o.d_max_score[q] = 0.f;
         } else {
             const float4 hf = A.s.headf[q];
-            const float* w = A.s.w + ((size_t)th * kMaxSlots + q) * 3;
+            const float* w = A.s.w + ((size_t)th * A.nq + q) * 3;
             const float hs = fmaf(w[2], hf.z, fmaf(w[1], hf.y, w[0] * hf.x));
             o.d_head_id[q] = (int64_t)key_gid(A.s.head[q]);
             o.d_head_score[q] = qi * hs;
@@ -958,7 +955,7 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_direct_kernel(const Sweep
     if (item >= A.n_theta * A.nq) return;
     const int th = item / A.nq, q = item % A.nq;
     const int K = A.K;
-    const float* w = A.s.w + ((size_t)th * kMaxSlots + q) * 3;
+    const float* w = A.s.w + ((size_t)th * A.nq + q) * 3;
     const float w0 = w[0], w1 = w[1], w2 = w[2];
     const int64_t b0 = A.s.qoff[q], b1 = A.s.qoff[q + 1];
     u64 top = 0ull;                                   // lane i: the (i+1)-th best key so far
@@ -1047,6 +1044,9 @@ void sweep_free(ewsjf_ctx* ctx) {
     if (!S) return;
     for (auto e : S->arg_ev)
         if (e) cudaEventDestroy(e);
+    for (auto e : S->w_ev)
+        if (e) cudaEventDestroy(e);
+    if (S->h_w) cudaFreeHost(S->h_w);
     if (S->h_args) cudaFreeHost(S->h_args);
     void* d[] = {S->d_args, S->direct, S->lentop, S->lenid, S->blkid, S->qidk, S->bcnt, S->bfill, S->lenkth, S->biglist, S->nbig, S->blktop, S->pref, S->rec2, S->qoff2, S->cpre2, S->qfill2,
                  S->qcnt2, S->rec, S->qcount, S->qoff, S->cpre, S->qfill, S->head, S->headf, S->bad, S->task_ctr, S->gthr,
@@ -1103,6 +1103,8 @@ ewsjf_status sweep_alloc(ewsjf_ctx* ctx, int64_t n, int64_t tasks, int K) {
         ok = ok && cudaMallocHost(&S->h_args, S->arg_slot * SweepScratch::kArgSlots) == cudaSuccess &&
              cudaMalloc(&S->d_args, S->arg_slot * SweepScratch::kArgSlots) == cudaSuccess;
         for (auto& e : S->arg_ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+        for (auto& e : S->w_ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaMallocHost(&S->h_w, 2 * sizeof(float) * 3 * (size_t)kSwBatch * kMaxSlots) == cudaSuccess;
         if (!ok) return fail(ctx, EWSJF_ERR_CUDA, "sweep scratch allocation failed");
     }
     if (S->n_cap < n) {
@@ -1240,7 +1242,7 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
         CU(cudaMemsetAsync(S->nbig, 0, 4, st));
         CU(cudaMemsetAsync(S->qcnt2, 0, 8 * kMaxSlots, st));
         const int sgrid = ctx->num_sms * 4;
-        const size_t pref_smem = 2 * (size_t)kSkyScanSeg * 32 * 8;
+        const size_t pref_smem = (size_t)kSkyScanSeg * 32 * 8;
         if (!S->sky_attr) {   // per ctx (its device)
             CU(cudaFuncSetAttribute(sky_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem));
             CU(cudaFuncSetAttribute(sky_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem));
@@ -1282,9 +1284,21 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
         CU(cudaMemsetAsync(S->gthr, 0, 8 * (size_t)kSwBatch * kMaxSlots, st));
         const SweepArgs* dB = sw_upload(ctx, A);
         if (!dB) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
-        {
-            LaunchScope ls(ctx, KIND_SWEEP);
-            sweep_weights_kernel<<<1, 256, 0, st>>>(dB);
+        {   // A7 on the host (O(n_theta x nq), the tick's ewsjf_weights_from_meta arithmetic:
+            // round(a b̄) + b in fp64 without contraction, clamp, fp32), one stream-ordered copy
+            const int slot = S->w_next;
+            S->w_next ^= 1;
+            CU(cudaEventSynchronize(S->w_ev[slot]));          // its previous copy has run
+            float* hw = S->h_w + (size_t)slot * 3 * kSwBatch * kMaxSlots;
+            for (int t = 0; t < nb; t++)
+                for (int q = 0; q < nq; q++)
+                    for (int x = 0; x < 3; x++) {
+                        volatile double prod = A.theta[t][2 * x] * A.mean[q];   // rounded once, as __dmul_rn
+                        const double v = prod + A.theta[t][2 * x + 1];
+                        hw[((size_t)t * nq + q) * 3 + x] = (float)(v > 0.0 ? v : 0.0);
+                    }
+            CU(cudaMemcpyAsync(S->w, hw, sizeof(float) * 3 * (size_t)nb * nq, cudaMemcpyHostToDevice, st));
+            CU(cudaEventRecord(S->w_ev[slot], st));
         }
         const int occ = S->occ;
         for (int ph = 0; ph < 2; ph++) {

@@ -42,12 +42,28 @@ def main():
     E.batch_build(ctx, ln, out, out.summary["n_queues"], 64, 20_000)
     thetas = [E.meta(**t) for t in workload.random_thetas(8, 4)]
     E.score_select_sweep(ctx, ln, ar, co, qid, part, thetas, E.select_params(k=8))
+    ln_hot = ln.clone()
+    ln_hot[:3000] = 100                  # one length with > 1024 records: the sweep's CTA-per-length path
+    qid_hot, _ = E.route(ctx, ln_hot, part)
+    E.score_select_sweep(ctx, ln_hot, ar, co, qid_hot, part, thetas, E.select_params(k=8))
+    # A1 long tail: lengths >= 2^20 through the overflow list
+    h_long = workload.heavy(50_000, 5)
+    h_long[:300] = np.random.default_rng(6).integers(1 << 20, 1 << 24, size=300)
+    E.partition(ctx, torch.from_numpy(h_long).to(dev))
     recs = [E.tick_local(ctx, ln[a:b], ar[a:b], co[a:b], a, part, th, E.select_params(k=16), qid_out=q[a:b]).clone()
             for a, b in (workload.shard_range(n, r, 2) for r in range(2))]
     E.tick_merge(ctx, torch.cat(recs), 2, 0, n // 2, q[: n // 2], E.make_partition(
         [(x["min_len"], x["max_len"]) for x in part.queues()]), th, E.select_params(k=16))
     torch.cuda.synchronize()
     ctx.close()
+    if os.environ.get("SANITIZE_BIG"):   # the pipelined ewsjf_tick_host (pools >= 2M)
+        nb = 2_100_000
+        big = E.Context(0, max_pool=nb, max_history=0, max_k=16)
+        pb = workload.pool("heavy", nb, 7)
+        hl, ha, hc = (torch.from_numpy(pb[k]).pin_memory() for k in ("len", "arrival", "cost"))
+        E.tick_host(big, hl, ha, hc, part, th, E.select_params(k=16), qid_out=torch.empty(nb, dtype=torch.int32).pin_memory())
+        torch.cuda.synchronize()
+        big.close()
     print("sanitize driver done")
 
 
