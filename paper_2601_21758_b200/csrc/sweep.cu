@@ -94,6 +94,11 @@ struct SweepScratch {
     size_t arg_slot = 0;
     cudaEvent_t arg_ev[kArgSlots] = {};
     int arg_next = 0;
+    unsigned char* d_fix = nullptr;   // [3] fixed argument blocks the sweep's graphs read (prep A, batch A, batch O)
+    cudaGraphExec_t g_prep = nullptr, g_batch = nullptr;
+    int64_t g_prep_key = -1, g_batch_key = -1;
+    int g_prep_kernels = 0, g_batch_kernels = 0;   // kernels per replay (launch accounting)
+    cudaStream_t cap_st = nullptr;                  // private stream the graphs are captured on
     int occ = 1;
     int last_nq = 0;                // diagnostics: the last sweep's queue count and record offsets used
     bool last_sky = false;
@@ -1039,6 +1044,21 @@ static const T* sw_upload(ewsjf_ctx* ctx, const T& a) {
     return (const T*)d;
 }
 
+// The same, into a fixed device block (the graphs' arguments).
+template <typename T>
+static const T* sw_upload_to(ewsjf_ctx* ctx, const T& a, T* dst) {
+    SweepScratch* S = ctx->sw;
+    const int i = S->arg_next;
+    S->arg_next = (i + 1) % SweepScratch::kArgSlots;
+    if (cudaEventSynchronize(S->arg_ev[i]) != cudaSuccess) return nullptr;
+    unsigned char* h = S->h_args + (size_t)i * S->arg_slot;
+    memcpy(h, &a, sizeof(T));
+    if (cudaMemcpyAsync(dst, h, sizeof(T), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+        cudaEventRecord(S->arg_ev[i], ctx->stream) != cudaSuccess)
+        return nullptr;
+    return dst;
+}
+
 void sweep_free(ewsjf_ctx* ctx) {
     SweepScratch* S = ctx->sw;
     if (!S) return;
@@ -1046,9 +1066,12 @@ void sweep_free(ewsjf_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto e : S->w_ev)
         if (e) cudaEventDestroy(e);
+    if (S->g_prep) cudaGraphExecDestroy(S->g_prep);
+    if (S->cap_st) cudaStreamDestroy(S->cap_st);
+    if (S->g_batch) cudaGraphExecDestroy(S->g_batch);
     if (S->h_w) cudaFreeHost(S->h_w);
     if (S->h_args) cudaFreeHost(S->h_args);
-    void* d[] = {S->d_args, S->direct, S->lentop, S->lenid, S->blkid, S->qidk, S->bcnt, S->bfill, S->lenkth, S->biglist, S->nbig, S->blktop, S->pref, S->rec2, S->qoff2, S->cpre2, S->qfill2,
+    void* d[] = {S->d_fix, S->d_args, S->direct, S->lentop, S->lenid, S->blkid, S->qidk, S->bcnt, S->bfill, S->lenkth, S->biglist, S->nbig, S->blktop, S->pref, S->rec2, S->qoff2, S->cpre2, S->qfill2,
                  S->qcnt2, S->rec, S->qcount, S->qoff, S->cpre, S->qfill, S->head, S->headf, S->bad, S->task_ctr, S->gthr,
                  S->rows, S->rowcnt, S->w};
     for (void* p : d)
@@ -1101,7 +1124,9 @@ ewsjf_status sweep_alloc(ewsjf_ctx* ctx, int64_t n, int64_t tasks, int K) {
                   cudaMalloc(&S->direct, 4) == cudaSuccess;
         S->arg_slot = (std::max(sizeof(SweepArgs), sizeof(SweepOutArgs)) + 255) & ~(size_t)255;
         ok = ok && cudaMallocHost(&S->h_args, S->arg_slot * SweepScratch::kArgSlots) == cudaSuccess &&
-             cudaMalloc(&S->d_args, S->arg_slot * SweepScratch::kArgSlots) == cudaSuccess;
+             cudaMalloc(&S->d_args, S->arg_slot * SweepScratch::kArgSlots) == cudaSuccess &&
+             cudaMalloc(&S->d_fix, S->arg_slot * 3) == cudaSuccess &&
+             cudaStreamCreateWithFlags(&S->cap_st, cudaStreamNonBlocking) == cudaSuccess;
         for (auto& e : S->arg_ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
         for (auto& e : S->w_ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
         ok = ok && cudaMallocHost(&S->h_w, 2 * sizeof(float) * 3 * (size_t)kSwBatch * kMaxSlots) == cudaSuccess;
@@ -1213,56 +1238,14 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
         A.sky_nbins = std::min(kSkyBins, std::max(1024, (maxhi + 1 + 1023) & ~1023));
     }
     cudaStream_t st = ctx->stream;
-    CU(cudaMemsetAsync(S->qcount, 0, 8 * kMaxSlots, st));
-    CU(cudaMemsetAsync(S->head, 0, 8 * kMaxSlots, st));
-    CU(cudaMemsetAsync(S->bad, 0, 32, st));
     const int pgrid = std::max(1, std::min(ctx->num_sms * 4, (int)((n + kSwPrepThreads - 1) / kSwPrepThreads)));
-    const SweepArgs* dA = sw_upload(ctx, A);
-    if (!dA) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
-    {
-        LaunchScope ls(ctx, KIND_SWEEP);
-        sweep_count_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(dA);
-    }
-    {
-        LaunchScope ls(ctx, KIND_SWEEP);
-        sweep_plan_kernel<<<1, 32, 0, st>>>(dA);
-    }
-    {
-        LaunchScope ls(ctx, KIND_SWEEP);
-        sweep_scatter_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(dA);
-    }
-    CU(cudaGetLastError());
-    // Θ-independent candidate prefilter (K <= 32): the select kernels run over the
-    // records no other K records dominate in every feature
-    S->last_nq = nq;
-    S->last_sky = sky;
-    CU(cudaMemsetAsync(S->direct, 0, 4, st));      // sky_plan sets it when the survivors are few
-    if (sky) {
-        CU(cudaMemsetAsync(S->bcnt, 0, 4 * (size_t)(kSkyBins + 1), st));
-        CU(cudaMemsetAsync(S->nbig, 0, 4, st));
-        CU(cudaMemsetAsync(S->qcnt2, 0, 8 * kMaxSlots, st));
-        const int sgrid = ctx->num_sms * 4;
-        const size_t pref_smem = (size_t)kSkyScanSeg * 32 * 8;
-        if (!S->sky_attr) {   // per ctx (its device)
-            CU(cudaFuncSetAttribute(sky_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem));
-            CU(cudaFuncSetAttribute(sky_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem));
-            CU(cudaFuncSetAttribute(sky_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pref_smem));
-            S->sky_attr = true;
-        }
-        LaunchScope ls(ctx, KIND_SWEEP);
-        sky_hist_kernel<<<ctx->num_sms, kSortThreads, kSortSmem, st>>>(dA);
-        sky_scan_kernel<<<1, 1024, 0, st>>>(dA);
-        sky_scatter_kernel<<<ctx->num_sms, kSortThreads, kSortSmem, st>>>(dA);
-        sky_group_kernel<false><<<sgrid, kSwPrepThreads, 0, st>>>(dA);
-        sky_group_kernel<true><<<ctx->num_sms * 2, kSwPrepThreads, 0, st>>>(dA);
-        sky_block_kernel<<<std::max(1, std::min(ctx->num_sms * 3, nb)), kSwPrepThreads, 0, st>>>(dA);
-        sky_prefix_kernel<<<nq, kSkyPrefThreads, pref_smem, st>>>(dA);
-        sky_count_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(dA);
-        sky_plan_kernel<<<1, 32, 0, st>>>(dA);
-        sky_compact_kernel<<<pgrid, kSwPrepThreads, 0, st>>>(dA);
-        CU(cudaGetLastError());
-        // the select / merge kernels read the survivors
-        A.s.rec = S->rec2; A.s.qoff = S->qoff2; A.s.cpre = S->cpre2;
+    const int sgrid = ctx->num_sms * 4;
+    const size_t pref_smem = (size_t)kSkyScanSeg * 32 * 8;
+    if (sky && !S->sky_attr) {   // per ctx (its device)
+        CU(cudaFuncSetAttribute(sky_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem));
+        CU(cudaFuncSetAttribute(sky_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem));
+        CU(cudaFuncSetAttribute(sky_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pref_smem));
+        S->sky_attr = true;
     }
     const size_t sel_smem = (size_t)kSwWarps * kSwT * (A.cap * 8 + 16 + 8 + 4 + 4);
     const size_t mrg_smem = (size_t)kSwWarps * A.cap * 8;
@@ -1272,60 +1255,142 @@ extern "C" ewsjf_status ewsjf_score_select_sweep(ewsjf_ctx* ctx, const int32_t* 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&S->occ, sweep_select_kernel, kSwWarps * 32, sel_smem);
         S->attr_smem = sel_smem;
     }
+    const int occ = S->occ;
+    S->last_nq = nq;
+    S->last_sky = sky;
+    // The launch sequences: the Θ-independent prep (K1-K3, the prefilter K3a-g) and one
+    // Θ batch (K4 x 2, K5 / K5d, K6).  Both are replayed as CUDA graphs (one capture per
+    // shape, kernel arguments in fixed device buffers refreshed by a stream-ordered copy
+    // before each replay): ~20 small kernels per sweep were launch-bound on the host.
+    // `scoped` brackets each launch with the ctx's timing events (direct launches only).
+    cudaStream_t cs = st;   // the stream the sequences enqueue on (a private one while capturing)
+    auto prep_seq = [&](const SweepArgs* dA, bool scoped) -> cudaError_t {
+        int nk = 0;
+        auto L = [&](auto f) { nk++; if (scoped) { LaunchScope ls(ctx, KIND_SWEEP); f(); } else f(); };
+        cudaMemsetAsync(S->qcount, 0, 8 * kMaxSlots, cs);
+        cudaMemsetAsync(S->head, 0, 8 * kMaxSlots, cs);
+        cudaMemsetAsync(S->bad, 0, 32, cs);
+        L([&] { sweep_count_kernel<<<pgrid, kSwPrepThreads, 0, cs>>>(dA); });
+        L([&] { sweep_plan_kernel<<<1, 32, 0, cs>>>(dA); });
+        L([&] { sweep_scatter_kernel<<<pgrid, kSwPrepThreads, 0, cs>>>(dA); });
+        // Θ-independent candidate prefilter (K <= 32): the select kernels run over the
+        // records no other K records dominate in every feature
+        cudaMemsetAsync(S->direct, 0, 4, cs);      // sky_plan sets it when the survivors are few
+        if (sky) {
+            cudaMemsetAsync(S->bcnt, 0, 4 * (size_t)(kSkyBins + 1), cs);
+            cudaMemsetAsync(S->nbig, 0, 4, cs);
+            cudaMemsetAsync(S->qcnt2, 0, 8 * kMaxSlots, cs);
+            L([&] { sky_hist_kernel<<<ctx->num_sms, kSortThreads, kSortSmem, cs>>>(dA); });
+            L([&] { sky_scan_kernel<<<1, 1024, 0, cs>>>(dA); });
+            L([&] { sky_scatter_kernel<<<ctx->num_sms, kSortThreads, kSortSmem, cs>>>(dA); });
+            L([&] { sky_group_kernel<false><<<sgrid, kSwPrepThreads, 0, cs>>>(dA); });
+            L([&] { sky_group_kernel<true><<<ctx->num_sms * 2, kSwPrepThreads, 0, cs>>>(dA); });
+            L([&] { sky_block_kernel<<<std::max(1, std::min(ctx->num_sms * 3, nb)), kSwPrepThreads, 0, cs>>>(dA); });
+            L([&] { sky_prefix_kernel<<<nq, kSkyPrefThreads, pref_smem, cs>>>(dA); });
+            L([&] { sky_count_kernel<<<pgrid, kSwPrepThreads, 0, cs>>>(dA); });
+            L([&] { sky_plan_kernel<<<1, 32, 0, cs>>>(dA); });
+            L([&] { sky_compact_kernel<<<pgrid, kSwPrepThreads, 0, cs>>>(dA); });
+        }
+        if (!scoped) S->g_prep_kernels = nk;
+        return cudaGetLastError();
+    };
+    auto batch_seq = [&](const SweepArgs* dB, const SweepOutArgs* dO, int bn, bool scoped) -> cudaError_t {
+        int nk = 0;
+        auto L = [&](auto f) { nk++; if (scoped) { LaunchScope ls(ctx, KIND_SWEEP); f(); } else f(); };
+        cudaMemsetAsync(S->gthr, 0, 8 * (size_t)kSwBatch * kMaxSlots, cs);
+        for (int ph = 0; ph < 2; ph++) {
+            cudaMemsetAsync(S->task_ctr, 0, 4, cs);
+            L([&] { sweep_select_kernel<<<ctx->num_sms * std::max(occ, 1), kSwWarps * 32, sel_smem, cs>>>(dB, ph); });
+        }
+        L([&] { sweep_merge_kernel<<<(bn * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, mrg_smem, cs>>>(dO); });
+        if (sky) L([&] { sweep_direct_kernel<<<(bn * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, 0, cs>>>(dO); });
+        L([&] { sweep_summary_kernel<<<bn, 32, 0, cs>>>(dO); });
+        if (!scoped) S->g_batch_kernels = nk;
+        return cudaGetLastError();
+    };
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    CU(cudaStreamIsCapturing(st, &cap_st));
+    const bool graphs = cap_st == cudaStreamCaptureStatusNone && !getenv("EWSJF_SWEEP_NO_GRAPH");
+    // capture `seq` into *exec for `key` unless it already holds that shape
+    auto ensure_graph = [&](cudaGraphExec_t* exec, int64_t* have, int64_t key, auto seq) -> cudaError_t {
+        if (*exec && *have == key) return cudaSuccess;
+        if (*exec) { cudaGraphExecDestroy(*exec); *exec = nullptr; }
+        cudaGraph_t g = nullptr;
+        // captured on the sweep's private stream (the ctx stream may be the legacy default
+        // stream, which cannot be captured); replayed on the ctx stream
+        cudaError_t e = cudaStreamBeginCapture(S->cap_st, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return e;
+        cs = S->cap_st;
+        const cudaError_t es = seq();
+        cs = st;
+        e = cudaStreamEndCapture(S->cap_st, &g);
+        if (es != cudaSuccess) e = es;
+        if (e == cudaSuccess) e = cudaGraphInstantiate(exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (e == cudaSuccess) *have = key;
+        return e;
+    };
+    if (graphs) {
+        const SweepArgs* dA = sw_upload_to(ctx, A, (SweepArgs*)S->d_fix);
+        if (!dA) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
+        const int64_t key = (((int64_t)n * 257 + nq) * 4099 + nb) * 64 + K * 2 + (sky ? 1 : 0);
+        cudaError_t e = ensure_graph(&S->g_prep, &S->g_prep_key, key, [&] { return prep_seq(dA, false); });
+        if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "sweep prep graph: %s", cudaGetErrorString(e));
+        LaunchScope ls(ctx, KIND_SWEEP);
+        CU(cudaGraphLaunch(S->g_prep, st));
+        ctx->launches += S->g_prep_kernels - 1;
+    } else {
+        const SweepArgs* dA = sw_upload(ctx, A);
+        if (!dA) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
+        CU(prep_seq(dA, true));
+    }
+    if (sky) { A.s.rec = S->rec2; A.s.qoff = S->qoff2; A.s.cpre = S->cpre2; }   // the select / merge kernels read the survivors
     static thread_local SweepOutArgs O;
     for (int32_t b0 = 0; b0 < n_theta; b0 += kSwBatch) {
-        const int nb = std::min(kSwBatch, n_theta - b0);
-        A.n_theta = nb;
-        for (int t = 0; t < nb; t++) {
+        const int bn = std::min(kSwBatch, n_theta - b0);
+        A.n_theta = bn;
+        for (int t = 0; t < bn; t++) {
             const ewsjf_meta& m = thetas[b0 + t];
             A.theta[t][0] = m.a_b; A.theta[t][1] = m.b_b; A.theta[t][2] = m.a_u;
             A.theta[t][3] = m.b_u; A.theta[t][4] = m.a_f; A.theta[t][5] = m.b_f;
         }
-        CU(cudaMemsetAsync(S->gthr, 0, 8 * (size_t)kSwBatch * kMaxSlots, st));
-        const SweepArgs* dB = sw_upload(ctx, A);
-        if (!dB) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
         {   // A7 on the host (O(n_theta x nq), the tick's ewsjf_weights_from_meta arithmetic:
             // round(a b̄) + b in fp64 without contraction, clamp, fp32), one stream-ordered copy
             const int slot = S->w_next;
             S->w_next ^= 1;
             CU(cudaEventSynchronize(S->w_ev[slot]));          // its previous copy has run
             float* hw = S->h_w + (size_t)slot * 3 * kSwBatch * kMaxSlots;
-            for (int t = 0; t < nb; t++)
+            for (int t = 0; t < bn; t++)
                 for (int q = 0; q < nq; q++)
                     for (int x = 0; x < 3; x++) {
                         volatile double prod = A.theta[t][2 * x] * A.mean[q];   // rounded once, as __dmul_rn
                         const double v = prod + A.theta[t][2 * x + 1];
                         hw[((size_t)t * nq + q) * 3 + x] = (float)(v > 0.0 ? v : 0.0);
                     }
-            CU(cudaMemcpyAsync(S->w, hw, sizeof(float) * 3 * (size_t)nb * nq, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(S->w, hw, sizeof(float) * 3 * (size_t)bn * nq, cudaMemcpyHostToDevice, st));
             CU(cudaEventRecord(S->w_ev[slot], st));
         }
-        const int occ = S->occ;
-        for (int ph = 0; ph < 2; ph++) {
-            CU(cudaMemsetAsync(S->task_ctr, 0, 4, st));
-            LaunchScope ls(ctx, KIND_SWEEP);
-            sweep_select_kernel<<<ctx->num_sms * std::max(occ, 1), kSwWarps * 32, sel_smem, st>>>(dB, ph);
-        }
-        O.s = A.s; O.nq = nq; O.K = K; O.cap = A.cap; O.n_theta = nb; O.rcap = A.rcap;
-        for (int t = 0; t < nb; t++) {
+        O.s = A.s; O.nq = nq; O.K = K; O.cap = A.cap; O.n_theta = bn; O.rcap = A.rcap;
+        for (int t = 0; t < bn; t++) {
             O.outs[t] = outs[b0 + t];
             O.outs[t].h_summary = nullptr;
         }
-        const SweepOutArgs* dO = sw_upload(ctx, O);
-        if (!dO) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
-        {
+        if (graphs) {
+            const SweepArgs* dB = sw_upload_to(ctx, A, (SweepArgs*)(S->d_fix + S->arg_slot));
+            const SweepOutArgs* dO = sw_upload_to(ctx, O, (SweepOutArgs*)(S->d_fix + 2 * S->arg_slot));
+            if (!dB || !dO) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
+            const int64_t key = ((((int64_t)bn * 257 + nq) * 64 + K) * 64 + occ) * 2 + (sky ? 1 : 0) + ((int64_t)sel_smem << 40);
+            cudaError_t e = ensure_graph(&S->g_batch, &S->g_batch_key, key, [&] { return batch_seq(dB, dO, bn, false); });
+            if (e != cudaSuccess) return fail(ctx, EWSJF_ERR_CUDA, "sweep batch graph: %s", cudaGetErrorString(e));
             LaunchScope ls(ctx, KIND_SWEEP);
-            sweep_merge_kernel<<<(nb * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, mrg_smem, st>>>(dO);
+            CU(cudaGraphLaunch(S->g_batch, st));
+            ctx->launches += S->g_batch_kernels - 1;
+        } else {
+            const SweepArgs* dB = sw_upload(ctx, A);
+            const SweepOutArgs* dO = sw_upload(ctx, O);
+            if (!dB || !dO) return fail(ctx, EWSJF_ERR_CUDA, "sweep: argument upload failed");
+            CU(batch_seq(dB, dO, bn, true));
         }
-        if (sky) {
-            LaunchScope ls(ctx, KIND_SWEEP);
-            sweep_direct_kernel<<<(nb * nq + kSwWarps - 1) / kSwWarps, kSwWarps * 32, 0, st>>>(dO);
-        }
-        {
-            LaunchScope ls(ctx, KIND_SWEEP);
-            sweep_summary_kernel<<<nb, 32, 0, st>>>(dO);
-        }
-        CU(cudaGetLastError());
     }
     return EWSJF_OK;
 }
