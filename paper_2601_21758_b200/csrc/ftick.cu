@@ -80,7 +80,7 @@ __host__ __device__ inline FSmem fsmem_layout(bool has_cost, int lut_size, int n
     L.lut = kFLutOff;
     o = fal(kFLutOff + lut_size + 1);
     L.ring = o;  o = fal(o + (int64_t)kFW * stages * narr * kFTile * 4);
-    L.bars = o;  o = fal(o + 12LL * kFMaxStages);   // mbarriers + release counters
+    L.bars = o;  o = fal(o + 20LL * kFMaxStages);   // mbarriers, release counters, stage chunk ids
     L.thr64 = o; o = fal(o + 8LL * kFMaxSlots);
     L.sec64 = o; o = fal(o + 8LL * kFMaxSlots);
     L.bmax = o;  o = fal(o + 8LL * kFMaxSlots * kFBoardMax);
@@ -305,23 +305,37 @@ __global__ void __launch_bounds__(kFT, 1)
     const int64_t nchunks = (A.n + CH - 1) / CH;
     const int64_t nfullc = A.n / CH;
     const int64_t nfull = A.n / kFTile;
+    // The last A.dyn_tail rounds of chunks are claimed from a grid-wide counter by whichever
+    // CTA refills a stage first (one atomic per chunk, by the refilling thread): the CTAs
+    // finish together instead of waiting for the slowest SM's last static chunks.  The
+    // chunk id of every stage is published in shared memory with the stage (-1: no more).
     const int my_iters = cta < nchunks ? (int)((nchunks - 1 - cta) / G + 1) : 0;
+    const int64_t srounds = A.dyn_tail > 0 ? max((int64_t)0, nchunks / G - A.dyn_tail) : (int64_t)my_iters;
+    const int my_static = (int)min((int64_t)my_iters, srounds);
+    const int64_t sbase = srounds * G;                                   // first dynamically claimed chunk
     unsigned char* ringc = smem + L.ring;
     uint64_t* fullb = (uint64_t*)(smem + L.bars);                       // [R] stage landed
     unsigned* relc = (unsigned*)(smem + L.bars + 8 * kFMaxStages);      // [R] warp releases (monotone)
+    int64_t* schunk = (int64_t*)(smem + L.bars + 12 * kFMaxStages);     // [R] chunk of the stage, -1: done
     auto stage = [&](int st, int a) -> unsigned char* { return ringc + (st * narr + a) * (CH * 4) + warp * (kFTile * 4); };
-    auto chunk_of = [&](int i) -> int64_t { return (int64_t)cta + (int64_t)G * i; };
-    auto issue_chunk = [&](int i) {   // one thread: iteration i's full chunk into stage i % R
-        if (i >= my_iters) return;
-        const int64_t c = chunk_of(i);
-        if (c >= nfullc) return;
+    auto issue_chunk = [&](int i) {   // one thread: iteration i's chunk into stage i % R
+        int64_t c = -1;
+        if (i < my_static) c = (int64_t)cta + (int64_t)G * i;
+        else if (A.dyn_tail > 0) c = sbase + (int64_t)atomicAdd(&A.ctr->ftiles, 1ull);
+        if (c >= nchunks) c = -1;
         const int s = i % R;
         uint64_t* b = &fullb[s];
-        mbar_arrive_expect_tx(b, (uint32_t)(narr * CH * 4));
-        unsigned char* d = ringc + s * narr * (CH * 4);
-        tma_load_1d(d, A.len + c * CH, CH * 4, b);
-        tma_load_1d(d + CH * 4, A.arrival + c * CH, CH * 4, b);
-        if (HAS_COST) tma_load_1d(d + 2 * CH * 4, A.cost + c * CH, CH * 4, b);
+        *(volatile int64_t*)&schunk[s] = c;
+        if (c >= 0 && c < nfullc) {
+            mbar_arrive_expect_tx(b, (uint32_t)(narr * CH * 4));     // release: orders the chunk id before
+            unsigned char* d = ringc + s * narr * (CH * 4);
+            tma_load_1d(d, A.len + c * CH, CH * 4, b);
+            tma_load_1d(d + CH * 4, A.arrival + c * CH, CH * 4, b);
+            if (HAS_COST) tma_load_1d(d + 2 * CH * 4, A.cost + c * CH, CH * 4, b);
+        } else {
+            // the ragged last chunk (direct loads) or the end: complete the phase without data
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+        }
     };
     {   // the LUT first (its own commit group, issued before the ring's bulk copies)
         const int l16 = (lutsz + 1 + 15) / 16;
@@ -345,8 +359,8 @@ __global__ void __launch_bounds__(kFT, 1)
         for (int i = 0; i < (A.sample_first ? 1 : R); i++) issue_chunk(i);
         // the chunks after the ring go to L2 while the CTAs agree on the sample bound
         // (the HBM would otherwise idle for ~6 us)
-        for (int i = R; i < R + A.l2_prefetch && i < my_iters; i++) {
-            const int64_t c = chunk_of(i);
+        for (int i = R; i < R + A.l2_prefetch && i < my_static; i++) {
+            const int64_t c = (int64_t)cta + (int64_t)G * i;
             if (c >= nfullc) break;
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.len + c * CH), "r"(CH * 4) : "memory");
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.arrival + c * CH), "r"(CH * 4) : "memory");
@@ -663,14 +677,15 @@ __global__ void __launch_bounds__(kFT, 1)
 
     // ---- sample tile, board, bound
     if (dbg && tid == 0) A.dbg[cta * kDbgStride + 25] = fgtime();
-    if (my_iters > 0) {
-        const int64_t c = chunk_of(0);
-        if (c < nfullc) {
-            mbar_wait(&fullb[0], 0u);
-            body(std::true_type(), std::true_type(), std::integral_constant<int, 0>(), c * kFW + warp, 0);
+    bool more = true;                     // iteration 0 is not the end of this CTA's chunks
+    {
+        mbar_wait(&fullb[0], 0u);
+        const int64_t c = *(volatile int64_t*)&schunk[0];
+        if (c < 0) more = false;
+        else {
+            if (c < nfullc) body(std::true_type(), std::true_type(), std::integral_constant<int, 0>(), c * kFW + warp, 0);
+            else body(std::false_type(), std::true_type(), std::integral_constant<int, 0>(), c * kFW + warp, 0);
             release(0, 0);
-        } else {
-            body(std::false_type(), std::true_type(), std::integral_constant<int, 0>(), c * kFW + warp, 0);
         }
     }
     if (dbg && tid == 0) A.dbg[cta * kDbgStride + 26] = fgtime();
@@ -777,7 +792,7 @@ __global__ void __launch_bounds__(kFT, 1)
     int chk = -1;
     if (A.refresh && warp < 6) {
         const int num = warp == 0 ? 1 : warp == 1 ? 2 : warp == 2 ? 4 : warp == 3 ? 6 : warp == 4 ? 8 : 12;
-        chk = (my_iters * num) >> 4;
+        chk = ((int)((nchunks + G - 1) / G) * num) >> 4;
         if (chk < 1) chk = -1;
     }
     auto refresh = [&]() {
@@ -812,17 +827,15 @@ __global__ void __launch_bounds__(kFT, 1)
         int st = 1 % RR;
         uint32_t ph = (1 / RR) & 1;
         int since_flush = 1;            // the sample iteration
-        for (int i = 1; i < my_iters; i++) {
+        for (int i = 1; more; i++) {
             if (*(volatile int*)&M->flag) collective();
-            const int64_t c = chunk_of(i);
+            mbar_wait(&fullb[st], ph);
+            const int64_t c = *(volatile int64_t*)&schunk[st];
+            if (c < 0) break;
             const int64_t t = c * kFW + warp;
-            if (c < nfullc) {
-                mbar_wait(&fullb[st], ph);
-                body(std::true_type(), std::false_type(), std::integral_constant<int, 0>(), t, st);
-                release(st, i);
-            } else {
-                body(std::false_type(), std::false_type(), std::integral_constant<int, 0>(), t, st);
-            }
+            if (c < nfullc) body(std::true_type(), std::false_type(), std::integral_constant<int, 0>(), t, st);
+            else body(std::false_type(), std::false_type(), std::integral_constant<int, 0>(), t, st);
+            release(st, i);
             if (++st == RR) { st = 0; ph ^= 1u; }
             if (++since_flush == A.cnt_flush) { flush_counters(); since_flush = 0; }
             if (i == chk) refresh();
@@ -954,6 +967,7 @@ __global__ void __launch_bounds__(kFT, 1)
     }
     __syncthreads();
     stamp(6);
+    if (cta == 0 && tid == 0) A.ctr->ftiles = 0ull;   // every chunk claim of this launch is done
     if (dbg && tid == 0) A.dbg[cta * kDbgStride + 24] = fgtime();
     if (A.refresh)   // nobody reads the refresh board past the barrier: clear this CTA's column for the next tick
         for (int q = tid; q < nslots; q += kFT) A.rboard[(size_t)q * G + cta] = 0ull;
