@@ -561,10 +561,20 @@ def main():
                        torch.from_numpy(pool["cost"]).to(dev), torch.empty(n, dtype=torch.int32, device=dev)))
     out = E.Outputs.alloc(args.k, dev)
     base = lo_r
+    # N > 1: the library's own NCCL communicator (ewsjf_ctx_init_nccl; the unique id goes
+    # over the torch process group once): ewsjf_tick then runs local -> ncclAllGather ->
+    # merge on the ctx stream.  torch's all_gather (tick_sharded) only if that fails.
+    lib_nccl = False
+    if ws > 1:
+        try:
+            ctx.init_nccl(rank=rank, world=ws, group=group)
+            lib_nccl = True
+        except Exception as e:  # noqa: BLE001
+            print(f"bench: library NCCL unavailable ({e}); torch all_gather instead", file=sys.stderr)
 
     def step(i):
         ln, ar, co, q = copies[i % 3]
-        if ws > 1:
+        if ws > 1 and not lib_nccl:
             E.tick_sharded(ctx, ln, ar, co, base, part, theta, sp, group=group, qid_out=q, out=out, sync=False)
         else:
             E.tick(ctx, ln, ar, co, part, theta, sp, global_base=base, qid_out=q, out=out, sync=False)
@@ -622,6 +632,9 @@ def main():
         "gpu_launches": int(tm["launches"] - launches0), "clocks": clocks, "strategic": strategic,
         "tick_summary": summary,
     }
+    if ws > 1:
+        line["exchange"] = ("library NCCL all-gather inside ewsjf_tick (ewsjf_ctx_init_nccl)" if lib_nccl
+                            else "torch.distributed all_gather_into_tensor between ewsjf_tick_local / ewsjf_tick_merge")
 
     # ---- e2e through the C ABI with host buffers (H2D + D2H inside the timed region)
     if not args.no_e2e and ws == 1:
