@@ -374,18 +374,24 @@ __global__ void __launch_bounds__(1024) kmeans_final_kernel(const int64_t* N, co
 
 // ------------------------------------------------------------------ A4 ---
 // Level-synchronous Eq. 2 over distinct-index segments.  flag[j] = 1 if a
-// segment starts at j.  One CTA; per level: segment bounds via a block scan of
-// the flags, then every index j tests the gap (v[j], v[j+1]) of its segment.
+// segment starts at j.  One CTA; per level: (1) segment starts compacted by a
+// block scan of the flags, every index j keeping its segment's ordinal in
+// sidx[j]; (2) one thread per segment: n, span and the Eq. 2 threshold
+// alpha * span (segments too small or too narrow get -1: final); (3) one thread
+// per index j tests the gap (v[j], v[j+1]) of its segment: g * (n - 1) > alpha * span.
+// (One warp per segment in (2)-(3) left the few wide coarse clusters of the first
+// levels to a handful of warps: 0.74 ms at 1M.)
 __global__ void __launch_bounds__(kHT, 1)
     refine_kernel(const int32_t* __restrict__ v, const int64_t* __restrict__ N, int64_t M, double alpha,
-                  int min_width, uint8_t* flag, int32_t* seg, int32_t* out, int* segend) {
+                  int min_width, uint8_t* flag, int32_t* seg, int32_t* out, int* segend, int32_t* sidx,
+                  double* srhs, double* sscale) {
     __shared__ int s_changed, s_m, s_level;
     __shared__ int wsum[32];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     if (tid == 0) { s_level = 1; }
     __syncthreads();
     for (;;) {
-        // 1) compact segment starts: seg[0..m) (ascending) ; segend[k] = next start
+        // 1) compact segment starts: seg[0..m) (ascending) ; sidx[j] = segment of j
         __syncthreads();
         if (tid == 0) s_m = 0;
         __syncthreads();
@@ -402,31 +408,37 @@ __global__ void __launch_bounds__(kHT, 1)
             }
             __syncthreads();
             const int base = s_m + (w ? wsum[w - 1] : 0);
-            if (f) seg[base + __popc(b & ((1u << lane) - 1u))] = (int32_t)j;
+            const int rank = base + __popc(b & ((1u << lane) - 1u));     // starts before j in the level
+            if (f) seg[rank] = (int32_t)j;
+            if (j < M) sidx[j] = rank + f - 1;                              // the last start <= j
             __syncthreads();
             if (tid == 0) s_m += wsum[31];
             __syncthreads();
         }
         const int m = s_m;
-        for (int k = tid; k < m; k += kHT) segend[k] = (k + 1 < m) ? seg[k + 1] : (int)M;
-        if (tid == 0) s_changed = 0;
-        __syncthreads();
-        // 2) each segment tests its gaps; new starts set after qualifying gaps
-        for (int k = w; k < m; k += kHT / 32) {
-            const int64_t x = seg[k], y = segend[k];
+        // 2) per segment: its end, and the Eq. 2 threshold (or -1: the segment is final)
+        for (int k = tid; k < m; k += kHT) {
+            const int64_t x = seg[k], y = (k + 1 < m) ? seg[k + 1] : M;
+            segend[k] = (int)y;
             const int64_t n = N[y] - N[x];
             const int64_t span = (int64_t)v[y - 1] - (int64_t)v[x];
-            if (n < 2 || span == 0 || span < (int64_t)min_width) continue;
-            const double lhs_scale = (double)(n - 1);
-            const double rhs = __dmul_rn(alpha, (double)span);
-            for (int64_t j = x + lane; j < y - 1; j += 32) {
-                const int64_t g = (int64_t)v[j + 1] - (int64_t)v[j];
-                if (__dmul_rn((double)g, lhs_scale) > rhs) {
-                    flag[j + 1] = 2;          // new start (marked 2 this level)
-                    s_changed = 1;
-                }
-            }
+            const bool fin = n < 2 || span == 0 || span < (int64_t)min_width;
+            srhs[k] = fin ? -1.0 : __dmul_rn(alpha, (double)span);
+            sscale[k] = (double)(n - 1);
         }
+        if (tid == 0) s_changed = 0;
+        __syncthreads();
+        // 3) per index: new starts after qualifying gaps (marked 2 this level)
+        int changed = 0;
+        for (int64_t j = tid; j + 1 < M; j += kHT) {
+            const int k = sidx[j];
+            if (j + 1 >= segend[k]) continue;             // the gap after j leaves the segment
+            const double rhs = srhs[k];
+            if (rhs < 0.0) continue;
+            const int64_t g = (int64_t)v[j + 1] - (int64_t)v[j];
+            if (__dmul_rn((double)g, sscale[k]) > rhs) { flag[j + 1] = 2; changed = 1; }
+        }
+        if (__any_sync(0xffffffffu, changed) && lane == 0) s_changed = 1;
         __syncthreads();
         if (!s_changed) break;
         for (int64_t j = tid; j < M; j += kHT)
@@ -1280,7 +1292,7 @@ static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int l
         // gap_rule 1 (set reading of G): Eq. 2 counts distinct lengths -> identity prefix
         if (p->gap_rule) iota_kernel<<<(int)((M + 1 + 255) / 256), 256, 0, st>>>(R->ps2, M + 1);
         refine_kernel<<<1, kHT, 0, st>>>(R->v, p->gap_rule ? R->ps2 : R->N, M, p->alpha, p->min_width, R->flag,
-                                          R->seg, R->out_i, R->segend);
+                                          R->seg, R->out_i, R->segend, R->plo, R->t1, R->t3);
     }
     CU(cudaGetLastError());
     CU(cudaEventRecord(R->ev[3], st));
