@@ -308,19 +308,34 @@ __device__ __forceinline__ bool better(double F, int64_t ij, double bF, int64_t 
     return F > bF || (F == bF && ij < bij);
 }
 
-// k = 3: block b handles i in a strided set, threads sweep j.  One result per block.
+// k = 3: block b handles tiles of kKmTile consecutive i (tile b, b + grid, ...), its
+// threads sweep j; each (S1[j], N[j], t3[j]) load serves the tile's kKmTile pairs
+// (one load triple per pair made the pair loop load-bound).  One result per block.
+constexpr int kKmTile = 8;
 __global__ void __launch_bounds__(256) kmeans3_kernel(const int64_t* __restrict__ N, const int64_t* __restrict__ S1,
                                                      const double* __restrict__ t1, const double* __restrict__ t3,
                                                      int64_t M, double* outF, int64_t* outIJ) {
     double bF = -1.0;
     int64_t bij = INT64_MAX;
-    for (int64_t i = 1 + blockIdx.x; i <= M - 2; i += gridDim.x) {
-        const int64_t Ni = N[i], Si = S1[i];
-        const double ti = t1[i];
-        for (int64_t j = i + 1 + threadIdx.x; j <= M - 1; j += blockDim.x) {
-            const double F = __dadd_rn(__dadd_rn(ti, sq_over(S1[j] - Si, N[j] - Ni)), t3[j]);
-            const int64_t ij = (i << 32) | j;
-            if (better(F, ij, bF, bij)) { bF = F; bij = ij; }
+    for (int64_t i0 = 1 + (int64_t)blockIdx.x * kKmTile; i0 <= M - 2; i0 += (int64_t)gridDim.x * kKmTile) {
+        int64_t Ni[kKmTile], Si[kKmTile];
+        double ti[kKmTile];
+#pragma unroll
+        for (int u = 0; u < kKmTile; u++) {
+            const int64_t i = min(i0 + u, M - 2);
+            Ni[u] = N[i]; Si[u] = S1[i]; ti[u] = t1[i];
+        }
+        for (int64_t j = i0 + 1 + threadIdx.x; j <= M - 1; j += blockDim.x) {
+            const int64_t Sj = S1[j], Nj = N[j];
+            const double tj = t3[j];
+#pragma unroll
+            for (int u = 0; u < kKmTile; u++) {
+                const int64_t i = i0 + u;
+                if (i > M - 2 || j <= i) continue;
+                const double F = __dadd_rn(__dadd_rn(ti[u], sq_over(Sj - Si[u], Nj - Ni[u])), tj);
+                const int64_t ij = (i << 32) | j;
+                if (better(F, ij, bF, bij)) { bF = F; bij = ij; }
+            }
         }
     }
     // block reduce
@@ -1270,7 +1285,7 @@ static ewsjf_status rp_from_hist(ewsjf_ctx* ctx, const unsigned int* hist, int l
             LaunchScope ls(ctx, KIND_PARTITION);
             kmeans_terms_kernel<<<256, 256, 0, st>>>(R->N, R->S1, M, R->t1, R->t3);
         }
-        const int kb = (int)std::min<int64_t>(R->kblocks, std::max<int64_t>(1, M - 2));
+        const int kb = (int)std::min<int64_t>(R->kblocks, std::max<int64_t>(1, (M - 2 + kKmTile - 1) / kKmTile));
         {
             LaunchScope ls(ctx, KIND_PARTITION);
             kmeans3_kernel<<<kb, 256, 0, st>>>(R->N, R->S1, R->t1, R->t3, M, R->kbF, R->kbI);
