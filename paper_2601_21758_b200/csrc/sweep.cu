@@ -188,28 +188,59 @@ __global__ void __launch_bounds__(kSwPrepThreads) sweep_count_kernel(const Sweep
     if (threadIdx.x < 2 && s_bad[threadIdx.x]) atomicAdd(&A.s.bad[threadIdx.x], (unsigned long long)s_bad[threadIdx.x]);
 }
 
+// One warp: exclusive prefix of the per-position counts cnt[0..nq) (nq <= 256, 8 per lane)
+// into off[0..nq], of their chunk counts into cp[0..nq], zeroed cursors; returns the
+// largest count (all lanes).  A one-thread loop over the positions took ~10 us (a
+// dependent L2 load per position).
+__device__ __forceinline__ int64_t sw_plan_warp(const int64_t* cnt, int nq, int chunk, int64_t* off, int32_t* cp,
+                                                int32_t* fill) {
+    const int lane = threadIdx.x & 31;
+    int64_t c[8], sum = 0, mx = 0;
+    int32_t sc = 0;
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+        const int q = lane * 8 + u;
+        c[u] = q < nq ? cnt[q] : 0;
+        sum += c[u];
+        sc += (int32_t)((c[u] + chunk - 1) / chunk);
+        mx = c[u] > mx ? c[u] : mx;
+    }
+    int64_t is = sum;
+    int32_t ic = sc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t us = __shfl_up_sync(0xffffffffu, is, o);
+        const int32_t uc = __shfl_up_sync(0xffffffffu, ic, o);
+        if (lane >= o) { is += us; ic += uc; }
+    }
+    int64_t bs = is - sum;
+    int32_t bc = ic - sc;
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+        const int q = lane * 8 + u;
+        if (q < nq) {
+            off[q] = bs;
+            cp[q] = bc;
+            if (fill) fill[q] = 0;
+            bs += c[u];
+            bc += (int32_t)((c[u] + chunk - 1) / chunk);
+        }
+    }
+    if (lane == 31) { off[nq] = is; cp[nq] = ic; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) { const int64_t v = __shfl_xor_sync(0xffffffffu, mx, o); mx = v > mx ? v : mx; }
+    return mx;
+}
+
 // K2 (one CTA of 32 threads): record offsets, chunk prefix, head features, reset cursors.
 __global__ void sweep_plan_kernel(const SweepArgs* __restrict__ Ap) {
     const SweepArgs& A = *Ap;
     __shared__ int s_ids[kMaxSlots], s_pos[kMaxSlots];
     for (int i = threadIdx.x; i < kMaxSlots; i += blockDim.x) { s_ids[i] = A.sorted_ids[i]; s_pos[i] = A.sorted_pos[i]; }
     __syncwarp();
-    if (threadIdx.x == 0) {
-        int64_t off = 0;
-        int32_t cp = 0;
-        for (int q = 0; q < A.nq; q++) {
-            A.s.qoff[q] = off;
-            A.s.cpre[q] = cp;
-            const int64_t c = A.s.qcount[q];
-            off += c;
-            cp += (int32_t)((c + A.chunk - 1) / A.chunk);
-        }
-        A.s.qoff[A.nq] = off;
-        A.s.cpre[A.nq] = cp;
-        *A.s.task_ctr = 0;
-    }
+    sw_plan_warp(A.s.qcount, A.nq, A.chunk, A.s.qoff, A.s.cpre, A.s.qfill);
+    if (threadIdx.x == 0) *A.s.task_ctr = 0;
     for (int q = threadIdx.x; q < A.nq; q += blockDim.x) {
-        A.s.qfill[q] = 0;
         float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
         const u64 hk = A.s.head[q];
         if (hk) {
@@ -645,22 +676,9 @@ __global__ void __launch_bounds__(kSwPrepThreads) sky_count_kernel(const SweepAr
 }
 __global__ void sky_plan_kernel(const SweepArgs* __restrict__ Ap) {
     const SweepArgs& A = *Ap;
-    if (threadIdx.x != 0) return;
-    int64_t off = 0;
-    int32_t cp = 0;
-    for (int q = 0; q < A.nq; q++) {
-        A.s.qoff2[q] = off;
-        A.s.cpre2[q] = cp;
-        const int64_t c = A.s.qcnt2[q];
-        off += c;
-        cp += (int32_t)((c + A.chunk - 1) / A.chunk);
-        A.s.qfill2[q] = 0;
-    }
-    A.s.qoff2[A.nq] = off;
-    A.s.cpre2[A.nq] = cp;
-    int64_t mx = 0;
-    for (int q = 0; q < A.nq; q++) mx = A.s.qcnt2[q] > mx ? A.s.qcnt2[q] : mx;
-    *A.s.direct = mx <= kSwDirectMax;
+    if (threadIdx.x >= 32) return;
+    const int64_t mx = sw_plan_warp(A.s.qcnt2, A.nq, A.chunk, A.s.qoff2, A.s.cpre2, A.s.qfill2);
+    if (threadIdx.x == 0) *A.s.direct = mx <= kSwDirectMax;
 }
 __global__ void __launch_bounds__(kSwPrepThreads) sky_compact_kernel(const SweepArgs* __restrict__ Ap) {
     const SweepArgs& A = *Ap;
@@ -1005,16 +1023,19 @@ __global__ void __launch_bounds__(kSwWarps * 32) sweep_direct_kernel(const Sweep
 __global__ void sweep_summary_kernel(const SweepOutArgs* __restrict__ Ap) {
     const SweepOutArgs& A = *Ap;
     const int th = blockIdx.x;
-    if (th >= A.n_theta || threadIdx.x != 0) return;
+    const int lane = threadIdx.x & 31;
+    if (th >= A.n_theta || threadIdx.x >= 32) return;
     const ewsjf_select_out& o = A.outs[th];
-    int primary = -1;
-    float best = 0.f;
-    for (int p = 0; p < A.nq; p++) {
+    // lane-parallel: key = (ordered head score, ~position), max = highest score, lowest position
+    u64 best = 0ull;
+    for (int p = lane; p < A.nq; p += 32)
         if (o.d_count[p] > 0) {
-            const float h = o.d_head_score[p];
-            if (primary < 0 || h > best) { primary = p; best = h; }
+            const u64 k = ((u64)ord_f32(o.d_head_score[p]) << 32) | (u64)(~(u32)p);
+            best = k > best ? k : best;
         }
-    }
+    best = warp_max_u64(best);
+    if (lane != 0) return;
+    const int primary = best ? (int)(~(u32)best) : -1;
     if (o.d_summary) {
         ewsjf_summary sm;
         memset(&sm, 0, sizeof sm);
