@@ -83,6 +83,12 @@ def test_partition_full_c4_bimodal(E, orc, ctx):
     _check(*_both(E, orc, ctx, workload.bimodal(100_000_000, 401)))
 
 
+def test_partition_full_c4_heavy(E, orc, ctx):
+    """C4 at full size, the benched input: a 100M heavy-tailed history (seed 402,
+    32,631 distinct lengths, 32,599 Stage-3 merges)."""
+    _check(*_both(E, orc, ctx, workload.heavy(100_000_000, 402)))
+
+
 @pytest.mark.parametrize("rule", [0, 1])
 @pytest.mark.parametrize("top", [12_000, 18_000, 25_000, 40_000])
 def test_partition_many_segments(E, orc, ctx, rule, top):
