@@ -632,7 +632,12 @@ static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, 
     A.gthr = ctx->gthr;
     A.board = ctx->board;
     A.rboard = ctx->board + (size_t)64 * G * 2;      // [64][G] after the sample board [64][G][<=2]
-    A.refresh = (K <= G && G <= 160 && merge_mode != 0 && !getenv("EWSJF_NO_REFRESH")) ? 1 : 0;
+    // progressive bound refresh (mid-stream board of CTA maxima): off by default -- the
+    // refreshing warp held its ring stage for the board's L2 round trip and stalled the
+    // CTA's pipeline (measured C3 68.4 -> 64.1 us without it, K=1 67.4 -> 60.6, balanced
+    // 76.3 -> 73.9, FIFO 84.0 -> 76.5; never slower); EWSJF_REFRESH=1 turns it on
+    A.refresh = (K <= G && G <= 160 && merge_mode != 0 && getenv("EWSJF_REFRESH") && atoi(getenv("EWSJF_REFRESH")))
+                    ? 1 : 0;
     A.ovf_keys = ctx->f_ovf_keys;
     A.ovf_code = ctx->f_ovf_code;
     A.gap = ctx->gap;
