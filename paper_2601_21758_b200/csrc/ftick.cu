@@ -1144,29 +1144,37 @@ __global__ void __launch_bounds__(kFT, 1)
         }
         if (dbg && tid == 0) { A.dbg[cta * kDbgStride + 16] = fgtime(); A.dbg[cta * kDbgStride + 17] = (unsigned long long)pn; }
         const int ns = min(pn, K);
-        if (pn <= 128) {
+        if (pn <= kFT) {
             // small pool: one counting pass ranks every candidate (keys are unique),
-            // rank < K are the top K already in order -- no radix select, no sort
-            // 4 threads per candidate (768 threads: up to 192), each counting the keys
-            // above it in every 4th 16-byte pair, 2 loads in flight; pool padded with zeros
+            // rank < K are the top K already in order -- no radix select, no sort.
+            // tpc = 4 / 2 / 1 threads per candidate (pools of <= 192 / 384 / 768), each
+            // counting the keys above it in every tpc-th 16-byte pair; pool padded with
+            // zeros.  (Up to 128 only, the merge fell back to the 8-pass radix select
+            // for the ~180 candidates of the dominant queue: 3.1 vs ~1 us.)
+            const int tpc = pn <= kFT / 4 ? 4 : (pn <= kFT / 2 ? 2 : 1);
             const int pn8 = (pn + 7) & ~7;
             if (tid >= pn && tid < pn8) pool[tid] = 0ull;
             __syncthreads();
-            const int ci = tid >> 2, part = tid & 3;
+            const int ci = tid / tpc, part = tid - ci * tpc;
             const u64 k0 = ci < pn ? pool[ci] : 0ull;
             int r0 = 0;
             if (ci < pn) {
                 int r1 = 0;
-                for (int j = 2 * part; j < pn8; j += 16) {
+                int j = 2 * part;
+                for (; j + 2 * tpc < pn8; j += 4 * tpc) {          // two pairs in flight
                     const ulonglong2 x = *(const ulonglong2*)(pool + j);
-                    const ulonglong2 y = *(const ulonglong2*)(pool + j + 8);
+                    const ulonglong2 y = *(const ulonglong2*)(pool + j + 2 * tpc);
                     r0 += (x.x > k0) + (x.y > k0);
-                    r1 += (j + 8 < pn8) ? (y.x > k0) + (y.y > k0) : 0;
+                    r1 += (y.x > k0) + (y.y > k0);
+                }
+                if (j < pn8) {
+                    const ulonglong2 x = *(const ulonglong2*)(pool + j);
+                    r0 += (x.x > k0) + (x.y > k0);
                 }
                 r0 += r1;
             }
-            r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
-            r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
+            if (tpc >= 2) r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
+            if (tpc == 4) r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
             __syncthreads();
             if (ci < pn && part == 0 && r0 < K) surv[r0] = k0;
             __syncthreads();

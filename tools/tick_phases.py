@@ -19,7 +19,7 @@ import workload  # noqa: E402
 
 SLOTS = {"start": 0, "issued": 10, "zero": 12, "setup": 1, "sample_tile": 26, "sample": 2, "pub": 13,
          "bound": 14, "thr": 3, "stream": 4, "rows_cut": 28, "counts": 29, "agg": 30, "pre_barrier": 5,
-         "barrier": 6, "merge_rows": 20, "merge_filtered": 16, "merge_selected": 18, "merge_out": 19, "merge": 7}
+         "barrier": 6, "merge_rows": 20, "merge_filtered": 16, "merge_selected": 18, "merge_out": 19, "merge_rep0_end": 27, "merge": 7}
 
 
 def main():
@@ -66,10 +66,12 @@ def main():
             v = v[(v > 0) & (v >= t0) & (v < t0 + 10_000_000)]
             if len(v):
                 r[name] = ((np.median(v) - t0) / 1e3, (v.max() - t0) / 1e3)
+        pn = ph[:, 17]
+        r["merge_pn_max"] = (float(pn[pn < 1_000_000].max()) if (pn < 1_000_000).any() else 0.0, 0.0)
         rows.append(r)
     res = {"n": a.n, "partition": a.partition, "k": a.k, "tick_us_event": ev_us,
            "ph": {name: "%.1f/%.1f" % tuple(np.median([r[name][j] for r in rows[2:] if name in r]) for j in (0, 1))
-                  for name in SLOTS if any(name in r for r in rows[2:])}}
+                  for name in list(SLOTS) + ["merge_pn_max"] if any(name in r for r in rows[2:])}}
     print(json.dumps(res))
 
 
