@@ -615,6 +615,7 @@ static bool run_ftick(ewsjf_ctx* ctx, const int32_t* d_len, const float* d_arr, 
     A.diag = getenv("EWSJF_DIAG") ? atoi(getenv("EWSJF_DIAG")) : 0;
     A.sample_first = getenv("EWSJF_SAMPLE_FIRST") ? atoi(getenv("EWSJF_SAMPLE_FIRST")) : 1;   // measured: -0.7 us (C3 balanced)
     A.dyn_tail = getenv("EWSJF_DYN_TAIL") ? std::max(0, atoi(getenv("EWSJF_DYN_TAIL"))) : 2;
+    A.l2_hint = getenv("EWSJF_L2_HINT") ? atoi(getenv("EWSJF_L2_HINT")) : 1;   // measured -0.45 us at C3
     A.cnt_flush = 62;     // a u8 counter gains <= 4 per iteration: (1 + 62) * 4 <= 255
     if (const char* e = getenv("EWSJF_CNT_FLUSH")) A.cnt_flush = std::max(1, std::min(62, atoi(e)));
     const int G = ctx->num_sms;

@@ -118,6 +118,16 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {
         default: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
     }
 }
+// 1-D bulk copy with an L2 cache-policy hint (evict-first for the pool, read exactly once:
+// the streamed 120 MB then stop evicting the kernel's code, LUT, boards and rows from L2)
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
 // non-aligned barrier: warps arrive from different call sites (the collective is entered from the
 // streaming loop and from the idle loop), which the .aligned form (bar.sync) does not allow
 __device__ __forceinline__ void fbar(int id) { asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(kFT) : "memory"); }
@@ -329,9 +339,17 @@ __global__ void __launch_bounds__(kFT, 1)
         if (c >= 0 && c < nfullc) {
             mbar_arrive_expect_tx(b, (uint32_t)(narr * CH * 4));     // release: orders the chunk id before
             unsigned char* d = ringc + s * narr * (CH * 4);
-            tma_load_1d(d, A.len + c * CH, CH * 4, b);
-            tma_load_1d(d + CH * 4, A.arrival + c * CH, CH * 4, b);
-            if (HAS_COST) tma_load_1d(d + 2 * CH * 4, A.cost + c * CH, CH * 4, b);
+            if (A.l2_hint) {
+                uint64_t pol;
+                asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+                tma_load_1d_hint(d, A.len + c * CH, CH * 4, b, pol);
+                tma_load_1d_hint(d + CH * 4, A.arrival + c * CH, CH * 4, b, pol);
+                if (HAS_COST) tma_load_1d_hint(d + 2 * CH * 4, A.cost + c * CH, CH * 4, b, pol);
+            } else {
+                tma_load_1d(d, A.len + c * CH, CH * 4, b);
+                tma_load_1d(d + CH * 4, A.arrival + c * CH, CH * 4, b);
+                if (HAS_COST) tma_load_1d(d + 2 * CH * 4, A.cost + c * CH, CH * 4, b);
+            }
         } else {
             // the ragged last chunk (direct loads) or the end: complete the phase without data
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");

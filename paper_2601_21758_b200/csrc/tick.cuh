@@ -65,6 +65,7 @@ struct FArgs {
     int32_t cnt_flush;          // iterations between u8 member-counter flushes (<= 62)
     int32_t sample_first;       // ring prologue: the sample chunk alone, the rest after the setup
     int32_t dyn_tail;           // last rounds of chunks claimed dynamically (0: all static)
+    int32_t l2_hint;            // evict-first L2 policy on the pool's bulk copies
     int32_t board_m;            // sample board keys per (queue, CTA); 0 = no sample bound
     int32_t merge;              // 0: rows only; 1: final outputs; 2: exchange record (merge_phase)
     int32_t diag;               // timing diagnostics (EWSJF_DIAG bits); 0 in normal use
