@@ -284,7 +284,10 @@ __global__ void __launch_bounds__(kFT, 1)
     constexpr int narr = HAS_COST ? 3 : 2;
     const FSmem L = fsmem_layout(HAS_COST, lutsz, nslots, R);
     unsigned char* lut = smem + kFLutOff;
-    float4* rec = (float4*)(smem + kFRecOff);           // [code][2]: {wb, wu, wf', thrf}, {secf, qid, cntoff, -}
+    // per-code records, two arrays of 16-byte entries (one [code][2] array put the lanes of
+    // a warp with mixed codes on 4 bank groups: 8 wavefronts per LDS.128 instead of 4)
+    float4* recA = (float4*)(smem + kFRecOff);          // [code]: {wb, wu, wf', thrf}
+    float4* recB = recA + 256;                          // [code]: {secf, qid, cntoff, -}
     u64* thr64 = (u64*)(smem + L.thr64);
     u64* sec64 = (u64*)(smem + L.sec64);
     u32* bmax = (u32*)(smem + L.bmax);     // [q][m] high words of the CTA's top keys (native u32 atomics)
@@ -430,8 +433,8 @@ __global__ void __launch_bounds__(kFT, 1)
             }
             b.y = __int_as_float(qid);
             b.z = __int_as_float(cnto * kFT);
-            rec[2 * c] = a;
-            rec[2 * c + 1] = b;
+            recA[c] = a;
+            recB[c] = b;
         }
         if (tid == 0 && lutsz >= 0) lut[lutsz] = (unsigned char)kFCodeFar;   // lengths >= lut_size
     }
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(kFT, 1)
         if (t > *(volatile u64*)&thr64[q]) {
             atomicMax(&thr64[q], t);
             const u32 hi = (u32)(t >> 32);
-            ((volatile float*)&rec[2 * q])[3] = SCORE ? __uint_as_float(hi) : fifo_hi_to_f(hi);
+            ((volatile float*)&recA[q])[3] = SCORE ? __uint_as_float(hi) : fifo_hi_to_f(hi);
         }
     };
     auto insert = [&](int q, u64 k) {
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(kFT, 1)
         if (k2 > *(volatile u64*)&sec64[q]) {
             atomicMax(&sec64[q], k2);
             const u32 hi = (u32)(k2 >> 32);
-            ((volatile float*)&rec[2 * q + 1])[0] = SCORE ? fifo_hi_to_f(hi) : __uint_as_float(hi);
+            ((volatile float*)&recB[q])[0] = SCORE ? fifo_hi_to_f(hi) : __uint_as_float(hi);
         }
     };
     // queue position of a length beyond the LUT (binary search over the policy bounds), -1 = gap
@@ -511,7 +514,7 @@ __global__ void __launch_bounds__(kFT, 1)
             atomicSub(cntw + nslots * kFCntRow, cinc);      // not invalid after all
             const int q = bsearch(b);
             if (q >= 0) {
-                const float4 w = rec[2 * q];
+                const float4 w = recA[q];
                 ok = score_sp(b, a, co, HAS_COST, A.sp, w.x, w.y, w.z, &sp);
                 atomicAdd(cntw + q * kFCntRow, cinc);
                 if (write_qid) A.qid_out[idx] = P.sid[q];
@@ -588,8 +591,8 @@ __global__ void __launch_bounds__(kFT, 1)
             // FAR / GAP codes, which the rare path takes back out); padding uncounted
             const int crow = min(c, nslots);
             if (FULL || j < nv) atomicAdd(cntw + crow * kFCntRow, cinc);
-            const float4 w = rec[2 * c];
-            const float4 r2 = rec[2 * c + 1];
+            const float4 w = recA[c];
+            const float4 r2 = recB[c];
             const bool ok = score_sp(b[j], a[j], co[j], HAS_COST, A.sp, w.x, w.y, w.z, &sp[j]);
             okv[j] = ok;
             qo[j] = __float_as_int(r2.y);
@@ -780,13 +783,13 @@ __global__ void __launch_bounds__(kFT, 1)
         const u64 g = thr64[q];
         const u32 hi = (u32)(g >> 32);
         const float inf = __int_as_float(0x7f800000);
-        rec[2 * q].w = SCORE ? __uint_as_float(hi) : (g ? fifo_hi_to_f(hi) : inf);
+        recA[q].w = SCORE ? __uint_as_float(hi) : (g ? fifo_hi_to_f(hi) : inf);
         const u64 s = sec64[q];
         const u32 sh = (u32)(s >> 32);
-        rec[2 * q + 1].x = SCORE ? (s ? fifo_hi_to_f(sh) : inf) : __uint_as_float(sh);
+        recB[q].x = SCORE ? (s ? fifo_hi_to_f(sh) : inf) : __uint_as_float(sh);
         if (A.diag & 1) {   // timing diagnostic only (EWSJF_DIAG=1): no candidate ever passes (wrong outputs)
-            rec[2 * q].w = SCORE ? inf : -inf;
-            rec[2 * q + 1].x = SCORE ? -inf : inf;
+            recA[q].w = SCORE ? inf : -inf;
+            recB[q].x = SCORE ? -inf : inf;
             thr64[q] = ~0ull;
             sec64[q] = ~0ull;
         }
@@ -1215,7 +1218,7 @@ __global__ void __launch_bounds__(kFT, 1)
         }
         if (dbg && tid == 0) A.dbg[cta * kDbgStride + 18] = fgtime();
         const float qi = (float)(q + 1);
-        const float4 wq = rec[2 * q];        // the staged weights (rec is untouched by the merge)
+        const float4 wq = recA[q];        // the staged weights (rec is untouched by the merge)
         const float wb = wq.x, wu = wq.y, wf = wq.z;
         auto payload = [&](u64 k) -> float {   // s' of the request with key k
             if (SCORE) return key_sp(k);
