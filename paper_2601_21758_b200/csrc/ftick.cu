@@ -701,6 +701,7 @@ __global__ void __launch_bounds__(kFT, 1)
     bool more = true;                     // iteration 0 is not the end of this CTA's chunks
     {
         mbar_wait(&fullb[0], 0u);
+        if (dbg && tid == 0) A.dbg[cta * kDbgStride + 15] = fgtime();   // the sample chunk has landed
         const int64_t c = *(volatile int64_t*)&schunk[0];
         if (c < 0) more = false;
         else {

@@ -17,7 +17,7 @@ sys.path.insert(0, ROOT)
 import paper_2601_21758_b200 as E  # noqa: E402
 import workload  # noqa: E402
 
-SLOTS = {"start": 0, "issued": 10, "zero": 12, "setup": 1, "sample_tile": 26, "sample": 2, "pub": 13,
+SLOTS = {"start": 0, "issued": 10, "zero": 12, "setup": 1, "sample_landed": 15, "sample_tile": 26, "sample": 2, "pub": 13,
          "bound": 14, "thr": 3, "stream": 4, "rows_cut": 28, "counts": 29, "agg": 30, "pre_barrier": 5,
          "barrier": 6, "merge_rows": 20, "merge_filtered": 16, "merge_selected": 18, "merge_out": 19, "merge_rep0_end": 27, "merge": 7}
 
