@@ -2,10 +2,11 @@
 // Eq. 4 score A10 + per-queue filter A11) and its fusion with the per-queue
 // merge (merge.cuh) behind one grid barrier.
 //
-// The tick is HBM-bound only if nothing makes the warps of an SM wait for each
-// other, so every warp owns a private ring of A.stages 1-D TMA bulk copies
-// (cp.async.bulk + mbarrier; 128 requests x {len, arrival, cost} per stage)
-// and walks its own warp tiles.  Per request the common path is: byte-LUT
+// (The round-1 tick, kept behind EWSJF_NO_FTICK / EWSJF_OLD_TICK; the default tick
+// is ftick.cu.)  Every warp owns a private ring of A.stages stages (128 requests x
+// {len, arrival, cost} per stage), filled by per-lane 16-byte cp.async copies
+// (LDGSTS; a ring of 1-D TMA bulk copies per warp behind EWSJF_TMA_RING measured
+// slower: ~90 cycles per 512-byte bulk copy), and walks its own warp tiles.  Per request the common path is: byte-LUT
 // route, qid store, weights (float4) + Eq. 4 (one MUFU.LG2, one MUFU.RCP), a
 // per-thread u16 member counter and two 32-bit threshold compares.
 //
