@@ -780,15 +780,8 @@ static ewsjf_status tick_host_pipelined(ewsjf_ctx* ctx, const int32_t* h_len, co
     if (s != EWSJF_OK) return s;
     CU(cudaEventRecord(ctx->pipe_d2h, ctx->d2h_st));
     CU(cudaStreamWaitEvent(st, ctx->pipe_d2h, 0));                // the qid slices are back before the ctx stream moves on
-    // peek at the summary: a capacity overflow of the records -> redo in one pass
-    CU(cudaMemcpyAsync(ctx->h_summary, ctx->d_summary, sizeof(ewsjf_summary), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
     *on_device = true;
-    if (ctx->h_summary->status == EWSJF_ERR_CAPACITY) return EWSJF_OK;   // *done stays false: the caller's
-                                                                         // single pass runs (pool on the device)
-    if (ctx->h_summary->n_gap > 0 && h_qid_out)                   // Alg. 2 rewrote gap requests' qid after the copies
-        CU(cudaMemcpyAsync(h_qid_out, ctx->d_qid, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
-    *done = true;
+    *done = true;            // the caller checks the summary (capacity -> single pass over the resident pool)
     return EWSJF_OK;
 }
 
@@ -810,6 +803,36 @@ extern "C" ewsjf_status ewsjf_tick_host(ewsjf_ctx* ctx, const int32_t* h_len, co
                                               params, h_qid_out, &piped, &on_device);
         if (ps != EWSJF_OK) return ps;
     }
+    const int K = params->k;
+    auto copy_results = [&]() -> ewsjf_status {
+        if (h_topk_id) CU(cudaMemcpyAsync(h_topk_id, ctx->d_topk_id, (size_t)kMaxSlots * K * 8, cudaMemcpyDeviceToHost, st));
+        if (h_topk_score)
+            CU(cudaMemcpyAsync(h_topk_score, ctx->d_topk_score, (size_t)kMaxSlots * K * 4, cudaMemcpyDeviceToHost, st));
+        if (h_count) CU(cudaMemcpyAsync(h_count, ctx->d_count, kMaxSlots * 8, cudaMemcpyDeviceToHost, st));
+        if (h_head_id) CU(cudaMemcpyAsync(h_head_id, ctx->d_head_id, kMaxSlots * 8, cudaMemcpyDeviceToHost, st));
+        if (h_head_score) CU(cudaMemcpyAsync(h_head_score, ctx->d_head_score, kMaxSlots * 4, cudaMemcpyDeviceToHost, st));
+        if (h_max_score) CU(cudaMemcpyAsync(h_max_score, ctx->d_max_score, kMaxSlots * 4, cudaMemcpyDeviceToHost, st));
+        return EWSJF_OK;
+    };
+    if (piped) {
+        // one synchronisation: results, summary and bubble log together; a capacity
+        // overflow of the exchange records falls through to the single pass below
+        ewsjf_status cs = copy_results();
+        if (cs != EWSJF_OK) return cs;
+        CU(cudaMemcpyAsync(ctx->h_summary, ctx->d_summary, sizeof(ewsjf_summary), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(ctx->h_blog, ctx->d_blog, sizeof(BubbleLog), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (ctx->h_summary->status != EWSJF_ERR_CAPACITY) {
+            if (ctx->h_summary->n_gap > 0 && h_qid_out) {   // Alg. 2 rewrote gap requests' qid after the copies
+                CU(cudaMemcpyAsync(h_qid_out, ctx->d_qid, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+                CU(cudaStreamSynchronize(st));
+            }
+            *h_summary = *ctx->h_summary;
+            if (ctx->h_summary->n_bubbles > 0) apply_bubbles(ctx->h_blog, part);
+            return (ewsjf_status)ctx->h_summary->status;
+        }
+        piped = false;
+    }
     if (!piped) {
         if (n > 0 && !on_device) {
             CU(cudaMemcpyAsync(ctx->d_len, h_len, (size_t)n * 4, cudaMemcpyHostToDevice, st));
@@ -823,14 +846,10 @@ extern "C" ewsjf_status ewsjf_tick_host(ewsjf_ctx* ctx, const int32_t* h_len, co
         if (s != EWSJF_OK) return s;
         if (h_qid_out && n > 0) CU(cudaMemcpyAsync(h_qid_out, ctx->d_qid, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
     }
-    const int K = params->k;
-    if (h_topk_id) CU(cudaMemcpyAsync(h_topk_id, ctx->d_topk_id, (size_t)kMaxSlots * K * 8, cudaMemcpyDeviceToHost, st));
-    if (h_topk_score)
-        CU(cudaMemcpyAsync(h_topk_score, ctx->d_topk_score, (size_t)kMaxSlots * K * 4, cudaMemcpyDeviceToHost, st));
-    if (h_count) CU(cudaMemcpyAsync(h_count, ctx->d_count, kMaxSlots * 8, cudaMemcpyDeviceToHost, st));
-    if (h_head_id) CU(cudaMemcpyAsync(h_head_id, ctx->d_head_id, kMaxSlots * 8, cudaMemcpyDeviceToHost, st));
-    if (h_head_score) CU(cudaMemcpyAsync(h_head_score, ctx->d_head_score, kMaxSlots * 4, cudaMemcpyDeviceToHost, st));
-    if (h_max_score) CU(cudaMemcpyAsync(h_max_score, ctx->d_max_score, kMaxSlots * 4, cudaMemcpyDeviceToHost, st));
+    {
+        ewsjf_status cs = copy_results();
+        if (cs != EWSJF_OK) return cs;
+    }
     return finish_sync(ctx, part, h_summary, ctx->d_summary);
 }
 
