@@ -559,10 +559,6 @@ __global__ void __launch_bounds__(kFT, 1)
             const float4 av = ((const float4*)stage(st, 1))[lane];
             float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
             if (HAS_COST) cv = ((const float4*)stage(st, 2))[lane];
-            if (!SAMPLE && (A.diag & 2)) {   // timing diagnostic (EWSJF_DIAG=2): stream only
-                if (write_qid) __stcs((int4*)(A.qid_out + i0), make_int4(bv.x ^ __float_as_int(av.x), bv.y, bv.z, __float_as_int(cv.w)));
-                return;
-            }
             b[0] = bv.x; b[1] = bv.y; b[2] = bv.z; b[3] = bv.w;
             a[0] = av.x; a[1] = av.y; a[2] = av.z; a[3] = av.w;
             co[0] = cv.x; co[1] = cv.y; co[2] = cv.z; co[3] = cv.w;
