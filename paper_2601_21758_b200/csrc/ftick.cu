@@ -857,7 +857,8 @@ __global__ void __launch_bounds__(kFT, 1)
             if (++st == RR) { st = 0; ph ^= 1u; }
             if (++since_flush == A.cnt_flush) { flush_counters(); since_flush = 0; }
             if (i == chk) refresh();
-            if ((i & 3) == 0 && nslots > 0) {
+            if (A.refresh && (i & 3) == 0 && nslots > 0) {   // the global bounds only move with the refresh
+                                                              // (or a rare collective: its CTA's own bound rises)
                 if (lane == 0) {
                     if (gpoll) raise_thr(rq, gpoll);
                     rq += kFW;
