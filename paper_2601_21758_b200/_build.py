@@ -9,13 +9,16 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libewsjf.so")
-BUILD = os.path.join(ROOT, "build", "ewsjf")
+# EWSJF_CHECKED=1: the bounds-checked variant (device EWSJF_CHECK sites compiled in,
+# common.cuh) as libewsjf_check.so; the binding loads it under the same variable
+CHECKED = os.environ.get("EWSJF_CHECKED") == "1"
+OUT = os.path.join(HERE, "libewsjf_check.so" if CHECKED else "libewsjf.so")
+BUILD = os.path.join(ROOT, "build", "ewsjf_check" if CHECKED else "ewsjf")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-ftz=true",
     "-Xcompiler", "-fPIC,-ffp-contract=off", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
-]
+] + (["-DEWSJF_BOUNDS_CHECK"] if CHECKED else [])
 
 
 def _stale() -> bool:

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libewsjf.so")
+LIB_PATH = os.path.join(HERE, "libewsjf_check.so" if os.environ.get("EWSJF_CHECKED") == "1" else "libewsjf.so")
 
 MAX_QUEUES = 256
 HIST_BINS = 1 << 20

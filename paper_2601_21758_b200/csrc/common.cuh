@@ -22,6 +22,24 @@ static inline cudaError_t ewsjf_counted_free_(void* p) { ewsjf_count_alloc_(); r
 #define cudaMallocHost(p, n) ewsjf_counted_malloc_host_((void**)(p), (n))
 #define cudaFree(p) ewsjf_counted_free_((void*)(p))
 
+// Device bounds checks of the bounds-checked build (EWSJF_CHECKED=1 builds
+// libewsjf_check.so with -DEWSJF_BOUNDS_CHECK; compute-sanitizer is not available on
+// the GPU pool): a failed check prints its site and traps (the call returns
+// EWSJF_ERR_CUDA).  Compiled out of libewsjf.so.
+#ifdef EWSJF_BOUNDS_CHECK
+#include <cstdio>
+#define EWSJF_CHECK(c)                                                                        \
+    do {                                                                                      \
+        if (!(c)) {                                                                           \
+            printf("EWSJF_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,    \
+                   (int)blockIdx.x, (int)threadIdx.x, #c);                                    \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define EWSJF_CHECK(c) do { } while (0)
+#endif
+
 namespace ewsjf {
 
 typedef unsigned long long u64;

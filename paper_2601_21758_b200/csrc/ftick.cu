@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kFT, 1)
         if (i < my_static) c = (int64_t)cta + (int64_t)G * i;
         else if (A.dyn_tail > 0) c = sbase + (int64_t)atomicAdd(&A.ctr->ftiles, 1ull);
         if (c >= nchunks) c = -1;
+        EWSJF_CHECK(c < nfullc ? (c + 1) * CH <= A.n : c == -1 || c == nchunks - 1);
         const int s = i % R;
         uint64_t* b = &fullb[s];
         *(volatile int64_t*)&schunk[s] = c;
@@ -475,6 +476,7 @@ __global__ void __launch_bounds__(kFT, 1)
     auto insert = [&](int q, u64 k) {
         const u32 kh = (u32)(k >> 32);       // CTA max high word (refresh board)
         if (kh > *(volatile u32*)&bmax[q * kFBoardMax]) atomicMax(&bmax[q * kFBoardMax], kh);
+        EWSJF_CHECK(q >= 0 && q < nslots);
         const int pos = atomicAdd(&rcnt[q], 1);
         if (pos < RC) {
             rows_cta[q * row_stride + pos] = k;
@@ -1102,6 +1104,7 @@ __global__ void __launch_bounds__(kFT, 1)
             if (lane == 31 && incl) wbase = atomicAdd(&M->pn, incl);
             wbase = __shfl_sync(0xffffffffu, wbase, 31);
             int o = wbase + incl - c;
+            EWSJF_CHECK(o + c <= pcap);
 #pragma unroll
             for (int u = 0; u < 8; u++)
                 if (pmask & (1u << u)) pool[o++] = kv[u];
@@ -1145,7 +1148,11 @@ __global__ void __launch_bounds__(kFT, 1)
                 }
 #pragma unroll
                 for (int u = 0; u < kChunk / kFT; u++)
-                    if (kx[u] && kx[u] >= thr) pool[atomicAdd(&M->pn, 1)] = kx[u];
+                    if (kx[u] && kx[u] >= thr) {
+                        const int o = atomicAdd(&M->pn, 1);
+                        EWSJF_CHECK(o < pcap);
+                        pool[o] = kx[u];
+                    }
                 __syncthreads();
                 pn = M->pn;
                 __syncthreads();

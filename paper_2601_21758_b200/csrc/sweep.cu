@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(kSortThreads) sky_scatter_kernel(const SweepAr
         if (!sky_grouped(A, p, b)) continue;
         const unsigned slot = b < kSortBins ? atomicAdd(&s_h[b], 1u)
                                             : (unsigned)A.s.bcnt[b] + (unsigned)atomicAdd(&A.s.bfill[b], 1);
+        EWSJF_CHECK(slot >= (unsigned)A.s.bcnt[b] && slot < (unsigned)A.s.bcnt[b + 1]);
         A.s.rec2[slot] = f;
     }
 }
@@ -691,7 +692,11 @@ __global__ void __launch_bounds__(kSwPrepThreads) sky_compact_kernel(const Sweep
     for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
         p = sky_pos_from(s_qoff, A.nq, p, i);
         const float4 f = A.s.rec[i];
-        if (sky_keep(A, f, p)) A.s.rec2[A.s.qoff2[p] + atomicAdd(&A.s.qfill2[p], 1)] = f;
+        if (sky_keep(A, f, p)) {
+            const int64_t o = A.s.qoff2[p] + atomicAdd(&A.s.qfill2[p], 1);
+            EWSJF_CHECK(o < A.s.qoff2[p + 1]);
+            A.s.rec2[o] = f;
+        }
     }
 }
 

@@ -104,6 +104,22 @@ def test_product_fails_loudly_without_the_extension(monkeypatch, tmp_path):
         _lib.load()
 
 
+def test_bounds_checked_variant_is_opt_in():
+    """EWSJF_CHECKED=1 selects libewsjf_check.so built with -DEWSJF_BOUNDS_CHECK (the
+    device EWSJF_CHECK sites); without it the product library has them compiled out."""
+    code = ("from paper_2601_21758_b200 import _build, _lib; "
+            "print(_build.OUT, '-DEWSJF_BOUNDS_CHECK' in _build.FLAGS, _lib.LIB_PATH)")
+    env = dict(os.environ)
+    for checked in ("0", "1"):
+        env["EWSJF_CHECKED"] = checked
+        out = subprocess.run(["python", "-c", code], cwd=ROOT, env=env, capture_output=True, text=True).stdout.split()
+        name = "libewsjf_check.so" if checked == "1" else "libewsjf.so"
+        assert os.path.basename(out[0]) == name and os.path.basename(out[2]) == name, out
+        assert out[1] == ("True" if checked == "1" else "False"), out
+    cu = open(os.path.join(ROOT, "paper_2601_21758_b200", "csrc", "common.cuh")).read()
+    assert "#ifdef EWSJF_BOUNDS_CHECK" in cu and "__trap()" in cu
+
+
 def test_product_never_imports_the_oracle():
     """The CUDA product path has no route to oracle/ (only tests/smoke/bench may use it):
     no Python import of it, no C include of its header, no load of its library."""
