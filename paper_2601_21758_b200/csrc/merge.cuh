@@ -110,6 +110,7 @@ static __device__ void pool_shrink(u64* pool, float* psp, int& pn, u64& lo, int 
     for (int i = tid; i < pn; i += NT) {
         if (pool[i] >= lo) {
             const int p = atomicAdd(&M->nsurv, 1);
+            EWSJF_CHECK(p < kRankMax);
             surv[p] = pool[i];
             if (psp) ssp[p] = psp[i];
         }
@@ -290,7 +291,9 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
                 if (cls == kClsIn || cls == kClsDrop || gid < cmin) keep = false;
                 else keep = cls == kClsNew || gid > mincre[gp];
                 if (keep) {
-                    unext[atomicAdd(&M->nkeep, 1)] = (int32_t)v;
+                    const int o = atomicAdd(&M->nkeep, 1);
+                    EWSJF_CHECK((unsigned long long)o < (unsigned long long)A.gap_cap);
+                    unext[o] = (int32_t)v;
                 } else {
                     A.g_slot[v] = slot == 1023 ? -1 : slot;
                     if (slot == 1023) atomicAdd(&M->ndrop, 1);
@@ -485,7 +488,11 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
             for (int i = 0; i < kFR; i++)
 #pragma unroll
                 for (int h = 0; h < 2; h++)
-                    if (kv[i][h] && kv[i][h] >= thr) uni[atomicAdd(&M->pn, 1)] = kv[i][h];
+                    if (kv[i][h] && kv[i][h] >= thr) {
+                        const int o = atomicAdd(&M->pn, 1);
+                        EWSJF_CHECK(o < L.esmem);
+                        uni[o] = kv[i][h];
+                    }
             __syncthreads();
             pn = M->pn;
             e0 = total_rows;            // rows done; the loop below appends gap requests only
@@ -538,6 +545,7 @@ __device__ __forceinline__ void merge_phase(const MergeArgs& A, const Policy& P,
                     }
                     if (ok[u] && key[u] >= thr) {
                         const int p = atomicAdd(&M->pn, 1);
+                        EWSJF_CHECK(p < L.esmem);
                         uni[p] = key[u];
                         if (psp) psp[p] = sp[u];
                     }

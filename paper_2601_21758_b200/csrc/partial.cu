@@ -245,6 +245,7 @@ __device__ __forceinline__ void partial_phase(const PartialArgs& A, const Policy
             if (pos == A.hwm || (pos == A.K && !s_exact[gs])) my_want = true;
         } else {
             const int o = atomicAdd(&M->novf, 1);
+            EWSJF_CHECK(o < kTile);
             s_ovfk[o] = key;
             s_ovfs[o] = (uint16_t)gs;
             atomicAdd(&s_ovfcnt[gs], 1);
